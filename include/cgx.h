@@ -1,0 +1,240 @@
+/*
+ * cgx.h — C ABI of the B200-native CUDA-Graph input-rebinding hot path (arXiv 2503.19779).
+ *
+ * The calls follow the paper's statement of the problem:
+ *   capture a kernel sequence ............ cgx_chain_* + cgx_exec_create   (§2.2)
+ *   replace mutable params ............... placeholders / pointer table
+ *   refresh them before each replay ...... cgx_bind
+ *   replay ............................... cgx_launch
+ *   decide per graph whether to deploy ... cgx_profile + cgx_select
+ * (P:Lnnn = line of the paper's LaTeX source, PAPER.md; S:Lnnn = SPEC.md.)
+ *
+ * Conventions
+ *  - Every function returns an int status (cgx_status) and never aborts. On a non-OK status
+ *    cgx_last_error() returns a thread-local human-readable message (CUDA/NCCL errors carry the
+ *    library's own message). Out-parameters are written only on CGX_OK.
+ *  - All pointers to tensor data are DEVICE pointers of the chain's device (plain addresses, no
+ *    framework types). Host-side arrays (ext_dptrs, attrs, profiles) are read during the call only.
+ *  - Ownership: the caller owns external input buffers, static buffers (weights) and any NCCL
+ *    communicator. The library owns placeholders, the pointer table and its pinned staging,
+ *    internal/output buffers, graphs and execs. Output buffers are static and are overwritten by
+ *    the next launch on that chain (PyTorch2-CG semantics).
+ *  - Lifetime of inputs: an input bound with cgx_bind must stay valid and unmodified until the
+ *    cgx_launch that reads it has completed in stream order. COPY mode stops reading it once the
+ *    copy kernel (enqueued by cgx_bind) has run; INDIRECT / SETPARAMS / EAGER read it during the
+ *    whole replay (the key semantic difference of parameter indirection).
+ *  - Threading: an exec belongs to one stream and one host thread. Execs of the same chain share
+ *    the chain's internal buffers, so they must not run concurrently (one stream per chain).
+ *    Chains on different devices are independent.
+ *  - Sizes are fixed at capture; there are no dynamic shapes.
+ */
+#ifndef CGX_H_
+#define CGX_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CGX_ABI_VERSION 1
+#define CGX_MAX_IN 4                    /* max inputs per node */
+#define CGX_MAX_PROFILE_KERNELS 1024    /* max kernels in one profiled segment */
+
+typedef struct cgx_chain cgx_chain;     /* a kernel sequence description (slots + nodes) */
+typedef struct cgx_exec cgx_exec;       /* one captured+instantiated graph (or eager runner) */
+
+typedef enum {
+  CGX_OK = 0,
+  CGX_E_INVALID_ARG = 1,      /* null/out-of-range argument, bad slot/node index, bad attr */
+  CGX_E_STATE = 2,            /* call not valid now (e.g. launch before the first bind) */
+  CGX_E_NOT_ELIGIBLE = 3,     /* host pointer bound (P:L264-265 dangling host pointer hazard),
+                                 node writes an EXTERNAL/STATIC slot */
+  CGX_E_MISSING_INPUT = 4,    /* bind with the wrong number of inputs */
+  CGX_E_SIZE_MISMATCH = 5,    /* node shapes inconsistent with its slots */
+  CGX_E_MISALIGNED = 6,       /* bound pointer not 16-byte aligned */
+  CGX_E_UNSUPPORTED = 7,      /* op/dtype/mode combination not built */
+  CGX_E_OFFSET_NOT_FOUND = 8, /* param-offset discovery: no match (NEXT-2) */
+  CGX_E_OFFSET_AMBIGUOUS = 9, /* param-offset discovery: >= 2 matches (NEXT-2) */
+  CGX_E_CUDA = 10,            /* CUDA runtime error; message in cgx_last_error() */
+  CGX_E_NCCL = 11             /* NCCL error; message in cgx_last_error() */
+} cgx_status;
+
+typedef enum { CGX_F32 = 0, CGX_BF16 = 1 } cgx_dtype;
+
+/* Slot kinds (P:L601-607 and footnote P:L522-525): EXTERNAL = supplied anew every replay
+ * (an application input: rebound); STATIC = captured by address, never rebound (weights,
+ * SURVEY reading 4); INTERNAL = produced by an earlier node of the same chain (never copied). */
+typedef enum { CGX_SLOT_EXTERNAL = 0, CGX_SLOT_STATIC = 1, CGX_SLOT_INTERNAL = 2 } cgx_slot_kind;
+
+/* Node ops (SPEC opcode algebra, plus the decoder nodes of SURVEY §8(a) a7).
+ * Inputs per op (in_slots order) and definitions:
+ *   ADD        [a, b]        out[i] = a[i] + b[i]                 f32 or bf16, i < attr.n
+ *   MUL        [a, b]        out[i] = a[i] * b[i]
+ *   SCALE_IMM  [a]           out[i] = a[i] * attr.scalar (by-value float)
+ *   COPY       [a]           out[i] = a[i]
+ *   REDUCE_SUM [a]           out[r] = sum_c a[r*cols + c], cols = attr.cols, r < n/cols (f32)
+ *   LAYERNORM  [x, g, b]     rows x cols bf16, population variance, attr.eps
+ *   GEMM_BF16  [A, W, bias(, residual)]  out[M,N] = epi(A[M,K] W[N,K]^T + bias), flags below
+ *   ATTN_CAUSAL [qkv]        qkv [T, 3*H*D] (q|k|v, head-major) -> out [T, H*D], causal softmax
+ *   ALLREDUCE_SUM [x]        out = sum over ranks of x (bf16), captured ncclAllReduce */
+typedef enum {
+  CGX_OP_ADD = 0, CGX_OP_MUL = 1, CGX_OP_SCALE_IMM = 2, CGX_OP_COPY = 3, CGX_OP_REDUCE_SUM = 4,
+  CGX_OP_LAYERNORM = 5, CGX_OP_GEMM_BF16 = 6, CGX_OP_ATTN_CAUSAL = 7, CGX_OP_ALLREDUCE_SUM = 8
+} cgx_op;
+
+#define CGX_GEMM_BIAS 1u
+#define CGX_GEMM_GELU 2u        /* tanh-approximate GELU after the bias */
+#define CGX_GEMM_RESIDUAL 4u    /* + in_slots[3] after the activation */
+
+typedef struct {
+  uint64_t n;          /* elementwise/reduce: elements processed (0 = whole first input) */
+  float scalar;        /* SCALE_IMM constant; ATTN_CAUSAL softmax scale */
+  float eps;           /* LAYERNORM epsilon */
+  uint32_t rows, cols; /* LAYERNORM rows x cols; REDUCE_SUM row length (cols) */
+  uint32_t M, N, K;    /* GEMM_BF16 */
+  uint32_t flags;      /* CGX_GEMM_* */
+  uint32_t T, H, D;    /* ATTN_CAUSAL */
+} cgx_attr;
+
+/* Execution modes (the arms of BASELINE.json north_star):
+ *   EAGER            launch every node from the host with the current pointers (PT2-No-CG)
+ *   GRAPH_COPY       placeholders + per-replay multi-tensor copy (PT2-CG baseline)
+ *   GRAPH_INDIRECT   parameter indirection: kernels read base pointers from a device pointer
+ *                    table patched once per replay
+ *   GRAPH_SETPARAMS  rewrite each consuming node's params with cudaGraphExecKernelNodeSetParams
+ *                    (comparison arm, "graph management APIs")
+ *   GRAPH_STALE      negative control: inputs recorded by value at the first bind and never
+ *                    rebound */
+typedef enum {
+  CGX_MODE_EAGER = 0, CGX_MODE_GRAPH_COPY = 1, CGX_MODE_GRAPH_INDIRECT = 2,
+  CGX_MODE_GRAPH_SETPARAMS = 3, CGX_MODE_GRAPH_STALE = 4
+} cgx_mode;
+
+/* INDIRECT pointer-table transports (the paper only says "host-to-device
+ * copies over the PCIe"):
+ *   H2D          T1: cudaMemcpyAsync of pinned staging into the table before cudaGraphLaunch
+ *   ROOT_MEMCPY  T2: memcpy node at the graph root from ping-pong pinned staging
+ *   ROOT_PARAMS  T3: root table-writer kernel whose by-value params carry the pointers, updated
+ *                    with one cudaGraphExecKernelNodeSetParams per bind
+ *   ROOT_MAPPED  T4: root kernel reading a mapped pinned staging ring (zero-copy) */
+typedef enum {
+  CGX_XPORT_DEFAULT = 0, CGX_XPORT_H2D = 1, CGX_XPORT_ROOT_MEMCPY = 2, CGX_XPORT_ROOT_PARAMS = 3,
+  CGX_XPORT_ROOT_MAPPED = 4
+} cgx_transport;
+
+typedef enum { CGX_DECIDE_EAGER = 0, CGX_DECIDE_GRAPH_COPY = 1, CGX_DECIDE_GRAPH_INDIRECT = 2 } cgx_decision;
+
+/* Exec options; an all-zero struct means "defaults". */
+typedef struct {
+  cgx_mode mode;
+  cgx_transport transport;  /* INDIRECT only (0 = ROOT_PARAMS) */
+  int first_node;           /* node range [first_node, first_node + n_nodes) */
+  int n_nodes;              /* 0 = to the end of the chain */
+  int no_pdl;               /* 1 = plain stream edges instead of programmatic dependent launch */
+  int validate;             /* bind-time residency check: 0 = cached per address (default),
+                               1 = every bind, 2 = off (alignment and count are always checked) */
+  int copy_impl;            /* GRAPH_COPY: 0 = multi-tensor kernel, 1 = cudaMemcpyAsync per tensor */
+} cgx_exec_opts;
+
+typedef struct {
+  uint64_t bytes_data_rebound;   /* last bind: data bytes copied into placeholders */
+  uint64_t bytes_ptr_rebound;    /* last bind: pointer bytes written to the table (8 x N_ext) */
+  uint64_t total_bytes_data, total_bytes_ptr;
+  uint64_t n_binds, n_launches;
+  uint32_t n_setparam_calls;     /* last bind: cudaGraphExecKernelNodeSetParams calls */
+  uint32_t n_copy_tensors;       /* last bind: tensors copied */
+  uint32_t n_nodes;              /* K: chain nodes in this exec */
+  uint32_t n_graph_nodes;        /* nodes in the instantiated graph (incl. a root node) */
+  uint32_t n_ext;                /* N_ext of this exec */
+  uint32_t kernels_per_replay;   /* library kernels per bind+launch (copy/root/chain) */
+  uint32_t mode, transport;
+} cgx_stats_t;
+
+/* One segment's slow-path measurements, all microseconds. */
+typedef struct {
+  int n_kernels;          /* K */
+  int ind_available;      /* 0 -> INDIRECT is not a candidate */
+  int use_measured;       /* 1 -> decide on the measured totals, else on the estimates */
+  int reserved;
+  double L_us;            /* host launch cost per kernel (eager) */
+  double G_us;            /* host cudaGraphLaunch cost */
+  double delta_us;        /* per-node in-graph overhead */
+  double c_copy_us;       /* COPY rebinding Δ */
+  double c_ind_us;        /* INDIRECT rebinding Δ */
+  double F_us;            /* fixed per-replay overhead term (0 unless set) */
+  double t_eager_us, t_copy_us, t_ind_us;   /* measured end-to-end per replay */
+  double d_us[CGX_MAX_PROFILE_KERNELS];     /* device time per kernel */
+} cgx_profile_t;
+
+int cgx_version(void);
+const char* cgx_last_error(void);
+
+/* ---- chain description -------------------------------------------------------------------- */
+int cgx_chain_create(int device, cgx_chain** out);
+/* nelems elements of dtype. STATIC: static_dptr is the caller's device buffer (not copied,
+ * must outlive the chain); EXTERNAL/INTERNAL: static_dptr must be NULL. slot_out: slot index.
+ * EXTERNAL slots are numbered j = 0.. in declaration order (table order). */
+int cgx_chain_add_slot(cgx_chain* c, cgx_slot_kind kind, cgx_dtype dtype, uint64_t nelems,
+                       void* static_dptr, int* slot_out);
+/* Appends a node. The output slot must be INTERNAL (CGX_E_NOT_ELIGIBLE otherwise). */
+int cgx_chain_add_node(cgx_chain* c, cgx_op op, const int* in_slots, int n_in, int out_slot,
+                       const cgx_attr* attr, int* node_out);
+/* Selector unit: an inclusive node range ("independently for each of the CGs"). */
+int cgx_chain_mark_segment(cgx_chain* c, int first_node, int last_node);
+/* ncclComm_t (caller-owned) used by ALLREDUCE_SUM nodes. */
+int cgx_chain_set_nccl(cgx_chain* c, void* nccl_comm);
+int cgx_chain_destroy(cgx_chain* c);
+
+/* ---- capture / bind / replay -------------------------------------------------------------- */
+/* Slow path: allocate internals/placeholders/table, capture the nodes (stream capture with
+ * programmatic-dependent-launch edges), instantiate and upload. cuda_stream: cudaStream_t. */
+int cgx_exec_create(cgx_chain* c, cgx_mode mode, void* cuda_stream, cgx_exec** out);
+int cgx_exec_create_ex(cgx_chain* c, const cgx_exec_opts* opts, void* cuda_stream, cgx_exec** out);
+/* Per replay: bind the fresh external inputs y_j (device pointers, declaration order).
+ * COPY enqueues the copy of every y_j whose address differs from its placeholder (SURVEY
+ * reading 1); INDIRECT patches the table (8 x N_ext bytes); SETPARAMS rewrites every node that
+ * reads an external; EAGER records the pointers; STALE records them at the first bind only. */
+int cgx_bind(cgx_exec* e, const void* const* ext_dptrs, int n_ext);
+/* Per replay: cudaGraphLaunch (or K eager launches). CGX_E_STATE if never bound. */
+int cgx_launch(cgx_exec* e);
+/* Library-owned device buffer of a slot (internal: shared per chain; external under COPY: the
+ * placeholder). nbytes may be NULL. */
+int cgx_output(cgx_exec* e, int slot, void** dptr, uint64_t* nbytes);
+int cgx_stats(const cgx_exec* e, cgx_stats_t* out);
+/* Parity hooks: the device pointer table (n entries, host copy; synchronises the stream) and the
+ * node indices a SETPARAMS bind rewrites. */
+int cgx_debug_read_table(const cgx_exec* e, uint64_t* host_out, int n);
+int cgx_debug_setparam_nodes(const cgx_exec* e, int* nodes_out, int cap, int* n_out);
+int cgx_exec_destroy(cgx_exec* e);
+
+/* ---- selective CUDA graphs ---------------------------------------------------------------- */
+/* Slow path: measure one segment (index into the marked segments, or -1 = whole chain) in the
+ * three candidate modules (eager, graph+copy, graph+PI) with the given inputs; reps timed
+ * iterations after warm-up (SURVEY reading 7). Fills every field of *out. */
+int cgx_profile(cgx_chain* c, int segment, const void* const* ext_dptrs, int n_ext, int reps,
+                void* cuda_stream, cgx_profile_t* out);
+/* Pure host function: per segment argmin over [eager, copy, ind]
+ * with strict '<' in that order (ties EAGER > COPY > INDIRECT). est_out (3*n_segments doubles,
+ * optional) receives the three estimates/totals used. */
+int cgx_select(const cgx_profile_t* prof, int n_segments, cgx_decision* out, double* est_out);
+
+/* ---- measurement helpers ------------------------------------------------------------------ */
+/* Single-dispatch floor: median host µs of cudaGraphLaunch of a 1-node
+ * empty-kernel graph and of cudaLaunchKernel of an empty kernel on cuda_stream. */
+int cgx_dispatch_floor(void* cuda_stream, int reps, double* graph_launch_us, double* kernel_launch_us);
+/* Stream-ordered copy between any two CUDA-visible addresses (cudaMemcpyAsync, kind inferred):
+ * used to read library-owned outputs and to stage end-to-end inputs. */
+int cgx_copy(void* dst, const void* src, uint64_t nbytes, void* cuda_stream);
+/* Fill a device f32 buffer with the synth.splitmix uniform recipe (k*2^-23 - 1) on device. */
+int cgx_fill_uniform_f32(void* dptr, uint64_t n, uint64_t seed, uint64_t stream_id, void* cuda_stream);
+
+/* ---- NCCL bootstrap (ncclComm_t for ALLREDUCE_SUM; caller owns it) ------------------------- */
+int cgx_nccl_unique_id(void* id_out /* 128 bytes */);
+int cgx_nccl_comm_init(int nranks, int rank, const void* id /* 128 bytes */, int device, void** comm_out);
+int cgx_nccl_comm_destroy(void* comm);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CGX_H_ */

@@ -1,0 +1,270 @@
+"""ctypes binding of include/cgx.h — argument marshalling only.
+
+Every step of the hot path runs inside libcgx.so (hand-written sm_100a kernels + the C++
+runtime). There is no Python or CPU fallback: if the library is missing or fails to load, import
+fails loudly. Names mirror the C ABI (cgx_chain_create -> chain_create, ...).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libcgx.so")
+
+# --------------------------------------------------------------------------- enums (cgx.h)
+OK = 0
+STATUS = {0: "CGX_OK", 1: "CGX_E_INVALID_ARG", 2: "CGX_E_STATE", 3: "CGX_E_NOT_ELIGIBLE",
+          4: "CGX_E_MISSING_INPUT", 5: "CGX_E_SIZE_MISMATCH", 6: "CGX_E_MISALIGNED",
+          7: "CGX_E_UNSUPPORTED", 8: "CGX_E_OFFSET_NOT_FOUND", 9: "CGX_E_OFFSET_AMBIGUOUS",
+          10: "CGX_E_CUDA", 11: "CGX_E_NCCL"}
+E_INVALID_ARG, E_STATE, E_NOT_ELIGIBLE, E_MISSING_INPUT, E_SIZE_MISMATCH, E_MISALIGNED, \
+    E_UNSUPPORTED, E_OFFSET_NOT_FOUND, E_OFFSET_AMBIGUOUS, E_CUDA, E_NCCL = range(1, 12)
+F32, BF16 = 0, 1
+SLOT_EXTERNAL, SLOT_STATIC, SLOT_INTERNAL = 0, 1, 2
+OP = {"ADD": 0, "MUL": 1, "SCALE_IMM": 2, "COPY": 3, "REDUCE_SUM": 4, "LAYERNORM": 5,
+      "GEMM_BF16": 6, "ATTN_CAUSAL": 7, "ALLREDUCE_SUM": 8}
+GEMM_BIAS, GEMM_GELU, GEMM_RESIDUAL = 1, 2, 4
+MODE = {"EAGER": 0, "COPY": 1, "INDIRECT": 2, "SETPARAMS": 3, "STALE": 4}
+XPORT = {"DEFAULT": 0, "H2D": 1, "ROOT_MEMCPY": 2, "ROOT_PARAMS": 3, "ROOT_MAPPED": 4}
+DECIDE = {0: "EAGER", 1: "GRAPH_COPY", 2: "GRAPH_INDIRECT"}
+MAX_PROFILE_KERNELS = 1024
+
+
+class Attr(C.Structure):
+    _fields_ = [("n", C.c_uint64), ("scalar", C.c_float), ("eps", C.c_float),
+                ("rows", C.c_uint32), ("cols", C.c_uint32), ("M", C.c_uint32), ("N", C.c_uint32),
+                ("K", C.c_uint32), ("flags", C.c_uint32), ("T", C.c_uint32), ("H", C.c_uint32),
+                ("D", C.c_uint32)]
+
+
+class ExecOpts(C.Structure):
+    _fields_ = [("mode", C.c_int), ("transport", C.c_int), ("first_node", C.c_int),
+                ("n_nodes", C.c_int), ("no_pdl", C.c_int), ("validate", C.c_int),
+                ("copy_impl", C.c_int)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("bytes_data_rebound", C.c_uint64), ("bytes_ptr_rebound", C.c_uint64),
+                ("total_bytes_data", C.c_uint64), ("total_bytes_ptr", C.c_uint64),
+                ("n_binds", C.c_uint64), ("n_launches", C.c_uint64),
+                ("n_setparam_calls", C.c_uint32), ("n_copy_tensors", C.c_uint32),
+                ("n_nodes", C.c_uint32), ("n_graph_nodes", C.c_uint32), ("n_ext", C.c_uint32),
+                ("kernels_per_replay", C.c_uint32), ("mode", C.c_uint32), ("transport", C.c_uint32)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class Profile(C.Structure):
+    _fields_ = [("n_kernels", C.c_int), ("ind_available", C.c_int), ("use_measured", C.c_int),
+                ("reserved", C.c_int), ("L_us", C.c_double), ("G_us", C.c_double),
+                ("delta_us", C.c_double), ("c_copy_us", C.c_double), ("c_ind_us", C.c_double),
+                ("F_us", C.c_double), ("t_eager_us", C.c_double), ("t_copy_us", C.c_double),
+                ("t_ind_us", C.c_double), ("d_us", C.c_double * MAX_PROFILE_KERNELS)]
+
+    def as_dict(self):
+        d = {f: getattr(self, f) for f, _ in self._fields_ if f != "d_us"}
+        d["d_us"] = list(self.d_us[: self.n_kernels])
+        return d
+
+
+class CgxError(RuntimeError):
+    def __init__(self, status: int, fn: str, msg: str):
+        super().__init__(f"{fn}: {STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libcgx.so not built at {LIB_PATH}: run __graft_entry__.build() "
+                          "(no CPU fallback exists)")
+    lib = C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)
+    P, I, U64, VP = C.POINTER, C.c_int, C.c_uint64, C.c_void_p
+    sig = {
+        "cgx_version": ([], I), "cgx_last_error": ([], C.c_char_p),
+        "cgx_chain_create": ([I, P(VP)], I),
+        "cgx_chain_add_slot": ([VP, I, I, U64, VP, P(I)], I),
+        "cgx_chain_add_node": ([VP, I, P(I), I, I, P(Attr), P(I)], I),
+        "cgx_chain_mark_segment": ([VP, I, I], I),
+        "cgx_chain_set_nccl": ([VP, VP], I),
+        "cgx_chain_destroy": ([VP], I),
+        "cgx_exec_create": ([VP, I, VP, P(VP)], I),
+        "cgx_exec_create_ex": ([VP, P(ExecOpts), VP, P(VP)], I),
+        "cgx_bind": ([VP, P(VP), I], I),
+        "cgx_launch": ([VP], I),
+        "cgx_output": ([VP, I, P(VP), P(U64)], I),
+        "cgx_stats": ([VP, P(Stats)], I),
+        "cgx_debug_read_table": ([VP, P(U64), I], I),
+        "cgx_debug_setparam_nodes": ([VP, P(I), I, P(I)], I),
+        "cgx_exec_destroy": ([VP], I),
+        "cgx_profile": ([VP, I, P(VP), I, I, VP, P(Profile)], I),
+        "cgx_select": ([P(Profile), I, P(I), P(C.c_double)], I),
+        "cgx_dispatch_floor": ([VP, I, P(C.c_double), P(C.c_double)], I),
+        "cgx_fill_uniform_f32": ([VP, U64, U64, U64, VP], I),
+        "cgx_copy": ([VP, VP, U64, VP], I),
+        "cgx_nccl_unique_id": ([VP], I),
+        "cgx_nccl_comm_init": ([I, I, VP, I, P(VP)], I),
+        "cgx_nccl_comm_destroy": ([VP], I),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = res
+    return lib
+
+
+LIB = _load()
+EXPORTED = ("cgx_version", "cgx_last_error", "cgx_chain_create", "cgx_chain_add_slot",
+            "cgx_chain_add_node", "cgx_chain_mark_segment", "cgx_chain_set_nccl",
+            "cgx_chain_destroy", "cgx_exec_create", "cgx_exec_create_ex", "cgx_bind",
+            "cgx_launch", "cgx_output", "cgx_stats", "cgx_debug_read_table",
+            "cgx_debug_setparam_nodes", "cgx_exec_destroy", "cgx_profile", "cgx_select",
+            "cgx_dispatch_floor", "cgx_fill_uniform_f32", "cgx_copy", "cgx_nccl_unique_id",
+            "cgx_nccl_comm_init", "cgx_nccl_comm_destroy")
+
+
+def _ck(status: int, fn: str):
+    if status != OK:
+        raise CgxError(status, fn, LIB.cgx_last_error().decode(errors="replace"))
+
+
+def last_error() -> str:
+    return LIB.cgx_last_error().decode(errors="replace")
+
+
+def version() -> int:
+    return LIB.cgx_version()
+
+
+# --------------------------------------------------------------------------- thin wrappers
+def chain_create(device: int = 0) -> int:
+    out = C.c_void_p()
+    _ck(LIB.cgx_chain_create(device, C.byref(out)), "cgx_chain_create")
+    return out.value
+
+
+def chain_add_slot(chain: int, kind: int, dtype: int, nelems: int, static_dptr: int | None = None) -> int:
+    out = C.c_int()
+    _ck(LIB.cgx_chain_add_slot(chain, kind, dtype, nelems, static_dptr, C.byref(out)),
+        "cgx_chain_add_slot")
+    return out.value
+
+
+def chain_add_node(chain: int, op: int, in_slots, out_slot: int, attr: Attr | None = None) -> int:
+    arr = (C.c_int * max(1, len(in_slots)))(*in_slots)
+    out = C.c_int()
+    _ck(LIB.cgx_chain_add_node(chain, op, arr, len(in_slots), out_slot,
+                               C.byref(attr) if attr is not None else None, C.byref(out)),
+        "cgx_chain_add_node")
+    return out.value
+
+
+def chain_mark_segment(chain: int, first: int, last: int):
+    _ck(LIB.cgx_chain_mark_segment(chain, first, last), "cgx_chain_mark_segment")
+
+
+def chain_set_nccl(chain: int, comm: int):
+    _ck(LIB.cgx_chain_set_nccl(chain, comm), "cgx_chain_set_nccl")
+
+
+def chain_destroy(chain: int):
+    _ck(LIB.cgx_chain_destroy(chain), "cgx_chain_destroy")
+
+
+def exec_create(chain: int, mode: str, stream: int, transport: str = "DEFAULT", first_node: int = 0,
+                n_nodes: int = 0, no_pdl: bool = False, validate: int = 0, copy_impl: int = 0) -> int:
+    o = ExecOpts(MODE[mode], XPORT[transport], first_node, n_nodes, int(no_pdl), validate, copy_impl)
+    out = C.c_void_p()
+    _ck(LIB.cgx_exec_create_ex(chain, C.byref(o), stream, C.byref(out)), "cgx_exec_create_ex")
+    return out.value
+
+
+def ptr_array(ptrs):
+    return (C.c_void_p * max(1, len(ptrs)))(*ptrs)
+
+
+def bind(ex: int, ptrs) -> None:
+    arr = ptrs if isinstance(ptrs, C.Array) else ptr_array(list(ptrs))
+    _ck(LIB.cgx_bind(ex, arr, len(arr) if isinstance(ptrs, C.Array) else len(ptrs)), "cgx_bind")
+
+
+def launch(ex: int) -> None:
+    _ck(LIB.cgx_launch(ex), "cgx_launch")
+
+
+def output(ex: int, slot: int):
+    p, n = C.c_void_p(), C.c_uint64()
+    _ck(LIB.cgx_output(ex, slot, C.byref(p), C.byref(n)), "cgx_output")
+    return p.value, n.value
+
+
+def stats(ex: int) -> dict:
+    s = Stats()
+    _ck(LIB.cgx_stats(ex, C.byref(s)), "cgx_stats")
+    return s.as_dict()
+
+
+def debug_read_table(ex: int, n: int) -> list:
+    buf = (C.c_uint64 * max(1, n))()
+    _ck(LIB.cgx_debug_read_table(ex, buf, n), "cgx_debug_read_table")
+    return list(buf[:n])
+
+
+def debug_setparam_nodes(ex: int) -> list:
+    n = C.c_int()
+    _ck(LIB.cgx_debug_setparam_nodes(ex, None, 0, C.byref(n)), "cgx_debug_setparam_nodes")
+    buf = (C.c_int * max(1, n.value))()
+    _ck(LIB.cgx_debug_setparam_nodes(ex, buf, n.value, C.byref(n)), "cgx_debug_setparam_nodes")
+    return list(buf[: n.value])
+
+
+def exec_destroy(ex: int):
+    _ck(LIB.cgx_exec_destroy(ex), "cgx_exec_destroy")
+
+
+def profile(chain: int, segment: int, ptrs, reps: int, stream: int) -> Profile:
+    p = Profile()
+    arr = ptr_array(list(ptrs))
+    _ck(LIB.cgx_profile(chain, segment, arr, len(ptrs), reps, stream, C.byref(p)), "cgx_profile")
+    return p
+
+
+def select(profiles) -> tuple:
+    n = len(profiles)
+    arr = (Profile * max(1, n))(*profiles)
+    out = (C.c_int * max(1, n))()
+    est = (C.c_double * max(3, 3 * n))()
+    _ck(LIB.cgx_select(arr, n, out, est), "cgx_select")
+    return list(out[:n]), [tuple(est[3 * i:3 * i + 3]) for i in range(n)]
+
+
+def dispatch_floor(stream: int, reps: int = 2000) -> tuple:
+    g, k = C.c_double(), C.c_double()
+    _ck(LIB.cgx_dispatch_floor(stream, reps, C.byref(g), C.byref(k)), "cgx_dispatch_floor")
+    return g.value, k.value
+
+
+def fill_uniform_f32(dptr: int, n: int, seed: int, stream_id: int, stream: int):
+    _ck(LIB.cgx_fill_uniform_f32(dptr, n, seed, stream_id, stream), "cgx_fill_uniform_f32")
+
+
+def copy(dst: int, src: int, nbytes: int, stream: int):
+    _ck(LIB.cgx_copy(dst, src, nbytes, stream), "cgx_copy")
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _ck(LIB.cgx_nccl_unique_id(buf), "cgx_nccl_unique_id")
+    return buf.raw
+
+
+def nccl_comm_init(nranks: int, rank: int, uid: bytes, device: int) -> int:
+    buf = C.create_string_buffer(uid, 128)
+    out = C.c_void_p()
+    _ck(LIB.cgx_nccl_comm_init(nranks, rank, buf, device, C.byref(out)), "cgx_nccl_comm_init")
+    return out.value
+
+
+def nccl_comm_destroy(comm: int):
+    _ck(LIB.cgx_nccl_comm_destroy(comm), "cgx_nccl_comm_destroy")

@@ -1,0 +1,95 @@
+// Kernel argument blocks shared by the runtime (host) and the kernels (device).
+// Every chain kernel takes exactly ONE by-value struct, so a node's whole parameter image is one
+// contiguous block: SETPARAMS rewrites it with cudaGraphExecKernelNodeSetParams, and the
+// parameter-indirection variant differs only in the table index fields ("replaces
+// each pointer argument with a pointer-to-pointer").
+#pragma once
+#include <stdint.h>
+
+namespace cgx {
+
+// Operand fetch rule ("de-references these pointers-to-pointers before performing
+// any computation"): operand i reads `ptr[i]` when tidx[i] < 0, else `table[tidx[i]]`; the load
+// happens once at kernel start into a register (warp-uniform address, one request per warp).
+struct ElemArgs {
+  const uint64_t* table;   // device pointer table (INDIRECT) or nullptr
+  const void* in0;
+  const void* in1;
+  void* out;
+  int32_t t0, t1;          // table index of in0/in1, -1 = direct pointer
+  uint32_t flags;          // kFlagTableAfterWait: fetch table entries after griddepcontrol.wait
+  uint32_t cols;           // REDUCE_SUM row length
+  uint64_t n;              // elements
+  float scalar;            // SCALE_IMM
+  float eps;
+};
+static constexpr uint32_t kFlagTableAfterWait = 1u;
+
+// Multi-tensor copy (BASELINE north_star (1)). Static part lives in device
+// memory (per exec, written once at capture); the fresh sources travel by value in the params.
+struct CopyDesc {
+  void* dst;               // placeholder
+  uint64_t nbytes;
+  uint32_t chunk_begin;    // first global chunk index of this tensor
+  uint32_t n_chunks;
+};
+template <int CAP>
+struct CopyArgs {
+  const CopyDesc* desc;    // [n_tensors]
+  const uint32_t* chunk_tensor;  // [n_chunks_total] tensor owning each chunk
+  uint32_t n_tensors;
+  uint32_t n_chunks;
+  uint32_t chunk_bytes;
+  uint32_t pad;
+  const void* src[CAP];
+};
+
+// T3 root table writer: pointers by value, one cudaGraphExecKernelNodeSetParams per bind.
+template <int CAP>
+struct TableWriteArgs {
+  uint64_t* table;
+  uint32_t n;
+  uint32_t pad;
+  uint64_t ptr[CAP];
+};
+
+// T4 root kernel: read slot (seq % ring) of a mapped pinned staging ring, ack through mapped
+// host memory so the host knows when a slot may be overwritten.
+struct MappedTableArgs {
+  const uint64_t* staging;       // device alias of pinned host ring [ring][n_pad]
+  uint64_t* table;
+  unsigned long long* seq;       // device counter (replays consumed)
+  unsigned long long* ack;       // device alias of pinned host word
+  uint32_t n, n_pad, ring, pad;
+};
+
+// Decoder nodes.
+struct LnArgs {
+  const uint64_t* table;
+  const void* x; const void* g; const void* b; void* out;
+  int32_t tx, pad0;
+  uint32_t flags, rows, cols, pad1;
+  float eps;
+};
+
+struct AttnArgs {
+  const void* qkv; void* out;
+  uint32_t T, H, D, flags;
+  float scale;
+};
+
+}  // namespace cgx
+
+// Kernel handles exported by the kernel translation units (host functions).
+extern "C++" {
+namespace cgx {
+const void* kfn_elem(int op, int dtype);          // ADD/MUL/SCALE_IMM/COPY f32|bf16
+const void* kfn_reduce_sum_f32();
+const void* kfn_copy(int cap);                    // CAP in {8, 64, 1024}
+const void* kfn_table_write(int cap);             // CAP in {8, 64, 512}
+const void* kfn_table_mapped();
+const void* kfn_empty();
+const void* kfn_fill_uniform_f32();
+int elem_block_threads();
+}  // namespace cgx
+}

@@ -1,0 +1,24 @@
+// Decoder-node kernels: LayerNorm, causal attention, tcgen05 bf16 GEMM.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace cgx {
+// LayerNorm: one warp per row, registers hold the row (cols <= 2048, cols % 8 == 0).
+const void* kfn_layernorm();
+void decoder_ln_launch_dims(uint32_t rows, uint32_t cols, dim3* grid, dim3* block);
+
+// Causal attention on CUDA cores (T <= 1024, D == 64).
+const void* kfn_attention();
+bool decoder_attn_supported(uint32_t T, uint32_t H, uint32_t D);
+void decoder_attn_launch_dims(uint32_t T, uint32_t H, uint32_t D, dim3* grid, dim3* block, size_t* smem);
+
+// tcgen05 GEMM out[M,N] = epi(A[M,K] * W[N,K]^T + bias): TMA tiles, TMEM accumulator.
+bool decoder_gemm_supported(uint32_t M, uint32_t N, uint32_t K);
+// Builds the by-value parameter block (tensor maps included) into args_out (64-B aligned) when
+// args_out != nullptr; always reports its size, launch geometry and kernel handle.
+int decoder_gemm_build(uint32_t M, uint32_t N, uint32_t K, uint32_t flags, const void* A, const void* W,
+                       const void* bias, const void* residual, void* out, void* args_out, size_t* argbytes,
+                       dim3* grid, dim3* block, size_t* smem, const void** func);
+}  // namespace cgx

@@ -1,0 +1,41 @@
+// Device-side helpers for sm_100a: programmatic dependent launch, cache-hinted loads/stores.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace cgx {
+
+// Programmatic dependent launch (PDL). A kernel's prologue (pointer-table fetch, index math) may
+// run while its predecessor drains; everything that reads a predecessor's output comes after
+// pdl_wait(). Every chain kernel triggers its dependents only AFTER its own wait, so a kernel
+// that starts early can rely on every node two or more steps upstream having completed.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
+// Pointer-table entry: L2-coherent load (the table is rewritten between replays).
+__device__ __forceinline__ uint64_t ld_table(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.global.cg.u64 %0, [%1];\n" : "=l"(v) : "l"(p));
+  return v;
+}
+
+// Streaming 16-byte load (read-only for the kernel's lifetime, do not allocate in L1).
+__device__ __forceinline__ int4 ld_stream16(const void* p) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_stream16(void* p, const int4& v) {
+  asm volatile("st.global.L1::no_allocate.v4.s32 [%0], {%1,%2,%3,%4};\n"
+               :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+
+__device__ __forceinline__ uint64_t splitmix_mix(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+}  // namespace cgx

@@ -1,0 +1,282 @@
+// Chain kernels for sm_100a: elementwise (ADD/MUL/SCALE_IMM/COPY, f32 and bf16), row reduction,
+// the multi-tensor copy of the COPY arm, the INDIRECT root table writers, and small utilities.
+//
+// All of them are HBM/L2-bandwidth or latency bound (no dense contraction): 128-bit coalesced
+// accesses, several loads in flight per thread, one CTA wave where possible, no tensor cores.
+//
+// Parameter indirection: an operand whose table index is >= 0 is fetched as
+// table[idx] ONCE at kernel start, before griddepcontrol.wait unless kFlagTableAfterWait is set
+// (the first node after a root table-writer node). The arithmetic after the fetch is the same code
+// for the direct and indirect variants, so all arms are bit-identical.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "cgx_args.h"
+#include "cgx_device.cuh"
+
+namespace cgx {
+
+static constexpr int kElemThreads = 256;
+static constexpr int kElemVec = 4;     // 16-B vectors per thread per operand (loads in flight)
+
+enum { OP_ADD = 0, OP_MUL = 1, OP_SCALE = 2, OP_COPY = 3 };
+
+template <int OP>
+__device__ __forceinline__ float apply_f32(float x, float y, float s) {
+  if (OP == OP_ADD) return __fadd_rn(x, y);
+  if (OP == OP_MUL) return __fmul_rn(x, y);
+  if (OP == OP_SCALE) return __fmul_rn(x, s);
+  return x;
+}
+
+__device__ __forceinline__ void fetch_operands(const ElemArgs& a, const void*& p0, const void*& p1) {
+  p0 = a.in0;
+  p1 = a.in1;
+  if (a.t0 >= 0) p0 = reinterpret_cast<const void*>(ld_table(a.table + a.t0));
+  if (a.t1 >= 0) p1 = reinterpret_cast<const void*>(ld_table(a.table + a.t1));
+}
+
+// Prologue shared by all chain kernels: table fetch (pre- or post-wait), PDL wait, trigger.
+#define CGX_PROLOGUE(a, p0, p1)                                        \
+  const void* p0;                                                      \
+  const void* p1;                                                      \
+  if (!((a).flags & kFlagTableAfterWait)) fetch_operands((a), p0, p1); \
+  pdl_wait();                                                          \
+  if ((a).flags & kFlagTableAfterWait) fetch_operands((a), p0, p1);    \
+  pdl_trigger();
+
+// ---------------------------------------------------------------------------- f32 elementwise
+template <int OP>
+__global__ void __launch_bounds__(kElemThreads) k_elem_f32(const __grid_constant__ ElemArgs a) {
+  CGX_PROLOGUE(a, p0, p1)
+  const float4* x = reinterpret_cast<const float4*>(p0);
+  const float4* y = reinterpret_cast<const float4*>(p1);
+  float4* o = reinterpret_cast<float4*>(a.out);
+  const uint64_t n4 = a.n >> 2;
+  const uint64_t base = (uint64_t)blockIdx.x * (kElemThreads * kElemVec) + threadIdx.x;
+  float4 xv[kElemVec], yv[kElemVec];
+#pragma unroll
+  for (int j = 0; j < kElemVec; ++j) {
+    const uint64_t i = base + (uint64_t)j * kElemThreads;
+    if (i < n4) {
+      xv[j] = x[i];
+      if (OP == OP_ADD || OP == OP_MUL) yv[j] = y[i];
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kElemVec; ++j) {
+    const uint64_t i = base + (uint64_t)j * kElemThreads;
+    if (i < n4) {
+      float4 r;
+      r.x = apply_f32<OP>(xv[j].x, yv[j].x, a.scalar);
+      r.y = apply_f32<OP>(xv[j].y, yv[j].y, a.scalar);
+      r.z = apply_f32<OP>(xv[j].z, yv[j].z, a.scalar);
+      r.w = apply_f32<OP>(xv[j].w, yv[j].w, a.scalar);
+      o[i] = r;
+    }
+  }
+  // scalar tail (n not a multiple of 4): block 0 only
+  if (blockIdx.x == 0) {
+    const uint64_t t = (n4 << 2) + threadIdx.x;
+    if (t < a.n) {
+      const float* xs = reinterpret_cast<const float*>(p0);
+      const float* ys = reinterpret_cast<const float*>(p1);
+      const float yy = (OP == OP_ADD || OP == OP_MUL) ? ys[t] : 0.f;
+      reinterpret_cast<float*>(a.out)[t] = apply_f32<OP>(xs[t], yy, a.scalar);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------- bf16 elementwise
+// Math in f32 with one RNE rounding to bf16 (exact sums/products of bf16 values whenever the
+// exponent gap is < 16; SURVEY ambiguity 11).
+template <int OP>
+__device__ __forceinline__ __nv_bfloat16 apply_bf16(__nv_bfloat16 x, __nv_bfloat16 y, float s) {
+  return __float2bfloat16_rn(apply_f32<OP>(__bfloat162float(x), __bfloat162float(y), s));
+}
+
+template <int OP>
+__global__ void __launch_bounds__(kElemThreads) k_elem_bf16(const __grid_constant__ ElemArgs a) {
+  CGX_PROLOGUE(a, p0, p1)
+  const uint4* x = reinterpret_cast<const uint4*>(p0);
+  const uint4* y = reinterpret_cast<const uint4*>(p1);
+  uint4* o = reinterpret_cast<uint4*>(a.out);
+  const uint64_t n8 = a.n >> 3;
+  const uint64_t base = (uint64_t)blockIdx.x * (kElemThreads * kElemVec) + threadIdx.x;
+  uint4 xv[kElemVec], yv[kElemVec];
+#pragma unroll
+  for (int j = 0; j < kElemVec; ++j) {
+    const uint64_t i = base + (uint64_t)j * kElemThreads;
+    if (i < n8) {
+      xv[j] = x[i];
+      if (OP == OP_ADD || OP == OP_MUL) yv[j] = y[i];
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kElemVec; ++j) {
+    const uint64_t i = base + (uint64_t)j * kElemThreads;
+    if (i < n8) {
+      const __nv_bfloat16* xb = reinterpret_cast<const __nv_bfloat16*>(&xv[j]);
+      const __nv_bfloat16* yb = reinterpret_cast<const __nv_bfloat16*>(&yv[j]);
+      uint4 r;
+      __nv_bfloat16* rb = reinterpret_cast<__nv_bfloat16*>(&r);
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        rb[e] = apply_bf16<OP>(xb[e], (OP == OP_ADD || OP == OP_MUL) ? yb[e] : xb[e], a.scalar);
+      o[i] = r;
+    }
+  }
+  if (blockIdx.x == 0) {
+    const uint64_t t = (n8 << 3) + threadIdx.x;
+    if (t < a.n) {
+      const __nv_bfloat16* xs = reinterpret_cast<const __nv_bfloat16*>(p0);
+      const __nv_bfloat16* ys = reinterpret_cast<const __nv_bfloat16*>(p1);
+      reinterpret_cast<__nv_bfloat16*>(a.out)[t] =
+          apply_bf16<OP>(xs[t], (OP == OP_ADD || OP == OP_MUL) ? ys[t] : xs[t], a.scalar);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------- REDUCE_SUM f32
+// One warp per row of `cols` floats; per-lane float64 accumulation in a fixed order, then a fixed
+// xor-shuffle tree; one rounding to f32. No atomics: every arm produces identical bits.
+static constexpr int kReduceThreads = 256;
+
+__global__ void __launch_bounds__(kReduceThreads) k_reduce_sum_f32(const __grid_constant__ ElemArgs a) {
+  CGX_PROLOGUE(a, p0, p1)
+  (void)p1;
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t rows = a.n / a.cols;
+  const uint64_t r = (uint64_t)blockIdx.x * (kReduceThreads / 32) + warp;
+  if (r >= rows) return;
+  const float4* row = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(p0) + r * a.cols);
+  const uint32_t c4 = a.cols >> 2;
+  double acc = 0.0;
+  for (uint32_t c = lane; c < c4; c += 32) {
+    const float4 v = row[c];
+    acc += (double)v.x;
+    acc += (double)v.y;
+    acc += (double)v.z;
+    acc += (double)v.w;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (lane == 0) reinterpret_cast<float*>(a.out)[r] = __double2float_rn(acc);
+}
+
+// ---------------------------------------------------------------------------- multi-tensor copy
+// COPY arm: ph_j <- y_j for every tensor whose fresh source differs from
+// its placeholder. Work is split into fixed-size chunks through a static device chunk map; each
+// CTA walks chunks with a grid stride, moving 16-B vectors with kCopyVec loads in flight per thread
+// before the matching stores; the <16-B tail of a tensor is copied bytewise by the first lanes.
+static constexpr int kCopyThreads = 256;
+static constexpr int kCopyVec = 8;
+
+template <int CAP>
+__global__ void __launch_bounds__(kCopyThreads) k_copy(const __grid_constant__ CopyArgs<CAP> a) {
+  for (uint32_t c = blockIdx.x; c < a.n_chunks; c += gridDim.x) {
+    const uint32_t t = __ldg(a.chunk_tensor + c);
+    const CopyDesc d = a.desc[t];
+    const char* src = reinterpret_cast<const char*>(a.src[t]);
+    char* dst = reinterpret_cast<char*>(d.dst);
+    if (src == dst) continue;                                   // SURVEY reading 1
+    const uint64_t off = (uint64_t)(c - d.chunk_begin) * a.chunk_bytes;
+    const uint64_t rem = d.nbytes - off;
+    const uint64_t len = rem < a.chunk_bytes ? rem : a.chunk_bytes;
+    const uint64_t nv = len >> 4;
+    const int4* s4 = reinterpret_cast<const int4*>(src + off);
+    int4* d4 = reinterpret_cast<int4*>(dst + off);
+    for (uint64_t v0 = threadIdx.x; v0 < nv; v0 += (uint64_t)kCopyThreads * kCopyVec) {
+      int4 buf[kCopyVec];
+#pragma unroll
+      for (int j = 0; j < kCopyVec; ++j) {
+        const uint64_t v = v0 + (uint64_t)j * kCopyThreads;
+        if (v < nv) buf[j] = ld_stream16(s4 + v);
+      }
+#pragma unroll
+      for (int j = 0; j < kCopyVec; ++j) {
+        const uint64_t v = v0 + (uint64_t)j * kCopyThreads;
+        if (v < nv) st_stream16(d4 + v, buf[j]);
+      }
+    }
+    const uint64_t tail = len & 15;
+    if (threadIdx.x < tail) dst[off + (nv << 4) + threadIdx.x] = src[off + (nv << 4) + threadIdx.x];
+  }
+}
+
+// ---------------------------------------------------------------------------- INDIRECT roots
+template <int CAP>
+__global__ void k_table_write(const __grid_constant__ TableWriteArgs<CAP> a) {
+  pdl_trigger();   // consumers fetch the table only after their own griddepcontrol.wait
+  for (uint32_t i = threadIdx.x; i < a.n; i += blockDim.x) a.table[i] = a.ptr[i];
+}
+
+__global__ void k_table_mapped(const __grid_constant__ MappedTableArgs a) {
+  __shared__ unsigned long long s_seq;
+  pdl_trigger();
+  if (threadIdx.x == 0) s_seq = *a.seq;
+  __syncthreads();
+  const uint32_t slot = (uint32_t)(s_seq % a.ring);
+  const uint64_t* src = a.staging + (uint64_t)slot * a.n_pad;
+  for (uint32_t i = threadIdx.x; i < a.n; i += blockDim.x) {
+    uint64_t v;
+    asm volatile("ld.volatile.global.u64 %0, [%1];\n" : "=l"(v) : "l"(src + i));
+    a.table[i] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *a.seq = s_seq + 1;
+    __threadfence_system();
+    asm volatile("st.volatile.global.u64 [%0], %1;\n" :: "l"(a.ack), "l"(s_seq + 1) : "memory");
+  }
+}
+
+// ---------------------------------------------------------------------------- utilities
+__global__ void k_empty() {}
+
+struct FillArgs { float* out; uint64_t n; uint64_t base; };
+__global__ void k_fill_uniform_f32(const __grid_constant__ FillArgs a) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = splitmix_mix(a.base + i) >> 40;           // synth.splitmix recipe
+    a.out[i] = __fsub_rn(__fmul_rn((float)k, 0x1p-23f), 1.0f);  // exact: k*2^-23 - 1
+  }
+}
+
+// ---------------------------------------------------------------------------- handles
+const void* kfn_elem(int op, int dtype) {
+  if (dtype == 0) {
+    switch (op) {
+      case OP_ADD: return (const void*)k_elem_f32<OP_ADD>;
+      case OP_MUL: return (const void*)k_elem_f32<OP_MUL>;
+      case OP_SCALE: return (const void*)k_elem_f32<OP_SCALE>;
+      case OP_COPY: return (const void*)k_elem_f32<OP_COPY>;
+    }
+  } else {
+    switch (op) {
+      case OP_ADD: return (const void*)k_elem_bf16<OP_ADD>;
+      case OP_MUL: return (const void*)k_elem_bf16<OP_MUL>;
+      case OP_SCALE: return (const void*)k_elem_bf16<OP_SCALE>;
+      case OP_COPY: return (const void*)k_elem_bf16<OP_COPY>;
+    }
+  }
+  return nullptr;
+}
+const void* kfn_reduce_sum_f32() { return (const void*)k_reduce_sum_f32; }
+const void* kfn_copy(int cap) {
+  if (cap <= 8) return (const void*)k_copy<8>;
+  if (cap <= 64) return (const void*)k_copy<64>;
+  return (const void*)k_copy<1024>;
+}
+const void* kfn_table_write(int cap) {
+  if (cap <= 8) return (const void*)k_table_write<8>;
+  if (cap <= 64) return (const void*)k_table_write<64>;
+  return (const void*)k_table_write<512>;
+}
+const void* kfn_table_mapped() { return (const void*)k_table_mapped; }
+const void* kfn_empty() { return (const void*)k_empty; }
+const void* kfn_fill_uniform_f32() { return (const void*)k_fill_uniform_f32; }
+int elem_block_threads() { return kElemThreads; }
+
+}  // namespace cgx

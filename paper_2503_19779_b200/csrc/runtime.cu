@@ -1,0 +1,1269 @@
+// cgx runtime: chain description, capture/instantiate/replay, the four rebinding arms, the
+// selector, and measurement helpers. Implements include/cgx.h.
+//
+// Design (B200-first):
+//  * One by-value parameter struct per kernel node. A node's parameter image is kept on the host
+//    (Launch::args) together with the byte offsets of its external pointer fields, so
+//      EAGER      patches the images and launches K kernels from the host,
+//      SETPARAMS  patches the images and calls cudaGraphExecKernelNodeSetParams per node,
+//      STALE      does that once, at the first bind (recorded by value),
+//      COPY       captures placeholder addresses and launches one multi-tensor copy kernel per
+//                 bind,
+//      INDIRECT   captures table indices; bind patches the device pointer table.
+//  * Capture = stream capture on a private stream with programmatic-dependent-launch edges
+//    (so NCCL collectives can be captured too); node handles are taken from
+//    cudaStreamGetCaptureInfo right after each launch.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <unordered_set>
+#include <vector>
+
+#include "../../include/cgx.h"
+#include "cgx_args.h"
+#include "cgx_decoder.h"
+
+using namespace cgx;
+
+// ============================================================================ errors
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+static int cuda_fail(cudaError_t e, const char* what, int line) {
+  char buf[512];
+  snprintf(buf, sizeof(buf), "%s failed (runtime.cu:%d): %s (%s)", what, line, cudaGetErrorString(e),
+           cudaGetErrorName(e));
+  g_err = buf;
+  return CGX_E_CUDA;
+}
+#define CK(expr)                                                   \
+  do {                                                             \
+    cudaError_t _e = (expr);                                       \
+    if (_e != cudaSuccess) return cuda_fail(_e, #expr, __LINE__);  \
+  } while (0)
+#define CKS(expr)                                                  \
+  do {                                                             \
+    int _s = (expr);                                               \
+    if (_s != CGX_OK) return _s;                                   \
+  } while (0)
+
+extern "C" int cgx_version(void) { return CGX_ABI_VERSION; }
+extern "C" const char* cgx_last_error(void) { return g_err.c_str(); }
+
+// ============================================================================ small utilities
+namespace {
+
+struct AlignedBuf {  // 64-B aligned byte buffer (CUtensorMap params need 64-B alignment)
+  uint8_t* p = nullptr;
+  size_t n = 0;
+  AlignedBuf() = default;
+  explicit AlignedBuf(size_t bytes) { reset(bytes); }
+  AlignedBuf(const AlignedBuf&) = delete;
+  AlignedBuf& operator=(const AlignedBuf&) = delete;
+  AlignedBuf(AlignedBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  AlignedBuf& operator=(AlignedBuf&& o) noexcept {
+    std::swap(p, o.p);
+    std::swap(n, o.n);
+    return *this;
+  }
+  void reset(size_t bytes) {
+    free(p);
+    n = bytes;
+    p = static_cast<uint8_t*>(aligned_alloc(64, ((bytes + 63) / 64) * 64));
+    memset(p, 0, n);
+  }
+  ~AlignedBuf() { free(p); }
+};
+
+inline double now_us() {
+  return std::chrono::duration<double, std::micro>(
+             std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+inline uint64_t host_mix(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+inline uint64_t ceil_div(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+}  // namespace
+
+// ============================================================================ chain
+struct Slot {
+  cgx_slot_kind kind;
+  cgx_dtype dtype;
+  uint64_t nelems, nbytes;
+  void* static_ptr;   // STATIC
+  void* buf;          // INTERNAL (chain arena)
+  int ext_j;          // EXTERNAL index (declaration order), else -1
+};
+
+struct Node {
+  cgx_op op;
+  int in[CGX_MAX_IN];
+  int n_in;
+  int out;
+  cgx_attr attr;
+};
+
+struct cgx_chain {
+  int device = 0;
+  std::vector<Slot> slots;
+  std::vector<Node> nodes;
+  std::vector<std::pair<int, int>> segments;
+  std::vector<int> ext_slots;   // j -> slot
+  void* nccl = nullptr;
+  void* arena = nullptr;        // internal buffers
+  bool allocated = false;
+  int live_execs = 0;
+};
+
+static size_t dtype_size(cgx_dtype d) { return d == CGX_F32 ? 4 : 2; }
+
+extern "C" int cgx_chain_create(int device, cgx_chain** out) {
+  if (!out) return fail(CGX_E_INVALID_ARG, "cgx_chain_create: out is NULL");
+  int n = 0;
+  CK(cudaGetDeviceCount(&n));
+  if (device < 0 || device >= n) return fail(CGX_E_INVALID_ARG, "cgx_chain_create: bad device");
+  auto* c = new cgx_chain();
+  c->device = device;
+  *out = c;
+  return CGX_OK;
+}
+
+extern "C" int cgx_chain_add_slot(cgx_chain* c, cgx_slot_kind kind, cgx_dtype dtype, uint64_t nelems,
+                                  void* static_dptr, int* slot_out) {
+  if (!c) return fail(CGX_E_INVALID_ARG, "add_slot: chain is NULL");
+  if (c->allocated) return fail(CGX_E_STATE, "add_slot: chain already captured");
+  if (kind < CGX_SLOT_EXTERNAL || kind > CGX_SLOT_INTERNAL) return fail(CGX_E_INVALID_ARG, "add_slot: kind");
+  if (dtype != CGX_F32 && dtype != CGX_BF16) return fail(CGX_E_INVALID_ARG, "add_slot: dtype");
+  if (nelems == 0) return fail(CGX_E_INVALID_ARG, "add_slot: nelems == 0");
+  if ((kind == CGX_SLOT_STATIC) != (static_dptr != nullptr))
+    return fail(CGX_E_INVALID_ARG, "add_slot: static_dptr must be given for STATIC slots only");
+  if (static_dptr && (reinterpret_cast<uintptr_t>(static_dptr) & 15))
+    return fail(CGX_E_MISALIGNED, "add_slot: static buffer not 16-byte aligned");
+  Slot s{kind, dtype, nelems, nelems * dtype_size(dtype), static_dptr, nullptr, -1};
+  if (kind == CGX_SLOT_EXTERNAL) {
+    s.ext_j = (int)c->ext_slots.size();
+    c->ext_slots.push_back((int)c->slots.size());
+  }
+  c->slots.push_back(s);
+  if (slot_out) *slot_out = (int)c->slots.size() - 1;
+  return CGX_OK;
+}
+
+static int check_node(const cgx_chain* c, const Node& n) {
+  auto S = [&](int i) -> const Slot& { return c->slots[n.in[i]]; };
+  const Slot& o = c->slots[n.out];
+  const cgx_attr& a = n.attr;
+  auto need = [&](bool ok, const char* m) { return ok ? CGX_OK : fail(CGX_E_SIZE_MISMATCH, m); };
+  switch (n.op) {
+    case CGX_OP_ADD:
+    case CGX_OP_MUL:
+    case CGX_OP_SCALE_IMM:
+    case CGX_OP_COPY: {
+      int nin = (n.op == CGX_OP_ADD || n.op == CGX_OP_MUL) ? 2 : 1;
+      if (n.n_in != nin) return fail(CGX_E_INVALID_ARG, "elementwise: wrong number of inputs");
+      for (int i = 0; i < nin; ++i) {
+        if (S(i).dtype != o.dtype) return fail(CGX_E_UNSUPPORTED, "elementwise: mixed dtypes");
+        CKS(need(S(i).nelems >= a.n, "elementwise: input shorter than attr.n"));
+      }
+      return need(o.nelems >= a.n, "elementwise: output shorter than attr.n");
+    }
+    case CGX_OP_REDUCE_SUM:
+      if (n.n_in != 1) return fail(CGX_E_INVALID_ARG, "reduce: one input");
+      if (S(0).dtype != CGX_F32 || o.dtype != CGX_F32) return fail(CGX_E_UNSUPPORTED, "reduce: f32 only");
+      if (a.cols == 0 || a.cols % 4 || a.n % a.cols) return fail(CGX_E_SIZE_MISMATCH, "reduce: cols must divide n, cols % 4 == 0");
+      CKS(need(S(0).nelems >= a.n, "reduce: input shorter than n"));
+      return need(o.nelems >= a.n / a.cols, "reduce: output shorter than n/cols");
+    case CGX_OP_LAYERNORM:
+      if (n.n_in != 3) return fail(CGX_E_INVALID_ARG, "layernorm: inputs x, gamma, beta");
+      for (int i = 0; i < 3; ++i)
+        if (S(i).dtype != CGX_BF16) return fail(CGX_E_UNSUPPORTED, "layernorm: bf16 only");
+      if (o.dtype != CGX_BF16) return fail(CGX_E_UNSUPPORTED, "layernorm: bf16 only");
+      CKS(need(a.rows > 0 && a.cols > 0 && a.cols % 8 == 0 && a.cols <= 8192, "layernorm: cols % 8, <= 8192"));
+      CKS(need(S(0).nelems >= (uint64_t)a.rows * a.cols && o.nelems >= (uint64_t)a.rows * a.cols, "layernorm: shape"));
+      return need(S(1).nelems >= a.cols && S(2).nelems >= a.cols, "layernorm: gamma/beta shape");
+    case CGX_OP_GEMM_BF16: {
+      int nin = (a.flags & CGX_GEMM_RESIDUAL) ? 4 : 3;
+      if (n.n_in != nin) return fail(CGX_E_INVALID_ARG, "gemm: inputs A, W, bias(, residual)");
+      for (int i = 0; i < nin; ++i)
+        if (S(i).dtype != CGX_BF16) return fail(CGX_E_UNSUPPORTED, "gemm: bf16 only");
+      CKS(need(S(0).nelems >= (uint64_t)a.M * a.K && S(1).nelems >= (uint64_t)a.N * a.K &&
+                   S(2).nelems >= a.N && o.nelems >= (uint64_t)a.M * a.N, "gemm: shape"));
+      return decoder_gemm_supported(a.M, a.N, a.K) ? CGX_OK
+                                                   : fail(CGX_E_UNSUPPORTED, "gemm: shape not supported by the tcgen05 kernel");
+    }
+    case CGX_OP_ATTN_CAUSAL:
+      if (n.n_in != 1) return fail(CGX_E_INVALID_ARG, "attention: one input qkv");
+      CKS(need(S(0).nelems >= (uint64_t)a.T * 3 * a.H * a.D && o.nelems >= (uint64_t)a.T * a.H * a.D, "attention: shape"));
+      return decoder_attn_supported(a.T, a.H, a.D) ? CGX_OK : fail(CGX_E_UNSUPPORTED, "attention: shape");
+    case CGX_OP_ALLREDUCE_SUM:
+      if (n.n_in != 1) return fail(CGX_E_INVALID_ARG, "allreduce: one input");
+      if (S(0).dtype != CGX_BF16 || o.dtype != CGX_BF16) return fail(CGX_E_UNSUPPORTED, "allreduce: bf16 only");
+      return need(S(0).nelems >= a.n && o.nelems >= a.n, "allreduce: shape");
+  }
+  return fail(CGX_E_INVALID_ARG, "unknown op");
+}
+
+extern "C" int cgx_chain_add_node(cgx_chain* c, cgx_op op, const int* in_slots, int n_in, int out_slot,
+                                  const cgx_attr* attr, int* node_out) {
+  if (!c) return fail(CGX_E_INVALID_ARG, "add_node: chain is NULL");
+  if (c->allocated) return fail(CGX_E_STATE, "add_node: chain already captured");
+  if (n_in < 0 || n_in > CGX_MAX_IN || (n_in > 0 && !in_slots)) return fail(CGX_E_INVALID_ARG, "add_node: inputs");
+  if (out_slot < 0 || out_slot >= (int)c->slots.size()) return fail(CGX_E_INVALID_ARG, "add_node: out slot");
+  Node n{};
+  n.op = op;
+  n.n_in = n_in;
+  n.out = out_slot;
+  if (attr) n.attr = *attr;
+  for (int i = 0; i < n_in; ++i) {
+    if (in_slots[i] < 0 || in_slots[i] >= (int)c->slots.size()) return fail(CGX_E_INVALID_ARG, "add_node: in slot");
+    n.in[i] = in_slots[i];
+  }
+  if (c->slots[out_slot].kind != CGX_SLOT_INTERNAL)
+    return fail(CGX_E_NOT_ELIGIBLE, "add_node: output must be an INTERNAL slot (no writes to inputs/weights)");
+  if ((op == CGX_OP_ADD || op == CGX_OP_MUL || op == CGX_OP_SCALE_IMM || op == CGX_OP_COPY ||
+       op == CGX_OP_REDUCE_SUM || op == CGX_OP_ALLREDUCE_SUM) && n.attr.n == 0 && n_in > 0)
+    n.attr.n = c->slots[n.in[0]].nelems;
+  if (op == CGX_OP_REDUCE_SUM && n.attr.cols == 0) n.attr.cols = 256;
+  CKS(check_node(c, n));
+  c->nodes.push_back(n);
+  if (node_out) *node_out = (int)c->nodes.size() - 1;
+  return CGX_OK;
+}
+
+extern "C" int cgx_chain_mark_segment(cgx_chain* c, int first, int last) {
+  if (!c || first < 0 || last < first || last >= (int)c->nodes.size())
+    return fail(CGX_E_INVALID_ARG, "mark_segment: bad range");
+  c->segments.push_back({first, last});
+  return CGX_OK;
+}
+
+extern "C" int cgx_chain_set_nccl(cgx_chain* c, void* comm) {
+  if (!c) return fail(CGX_E_INVALID_ARG, "set_nccl: chain is NULL");
+  c->nccl = comm;
+  return CGX_OK;
+}
+
+static int chain_allocate(cgx_chain* c) {
+  if (c->allocated) return CGX_OK;
+  CK(cudaSetDevice(c->device));
+  size_t total = 0;
+  for (auto& s : c->slots)
+    if (s.kind == CGX_SLOT_INTERNAL) total += ceil_div(s.nbytes, 256) * 256;
+  if (total) {
+    CK(cudaMalloc(&c->arena, total));
+    CK(cudaMemset(c->arena, 0, total));
+  }
+  size_t off = 0;
+  for (auto& s : c->slots)
+    if (s.kind == CGX_SLOT_INTERNAL) {
+      s.buf = static_cast<char*>(c->arena) + off;
+      off += ceil_div(s.nbytes, 256) * 256;
+    }
+  c->allocated = true;
+  return CGX_OK;
+}
+
+extern "C" int cgx_chain_destroy(cgx_chain* c) {
+  if (!c) return CGX_OK;
+  if (c->live_execs) return fail(CGX_E_STATE, "chain_destroy: execs still alive");
+  if (c->arena) cudaFree(c->arena);
+  delete c;
+  return CGX_OK;
+}
+
+// ============================================================================ exec
+namespace {
+
+enum LaunchKind { LK_KERNEL = 0, LK_NCCL = 1 };
+
+struct PtrField {  // a pointer-valued field in a node's param image
+  size_t off;      // byte offset of the void* field
+  size_t tidx_off; // byte offset of the int32 table-index field (or SIZE_MAX)
+  int ext_j;       // external index
+};
+
+struct Launch {
+  LaunchKind kind = LK_KERNEL;
+  int node = -1;
+  const void* func = nullptr;
+  dim3 grid, block;
+  size_t smem = 0;
+  bool pdl = true;
+  AlignedBuf args;
+  std::vector<PtrField> ext;  // external operand fields
+  cudaGraphNode_t gnode[2] = {nullptr, nullptr};
+  // NCCL
+  const void* nc_in = nullptr;
+  void* nc_out = nullptr;
+  size_t nc_count = 0;
+};
+
+}  // namespace
+
+struct cgx_exec {
+  cgx_chain* c = nullptr;
+  cgx_exec_opts o{};
+  cudaStream_t s = nullptr;       // replay stream (caller's)
+  cudaStream_t cs = nullptr;      // private capture stream
+  int first = 0, last = -1;       // node range (inclusive)
+  std::vector<Launch> L;
+  int n_graphs = 0;
+  cudaGraph_t g[2] = {nullptr, nullptr};
+  cudaGraphExec_t ge[2] = {nullptr, nullptr};
+  uint32_t graph_nodes = 0;
+  std::vector<int> ext_read;      // externals read by nodes in range (ordered by j)
+  std::vector<const void*> cur;   // currently bound pointers (by j)
+  bool bound = false;
+  bool stale_frozen = false;
+  bool launched_since_bind = true;   // T4: a bind before any launch reuses the pending slot
+  uint64_t seq = 0;               // binds so far
+  std::unordered_set<uintptr_t> validated;
+  cgx_stats_t st{};
+  // COPY
+  std::vector<void*> ph;          // by j (nullptr if not read)
+  void* ph_arena = nullptr;
+  CopyDesc* d_desc = nullptr;
+  uint32_t* d_chunk = nullptr;
+  uint32_t n_chunks = 0, chunk_bytes = 0;
+  int copy_cap = 0;
+  const void* copy_fn = nullptr;
+  dim3 copy_grid;
+  AlignedBuf copy_args;
+  // INDIRECT
+  uint64_t* d_table = nullptr;
+  uint64_t* h_stage = nullptr;    // pinned ring [ring][n_pad]
+  uint64_t* d_stage = nullptr;    // device alias (mapped, T4)
+  int ring = 0;
+  uint32_t n_pad = 0;
+  std::vector<cudaEvent_t> ev;
+  std::vector<bool> ev_used;
+  // T3 / T4 root
+  const void* root_fn = nullptr;
+  AlignedBuf root_args;
+  cudaGraphNode_t root_node[2] = {nullptr, nullptr};
+  unsigned long long* d_seq = nullptr;
+  volatile unsigned long long* h_ack = nullptr;
+  unsigned long long* d_ack = nullptr;
+};
+
+static cgx_transport eff_transport(const cgx_exec_opts& o) {
+  return o.transport == CGX_XPORT_DEFAULT ? CGX_XPORT_ROOT_PARAMS : o.transport;
+}
+
+template <typename T>
+static T* argp(Launch& l) { return reinterpret_cast<T*>(l.args.p); }
+
+// Build the launch record of one node. Operand addresses are resolved for `mode`:
+// EXTERNAL -> placeholder (COPY), table index (INDIRECT), or a patchable field (others).
+static int build_launch(cgx_exec* e, int k, Launch& l) {
+  cgx_chain* c = e->c;
+  const Node& n = c->nodes[k];
+  const cgx_mode mode = e->o.mode;
+  l.node = k;
+  l.pdl = !e->o.no_pdl;
+  auto slot_ptr = [&](int si) -> void* {
+    const Slot& s = c->slots[si];
+    if (s.kind == CGX_SLOT_STATIC) return s.static_ptr;
+    if (s.kind == CGX_SLOT_INTERNAL) return s.buf;
+    if (mode == CGX_MODE_GRAPH_COPY) return e->ph[s.ext_j];
+    return const_cast<void*>(e->cur[s.ext_j]);   // EAGER/SETPARAMS/STALE: patched at bind
+  };
+  auto is_ext = [&](int si) { return c->slots[si].kind == CGX_SLOT_EXTERNAL; };
+  const bool indirect = mode == CGX_MODE_GRAPH_INDIRECT;
+  const bool patch = mode == CGX_MODE_EAGER || mode == CGX_MODE_GRAPH_SETPARAMS || mode == CGX_MODE_GRAPH_STALE;
+
+  switch (n.op) {
+    case CGX_OP_ADD:
+    case CGX_OP_MUL:
+    case CGX_OP_SCALE_IMM:
+    case CGX_OP_COPY:
+    case CGX_OP_REDUCE_SUM: {
+      l.args.reset(sizeof(ElemArgs));
+      ElemArgs* a = argp<ElemArgs>(l);
+      a->table = indirect ? e->d_table : nullptr;
+      a->t0 = a->t1 = -1;
+      a->out = slot_ptr(n.out);
+      a->n = n.attr.n;
+      a->scalar = n.attr.scalar;
+      a->cols = n.attr.cols;
+      const void** ins[2] = {&a->in0, &a->in1};
+      int32_t* tid[2] = {&a->t0, &a->t1};
+      for (int i = 0; i < n.n_in && i < 2; ++i) {
+        *ins[i] = slot_ptr(n.in[i]);
+        if (is_ext(n.in[i])) {
+          const int j = c->slots[n.in[i]].ext_j;
+          if (indirect) {
+            *ins[i] = nullptr;
+            *tid[i] = j;
+          } else if (patch) {
+            l.ext.push_back({(size_t)((uint8_t*)ins[i] - l.args.p), (size_t)((uint8_t*)tid[i] - l.args.p), j});
+          }
+        }
+      }
+      if (n.op == CGX_OP_REDUCE_SUM) {
+        l.func = kfn_reduce_sum_f32();
+        l.block = dim3(256);
+        l.grid = dim3((unsigned)std::max<uint64_t>(1, ceil_div(n.attr.n / n.attr.cols, 8)));
+      } else {
+        const int opi = n.op == CGX_OP_ADD ? 0 : n.op == CGX_OP_MUL ? 1 : n.op == CGX_OP_SCALE_IMM ? 2 : 3;
+        const int dt = c->slots[n.out].dtype == CGX_F32 ? 0 : 1;
+        l.func = kfn_elem(opi, dt);
+        l.block = dim3(elem_block_threads());
+        const uint64_t per_vec = dt == 0 ? 4 : 8;
+        const uint64_t nv = n.attr.n / per_vec;
+        l.grid = dim3((unsigned)std::max<uint64_t>(1, ceil_div(nv, (uint64_t)elem_block_threads() * 4)));
+      }
+      return CGX_OK;
+    }
+    case CGX_OP_LAYERNORM: {
+      l.args.reset(sizeof(LnArgs));
+      LnArgs* a = argp<LnArgs>(l);
+      a->table = indirect ? e->d_table : nullptr;
+      a->tx = -1;
+      a->x = slot_ptr(n.in[0]);
+      a->g = slot_ptr(n.in[1]);
+      a->b = slot_ptr(n.in[2]);
+      a->out = slot_ptr(n.out);
+      a->rows = n.attr.rows;
+      a->cols = n.attr.cols;
+      a->eps = n.attr.eps;
+      if (is_ext(n.in[1]) || is_ext(n.in[2])) return fail(CGX_E_UNSUPPORTED, "layernorm: external gamma/beta");
+      if (is_ext(n.in[0])) {
+        const int j = c->slots[n.in[0]].ext_j;
+        if (indirect) {
+          a->x = nullptr;
+          a->tx = j;
+        } else if (patch) {
+          l.ext.push_back({offsetof(LnArgs, x), offsetof(LnArgs, tx), j});
+        }
+      }
+      decoder_ln_launch_dims(n.attr.rows, n.attr.cols, &l.grid, &l.block);
+      l.func = kfn_layernorm();
+      return CGX_OK;
+    }
+    case CGX_OP_GEMM_BF16: {
+      for (int i = 0; i < n.n_in; ++i)
+        if (is_ext(n.in[i])) {
+          if (indirect)
+            return fail(CGX_E_UNSUPPORTED, "gemm: an EXTERNAL operand of a GEMM needs the prelude path (NEXT-1)");
+          if (i != 0 && i != 3) return fail(CGX_E_UNSUPPORTED, "gemm: external weights");
+        }
+      void* A = slot_ptr(n.in[0]);
+      void* W = slot_ptr(n.in[1]);
+      void* bias = slot_ptr(n.in[2]);
+      void* res = (n.attr.flags & CGX_GEMM_RESIDUAL) ? slot_ptr(n.in[3]) : nullptr;
+      size_t argbytes = 0;
+      CKS(decoder_gemm_build(n.attr.M, n.attr.N, n.attr.K, n.attr.flags, A, W, bias, res, slot_ptr(n.out),
+                             nullptr, &argbytes, &l.grid, &l.block, &l.smem, &l.func));
+      l.args.reset(argbytes);
+      CKS(decoder_gemm_build(n.attr.M, n.attr.N, n.attr.K, n.attr.flags, A, W, bias, res, slot_ptr(n.out),
+                             l.args.p, &argbytes, &l.grid, &l.block, &l.smem, &l.func));
+      if (patch && (is_ext(n.in[0]) || ((n.attr.flags & CGX_GEMM_RESIDUAL) && is_ext(n.in[3]))))
+        return fail(CGX_E_UNSUPPORTED, "gemm: external A/residual needs a rebuilt tensor map");
+      return CGX_OK;
+    }
+    case CGX_OP_ATTN_CAUSAL: {
+      if (is_ext(n.in[0])) return fail(CGX_E_UNSUPPORTED, "attention: external qkv");
+      l.args.reset(sizeof(AttnArgs));
+      AttnArgs* a = argp<AttnArgs>(l);
+      a->qkv = slot_ptr(n.in[0]);
+      a->out = slot_ptr(n.out);
+      a->T = n.attr.T;
+      a->H = n.attr.H;
+      a->D = n.attr.D;
+      a->scale = n.attr.scalar;
+      decoder_attn_launch_dims(n.attr.T, n.attr.H, n.attr.D, &l.grid, &l.block, &l.smem);
+      l.func = kfn_attention();
+      return CGX_OK;
+    }
+    case CGX_OP_ALLREDUCE_SUM: {
+      if (is_ext(n.in[0])) return fail(CGX_E_UNSUPPORTED, "allreduce: external input");
+      if (!c->nccl) return fail(CGX_E_STATE, "allreduce: no NCCL communicator (cgx_chain_set_nccl)");
+      l.kind = LK_NCCL;
+      l.nc_in = slot_ptr(n.in[0]);
+      l.nc_out = slot_ptr(n.out);
+      l.nc_count = n.attr.n;
+      return CGX_OK;
+    }
+  }
+  return fail(CGX_E_INVALID_ARG, "build_launch: unknown op");
+}
+
+static int issue(cgx_exec* e, Launch& l, cudaStream_t s) {
+  if (l.kind == LK_NCCL) {
+    ncclResult_t r = ncclAllReduce(l.nc_in, l.nc_out, l.nc_count, ncclBfloat16, ncclSum,
+                                   static_cast<ncclComm_t>(e->c->nccl), s);
+    if (r != ncclSuccess) return fail(CGX_E_NCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(r));
+    return CGX_OK;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = l.grid;
+  cfg.blockDim = l.block;
+  cfg.dynamicSmemBytes = l.smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  if (l.pdl) {
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  void* argv[1] = {l.args.p};
+  CK(cudaLaunchKernelExC(&cfg, l.func, argv));
+  return CGX_OK;
+}
+
+static int last_captured_node(cudaStream_t cs, cudaGraphNode_t* out) {
+  cudaStreamCaptureStatus status;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  CK(cudaStreamGetCaptureInfo(cs, &status, nullptr, nullptr, &deps, &nd));
+  if (status != cudaStreamCaptureStatusActive || nd != 1)
+    return fail(CGX_E_CUDA, "capture: could not identify the captured node");
+  *out = deps[0];
+  return CGX_OK;
+}
+
+// ---------------------------------------------------------------------------- COPY plan
+static int setup_copy(cgx_exec* e) {
+  cgx_chain* c = e->c;
+  const int n_ext = (int)c->ext_slots.size();
+  e->ph.assign(n_ext, nullptr);
+  size_t total = 0;
+  uint64_t data = 0;
+  for (int j : e->ext_read) {
+    total += ceil_div(c->slots[c->ext_slots[j]].nbytes, 256) * 256;
+    data += c->slots[c->ext_slots[j]].nbytes;
+  }
+  if (total) CK(cudaMalloc(&e->ph_arena, total));
+  size_t off = 0;
+  for (int j : e->ext_read) {
+    e->ph[j] = static_cast<char*>(e->ph_arena) + off;
+    off += ceil_div(c->slots[c->ext_slots[j]].nbytes, 256) * 256;
+  }
+  const int nt = (int)e->ext_read.size();
+  if (nt > 1024) return fail(CGX_E_UNSUPPORTED, "COPY: more than 1024 external tensors");
+  // chunk size: spread the bytes over ~8 CTAs per SM, 16 KiB..256 KiB, 4 KiB multiple
+  uint64_t cb = ceil_div(data, 148ull * 8);
+  cb = std::min<uint64_t>(std::max<uint64_t>(cb, 16384), 262144);
+  cb = ceil_div(cb, 4096) * 4096;
+  e->chunk_bytes = (uint32_t)cb;
+  std::vector<CopyDesc> desc(nt);
+  std::vector<uint32_t> chunk;
+  for (int t = 0; t < nt; ++t) {
+    const Slot& s = c->slots[c->ext_slots[e->ext_read[t]]];
+    desc[t].dst = e->ph[e->ext_read[t]];
+    desc[t].nbytes = s.nbytes;
+    desc[t].chunk_begin = (uint32_t)chunk.size();
+    desc[t].n_chunks = (uint32_t)std::max<uint64_t>(1, ceil_div(s.nbytes, cb));
+    for (uint32_t q = 0; q < desc[t].n_chunks; ++q) chunk.push_back((uint32_t)t);
+  }
+  e->n_chunks = (uint32_t)chunk.size();
+  if (nt) {
+    CK(cudaMalloc(&e->d_desc, sizeof(CopyDesc) * nt));
+    CK(cudaMemcpy(e->d_desc, desc.data(), sizeof(CopyDesc) * nt, cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&e->d_chunk, sizeof(uint32_t) * chunk.size()));
+    CK(cudaMemcpy(e->d_chunk, chunk.data(), sizeof(uint32_t) * chunk.size(), cudaMemcpyHostToDevice));
+  }
+  e->copy_cap = nt <= 8 ? 8 : nt <= 64 ? 64 : 1024;
+  e->copy_fn = kfn_copy(e->copy_cap);
+  e->copy_grid = dim3(std::max<uint32_t>(1, std::min<uint32_t>(e->n_chunks, 148 * 8)));
+  const size_t hdr = offsetof(CopyArgs<8>, src);
+  e->copy_args.reset(hdr + sizeof(void*) * e->copy_cap);
+  CopyArgs<8>* a = reinterpret_cast<CopyArgs<8>*>(e->copy_args.p);   // header layout is CAP-independent
+  a->desc = e->d_desc;
+  a->chunk_tensor = e->d_chunk;
+  a->n_tensors = (uint32_t)nt;
+  a->n_chunks = e->n_chunks;
+  a->chunk_bytes = e->chunk_bytes;
+  return CGX_OK;
+}
+
+// ---------------------------------------------------------------------------- INDIRECT setup
+static int setup_table(cgx_exec* e) {
+  const int n = (int)e->c->ext_slots.size();
+  const int nalloc = std::max(n, 1);
+  CK(cudaMalloc(&e->d_table, sizeof(uint64_t) * ((nalloc + 15) / 16) * 16));
+  CK(cudaMemset(e->d_table, 0, sizeof(uint64_t) * nalloc));
+  const cgx_transport t = eff_transport(e->o);
+  e->n_pad = (uint32_t)(((nalloc + 15) / 16) * 16);   // 128-B aligned ring slots
+  if (t == CGX_XPORT_H2D || t == CGX_XPORT_ROOT_MEMCPY || t == CGX_XPORT_ROOT_MAPPED) {
+    e->ring = t == CGX_XPORT_ROOT_MEMCPY ? 2 : 4;
+    const unsigned flags = t == CGX_XPORT_ROOT_MAPPED ? cudaHostAllocMapped : cudaHostAllocDefault;
+    CK(cudaHostAlloc((void**)&e->h_stage, sizeof(uint64_t) * e->n_pad * e->ring, flags));
+    memset(e->h_stage, 0, sizeof(uint64_t) * e->n_pad * e->ring);
+    if (t != CGX_XPORT_ROOT_MAPPED) {
+      e->ev.resize(e->ring);
+      e->ev_used.assign(e->ring, false);
+      for (auto& v : e->ev) CK(cudaEventCreateWithFlags(&v, cudaEventDisableTiming));
+    } else {
+      CK(cudaHostGetDevicePointer((void**)&e->d_stage, e->h_stage, 0));
+      unsigned long long* hack = nullptr;
+      CK(cudaHostAlloc((void**)&hack, 64, cudaHostAllocMapped));
+      *hack = 0;
+      e->h_ack = hack;
+      CK(cudaHostGetDevicePointer((void**)&e->d_ack, hack, 0));
+      CK(cudaMalloc(&e->d_seq, 64));
+      CK(cudaMemset(e->d_seq, 0, 64));
+    }
+  }
+  if (t == CGX_XPORT_ROOT_PARAMS) {
+    if (n > 512) return fail(CGX_E_UNSUPPORTED, "ROOT_PARAMS transport: more than 512 externals");
+    const int cap = n <= 8 ? 8 : n <= 64 ? 64 : 512;
+    e->root_fn = kfn_table_write(cap);
+    e->root_args.reset(offsetof(TableWriteArgs<8>, ptr) + sizeof(uint64_t) * cap);
+    auto* a = reinterpret_cast<TableWriteArgs<8>*>(e->root_args.p);
+    a->table = e->d_table;
+    a->n = (uint32_t)n;
+  } else if (t == CGX_XPORT_ROOT_MAPPED) {
+    e->root_fn = kfn_table_mapped();
+    e->root_args.reset(sizeof(MappedTableArgs));
+    auto* a = reinterpret_cast<MappedTableArgs*>(e->root_args.p);
+    a->staging = e->d_stage;
+    a->table = e->d_table;
+    a->seq = e->d_seq;
+    a->ack = e->d_ack;
+    a->n = (uint32_t)n;
+    a->n_pad = e->n_pad;
+    a->ring = (uint32_t)e->ring;
+  }
+  return CGX_OK;
+}
+
+static int capture_graph(cgx_exec* e, int gi) {
+  cudaStream_t cs = e->cs;
+  CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+  const cgx_transport t = eff_transport(e->o);
+  bool after_root = false;
+  bool root_is_copy = false;
+  if (e->o.mode == CGX_MODE_GRAPH_INDIRECT) {
+    const size_t tb = sizeof(uint64_t) * std::max<size_t>(1, e->c->ext_slots.size());
+    if (t == CGX_XPORT_ROOT_MEMCPY) {
+      CK(cudaMemcpyAsync(e->d_table, e->h_stage + (size_t)gi * e->n_pad, tb, cudaMemcpyHostToDevice, cs));
+      after_root = root_is_copy = true;
+    } else if (t == CGX_XPORT_ROOT_PARAMS || t == CGX_XPORT_ROOT_MAPPED) {
+      Launch r;
+      r.func = e->root_fn;
+      r.grid = dim3(1);
+      r.block = dim3(t == CGX_XPORT_ROOT_MAPPED ? 64 : 128);
+      r.pdl = false;
+      r.args.reset(e->root_args.n);
+      memcpy(r.args.p, e->root_args.p, e->root_args.n);
+      CKS(issue(e, r, cs));
+      CKS(last_captured_node(cs, &e->root_node[gi]));
+      after_root = true;
+    }
+  }
+  bool first_kernel = true;
+  for (auto& l : e->L) {
+    if (l.kind == LK_KERNEL && first_kernel && after_root) {
+      // the first consumer after a root node fetches table entries after its wait
+      if (e->o.mode == CGX_MODE_GRAPH_INDIRECT) {
+        // ElemArgs/LnArgs both keep `flags` right after the operand fields; set per type
+        const Node& n = e->c->nodes[l.node];
+        if (n.op == CGX_OP_LAYERNORM) argp<LnArgs>(l)->flags |= kFlagTableAfterWait;
+        else if (n.op <= CGX_OP_REDUCE_SUM) argp<ElemArgs>(l)->flags |= kFlagTableAfterWait;
+      }
+      if (root_is_copy) l.pdl = false;
+    }
+    if (l.kind == LK_KERNEL) first_kernel = false;
+    CKS(issue(e, l, cs));
+    if (l.kind == LK_KERNEL) CKS(last_captured_node(cs, &l.gnode[gi]));
+  }
+  CK(cudaStreamEndCapture(cs, &e->g[gi]));
+  CK(cudaGraphInstantiateWithFlags(&e->ge[gi], e->g[gi], 0));
+  CK(cudaGraphUpload(e->ge[gi], e->s));
+  size_t nn = 0;
+  CK(cudaGraphGetNodes(e->g[gi], nullptr, &nn));
+  e->graph_nodes = (uint32_t)nn;
+  return CGX_OK;
+}
+
+static void exec_free(cgx_exec* e) {
+  for (int i = 0; i < 2; ++i) {
+    if (e->ge[i]) cudaGraphExecDestroy(e->ge[i]);
+    if (e->g[i]) cudaGraphDestroy(e->g[i]);
+  }
+  if (e->cs) cudaStreamDestroy(e->cs);
+  if (e->ph_arena) cudaFree(e->ph_arena);
+  if (e->d_desc) cudaFree(e->d_desc);
+  if (e->d_chunk) cudaFree(e->d_chunk);
+  if (e->d_table) cudaFree(e->d_table);
+  if (e->h_stage) cudaFreeHost(e->h_stage);
+  if (e->h_ack) cudaFreeHost((void*)e->h_ack);
+  if (e->d_seq) cudaFree(e->d_seq);
+  for (auto& v : e->ev) cudaEventDestroy(v);
+  if (e->c) e->c->live_execs--;
+  delete e;
+}
+
+extern "C" int cgx_exec_create_ex(cgx_chain* c, const cgx_exec_opts* opts, void* stream, cgx_exec** out) {
+  if (!c || !out) return fail(CGX_E_INVALID_ARG, "exec_create: NULL argument");
+  cgx_exec_opts o{};
+  if (opts) o = *opts;
+  if (o.mode < CGX_MODE_EAGER || o.mode > CGX_MODE_GRAPH_STALE) return fail(CGX_E_INVALID_ARG, "exec_create: mode");
+  if (o.transport < CGX_XPORT_DEFAULT || o.transport > CGX_XPORT_ROOT_MAPPED)
+    return fail(CGX_E_INVALID_ARG, "exec_create: transport");
+  const int K = (int)c->nodes.size();
+  if (K == 0) return fail(CGX_E_STATE, "exec_create: empty chain");
+  const int first = o.first_node, last = o.n_nodes ? o.first_node + o.n_nodes - 1 : K - 1;
+  if (first < 0 || first >= K || last < first || last >= K) return fail(CGX_E_INVALID_ARG, "exec_create: node range");
+  CK(cudaSetDevice(c->device));
+  CKS(chain_allocate(c));
+  auto* e = new cgx_exec();
+  e->c = c;
+  c->live_execs++;
+  e->o = o;
+  e->s = static_cast<cudaStream_t>(stream);
+  e->first = first;
+  e->last = last;
+  const int n_ext = (int)c->ext_slots.size();
+  e->cur.assign(n_ext, nullptr);
+  std::vector<bool> read(n_ext, false);
+  for (int k = first; k <= last; ++k)
+    for (int i = 0; i < c->nodes[k].n_in; ++i)
+      if (c->slots[c->nodes[k].in[i]].kind == CGX_SLOT_EXTERNAL) read[c->slots[c->nodes[k].in[i]].ext_j] = true;
+  for (int j = 0; j < n_ext; ++j)
+    if (read[j]) e->ext_read.push_back(j);
+  auto bail = [&](int st) { exec_free(e); return st; };
+  int st;
+  if (o.mode == CGX_MODE_GRAPH_COPY && (st = setup_copy(e)) != CGX_OK) return bail(st);
+  if (o.mode == CGX_MODE_GRAPH_INDIRECT && (st = setup_table(e)) != CGX_OK) return bail(st);
+  e->L.resize(last - first + 1);
+  for (int k = first; k <= last; ++k)
+    if ((st = build_launch(e, k, e->L[k - first])) != CGX_OK) return bail(st);
+  if (o.mode != CGX_MODE_EAGER) {
+    cudaError_t ce = cudaStreamCreateWithFlags(&e->cs, cudaStreamNonBlocking);
+    if (ce != cudaSuccess) return bail(cuda_fail(ce, "cudaStreamCreate", __LINE__));
+    e->n_graphs = (o.mode == CGX_MODE_GRAPH_INDIRECT && eff_transport(o) == CGX_XPORT_ROOT_MEMCPY) ? 2 : 1;
+    for (int gi = 0; gi < e->n_graphs; ++gi)
+      if ((st = capture_graph(e, gi)) != CGX_OK) {
+        cudaStreamCaptureStatus cst;
+        if (cudaStreamIsCapturing(e->cs, &cst) == cudaSuccess && cst != cudaStreamCaptureStatusNone) {
+          cudaGraph_t junk;
+          cudaStreamEndCapture(e->cs, &junk);
+          if (junk) cudaGraphDestroy(junk);
+        }
+        return bail(st);
+      }
+    cudaError_t se = cudaStreamSynchronize(e->s);
+    if (se != cudaSuccess) return bail(cuda_fail(se, "upload sync", __LINE__));
+  }
+  int kernels = 0;
+  for (auto& l : e->L) kernels += l.kind == LK_KERNEL;
+  e->st.n_nodes = (uint32_t)e->L.size();
+  e->st.n_ext = (uint32_t)n_ext;
+  e->st.n_graph_nodes = e->graph_nodes;
+  e->st.mode = (uint32_t)o.mode;
+  e->st.transport = o.mode == CGX_MODE_GRAPH_INDIRECT ? (uint32_t)eff_transport(o) : 0;
+  e->st.kernels_per_replay = (uint32_t)kernels + (o.mode == CGX_MODE_GRAPH_COPY && o.copy_impl == 0 && !e->ext_read.empty()) +
+                             ((o.mode == CGX_MODE_GRAPH_INDIRECT && e->root_fn) ? 1 : 0);
+  *out = e;
+  return CGX_OK;
+}
+
+extern "C" int cgx_exec_create(cgx_chain* c, cgx_mode mode, void* stream, cgx_exec** out) {
+  cgx_exec_opts o{};
+  o.mode = mode;
+  return cgx_exec_create_ex(c, &o, stream, out);
+}
+
+extern "C" int cgx_exec_destroy(cgx_exec* e) {
+  if (!e) return CGX_OK;
+  cudaStreamSynchronize(e->s);
+  exec_free(e);
+  return CGX_OK;
+}
+
+// ---------------------------------------------------------------------------- bind
+static int validate_ptrs(cgx_exec* e, const void* const* p, int n) {
+  for (int j = 0; j < n; ++j) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p[j]);
+    if (!a) return fail(CGX_E_MISSING_INPUT, "bind: NULL input " + std::to_string(j));
+    if (a & 15) return fail(CGX_E_MISALIGNED, "bind: input " + std::to_string(j) + " not 16-byte aligned");
+    if (e->o.validate == 2) continue;
+    if (e->o.validate == 0 && e->validated.count(a)) continue;
+    cudaPointerAttributes at{};
+    cudaError_t ce = cudaPointerGetAttributes(&at, p[j]);
+    if (ce != cudaSuccess) {
+      cudaGetLastError();
+      return fail(CGX_E_NOT_ELIGIBLE, "bind: input " + std::to_string(j) + " is not a CUDA allocation");
+    }
+    if (at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged)
+      return fail(CGX_E_NOT_ELIGIBLE, "bind: input " + std::to_string(j) +
+                                          " is host memory (dangling-host-pointer hazard, P:L264-265)");
+    if (at.type == cudaMemoryTypeDevice && at.device != e->c->device)
+      return fail(CGX_E_NOT_ELIGIBLE, "bind: input " + std::to_string(j) + " lives on another device");
+    if (e->o.validate == 0) {
+      if (e->validated.size() > 65536) e->validated.clear();
+      e->validated.insert(a);
+    }
+  }
+  return CGX_OK;
+}
+
+static inline void patch_images(cgx_exec* e) {
+  for (auto& l : e->L)
+    for (auto& f : l.ext) memcpy(l.args.p + f.off, &e->cur[f.ext_j], sizeof(void*));
+}
+
+static int setparams_all(cgx_exec* e, uint32_t* calls) {
+  uint32_t n = 0;
+  for (auto& l : e->L) {
+    if (l.ext.empty()) continue;
+    cudaKernelNodeParams kp{};
+    kp.func = const_cast<void*>(l.func);
+    kp.gridDim = l.grid;
+    kp.blockDim = l.block;
+    kp.sharedMemBytes = (unsigned)l.smem;
+    void* argv[1] = {l.args.p};
+    kp.kernelParams = argv;
+    for (int gi = 0; gi < e->n_graphs; ++gi) CK(cudaGraphExecKernelNodeSetParams(e->ge[gi], l.gnode[gi], &kp));
+    ++n;
+  }
+  *calls = n;
+  return CGX_OK;
+}
+
+extern "C" int cgx_bind(cgx_exec* e, const void* const* ext, int n_ext) {
+  if (!e) return fail(CGX_E_INVALID_ARG, "bind: exec is NULL");
+  const int N = (int)e->c->ext_slots.size();
+  if (n_ext != N || (N > 0 && !ext)) return fail(CGX_E_MISSING_INPUT, "bind: expected " + std::to_string(N) + " inputs");
+  CKS(validate_ptrs(e, ext, N));
+  for (int j = 0; j < N; ++j) e->cur[j] = ext[j];
+  e->st.bytes_data_rebound = e->st.bytes_ptr_rebound = 0;
+  e->st.n_setparam_calls = e->st.n_copy_tensors = 0;
+  const cgx_chain* c = e->c;
+  switch (e->o.mode) {
+    case CGX_MODE_EAGER:
+      patch_images(e);
+      break;
+    case CGX_MODE_GRAPH_SETPARAMS:
+      patch_images(e);
+      CKS(setparams_all(e, &e->st.n_setparam_calls));
+      break;
+    case CGX_MODE_GRAPH_STALE:
+      if (!e->stale_frozen) {   // recorded by value at the first bind, never again
+        patch_images(e);
+        CKS(setparams_all(e, &e->st.n_setparam_calls));
+        e->stale_frozen = true;
+      }
+      break;
+    case CGX_MODE_GRAPH_COPY: {
+      uint64_t bytes = 0;
+      uint32_t nt = 0;
+      if (e->o.copy_impl == 1) {
+        for (int j : e->ext_read)
+          if (ext[j] != e->ph[j]) {
+            const uint64_t nb = c->slots[c->ext_slots[j]].nbytes;
+            CK(cudaMemcpyAsync(e->ph[j], ext[j], nb, cudaMemcpyDeviceToDevice, e->s));
+            bytes += nb;
+            ++nt;
+          }
+      } else if (!e->ext_read.empty()) {
+        auto* a = reinterpret_cast<CopyArgs<8>*>(e->copy_args.p);
+        const void** src = a->src;
+        for (size_t t = 0; t < e->ext_read.size(); ++t) {
+          const int j = e->ext_read[t];
+          src[t] = ext[j];
+          if (ext[j] != e->ph[j]) {
+            bytes += c->slots[c->ext_slots[j]].nbytes;
+            ++nt;
+          }
+        }
+        if (nt) {
+          cudaLaunchConfig_t cfg{};
+          cfg.gridDim = e->copy_grid;
+          cfg.blockDim = dim3(256);
+          cfg.stream = e->s;
+          void* argv[1] = {e->copy_args.p};
+          CK(cudaLaunchKernelExC(&cfg, e->copy_fn, argv));
+        }
+      }
+      e->st.bytes_data_rebound = bytes;
+      e->st.n_copy_tensors = nt;
+      break;
+    }
+    case CGX_MODE_GRAPH_INDIRECT: {
+      const cgx_transport t = eff_transport(e->o);
+      if (t == CGX_XPORT_ROOT_PARAMS) {
+        auto* a = reinterpret_cast<TableWriteArgs<8>*>(e->root_args.p);
+        memcpy(a->ptr, ext, sizeof(uint64_t) * N);
+        cudaKernelNodeParams kp{};
+        kp.func = const_cast<void*>(e->root_fn);
+        kp.gridDim = dim3(1);
+        kp.blockDim = dim3(128);
+        void* argv[1] = {e->root_args.p};
+        kp.kernelParams = argv;
+        CK(cudaGraphExecKernelNodeSetParams(e->ge[0], e->root_node[0], &kp));
+      } else if (t == CGX_XPORT_H2D) {
+        const int slot = (int)(e->seq % e->ring);
+        if (e->ev_used[slot]) CK(cudaEventSynchronize(e->ev[slot]));
+        uint64_t* h = e->h_stage + (size_t)slot * e->n_pad;
+        memcpy(h, ext, sizeof(uint64_t) * N);
+        CK(cudaMemcpyAsync(e->d_table, h, sizeof(uint64_t) * N, cudaMemcpyHostToDevice, e->s));
+        CK(cudaEventRecord(e->ev[slot], e->s));
+        e->ev_used[slot] = true;
+      } else if (t == CGX_XPORT_ROOT_MEMCPY) {
+        const int b = (int)(e->seq % 2);
+        if (e->ev_used[b]) CK(cudaEventSynchronize(e->ev[b]));   // exec b's last replay done
+        memcpy(e->h_stage + (size_t)b * e->n_pad, ext, sizeof(uint64_t) * N);
+      } else {  // ROOT_MAPPED: replay number r reads ring slot r % ring
+        if (!e->launched_since_bind) e->seq--;     // overwrite the not-yet-launched slot
+        const uint64_t need = e->seq >= (uint64_t)e->ring ? e->seq - e->ring + 1 : 0;
+        while (*e->h_ack < need) { /* slot still owned by an in-flight replay */ }
+        uint64_t* h = e->h_stage + (size_t)(e->seq % e->ring) * e->n_pad;
+        volatile uint64_t* vh = h;
+        for (int j = 0; j < N; ++j) vh[j] = reinterpret_cast<uint64_t>(ext[j]);
+      }
+      e->st.bytes_ptr_rebound = 8ull * N;
+      break;
+    }
+  }
+  e->st.total_bytes_data += e->st.bytes_data_rebound;
+  e->st.total_bytes_ptr += e->st.bytes_ptr_rebound;
+  e->st.n_binds++;
+  e->bound = true;
+  e->seq++;
+  e->launched_since_bind = false;
+  return CGX_OK;
+}
+
+extern "C" int cgx_launch(cgx_exec* e) {
+  if (!e) return fail(CGX_E_INVALID_ARG, "launch: exec is NULL");
+  if (!e->bound) return fail(CGX_E_STATE, "launch: exec was never bound (cgx_bind first)");
+  if (e->o.mode == CGX_MODE_EAGER) {
+    for (auto& l : e->L) CKS(issue(e, l, e->s));
+  } else {
+    int gi = 0;
+    const bool pingpong = e->o.mode == CGX_MODE_GRAPH_INDIRECT && eff_transport(e->o) == CGX_XPORT_ROOT_MEMCPY;
+    if (pingpong) gi = (int)((e->seq - 1) % 2);
+    if (e->o.mode == CGX_MODE_GRAPH_INDIRECT && eff_transport(e->o) == CGX_XPORT_ROOT_MAPPED &&
+        e->launched_since_bind) {
+      // a launch without a fresh bind consumes the next ring slot: republish the bound pointers
+      CKS(cgx_bind(e, e->cur.data(), (int)e->cur.size()));
+    }
+    CK(cudaGraphLaunch(e->ge[gi], e->s));
+    if (pingpong) {
+      CK(cudaEventRecord(e->ev[gi], e->s));
+      e->ev_used[gi] = true;
+    }
+  }
+  e->st.n_launches++;
+  e->launched_since_bind = true;
+  return CGX_OK;
+}
+
+extern "C" int cgx_output(cgx_exec* e, int slot, void** dptr, uint64_t* nbytes) {
+  if (!e || !dptr || slot < 0 || slot >= (int)e->c->slots.size()) return fail(CGX_E_INVALID_ARG, "output: bad argument");
+  const Slot& s = e->c->slots[slot];
+  void* p = nullptr;
+  if (s.kind == CGX_SLOT_INTERNAL) p = s.buf;
+  else if (s.kind == CGX_SLOT_EXTERNAL && e->o.mode == CGX_MODE_GRAPH_COPY) p = e->ph[s.ext_j];
+  else return fail(CGX_E_INVALID_ARG, "output: slot has no library-owned buffer in this exec");
+  if (!p) return fail(CGX_E_INVALID_ARG, "output: slot not read by this exec");
+  *dptr = p;
+  if (nbytes) *nbytes = s.nbytes;
+  return CGX_OK;
+}
+
+extern "C" int cgx_stats(const cgx_exec* e, cgx_stats_t* out) {
+  if (!e || !out) return fail(CGX_E_INVALID_ARG, "stats: NULL argument");
+  *out = e->st;
+  return CGX_OK;
+}
+
+extern "C" int cgx_debug_read_table(const cgx_exec* e, uint64_t* host_out, int n) {
+  if (!e || !host_out || n < 0) return fail(CGX_E_INVALID_ARG, "read_table: bad argument");
+  if (!e->d_table) return fail(CGX_E_STATE, "read_table: exec has no pointer table (not INDIRECT)");
+  if (n > (int)e->c->ext_slots.size()) return fail(CGX_E_INVALID_ARG, "read_table: n > N_ext");
+  CK(cudaStreamSynchronize(e->s));
+  CK(cudaMemcpy(host_out, e->d_table, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost));
+  return CGX_OK;
+}
+
+extern "C" int cgx_debug_setparam_nodes(const cgx_exec* e, int* nodes_out, int cap, int* n_out) {
+  if (!e || !n_out) return fail(CGX_E_INVALID_ARG, "setparam_nodes: bad argument");
+  int n = 0;
+  for (auto& l : e->L)
+    if (!l.ext.empty()) {
+      if (nodes_out && n < cap) nodes_out[n] = l.node;
+      ++n;
+    }
+  *n_out = n;
+  return CGX_OK;
+}
+
+// ============================================================================ selector
+// Estimates and decision: IEEE double, left to right, no contraction (built with
+// -ffp-contract=off) so they match oracle/selector.py bit for bit.
+static double est_eager(double L, const double* d, int K) {
+  double free_t = 0.0;
+  for (int k = 1; k <= K; ++k) {
+    const double issue_t = (double)k * L;
+    const double start = free_t > issue_t ? free_t : issue_t;
+    free_t = start + d[k - 1];
+  }
+  return free_t;
+}
+static double est_graph(double G, double delta, const double* d, int K, double F) {
+  double s = G;
+  for (int k = 0; k < K; ++k) s = s + (delta + d[k]);
+  return s + F;
+}
+
+extern "C" int cgx_select(const cgx_profile_t* prof, int n, cgx_decision* out, double* est) {
+  if (!prof || !out || n < 0) return fail(CGX_E_INVALID_ARG, "select: bad argument");
+  for (int i = 0; i < n; ++i) {
+    const cgx_profile_t& p = prof[i];
+    if (p.n_kernels < 0 || p.n_kernels > CGX_MAX_PROFILE_KERNELS) return fail(CGX_E_INVALID_ARG, "select: n_kernels");
+    double te, tc, ti;
+    if (p.use_measured) {
+      te = p.t_eager_us;
+      tc = p.t_copy_us;
+      ti = p.t_ind_us;
+    } else {
+      const double tg = est_graph(p.G_us, p.delta_us, p.d_us, p.n_kernels, p.F_us);
+      te = est_eager(p.L_us, p.d_us, p.n_kernels);
+      tc = tg + p.c_copy_us;
+      ti = tg + p.c_ind_us;
+    }
+    cgx_decision best = CGX_DECIDE_EAGER;
+    double bt = te;
+    if (tc < bt) { best = CGX_DECIDE_GRAPH_COPY; bt = tc; }
+    if (p.ind_available && ti < bt) { best = CGX_DECIDE_GRAPH_INDIRECT; bt = ti; }
+    out[i] = best;
+    if (est) { est[3 * i] = te; est[3 * i + 1] = tc; est[3 * i + 2] = ti; }
+  }
+  return CGX_OK;
+}
+
+// profile: implemented in profile.cu
+extern "C" int cgx_profile_impl(cgx_chain* c, int segment, const void* const* ext, int n_ext, int reps,
+                                void* stream, cgx_profile_t* out);
+extern "C" int cgx_profile(cgx_chain* c, int segment, const void* const* ext, int n_ext, int reps, void* stream,
+                           cgx_profile_t* out) {
+  return cgx_profile_impl(c, segment, ext, n_ext, reps, stream, out);
+}
+
+// ============================================================================ helpers
+extern "C" int cgx_dispatch_floor(void* stream, int reps, double* g_us, double* k_us) {
+  if (reps <= 0 || !g_us || !k_us) return fail(CGX_E_INVALID_ARG, "dispatch_floor: bad argument");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaStream_t cs;
+  CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+  void* noargs[1] = {nullptr};
+  CK(cudaLaunchKernel(kfn_empty(), dim3(1), dim3(32), noargs, 0, cs));
+  cudaGraph_t g;
+  cudaGraphExec_t ge;
+  CK(cudaStreamEndCapture(cs, &g));
+  CK(cudaGraphInstantiateWithFlags(&ge, g, 0));
+  CK(cudaGraphUpload(ge, s));
+  std::vector<double> tg, tk;
+  for (int r = 0; r < reps + 20; ++r) {
+    const double t0 = now_us();
+    CK(cudaGraphLaunch(ge, s));
+    const double t1 = now_us();
+    CK(cudaLaunchKernel(kfn_empty(), dim3(1), dim3(32), noargs, 0, s));
+    const double t2 = now_us();
+    if (r >= 20) { tg.push_back(t1 - t0); tk.push_back(t2 - t1); }
+    if (r % 64 == 63) CK(cudaStreamSynchronize(s));
+  }
+  CK(cudaStreamSynchronize(s));
+  std::sort(tg.begin(), tg.end());
+  std::sort(tk.begin(), tk.end());
+  *g_us = tg[tg.size() / 2];
+  *k_us = tk[tk.size() / 2];
+  cudaGraphExecDestroy(ge);
+  cudaGraphDestroy(g);
+  cudaStreamDestroy(cs);
+  return CGX_OK;
+}
+
+extern "C" int cgx_copy(void* dst, const void* src, uint64_t nbytes, void* stream) {
+  if ((!dst || !src) && nbytes) return fail(CGX_E_INVALID_ARG, "copy: NULL");
+  if (nbytes) CK(cudaMemcpyAsync(dst, src, nbytes, cudaMemcpyDefault, static_cast<cudaStream_t>(stream)));
+  return CGX_OK;
+}
+
+extern "C" int cgx_fill_uniform_f32(void* dptr, uint64_t n, uint64_t seed, uint64_t stream_id, void* stream) {
+  if (!dptr) return fail(CGX_E_INVALID_ARG, "fill: NULL");
+  struct { float* out; uint64_t n; uint64_t base; } a{static_cast<float*>(dptr), n,
+                                                      host_mix(seed ^ host_mix(stream_id))};
+  void* argv[1] = {&a};
+  const unsigned grid = (unsigned)std::min<uint64_t>(std::max<uint64_t>(1, ceil_div(n, 256)), 148 * 16);
+  CK(cudaLaunchKernel(kfn_fill_uniform_f32(), dim3(grid), dim3(256), argv, 0, static_cast<cudaStream_t>(stream)));
+  return CGX_OK;
+}
+
+extern "C" int cgx_nccl_unique_id(void* id_out) {
+  if (!id_out) return fail(CGX_E_INVALID_ARG, "nccl_unique_id: NULL");
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return fail(CGX_E_NCCL, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+  memcpy(id_out, &id, sizeof(id));
+  return CGX_OK;
+}
+
+extern "C" int cgx_nccl_comm_init(int nranks, int rank, const void* id, int device, void** comm_out) {
+  if (!id || !comm_out || nranks <= 0 || rank < 0 || rank >= nranks) return fail(CGX_E_INVALID_ARG, "nccl_comm_init: bad argument");
+  CK(cudaSetDevice(device));
+  ncclUniqueId uid;
+  memcpy(&uid, id, sizeof(uid));
+  ncclComm_t comm;
+  ncclResult_t r = ncclCommInitRank(&comm, nranks, uid, rank);
+  if (r != ncclSuccess) return fail(CGX_E_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+  *comm_out = comm;
+  return CGX_OK;
+}
+
+extern "C" int cgx_nccl_comm_destroy(void* comm) {
+  if (!comm) return CGX_OK;
+  ncclResult_t r = ncclCommDestroy(static_cast<ncclComm_t>(comm));
+  if (r != ncclSuccess) return fail(CGX_E_NCCL, std::string("ncclCommDestroy: ") + ncclGetErrorString(r));
+  return CGX_OK;
+}
+
+// ============================================================================ profiler (slow path)
+// P:L413-417 / L630-639: run the candidate modules of one segment, measure, and hand the numbers
+// to the pure decision function. Timings follow SURVEY §8(d) and reading 7 (5 warm-up runs, then
+// the median of `reps` iterations, three trials for the per-iteration totals).
+namespace {
+double median(std::vector<double> v) {
+  std::sort(v.begin(), v.end());
+  return v.empty() ? 0.0 : v[v.size() / 2];
+}
+}  // namespace
+
+static int time_loop(cgx_exec* e, const void* const* ext, int n_ext, bool do_bind, int n, double* us) {
+  CK(cudaStreamSynchronize(e->s));
+  const double t0 = now_us();
+  for (int i = 0; i < n; ++i) {
+    if (do_bind) CKS(cgx_bind(e, ext, n_ext));
+    CKS(cgx_launch(e));
+  }
+  CK(cudaStreamSynchronize(e->s));
+  *us = (now_us() - t0) / n;
+  return CGX_OK;
+}
+
+static int time_loop3(cgx_exec* e, const void* const* ext, int n_ext, bool do_bind, int n, double* us) {
+  std::vector<double> v(3);
+  for (int t = 0; t < 3; ++t) CKS(time_loop(e, ext, n_ext, do_bind, n, &v[t]));
+  *us = median(v);
+  return CGX_OK;
+}
+
+extern "C" int cgx_profile_impl(cgx_chain* c, int segment, const void* const* ext, int n_ext, int reps, void* stream,
+                                cgx_profile_t* out) {
+  if (!c || !out || reps <= 0) return fail(CGX_E_INVALID_ARG, "profile: bad argument");
+  int first = 0, last = (int)c->nodes.size() - 1;
+  if (segment >= 0) {
+    if (segment >= (int)c->segments.size()) return fail(CGX_E_INVALID_ARG, "profile: segment index");
+    first = c->segments[segment].first;
+    last = c->segments[segment].second;
+  }
+  const int K = last - first + 1;
+  if (K > CGX_MAX_PROFILE_KERNELS) return fail(CGX_E_UNSUPPORTED, "profile: segment too long");
+  cgx_exec_opts o{};
+  o.first_node = first;
+  o.n_nodes = K;
+  cgx_exec *ee = nullptr, *ec = nullptr, *ei = nullptr;
+  struct Guard {
+    cgx_exec** p[3];
+    ~Guard() { for (auto q : p) if (*q) cgx_exec_destroy(*q); }
+  } guard{{&ee, &ec, &ei}};
+  o.mode = CGX_MODE_EAGER;
+  CKS(cgx_exec_create_ex(c, &o, stream, &ee));
+  o.mode = CGX_MODE_GRAPH_COPY;
+  CKS(cgx_exec_create_ex(c, &o, stream, &ec));
+  o.mode = CGX_MODE_GRAPH_INDIRECT;
+  int ind_ok = 1;
+  int st = cgx_exec_create_ex(c, &o, stream, &ei);
+  if (st == CGX_E_UNSUPPORTED) { ind_ok = 0; ei = nullptr; }
+  else if (st != CGX_OK) return st;
+  cgx_profile_t p{};
+  p.n_kernels = K;
+  p.ind_available = ind_ok;
+  p.use_measured = 1;
+  // warm-up (reading 7: 5 runs)
+  CKS(time_loop(ee, ext, n_ext, true, 5, &p.t_eager_us));
+  CKS(time_loop(ec, ext, n_ext, true, 5, &p.t_copy_us));
+  if (ei) CKS(time_loop(ei, ext, n_ext, true, 5, &p.t_ind_us));
+  // measured end-to-end totals per replay and the rebinding deltas
+  double t_base = 0;
+  CKS(time_loop3(ee, ext, n_ext, true, reps, &p.t_eager_us));
+  CKS(time_loop3(ec, ext, n_ext, true, reps, &p.t_copy_us));
+  CKS(time_loop3(ec, ext, n_ext, false, reps, &t_base));
+  if (ei) CKS(time_loop3(ei, ext, n_ext, true, reps, &p.t_ind_us));
+  else p.t_ind_us = INFINITY;
+  p.c_copy_us = p.t_copy_us - t_base;
+  p.c_ind_us = ei ? p.t_ind_us - t_base : INFINITY;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // L: host issue cost per eager kernel; G: host cost of cudaGraphLaunch
+  std::vector<double> vl, vg, vspan;
+  for (int r = 0; r < reps; ++r) {
+    CK(cudaStreamSynchronize(s));
+    double t0 = now_us();
+    CKS(cgx_launch(ee));
+    vl.push_back((now_us() - t0) / K);
+    CK(cudaStreamSynchronize(s));
+    t0 = now_us();
+    CKS(cgx_launch(ec));
+    vg.push_back(now_us() - t0);
+  }
+  p.L_us = median(vl);
+  p.G_us = median(vg);
+  // d_k: device time of each kernel (events around each eager launch); graph span with events
+  std::vector<cudaEvent_t> ev(2 * K + 2);
+  for (auto& v : ev) CK(cudaEventCreate(&v));
+  std::vector<std::vector<double>> dk(K);
+  for (int r = 0; r < reps; ++r) {
+    CK(cudaStreamSynchronize(s));
+    for (int k = 0; k < K; ++k) {
+      CK(cudaEventRecord(ev[2 * k], s));
+      CKS(issue(ee, ee->L[k], s));
+      CK(cudaEventRecord(ev[2 * k + 1], s));
+    }
+    CK(cudaEventRecord(ev[2 * K], s));
+    CKS(cgx_launch(ec));
+    CK(cudaEventRecord(ev[2 * K + 1], s));
+    CK(cudaStreamSynchronize(s));
+    for (int k = 0; k < K; ++k) {
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, ev[2 * k], ev[2 * k + 1]));
+      dk[k].push_back(ms * 1e3);
+    }
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, ev[2 * K], ev[2 * K + 1]));
+    vspan.push_back(ms * 1e3);
+  }
+  for (auto& v : ev) cudaEventDestroy(v);
+  double sum_d = 0.0;
+  for (int k = 0; k < K; ++k) {
+    p.d_us[k] = median(dk[k]);
+    sum_d = sum_d + p.d_us[k];
+  }
+  p.delta_us = (median(vspan) - sum_d) / K;
+  p.F_us = 0.0;
+  *out = p;
+  return CGX_OK;
+}

@@ -1,0 +1,65 @@
+"""The C-ABI library builds, loads and exports every symbol include/cgx.h declares (no GPU, no
+compute calls). Also checks the product path never imports the oracle and vice versa."""
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2503_19779_b200 import build
+    build.build()
+    from paper_2503_19779_b200 import cgx
+    return cgx
+
+
+def declared():
+    src = open(os.path.join(ROOT, "include", "cgx.h")).read()
+    return sorted(set(re.findall(r"^(?:int|const char\*)\s+(cgx_\w+)\(", src, re.M)))
+
+
+def test_header_symbols_exported(lib):
+    names = declared()
+    assert len(names) >= 20
+    out = subprocess.run(["nm", "-D", "--defined-only", lib.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (cgx_\w+)", out))
+    missing = [n for n in names if n not in exported]
+    assert not missing, missing
+    assert set(lib.EXPORTED) == set(names)
+
+
+def test_version_and_pure_select_on_cpu(lib):
+    assert lib.version() == 1
+    # cgx_select is a pure host function: callable without a GPU
+    p = lib.Profile()
+    p.n_kernels, p.ind_available, p.use_measured = 2, 1, 0
+    p.L_us, p.G_us, p.delta_us, p.c_copy_us, p.c_ind_us = 10.0, 7.5, 0.5, 3.0, 1.0
+    p.d_us[0], p.d_us[1] = 2.0, 2.0
+    dec, est = lib.select([p])
+    from oracle import selector as sel
+    pe = dict(L=10.0, G=7.5, delta=0.5, d=[2.0, 2.0], c_copy=3.0, c_ind=1.0)
+    assert est[0] == sel.estimates(pe)
+    assert dec[0] == sel.select([pe])[0]
+
+
+def test_no_cpu_device_without_gpu(lib):
+    import ctypes as C
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    out = C.c_void_p()
+    st = lib.LIB.cgx_chain_create(0, C.byref(out))
+    assert st != 0    # no CUDA device here: fails loudly instead of falling back
+
+
+def test_product_and_oracle_are_independent():
+    for d, forbidden in (("paper_2503_19779_b200", "oracle"), ("oracle", "paper_2503_19779_b200")):
+        for dirpath, _, files in os.walk(os.path.join(ROOT, d)):
+            for f in files:
+                if f.endswith((".py", ".cu", ".h", ".cuh", ".cpp")):
+                    txt = open(os.path.join(dirpath, f)).read()
+                    assert not re.search(rf"^\s*(from|import)\s+{forbidden}\b", txt, re.M), (f, forbidden)
