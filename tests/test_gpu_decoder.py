@@ -1,0 +1,184 @@
+"""GPU parity of the decoder-shaped chain (C3): tcgen05 GEMM, LayerNorm, causal attention, and
+the 12-layer GPT-2-small chain, through the C ABI against the CPU oracle.
+
+Bar: bf16 nodes node-local (the oracle is fed the GPU's actual node inputs so
+errors do not compound), per element |g - o| <= 2e-2 |o| + 2e-2 rms(o); integer-mode GEMMs
+exact; end to end ||g - o||_2 / ||o||_2 <= 2e-2; bit-identical across GPU arms.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+from oracle import ops  # noqa: E402
+from oracle.chain import eval_chain  # noqa: E402
+from oracle.numerics import bf16_bits, bits_to_f64  # noqa: E402
+from synth import workloads as wl  # noqa: E402
+from synth.workloads import ChainSpec, NodeSpec, SlotSpec  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def rt():
+    from paper_2503_19779_b200 import build
+    build.build()
+    from paper_2503_19779_b200 import cgx, runner
+    return cgx, runner
+
+
+def _close(g_bits, o, what=""):
+    g = bits_to_f64(g_bits)
+    o = np.asarray(o, dtype=np.float64)
+    rms = np.sqrt(np.mean(o ** 2)) if o.size else 0.0
+    bad = np.abs(g - o) > 2e-2 * np.abs(o) + 2e-2 * rms
+    assert not bad.any(), f"{what}: {bad.sum()} of {bad.size} outside tolerance; " \
+                          f"max err {np.max(np.abs(g - o)):.4g}, rms {rms:.4g}"
+
+
+def _gemm_chain(M, N, K, bias=True, gelu=False, residual=False):
+    slots = [SlotSpec("x", "external", "bf16", M * K), SlotSpec("w", "static", "bf16", N * K, "weight"),
+             SlotSpec("b", "static", "bf16", N, "bias"), SlotSpec("a", "internal", "bf16", M * K),
+             SlotSpec("y", "internal", "bf16", M * N)]
+    ins = ("a", "w", "b")
+    if residual:
+        slots.append(SlotSpec("r", "static", "bf16", M * N, "uniform"))
+        ins = ins + ("r",)
+    nodes = [NodeSpec("COPY", ("x",), "a", {"n": M * K}),
+             NodeSpec("GEMM_BF16", ins, "y", {"M": M, "N": N, "K": K, "bias": bias, "gelu": gelu,
+                                              "residual": residual})]
+    return ChainSpec(f"gemm{M}x{N}x{K}", slots, nodes, [(0, 1)])
+
+
+def _run(rt, spec, mode, replays, st, mode_vals="uniform"):
+    cgx, runner = rt
+    dev = torch.device("cuda:0")
+    chain = runner.Chain(spec, runner.upload_statics(spec, st, dev))
+    ex = chain.exec(mode)
+    outs, keep = [], []
+    for r in range(replays):
+        ext = wl.external_values(spec, r, mode_vals)
+        t = runner.upload_externals(spec, ext, dev)
+        keep.append(t)
+        ex.bind(t)
+        ex.launch()
+        outs.append({s.name: ex.output(s.name) for s in spec.internals()})
+    chain.close()
+    return outs
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 2304, 768), (128, 768, 3072), (128, 3072, 768), (128, 768, 768),
+                                   (4, 64, 64), (1, 768, 768), (77, 384, 192), (256, 128, 128),
+                                   (200, 1536, 384)])
+def test_gemm_parity(rt, M, N, K):
+    spec = _gemm_chain(M, N, K)
+    st = wl.static_values(spec)
+    for mode in ("EAGER", "INDIRECT"):
+        outs = _run(rt, spec, mode, 2, st)
+        for r, got in enumerate(outs):
+            env = eval_chain(spec, wl.external_values(spec, r), st)
+            _close(got["y"], env["y"], f"gemm {M}x{N}x{K} {mode}")
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 64, 64), (64, 768, 64), (3, 32, 64)])
+def test_gemm_integer_exact(rt, M, N, K):
+    spec = _gemm_chain(M, N, K)
+    st = wl.static_values(spec, mode="int")
+    outs = _run(rt, spec, "INDIRECT", 2, st, mode_vals="int")
+    for r, got in enumerate(outs):
+        env = eval_chain(spec, wl.external_values(spec, r, "int"), st)
+        assert np.array_equal(got["y"], bf16_bits(env["y"]))
+
+
+def test_gemm_gelu_and_residual(rt):
+    for gelu, res in ((True, False), (False, True), (True, True)):
+        spec = _gemm_chain(128, 3072 if gelu else 768, 768, gelu=gelu, residual=res)
+        st = wl.static_values(spec)
+        outs = _run(rt, spec, "COPY", 1, st)
+        env = eval_chain(spec, wl.external_values(spec, 0), st)
+        _close(outs[0]["y"], env["y"], f"gelu={gelu} residual={res}")
+
+
+def test_layernorm_and_attention_nodes(rt):
+    T, d, H, D = 128, 768, 12, 64
+    slots = [SlotSpec("x", "external", "bf16", T * d), SlotSpec("g", "static", "bf16", d, "gamma"),
+             SlotSpec("b", "static", "bf16", d, "bias"), SlotSpec("q", "external", "bf16", T * 3 * H * D),
+             SlotSpec("ln", "internal", "bf16", T * d), SlotSpec("qq", "internal", "bf16", T * 3 * H * D),
+             SlotSpec("att", "internal", "bf16", T * H * D)]
+    nodes = [NodeSpec("LAYERNORM", ("x", "g", "b"), "ln", {"rows": T, "cols": d, "eps": 1e-5}),
+             NodeSpec("COPY", ("q",), "qq", {"n": T * 3 * H * D}),
+             NodeSpec("ATTN_CAUSAL", ("qq",), "att", {"T": T, "H": H, "D": D, "scale": 0.125})]
+    spec = ChainSpec("ln_attn", slots, nodes, [(0, 2)])
+    st = wl.static_values(spec)
+    for mode in ("EAGER", "INDIRECT", "SETPARAMS"):
+        outs = _run(rt, spec, mode, 2, st)
+        for r, got in enumerate(outs):
+            env = eval_chain(spec, wl.external_values(spec, r), st)
+            _close(got["ln"], env["ln"], f"layernorm {mode}")
+            _close(got["att"], env["att"], f"attention {mode}")
+
+
+@pytest.mark.parametrize("T", [1, 5, 128, 256])
+def test_attention_lengths(rt, T):
+    H, D = 2, 64
+    slots = [SlotSpec("q", "external", "bf16", T * 3 * H * D),
+             SlotSpec("qq", "internal", "bf16", T * 3 * H * D), SlotSpec("att", "internal", "bf16", T * H * D)]
+    nodes = [NodeSpec("COPY", ("q",), "qq", {"n": T * 3 * H * D}),
+             NodeSpec("ATTN_CAUSAL", ("qq",), "att", {"T": T, "H": H, "D": D, "scale": 0.125})]
+    spec = ChainSpec("attn", slots, nodes, [(0, 1)])
+    outs = _run(rt, spec, "INDIRECT", 1, {})
+    env = eval_chain(spec, wl.external_values(spec, 0), {})
+    _close(outs[0]["att"], env["att"], f"attention T={T}")
+
+
+def _node_local_check(spec, st, ext, got):
+    """Feed every node the GPU's own inputs and compare its output (no error compounding)."""
+    env = {}
+    for s in spec.slots:
+        if s.kind == "external":
+            env[s.name] = bits_to_f64(ext[s.name])
+        elif s.kind == "static":
+            env[s.name] = bits_to_f64(st[s.name])
+        else:
+            env[s.name] = bits_to_f64(got[s.name])
+    for node in spec.nodes:
+        a = node.attrs
+        if node.op == "LAYERNORM":
+            ref = ops.layernorm(env[node.ins[0]], env[node.ins[1]], env[node.ins[2]], a)
+        elif node.op == "GEMM_BF16":
+            ref = ops.gemm_bf16(env[node.ins[0]], env[node.ins[1]], env[node.ins[2]], a)
+        elif node.op == "ATTN_CAUSAL":
+            ref = ops.attn_causal(env[node.ins[0]], a)
+        elif node.op == "ADD":
+            ref = ops.add(env[node.ins[0]], env[node.ins[1]], a, "bf16")
+        else:
+            raise AssertionError(node.op)
+        _close(got[node.out], ref, f"{node.out} ({node.op})")
+
+
+@pytest.mark.parametrize("n_layers", [1, 12])
+def test_c3_decoder_chain(rt, n_layers):
+    spec = wl.c3_chain(T=128, n_layers=n_layers)
+    st = wl.static_values(spec)
+    res = {}
+    for mode in ("EAGER", "COPY", "INDIRECT", "SETPARAMS"):
+        res[mode] = _run(rt, spec, mode, 2, st)
+    for r in range(2):
+        ext = wl.external_values(spec, r)
+        got = res["INDIRECT"][r]
+        _node_local_check(spec, st, ext, got)
+        env = eval_chain(spec, ext, st)
+        last = spec.nodes[-1].out
+        g = bits_to_f64(got[last])
+        o = env[last]
+        assert np.linalg.norm(g - o) / np.linalg.norm(o) <= 2e-2
+        for mode in ("EAGER", "COPY", "SETPARAMS"):      # bit-identical across arms
+            for k in got:
+                assert np.array_equal(res[mode][r][k], got[k]), (mode, k)
+
+
+def test_c3_t1_decode_shape(rt):
+    spec = wl.c3_chain(T=1, n_layers=2)
+    st = wl.static_values(spec)
+    outs = _run(rt, spec, "INDIRECT", 1, st)
+    ext = wl.external_values(spec, 0)
+    _node_local_check(spec, st, ext, outs[0])
