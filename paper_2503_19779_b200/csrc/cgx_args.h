@@ -21,7 +21,8 @@ struct ElemArgs {
   uint32_t cols;           // REDUCE_SUM row length
   uint64_t n;              // elements
   float scalar;            // SCALE_IMM
-  float eps;
+  uint32_t pre;            // bit i: operand i may be loaded BEFORE griddepcontrol.wait (it is not
+                           // written by the immediately preceding kernel; see runtime.cu)
 };
 static constexpr uint32_t kFlagTableAfterWait = 1u;
 

@@ -47,23 +47,58 @@ __device__ __forceinline__ void fetch_operands(const ElemArgs& a, const void*& p
   pdl_trigger();
 
 // ---------------------------------------------------------------------------- f32 elementwise
+// Operands whose `pre` bit is set are loaded before griddepcontrol.wait, overlapping the
+// predecessor's tail (they are not written by it); the rest are loaded after the wait.
 template <int OP>
 __global__ void __launch_bounds__(kElemThreads) k_elem_f32(const __grid_constant__ ElemArgs a) {
-  CGX_PROLOGUE(a, p0, p1)
+  constexpr bool kBinary = (OP == OP_ADD || OP == OP_MUL);
+  const bool late = a.flags & kFlagTableAfterWait;
+  const void* p0;
+  const void* p1;
+  if (!late) fetch_operands(a, p0, p1);
   const float4* x = reinterpret_cast<const float4*>(p0);
   const float4* y = reinterpret_cast<const float4*>(p1);
-  float4* o = reinterpret_cast<float4*>(a.out);
   const uint64_t n4 = a.n >> 2;
   const uint64_t base = (uint64_t)blockIdx.x * (kElemThreads * kElemVec) + threadIdx.x;
   float4 xv[kElemVec], yv[kElemVec];
+  const bool pre_x = !late && (a.pre & 1u);
+  const bool pre_y = kBinary && !late && (a.pre & 2u);
+  if (pre_x) {
 #pragma unroll
-  for (int j = 0; j < kElemVec; ++j) {
-    const uint64_t i = base + (uint64_t)j * kElemThreads;
-    if (i < n4) {
-      xv[j] = x[i];
-      if (OP == OP_ADD || OP == OP_MUL) yv[j] = y[i];
+    for (int j = 0; j < kElemVec; ++j) {
+      const uint64_t i = base + (uint64_t)j * kElemThreads;
+      if (i < n4) xv[j] = x[i];
     }
   }
+  if (pre_y) {
+#pragma unroll
+    for (int j = 0; j < kElemVec; ++j) {
+      const uint64_t i = base + (uint64_t)j * kElemThreads;
+      if (i < n4) yv[j] = y[i];
+    }
+  }
+  pdl_wait();
+  if (late) {
+    fetch_operands(a, p0, p1);
+    x = reinterpret_cast<const float4*>(p0);
+    y = reinterpret_cast<const float4*>(p1);
+  }
+  pdl_trigger();
+  if (!pre_x) {
+#pragma unroll
+    for (int j = 0; j < kElemVec; ++j) {
+      const uint64_t i = base + (uint64_t)j * kElemThreads;
+      if (i < n4) xv[j] = x[i];
+    }
+  }
+  if (kBinary && !pre_y) {
+#pragma unroll
+    for (int j = 0; j < kElemVec; ++j) {
+      const uint64_t i = base + (uint64_t)j * kElemThreads;
+      if (i < n4) yv[j] = y[i];
+    }
+  }
+  float4* o = reinterpret_cast<float4*>(a.out);
 #pragma unroll
   for (int j = 0; j < kElemVec; ++j) {
     const uint64_t i = base + (uint64_t)j * kElemThreads;
@@ -82,7 +117,7 @@ __global__ void __launch_bounds__(kElemThreads) k_elem_f32(const __grid_constant
     if (t < a.n) {
       const float* xs = reinterpret_cast<const float*>(p0);
       const float* ys = reinterpret_cast<const float*>(p1);
-      const float yy = (OP == OP_ADD || OP == OP_MUL) ? ys[t] : 0.f;
+      const float yy = kBinary ? ys[t] : 0.f;
       reinterpret_cast<float*>(a.out)[t] = apply_f32<OP>(xs[t], yy, a.scalar);
     }
   }

@@ -506,6 +506,27 @@ static int build_launch(cgx_exec* e, int k, Launch& l) {
   return fail(CGX_E_INVALID_ARG, "build_launch: unknown op");
 }
 
+// An operand of launch i may be loaded before griddepcontrol.wait iff it is not the output of the
+// launch that immediately precedes it in stream/graph order (for the first launch: the last one,
+// which precedes it across eager iterations). Every chain kernel triggers its dependents only after
+// its own wait, so all earlier launches have completed when launch i starts executing.
+static void set_prewait_masks(cgx_exec* e) {
+  if (e->o.no_pdl) return;
+  const int n = (int)e->L.size();
+  for (int i = 0; i < n; ++i) {
+    Launch& l = e->L[i];
+    if (l.kind != LK_KERNEL) continue;
+    const Node& node = e->c->nodes[l.node];
+    if (node.op > CGX_OP_REDUCE_SUM) continue;
+    const Launch& prev = e->L[(i + n - 1) % n];
+    const int prev_out = e->c->nodes[prev.node].out;
+    uint32_t pre = 0;
+    for (int j = 0; j < node.n_in && j < 2; ++j)
+      if (node.in[j] != prev_out) pre |= 1u << j;
+    argp<ElemArgs>(l)->pre = pre;
+  }
+}
+
 static int issue(cgx_exec* e, Launch& l, cudaStream_t s) {
   if (l.kind == LK_NCCL) {
     ncclResult_t r = ncclAllReduce(l.nc_in, l.nc_out, l.nc_count, ncclBfloat16, ncclSum,
@@ -749,6 +770,7 @@ extern "C" int cgx_exec_create_ex(cgx_chain* c, const cgx_exec_opts* opts, void*
   e->L.resize(last - first + 1);
   for (int k = first; k <= last; ++k)
     if ((st = build_launch(e, k, e->L[k - first])) != CGX_OK) return bail(st);
+  set_prewait_masks(e);
   if (o.mode != CGX_MODE_EAGER) {
     cudaError_t ce = cudaStreamCreateWithFlags(&e->cs, cudaStreamNonBlocking);
     if (ce != cudaSuccess) return bail(cuda_fail(ce, "cudaStreamCreate", __LINE__));
