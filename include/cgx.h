@@ -117,10 +117,15 @@ typedef enum {
  *   ROOT_MEMCPY  T2: memcpy node at the graph root from ping-pong pinned staging
  *   ROOT_PARAMS  T3: root table-writer kernel whose by-value params carry the pointers, updated
  *                    with one cudaGraphExecKernelNodeSetParams per bind
- *   ROOT_MAPPED  T4: root kernel reading a mapped pinned staging ring (zero-copy) */
+ *   ROOT_MAPPED  T4: root kernel reading a mapped pinned staging ring (zero-copy)
+ *   FIRST_NODE   T5: no extra node. The first node's by-value params carry the pointers (one
+ *                    cudaGraphExecKernelNodeSetParams per bind) and its CTA 0 publishes the table
+ *                    while it computes; the second node also reads its operands by value and
+ *                    releases its dependents only after its wait. Needs an elementwise/reduce/LN
+ *                    first node and <= 512 externals (else CGX_E_UNSUPPORTED). */
 typedef enum {
   CGX_XPORT_DEFAULT = 0, CGX_XPORT_H2D = 1, CGX_XPORT_ROOT_MEMCPY = 2, CGX_XPORT_ROOT_PARAMS = 3,
-  CGX_XPORT_ROOT_MAPPED = 4
+  CGX_XPORT_ROOT_MAPPED = 4, CGX_XPORT_FIRST_NODE = 5
 } cgx_transport;
 
 typedef enum { CGX_DECIDE_EAGER = 0, CGX_DECIDE_GRAPH_COPY = 1, CGX_DECIDE_GRAPH_INDIRECT = 2 } cgx_decision;
@@ -134,7 +139,8 @@ typedef struct {
   int no_pdl;               /* 1 = plain stream edges instead of programmatic dependent launch */
   int validate;             /* bind-time residency check: 0 = cached per address (default),
                                1 = every bind, 2 = off (alignment and count are always checked) */
-  int copy_impl;            /* GRAPH_COPY: 0 = multi-tensor kernel, 1 = cudaMemcpyAsync per tensor */
+  int copy_impl;            /* GRAPH_COPY: 0 = multi-tensor LDG/STG kernel, 1 = cudaMemcpyAsync per
+                               tensor, 2 = multi-tensor TMA bulk-copy kernel */
 } cgx_exec_opts;
 
 typedef struct {

@@ -26,7 +26,7 @@ OP = {"ADD": 0, "MUL": 1, "SCALE_IMM": 2, "COPY": 3, "REDUCE_SUM": 4, "LAYERNORM
       "GEMM_BF16": 6, "ATTN_CAUSAL": 7, "ALLREDUCE_SUM": 8}
 GEMM_BIAS, GEMM_GELU, GEMM_RESIDUAL = 1, 2, 4
 MODE = {"EAGER": 0, "COPY": 1, "INDIRECT": 2, "SETPARAMS": 3, "STALE": 4}
-XPORT = {"DEFAULT": 0, "H2D": 1, "ROOT_MEMCPY": 2, "ROOT_PARAMS": 3, "ROOT_MAPPED": 4}
+XPORT = {"DEFAULT": 0, "H2D": 1, "ROOT_MEMCPY": 2, "ROOT_PARAMS": 3, "ROOT_MAPPED": 4, "FIRST_NODE": 5}
 DECIDE = {0: "EAGER", 1: "GRAPH_COPY", 2: "GRAPH_INDIRECT"}
 MAX_PROFILE_KERNELS = 1024
 

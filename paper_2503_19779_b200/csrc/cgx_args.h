@@ -21,10 +21,16 @@ struct ElemArgs {
   uint32_t cols;           // REDUCE_SUM row length
   uint64_t n;              // elements
   float scalar;            // SCALE_IMM
-  uint32_t pre;            // bit i: operand i may be loaded BEFORE griddepcontrol.wait (it is not
-                           // written by the immediately preceding kernel; see runtime.cu)
+  uint32_t pre;            // bit i: operand i may be loaded BEFORE griddepcontrol.wait (an
+                           // EXTERNAL or STATIC slot, never written inside the graph)
 };
+// PDL protocol (see runtime.cu, set_pdl_flags): every chain kernel triggers its dependents at
+// entry, so consecutive nodes' prologues cascade; only data nothing in the graph writes (inputs,
+// weights, the table under T1) is read before griddepcontrol.wait. The first consumer after a
+// root table-writer reads the table after its wait and triggers only then, so no later node can
+// start before the root has completed.
 static constexpr uint32_t kFlagTableAfterWait = 1u;
+static constexpr uint32_t kFlagTriggerAfterWait = 2u;
 
 // Multi-tensor copy (BASELINE north_star (1)). Static part lives in device
 // memory (per exec, written once at capture); the fresh sources travel by value in the params.
@@ -79,14 +85,39 @@ struct AttnArgs {
   float scale;
 };
 
+// T5 (FIRST_NODE transport): the first node of the graph carries the bound pointers by value and
+// publishes the table (CTA 0) while computing; the second node reads its own external operands by
+// value too and triggers its dependents only after its wait, so every later node's pre-wait table
+// fetch happens after the first node completed. ArgsTW<Base, 0> is the plain parameter block.
+template <int CAP>
+struct TWPart {
+  uint64_t* table;
+  uint32_t n;
+  uint32_t pad;
+  uint64_t ptr[CAP];
+};
+template <typename Base, int CAP>
+struct ArgsTW {
+  Base a;
+  TWPart<CAP> tw;
+};
+template <typename Base>
+struct ArgsTW<Base, 0> {
+  Base a;
+};
 }  // namespace cgx
 
-// Kernel handles exported by the kernel translation units (host functions).
+// Kernel handles exported by the kernel translation units (host functions). `tw` = table-writer
+// capacity for the T5 first node (0 = plain kernel; else 8, 64 or 512 pointers).
 extern "C++" {
 namespace cgx {
-const void* kfn_elem(int op, int dtype);          // ADD/MUL/SCALE_IMM/COPY f32|bf16
-const void* kfn_reduce_sum_f32();
+const void* kfn_elem(int op, int dtype, int tw = 0);   // ADD/MUL/SCALE_IMM/COPY f32|bf16
+const void* kfn_reduce_sum_f32(int tw = 0);
+int tw_cap(int n);                                // 8, 64, 512 (0 if n > 512)
 const void* kfn_copy(int cap);                    // CAP in {8, 64, 1024}
+const void* kfn_copy_bulk(int cap);               // TMA bulk-copy variant
+size_t copy_bulk_smem();
+uint32_t copy_bulk_chunk();
 const void* kfn_table_write(int cap);             // CAP in {8, 64, 512}
 const void* kfn_table_mapped();
 const void* kfn_empty();

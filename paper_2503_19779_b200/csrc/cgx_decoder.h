@@ -6,7 +6,7 @@
 
 namespace cgx {
 // LayerNorm: one warp per row, registers hold the row (cols <= 2048, cols % 8 == 0).
-const void* kfn_layernorm();
+const void* kfn_layernorm(int tw = 0);
 void decoder_ln_launch_dims(uint32_t rows, uint32_t cols, dim3* grid, dim3* block);
 
 // Causal attention on CUDA cores (T <= 1024, D == 64).
@@ -21,4 +21,6 @@ bool decoder_gemm_supported(uint32_t M, uint32_t N, uint32_t K);
 int decoder_gemm_build(uint32_t M, uint32_t N, uint32_t K, uint32_t flags, const void* A, const void* W,
                        const void* bias, const void* residual, void* out, void* args_out, size_t* argbytes,
                        dim3* grid, dim3* block, size_t* smem, const void** func);
+// Make a built GEMM parameter block trigger its PDL dependents only after its wait (T5 node 2).
+void decoder_gemm_set_trigger_after_wait(void* args);
 }  // namespace cgx

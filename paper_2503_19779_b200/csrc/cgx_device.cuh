@@ -3,12 +3,22 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "cgx_args.h"
+
 namespace cgx {
 
-// Programmatic dependent launch (PDL). A kernel's prologue (pointer-table fetch, index math) may
-// run while its predecessor drains; everything that reads a predecessor's output comes after
-// pdl_wait(). Every chain kernel triggers its dependents only AFTER its own wait, so a kernel
-// that starts early can rely on every node two or more steps upstream having completed.
+// T5 first node: CTA 0 publishes the by-value pointer array into the device table.
+template <typename Base, int CAP>
+__device__ __forceinline__ void tw_publish(const ArgsTW<Base, CAP>& A) {
+  if constexpr (CAP > 0) {
+    if (blockIdx.x == 0)
+      for (uint32_t i = threadIdx.x; i < A.tw.n; i += blockDim.x) A.tw.table[i] = A.tw.ptr[i];
+  }
+}
+
+// Programmatic dependent launch (PDL). A kernel's prologue (pointer-table fetch, loads of slots
+// nothing in the graph writes) may run while its predecessors drain; everything that reads another
+// node's output comes after pdl_wait(). See the protocol note in cgx_args.h.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 

@@ -37,22 +37,27 @@ __device__ __forceinline__ void fetch_operands(const ElemArgs& a, const void*& p
   if (a.t1 >= 0) p1 = reinterpret_cast<const void*>(ld_table(a.table + a.t1));
 }
 
-// Prologue shared by all chain kernels: table fetch (pre- or post-wait), PDL wait, trigger.
+// Prologue shared by the chain kernels: trigger dependents (at entry unless the node is the first
+// consumer after a root table-writer), table fetch (pre- or post-wait), PDL wait.
 #define CGX_PROLOGUE(a, p0, p1)                                        \
   const void* p0;                                                      \
   const void* p1;                                                      \
+  if (!((a).flags & kFlagTriggerAfterWait)) pdl_trigger();             \
   if (!((a).flags & kFlagTableAfterWait)) fetch_operands((a), p0, p1); \
   pdl_wait();                                                          \
   if ((a).flags & kFlagTableAfterWait) fetch_operands((a), p0, p1);    \
-  pdl_trigger();
+  if ((a).flags & kFlagTriggerAfterWait) pdl_trigger();
 
 // ---------------------------------------------------------------------------- f32 elementwise
-// Operands whose `pre` bit is set are loaded before griddepcontrol.wait, overlapping the
-// predecessor's tail (they are not written by it); the rest are loaded after the wait.
-template <int OP>
-__global__ void __launch_bounds__(kElemThreads) k_elem_f32(const __grid_constant__ ElemArgs a) {
+// Operands whose `pre` bit is set (EXTERNAL / STATIC slots: never written inside the graph) are
+// loaded before griddepcontrol.wait, overlapping the predecessors; the rest after the wait.
+template <int OP, int TW>
+__global__ void __launch_bounds__(kElemThreads) k_elem_f32(const __grid_constant__ ArgsTW<ElemArgs, TW> A) {
+  const ElemArgs& a = A.a;
+  tw_publish(A);
   constexpr bool kBinary = (OP == OP_ADD || OP == OP_MUL);
   const bool late = a.flags & kFlagTableAfterWait;
+  if (!(a.flags & kFlagTriggerAfterWait)) pdl_trigger();
   const void* p0;
   const void* p1;
   if (!late) fetch_operands(a, p0, p1);
@@ -83,7 +88,7 @@ __global__ void __launch_bounds__(kElemThreads) k_elem_f32(const __grid_constant
     x = reinterpret_cast<const float4*>(p0);
     y = reinterpret_cast<const float4*>(p1);
   }
-  pdl_trigger();
+  if (a.flags & kFlagTriggerAfterWait) pdl_trigger();
   if (!pre_x) {
 #pragma unroll
     for (int j = 0; j < kElemVec; ++j) {
@@ -131,8 +136,10 @@ __device__ __forceinline__ __nv_bfloat16 apply_bf16(__nv_bfloat16 x, __nv_bfloat
   return __float2bfloat16_rn(apply_f32<OP>(__bfloat162float(x), __bfloat162float(y), s));
 }
 
-template <int OP>
-__global__ void __launch_bounds__(kElemThreads) k_elem_bf16(const __grid_constant__ ElemArgs a) {
+template <int OP, int TW>
+__global__ void __launch_bounds__(kElemThreads) k_elem_bf16(const __grid_constant__ ArgsTW<ElemArgs, TW> A) {
+  const ElemArgs& a = A.a;
+  tw_publish(A);
   CGX_PROLOGUE(a, p0, p1)
   const uint4* x = reinterpret_cast<const uint4*>(p0);
   const uint4* y = reinterpret_cast<const uint4*>(p1);
@@ -178,7 +185,10 @@ __global__ void __launch_bounds__(kElemThreads) k_elem_bf16(const __grid_constan
 // xor-shuffle tree; one rounding to f32. No atomics: every arm produces identical bits.
 static constexpr int kReduceThreads = 256;
 
-__global__ void __launch_bounds__(kReduceThreads) k_reduce_sum_f32(const __grid_constant__ ElemArgs a) {
+template <int TW>
+__global__ void __launch_bounds__(kReduceThreads) k_reduce_sum_f32(const __grid_constant__ ArgsTW<ElemArgs, TW> A) {
+  const ElemArgs& a = A.a;
+  tw_publish(A);
   CGX_PROLOGUE(a, p0, p1)
   (void)p1;
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -240,10 +250,98 @@ __global__ void __launch_bounds__(kCopyThreads) k_copy(const __grid_constant__ C
   }
 }
 
+// TMA bulk-copy variant (copy_impl = 2): one warp per CTA; lane 0 streams chunks through a
+// kBulkStages-deep shared-memory ring with cp.async.bulk (global -> smem, mbarrier completion) and
+// cp.async.bulk (smem -> global, bulk async-group completion). No register staging at all.
+static constexpr int kBulkStages = 4;
+static constexpr uint32_t kBulkChunk = 32768;
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+template <int CAP>
+__global__ void __launch_bounds__(32, 1) k_copy_bulk(const __grid_constant__ CopyArgs<CAP> a) {
+  extern __shared__ __align__(128) uint8_t ring[];
+  __shared__ __align__(8) uint64_t bar[kBulkStages];
+  const uint32_t lane = threadIdx.x;
+  if (lane == 0) {
+    for (int s = 0; s < kBulkStages; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_addr(&bar[s])));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncwarp();
+  // chunk list of this CTA: c_i = blockIdx.x + i * gridDim.x
+  const uint32_t my_n = a.n_chunks > blockIdx.x ? (a.n_chunks - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  auto chunk_of = [&](uint32_t i, const char*& src, char*& dst, uint32_t& len, uint32_t& tail) -> bool {
+    const uint32_t c = blockIdx.x + i * gridDim.x;
+    const uint32_t t = a.chunk_tensor[c];
+    const CopyDesc d = a.desc[t];
+    src = reinterpret_cast<const char*>(a.src[t]);
+    dst = reinterpret_cast<char*>(d.dst);
+    if (src == dst) return false;
+    const uint64_t off = (uint64_t)(c - d.chunk_begin) * a.chunk_bytes;
+    const uint64_t rem = d.nbytes - off;
+    const uint32_t l = (uint32_t)(rem < a.chunk_bytes ? rem : a.chunk_bytes);
+    src += off;
+    dst += off;
+    len = l & ~15u;
+    tail = l & 15u;
+    return true;
+  };
+  if (lane == 0) {
+    const uint32_t pre = my_n < (uint32_t)kBulkStages ? my_n : (uint32_t)kBulkStages;
+    for (uint32_t i = 0; i < pre; ++i) {
+      const char* src; char* dst; uint32_t len, tail;
+      if (!chunk_of(i, src, dst, len, tail) || len == 0) {
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_addr(&bar[i])) : "memory");
+        continue;
+      }
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr(&bar[i])), "r"(len) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                   ::"r"(smem_addr(ring + i * kBulkChunk)), "l"(src), "r"(len), "r"(smem_addr(&bar[i])) : "memory");
+    }
+    for (uint32_t i = 0; i < my_n; ++i) {
+      const uint32_t s = i % kBulkStages;
+      const uint32_t ph = (i / kBulkStages) & 1u;
+      uint32_t done;
+      do {
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                     : "=r"(done) : "r"(smem_addr(&bar[s])), "r"(ph) : "memory");
+      } while (!done);
+      const char* src; char* dst; uint32_t len, tail;
+      if (chunk_of(i, src, dst, len, tail) && len) {
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n"
+                     ::"l"(dst), "r"(smem_addr(ring + s * kBulkChunk)), "r"(len) : "memory");
+      }
+      asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+      // reuse the stage of chunk i for chunk i + kBulkStages once store i has read it
+      const uint32_t nx = i + kBulkStages;
+      if (nx < my_n) {
+        asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+        if (!chunk_of(nx, src, dst, len, tail) || len == 0) {
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_addr(&bar[s])) : "memory");
+        } else {
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr(&bar[s])), "r"(len) : "memory");
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                       ::"r"(smem_addr(ring + s * kBulkChunk)), "l"(src), "r"(len), "r"(smem_addr(&bar[s])) : "memory");
+        }
+      }
+    }
+    asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+  }
+  __syncwarp();
+  // bytewise tails (< 16 B per chunk) by the warp
+  for (uint32_t i = 0; i < my_n; ++i) {
+    const char* src; char* dst; uint32_t len, tail;
+    if (chunk_of(i, src, dst, len, tail) && lane < tail) dst[len + lane] = src[len + lane];
+  }
+}
+
 // ---------------------------------------------------------------------------- INDIRECT roots
 template <int CAP>
 __global__ void k_table_write(const __grid_constant__ TableWriteArgs<CAP> a) {
-  pdl_trigger();   // consumers fetch the table only after their own griddepcontrol.wait
+  pdl_trigger();   // node 1 fetches the table after its wait and triggers only after it
   for (uint32_t i = threadIdx.x; i < a.n; i += blockDim.x) a.table[i] = a.ptr[i];
 }
 
@@ -280,30 +378,65 @@ __global__ void k_fill_uniform_f32(const __grid_constant__ FillArgs a) {
 }
 
 // ---------------------------------------------------------------------------- handles
-const void* kfn_elem(int op, int dtype) {
+template <int TW>
+static const void* elem_fn(int op, int dtype) {
   if (dtype == 0) {
     switch (op) {
-      case OP_ADD: return (const void*)k_elem_f32<OP_ADD>;
-      case OP_MUL: return (const void*)k_elem_f32<OP_MUL>;
-      case OP_SCALE: return (const void*)k_elem_f32<OP_SCALE>;
-      case OP_COPY: return (const void*)k_elem_f32<OP_COPY>;
+      case OP_ADD: return (const void*)k_elem_f32<OP_ADD, TW>;
+      case OP_MUL: return (const void*)k_elem_f32<OP_MUL, TW>;
+      case OP_SCALE: return (const void*)k_elem_f32<OP_SCALE, TW>;
+      case OP_COPY: return (const void*)k_elem_f32<OP_COPY, TW>;
     }
   } else {
     switch (op) {
-      case OP_ADD: return (const void*)k_elem_bf16<OP_ADD>;
-      case OP_MUL: return (const void*)k_elem_bf16<OP_MUL>;
-      case OP_SCALE: return (const void*)k_elem_bf16<OP_SCALE>;
-      case OP_COPY: return (const void*)k_elem_bf16<OP_COPY>;
+      case OP_ADD: return (const void*)k_elem_bf16<OP_ADD, TW>;
+      case OP_MUL: return (const void*)k_elem_bf16<OP_MUL, TW>;
+      case OP_SCALE: return (const void*)k_elem_bf16<OP_SCALE, TW>;
+      case OP_COPY: return (const void*)k_elem_bf16<OP_COPY, TW>;
     }
   }
   return nullptr;
 }
-const void* kfn_reduce_sum_f32() { return (const void*)k_reduce_sum_f32; }
+const void* kfn_elem(int op, int dtype, int tw) {
+  switch (tw) {
+    case 0: return elem_fn<0>(op, dtype);
+    case 8: return elem_fn<8>(op, dtype);
+    case 64: return elem_fn<64>(op, dtype);
+    case 512: return elem_fn<512>(op, dtype);
+  }
+  return nullptr;
+}
+const void* kfn_reduce_sum_f32(int tw) {
+  switch (tw) {
+    case 0: return (const void*)k_reduce_sum_f32<0>;
+    case 8: return (const void*)k_reduce_sum_f32<8>;
+    case 64: return (const void*)k_reduce_sum_f32<64>;
+    case 512: return (const void*)k_reduce_sum_f32<512>;
+  }
+  return nullptr;
+}
+int tw_cap(int n) { return n <= 8 ? 8 : n <= 64 ? 64 : n <= 512 ? 512 : 0; }
 const void* kfn_copy(int cap) {
   if (cap <= 8) return (const void*)k_copy<8>;
   if (cap <= 64) return (const void*)k_copy<64>;
   return (const void*)k_copy<1024>;
 }
+const void* kfn_copy_bulk(int cap) {
+  const void* f;
+  if (cap <= 8) f = (const void*)k_copy_bulk<8>;
+  else if (cap <= 64) f = (const void*)k_copy_bulk<64>;
+  else f = (const void*)k_copy_bulk<1024>;
+  static bool set[3] = {false, false, false};
+  const int i = cap <= 8 ? 0 : cap <= 64 ? 1 : 2;
+  if (!set[i]) {
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkStages * kBulkChunk);
+    set[i] = true;
+  }
+  return f;
+}
+size_t copy_bulk_smem() { return (size_t)kBulkStages * kBulkChunk; }
+uint32_t copy_bulk_chunk() { return kBulkChunk; }
+
 const void* kfn_table_write(int cap) {
   if (cap <= 8) return (const void*)k_table_write<8>;
   if (cap <= 64) return (const void*)k_table_write<64>;

@@ -27,13 +27,17 @@ __device__ __forceinline__ float warp_max(float v) {
 static constexpr int kLnWarps = 4;
 static constexpr int kLnMaxVec = 8;    // 8 x 16 B per lane -> cols <= 2048
 
-__global__ void __launch_bounds__(kLnWarps * 32) k_layernorm(const __grid_constant__ LnArgs a) {
+template <int TW>
+__global__ void __launch_bounds__(kLnWarps * 32) k_layernorm(const __grid_constant__ ArgsTW<LnArgs, TW> A) {
+  const LnArgs& a = A.a;
+  tw_publish(A);
   const void* px = a.x;
   const bool late = a.flags & kFlagTableAfterWait;
+  if (!(a.flags & kFlagTriggerAfterWait)) pdl_trigger();
   if (a.tx >= 0 && !late) px = reinterpret_cast<const void*>(ld_table(a.table + a.tx));
   pdl_wait();
   if (a.tx >= 0 && late) px = reinterpret_cast<const void*>(ld_table(a.table + a.tx));
-  pdl_trigger();
+  if (a.flags & kFlagTriggerAfterWait) pdl_trigger();
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t row = blockIdx.x * kLnWarps + warp;
   if (row >= a.rows) return;
@@ -86,7 +90,15 @@ __global__ void __launch_bounds__(kLnWarps * 32) k_layernorm(const __grid_consta
   }
 }
 
-const void* kfn_layernorm() { return (const void*)k_layernorm; }
+const void* kfn_layernorm(int tw) {
+  switch (tw) {
+    case 0: return (const void*)k_layernorm<0>;
+    case 8: return (const void*)k_layernorm<8>;
+    case 64: return (const void*)k_layernorm<64>;
+    case 512: return (const void*)k_layernorm<512>;
+  }
+  return nullptr;
+}
 void decoder_ln_launch_dims(uint32_t rows, uint32_t cols, dim3* grid, dim3* block) {
   (void)cols;
   *grid = dim3((rows + kLnWarps - 1) / kLnWarps);
@@ -105,8 +117,9 @@ static constexpr int kKStride = kAttnD / 2 + 1;   // words per staged row
 
 __global__ void __launch_bounds__(kAttnWarps * 32) k_attention(const __grid_constant__ AttnArgs a) {
   extern __shared__ uint32_t sm[];
+  if (!(a.flags & kFlagTriggerAfterWait)) pdl_trigger();
   pdl_wait();
-  pdl_trigger();
+  if (a.flags & kFlagTriggerAfterWait) pdl_trigger();
   const uint32_t T = a.T, H = a.H;
   const uint32_t h = blockIdx.y;
   const uint32_t q0 = blockIdx.x * kAttnRows;

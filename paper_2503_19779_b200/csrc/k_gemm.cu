@@ -31,6 +31,7 @@ static constexpr int kBM = 128;
 static constexpr int kBK = 64;          // 64 bf16 = 128 B = one swizzle-128B row
 static constexpr int kStages = 4;
 static constexpr int kGemmThreads = 192;
+static constexpr uint32_t kGemmTriggerAfterWait = 1u << 8;   // internal flag bit (above CGX_GEMM_*)
 
 struct alignas(64) GemmArgs {
   CUtensorMap tmA;            // A [M, K] bf16, box {64, 128}
@@ -137,6 +138,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
   uint64_t* tmem_full = empty + kStages;
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(tmem_full + 1);
 
+  const bool late_trigger = a.flags & kGemmTriggerAfterWait;
+  if (!late_trigger) pdl_trigger();   // dependents may start their prologues (they read our output after their wait)
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n0 = blockIdx.x * BN;
   const int m0 = blockIdx.y * kBM;
@@ -172,7 +175,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
         tma_load_2d(sB + kb * kBBytes, &a.tmB, &full[kb], kb * kBK, n0);
       }
       pdl_wait();
-      pdl_trigger();
+      if (late_trigger) pdl_trigger();
       for (int kb = 0; kb < pre; ++kb) tma_load_2d(sA + kb * kABytes, &a.tmA, &full[kb], kb * kBK, m0);
       for (int kb = pre; kb < nk; ++kb) {
         const int s = kb % kStages;
@@ -305,6 +308,10 @@ static const void* setup_kernel() {
     cudaFuncSetAttribute(k_gemm_bf16<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<BN>());
   });
   return (const void*)k_gemm_bf16<BN>;
+}
+
+void decoder_gemm_set_trigger_after_wait(void* args) {
+  static_cast<GemmArgs*>(args)->flags |= kGemmTriggerAfterWait;
 }
 
 bool decoder_gemm_supported(uint32_t M, uint32_t N, uint32_t K) {

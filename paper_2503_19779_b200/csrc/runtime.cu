@@ -308,6 +308,7 @@ struct Launch {
   bool pdl = true;
   AlignedBuf args;
   std::vector<PtrField> ext;  // external operand fields
+  size_t tw_ptr_off = 0;      // T5 first node: byte offset of the by-value pointer array (0 = none)
   cudaGraphNode_t gnode[2] = {nullptr, nullptr};
   // NCCL
   const void* nc_in = nullptr;
@@ -345,6 +346,8 @@ struct cgx_exec {
   int copy_cap = 0;
   const void* copy_fn = nullptr;
   dim3 copy_grid;
+  unsigned copy_block = 256;
+  size_t copy_smem = 0;
   AlignedBuf copy_args;
   // INDIRECT
   uint64_t* d_table = nullptr;
@@ -372,10 +375,53 @@ static T* argp(Launch& l) { return reinterpret_cast<T*>(l.args.p); }
 
 // Build the launch record of one node. Operand addresses are resolved for `mode`:
 // EXTERNAL -> placeholder (COPY), table index (INDIRECT), or a patchable field (others).
+// T5 (FIRST_NODE): the first two launches of an INDIRECT exec take their external operands by value
+// (patched like SETPARAMS); the first one also publishes the table.
+static bool t5_byvalue(const cgx_exec* e, int pos) {
+  return e->o.mode == CGX_MODE_GRAPH_INDIRECT && eff_transport(e->o) == CGX_XPORT_FIRST_NODE && pos < 2;
+}
+
+template <typename Base>
+static void make_args(cgx_exec* e, Launch& l, bool tw) {
+  if (!tw) {
+    l.args.reset(sizeof(Base));
+    return;
+  }
+  const int n = (int)e->c->ext_slots.size();
+  const int cap = tw_cap(n);
+  size_t bytes = 0, ptr_off = 0;
+  switch (cap) {
+    case 8: {
+      using T = ArgsTW<Base, 8>;
+      bytes = sizeof(T);
+      ptr_off = offsetof(T, tw) + offsetof(TWPart<8>, ptr);
+      break;
+    }
+    case 64: {
+      using T = ArgsTW<Base, 64>;
+      bytes = sizeof(T);
+      ptr_off = offsetof(T, tw) + offsetof(TWPart<64>, ptr);
+      break;
+    }
+    default: {
+      using T = ArgsTW<Base, 512>;
+      bytes = sizeof(T);
+      ptr_off = offsetof(T, tw) + offsetof(TWPart<512>, ptr);
+      break;
+    }
+  }
+  l.args.reset(bytes);
+  TWPart<8>* tw8 = reinterpret_cast<TWPart<8>*>(l.args.p + ptr_off - offsetof(TWPart<8>, ptr));
+  tw8->table = e->d_table;
+  tw8->n = (uint32_t)n;
+  l.tw_ptr_off = ptr_off;
+}
+
 static int build_launch(cgx_exec* e, int k, Launch& l) {
   cgx_chain* c = e->c;
   const Node& n = c->nodes[k];
   const cgx_mode mode = e->o.mode;
+  const int pos = k - e->first;
   l.node = k;
   l.pdl = !e->o.no_pdl;
   auto slot_ptr = [&](int si) -> void* {
@@ -386,8 +432,14 @@ static int build_launch(cgx_exec* e, int k, Launch& l) {
     return const_cast<void*>(e->cur[s.ext_j]);   // EAGER/SETPARAMS/STALE: patched at bind
   };
   auto is_ext = [&](int si) { return c->slots[si].kind == CGX_SLOT_EXTERNAL; };
-  const bool indirect = mode == CGX_MODE_GRAPH_INDIRECT;
-  const bool patch = mode == CGX_MODE_EAGER || mode == CGX_MODE_GRAPH_SETPARAMS || mode == CGX_MODE_GRAPH_STALE;
+  const bool byvalue = t5_byvalue(e, pos);
+  const bool tw = byvalue && pos == 0;
+  const bool indirect = mode == CGX_MODE_GRAPH_INDIRECT && !byvalue;
+  const bool patch = mode == CGX_MODE_EAGER || mode == CGX_MODE_GRAPH_SETPARAMS || mode == CGX_MODE_GRAPH_STALE ||
+                     byvalue;
+  const int twc = tw ? tw_cap((int)c->ext_slots.size()) : 0;
+  if (tw && (twc == 0 || !(n.op <= CGX_OP_REDUCE_SUM || n.op == CGX_OP_LAYERNORM)))
+    return fail(CGX_E_UNSUPPORTED, "FIRST_NODE transport: first node must be elementwise/reduce/LN, <= 512 externals");
 
   switch (n.op) {
     case CGX_OP_ADD:
@@ -395,7 +447,7 @@ static int build_launch(cgx_exec* e, int k, Launch& l) {
     case CGX_OP_SCALE_IMM:
     case CGX_OP_COPY:
     case CGX_OP_REDUCE_SUM: {
-      l.args.reset(sizeof(ElemArgs));
+      make_args<ElemArgs>(e, l, tw);
       ElemArgs* a = argp<ElemArgs>(l);
       a->table = indirect ? e->d_table : nullptr;
       a->t0 = a->t1 = -1;
@@ -418,13 +470,13 @@ static int build_launch(cgx_exec* e, int k, Launch& l) {
         }
       }
       if (n.op == CGX_OP_REDUCE_SUM) {
-        l.func = kfn_reduce_sum_f32();
+        l.func = kfn_reduce_sum_f32(twc);
         l.block = dim3(256);
         l.grid = dim3((unsigned)std::max<uint64_t>(1, ceil_div(n.attr.n / n.attr.cols, 8)));
       } else {
         const int opi = n.op == CGX_OP_ADD ? 0 : n.op == CGX_OP_MUL ? 1 : n.op == CGX_OP_SCALE_IMM ? 2 : 3;
         const int dt = c->slots[n.out].dtype == CGX_F32 ? 0 : 1;
-        l.func = kfn_elem(opi, dt);
+        l.func = kfn_elem(opi, dt, twc);
         l.block = dim3(elem_block_threads());
         const uint64_t per_vec = dt == 0 ? 4 : 8;
         const uint64_t nv = n.attr.n / per_vec;
@@ -433,7 +485,7 @@ static int build_launch(cgx_exec* e, int k, Launch& l) {
       return CGX_OK;
     }
     case CGX_OP_LAYERNORM: {
-      l.args.reset(sizeof(LnArgs));
+      make_args<LnArgs>(e, l, tw);
       LnArgs* a = argp<LnArgs>(l);
       a->table = indirect ? e->d_table : nullptr;
       a->tx = -1;
@@ -455,7 +507,7 @@ static int build_launch(cgx_exec* e, int k, Launch& l) {
         }
       }
       decoder_ln_launch_dims(n.attr.rows, n.attr.cols, &l.grid, &l.block);
-      l.func = kfn_layernorm();
+      l.func = kfn_layernorm(twc);
       return CGX_OK;
     }
     case CGX_OP_GEMM_BF16: {
@@ -506,23 +558,21 @@ static int build_launch(cgx_exec* e, int k, Launch& l) {
   return fail(CGX_E_INVALID_ARG, "build_launch: unknown op");
 }
 
-// An operand of launch i may be loaded before griddepcontrol.wait iff it is not the output of the
-// launch that immediately precedes it in stream/graph order (for the first launch: the last one,
-// which precedes it across eager iterations). Every chain kernel triggers its dependents only after
-// its own wait, so all earlier launches have completed when launch i starts executing.
+// Pre-wait loads: with every kernel triggering at entry, a kernel may start while ANY earlier node
+// of the replay is still running, so only slots nothing inside the graph writes may be read before
+// griddepcontrol.wait: EXTERNAL inputs (bound before the replay; COPY placeholders are written by
+// the copy kernel, which fully precedes the graph) and STATIC weights.
 static void set_prewait_masks(cgx_exec* e) {
   if (e->o.no_pdl) return;
-  const int n = (int)e->L.size();
-  for (int i = 0; i < n; ++i) {
-    Launch& l = e->L[i];
+  for (auto& l : e->L) {
     if (l.kind != LK_KERNEL) continue;
     const Node& node = e->c->nodes[l.node];
     if (node.op > CGX_OP_REDUCE_SUM) continue;
-    const Launch& prev = e->L[(i + n - 1) % n];
-    const int prev_out = e->c->nodes[prev.node].out;
     uint32_t pre = 0;
-    for (int j = 0; j < node.n_in && j < 2; ++j)
-      if (node.in[j] != prev_out) pre |= 1u << j;
+    for (int j = 0; j < node.n_in && j < 2; ++j) {
+      const cgx_slot_kind k = e->c->slots[node.in[j]].kind;
+      if (k == CGX_SLOT_EXTERNAL || k == CGX_SLOT_STATIC) pre |= 1u << j;
+    }
     argp<ElemArgs>(l)->pre = pre;
   }
 }
@@ -581,10 +631,11 @@ static int setup_copy(cgx_exec* e) {
   }
   const int nt = (int)e->ext_read.size();
   if (nt > 1024) return fail(CGX_E_UNSUPPORTED, "COPY: more than 1024 external tensors");
-  // chunk size: spread the bytes over ~8 CTAs per SM, 16 KiB..256 KiB, 4 KiB multiple
-  uint64_t cb = ceil_div(data, 148ull * 8);
-  cb = std::min<uint64_t>(std::max<uint64_t>(cb, 16384), 262144);
-  cb = ceil_div(cb, 4096) * 4096;
+  // chunk = one unrolled sweep of a CTA (256 threads x 8 x 16 B = 32 KiB); many chunks per CTA
+  // keep the static round-robin balanced (<= ~1% tail at the 1 GiB point). Small totals use
+  // 8 KiB chunks so a few MB still spread over the SMs. The bulk variant uses its smem stage size.
+  uint64_t cb = data >= (64ull << 20) ? 32768 : 8192;
+  if (e->o.copy_impl == 2) cb = copy_bulk_chunk();
   e->chunk_bytes = (uint32_t)cb;
   std::vector<CopyDesc> desc(nt);
   std::vector<uint32_t> chunk;
@@ -604,8 +655,17 @@ static int setup_copy(cgx_exec* e) {
     CK(cudaMemcpy(e->d_chunk, chunk.data(), sizeof(uint32_t) * chunk.size(), cudaMemcpyHostToDevice));
   }
   e->copy_cap = nt <= 8 ? 8 : nt <= 64 ? 64 : 1024;
-  e->copy_fn = kfn_copy(e->copy_cap);
-  e->copy_grid = dim3(std::max<uint32_t>(1, std::min<uint32_t>(e->n_chunks, 148 * 8)));
+  if (e->o.copy_impl == 2) {
+    e->copy_fn = kfn_copy_bulk(e->copy_cap);
+    e->copy_block = 32;
+    e->copy_smem = copy_bulk_smem();
+    e->copy_grid = dim3(std::max<uint32_t>(1, std::min<uint32_t>(e->n_chunks, 148)));
+  } else {
+    e->copy_fn = kfn_copy(e->copy_cap);
+    e->copy_block = 256;
+    e->copy_smem = 0;
+    e->copy_grid = dim3(std::max<uint32_t>(1, std::min<uint32_t>(e->n_chunks, 148 * 8)));
+  }
   const size_t hdr = offsetof(CopyArgs<8>, src);
   e->copy_args.reset(hdr + sizeof(void*) * e->copy_cap);
   CopyArgs<8>* a = reinterpret_cast<CopyArgs<8>*>(e->copy_args.p);   // header layout is CAP-independent
@@ -645,6 +705,8 @@ static int setup_table(cgx_exec* e) {
       CK(cudaMemset(e->d_seq, 0, 64));
     }
   }
+  if (t == CGX_XPORT_FIRST_NODE && n > 512)
+    return fail(CGX_E_UNSUPPORTED, "FIRST_NODE transport: more than 512 externals");
   if (t == CGX_XPORT_ROOT_PARAMS) {
     if (n > 512) return fail(CGX_E_UNSUPPORTED, "ROOT_PARAMS transport: more than 512 externals");
     const int cap = n <= 8 ? 8 : n <= 64 ? 64 : 512;
@@ -697,10 +759,11 @@ static int capture_graph(cgx_exec* e, int gi) {
     if (l.kind == LK_KERNEL && first_kernel && after_root) {
       // the first consumer after a root node fetches table entries after its wait
       if (e->o.mode == CGX_MODE_GRAPH_INDIRECT) {
-        // ElemArgs/LnArgs both keep `flags` right after the operand fields; set per type
         const Node& n = e->c->nodes[l.node];
-        if (n.op == CGX_OP_LAYERNORM) argp<LnArgs>(l)->flags |= kFlagTableAfterWait;
-        else if (n.op <= CGX_OP_REDUCE_SUM) argp<ElemArgs>(l)->flags |= kFlagTableAfterWait;
+        const uint32_t f = kFlagTableAfterWait | kFlagTriggerAfterWait;
+        if (n.op == CGX_OP_LAYERNORM) argp<LnArgs>(l)->flags |= f;
+        else if (n.op <= CGX_OP_REDUCE_SUM) argp<ElemArgs>(l)->flags |= f;
+        else return fail(CGX_E_UNSUPPORTED, "first node after the root table writer must be elementwise/LN");
       }
       if (root_is_copy) l.pdl = false;
     }
@@ -740,8 +803,9 @@ extern "C" int cgx_exec_create_ex(cgx_chain* c, const cgx_exec_opts* opts, void*
   cgx_exec_opts o{};
   if (opts) o = *opts;
   if (o.mode < CGX_MODE_EAGER || o.mode > CGX_MODE_GRAPH_STALE) return fail(CGX_E_INVALID_ARG, "exec_create: mode");
-  if (o.transport < CGX_XPORT_DEFAULT || o.transport > CGX_XPORT_ROOT_MAPPED)
+  if (o.transport < CGX_XPORT_DEFAULT || o.transport > CGX_XPORT_FIRST_NODE)
     return fail(CGX_E_INVALID_ARG, "exec_create: transport");
+  if (o.copy_impl < 0 || o.copy_impl > 2) return fail(CGX_E_INVALID_ARG, "exec_create: copy_impl");
   const int K = (int)c->nodes.size();
   if (K == 0) return fail(CGX_E_STATE, "exec_create: empty chain");
   const int first = o.first_node, last = o.n_nodes ? o.first_node + o.n_nodes - 1 : K - 1;
@@ -771,6 +835,17 @@ extern "C" int cgx_exec_create_ex(cgx_chain* c, const cgx_exec_opts* opts, void*
   for (int k = first; k <= last; ++k)
     if ((st = build_launch(e, k, e->L[k - first])) != CGX_OK) return bail(st);
   set_prewait_masks(e);
+  if (o.mode == CGX_MODE_GRAPH_INDIRECT && eff_transport(o) == CGX_XPORT_FIRST_NODE && e->L.size() > 1) {
+    // second launch: by-value pointers, triggers its dependents only after its wait (so every later
+    // node starts after the first node -- the table writer -- has completed)
+    Launch& l2 = e->L[1];
+    const Node& n2 = c->nodes[l2.node];
+    if (l2.kind != LK_KERNEL) return bail(fail(CGX_E_UNSUPPORTED, "FIRST_NODE transport: second node is a collective"));
+    if (n2.op <= CGX_OP_REDUCE_SUM) argp<ElemArgs>(l2)->flags |= kFlagTriggerAfterWait;
+    else if (n2.op == CGX_OP_LAYERNORM) argp<LnArgs>(l2)->flags |= kFlagTriggerAfterWait;
+    else if (n2.op == CGX_OP_ATTN_CAUSAL) argp<AttnArgs>(l2)->flags |= kFlagTriggerAfterWait;
+    else if (n2.op == CGX_OP_GEMM_BF16) decoder_gemm_set_trigger_after_wait(l2.args.p);
+  }
   if (o.mode != CGX_MODE_EAGER) {
     cudaError_t ce = cudaStreamCreateWithFlags(&e->cs, cudaStreamNonBlocking);
     if (ce != cudaSuccess) return bail(cuda_fail(ce, "cudaStreamCreate", __LINE__));
@@ -795,7 +870,7 @@ extern "C" int cgx_exec_create_ex(cgx_chain* c, const cgx_exec_opts* opts, void*
   e->st.n_graph_nodes = e->graph_nodes;
   e->st.mode = (uint32_t)o.mode;
   e->st.transport = o.mode == CGX_MODE_GRAPH_INDIRECT ? (uint32_t)eff_transport(o) : 0;
-  e->st.kernels_per_replay = (uint32_t)kernels + (o.mode == CGX_MODE_GRAPH_COPY && o.copy_impl == 0 && !e->ext_read.empty()) +
+  e->st.kernels_per_replay = (uint32_t)kernels + (o.mode == CGX_MODE_GRAPH_COPY && o.copy_impl != 1 && !e->ext_read.empty()) +
                              ((o.mode == CGX_MODE_GRAPH_INDIRECT && e->root_fn) ? 1 : 0);
   *out = e;
   return CGX_OK;
@@ -913,7 +988,8 @@ extern "C" int cgx_bind(cgx_exec* e, const void* const* ext, int n_ext) {
         if (nt) {
           cudaLaunchConfig_t cfg{};
           cfg.gridDim = e->copy_grid;
-          cfg.blockDim = dim3(256);
+          cfg.blockDim = dim3(e->copy_block);
+          cfg.dynamicSmemBytes = e->copy_smem;
           cfg.stream = e->s;
           void* argv[1] = {e->copy_args.p};
           CK(cudaLaunchKernelExC(&cfg, e->copy_fn, argv));
@@ -925,7 +1001,24 @@ extern "C" int cgx_bind(cgx_exec* e, const void* const* ext, int n_ext) {
     }
     case CGX_MODE_GRAPH_INDIRECT: {
       const cgx_transport t = eff_transport(e->o);
-      if (t == CGX_XPORT_ROOT_PARAMS) {
+      if (t == CGX_XPORT_FIRST_NODE) {
+        patch_images(e);   // by-value operands of the first two launches
+        Launch& l0 = e->L[0];
+        memcpy(l0.args.p + l0.tw_ptr_off, ext, sizeof(uint64_t) * N);
+        for (size_t i = 0; i < e->L.size() && i < 2; ++i) {
+          Launch& l = e->L[i];
+          if (i == 1 && l.ext.empty()) continue;
+          cudaKernelNodeParams kp{};
+          kp.func = const_cast<void*>(l.func);
+          kp.gridDim = l.grid;
+          kp.blockDim = l.block;
+          kp.sharedMemBytes = (unsigned)l.smem;
+          void* argv[1] = {l.args.p};
+          kp.kernelParams = argv;
+          CK(cudaGraphExecKernelNodeSetParams(e->ge[0], l.gnode[0], &kp));
+          e->st.n_setparam_calls++;
+        }
+      } else if (t == CGX_XPORT_ROOT_PARAMS) {
         auto* a = reinterpret_cast<TableWriteArgs<8>*>(e->root_args.p);
         memcpy(a->ptr, ext, sizeof(uint64_t) * N);
         cudaKernelNodeParams kp{};

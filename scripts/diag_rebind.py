@@ -47,7 +47,7 @@ for cfg in sys.argv[1:] or ["C2", "C1"]:
     out = {}
     for name, mode, xp, nopdl in [("copy", "COPY", "DEFAULT", False), ("copy_nopdl", "COPY", "DEFAULT", True),
                                   ("t1", "INDIRECT", "H2D", False), ("t2", "INDIRECT", "ROOT_MEMCPY", False),
-                                  ("t3", "INDIRECT", "ROOT_PARAMS", False), ("t4", "INDIRECT", "ROOT_MAPPED", False),
+                                  ("t3", "INDIRECT", "ROOT_PARAMS", False), ("t4", "INDIRECT", "ROOT_MAPPED", False), ("t5", "INDIRECT", "FIRST_NODE", False),
                                   ("t3_nopdl", "INDIRECT", "ROOT_PARAMS", True), ("setparams", "SETPARAMS", "DEFAULT", False),
                                   ("eager", "EAGER", "DEFAULT", False)]:
         ex = chain.exec(mode, stream=stream, transport=xp, no_pdl=nopdl)
@@ -62,3 +62,37 @@ for cfg in sys.argv[1:] or ["C2", "C1"]:
     res[cfg] = out
     chain.close()
 print(json.dumps(res, indent=1))
+
+# ---- copy kernel variants at the C4 1 GiB point (bind = copy only)
+S = 1 << 30
+c4 = wl.c4_chain(S, window_mode=True)
+ch = runner.Chain(c4, runner.upload_statics(c4, wl.static_values(c4), dev))
+srcs = [torch.empty(S // 4, dtype=torch.float32, device=dev) for _ in range(3)]
+for i, t in enumerate(srcs):
+    cgx.fill_uniform_f32(t.data_ptr(), S // 4, sm.SEED, i, sh)
+arr = cgx.ptr_array([t.data_ptr() for t in srcs])
+cres = {}
+for impl in (0, 2, 1):
+    ex = ch.exec("COPY", stream=stream, copy_impl=impl)
+    ds = []
+    for i in range(12):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        stream.synchronize()
+        a.record(stream)
+        LIB.cgx_bind(ex.handle, arr, 3)
+        b.record(stream)
+        b.synchronize()
+        if i >= 2:
+            ds.append(a.elapsed_time(b) * 1e-3)
+    dt = statistics.median(ds)
+    cres[f"impl{impl}"] = {"us": dt * 1e6, "GBps": 6 * S / dt / 1e9}
+    ex.close()
+t = torch.empty(3 * S // 2, dtype=torch.bfloat16, device=dev)
+u = torch.empty_like(t)
+ds = []
+for i in range(12):
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(); u.copy_(t); b.record(); b.synchronize()
+    if i >= 2: ds.append(a.elapsed_time(b) * 1e-3)
+cres["torch_copy_3GiB"] = {"GBps": 2 * 3 * S / statistics.median(ds) / 1e9}
+print(json.dumps({"copy_1GiBx3": cres}, indent=1))

@@ -18,7 +18,7 @@ from synth.workloads import ChainSpec, NodeSpec, SlotSpec  # noqa: E402
 
 ARMS = [("EAGER", "DEFAULT"), ("COPY", "DEFAULT"), ("SETPARAMS", "DEFAULT"),
         ("INDIRECT", "H2D"), ("INDIRECT", "ROOT_MEMCPY"), ("INDIRECT", "ROOT_PARAMS"),
-        ("INDIRECT", "ROOT_MAPPED")]
+        ("INDIRECT", "ROOT_MAPPED"), ("INDIRECT", "FIRST_NODE")]
 
 
 @pytest.fixture(scope="module")
@@ -111,7 +111,7 @@ def test_stale_negative_control(rt):
 
 @pytest.mark.parametrize("mode,transport", [("EAGER", "DEFAULT"), ("COPY", "DEFAULT"),
                                             ("INDIRECT", "ROOT_PARAMS"), ("INDIRECT", "H2D"),
-                                            ("SETPARAMS", "DEFAULT")])
+                                            ("INDIRECT", "FIRST_NODE"), ("SETPARAMS", "DEFAULT")])
 def test_c2_parity_and_cross_arm_identity(rt, mode, transport):
     dev = torch.device("cuda:0")
     spec = wl.c2_chain()
@@ -176,8 +176,9 @@ def test_ragged_sizes(rt, n, cols):
     dev = torch.device("cuda:0")
     spec = _ragged_chain(n, cols)
     st = wl.static_values(spec)
-    for mode in ("EAGER", "INDIRECT", "COPY"):
-        outs, _, _ = _run(rt, spec, mode, "DEFAULT", 2, st, dev)
+    for mode, xp in (("EAGER", "DEFAULT"), ("INDIRECT", "DEFAULT"), ("INDIRECT", "FIRST_NODE"),
+                     ("COPY", "DEFAULT")):
+        outs, _, _ = _run(rt, spec, mode, xp, 2, st, dev)
         for r, got in enumerate(outs):
             env = eval_chain(spec, wl.external_values(spec, r), st)
             for k in ("a", "b", "c"):
@@ -290,4 +291,29 @@ def test_profile_select_matches_oracle(rt):
     dec2, est2 = cgx.select([p])
     prof["use_measured"] = False
     assert est2[0] == sel.estimates(prof) and dec2 == sel.select([prof])
+    chain.close()
+
+
+@pytest.mark.parametrize("impl", [0, 1, 2])
+def test_copy_impls_placeholders_bitexact(rt, impl):
+    """Every COPY implementation leaves placeholders byte-identical to the bound inputs, including
+    ragged tails (n*4 bytes not a multiple of 16) and tensors spanning many chunks."""
+    cgx, runner = rt
+    dev = torch.device("cuda:0")
+    sizes = [1, 3, 4099, 8191, 65536 + 5, (1 << 20) + 3, 3 << 20]
+    slots = [SlotSpec(f"x{i}", "external", "f32", n) for i, n in enumerate(sizes)]
+    slots += [SlotSpec(f"y{i}", "internal", "f32", n) for i, n in enumerate(sizes)]
+    nodes = [NodeSpec("COPY", (f"x{i}",), f"y{i}", {"n": n}) for i, n in enumerate(sizes)]
+    spec = ChainSpec("copies", slots, nodes, [(0, len(nodes) - 1)])
+    chain = runner.Chain(spec, {})
+    ex = chain.exec("COPY", copy_impl=impl)
+    for r in range(3):
+        vals = wl.external_values(spec, r)
+        t = runner.upload_externals(spec, vals, dev)
+        ex.bind(t)
+        ex.launch()
+        for i in range(len(sizes)):
+            assert np.array_equal(ex.output(f"x{i}"), vals[f"x{i}"]), (impl, i)   # placeholder
+            assert np.array_equal(ex.output(f"y{i}"), vals[f"x{i}"]), (impl, i)
+        assert ex.stats()["bytes_data_rebound"] == 4 * sum(sizes)
     chain.close()

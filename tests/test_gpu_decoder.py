@@ -49,11 +49,11 @@ def _gemm_chain(M, N, K, bias=True, gelu=False, residual=False):
     return ChainSpec(f"gemm{M}x{N}x{K}", slots, nodes, [(0, 1)])
 
 
-def _run(rt, spec, mode, replays, st, mode_vals="uniform"):
+def _run(rt, spec, mode, replays, st, mode_vals="uniform", transport="DEFAULT"):
     cgx, runner = rt
     dev = torch.device("cuda:0")
     chain = runner.Chain(spec, runner.upload_statics(spec, st, dev))
-    ex = chain.exec(mode)
+    ex = chain.exec(mode, transport=transport)
     outs, keep = [], []
     for r in range(replays):
         ext = wl.external_values(spec, r, mode_vals)
@@ -162,6 +162,7 @@ def test_c3_decoder_chain(rt, n_layers):
     res = {}
     for mode in ("EAGER", "COPY", "INDIRECT", "SETPARAMS"):
         res[mode] = _run(rt, spec, mode, 2, st)
+    res["FIRST_NODE"] = _run(rt, spec, "INDIRECT", 2, st, transport="FIRST_NODE")
     for r in range(2):
         ext = wl.external_values(spec, r)
         got = res["INDIRECT"][r]
@@ -171,9 +172,39 @@ def test_c3_decoder_chain(rt, n_layers):
         g = bits_to_f64(got[last])
         o = env[last]
         assert np.linalg.norm(g - o) / np.linalg.norm(o) <= 2e-2
-        for mode in ("EAGER", "COPY", "SETPARAMS"):      # bit-identical across arms
+        for mode in ("EAGER", "COPY", "SETPARAMS", "FIRST_NODE"):      # bit-identical across arms
             for k in got:
                 assert np.array_equal(res[mode][r][k], got[k]), (mode, k)
+
+
+def test_captured_allreduce_single_rank(rt):
+    """ALLREDUCE_SUM nodes are ncclAllReduce calls captured inside the graph.
+    With one rank (this run has one GPU) the sum over ranks is the identity: bit-exact."""
+    cgx, runner = rt
+    from paper_2503_19779_b200 import cgx as c
+    comm = c.nccl_comm_init(1, 0, c.nccl_unique_id(), 0)
+    try:
+        n = 128 * 768
+        slots = [SlotSpec("x", "external", "bf16", n), SlotSpec("a", "internal", "bf16", n),
+                 SlotSpec("b", "internal", "bf16", n), SlotSpec("c", "internal", "bf16", n)]
+        nodes = [NodeSpec("COPY", ("x",), "a", {"n": n}), NodeSpec("ALLREDUCE_SUM", ("a",), "b", {"n": n}),
+                 NodeSpec("ADD", ("b", "a"), "c", {"n": n})]
+        spec = ChainSpec("ar", slots, nodes, [(0, 2)])
+        dev = torch.device("cuda:0")
+        for mode in ("EAGER", "INDIRECT", "COPY"):
+            chain = runner.Chain(spec, {}, nccl_comm=comm)
+            ex = chain.exec(mode)
+            for r in range(2):
+                vals = wl.external_values(spec, r)
+                t = runner.upload_externals(spec, vals, dev)
+                ex.bind(t)
+                ex.launch()
+                assert np.array_equal(ex.output("b"), vals["x"])
+                ref = bf16_bits(ops.add(bits_to_f64(vals["x"]), bits_to_f64(vals["x"]), {}, "bf16"))
+                assert np.array_equal(ex.output("c"), ref)
+            chain.close()
+    finally:
+        c.nccl_comm_destroy(comm)
 
 
 def test_c3_t1_decode_shape(rt):
