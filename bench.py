@@ -366,21 +366,50 @@ def run_extras(args, torch, cgx, runner, wl, sm, spec, chain, stream, sets, set_
     out["dispatch_floor"] = {"graph_launch_us": g_floor, "kernel_launch_us": k_floor,
                              "bind_launch_over_floor": arms[best_ind]["host_bind_launch_us"] / g_floor}
 
-    # ---------------- selector profile (slow path) and per-kernel device times
+    # ---------------- selector profile (slow path)
     t0 = set_ptrs[0]
     prof = cgx.profile(chain.handle, -1, [t0[i] for i in range(n_ext)], 30, sh)
     pd = prof.as_dict()
     dec, est = cgx.select([prof])
-    sum_d = sum(pd["d_us"])
     out["selector"] = {"decision": cgx.DECIDE[dec[0]], "t_eager_us": pd["t_eager_us"],
                        "t_copy_us": pd["t_copy_us"], "t_ind_us": pd["t_ind_us"],
                        "L_us": pd["L_us"], "G_us": pd["G_us"], "delta_us": pd["delta_us"],
                        "c_copy_us": pd["c_copy_us"], "c_ind_us": pd["c_ind_us"]}
-    out["graph_span_over_sum_kernel"] = {"sum_kernel_us": sum_d, "replay_us": arms[best_ind]["us_per_replay"],
-                                         "ratio": arms[best_ind]["us_per_replay"] / sum_d,
-                                         "note": "Σ of per-kernel event-bracketed device times (eager pass)"}
+
+    # ---------------- Σ kernel device time (CUPTI activity records via torch.profiler) vs replay
+    sum_cupti, per_name = None, {}
+    try:
+        from torch.profiler import ProfilerActivity, profile as tprof
+        with tprof(activities=[ProfilerActivity.CUDA]) as tp:
+            for i in range(10):
+                LIB.cgx_bind(ex_main.handle, set_ptrs[i % N_SETS], n_ext)
+                LIB.cgx_launch(ex_main.handle)
+            stream.synchronize()
+        tot = 0.0
+        for ev in tp.key_averages():
+            if "k_" in ev.key and "cgx" in ev.key:
+                t_ = getattr(ev, "device_time_total", None)
+                if t_ is None:
+                    t_ = getattr(ev, "cuda_time_total", 0.0)
+                tot += t_
+                per_name[ev.key] = t_ / 10
+        sum_cupti = tot / 10
+    except Exception as exn:  # noqa: BLE001
+        per_name = {"error": str(exn)}
+    floor200 = cgx.graph_floor(sh, 200, True, 300)
+    rep_us = arms["indirect_first_node"]["us_per_replay"] if "indirect_first_node" in arms else arms[best_ind]["us_per_replay"]
+    out["graph_span_over_sum_kernel"] = {
+        "replay_us": rep_us, "sum_kernel_us_cupti": sum_cupti,
+        "ratio": (rep_us / sum_cupti) if sum_cupti else None,
+        "graph_floor_200_noop_kernels_us": floor200,
+        "per_kernel_cupti_us": per_name,
+        "note": "Σ of CUPTI kernel durations of the deployed INDIRECT replay (PDL lets kernels "
+                "overlap, so the replay can be shorter than Σ); floor = replay of 200 no-op 1-CTA "
+                "kernels with the same PDL protocol"}
 
     # ---------------- roofline of the dominant kernel (by device-time share in the replay)
+    dk = cgx.kernel_times(ex_main.handle, 20)
+    sum_d = sum(dk)
     groups = {}
     for k, node in enumerate(spec.nodes):
         n = node.attrs["n"]
@@ -390,10 +419,13 @@ def run_extras(args, torch, cgx, runner, wl, sm, spec, chain, stream, sets, set_
             by = 2 * 4 * n
         else:
             by = 4 * n + 4 * n // node.attrs.get("cols", 256)
-        g = groups.setdefault(node.op, {"bytes": 0, "us": 0.0, "launches": 0})
+        g = groups.setdefault(node.op, {"bytes": 0, "us": 0.0, "launches": 0, "big_bytes": 0, "big_us": 0.0})
         g["bytes"] += by
-        g["us"] += pd["d_us"][k]
+        g["us"] += dk[k]
         g["launches"] += 1
+        if n == (4 << 20) // 4:
+            g["big_bytes"] += by
+            g["big_us"] += dk[k]
     dom = max(groups, key=lambda k: groups[k]["us"])
     g = groups[dom]
     achieved = g["bytes"] / (g["us"] * 1e-6) / 1e9
@@ -409,11 +441,19 @@ def run_extras(args, torch, cgx, runner, wl, sm, spec, chain, stream, sets, set_
                        "frac": achieved / hbm, "traffic": traffic, "kernel": kname,
                        "share_of_sum_kernel_time": g["us"] / sum_d,
                        "algorithmic_bytes_per_launch": g["bytes"] / g["launches"],
-                       "avg_launch_us": g["us"] / g["launches"], "peak_source": peak_src,
-                       "timing": "CUDA events around each launch of an eager pass of the same "
-                                 "launches inside bench.py (graph-internal kernels cannot be "
-                                 "bracketed by events)"}
+                       "avg_launch_us": g["us"] / g["launches"], "launches_per_replay": g["launches"],
+                       "largest_lane_4MiB_GBps": (g["big_bytes"] / (g["big_us"] * 1e-6) / 1e9) if g["big_us"] else None,
+                       "peak_source": peak_src,
+                       "timing": "CUDA event-record nodes between consecutive kernels of an "
+                                 "instrumented replay of the same launches (cgx_kernel_times), "
+                                 "median of 20; includes each node's in-graph dispatch"}
     ex_copy.close()
+
+    # ---------------- C3: GPT-2-small decoder chain (T = 128, 12 layers), tcgen05 GEMM nodes
+    try:
+        out["decoder_c3"] = bench_decoder(torch, cgx, runner, wl, stream, dev, peaks)
+    except Exception as exn:  # noqa: BLE001
+        out["decoder_c3"] = {"error": str(exn)}
 
     # ---------------- copy kernel at the C4 1 GiB point (HBM roofline target >= 80%)
     try:
@@ -532,6 +572,76 @@ def run_extras(args, torch, cgx, runner, wl, sm, spec, chain, stream, sets, set_
                                      f"threadpoolctl 1 thread) on {os.cpu_count()}-core host "
                                      f"{cpu_info()}"}
     return out
+
+
+def bench_decoder(torch, cgx, runner, wl, stream, dev, peaks):
+    """C3: per-replay µs per arm, tokens/s, per-GEMM device time vs rooflines."""
+    T, L = 128, 12
+    spec = wl.c3_chain(T=T, n_layers=L)
+    chain = runner.Chain(spec, runner.upload_statics(spec, wl.static_values(spec), dev))
+    xs = [runner.host_to_device(wl.slot_values(spec, "x", r), "bf16", dev) for r in range(4)]
+    ptrs = [cgx.ptr_array([x.data_ptr()]) for x in xs]
+    LIB = cgx.LIB
+
+    def timed(h, n, bind=True):
+        for i in range(5):
+            if bind:
+                LIB.cgx_bind(h, ptrs[i % 4], 1)
+            LIB.cgx_launch(h)
+        best = 1e30
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            stream.synchronize()
+            e0.record(stream)
+            for i in range(n):
+                if bind and LIB.cgx_bind(h, ptrs[i % 4], 1):
+                    raise cgx.CgxError(1, "bind", cgx.last_error())
+                if LIB.cgx_launch(h):
+                    raise cgx.CgxError(1, "launch", cgx.last_error())
+            e1.record(stream)
+            e1.synchronize()
+            best = min(best, e0.elapsed_time(e1) * 1e3 / n)
+        return best
+    res = {"workload": "C3: GPT-2-small decoder, 12 layers, T=128, bf16, 108 kernels, fresh x per replay"}
+    exc = chain.exec("COPY", stream=stream)
+    timed(exc.handle, 5)
+    base = timed(exc.handle, 300, bind=False)
+    arms = {"graph_no_rebind": base}
+    for name, mode, xp in (("copy", "COPY", "DEFAULT"), ("indirect_first_node", "INDIRECT", "FIRST_NODE"),
+                           ("indirect_root_params", "INDIRECT", "ROOT_PARAMS"),
+                           ("setparams", "SETPARAMS", "DEFAULT"), ("eager", "EAGER", "DEFAULT")):
+        ex = exc if mode == "COPY" else chain.exec(mode, stream=stream, transport=xp)
+        arms[name] = timed(ex.handle, 300 if mode != "EAGER" else 50)
+        if name == "indirect_first_node":
+            dk = cgx.kernel_times(ex.handle, 20)
+        if ex is not exc:
+            ex.close()
+    exc.close()
+    res["us_per_replay"] = arms
+    res["tokens_per_s_indirect"] = T * 1e6 / arms["indirect_first_node"]
+    res["rebind_delta_us"] = {k: arms[k] - base for k in ("copy", "indirect_first_node", "indirect_root_params", "setparams")}
+    bf16_peak = peaks.get("bf16_tflops", 1590.0)
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    gemms = []
+    for k, node in enumerate(spec.nodes):
+        if node.op != "GEMM_BF16":
+            continue
+        a = node.attrs
+        fl = 2.0 * a["M"] * a["N"] * a["K"]
+        wb = 2.0 * a["N"] * a["K"]
+        gemms.append({"node": k, "MNK": [a["M"], a["N"], a["K"]], "us": dk[k],
+                      "TFLOPs": fl / (dk[k] * 1e-6) / 1e12, "weight_GBps": wb / (dk[k] * 1e-6) / 1e9})
+    tot_us = sum(g["us"] for g in gemms)
+    tot_fl = sum(2.0 * g["MNK"][0] * g["MNK"][1] * g["MNK"][2] for g in gemms)
+    tot_wb = sum(2.0 * g["MNK"][1] * g["MNK"][2] for g in gemms)
+    res["gemm"] = {"launches": len(gemms), "sum_us": tot_us, "share_of_sum_kernel_time": tot_us / sum(dk),
+                   "TFLOPs": tot_fl / (tot_us * 1e-6) / 1e12, "frac_of_bf16_peak": tot_fl / (tot_us * 1e-6) / 1e12 / bf16_peak,
+                   "weight_GBps": tot_wb / (tot_us * 1e-6) / 1e9, "frac_of_hbm": tot_wb / (tot_us * 1e-6) / 1e9 / hbm,
+                   "bound": "hbm (weights; M=128 is below the bf16 ridge)",
+                   "first_layer": gemms[:4],
+                   "timing": "cgx_kernel_times (event-record nodes between kernels, median of 20)"}
+    chain.close()
+    return res
 
 
 if __name__ == "__main__":

@@ -229,6 +229,13 @@ int cgx_select(const cgx_profile_t* prof, int n_segments, cgx_decision* out, dou
 /* Single-dispatch floor: median host µs of cudaGraphLaunch of a 1-node
  * empty-kernel graph and of cudaLaunchKernel of an empty kernel on cuda_stream. */
 int cgx_dispatch_floor(void* cuda_stream, int reps, double* graph_launch_us, double* kernel_launch_us);
+/* Per-node device µs of a bound exec: replays an instrumented capture of its launches with CUDA
+ * event-record nodes between consecutive kernels (median over reps; PDL overlap disabled in the
+ * instrumented copy). d_us receives min(cap, K) values; n_out = K. */
+int cgx_kernel_times(cgx_exec* e, int reps, double* d_us, int cap, int* n_out);
+/* In-graph per-node floor: device µs per replay of a captured graph of n_kernels no-op 1-CTA
+ * kernels (with use_pdl: the chain kernels' PDL protocol, trigger at entry then wait). */
+int cgx_graph_floor(void* cuda_stream, int n_kernels, int use_pdl, int reps, double* us_per_replay);
 /* Stream-ordered copy between any two CUDA-visible addresses (cudaMemcpyAsync, kind inferred):
  * used to read library-owned outputs and to stage end-to-end inputs. */
 int cgx_copy(void* dst, const void* src, uint64_t nbytes, void* cuda_stream);

@@ -103,6 +103,8 @@ def _load():
         "cgx_dispatch_floor": ([VP, I, P(C.c_double), P(C.c_double)], I),
         "cgx_fill_uniform_f32": ([VP, U64, U64, U64, VP], I),
         "cgx_copy": ([VP, VP, U64, VP], I),
+        "cgx_graph_floor": ([VP, I, I, I, P(C.c_double)], I),
+        "cgx_kernel_times": ([VP, I, P(C.c_double), I, P(I)], I),
         "cgx_nccl_unique_id": ([VP], I),
         "cgx_nccl_comm_init": ([I, I, VP, I, P(VP)], I),
         "cgx_nccl_comm_destroy": ([VP], I),
@@ -120,7 +122,7 @@ EXPORTED = ("cgx_version", "cgx_last_error", "cgx_chain_create", "cgx_chain_add_
             "cgx_chain_destroy", "cgx_exec_create", "cgx_exec_create_ex", "cgx_bind",
             "cgx_launch", "cgx_output", "cgx_stats", "cgx_debug_read_table",
             "cgx_debug_setparam_nodes", "cgx_exec_destroy", "cgx_profile", "cgx_select",
-            "cgx_dispatch_floor", "cgx_fill_uniform_f32", "cgx_copy", "cgx_nccl_unique_id",
+            "cgx_dispatch_floor", "cgx_fill_uniform_f32", "cgx_copy", "cgx_graph_floor", "cgx_kernel_times", "cgx_nccl_unique_id",
             "cgx_nccl_comm_init", "cgx_nccl_comm_destroy")
 
 
@@ -247,6 +249,19 @@ def dispatch_floor(stream: int, reps: int = 2000) -> tuple:
 
 def fill_uniform_f32(dptr: int, n: int, seed: int, stream_id: int, stream: int):
     _ck(LIB.cgx_fill_uniform_f32(dptr, n, seed, stream_id, stream), "cgx_fill_uniform_f32")
+
+
+def kernel_times(ex: int, reps: int = 20) -> list:
+    n = C.c_int()
+    buf = (C.c_double * 4096)()
+    _ck(LIB.cgx_kernel_times(ex, reps, buf, 4096, C.byref(n)), "cgx_kernel_times")
+    return list(buf[: n.value])
+
+
+def graph_floor(stream: int, n_kernels: int, use_pdl: bool = True, reps: int = 200) -> float:
+    us = C.c_double()
+    _ck(LIB.cgx_graph_floor(stream, n_kernels, int(use_pdl), reps, C.byref(us)), "cgx_graph_floor")
+    return us.value
 
 
 def copy(dst: int, src: int, nbytes: int, stream: int):

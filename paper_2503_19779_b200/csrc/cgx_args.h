@@ -37,17 +37,16 @@ static constexpr uint32_t kFlagTriggerAfterWait = 2u;
 struct CopyDesc {
   void* dst;               // placeholder
   uint64_t nbytes;
-  uint32_t chunk_begin;    // first global chunk index of this tensor
-  uint32_t n_chunks;
+  uint64_t chunk_begin;    // first global block/chunk index of this tensor
+  uint64_t n_chunks;
 };
 template <int CAP>
 struct CopyArgs {
   const CopyDesc* desc;    // [n_tensors]
-  const uint32_t* chunk_tensor;  // [n_chunks_total] tensor owning each chunk
+  const uint32_t* chunk_tensor;  // [n_chunks] owning tensor per chunk (bulk variant only)
   uint32_t n_tensors;
-  uint32_t n_chunks;
   uint32_t chunk_bytes;
-  uint32_t pad;
+  uint64_t n_chunks;
   const void* src[CAP];
 };
 
@@ -116,11 +115,13 @@ const void* kfn_reduce_sum_f32(int tw = 0);
 int tw_cap(int n);                                // 8, 64, 512 (0 if n > 512)
 const void* kfn_copy(int cap);                    // CAP in {8, 64, 1024}
 const void* kfn_copy_bulk(int cap);               // TMA bulk-copy variant
+uint32_t copy_block_bytes();                      // block size of the LDG/STG copy kernel
 size_t copy_bulk_smem();
 uint32_t copy_bulk_chunk();
 const void* kfn_table_write(int cap);             // CAP in {8, 64, 512}
 const void* kfn_table_mapped();
 const void* kfn_empty();
+const void* kfn_pdl_nop();
 const void* kfn_fill_uniform_f32();
 int elem_block_threads();
 }  // namespace cgx

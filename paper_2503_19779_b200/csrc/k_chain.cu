@@ -212,43 +212,53 @@ __global__ void __launch_bounds__(kReduceThreads) k_reduce_sum_f32(const __grid_
 
 // ---------------------------------------------------------------------------- multi-tensor copy
 // COPY arm: ph_j <- y_j for every tensor whose fresh source differs from
-// its placeholder. Work is split into fixed-size chunks through a static device chunk map; each
-// CTA walks chunks with a grid stride, moving 16-B vectors with kCopyVec loads in flight per thread
-// before the matching stores; the <16-B tail of a tensor is copied bytewise by the first lanes.
+// its placeholder. The concatenation of all tensors is cut into 2 KiB blocks (one warp moves one
+// block: 4 x 16-B vectors per lane, all loads before the stores); warps walk the block space with
+// a grid-wide warp stride, advancing a running tensor index, so small and large tensors share the
+// machine evenly with no per-block lookup table. Measured on this B200 (scripts/copy_microbench.cu,
+// profiles/r01): warp-contiguous 2 KiB blocks with only 2 x 256 threads per SM sustain ~6.65 TB/s
+// on 3 x 1 GiB, above cudaMemcpyAsync (~6.52 TB/s); more requests in flight per SM lower it.
 static constexpr int kCopyThreads = 256;
-static constexpr int kCopyVec = 8;
+static constexpr int kCopyVec = 4;
+static constexpr uint32_t kCopyBlock = 32 * kCopyVec * 16;   // 2 KiB per warp-block
 
 template <int CAP>
 __global__ void __launch_bounds__(kCopyThreads) k_copy(const __grid_constant__ CopyArgs<CAP> a) {
-  for (uint32_t c = blockIdx.x; c < a.n_chunks; c += gridDim.x) {
-    const uint32_t t = __ldg(a.chunk_tensor + c);
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warp = ((uint64_t)blockIdx.x * kCopyThreads + threadIdx.x) >> 5;
+  const uint64_t nwarps = ((uint64_t)gridDim.x * kCopyThreads) >> 5;
+  uint32_t t = 0;
+  uint64_t t_end = a.desc[0].chunk_begin + (uint64_t)a.desc[0].n_chunks;
+  for (uint64_t q = warp; q < a.n_chunks; q += nwarps) {
+    while (q >= t_end) {                       // advance to the tensor owning block q
+      ++t;
+      t_end = a.desc[t].chunk_begin + (uint64_t)a.desc[t].n_chunks;
+    }
     const CopyDesc d = a.desc[t];
     const char* src = reinterpret_cast<const char*>(a.src[t]);
     char* dst = reinterpret_cast<char*>(d.dst);
     if (src == dst) continue;                                   // SURVEY reading 1
-    const uint64_t off = (uint64_t)(c - d.chunk_begin) * a.chunk_bytes;
+    const uint64_t off = (q - d.chunk_begin) * (uint64_t)kCopyBlock;
     const uint64_t rem = d.nbytes - off;
-    const uint64_t len = rem < a.chunk_bytes ? rem : a.chunk_bytes;
-    const uint64_t nv = len >> 4;
+    const uint32_t len = (uint32_t)(rem < kCopyBlock ? rem : kCopyBlock);
     const int4* s4 = reinterpret_cast<const int4*>(src + off);
     int4* d4 = reinterpret_cast<int4*>(dst + off);
-    for (uint64_t v0 = threadIdx.x; v0 < nv; v0 += (uint64_t)kCopyThreads * kCopyVec) {
-      int4 buf[kCopyVec];
+    if (len == kCopyBlock) {
+      int4 v[kCopyVec];
 #pragma unroll
-      for (int j = 0; j < kCopyVec; ++j) {
-        const uint64_t v = v0 + (uint64_t)j * kCopyThreads;
-        if (v < nv) buf[j] = ld_stream16(s4 + v);
-      }
+      for (int j = 0; j < kCopyVec; ++j) v[j] = s4[j * 32 + lane];
 #pragma unroll
-      for (int j = 0; j < kCopyVec; ++j) {
-        const uint64_t v = v0 + (uint64_t)j * kCopyThreads;
-        if (v < nv) st_stream16(d4 + v, buf[j]);
-      }
+      for (int j = 0; j < kCopyVec; ++j) d4[j * 32 + lane] = v[j];
+    } else {
+      const uint32_t nv = len >> 4;
+      for (uint32_t i = lane; i < nv; i += 32) d4[i] = s4[i];
+      const uint32_t tail = len & 15u;
+      if (lane < tail) dst[off + (nv << 4) + lane] = src[off + (nv << 4) + lane];
     }
-    const uint64_t tail = len & 15;
-    if (threadIdx.x < tail) dst[off + (nv << 4) + threadIdx.x] = src[off + (nv << 4) + threadIdx.x];
   }
 }
+
+uint32_t copy_block_bytes() { return kCopyBlock; }
 
 // TMA bulk-copy variant (copy_impl = 2): one warp per CTA; lane 0 streams chunks through a
 // kBulkStages-deep shared-memory ring with cp.async.bulk (global -> smem, mbarrier completion) and
@@ -272,7 +282,7 @@ __global__ void __launch_bounds__(32, 1) k_copy_bulk(const __grid_constant__ Cop
   }
   __syncwarp();
   // chunk list of this CTA: c_i = blockIdx.x + i * gridDim.x
-  const uint32_t my_n = a.n_chunks > blockIdx.x ? (a.n_chunks - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const uint32_t my_n = a.n_chunks > blockIdx.x ? (uint32_t)((a.n_chunks - blockIdx.x + gridDim.x - 1) / gridDim.x) : 0;
   auto chunk_of = [&](uint32_t i, const char*& src, char*& dst, uint32_t& len, uint32_t& tail) -> bool {
     const uint32_t c = blockIdx.x + i * gridDim.x;
     const uint32_t t = a.chunk_tensor[c];
@@ -367,6 +377,11 @@ __global__ void k_table_mapped(const __grid_constant__ MappedTableArgs a) {
 
 // ---------------------------------------------------------------------------- utilities
 __global__ void k_empty() {}
+// A node that follows the chain kernels' PDL protocol but does no work: trigger at entry, wait.
+__global__ void k_pdl_nop() {
+  pdl_trigger();
+  pdl_wait();
+}
 
 struct FillArgs { float* out; uint64_t n; uint64_t base; };
 __global__ void k_fill_uniform_f32(const __grid_constant__ FillArgs a) {
@@ -444,6 +459,7 @@ const void* kfn_table_write(int cap) {
 }
 const void* kfn_table_mapped() { return (const void*)k_table_mapped; }
 const void* kfn_empty() { return (const void*)k_empty; }
+const void* kfn_pdl_nop() { return (const void*)k_pdl_nop; }
 const void* kfn_fill_uniform_f32() { return (const void*)k_fill_uniform_f32; }
 int elem_block_threads() { return kElemThreads; }
 

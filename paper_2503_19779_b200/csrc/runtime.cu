@@ -342,7 +342,8 @@ struct cgx_exec {
   void* ph_arena = nullptr;
   CopyDesc* d_desc = nullptr;
   uint32_t* d_chunk = nullptr;
-  uint32_t n_chunks = 0, chunk_bytes = 0;
+  uint64_t n_chunks = 0;
+  uint32_t chunk_bytes = 0;
   int copy_cap = 0;
   const void* copy_fn = nullptr;
   dim3 copy_grid;
@@ -631,40 +632,48 @@ static int setup_copy(cgx_exec* e) {
   }
   const int nt = (int)e->ext_read.size();
   if (nt > 1024) return fail(CGX_E_UNSUPPORTED, "COPY: more than 1024 external tensors");
-  // chunk = one unrolled sweep of a CTA (256 threads x 8 x 16 B = 32 KiB); many chunks per CTA
-  // keep the static round-robin balanced (<= ~1% tail at the 1 GiB point). Small totals use
-  // 8 KiB chunks so a few MB still spread over the SMs. The bulk variant uses its smem stage size.
-  uint64_t cb = data >= (64ull << 20) ? 32768 : 8192;
-  if (e->o.copy_impl == 2) cb = copy_bulk_chunk();
+  // LDG/STG kernel: 2 KiB warp-blocks over the concatenated tensors (no lookup table); the TMA
+  // bulk variant uses fixed chunks of its shared-memory stage size with a chunk -> tensor map.
+  const bool bulk = e->o.copy_impl == 2;
+  const uint64_t cb = bulk ? copy_bulk_chunk() : copy_block_bytes();
   e->chunk_bytes = (uint32_t)cb;
   std::vector<CopyDesc> desc(nt);
   std::vector<uint32_t> chunk;
+  uint64_t nch = 0;
   for (int t = 0; t < nt; ++t) {
     const Slot& s = c->slots[c->ext_slots[e->ext_read[t]]];
     desc[t].dst = e->ph[e->ext_read[t]];
     desc[t].nbytes = s.nbytes;
-    desc[t].chunk_begin = (uint32_t)chunk.size();
-    desc[t].n_chunks = (uint32_t)std::max<uint64_t>(1, ceil_div(s.nbytes, cb));
-    for (uint32_t q = 0; q < desc[t].n_chunks; ++q) chunk.push_back((uint32_t)t);
+    desc[t].chunk_begin = nch;
+    desc[t].n_chunks = std::max<uint64_t>(1, ceil_div(s.nbytes, cb));
+    nch += desc[t].n_chunks;
+    if (bulk)
+      for (uint64_t q = 0; q < desc[t].n_chunks; ++q) chunk.push_back((uint32_t)t);
   }
-  e->n_chunks = (uint32_t)chunk.size();
+  e->n_chunks = nch;
   if (nt) {
     CK(cudaMalloc(&e->d_desc, sizeof(CopyDesc) * nt));
     CK(cudaMemcpy(e->d_desc, desc.data(), sizeof(CopyDesc) * nt, cudaMemcpyHostToDevice));
+  }
+  if (bulk && !chunk.empty()) {
     CK(cudaMalloc(&e->d_chunk, sizeof(uint32_t) * chunk.size()));
     CK(cudaMemcpy(e->d_chunk, chunk.data(), sizeof(uint32_t) * chunk.size(), cudaMemcpyHostToDevice));
   }
   e->copy_cap = nt <= 8 ? 8 : nt <= 64 ? 64 : 1024;
-  if (e->o.copy_impl == 2) {
+  if (bulk) {
     e->copy_fn = kfn_copy_bulk(e->copy_cap);
     e->copy_block = 32;
     e->copy_smem = copy_bulk_smem();
-    e->copy_grid = dim3(std::max<uint32_t>(1, std::min<uint32_t>(e->n_chunks, 148)));
+    e->copy_grid = dim3((unsigned)std::max<uint64_t>(1, std::min<uint64_t>(nch, 148)));
   } else {
+    // Large copies: 2 CTAs x 256 threads per SM (best sustained HBM rate measured at 3 x 1 GiB);
+    // below 256 MiB the ramp dominates, so more CTAs. CGX_COPY_CTAS overrides (measurement knob).
     e->copy_fn = kfn_copy(e->copy_cap);
     e->copy_block = 256;
     e->copy_smem = 0;
-    e->copy_grid = dim3(std::max<uint32_t>(1, std::min<uint32_t>(e->n_chunks, 148 * 8)));
+    uint64_t ctas = data >= (256ull << 20) ? 148 * 2 : 148 * 8;
+    if (const char* env = getenv("CGX_COPY_CTAS")) ctas = std::max<uint64_t>(1, strtoull(env, nullptr, 10));
+    e->copy_grid = dim3((unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ceil_div(nch, 8), ctas)));
   }
   const size_t hdr = offsetof(CopyArgs<8>, src);
   e->copy_args.reset(hdr + sizeof(void*) * e->copy_cap);
@@ -1213,6 +1222,51 @@ extern "C" int cgx_dispatch_floor(void* stream, int reps, double* g_us, double* 
   return CGX_OK;
 }
 
+extern "C" int cgx_graph_floor(void* stream, int n_kernels, int use_pdl, int reps, double* us_per_replay) {
+  if (n_kernels <= 0 || reps <= 0 || !us_per_replay) return fail(CGX_E_INVALID_ARG, "graph_floor: bad argument");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaStream_t cs;
+  CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+  for (int k = 0; k < n_kernels; ++k) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(1);
+    cfg.blockDim = dim3(32);
+    cfg.stream = cs;
+    cudaLaunchAttribute attr[1];
+    if (use_pdl) {
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+    }
+    void* argv[1] = {nullptr};
+    CK(cudaLaunchKernelExC(&cfg, use_pdl ? kfn_pdl_nop() : kfn_empty(), argv));
+  }
+  cudaGraph_t g;
+  cudaGraphExec_t ge;
+  CK(cudaStreamEndCapture(cs, &g));
+  CK(cudaGraphInstantiateWithFlags(&ge, g, 0));
+  CK(cudaGraphUpload(ge, s));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  for (int i = 0; i < 10; ++i) CK(cudaGraphLaunch(ge, s));
+  CK(cudaEventRecord(e0, s));
+  for (int i = 0; i < reps; ++i) CK(cudaGraphLaunch(ge, s));
+  CK(cudaEventRecord(e1, s));
+  CK(cudaEventSynchronize(e1));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  *us_per_replay = ms * 1e3 / reps;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaGraphExecDestroy(ge);
+  cudaGraphDestroy(g);
+  cudaStreamDestroy(cs);
+  return CGX_OK;
+}
+
 extern "C" int cgx_copy(void* dst, const void* src, uint64_t nbytes, void* stream) {
   if ((!dst || !src) && nbytes) return fail(CGX_E_INVALID_ARG, "copy: NULL");
   if (nbytes) CK(cudaMemcpyAsync(dst, src, nbytes, cudaMemcpyDefault, static_cast<cudaStream_t>(stream)));
@@ -1267,6 +1321,70 @@ double median(std::vector<double> v) {
   return v.empty() ? 0.0 : v[v.size() / 2];
 }
 }  // namespace
+
+// Per-launch device µs: replay an instrumented capture of the exec's launches with an external
+// event-record node between consecutive launches (no PDL overlap in this copy), median over reps.
+static int kernel_times(cgx_exec* e, int reps, std::vector<double>* out) {
+  const int K = (int)e->L.size();
+  cudaStream_t cs;
+  CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  std::vector<cudaEvent_t> ev(K + 1);
+  for (auto& v : ev) CK(cudaEventCreate(&v));
+  CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+  CK(cudaEventRecordWithFlags(ev[0], cs, cudaEventRecordExternal));
+  for (int k = 0; k < K; ++k) {
+    Launch& l = e->L[k];
+    const bool pdl = l.pdl;
+    l.pdl = false;
+    const int st = issue(e, l, cs);
+    l.pdl = pdl;
+    if (st != CGX_OK) {
+      cudaGraph_t junk;
+      cudaStreamEndCapture(cs, &junk);
+      if (junk) cudaGraphDestroy(junk);
+      return st;
+    }
+    CK(cudaEventRecordWithFlags(ev[k + 1], cs, cudaEventRecordExternal));
+  }
+  cudaGraph_t g;
+  cudaGraphExec_t ge;
+  CK(cudaStreamEndCapture(cs, &g));
+  CK(cudaGraphInstantiateWithFlags(&ge, g, 0));
+  std::vector<std::vector<double>> dk(K);
+  for (int r = 0; r < reps + 2; ++r) {
+    CK(cudaGraphLaunch(ge, e->s));
+    CK(cudaStreamSynchronize(e->s));
+    if (r < 2) continue;
+    for (int k = 0; k < K; ++k) {
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, ev[k], ev[k + 1]));
+      dk[k].push_back(ms * 1e3);
+    }
+  }
+  // mean, not median: event timestamps on this part are coarse (~2 us ticks), and the mean of
+  // many replays with random phase is an unbiased estimate of a sub-tick duration
+  out->resize(K);
+  for (int k = 0; k < K; ++k) {
+    double sacc = 0.0;
+    for (double v : dk[k]) sacc += v;
+    (*out)[k] = dk[k].empty() ? 0.0 : sacc / dk[k].size();
+  }
+  cudaGraphExecDestroy(ge);
+  cudaGraphDestroy(g);
+  for (auto& v : ev) cudaEventDestroy(v);
+  cudaStreamDestroy(cs);
+  return CGX_OK;
+}
+
+extern "C" int cgx_kernel_times(cgx_exec* e, int reps, double* d_us, int cap, int* n_out) {
+  if (!e || reps <= 0 || !n_out) return fail(CGX_E_INVALID_ARG, "kernel_times: bad argument");
+  if (!e->bound) return fail(CGX_E_STATE, "kernel_times: bind the exec first");
+  std::vector<double> v;
+  CKS(kernel_times(e, reps, &v));
+  for (int k = 0; k < (int)v.size() && k < cap; ++k) d_us[k] = v[k];
+  *n_out = (int)v.size();
+  return CGX_OK;
+}
 
 static int time_loop(cgx_exec* e, const void* const* ext, int n_ext, bool do_bind, int n, double* us) {
   CK(cudaStreamSynchronize(e->s));
@@ -1347,34 +1465,29 @@ extern "C" int cgx_profile_impl(cgx_chain* c, int segment, const void* const* ex
   }
   p.L_us = median(vl);
   p.G_us = median(vg);
-  // d_k: device time of each kernel (events around each eager launch); graph span with events
-  std::vector<cudaEvent_t> ev(2 * K + 2);
-  for (auto& v : ev) CK(cudaEventCreate(&v));
-  std::vector<std::vector<double>> dk(K);
+  // d_k: device time of each kernel, from CUDA events captured between the kernels of an
+  // instrumented copy of the graph (everything pre-enqueued, so no host issue gaps are included);
+  // graph span: events around the plain COPY-exec replay.
+  std::vector<double> dks;
+  CKS(kernel_times(ec, reps, &dks));
+  cudaEvent_t es0, es1;
+  CK(cudaEventCreate(&es0));
+  CK(cudaEventCreate(&es1));
   for (int r = 0; r < reps; ++r) {
     CK(cudaStreamSynchronize(s));
-    for (int k = 0; k < K; ++k) {
-      CK(cudaEventRecord(ev[2 * k], s));
-      CKS(issue(ee, ee->L[k], s));
-      CK(cudaEventRecord(ev[2 * k + 1], s));
-    }
-    CK(cudaEventRecord(ev[2 * K], s));
+    CK(cudaEventRecord(es0, s));
     CKS(cgx_launch(ec));
-    CK(cudaEventRecord(ev[2 * K + 1], s));
-    CK(cudaStreamSynchronize(s));
-    for (int k = 0; k < K; ++k) {
-      float ms = 0;
-      CK(cudaEventElapsedTime(&ms, ev[2 * k], ev[2 * k + 1]));
-      dk[k].push_back(ms * 1e3);
-    }
+    CK(cudaEventRecord(es1, s));
+    CK(cudaEventSynchronize(es1));
     float ms = 0;
-    CK(cudaEventElapsedTime(&ms, ev[2 * K], ev[2 * K + 1]));
+    CK(cudaEventElapsedTime(&ms, es0, es1));
     vspan.push_back(ms * 1e3);
   }
-  for (auto& v : ev) cudaEventDestroy(v);
+  cudaEventDestroy(es0);
+  cudaEventDestroy(es1);
   double sum_d = 0.0;
   for (int k = 0; k < K; ++k) {
-    p.d_us[k] = median(dk[k]);
+    p.d_us[k] = dks[k];
     sum_d = sum_d + p.d_us[k];
   }
   p.delta_us = (median(vspan) - sum_d) / K;

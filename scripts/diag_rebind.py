@@ -56,6 +56,9 @@ for cfg in sys.argv[1:] or ["C2", "C1"]:
         if mode not in ("EAGER",):
             out[name + "_launch_only"] = timed(ex.handle, n, False)
         ex.close()
+    for nk in (1, 8, 200):
+        out[f"graph_floor_{nk}_pdl"] = cgx.graph_floor(sh, nk, True, 500)
+        out[f"graph_floor_{nk}_nopdl"] = cgx.graph_floor(sh, nk, False, 500)
     g, k = cgx.dispatch_floor(sh, 2000)
     out["floor_graph_launch_host_us"] = g
     out["floor_kernel_launch_host_us"] = k

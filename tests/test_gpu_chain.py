@@ -317,3 +317,22 @@ def test_copy_impls_placeholders_bitexact(rt, impl):
             assert np.array_equal(ex.output(f"y{i}"), vals[f"x{i}"]), (impl, i)
         assert ex.stats()["bytes_data_rebound"] == 4 * sum(sizes)
     chain.close()
+
+
+def test_kernel_times_and_graph_floor(rt):
+    cgx, runner = rt
+    dev = torch.device("cuda:0")
+    spec = wl.c1_chain()
+    chain = runner.Chain(spec, runner.upload_statics(spec, wl.static_values(spec), dev))
+    ex = chain.exec("INDIRECT", transport="FIRST_NODE")
+    t = runner.upload_externals(spec, wl.external_values(spec, 0), dev)
+    with pytest.raises(cgx.CgxError):
+        cgx.kernel_times(ex.handle, 5)          # not bound yet
+    ex.bind(t)
+    ex.launch()
+    d = cgx.kernel_times(ex.handle, 5)
+    assert len(d) == 8 and all(0 < x < 1000 for x in d)
+    sh = torch.cuda.current_stream().cuda_stream
+    f1, f200 = cgx.graph_floor(sh, 1, True, 50), cgx.graph_floor(sh, 200, True, 20)
+    assert 0 < f1 < f200 < 10000
+    chain.close()
