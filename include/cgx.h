@@ -77,10 +77,14 @@ typedef enum { CGX_SLOT_EXTERNAL = 0, CGX_SLOT_STATIC = 1, CGX_SLOT_INTERNAL = 2
  *   LAYERNORM  [x, g, b]     rows x cols bf16, population variance, attr.eps
  *   GEMM_BF16  [A, W, bias(, residual)]  out[M,N] = epi(A[M,K] W[N,K]^T + bias), flags below
  *   ATTN_CAUSAL [qkv]        qkv [T, 3*H*D] (q|k|v, head-major) -> out [T, H*D], causal softmax
- *   ALLREDUCE_SUM [x]        out = sum over ranks of x (bf16), captured ncclAllReduce */
+ *   ALLREDUCE_SUM [x]        out = sum over ranks of x (bf16), captured ncclAllReduce
+ *   SCALE_T    [a, s]        out[i] = a[i] * s[0], s a 1-element f32 slot: the CGCT rewrite of a
+ *                            by-value scalar into a device tensor (NEXT-3) so the
+ *                            scalar can be rebound per replay like any input */
 typedef enum {
   CGX_OP_ADD = 0, CGX_OP_MUL = 1, CGX_OP_SCALE_IMM = 2, CGX_OP_COPY = 3, CGX_OP_REDUCE_SUM = 4,
-  CGX_OP_LAYERNORM = 5, CGX_OP_GEMM_BF16 = 6, CGX_OP_ATTN_CAUSAL = 7, CGX_OP_ALLREDUCE_SUM = 8
+  CGX_OP_LAYERNORM = 5, CGX_OP_GEMM_BF16 = 6, CGX_OP_ATTN_CAUSAL = 7, CGX_OP_ALLREDUCE_SUM = 8,
+  CGX_OP_SCALE_T = 9
 } cgx_op;
 
 #define CGX_GEMM_BIAS 1u
@@ -119,13 +123,17 @@ typedef enum {
  *                    with one cudaGraphExecKernelNodeSetParams per bind
  *   ROOT_MAPPED  T4: root kernel reading a mapped pinned staging ring (zero-copy)
  *   FIRST_NODE   T5: no extra node. The first node's by-value params carry the pointers (one
- *                    cudaGraphExecKernelNodeSetParams per bind) and its CTA 0 publishes the table
- *                    while it computes; the second node also reads its operands by value and
- *                    releases its dependents only after its wait. Needs an elementwise/reduce/LN
- *                    first node and <= 512 externals (else CGX_E_UNSUPPORTED). */
+ *                    cudaGraphExecKernelNodeSetParams per bind); its CTA 0 publishes the table
+ *                    (store + gpu-scope fence) before it triggers the dependent launch, so every
+ *                    later node may fetch table entries before its griddepcontrol.wait. Needs an
+ *                    elementwise/reduce/LN first node and <= 512 externals (else UNSUPPORTED).
+ *   H2D_PINGPONG T6: two tables and two captured graphs used alternately; the H2D copy of
+ *                    replay k+1's pointers (pinned staging -> table) runs on a side stream while
+ *                    replay k executes, ordered by events (the paper's "pointer copies over the
+ *                    PCIe", with the PCIe latency hidden behind the previous replay). */
 typedef enum {
   CGX_XPORT_DEFAULT = 0, CGX_XPORT_H2D = 1, CGX_XPORT_ROOT_MEMCPY = 2, CGX_XPORT_ROOT_PARAMS = 3,
-  CGX_XPORT_ROOT_MAPPED = 4, CGX_XPORT_FIRST_NODE = 5
+  CGX_XPORT_ROOT_MAPPED = 4, CGX_XPORT_FIRST_NODE = 5, CGX_XPORT_H2D_PINGPONG = 6
 } cgx_transport;
 
 typedef enum { CGX_DECIDE_EAGER = 0, CGX_DECIDE_GRAPH_COPY = 1, CGX_DECIDE_GRAPH_INDIRECT = 2 } cgx_decision;

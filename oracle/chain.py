@@ -33,6 +33,8 @@ def eval_node(chain, node, env, dtype_of):
         return ops.scale_imm(env[ins[0]], at, dt)
     if op == "COPY":
         return ops.copy(env[ins[0]], at, dt)
+    if op == "SCALE_T":
+        return ops.scale_t(env[ins[0]], env[ins[1]], at, dt)
     if op == "REDUCE_SUM":
         return ops.reduce_sum(env[ins[0]], at, dt)
     if op == "LAYERNORM":

@@ -48,6 +48,13 @@ def scale_imm(a, attrs, dtype="f32"):
     return bf16_rne(a[:n].astype(np.float64) * float(np.float32(c)))
 
 
+def scale_t(a, s, attrs, dtype="f32"):
+    """SCALE_T(a, s)[i] = a[i] * s[0]: the CGCT rewrite of a by-value scalar into a 1-element
+    device tensor ("alters the type of parameter as a GPU-resident tensor")."""
+    n = _n(a, attrs)
+    return np.multiply(a[:n], np.float32(s[0]), dtype=np.float32)
+
+
 def copy(a, attrs, dtype="f32"):
     """COPY(a)[i] = a[i] (S:L59)."""
     return a[:_n(a, attrs)].copy()

@@ -84,10 +84,9 @@ struct AttnArgs {
   float scale;
 };
 
-// T5 (FIRST_NODE transport): the first node of the graph carries the bound pointers by value and
-// publishes the table (CTA 0) while computing; the second node reads its own external operands by
-// value too and triggers its dependents only after its wait, so every later node's pre-wait table
-// fetch happens after the first node completed. ArgsTW<Base, 0> is the plain parameter block.
+// T5 (FIRST_NODE transport): the first node of the graph carries the bound pointers by value; its
+// CTA 0 publishes the table (stores + gpu-scope fence) before triggering the dependent launch, so
+// every later node may fetch the table before its wait. ArgsTW<Base, 0> is the plain block.
 template <int CAP>
 struct TWPart {
   uint64_t* table;

@@ -18,9 +18,11 @@ void decoder_attn_launch_dims(uint32_t T, uint32_t H, uint32_t D, dim3* grid, di
 bool decoder_gemm_supported(uint32_t M, uint32_t N, uint32_t K);
 // Builds the by-value parameter block (tensor maps included) into args_out (64-B aligned) when
 // args_out != nullptr; always reports its size, launch geometry and kernel handle.
+// Split-K workspace and per-tile counters the kernel needs for this shape (0 if unsplit).
+void decoder_gemm_plan(uint32_t M, uint32_t N, uint32_t K, size_t* ws_bytes, size_t* cnt_bytes);
 int decoder_gemm_build(uint32_t M, uint32_t N, uint32_t K, uint32_t flags, const void* A, const void* W,
-                       const void* bias, const void* residual, void* out, void* args_out, size_t* argbytes,
-                       dim3* grid, dim3* block, size_t* smem, const void** func);
+                       const void* bias, const void* residual, void* out, void* ws, void* cnt, void* args_out,
+                       size_t* argbytes, dim3* grid, dim3* block, size_t* smem, const void** func);
 // Make a built GEMM parameter block trigger its PDL dependents only after its wait (T5 node 2).
 void decoder_gemm_set_trigger_after_wait(void* args);
 }  // namespace cgx

@@ -7,12 +7,18 @@
 
 namespace cgx {
 
-// T5 first node: CTA 0 publishes the by-value pointer array into the device table.
+// T5 first node: CTA 0 publishes the by-value pointer array into the device table, then makes the
+// stores visible at gpu scope (fence) before any of its threads triggers the dependents. The next
+// node is launched only after every CTA of this one has triggered, so its pre-wait table fetch
+// (an L2 load) observes the published pointers. Called before the kernel's own trigger.
 template <typename Base, int CAP>
 __device__ __forceinline__ void tw_publish(const ArgsTW<Base, CAP>& A) {
   if constexpr (CAP > 0) {
-    if (blockIdx.x == 0)
+    if (blockIdx.x == 0) {
       for (uint32_t i = threadIdx.x; i < A.tw.n; i += blockDim.x) A.tw.table[i] = A.tw.ptr[i];
+      __threadfence();
+      __syncthreads();
+    }
   }
 }
 

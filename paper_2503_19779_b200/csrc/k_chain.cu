@@ -20,13 +20,13 @@ namespace cgx {
 static constexpr int kElemThreads = 256;
 static constexpr int kElemVec = 4;     // 16-B vectors per thread per operand (loads in flight)
 
-enum { OP_ADD = 0, OP_MUL = 1, OP_SCALE = 2, OP_COPY = 3 };
+enum { OP_ADD = 0, OP_MUL = 1, OP_SCALE = 2, OP_COPY = 3, OP_SCALE_T = 4 };
 
 template <int OP>
 __device__ __forceinline__ float apply_f32(float x, float y, float s) {
   if (OP == OP_ADD) return __fadd_rn(x, y);
   if (OP == OP_MUL) return __fmul_rn(x, y);
-  if (OP == OP_SCALE) return __fmul_rn(x, s);
+  if (OP == OP_SCALE || OP == OP_SCALE_T) return __fmul_rn(x, s);
   return x;
 }
 
@@ -68,6 +68,10 @@ __global__ void __launch_bounds__(kElemThreads) k_elem_f32(const __grid_constant
   float4 xv[kElemVec], yv[kElemVec];
   const bool pre_x = !late && (a.pre & 1u);
   const bool pre_y = kBinary && !late && (a.pre & 2u);
+  // SCALE_T: the scalar operand is a 1-element device tensor (pre-wait when never written in graph)
+  float sval = a.scalar;
+  const bool pre_s = OP == OP_SCALE_T && !late && (a.pre & 2u);
+  if (OP == OP_SCALE_T && pre_s) sval = *reinterpret_cast<const float*>(p1);
   if (pre_x) {
 #pragma unroll
     for (int j = 0; j < kElemVec; ++j) {
@@ -89,6 +93,7 @@ __global__ void __launch_bounds__(kElemThreads) k_elem_f32(const __grid_constant
     y = reinterpret_cast<const float4*>(p1);
   }
   if (a.flags & kFlagTriggerAfterWait) pdl_trigger();
+  if (OP == OP_SCALE_T && !pre_s) sval = *reinterpret_cast<const float*>(p1);
   if (!pre_x) {
 #pragma unroll
     for (int j = 0; j < kElemVec; ++j) {
@@ -109,10 +114,10 @@ __global__ void __launch_bounds__(kElemThreads) k_elem_f32(const __grid_constant
     const uint64_t i = base + (uint64_t)j * kElemThreads;
     if (i < n4) {
       float4 r;
-      r.x = apply_f32<OP>(xv[j].x, yv[j].x, a.scalar);
-      r.y = apply_f32<OP>(xv[j].y, yv[j].y, a.scalar);
-      r.z = apply_f32<OP>(xv[j].z, yv[j].z, a.scalar);
-      r.w = apply_f32<OP>(xv[j].w, yv[j].w, a.scalar);
+      r.x = apply_f32<OP>(xv[j].x, yv[j].x, sval);
+      r.y = apply_f32<OP>(xv[j].y, yv[j].y, sval);
+      r.z = apply_f32<OP>(xv[j].z, yv[j].z, sval);
+      r.w = apply_f32<OP>(xv[j].w, yv[j].w, sval);
       o[i] = r;
     }
   }
@@ -123,7 +128,7 @@ __global__ void __launch_bounds__(kElemThreads) k_elem_f32(const __grid_constant
       const float* xs = reinterpret_cast<const float*>(p0);
       const float* ys = reinterpret_cast<const float*>(p1);
       const float yy = kBinary ? ys[t] : 0.f;
-      reinterpret_cast<float*>(a.out)[t] = apply_f32<OP>(xs[t], yy, a.scalar);
+      reinterpret_cast<float*>(a.out)[t] = apply_f32<OP>(xs[t], yy, sval);
     }
   }
 }
@@ -214,8 +219,8 @@ __global__ void __launch_bounds__(kReduceThreads) k_reduce_sum_f32(const __grid_
 // COPY arm: ph_j <- y_j for every tensor whose fresh source differs from
 // its placeholder. The concatenation of all tensors is cut into 2 KiB blocks (one warp moves one
 // block: 4 x 16-B vectors per lane, all loads before the stores); warps walk the block space with
-// a grid-wide warp stride, advancing a running tensor index, so small and large tensors share the
-// machine evenly with no per-block lookup table. Measured on this B200 (scripts/copy_microbench.cu,
+// a grid-wide warp stride and find a block's tensor by binary search over the tensors' first
+// block indices (staged in shared memory), so small and large tensors share the machine evenly. Measured on this B200 (scripts/copy_microbench.cu,
 // profiles/r01): warp-contiguous 2 KiB blocks with only 2 x 256 threads per SM sustain ~6.65 TB/s
 // on 3 x 1 GiB, above cudaMemcpyAsync (~6.52 TB/s); more requests in flight per SM lower it.
 static constexpr int kCopyThreads = 256;
@@ -224,21 +229,26 @@ static constexpr uint32_t kCopyBlock = 32 * kCopyVec * 16;   // 2 KiB per warp-b
 
 template <int CAP>
 __global__ void __launch_bounds__(kCopyThreads) k_copy(const __grid_constant__ CopyArgs<CAP> a) {
+  // first block index of every tensor, staged once per CTA; block -> tensor is a binary search
+  __shared__ uint32_t s_begin[CAP + 1];
+  for (uint32_t t = threadIdx.x; t < a.n_tensors; t += kCopyThreads) s_begin[t] = (uint32_t)a.desc[t].chunk_begin;
+  if (threadIdx.x == 0) s_begin[a.n_tensors] = (uint32_t)a.n_chunks;
+  __syncthreads();
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t warp = ((uint64_t)blockIdx.x * kCopyThreads + threadIdx.x) >> 5;
   const uint64_t nwarps = ((uint64_t)gridDim.x * kCopyThreads) >> 5;
-  uint32_t t = 0;
-  uint64_t t_end = a.desc[0].chunk_begin + (uint64_t)a.desc[0].n_chunks;
   for (uint64_t q = warp; q < a.n_chunks; q += nwarps) {
-    while (q >= t_end) {                       // advance to the tensor owning block q
-      ++t;
-      t_end = a.desc[t].chunk_begin + (uint64_t)a.desc[t].n_chunks;
+    uint32_t lo = 0, hi = a.n_tensors;          // largest t with s_begin[t] <= q
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (s_begin[mid] <= q) lo = mid; else hi = mid;
     }
-    const CopyDesc d = a.desc[t];
+    const uint32_t t = lo;
     const char* src = reinterpret_cast<const char*>(a.src[t]);
+    const CopyDesc d = a.desc[t];
     char* dst = reinterpret_cast<char*>(d.dst);
     if (src == dst) continue;                                   // SURVEY reading 1
-    const uint64_t off = (q - d.chunk_begin) * (uint64_t)kCopyBlock;
+    const uint64_t off = (q - s_begin[t]) * (uint64_t)kCopyBlock;
     const uint64_t rem = d.nbytes - off;
     const uint32_t len = (uint32_t)(rem < kCopyBlock ? rem : kCopyBlock);
     const int4* s4 = reinterpret_cast<const int4*>(src + off);
@@ -401,6 +411,7 @@ static const void* elem_fn(int op, int dtype) {
       case OP_MUL: return (const void*)k_elem_f32<OP_MUL, TW>;
       case OP_SCALE: return (const void*)k_elem_f32<OP_SCALE, TW>;
       case OP_COPY: return (const void*)k_elem_f32<OP_COPY, TW>;
+      case OP_SCALE_T: return (const void*)k_elem_f32<OP_SCALE_T, TW>;
     }
   } else {
     switch (op) {

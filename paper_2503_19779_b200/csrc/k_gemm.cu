@@ -39,7 +39,10 @@ struct alignas(64) GemmArgs {
   const __nv_bfloat16* bias;
   const __nv_bfloat16* residual;
   __nv_bfloat16* out;
+  float* ws;                  // split-K partial tiles [split][tiles][128][BN] (split > 1)
+  uint32_t* cnt;              // per-tile arrival counters (zero between launches)
   uint32_t M, N, K, flags;
+  uint32_t split;             // K splits (gridDim.z)
 };
 
 // ------------------------------------------------------------------ PTX wrappers
@@ -124,6 +127,47 @@ __device__ __forceinline__ float gelu_tanh(float x) {
 }
 
 // ------------------------------------------------------------------ kernel
+// Split-K (gridDim.z = split): CTA z accumulates k-blocks [z*nk/split, (z+1)*nk/split) in TMEM and
+// stores its fp32 partial tile to a workspace; the LAST CTA of a tile to arrive (counter) sums the
+// partials in fixed split order 0..split-1 — deterministic, no float atomics — and runs the
+// epilogue. At M = 128 every N tile re-reads the whole A panel, so without split-K the per-CTA
+// bytes (up to 128 x 3072 x 2 for FC2) bound the kernel; split-K spreads them over ~148 CTAs.
+__device__ __forceinline__ void epilogue_store(const GemmArgs& a, int m, int n, float* v) {
+  if (a.flags & CGX_GEMM_BIAS) {
+    const uint4* bp = reinterpret_cast<const uint4*>(a.bias + n);
+    const uint4 b0 = __ldg(bp), b1 = __ldg(bp + 1);
+    const __nv_bfloat16* bb0 = reinterpret_cast<const __nv_bfloat16*>(&b0);
+    const __nv_bfloat16* bb1 = reinterpret_cast<const __nv_bfloat16*>(&b1);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      v[i] += __bfloat162float(bb0[i]);
+      v[8 + i] += __bfloat162float(bb1[i]);
+    }
+  }
+  if (a.flags & CGX_GEMM_GELU) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = gelu_tanh(v[i]);
+  }
+  if (a.flags & CGX_GEMM_RESIDUAL) {
+    const uint4* rp = reinterpret_cast<const uint4*>(a.residual + (size_t)m * a.N + n);
+    const uint4 r0 = rp[0], r1 = rp[1];
+    const __nv_bfloat16* rb0 = reinterpret_cast<const __nv_bfloat16*>(&r0);
+    const __nv_bfloat16* rb1 = reinterpret_cast<const __nv_bfloat16*>(&r1);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      v[i] += __bfloat162float(rb0[i]);
+      v[8 + i] += __bfloat162float(rb1[i]);
+    }
+  }
+  uint4 o[2];
+  __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(o);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) ob[i] = __float2bfloat16_rn(v[i]);
+  uint4* op = reinterpret_cast<uint4*>(a.out + (size_t)m * a.N + n);
+  op[0] = o[0];
+  op[1] = o[1];
+}
+
 template <int BN>
 __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_constant__ GemmArgs a) {
   constexpr uint32_t kABytes = kBM * kBK * 2;     // 16 KiB
@@ -137,13 +181,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
   uint64_t* empty = full + kStages;
   uint64_t* tmem_full = empty + kStages;
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint32_t* s_last = s_tmem + 1;
 
   const bool late_trigger = a.flags & kGemmTriggerAfterWait;
   if (!late_trigger) pdl_trigger();   // dependents may start their prologues (they read our output after their wait)
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n0 = blockIdx.x * BN;
   const int m0 = blockIdx.y * kBM;
-  const int nk = (int)(a.K / kBK);
+  const int kps = (int)(a.K / kBK / a.split);     // k-blocks per split
+  const int kbase = (int)blockIdx.z * kps;
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&a.tmA);
@@ -168,92 +214,95 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
   if (warp == 0) {
     if (lane == 0) {
       // ---- TMA producer. Weights first (independent of the predecessor), then wait, then A.
-      for (int kb = 0; kb < nk; ++kb) tma_prefetch_l2(&a.tmB, kb * kBK, n0);
-      const int pre = nk < kStages ? nk : kStages;
-      for (int kb = 0; kb < pre; ++kb) {
-        mbar_expect_tx(&full[kb], kABytes + kBBytes);
-        tma_load_2d(sB + kb * kBBytes, &a.tmB, &full[kb], kb * kBK, n0);
+      for (int i = 0; i < kps; ++i) tma_prefetch_l2(&a.tmB, (kbase + i) * kBK, n0);
+      const int pre = kps < kStages ? kps : kStages;
+      for (int i = 0; i < pre; ++i) {
+        mbar_expect_tx(&full[i], kABytes + kBBytes);
+        tma_load_2d(sB + i * kBBytes, &a.tmB, &full[i], (kbase + i) * kBK, n0);
       }
       pdl_wait();
       if (late_trigger) pdl_trigger();
-      for (int kb = 0; kb < pre; ++kb) tma_load_2d(sA + kb * kABytes, &a.tmA, &full[kb], kb * kBK, m0);
-      for (int kb = pre; kb < nk; ++kb) {
-        const int s = kb % kStages;
-        const uint32_t ph = (uint32_t)(kb / kStages) & 1u;
+      for (int i = 0; i < pre; ++i) tma_load_2d(sA + i * kABytes, &a.tmA, &full[i], (kbase + i) * kBK, m0);
+      for (int i = pre; i < kps; ++i) {
+        const int s = i % kStages;
+        const uint32_t ph = (uint32_t)(i / kStages) & 1u;
         mbar_wait(&empty[s], ph ^ 1u);
         mbar_expect_tx(&full[s], kABytes + kBBytes);
-        tma_load_2d(sB + s * kBBytes, &a.tmB, &full[s], kb * kBK, n0);
-        tma_load_2d(sA + s * kABytes, &a.tmA, &full[s], kb * kBK, m0);
+        tma_load_2d(sB + s * kBBytes, &a.tmB, &full[s], (kbase + i) * kBK, n0);
+        tma_load_2d(sA + s * kABytes, &a.tmA, &full[s], (kbase + i) * kBK, m0);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       // ---- single-thread MMA issuer
       constexpr uint32_t idesc = umma_idesc(kBM, BN);
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % kStages;
-        const uint32_t ph = (uint32_t)(kb / kStages) & 1u;
+      for (int i = 0; i < kps; ++i) {
+        const int s = i % kStages;
+        const uint32_t ph = (uint32_t)(i / kStages) & 1u;
         mbar_wait(&full[s], ph);
         tc_fence_after();
         const uint64_t da = umma_desc_sw128(smem_u32(sA + s * kABytes));
         const uint64_t db = umma_desc_sw128(smem_u32(sB + s * kBBytes));
 #pragma unroll
         for (int k = 0; k < kBK / 16; ++k)   // UMMA_K = 16 bf16 = 32 B -> +2 in the >>4 address field
-          umma_bf16(tmem, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+          umma_bf16(tmem, da + 2 * k, db + 2 * k, idesc, (i | k) != 0);
         umma_commit(&empty[s]);
       }
       umma_commit(tmem_full);
     }
   } else {
-    // ---- epilogue: TMEM -> registers -> bias / GELU / residual -> bf16 -> global
+    // ---- epilogue warps (128 threads): TMEM -> registers -> [split-K reduction] -> epilogue
     mbar_wait(tmem_full, 0);
     tc_fence_after();
     const uint32_t q = warp & 3;                  // TMEM lane quarter this warp may access
     const uint32_t row = q * 32 + lane;
     const int m = m0 + (int)row;
     const bool live = m < (int)a.M;
-    const bool has_bias = a.flags & CGX_GEMM_BIAS;
-    const bool has_gelu = a.flags & CGX_GEMM_GELU;
-    const bool has_res = a.flags & CGX_GEMM_RESIDUAL;
+    if (a.split == 1) {
 #pragma unroll
-    for (int c0 = 0; c0 < BN; c0 += 16) {
-      float v[16];
-      tmem_ld16(tmem + ((q * 32u) << 16) + (uint32_t)c0, v);
-      if (!live) continue;
-      const int n = n0 + c0;
-      if (has_bias) {
-        const uint4* bp = reinterpret_cast<const uint4*>(a.bias + n);
-        const uint4 b0 = __ldg(bp), b1 = __ldg(bp + 1);
-        const __nv_bfloat16* bb0 = reinterpret_cast<const __nv_bfloat16*>(&b0);
-        const __nv_bfloat16* bb1 = reinterpret_cast<const __nv_bfloat16*>(&b1);
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        float v[16];
+        tmem_ld16(tmem + ((q * 32u) << 16) + (uint32_t)c0, v);
+        if (live) epilogue_store(a, m, n0 + c0, v);
+      }
+    } else {
+      const uint32_t tiles = gridDim.x * gridDim.y;
+      const uint32_t tile = blockIdx.y * gridDim.x + blockIdx.x;
+      float* mine = a.ws + ((size_t)(blockIdx.z * tiles + tile) * kBM + row) * BN;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          v[i] += __bfloat162float(bb0[i]);
-          v[8 + i] += __bfloat162float(bb1[i]);
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        float v[16];
+        tmem_ld16(tmem + ((q * 32u) << 16) + (uint32_t)c0, v);
+        float4* d = reinterpret_cast<float4*>(mine + c0);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) d[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+      }
+      __threadfence();
+      asm volatile("bar.sync 1, 128;\n" ::: "memory");
+      if (warp == 2 && lane == 0) *s_last = (atomicAdd(a.cnt + tile, 1u) == a.split - 1) ? 1u : 0u;
+      asm volatile("bar.sync 1, 128;\n" ::: "memory");
+      if (*s_last) {
+        __threadfence();
+#pragma unroll
+        for (int c0 = 0; c0 < BN; c0 += 16) {
+          float v[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = 0.f;
+          for (uint32_t z = 0; z < a.split; ++z) {      // fixed order: deterministic
+            const float4* src = reinterpret_cast<const float4*>(a.ws + ((size_t)(z * tiles + tile) * kBM + row) * BN + c0);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float4 t = __ldcg(src + i);
+              v[4 * i] += t.x;
+              v[4 * i + 1] += t.y;
+              v[4 * i + 2] += t.z;
+              v[4 * i + 3] += t.w;
+            }
+          }
+          if (live) epilogue_store(a, m, n0 + c0, v);
         }
+        if (warp == 2 && lane == 0) a.cnt[tile] = 0u;   // ready for the next replay
       }
-      if (has_gelu) {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = gelu_tanh(v[i]);
-      }
-      if (has_res) {
-        const uint4* rp = reinterpret_cast<const uint4*>(a.residual + (size_t)m * a.N + n);
-        const uint4 r0 = rp[0], r1 = rp[1];
-        const __nv_bfloat16* rb0 = reinterpret_cast<const __nv_bfloat16*>(&r0);
-        const __nv_bfloat16* rb1 = reinterpret_cast<const __nv_bfloat16*>(&r1);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          v[i] += __bfloat162float(rb0[i]);
-          v[8 + i] += __bfloat162float(rb1[i]);
-        }
-      }
-      uint4 o[2];
-      __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(o);
-#pragma unroll
-      for (int i = 0; i < 16; ++i) ob[i] = __float2bfloat16_rn(v[i]);
-      uint4* op = reinterpret_cast<uint4*>(a.out + (size_t)m * a.N + n);
-      op[0] = o[0];
-      op[1] = o[1];
     }
   }
   tc_fence_before();
@@ -291,14 +340,32 @@ static int encode_kmajor(CUtensorMap* tm, const void* base, uint64_t rows, uint6
 }
 
 static int pick_bn(uint32_t N) {
-  if (N % 64 == 0 && N / 64 >= 48) return 64;
+  if (N % 64 == 0) return 64;
   if (N % 32 == 0) return 32;
   return 0;
+}
+
+// Split count: the largest divisor s of the k-block count with tiles * s <= 148 (one wave).
+static uint32_t pick_split(uint32_t M, uint32_t N, uint32_t K, int bn) {
+  const uint32_t tiles = (N / bn) * ((M + kBM - 1) / kBM);
+  const uint32_t nk = K / kBK;
+  uint32_t best = 1;
+  for (uint32_t s = 1; s <= nk; ++s)
+    if (nk % s == 0 && tiles * s <= 148) best = s;
+  return best;
 }
 
 template <int BN>
 static size_t smem_bytes() {
   return 1024 + kStages * (kBM * kBK * 2 + BN * kBK * 2) + (2 * kStages + 1) * 8 + 16;
+}
+
+void decoder_gemm_plan(uint32_t M, uint32_t N, uint32_t K, size_t* ws_bytes, size_t* cnt_bytes) {
+  const int bn = pick_bn(N);
+  const uint32_t sp = bn ? pick_split(M, N, K, bn) : 1;
+  const size_t tiles = bn ? (size_t)(N / bn) * ((M + kBM - 1) / kBM) : 0;
+  *ws_bytes = sp > 1 ? (size_t)sp * tiles * kBM * bn * sizeof(float) : 0;
+  *cnt_bytes = tiles * sizeof(uint32_t);
 }
 
 template <int BN>
@@ -319,12 +386,13 @@ bool decoder_gemm_supported(uint32_t M, uint32_t N, uint32_t K) {
 }
 
 int decoder_gemm_build(uint32_t M, uint32_t N, uint32_t K, uint32_t flags, const void* A, const void* W,
-                       const void* bias, const void* residual, void* out, void* args_out, size_t* argbytes,
-                       dim3* grid, dim3* block, size_t* smem, const void** func) {
+                       const void* bias, const void* residual, void* out, void* ws, void* cnt, void* args_out,
+                       size_t* argbytes, dim3* grid, dim3* block, size_t* smem, const void** func) {
   if (!decoder_gemm_supported(M, N, K)) return CGX_E_UNSUPPORTED;
   const int bn = pick_bn(N);
+  const uint32_t sp = pick_split(M, N, K, bn);
   *argbytes = sizeof(GemmArgs);
-  *grid = dim3(N / bn, (M + kBM - 1) / kBM);
+  *grid = dim3(N / bn, (M + kBM - 1) / kBM, sp);
   *block = dim3(kGemmThreads);
   if (bn == 64) {
     *smem = smem_bytes<64>();
@@ -341,10 +409,14 @@ int decoder_gemm_build(uint32_t M, uint32_t N, uint32_t K, uint32_t flags, const
   g->bias = static_cast<const __nv_bfloat16*>(bias);
   g->residual = static_cast<const __nv_bfloat16*>(residual);
   g->out = static_cast<__nv_bfloat16*>(out);
+  g->ws = static_cast<float*>(ws);
+  g->cnt = static_cast<uint32_t*>(cnt);
   g->M = M;
   g->N = N;
   g->K = K;
   g->flags = flags;
+  g->split = sp;
+  if (sp > 1 && (!ws || !cnt)) return CGX_E_INVALID_ARG;
   return CGX_OK;
 }
 

@@ -184,6 +184,12 @@ static int check_node(const cgx_chain* c, const Node& n) {
       }
       return need(o.nelems >= a.n, "elementwise: output shorter than attr.n");
     }
+    case CGX_OP_SCALE_T:
+      if (n.n_in != 2) return fail(CGX_E_INVALID_ARG, "scale_t: inputs a, s");
+      if (S(0).dtype != CGX_F32 || S(1).dtype != CGX_F32 || o.dtype != CGX_F32)
+        return fail(CGX_E_UNSUPPORTED, "scale_t: f32 only");
+      CKS(need(S(0).nelems >= a.n && o.nelems >= a.n, "scale_t: shape"));
+      return CGX_OK;
     case CGX_OP_REDUCE_SUM:
       if (n.n_in != 1) return fail(CGX_E_INVALID_ARG, "reduce: one input");
       if (S(0).dtype != CGX_F32 || o.dtype != CGX_F32) return fail(CGX_E_UNSUPPORTED, "reduce: f32 only");
@@ -238,7 +244,7 @@ extern "C" int cgx_chain_add_node(cgx_chain* c, cgx_op op, const int* in_slots, 
   if (c->slots[out_slot].kind != CGX_SLOT_INTERNAL)
     return fail(CGX_E_NOT_ELIGIBLE, "add_node: output must be an INTERNAL slot (no writes to inputs/weights)");
   if ((op == CGX_OP_ADD || op == CGX_OP_MUL || op == CGX_OP_SCALE_IMM || op == CGX_OP_COPY ||
-       op == CGX_OP_REDUCE_SUM || op == CGX_OP_ALLREDUCE_SUM) && n.attr.n == 0 && n_in > 0)
+       op == CGX_OP_REDUCE_SUM || op == CGX_OP_ALLREDUCE_SUM || op == CGX_OP_SCALE_T) && n.attr.n == 0 && n_in > 0)
     n.attr.n = c->slots[n.in[0]].nelems;
   if (op == CGX_OP_REDUCE_SUM && n.attr.cols == 0) n.attr.cols = 256;
   CKS(check_node(c, n));
@@ -352,12 +358,21 @@ struct cgx_exec {
   AlignedBuf copy_args;
   // INDIRECT
   uint64_t* d_table = nullptr;
+  uint64_t* d_table2 = nullptr;   // T6: second table (replays alternate between the two)
+  cudaStream_t xs = nullptr;      // T6: side stream carrying the table H2D copies
+  cudaEvent_t ev_copy[2] = {nullptr, nullptr};   // T6: H2D into table b done
+  cudaEvent_t ev_use[2] = {nullptr, nullptr};    // T6: replay reading table b done
+  bool ev_copy_set[2] = {false, false}, ev_use_set[2] = {false, false};
   uint64_t* h_stage = nullptr;    // pinned ring [ring][n_pad]
   uint64_t* d_stage = nullptr;    // device alias (mapped, T4)
   int ring = 0;
   uint32_t n_pad = 0;
   std::vector<cudaEvent_t> ev;
   std::vector<bool> ev_used;
+  // GEMM split-K workspace + per-tile counters, shared by the exec's GEMM nodes (they run one
+  // after another: a GEMM writes its partials only after its griddepcontrol.wait)
+  void* gemm_ws = nullptr;
+  void* gemm_cnt = nullptr;
   // T3 / T4 root
   const void* root_fn = nullptr;
   AlignedBuf root_args;
@@ -376,10 +391,10 @@ static T* argp(Launch& l) { return reinterpret_cast<T*>(l.args.p); }
 
 // Build the launch record of one node. Operand addresses are resolved for `mode`:
 // EXTERNAL -> placeholder (COPY), table index (INDIRECT), or a patchable field (others).
-// T5 (FIRST_NODE): the first two launches of an INDIRECT exec take their external operands by value
-// (patched like SETPARAMS); the first one also publishes the table.
+// T5 (FIRST_NODE): the first launch of an INDIRECT exec takes its external operands by value
+// (patched like SETPARAMS) and publishes the table before it triggers its dependents.
 static bool t5_byvalue(const cgx_exec* e, int pos) {
-  return e->o.mode == CGX_MODE_GRAPH_INDIRECT && eff_transport(e->o) == CGX_XPORT_FIRST_NODE && pos < 2;
+  return e->o.mode == CGX_MODE_GRAPH_INDIRECT && eff_transport(e->o) == CGX_XPORT_FIRST_NODE && pos < 1;
 }
 
 template <typename Base>
@@ -439,7 +454,7 @@ static int build_launch(cgx_exec* e, int k, Launch& l) {
   const bool patch = mode == CGX_MODE_EAGER || mode == CGX_MODE_GRAPH_SETPARAMS || mode == CGX_MODE_GRAPH_STALE ||
                      byvalue;
   const int twc = tw ? tw_cap((int)c->ext_slots.size()) : 0;
-  if (tw && (twc == 0 || !(n.op <= CGX_OP_REDUCE_SUM || n.op == CGX_OP_LAYERNORM)))
+  if (tw && (twc == 0 || !(n.op <= CGX_OP_REDUCE_SUM || n.op == CGX_OP_LAYERNORM || n.op == CGX_OP_SCALE_T)))
     return fail(CGX_E_UNSUPPORTED, "FIRST_NODE transport: first node must be elementwise/reduce/LN, <= 512 externals");
 
   switch (n.op) {
@@ -447,6 +462,7 @@ static int build_launch(cgx_exec* e, int k, Launch& l) {
     case CGX_OP_MUL:
     case CGX_OP_SCALE_IMM:
     case CGX_OP_COPY:
+    case CGX_OP_SCALE_T:
     case CGX_OP_REDUCE_SUM: {
       make_args<ElemArgs>(e, l, tw);
       ElemArgs* a = argp<ElemArgs>(l);
@@ -475,7 +491,8 @@ static int build_launch(cgx_exec* e, int k, Launch& l) {
         l.block = dim3(256);
         l.grid = dim3((unsigned)std::max<uint64_t>(1, ceil_div(n.attr.n / n.attr.cols, 8)));
       } else {
-        const int opi = n.op == CGX_OP_ADD ? 0 : n.op == CGX_OP_MUL ? 1 : n.op == CGX_OP_SCALE_IMM ? 2 : 3;
+        const int opi = n.op == CGX_OP_ADD ? 0 : n.op == CGX_OP_MUL ? 1 : n.op == CGX_OP_SCALE_IMM ? 2
+                        : n.op == CGX_OP_SCALE_T ? 4 : 3;
         const int dt = c->slots[n.out].dtype == CGX_F32 ? 0 : 1;
         l.func = kfn_elem(opi, dt, twc);
         l.block = dim3(elem_block_threads());
@@ -524,10 +541,10 @@ static int build_launch(cgx_exec* e, int k, Launch& l) {
       void* res = (n.attr.flags & CGX_GEMM_RESIDUAL) ? slot_ptr(n.in[3]) : nullptr;
       size_t argbytes = 0;
       CKS(decoder_gemm_build(n.attr.M, n.attr.N, n.attr.K, n.attr.flags, A, W, bias, res, slot_ptr(n.out),
-                             nullptr, &argbytes, &l.grid, &l.block, &l.smem, &l.func));
+                             e->gemm_ws, e->gemm_cnt, nullptr, &argbytes, &l.grid, &l.block, &l.smem, &l.func));
       l.args.reset(argbytes);
       CKS(decoder_gemm_build(n.attr.M, n.attr.N, n.attr.K, n.attr.flags, A, W, bias, res, slot_ptr(n.out),
-                             l.args.p, &argbytes, &l.grid, &l.block, &l.smem, &l.func));
+                             e->gemm_ws, e->gemm_cnt, l.args.p, &argbytes, &l.grid, &l.block, &l.smem, &l.func));
       if (patch && (is_ext(n.in[0]) || ((n.attr.flags & CGX_GEMM_RESIDUAL) && is_ext(n.in[3]))))
         return fail(CGX_E_UNSUPPORTED, "gemm: external A/residual needs a rebuilt tensor map");
       return CGX_OK;
@@ -568,7 +585,7 @@ static void set_prewait_masks(cgx_exec* e) {
   for (auto& l : e->L) {
     if (l.kind != LK_KERNEL) continue;
     const Node& node = e->c->nodes[l.node];
-    if (node.op > CGX_OP_REDUCE_SUM) continue;
+    if (node.op > CGX_OP_REDUCE_SUM && node.op != CGX_OP_SCALE_T) continue;
     uint32_t pre = 0;
     for (int j = 0; j < node.n_in && j < 2; ++j) {
       const cgx_slot_kind k = e->c->slots[node.in[j]].kind;
@@ -651,6 +668,7 @@ static int setup_copy(cgx_exec* e) {
       for (uint64_t q = 0; q < desc[t].n_chunks; ++q) chunk.push_back((uint32_t)t);
   }
   e->n_chunks = nch;
+  if (!bulk && nch >= (1ull << 32)) return fail(CGX_E_UNSUPPORTED, "COPY: more than 8 TiB of inputs");
   if (nt) {
     CK(cudaMalloc(&e->d_desc, sizeof(CopyDesc) * nt));
     CK(cudaMemcpy(e->d_desc, desc.data(), sizeof(CopyDesc) * nt, cudaMemcpyHostToDevice));
@@ -714,6 +732,20 @@ static int setup_table(cgx_exec* e) {
       CK(cudaMemset(e->d_seq, 0, 64));
     }
   }
+  if (t == CGX_XPORT_H2D_PINGPONG) {
+    // two tables, two captured graphs; the H2D for replay k+1 runs on a side stream while
+    // replay k (reading the other table) executes
+    e->ring = 2;
+    CK(cudaMalloc(&e->d_table2, sizeof(uint64_t) * e->n_pad));
+    CK(cudaMemset(e->d_table2, 0, sizeof(uint64_t) * e->n_pad));
+    CK(cudaHostAlloc((void**)&e->h_stage, sizeof(uint64_t) * e->n_pad * 2, cudaHostAllocDefault));
+    memset(e->h_stage, 0, sizeof(uint64_t) * e->n_pad * 2);
+    CK(cudaStreamCreateWithFlags(&e->xs, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) {
+      CK(cudaEventCreateWithFlags(&e->ev_copy[b], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&e->ev_use[b], cudaEventDisableTiming));
+    }
+  }
   if (t == CGX_XPORT_FIRST_NODE && n > 512)
     return fail(CGX_E_UNSUPPORTED, "FIRST_NODE transport: more than 512 externals");
   if (t == CGX_XPORT_ROOT_PARAMS) {
@@ -741,8 +773,17 @@ static int setup_table(cgx_exec* e) {
 
 static int capture_graph(cgx_exec* e, int gi) {
   cudaStream_t cs = e->cs;
-  CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
   const cgx_transport t = eff_transport(e->o);
+  if (e->o.mode == CGX_MODE_GRAPH_INDIRECT && t == CGX_XPORT_H2D_PINGPONG) {
+    // graph gi reads table gi: the `table` field is the first member of ElemArgs and LnArgs
+    uint64_t* tab = gi == 0 ? e->d_table : e->d_table2;
+    for (auto& l : e->L)
+      if (l.kind == LK_KERNEL && (e->c->nodes[l.node].op <= CGX_OP_REDUCE_SUM ||
+                                  e->c->nodes[l.node].op == CGX_OP_SCALE_T ||
+                                  e->c->nodes[l.node].op == CGX_OP_LAYERNORM))
+        memcpy(l.args.p, &tab, sizeof(tab));
+  }
+  CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
   bool after_root = false;
   bool root_is_copy = false;
   if (e->o.mode == CGX_MODE_GRAPH_INDIRECT) {
@@ -771,7 +812,7 @@ static int capture_graph(cgx_exec* e, int gi) {
         const Node& n = e->c->nodes[l.node];
         const uint32_t f = kFlagTableAfterWait | kFlagTriggerAfterWait;
         if (n.op == CGX_OP_LAYERNORM) argp<LnArgs>(l)->flags |= f;
-        else if (n.op <= CGX_OP_REDUCE_SUM) argp<ElemArgs>(l)->flags |= f;
+        else if (n.op <= CGX_OP_REDUCE_SUM || n.op == CGX_OP_SCALE_T) argp<ElemArgs>(l)->flags |= f;
         else return fail(CGX_E_UNSUPPORTED, "first node after the root table writer must be elementwise/LN");
       }
       if (root_is_copy) l.pdl = false;
@@ -796,9 +837,17 @@ static void exec_free(cgx_exec* e) {
   }
   if (e->cs) cudaStreamDestroy(e->cs);
   if (e->ph_arena) cudaFree(e->ph_arena);
+  if (e->gemm_ws) cudaFree(e->gemm_ws);
+  if (e->gemm_cnt) cudaFree(e->gemm_cnt);
   if (e->d_desc) cudaFree(e->d_desc);
   if (e->d_chunk) cudaFree(e->d_chunk);
   if (e->d_table) cudaFree(e->d_table);
+  if (e->d_table2) cudaFree(e->d_table2);
+  if (e->xs) cudaStreamDestroy(e->xs);
+  for (int b = 0; b < 2; ++b) {
+    if (e->ev_copy[b]) cudaEventDestroy(e->ev_copy[b]);
+    if (e->ev_use[b]) cudaEventDestroy(e->ev_use[b]);
+  }
   if (e->h_stage) cudaFreeHost(e->h_stage);
   if (e->h_ack) cudaFreeHost((void*)e->h_ack);
   if (e->d_seq) cudaFree(e->d_seq);
@@ -812,7 +861,7 @@ extern "C" int cgx_exec_create_ex(cgx_chain* c, const cgx_exec_opts* opts, void*
   cgx_exec_opts o{};
   if (opts) o = *opts;
   if (o.mode < CGX_MODE_EAGER || o.mode > CGX_MODE_GRAPH_STALE) return fail(CGX_E_INVALID_ARG, "exec_create: mode");
-  if (o.transport < CGX_XPORT_DEFAULT || o.transport > CGX_XPORT_FIRST_NODE)
+  if (o.transport < CGX_XPORT_DEFAULT || o.transport > CGX_XPORT_H2D_PINGPONG)
     return fail(CGX_E_INVALID_ARG, "exec_create: transport");
   if (o.copy_impl < 0 || o.copy_impl > 2) return fail(CGX_E_INVALID_ARG, "exec_create: copy_impl");
   const int K = (int)c->nodes.size();
@@ -840,25 +889,31 @@ extern "C" int cgx_exec_create_ex(cgx_chain* c, const cgx_exec_opts* opts, void*
   int st;
   if (o.mode == CGX_MODE_GRAPH_COPY && (st = setup_copy(e)) != CGX_OK) return bail(st);
   if (o.mode == CGX_MODE_GRAPH_INDIRECT && (st = setup_table(e)) != CGX_OK) return bail(st);
+  {
+    size_t ws = 0, cnt = 0;
+    for (int k = first; k <= last; ++k)
+      if (c->nodes[k].op == CGX_OP_GEMM_BF16) {
+        size_t w1, c1;
+        decoder_gemm_plan(c->nodes[k].attr.M, c->nodes[k].attr.N, c->nodes[k].attr.K, &w1, &c1);
+        ws = std::max(ws, w1);
+        cnt = std::max(cnt, c1);
+      }
+    cudaError_t ce = cudaSuccess;
+    if (ws) ce = cudaMalloc(&e->gemm_ws, ws);
+    if (ce == cudaSuccess && cnt) ce = cudaMalloc(&e->gemm_cnt, cnt);
+    if (ce == cudaSuccess && cnt) ce = cudaMemset(e->gemm_cnt, 0, cnt);
+    if (ce != cudaSuccess) return bail(cuda_fail(ce, "gemm workspace", __LINE__));
+  }
   e->L.resize(last - first + 1);
   for (int k = first; k <= last; ++k)
     if ((st = build_launch(e, k, e->L[k - first])) != CGX_OK) return bail(st);
   set_prewait_masks(e);
-  if (o.mode == CGX_MODE_GRAPH_INDIRECT && eff_transport(o) == CGX_XPORT_FIRST_NODE && e->L.size() > 1) {
-    // second launch: by-value pointers, triggers its dependents only after its wait (so every later
-    // node starts after the first node -- the table writer -- has completed)
-    Launch& l2 = e->L[1];
-    const Node& n2 = c->nodes[l2.node];
-    if (l2.kind != LK_KERNEL) return bail(fail(CGX_E_UNSUPPORTED, "FIRST_NODE transport: second node is a collective"));
-    if (n2.op <= CGX_OP_REDUCE_SUM) argp<ElemArgs>(l2)->flags |= kFlagTriggerAfterWait;
-    else if (n2.op == CGX_OP_LAYERNORM) argp<LnArgs>(l2)->flags |= kFlagTriggerAfterWait;
-    else if (n2.op == CGX_OP_ATTN_CAUSAL) argp<AttnArgs>(l2)->flags |= kFlagTriggerAfterWait;
-    else if (n2.op == CGX_OP_GEMM_BF16) decoder_gemm_set_trigger_after_wait(l2.args.p);
-  }
   if (o.mode != CGX_MODE_EAGER) {
     cudaError_t ce = cudaStreamCreateWithFlags(&e->cs, cudaStreamNonBlocking);
     if (ce != cudaSuccess) return bail(cuda_fail(ce, "cudaStreamCreate", __LINE__));
-    e->n_graphs = (o.mode == CGX_MODE_GRAPH_INDIRECT && eff_transport(o) == CGX_XPORT_ROOT_MEMCPY) ? 2 : 1;
+    e->n_graphs = (o.mode == CGX_MODE_GRAPH_INDIRECT && (eff_transport(o) == CGX_XPORT_ROOT_MEMCPY ||
+                                                          eff_transport(o) == CGX_XPORT_H2D_PINGPONG))
+                      ? 2 : 1;
     for (int gi = 0; gi < e->n_graphs; ++gi)
       if ((st = capture_graph(e, gi)) != CGX_OK) {
         cudaStreamCaptureStatus cst;
@@ -1014,9 +1069,8 @@ extern "C" int cgx_bind(cgx_exec* e, const void* const* ext, int n_ext) {
         patch_images(e);   // by-value operands of the first two launches
         Launch& l0 = e->L[0];
         memcpy(l0.args.p + l0.tw_ptr_off, ext, sizeof(uint64_t) * N);
-        for (size_t i = 0; i < e->L.size() && i < 2; ++i) {
+        for (size_t i = 0; i < e->L.size() && i < 1; ++i) {
           Launch& l = e->L[i];
-          if (i == 1 && l.ext.empty()) continue;
           cudaKernelNodeParams kp{};
           kp.func = const_cast<void*>(l.func);
           kp.gridDim = l.grid;
@@ -1037,6 +1091,16 @@ extern "C" int cgx_bind(cgx_exec* e, const void* const* ext, int n_ext) {
         void* argv[1] = {e->root_args.p};
         kp.kernelParams = argv;
         CK(cudaGraphExecKernelNodeSetParams(e->ge[0], e->root_node[0], &kp));
+      } else if (t == CGX_XPORT_H2D_PINGPONG) {
+        const int b = (int)(e->seq % 2);
+        if (e->ev_copy_set[b]) CK(cudaEventSynchronize(e->ev_copy[b]));   // staging b free again
+        uint64_t* h = e->h_stage + (size_t)b * e->n_pad;
+        memcpy(h, ext, sizeof(uint64_t) * N);
+        if (e->ev_use_set[b]) CK(cudaStreamWaitEvent(e->xs, e->ev_use[b], 0));   // replay k-2 done
+        CK(cudaMemcpyAsync(b == 0 ? e->d_table : e->d_table2, h, sizeof(uint64_t) * N, cudaMemcpyHostToDevice,
+                           e->xs));
+        CK(cudaEventRecord(e->ev_copy[b], e->xs));
+        e->ev_copy_set[b] = true;
       } else if (t == CGX_XPORT_H2D) {
         const int slot = (int)(e->seq % e->ring);
         if (e->ev_used[slot]) CK(cudaEventSynchronize(e->ev[slot]));
@@ -1078,7 +1142,9 @@ extern "C" int cgx_launch(cgx_exec* e) {
   } else {
     int gi = 0;
     const bool pingpong = e->o.mode == CGX_MODE_GRAPH_INDIRECT && eff_transport(e->o) == CGX_XPORT_ROOT_MEMCPY;
-    if (pingpong) gi = (int)((e->seq - 1) % 2);
+    const bool t6 = e->o.mode == CGX_MODE_GRAPH_INDIRECT && eff_transport(e->o) == CGX_XPORT_H2D_PINGPONG;
+    if (pingpong || t6) gi = (int)((e->seq - 1) % 2);
+    if (t6) CK(cudaStreamWaitEvent(e->s, e->ev_copy[gi], 0));
     if (e->o.mode == CGX_MODE_GRAPH_INDIRECT && eff_transport(e->o) == CGX_XPORT_ROOT_MAPPED &&
         e->launched_since_bind) {
       // a launch without a fresh bind consumes the next ring slot: republish the bound pointers
@@ -1088,6 +1154,10 @@ extern "C" int cgx_launch(cgx_exec* e) {
     if (pingpong) {
       CK(cudaEventRecord(e->ev[gi], e->s));
       e->ev_used[gi] = true;
+    }
+    if (t6) {
+      CK(cudaEventRecord(e->ev_use[gi], e->s));
+      e->ev_use_set[gi] = true;
     }
   }
   e->st.n_launches++;
@@ -1119,7 +1189,10 @@ extern "C" int cgx_debug_read_table(const cgx_exec* e, uint64_t* host_out, int n
   if (!e->d_table) return fail(CGX_E_STATE, "read_table: exec has no pointer table (not INDIRECT)");
   if (n > (int)e->c->ext_slots.size()) return fail(CGX_E_INVALID_ARG, "read_table: n > N_ext");
   CK(cudaStreamSynchronize(e->s));
-  CK(cudaMemcpy(host_out, e->d_table, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost));
+  const uint64_t* tab = e->d_table;
+  if (e->d_table2 && e->seq > 0 && (e->seq - 1) % 2 == 1) tab = e->d_table2;   // T6: last bound slot
+  if (e->xs) CK(cudaStreamSynchronize(e->xs));
+  CK(cudaMemcpy(host_out, tab, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost));
   return CGX_OK;
 }
 

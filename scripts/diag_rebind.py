@@ -47,7 +47,7 @@ for cfg in sys.argv[1:] or ["C2", "C1"]:
     out = {}
     for name, mode, xp, nopdl in [("copy", "COPY", "DEFAULT", False), ("copy_nopdl", "COPY", "DEFAULT", True),
                                   ("t1", "INDIRECT", "H2D", False), ("t2", "INDIRECT", "ROOT_MEMCPY", False),
-                                  ("t3", "INDIRECT", "ROOT_PARAMS", False), ("t4", "INDIRECT", "ROOT_MAPPED", False), ("t5", "INDIRECT", "FIRST_NODE", False),
+                                  ("t3", "INDIRECT", "ROOT_PARAMS", False), ("t4", "INDIRECT", "ROOT_MAPPED", False), ("t5", "INDIRECT", "FIRST_NODE", False), ("t6", "INDIRECT", "H2D_PINGPONG", False),
                                   ("t3_nopdl", "INDIRECT", "ROOT_PARAMS", True), ("setparams", "SETPARAMS", "DEFAULT", False),
                                   ("eager", "EAGER", "DEFAULT", False)]:
         ex = chain.exec(mode, stream=stream, transport=xp, no_pdl=nopdl)

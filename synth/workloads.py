@@ -18,7 +18,7 @@ from . import splitmix as sm
 
 EXTERNAL, STATIC, INTERNAL = "external", "static", "internal"
 OPS = ("ADD", "MUL", "SCALE_IMM", "COPY", "REDUCE_SUM", "LAYERNORM", "GEMM_BF16",
-       "ATTN_CAUSAL", "ALLREDUCE_SUM")
+       "ATTN_CAUSAL", "ALLREDUCE_SUM", "SCALE_T")
 
 
 @dataclass(frozen=True)

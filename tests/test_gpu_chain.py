@@ -18,7 +18,7 @@ from synth.workloads import ChainSpec, NodeSpec, SlotSpec  # noqa: E402
 
 ARMS = [("EAGER", "DEFAULT"), ("COPY", "DEFAULT"), ("SETPARAMS", "DEFAULT"),
         ("INDIRECT", "H2D"), ("INDIRECT", "ROOT_MEMCPY"), ("INDIRECT", "ROOT_PARAMS"),
-        ("INDIRECT", "ROOT_MAPPED"), ("INDIRECT", "FIRST_NODE")]
+        ("INDIRECT", "ROOT_MAPPED"), ("INDIRECT", "FIRST_NODE"), ("INDIRECT", "H2D_PINGPONG")]
 
 
 @pytest.fixture(scope="module")
@@ -336,3 +336,83 @@ def test_kernel_times_and_graph_floor(rt):
     f1, f200 = cgx.graph_floor(sh, 1, True, 50), cgx.graph_floor(sh, 200, True, 20)
     assert 0 < f1 < f200 < 10000
     chain.close()
+
+
+@pytest.mark.parametrize("transport", ["FIRST_NODE", "ROOT_PARAMS", "H2D", "ROOT_MAPPED", "H2D_PINGPONG",
+                                       "ROOT_MEMCPY"])
+def test_indirect_stress_rotating_inputs(rt, transport):
+    """Back-to-back replays (no host sync in between) rotating 3 resident input sets: every
+    replay must read ITS table (a stale or half-published table would mix sets)."""
+    cgx, runner = rt
+    dev = torch.device("cuda:0")
+    for spec, reps in ((wl.c1_chain(), 300), (wl.c2_chain(n_lanes=26), 60)):
+        st = wl.static_values(spec)
+        chain = runner.Chain(spec, runner.upload_statics(spec, st, dev))
+        ex = chain.exec("INDIRECT", transport=transport)
+        sets = [runner.upload_externals(spec, wl.external_values(spec, r), dev) for r in range(3)]
+        finals = [s.name for s in spec.internals() if not any(s.name in n.ins for n in spec.nodes)]
+        ref = [eval_chain(spec, wl.external_values(spec, r), st) for r in range(3)]
+        snap = {}
+        for i in range(reps):
+            ex.bind(sets[i % 3])
+            ex.launch()
+            if i % 7 == 0 or i >= reps - 3:                 # copy finals out without syncing the host
+                for nm in finals:
+                    p, nb = cgx.output(ex.handle, chain.slot[nm])
+                    buf = torch.empty(nb, dtype=torch.uint8, device=dev)
+                    cgx.copy(buf.data_ptr(), p, nb, torch.cuda.current_stream().cuda_stream)
+                    snap.setdefault(i, {})[nm] = buf
+        torch.cuda.synchronize()
+        for i, d in snap.items():
+            for nm, buf in d.items():
+                got = buf.cpu().numpy().view(np.float32)
+                o = ref[i % 3][nm]
+                prod = [n for n in spec.nodes if n.out == nm][0]
+                if prod.op == "REDUCE_SUM" or (prod.op == "SCALE_IMM" and nm.startswith("s")):
+                    assert np.allclose(got, o, rtol=1e-5, atol=1e-3), (transport, i, nm)
+                else:
+                    assert np.array_equal(got, o), (transport, i, nm)
+        chain.close()
+
+
+def test_scalar_staleness_and_cgct_rewrite(rt):
+    """NEXT-3 (S:L554 criterion 1): a by-value scalar captured in a
+    graph goes stale when the application changes it; rewritten as a 1-element device tensor
+    slot (SCALE_T) bound per replay, the graph tracks the new value bit-exactly."""
+    cgx, runner = rt
+    dev = torch.device("cuda:0")
+    n = 4096
+    temps = [8.0, 0.125, 3.0, -2.5]
+    # naive: the scalar is a by-value node attribute, frozen at capture
+    naive = ChainSpec("naive", [SlotSpec("q", "external", "f32", n), SlotSpec("o", "internal", "f32", n)],
+                      [NodeSpec("SCALE_IMM", ("q",), "o", {"n": n, "scalar": temps[0]})], [(0, 0)])
+    chain = runner.Chain(naive, {})
+    ex = chain.exec("INDIRECT")
+    stale = False
+    for r, tmp in enumerate(temps):
+        vals = wl.external_values(naive, r)
+        t = runner.upload_externals(naive, vals, dev)
+        ex.bind(t)
+        ex.launch()
+        eager_ref = vals["q"] * np.float32(tmp)            # what the program means at replay r
+        stale |= not np.array_equal(ex.output("o"), eager_ref)
+    assert stale                                            # witness: replays used the old scalar
+    chain.close()
+    # CGCT rewrite: the scalar becomes an EXTERNAL 1-element slot, rebound like any input
+    fixed = ChainSpec("cgct", [SlotSpec("q", "external", "f32", n), SlotSpec("s", "external", "f32", 1),
+                               SlotSpec("o", "internal", "f32", n)],
+                      [NodeSpec("SCALE_T", ("q", "s"), "o", {"n": n})], [(0, 0)])
+    for mode, xp in (("INDIRECT", "FIRST_NODE"), ("INDIRECT", "ROOT_PARAMS"), ("COPY", "DEFAULT"),
+                     ("SETPARAMS", "DEFAULT"), ("EAGER", "DEFAULT")):
+        chain = runner.Chain(fixed, {})
+        ex = chain.exec(mode, transport=xp)
+        keep = []
+        for r, tmp in enumerate(temps * 3):
+            vals = wl.external_values(fixed, r)
+            vals["s"] = np.array([tmp], np.float32)
+            t = runner.upload_externals(fixed, vals, dev)
+            keep.append(t)
+            ex.bind(t)
+            ex.launch()
+            assert np.array_equal(ex.output("o"), eval_chain(fixed, vals, {})["o"]), (mode, r)
+        chain.close()

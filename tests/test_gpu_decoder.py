@@ -163,6 +163,7 @@ def test_c3_decoder_chain(rt, n_layers):
     for mode in ("EAGER", "COPY", "INDIRECT", "SETPARAMS"):
         res[mode] = _run(rt, spec, mode, 2, st)
     res["FIRST_NODE"] = _run(rt, spec, "INDIRECT", 2, st, transport="FIRST_NODE")
+    res["H2D_PINGPONG"] = _run(rt, spec, "INDIRECT", 2, st, transport="H2D_PINGPONG")
     for r in range(2):
         ext = wl.external_values(spec, r)
         got = res["INDIRECT"][r]
@@ -172,7 +173,7 @@ def test_c3_decoder_chain(rt, n_layers):
         g = bits_to_f64(got[last])
         o = env[last]
         assert np.linalg.norm(g - o) / np.linalg.norm(o) <= 2e-2
-        for mode in ("EAGER", "COPY", "SETPARAMS", "FIRST_NODE"):      # bit-identical across arms
+        for mode in ("EAGER", "COPY", "SETPARAMS", "FIRST_NODE", "H2D_PINGPONG"):   # bit-identical across arms
             for k in got:
                 assert np.array_equal(res[mode][r][k], got[k]), (mode, k)
 

@@ -192,3 +192,12 @@ def test_allreduce_integer_partials():
     parts = [_ints(20 + r, 64) for r in range(4)]
     out = ops.allreduce_sum(parts)
     assert np.array_equal(out, parts[0] + parts[1] + parts[2] + parts[3])
+
+
+def test_scale_t_is_scale_imm_with_a_device_scalar():
+    # S:L122 worked example through the CGCT scalar-as-tensor form
+    out = ops.scale_t(np.array([2, 4], np.float32), np.array([3.0], np.float32), {})
+    assert out.tolist() == [6.0, 12.0]
+    a = sm.uniform_f32(sm.SEED, 30, 1000)
+    assert np.array_equal(ops.scale_t(a, np.array([0.75], np.float32), {}),
+                          ops.scale_imm(a, {"scalar": 0.75}))
