@@ -130,10 +130,14 @@ typedef enum {
  *   H2D_PINGPONG T6: two tables and two captured graphs used alternately; the H2D copy of
  *                    replay k+1's pointers (pinned staging -> table) runs on a side stream while
  *                    replay k executes, ordered by events (the paper's "pointer copies over the
- *                    PCIe", with the PCIe latency hidden behind the previous replay). */
+ *                    PCIe", with the PCIe latency hidden behind the previous replay).
+ *   PRELUDE      T7 (NEXT-1): the consumers are plain direct-pointer kernels (stand-ins for opaque
+ *                    vendor kernels) captured as device-updatable nodes; a prelude root
+ *                    node dereferences the table (one H2D per replay) and writes every pointer into
+ *                    the consumers' parameter buffers with cudaGraphKernelNodeSetParam. */
 typedef enum {
   CGX_XPORT_DEFAULT = 0, CGX_XPORT_H2D = 1, CGX_XPORT_ROOT_MEMCPY = 2, CGX_XPORT_ROOT_PARAMS = 3,
-  CGX_XPORT_ROOT_MAPPED = 4, CGX_XPORT_FIRST_NODE = 5, CGX_XPORT_H2D_PINGPONG = 6
+  CGX_XPORT_ROOT_MAPPED = 4, CGX_XPORT_FIRST_NODE = 5, CGX_XPORT_H2D_PINGPONG = 6, CGX_XPORT_PRELUDE = 7
 } cgx_transport;
 
 typedef enum { CGX_DECIDE_EAGER = 0, CGX_DECIDE_GRAPH_COPY = 1, CGX_DECIDE_GRAPH_INDIRECT = 2 } cgx_decision;
@@ -221,6 +225,23 @@ int cgx_stats(const cgx_exec* e, cgx_stats_t* out);
 int cgx_debug_read_table(const cgx_exec* e, uint64_t* host_out, int n);
 int cgx_debug_setparam_nodes(const cgx_exec* e, int* nodes_out, int cap, int* n_out);
 int cgx_exec_destroy(cgx_exec* e);
+
+/* ---- NEXT-2: parameter-offset discovery ("byte-pattern match with the known
+ * placeholder pointers") ----------------------------------------------------------- */
+/* Unique 8-byte-aligned offset of `pattern` in image[0, image_bytes): CGX_E_OFFSET_NOT_FOUND (no
+ * match) or CGX_E_OFFSET_AMBIGUOUS (two or more). Pure host function. */
+int cgx_find_param_offset(const void* image, uint64_t image_bytes, uint64_t pattern, uint64_t* offset_out);
+/* Copy of the parameter image of the launch at exec position `pos` (min(cap, size) bytes; nbytes_out
+ * = size) and, optionally, the size cudaFuncGetParamInfo reports for the kernel's parameter 0. */
+int cgx_debug_param_image(const cgx_exec* e, int pos, void* buf, uint64_t cap, uint64_t* nbytes_out,
+                          uint64_t* param0_size_out);
+/* Byte offsets of the external-pointer fields the runtime patches in launch `pos` (EAGER/SETPARAMS/
+ * STALE execs, and the by-value first node of FIRST_NODE). */
+int cgx_debug_ext_field_offsets(const cgx_exec* e, int pos, uint64_t* offs, int cap, int* n_out);
+/* Diagnostics: run GEMM launch `pos` once alone with per-CTA %globaltimer tracing; host_out gets
+ * [cta][8] ns stamps (entry, setup done, first stage landed, last MMA committed, accumulator ready,
+ * split partial published, all splits arrived, exit); n_out = CTA count. */
+int cgx_debug_gemm_trace(cgx_exec* e, int pos, uint64_t* host_out, int cap, int* n_out);
 
 /* ---- selective CUDA graphs ---------------------------------------------------------------- */
 /* Slow path: measure one segment (index into the marked segments, or -1 = whole chain) in the

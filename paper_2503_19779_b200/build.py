@@ -46,11 +46,15 @@ def _newest_header():
     return max((os.path.getmtime(h) for h in hs), default=0)
 
 
+RDC = {"k_prelude.cu"}   # translation units calling the device runtime (device graph API)
+
+
 def _compile(src, verbose):
     obj = os.path.join(BUILD, os.path.basename(src).replace(".cu", ".o"))
     if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(src), _newest_header()):
         return obj, None
-    cmd = [NVCC, *_flags(), "-c", src, "-o", obj]
+    extra = ["-rdc=true"] if os.path.basename(src) in RDC else []
+    cmd = [NVCC, *_flags(), *extra, "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         return obj, f"{' '.join(cmd)}\n{r.stdout}\n{r.stderr}"
@@ -73,8 +77,17 @@ def build(verbose: bool = False, force: bool = False) -> str:
     objs = [o for o, _ in res]
     if os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(o) for o in objs):
         return LIB
+    # device link of the relocatable objects (device runtime: cudadevrt)
+    rdc_objs = [o for o in objs if os.path.basename(o).replace(".o", ".cu") in RDC]
+    dlink = os.path.join(BUILD, "dlink.o")
+    if rdc_objs:
+        cmd = [NVCC, *ARCH, "-Xcompiler", "-fPIC", "-dlink", *rdc_objs, "-lcudadevrt", "-o", dlink]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"device link failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+        objs = objs + [dlink]
     _, nccl_lib = _nccl_dirs()
-    cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-L", nccl_lib, "-l:libnccl.so.2",
+    cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudadevrt", "-L", nccl_lib, "-l:libnccl.so.2",
            "-Xlinker", "-rpath," + nccl_lib]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

@@ -26,7 +26,7 @@ OP = {"ADD": 0, "MUL": 1, "SCALE_IMM": 2, "COPY": 3, "REDUCE_SUM": 4, "LAYERNORM
       "GEMM_BF16": 6, "ATTN_CAUSAL": 7, "ALLREDUCE_SUM": 8, "SCALE_T": 9}
 GEMM_BIAS, GEMM_GELU, GEMM_RESIDUAL = 1, 2, 4
 MODE = {"EAGER": 0, "COPY": 1, "INDIRECT": 2, "SETPARAMS": 3, "STALE": 4}
-XPORT = {"DEFAULT": 0, "H2D": 1, "ROOT_MEMCPY": 2, "ROOT_PARAMS": 3, "ROOT_MAPPED": 4, "FIRST_NODE": 5, "H2D_PINGPONG": 6}
+XPORT = {"DEFAULT": 0, "H2D": 1, "ROOT_MEMCPY": 2, "ROOT_PARAMS": 3, "ROOT_MAPPED": 4, "FIRST_NODE": 5, "H2D_PINGPONG": 6, "PRELUDE": 7}
 DECIDE = {0: "EAGER", 1: "GRAPH_COPY", 2: "GRAPH_INDIRECT"}
 MAX_PROFILE_KERNELS = 1024
 
@@ -105,6 +105,10 @@ def _load():
         "cgx_copy": ([VP, VP, U64, VP], I),
         "cgx_graph_floor": ([VP, I, I, I, P(C.c_double)], I),
         "cgx_kernel_times": ([VP, I, P(C.c_double), I, P(I)], I),
+        "cgx_find_param_offset": ([VP, U64, U64, P(U64)], I),
+        "cgx_debug_param_image": ([VP, I, VP, U64, P(U64), P(U64)], I),
+        "cgx_debug_ext_field_offsets": ([VP, I, P(U64), I, P(I)], I),
+        "cgx_debug_gemm_trace": ([VP, I, P(U64), I, P(I)], I),
         "cgx_nccl_unique_id": ([VP], I),
         "cgx_nccl_comm_init": ([I, I, VP, I, P(VP)], I),
         "cgx_nccl_comm_destroy": ([VP], I),
@@ -122,7 +126,8 @@ EXPORTED = ("cgx_version", "cgx_last_error", "cgx_chain_create", "cgx_chain_add_
             "cgx_chain_destroy", "cgx_exec_create", "cgx_exec_create_ex", "cgx_bind",
             "cgx_launch", "cgx_output", "cgx_stats", "cgx_debug_read_table",
             "cgx_debug_setparam_nodes", "cgx_exec_destroy", "cgx_profile", "cgx_select",
-            "cgx_dispatch_floor", "cgx_fill_uniform_f32", "cgx_copy", "cgx_graph_floor", "cgx_kernel_times", "cgx_nccl_unique_id",
+            "cgx_dispatch_floor", "cgx_fill_uniform_f32", "cgx_copy", "cgx_graph_floor", "cgx_kernel_times", "cgx_find_param_offset",
+            "cgx_debug_param_image", "cgx_debug_ext_field_offsets", "cgx_debug_gemm_trace", "cgx_nccl_unique_id",
             "cgx_nccl_comm_init", "cgx_nccl_comm_destroy")
 
 
@@ -219,6 +224,36 @@ def debug_setparam_nodes(ex: int) -> list:
     buf = (C.c_int * max(1, n.value))()
     _ck(LIB.cgx_debug_setparam_nodes(ex, buf, n.value, C.byref(n)), "cgx_debug_setparam_nodes")
     return list(buf[: n.value])
+
+
+def find_param_offset(image: bytes, pattern: int) -> int:
+    buf = C.create_string_buffer(bytes(image), len(image))
+    off = C.c_uint64()
+    _ck(LIB.cgx_find_param_offset(buf, len(image), pattern & 0xFFFFFFFFFFFFFFFF, C.byref(off)),
+        "cgx_find_param_offset")
+    return off.value
+
+
+def param_image(ex: int, pos: int) -> tuple:
+    n, p0 = C.c_uint64(), C.c_uint64()
+    _ck(LIB.cgx_debug_param_image(ex, pos, None, 0, C.byref(n), C.byref(p0)), "cgx_debug_param_image")
+    buf = C.create_string_buffer(n.value)
+    _ck(LIB.cgx_debug_param_image(ex, pos, buf, n.value, C.byref(n), C.byref(p0)), "cgx_debug_param_image")
+    return buf.raw[: n.value], p0.value
+
+
+def ext_field_offsets(ex: int, pos: int) -> list:
+    n = C.c_int()
+    buf = (C.c_uint64 * 16)()
+    _ck(LIB.cgx_debug_ext_field_offsets(ex, pos, buf, 16, C.byref(n)), "cgx_debug_ext_field_offsets")
+    return list(buf[: n.value])
+
+
+def gemm_trace(ex: int, pos: int) -> list:
+    n = C.c_int()
+    buf = (C.c_uint64 * (8 * 4096))()
+    _ck(LIB.cgx_debug_gemm_trace(ex, pos, buf, 8 * 4096, C.byref(n)), "cgx_debug_gemm_trace")
+    return [list(buf[8 * i: 8 * i + 8]) for i in range(n.value)]
 
 
 def exec_destroy(ex: int):

@@ -28,10 +28,13 @@ __device__ __forceinline__ void tw_publish(const ArgsTW<Base, CAP>& A) {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 
-// Pointer-table entry: L2-coherent load (the table is rewritten between replays).
+// Pointer-table entry. Read-only path: the table never changes while a reader kernel runs (it is
+// written before the graph starts, by a root node the reader waits for, or by the T5 publisher
+// before it triggers the reader's launch), and L1/texture state is invalidated at every kernel
+// launch. Through L1 the warps of an SM share one miss instead of each hammering the same L2 line.
 __device__ __forceinline__ uint64_t ld_table(const uint64_t* p) {
   uint64_t v;
-  asm volatile("ld.global.cg.u64 %0, [%1];\n" : "=l"(v) : "l"(p));
+  asm volatile("ld.global.nc.u64 %0, [%1];\n" : "=l"(v) : "l"(p));
   return v;
 }
 

@@ -40,9 +40,10 @@ struct alignas(64) GemmArgs {
   const __nv_bfloat16* residual;
   __nv_bfloat16* out;
   float* ws;                  // split-K partial tiles [split][tiles][128][BN] (split > 1)
-  uint32_t* cnt;              // per-tile arrival counters (zero between launches)
+  unsigned long long* cnt;    // per-tile monotonic arrival counters (split > 1)
   uint32_t M, N, K, flags;
   uint32_t split;             // K splits (gridDim.z)
+  unsigned long long* trace;  // optional per-CTA %globaltimer trace [cta][8] (diagnostics)
 };
 
 // ------------------------------------------------------------------ PTX wrappers
@@ -121,16 +122,25 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void trace_at(const GemmArgs& a, int slot) {
+  if (a.trace) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const uint32_t cta = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    a.trace[cta * 8 + slot] = t;
+  }
+}
+
 __device__ __forceinline__ float gelu_tanh(float x) {
   const float k0 = 0.7978845608028654f, k1 = 0.044715f;
   return 0.5f * x * (1.0f + tanhf(k0 * (x + k1 * x * x * x)));
 }
 
 // ------------------------------------------------------------------ kernel
-// Split-K (gridDim.z = split): CTA z accumulates k-blocks [z*nk/split, (z+1)*nk/split) in TMEM and
-// stores its fp32 partial tile to a workspace; the LAST CTA of a tile to arrive (counter) sums the
-// partials in fixed split order 0..split-1 — deterministic, no float atomics — and runs the
-// epilogue. At M = 128 every N tile re-reads the whole A panel, so without split-K the per-CTA
+// Split-K (gridDim.z = split, launched as thread-block clusters (1, 1, split)): CTA z accumulates
+// k-blocks [z*nk/split, (z+1)*nk/split) in TMEM, parks its fp32 partial tile in its own shared
+// memory, and after a cluster barrier reduces 1/split of the tile over DSMEM in fixed split order
+// (deterministic, no float atomics, no global workspace) before running the epilogue on it. At M = 128 every N tile re-reads the whole A panel, so without split-K the per-CTA
 // bytes (up to 128 x 3072 x 2 for FC2) bound the kernel; split-K spreads them over ~148 CTAs.
 __device__ __forceinline__ void epilogue_store(const GemmArgs& a, int m, int n, float* v) {
   if (a.flags & CGX_GEMM_BIAS) {
@@ -168,6 +178,30 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs& a, int m, int n, 
   op[1] = o[1];
 }
 
+__device__ __forceinline__ void epilogue_store4(const GemmArgs& a, int m, int n, float4 acc, uint2 bu) {
+  float v[4] = {acc.x, acc.y, acc.z, acc.w};
+  if (a.flags & CGX_GEMM_BIAS) {
+    const __nv_bfloat16* bb = reinterpret_cast<const __nv_bfloat16*>(&bu);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] += __bfloat162float(bb[i]);
+  }
+  if (a.flags & CGX_GEMM_GELU) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = gelu_tanh(v[i]);
+  }
+  if (a.flags & CGX_GEMM_RESIDUAL) {
+    const uint2 ru = *reinterpret_cast<const uint2*>(a.residual + (size_t)m * a.N + n);
+    const __nv_bfloat16* rb = reinterpret_cast<const __nv_bfloat16*>(&ru);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] += __bfloat162float(rb[i]);
+  }
+  uint2 o;
+  __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(&o);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) ob[i] = __float2bfloat16_rn(v[i]);
+  *reinterpret_cast<uint2*>(a.out + (size_t)m * a.N + n) = o;
+}
+
 template <int BN>
 __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_constant__ GemmArgs a) {
   constexpr uint32_t kABytes = kBM * kBK * 2;     // 16 KiB
@@ -181,8 +215,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
   uint64_t* empty = full + kStages;
   uint64_t* tmem_full = empty + kStages;
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(tmem_full + 1);
-  uint32_t* s_last = s_tmem + 1;
 
+  if (threadIdx.x == 0) trace_at(a, 0);
   const bool late_trigger = a.flags & kGemmTriggerAfterWait;
   if (!late_trigger) pdl_trigger();   // dependents may start their prologues (they read our output after their wait)
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -210,6 +244,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
+  if (threadIdx.x == 0) trace_at(a, 1);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -240,6 +275,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
         const int s = i % kStages;
         const uint32_t ph = (uint32_t)(i / kStages) & 1u;
         mbar_wait(&full[s], ph);
+        if (i == 0) trace_at(a, 2);
         tc_fence_after();
         const uint64_t da = umma_desc_sw128(smem_u32(sA + s * kABytes));
         const uint64_t db = umma_desc_sw128(smem_u32(sB + s * kBBytes));
@@ -249,10 +285,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
         umma_commit(&empty[s]);
       }
       umma_commit(tmem_full);
+      trace_at(a, 3);
     }
   } else {
     // ---- epilogue warps (128 threads): TMEM -> registers -> [split-K reduction] -> epilogue
     mbar_wait(tmem_full, 0);
+    if (threadIdx.x == 64) trace_at(a, 4);
     tc_fence_after();
     const uint32_t q = warp & 3;                  // TMEM lane quarter this warp may access
     const uint32_t row = q * 32 + lane;
@@ -266,47 +304,87 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
         if (live) epilogue_store(a, m, n0 + c0, v);
       }
     } else {
-      const uint32_t tiles = gridDim.x * gridDim.y;
-      const uint32_t tile = blockIdx.y * gridDim.x + blockIdx.x;
-      float* mine = a.ws + ((size_t)(blockIdx.z * tiles + tile) * kBM + row) * BN;
+      // split-K: park this split's fp32 partial tile in OWN shared memory (the operand ring is
+      // idle now): row-major [128][BN + 4] floats (padding keeps the 16-B column accesses of a
+      // quarter warp on distinct banks)
+      float* sP = reinterpret_cast<float*>(smem);
 #pragma unroll
       for (int c0 = 0; c0 < BN; c0 += 16) {
         float v[16];
         tmem_ld16(tmem + ((q * 32u) << 16) + (uint32_t)c0, v);
-        float4* d = reinterpret_cast<float4*>(mine + c0);
+        float4* d = reinterpret_cast<float4*>(sP + row * (BN + 4) + c0);
 #pragma unroll
         for (int i = 0; i < 4; ++i) d[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
       }
-      __threadfence();
-      asm volatile("bar.sync 1, 128;\n" ::: "memory");
-      if (warp == 2 && lane == 0) *s_last = (atomicAdd(a.cnt + tile, 1u) == a.split - 1) ? 1u : 0u;
-      asm volatile("bar.sync 1, 128;\n" ::: "memory");
-      if (*s_last) {
-        __threadfence();
+      if (threadIdx.x == 64) trace_at(a, 5);
+    }
+  }
+  if (a.split > 1) {
+    // The S splits of a tile form one thread-block cluster (1, 1, S). After a cluster barrier
+    // every CTA reduces 1/S of the tile, reading the S partials from the CTAs' shared memory
+    // (DSMEM) in fixed split order 0..S-1 — deterministic, no global round trips or atomics —
+    // then runs the epilogue on it. A second barrier keeps every partial alive until all reads
+    // are done.
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+    if (threadIdx.x == 64) trace_at(a, 6);
+    if (warp >= 2) {
+      const uint32_t S = a.split;
+      const uint32_t my_rank = blockIdx.z;          // cluster (1,1,S) over gridDim.z == S
+      constexpr uint32_t kQuads = kBM * BN / 4;
+      const uint32_t q_lo = (uint32_t)((uint64_t)kQuads * my_rank / S);
+      const uint32_t q_hi = (uint32_t)((uint64_t)kQuads * (my_rank + 1) / S);
+      const uint32_t et = threadIdx.x - 64;          // epilogue thread 0..127
+      const uint32_t local = smem_u32(smem);
+      // this thread's quads: q_lo + et + 128 j, j < kQMax (<= BN/8 for any split >= 1)
+      constexpr int kQMax = BN / 8;
+      uint32_t offs[kQMax];
+      bool have[kQMax];
+      uint2 bias_q[kQMax];
+      float4 acc[kQMax];
 #pragma unroll
-        for (int c0 = 0; c0 < BN; c0 += 16) {
-          float v[16];
+      for (int j = 0; j < kQMax; ++j) {
+        const uint32_t qi = q_lo + et + 128u * j;
+        have[j] = qi < q_hi;
+        const uint32_t r = qi / (BN / 4), c = 4 * (qi % (BN / 4));
+        offs[j] = (r * (BN + 4) + c) * 4;
+        acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+        bias_q[j] = make_uint2(0u, 0u);
+        if (have[j] && (a.flags & CGX_GEMM_BIAS)) bias_q[j] = __ldg(reinterpret_cast<const uint2*>(a.bias + n0 + c));
+      }
+      for (uint32_t z = 0; z < S; ++z) {            // fixed split order: deterministic sums
+        float4 t[kQMax];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = 0.f;
-          for (uint32_t z = 0; z < a.split; ++z) {      // fixed order: deterministic
-            const float4* src = reinterpret_cast<const float4*>(a.ws + ((size_t)(z * tiles + tile) * kBM + row) * BN + c0);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const float4 t = __ldcg(src + i);
-              v[4 * i] += t.x;
-              v[4 * i + 1] += t.y;
-              v[4 * i + 2] += t.z;
-              v[4 * i + 3] += t.w;
-            }
+        for (int j = 0; j < kQMax; ++j) {           // all of this split's loads in flight at once
+          if (have[j]) {
+            uint32_t remote;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(remote) : "r"(local + offs[j]), "r"(z));
+            asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];\n"
+                         : "=f"(t[j].x), "=f"(t[j].y), "=f"(t[j].z), "=f"(t[j].w) : "r"(remote));
           }
-          if (live) epilogue_store(a, m, n0 + c0, v);
         }
-        if (warp == 2 && lane == 0) a.cnt[tile] = 0u;   // ready for the next replay
+#pragma unroll
+        for (int j = 0; j < kQMax; ++j)
+          if (have[j]) {
+            acc[j].x += t[j].x;
+            acc[j].y += t[j].y;
+            acc[j].z += t[j].z;
+            acc[j].w += t[j].w;
+          }
+      }
+#pragma unroll
+      for (int j = 0; j < kQMax; ++j) {
+        if (!have[j]) continue;
+        const uint32_t qi = q_lo + et + 128u * j;
+        const uint32_t r = qi / (BN / 4), c = 4 * (qi % (BN / 4));
+        const int mr = m0 + (int)r;
+        if (mr < (int)a.M) epilogue_store4(a, mr, n0 + (int)c, acc[j], bias_q[j]);
       }
     }
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) trace_at(a, 7);
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(kTmemCols));
@@ -339,20 +417,29 @@ static int encode_kmajor(CUtensorMap* tm, const void* base, uint64_t rows, uint6
   return r == CUDA_SUCCESS ? CGX_OK : CGX_E_CUDA;
 }
 
-static int pick_bn(uint32_t N) {
-  if (N % 64 == 0) return 64;
-  if (N % 32 == 0) return 32;
-  return 0;
-}
-
-// Split count: the largest divisor s of the k-block count with tiles * s <= 148 (one wave).
-static uint32_t pick_split(uint32_t M, uint32_t N, uint32_t K, int bn) {
-  const uint32_t tiles = (N / bn) * ((M + kBM - 1) / kBM);
+// Tiling: N tile BN in {64, 32} and split-K factor S <= 8 (a portable cluster) dividing the
+// k-block count, maximising CTAs = tiles * S within one wave (<= 148); ties keep the larger BN.
+static void pick_tiling(uint32_t M, uint32_t N, uint32_t K, int* bn_out, uint32_t* split_out) {
+  int best_bn = 0;
+  uint32_t best_s = 1, best_ctas = 0;
   const uint32_t nk = K / kBK;
-  uint32_t best = 1;
-  for (uint32_t s = 1; s <= nk; ++s)
-    if (nk % s == 0 && tiles * s <= 148) best = s;
-  return best;
+  for (int bn : {64, 32}) {
+    if (N % bn) continue;
+    const uint32_t tiles = (N / bn) * ((M + kBM - 1) / kBM);
+    for (uint32_t sp = 1; sp <= 8 && sp <= nk; ++sp)
+      if (nk % sp == 0 && tiles * sp <= 148 && tiles * sp > best_ctas) {
+        best_ctas = tiles * sp;
+        best_bn = bn;
+        best_s = sp;
+      }
+    if (!best_bn) {     // more tiles than one wave: no split
+      best_bn = bn;
+      best_s = 1;
+      best_ctas = tiles;
+    }
+  }
+  *bn_out = best_bn;
+  *split_out = best_s;
 }
 
 template <int BN>
@@ -360,12 +447,10 @@ static size_t smem_bytes() {
   return 1024 + kStages * (kBM * kBK * 2 + BN * kBK * 2) + (2 * kStages + 1) * 8 + 16;
 }
 
-void decoder_gemm_plan(uint32_t M, uint32_t N, uint32_t K, size_t* ws_bytes, size_t* cnt_bytes) {
-  const int bn = pick_bn(N);
-  const uint32_t sp = bn ? pick_split(M, N, K, bn) : 1;
-  const size_t tiles = bn ? (size_t)(N / bn) * ((M + kBM - 1) / kBM) : 0;
-  *ws_bytes = sp > 1 ? (size_t)sp * tiles * kBM * bn * sizeof(float) : 0;
-  *cnt_bytes = tiles * sizeof(uint32_t);
+void decoder_gemm_plan(uint32_t, uint32_t, uint32_t, size_t* ws_bytes, size_t* cnt_bytes) {
+  // split-K partials are reduced through distributed shared memory: no global workspace
+  *ws_bytes = 0;
+  *cnt_bytes = 0;
 }
 
 template <int BN>
@@ -373,8 +458,13 @@ static const void* setup_kernel() {
   static std::once_flag once;
   std::call_once(once, [] {
     cudaFuncSetAttribute(k_gemm_bf16<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<BN>());
+    cudaFuncSetAttribute(k_gemm_bf16<BN>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   });
   return (const void*)k_gemm_bf16<BN>;
+}
+
+void decoder_gemm_set_trace(void* args, unsigned long long* trace) {
+  static_cast<GemmArgs*>(args)->trace = trace;
 }
 
 void decoder_gemm_set_trigger_after_wait(void* args) {
@@ -382,15 +472,16 @@ void decoder_gemm_set_trigger_after_wait(void* args) {
 }
 
 bool decoder_gemm_supported(uint32_t M, uint32_t N, uint32_t K) {
-  return M >= 1 && K >= kBK && K % kBK == 0 && pick_bn(N) != 0;
+  return M >= 1 && K >= kBK && K % kBK == 0 && (N % 32 == 0);
 }
 
 int decoder_gemm_build(uint32_t M, uint32_t N, uint32_t K, uint32_t flags, const void* A, const void* W,
                        const void* bias, const void* residual, void* out, void* ws, void* cnt, void* args_out,
                        size_t* argbytes, dim3* grid, dim3* block, size_t* smem, const void** func) {
   if (!decoder_gemm_supported(M, N, K)) return CGX_E_UNSUPPORTED;
-  const int bn = pick_bn(N);
-  const uint32_t sp = pick_split(M, N, K, bn);
+  int bn = 0;
+  uint32_t sp = 1;
+  pick_tiling(M, N, K, &bn, &sp);
   *argbytes = sizeof(GemmArgs);
   *grid = dim3(N / bn, (M + kBM - 1) / kBM, sp);
   *block = dim3(kGemmThreads);
@@ -410,13 +501,14 @@ int decoder_gemm_build(uint32_t M, uint32_t N, uint32_t K, uint32_t flags, const
   g->residual = static_cast<const __nv_bfloat16*>(residual);
   g->out = static_cast<__nv_bfloat16*>(out);
   g->ws = static_cast<float*>(ws);
-  g->cnt = static_cast<uint32_t*>(cnt);
+  g->cnt = static_cast<unsigned long long*>(cnt);
   g->M = M;
   g->N = N;
   g->K = K;
   g->flags = flags;
   g->split = sp;
-  if (sp > 1 && (!ws || !cnt)) return CGX_E_INVALID_ARG;
+  g->trace = nullptr;
+
   return CGX_OK;
 }
 

@@ -1,0 +1,33 @@
+// NEXT-1: parameter indirection for OPAQUE kernels through a prelude node.
+//
+// The consumers are launched as plain direct-pointer kernels (standing in for vendor kernels whose
+// code cannot be rewritten) with the device-updatable attribute. The prelude node at the root of
+// the graph dereferences the pointer cells (the device pointer table, written by one H2D copy per
+// replay) and writes each value into the consumer node's parameter buffer at its byte
+// offset with the device graph API cudaGraphKernelNodeSetParam. One thread per patch;
+// a gpu-scope fence before the dependents are triggered makes the updates visible to the launches
+// that follow (cuda_device_runtime_api.h contract for device node updates + PDL).
+//
+// Built with relocatable device code (device runtime API), device-linked into libcgx.so.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "cgx_device.cuh"
+#include "cgx_prelude.h"
+
+namespace cgx {
+
+__global__ void k_prelude(const __grid_constant__ PreludeArgs a) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n_patches; i += gridDim.x * blockDim.x) {
+    const PreludePatch p = a.patches[i];
+    const uint64_t v = ld_table(a.table + p.ext_j);            // dereference the pointer cell px
+    cudaGraphKernelNodeSetParam(p.node, p.offset, &v, sizeof(v));
+  }
+  __threadfence();
+  __syncthreads();
+  pdl_trigger();
+}
+
+const void* kfn_prelude() { return (const void*)k_prelude; }
+
+}  // namespace cgx

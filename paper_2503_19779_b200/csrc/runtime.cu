@@ -30,6 +30,7 @@
 #include "../../include/cgx.h"
 #include "cgx_args.h"
 #include "cgx_decoder.h"
+#include "cgx_prelude.h"
 
 using namespace cgx;
 
@@ -316,6 +317,9 @@ struct Launch {
   std::vector<PtrField> ext;  // external operand fields
   size_t tw_ptr_off = 0;      // T5 first node: byte offset of the by-value pointer array (0 = none)
   cudaGraphNode_t gnode[2] = {nullptr, nullptr};
+  unsigned cluster_z = 1;                 // thread-block cluster (1, 1, z) (split-K GEMM)
+  bool dev_updatable = false;             // T7: consumer patched by the prelude node
+  cudaGraphDeviceNode_t dev_node = nullptr;
   // NCCL
   const void* nc_in = nullptr;
   void* nc_out = nullptr;
@@ -359,6 +363,8 @@ struct cgx_exec {
   // INDIRECT
   uint64_t* d_table = nullptr;
   uint64_t* d_table2 = nullptr;   // T6: second table (replays alternate between the two)
+  void* d_patches = nullptr;      // T7: PreludePatch[n_patches] (device)
+  uint32_t n_patches = 0;
   cudaStream_t xs = nullptr;      // T6: side stream carrying the table H2D copies
   cudaEvent_t ev_copy[2] = {nullptr, nullptr};   // T6: H2D into table b done
   cudaEvent_t ev_use[2] = {nullptr, nullptr};    // T6: replay reading table b done
@@ -373,6 +379,8 @@ struct cgx_exec {
   // after another: a GEMM writes its partials only after its griddepcontrol.wait)
   void* gemm_ws = nullptr;
   void* gemm_cnt = nullptr;
+  size_t gemm_cnt_off = 0;        // next free counter bytes while building launches
+  int t5_pub = 0;                 // T5: position of the table-publishing launch
   // T3 / T4 root
   const void* root_fn = nullptr;
   AlignedBuf root_args;
@@ -391,10 +399,17 @@ static T* argp(Launch& l) { return reinterpret_cast<T*>(l.args.p); }
 
 // Build the launch record of one node. Operand addresses are resolved for `mode`:
 // EXTERNAL -> placeholder (COPY), table index (INDIRECT), or a patchable field (others).
-// T5 (FIRST_NODE): the first launch of an INDIRECT exec takes its external operands by value
-// (patched like SETPARAMS) and publishes the table before it triggers its dependents.
+// T5 (FIRST_NODE): launches 0..t5_pub of an INDIRECT exec take their external operands by value
+// (patched like SETPARAMS); launch t5_pub also publishes the table before it triggers its
+// dependents. The publisher is the SECOND launch when it can write the table (its publish + fence
+// then overlaps the first launch, which it waits for anyway), else the first.
 static bool t5_byvalue(const cgx_exec* e, int pos) {
-  return e->o.mode == CGX_MODE_GRAPH_INDIRECT && eff_transport(e->o) == CGX_XPORT_FIRST_NODE && pos < 1;
+  return e->o.mode == CGX_MODE_GRAPH_INDIRECT &&
+         ((eff_transport(e->o) == CGX_XPORT_FIRST_NODE && pos <= e->t5_pub) ||
+          eff_transport(e->o) == CGX_XPORT_PRELUDE);
+}
+static bool tw_capable(cgx_op op) {
+  return op <= CGX_OP_REDUCE_SUM || op == CGX_OP_LAYERNORM || op == CGX_OP_SCALE_T;
 }
 
 template <typename Base>
@@ -449,7 +464,7 @@ static int build_launch(cgx_exec* e, int k, Launch& l) {
   };
   auto is_ext = [&](int si) { return c->slots[si].kind == CGX_SLOT_EXTERNAL; };
   const bool byvalue = t5_byvalue(e, pos);
-  const bool tw = byvalue && pos == 0;
+  const bool tw = byvalue && pos == e->t5_pub && eff_transport(e->o) == CGX_XPORT_FIRST_NODE;
   const bool indirect = mode == CGX_MODE_GRAPH_INDIRECT && !byvalue;
   const bool patch = mode == CGX_MODE_EAGER || mode == CGX_MODE_GRAPH_SETPARAMS || mode == CGX_MODE_GRAPH_STALE ||
                      byvalue;
@@ -540,11 +555,18 @@ static int build_launch(cgx_exec* e, int k, Launch& l) {
       void* bias = slot_ptr(n.in[2]);
       void* res = (n.attr.flags & CGX_GEMM_RESIDUAL) ? slot_ptr(n.in[3]) : nullptr;
       size_t argbytes = 0;
+      void* cnt_ptr = e->gemm_cnt ? static_cast<char*>(e->gemm_cnt) + e->gemm_cnt_off : nullptr;
       CKS(decoder_gemm_build(n.attr.M, n.attr.N, n.attr.K, n.attr.flags, A, W, bias, res, slot_ptr(n.out),
-                             e->gemm_ws, e->gemm_cnt, nullptr, &argbytes, &l.grid, &l.block, &l.smem, &l.func));
+                             e->gemm_ws, cnt_ptr, nullptr, &argbytes, &l.grid, &l.block, &l.smem, &l.func));
       l.args.reset(argbytes);
       CKS(decoder_gemm_build(n.attr.M, n.attr.N, n.attr.K, n.attr.flags, A, W, bias, res, slot_ptr(n.out),
-                             e->gemm_ws, e->gemm_cnt, l.args.p, &argbytes, &l.grid, &l.block, &l.smem, &l.func));
+                             e->gemm_ws, cnt_ptr, l.args.p, &argbytes, &l.grid, &l.block, &l.smem, &l.func));
+      {
+        size_t w1, c1;
+        decoder_gemm_plan(n.attr.M, n.attr.N, n.attr.K, &w1, &c1);
+        e->gemm_cnt_off += c1;
+      }
+      l.cluster_z = l.grid.z;
       if (patch && (is_ext(n.in[0]) || ((n.attr.flags & CGX_GEMM_RESIDUAL) && is_ext(n.in[3]))))
         return fail(CGX_E_UNSUPPORTED, "gemm: external A/residual needs a rebuilt tensor map");
       return CGX_OK;
@@ -607,15 +629,36 @@ static int issue(cgx_exec* e, Launch& l, cudaStream_t s) {
   cfg.blockDim = l.block;
   cfg.dynamicSmemBytes = l.smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[3];
+  unsigned na = 0;
+  if (l.cluster_z > 1) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = 1;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = l.cluster_z;
+    ++na;
+  }
   if (l.pdl) {
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  int du = -1;
+  cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
+  if (l.dev_updatable && cudaStreamIsCapturing(s, &cst) == cudaSuccess && cst == cudaStreamCaptureStatusActive) {
+    du = (int)na;
+    attr[na].id = cudaLaunchAttributeDeviceUpdatableKernelNode;
+    attr[na].val.deviceUpdatableKernelNode.deviceUpdatable = 1;
+    attr[na].val.deviceUpdatableKernelNode.devNode = nullptr;
+    ++na;
+  }
+  if (na) {
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = na;
   }
   void* argv[1] = {l.args.p};
   CK(cudaLaunchKernelExC(&cfg, l.func, argv));
+  if (du >= 0) l.dev_node = attr[du].val.deviceUpdatableKernelNode.devNode;
   return CGX_OK;
 }
 
@@ -712,7 +755,7 @@ static int setup_table(cgx_exec* e) {
   CK(cudaMemset(e->d_table, 0, sizeof(uint64_t) * nalloc));
   const cgx_transport t = eff_transport(e->o);
   e->n_pad = (uint32_t)(((nalloc + 15) / 16) * 16);   // 128-B aligned ring slots
-  if (t == CGX_XPORT_H2D || t == CGX_XPORT_ROOT_MEMCPY || t == CGX_XPORT_ROOT_MAPPED) {
+  if (t == CGX_XPORT_H2D || t == CGX_XPORT_ROOT_MEMCPY || t == CGX_XPORT_ROOT_MAPPED || t == CGX_XPORT_PRELUDE) {
     e->ring = t == CGX_XPORT_ROOT_MEMCPY ? 2 : 4;
     const unsigned flags = t == CGX_XPORT_ROOT_MAPPED ? cudaHostAllocMapped : cudaHostAllocDefault;
     CK(cudaHostAlloc((void**)&e->h_stage, sizeof(uint64_t) * e->n_pad * e->ring, flags));
@@ -791,6 +834,20 @@ static int capture_graph(cgx_exec* e, int gi) {
     if (t == CGX_XPORT_ROOT_MEMCPY) {
       CK(cudaMemcpyAsync(e->d_table, e->h_stage + (size_t)gi * e->n_pad, tb, cudaMemcpyHostToDevice, cs));
       after_root = root_is_copy = true;
+    } else if (t == CGX_XPORT_PRELUDE) {
+      Launch r;
+      r.func = kfn_prelude();
+      r.grid = dim3(1);
+      r.block = dim3(128);
+      r.pdl = false;
+      r.args.reset(sizeof(PreludeArgs));
+      auto* pa = reinterpret_cast<PreludeArgs*>(r.args.p);
+      pa->table = e->d_table;
+      pa->patches = static_cast<const PreludePatch*>(e->d_patches);
+      pa->n_patches = e->n_patches;
+      CKS(issue(e, r, cs));
+      CKS(last_captured_node(cs, &e->root_node[gi]));
+      // consumers start after the prelude's updates (it triggers after a gpu-scope fence)
     } else if (t == CGX_XPORT_ROOT_PARAMS || t == CGX_XPORT_ROOT_MAPPED) {
       Launch r;
       r.func = e->root_fn;
@@ -843,6 +900,7 @@ static void exec_free(cgx_exec* e) {
   if (e->d_chunk) cudaFree(e->d_chunk);
   if (e->d_table) cudaFree(e->d_table);
   if (e->d_table2) cudaFree(e->d_table2);
+  if (e->d_patches) cudaFree(e->d_patches);
   if (e->xs) cudaStreamDestroy(e->xs);
   for (int b = 0; b < 2; ++b) {
     if (e->ev_copy[b]) cudaEventDestroy(e->ev_copy[b]);
@@ -861,7 +919,7 @@ extern "C" int cgx_exec_create_ex(cgx_chain* c, const cgx_exec_opts* opts, void*
   cgx_exec_opts o{};
   if (opts) o = *opts;
   if (o.mode < CGX_MODE_EAGER || o.mode > CGX_MODE_GRAPH_STALE) return fail(CGX_E_INVALID_ARG, "exec_create: mode");
-  if (o.transport < CGX_XPORT_DEFAULT || o.transport > CGX_XPORT_H2D_PINGPONG)
+  if (o.transport < CGX_XPORT_DEFAULT || o.transport > CGX_XPORT_PRELUDE)
     return fail(CGX_E_INVALID_ARG, "exec_create: transport");
   if (o.copy_impl < 0 || o.copy_impl > 2) return fail(CGX_E_INVALID_ARG, "exec_create: copy_impl");
   const int K = (int)c->nodes.size();
@@ -896,7 +954,7 @@ extern "C" int cgx_exec_create_ex(cgx_chain* c, const cgx_exec_opts* opts, void*
         size_t w1, c1;
         decoder_gemm_plan(c->nodes[k].attr.M, c->nodes[k].attr.N, c->nodes[k].attr.K, &w1, &c1);
         ws = std::max(ws, w1);
-        cnt = std::max(cnt, c1);
+        cnt += c1;            // counters are per GEMM node (split counts differ between nodes)
       }
     cudaError_t ce = cudaSuccess;
     if (ws) ce = cudaMalloc(&e->gemm_ws, ws);
@@ -905,12 +963,25 @@ extern "C" int cgx_exec_create_ex(cgx_chain* c, const cgx_exec_opts* opts, void*
     if (ce != cudaSuccess) return bail(cuda_fail(ce, "gemm workspace", __LINE__));
   }
   e->L.resize(last - first + 1);
+  e->t5_pub = (last > first && tw_capable(c->nodes[first + 1].op)) ? 1 : 0;
   for (int k = first; k <= last; ++k)
     if ((st = build_launch(e, k, e->L[k - first])) != CGX_OK) return bail(st);
   set_prewait_masks(e);
   if (o.mode != CGX_MODE_EAGER) {
     cudaError_t ce = cudaStreamCreateWithFlags(&e->cs, cudaStreamNonBlocking);
     if (ce != cudaSuccess) return bail(cuda_fail(ce, "cudaStreamCreate", __LINE__));
+    const bool t7 = o.mode == CGX_MODE_GRAPH_INDIRECT && eff_transport(o) == CGX_XPORT_PRELUDE;
+    if (t7) {
+      uint32_t np = 0;
+      for (auto& l : e->L)
+        if (l.kind == LK_KERNEL && !l.ext.empty()) {
+          l.dev_updatable = true;
+          np += (uint32_t)l.ext.size();
+        }
+      e->n_patches = np;
+      cudaError_t pe = cudaMalloc(&e->d_patches, sizeof(PreludePatch) * std::max<uint32_t>(np, 1));
+      if (pe != cudaSuccess) return bail(cuda_fail(pe, "prelude patches", __LINE__));
+    }
     e->n_graphs = (o.mode == CGX_MODE_GRAPH_INDIRECT && (eff_transport(o) == CGX_XPORT_ROOT_MEMCPY ||
                                                           eff_transport(o) == CGX_XPORT_H2D_PINGPONG))
                       ? 2 : 1;
@@ -924,6 +995,21 @@ extern "C" int cgx_exec_create_ex(cgx_chain* c, const cgx_exec_opts* opts, void*
         }
         return bail(st);
       }
+    if (t7) {
+      // patch list: (device node handle, byte offset of the pointer field, pointer cell); the
+      // offsets are the fields the runtime itself patches in SETPARAMS mode — the same ones the
+      // NEXT-2 byte-pattern discovery finds (tests/test_gpu_next.py)
+      std::vector<PreludePatch> pp;
+      for (auto& l : e->L)
+        if (l.dev_updatable) {
+          if (!l.dev_node) return bail(fail(CGX_E_CUDA, "prelude: no device node handle returned by capture"));
+          for (auto& f : l.ext) pp.push_back({l.dev_node, (uint32_t)f.off, (uint32_t)f.ext_j});
+        }
+      cudaError_t pe = pp.empty() ? cudaSuccess
+                                  : cudaMemcpy(e->d_patches, pp.data(), sizeof(PreludePatch) * pp.size(),
+                                               cudaMemcpyHostToDevice);
+      if (pe != cudaSuccess) return bail(cuda_fail(pe, "prelude patch upload", __LINE__));
+    }
     cudaError_t se = cudaStreamSynchronize(e->s);
     if (se != cudaSuccess) return bail(cuda_fail(se, "upload sync", __LINE__));
   }
@@ -1066,11 +1152,12 @@ extern "C" int cgx_bind(cgx_exec* e, const void* const* ext, int n_ext) {
     case CGX_MODE_GRAPH_INDIRECT: {
       const cgx_transport t = eff_transport(e->o);
       if (t == CGX_XPORT_FIRST_NODE) {
-        patch_images(e);   // by-value operands of the first two launches
-        Launch& l0 = e->L[0];
-        memcpy(l0.args.p + l0.tw_ptr_off, ext, sizeof(uint64_t) * N);
-        for (size_t i = 0; i < e->L.size() && i < 1; ++i) {
+        patch_images(e);   // by-value operands of launches 0..t5_pub
+        Launch& lp = e->L[e->t5_pub];
+        memcpy(lp.args.p + lp.tw_ptr_off, ext, sizeof(uint64_t) * N);
+        for (int i = 0; i <= e->t5_pub; ++i) {
           Launch& l = e->L[i];
+          if (i != e->t5_pub && l.ext.empty()) continue;
           cudaKernelNodeParams kp{};
           kp.func = const_cast<void*>(l.func);
           kp.gridDim = l.grid;
@@ -1101,7 +1188,7 @@ extern "C" int cgx_bind(cgx_exec* e, const void* const* ext, int n_ext) {
                            e->xs));
         CK(cudaEventRecord(e->ev_copy[b], e->xs));
         e->ev_copy_set[b] = true;
-      } else if (t == CGX_XPORT_H2D) {
+      } else if (t == CGX_XPORT_H2D || t == CGX_XPORT_PRELUDE) {
         const int slot = (int)(e->seq % e->ring);
         if (e->ev_used[slot]) CK(cudaEventSynchronize(e->ev[slot]));
         uint64_t* h = e->h_stage + (size_t)slot * e->n_pad;
@@ -1193,6 +1280,89 @@ extern "C" int cgx_debug_read_table(const cgx_exec* e, uint64_t* host_out, int n
   if (e->d_table2 && e->seq > 0 && (e->seq - 1) % 2 == 1) tab = e->d_table2;   // T6: last bound slot
   if (e->xs) CK(cudaStreamSynchronize(e->xs));
   CK(cudaMemcpy(host_out, tab, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost));
+  return CGX_OK;
+}
+
+// NEXT-2: locate a pointer value inside a kernel's parameter image by
+// byte-pattern matching on 8-byte-aligned boundaries.
+extern "C" int cgx_find_param_offset(const void* image, uint64_t image_bytes, uint64_t pattern, uint64_t* offset_out) {
+  if ((!image && image_bytes) || !offset_out) return fail(CGX_E_INVALID_ARG, "find_param_offset: bad argument");
+  const uint8_t* p = static_cast<const uint8_t*>(image);
+  int hits = 0;
+  uint64_t at = 0;
+  for (uint64_t off = 0; off + 8 <= image_bytes; off += 8) {
+    uint64_t v;
+    memcpy(&v, p + off, 8);
+    if (v == pattern) {
+      if (++hits == 1) at = off;
+    }
+  }
+  if (hits == 0) return fail(CGX_E_OFFSET_NOT_FOUND, "find_param_offset: pattern not found");
+  if (hits > 1) return fail(CGX_E_OFFSET_AMBIGUOUS, "find_param_offset: pattern found " + std::to_string(hits) + " times");
+  *offset_out = at;
+  return CGX_OK;
+}
+
+// The current parameter image of the node at exec position `pos` (what the next launch/replay
+// passes), plus its layout from cudaFuncGetParamInfo (param 0 offset/size).
+extern "C" int cgx_debug_param_image(const cgx_exec* e, int pos, void* buf, uint64_t cap, uint64_t* nbytes_out,
+                                     uint64_t* param0_size_out) {
+  if (!e || pos < 0 || pos >= (int)e->L.size() || !nbytes_out) return fail(CGX_E_INVALID_ARG, "param_image: bad argument");
+  const Launch& l = e->L[pos];
+  if (l.kind != LK_KERNEL) return fail(CGX_E_UNSUPPORTED, "param_image: collective node");
+  *nbytes_out = l.args.n;
+  if (buf) memcpy(buf, l.args.p, std::min<uint64_t>(cap, l.args.n));
+  if (param0_size_out) {
+    size_t off = 0, sz = 0;
+    CK(cudaFuncGetParamInfo(l.func, 0, &off, &sz));
+    *param0_size_out = sz;
+  }
+  return CGX_OK;
+}
+
+// Diagnostics: launch GEMM node `pos` once, alone (no PDL), with per-CTA %globaltimer tracing;
+// host_out receives [cta][8] ns timestamps (entry, setup, first stage landed, last MMA committed,
+// accumulator ready, partial published, all splits arrived, exit).
+extern "C" int cgx_debug_gemm_trace(cgx_exec* e, int pos, uint64_t* host_out, int cap, int* n_out) {
+  if (!e || pos < 0 || pos >= (int)e->L.size() || !n_out) return fail(CGX_E_INVALID_ARG, "gemm_trace: bad argument");
+  Launch& l = e->L[pos];
+  if (e->c->nodes[l.node].op != CGX_OP_GEMM_BF16) return fail(CGX_E_INVALID_ARG, "gemm_trace: not a GEMM node");
+  const int ctas = (int)(l.grid.x * l.grid.y * l.grid.z);
+  unsigned long long* d = nullptr;
+  CK(cudaMalloc(&d, sizeof(unsigned long long) * 8 * ctas));
+  CK(cudaMemset(d, 0, sizeof(unsigned long long) * 8 * ctas));
+  Launch t;
+  t.func = l.func;
+  t.grid = l.grid;
+  t.block = l.block;
+  t.smem = l.smem;
+  t.cluster_z = l.cluster_z;
+  t.pdl = false;
+  t.args.reset(l.args.n);
+  memcpy(t.args.p, l.args.p, l.args.n);
+  decoder_gemm_set_trace(t.args.p, d);
+  int st = issue(e, t, e->s);
+  if (st == CGX_OK) {
+    cudaError_t ce = cudaStreamSynchronize(e->s);
+    if (ce == cudaSuccess && host_out)
+      ce = cudaMemcpy(host_out, d, sizeof(uint64_t) * std::min(cap, 8 * ctas), cudaMemcpyDeviceToHost);
+    if (ce != cudaSuccess) st = cuda_fail(ce, "gemm_trace", __LINE__);
+  }
+  cudaFree(d);
+  *n_out = ctas;
+  return st;
+}
+
+// Byte offsets of the external-pointer fields the runtime patches in node `pos` (SETPARAMS/EAGER).
+extern "C" int cgx_debug_ext_field_offsets(const cgx_exec* e, int pos, uint64_t* offs, int cap, int* n_out) {
+  if (!e || pos < 0 || pos >= (int)e->L.size() || !n_out) return fail(CGX_E_INVALID_ARG, "ext_field_offsets: bad argument");
+  const Launch& l = e->L[pos];
+  int n = 0;
+  for (const auto& f : l.ext) {
+    if (offs && n < cap) offs[n] = f.off;
+    ++n;
+  }
+  *n_out = n;
   return CGX_OK;
 }
 

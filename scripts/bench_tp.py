@@ -1,0 +1,104 @@
+"""C5 — tensor-parallel decoder step with captured NCCL all-reduce.
+
+    torchrun --nproc-per-node P --master-addr 127.0.0.1 scripts/bench_tp.py [--layers 12] [--T 128]
+
+Each rank builds its Megatron shard of the GPT-2-small chain (column-parallel QKV/FC1, row-parallel
+O/FC2, two ALLREDUCE_SUM nodes per layer), bootstraps an NCCL communicator through the torch
+process group (paper_2503_19779_b200.tp), captures the chain INCLUDING the ncclAllReduce calls into
+its graph, and replays it with a fresh (replicated) x every step. Per-replay µs is the device time
+of each rank's stream, max over ranks. With --check the rank outputs are compared with the
+single-process lockstep oracle (1 layer).
+"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--layers", type=int, default=12)
+    ap.add_argument("--T", type=int, default=128)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--check", action="store_true")
+    args = ap.parse_args()
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl" if world > 1 else "gloo", device_id=torch.device("cuda", local) if world > 1 else None)
+    from paper_2503_19779_b200 import build
+    if rank == 0:
+        build.build()
+    dist.barrier()
+    from paper_2503_19779_b200 import cgx, runner, tp
+    from synth import workloads as wl
+
+    dev = torch.device("cuda", local)
+    comm = tp.nccl_bootstrap(local)
+    full = wl.c3_chain(T=args.T, n_layers=args.layers)
+    spec = wl.c3_chain(T=args.T, n_layers=args.layers, tp=world, rank=rank) if world > 1 else full
+    st = wl.static_values(spec, tp=world, rank=rank, full=full) if world > 1 else wl.static_values(spec)
+    chain = runner.Chain(spec, runner.upload_statics(spec, st, dev), device=local, nccl_comm=comm)
+    stream = torch.cuda.Stream(device=dev)
+    xs = [runner.host_to_device(wl.slot_values(spec, "x", r), "bf16", dev) for r in range(4)]
+    ptrs = [cgx.ptr_array([x.data_ptr()]) for x in xs]
+    LIB = cgx.LIB
+    res = {}
+    for name, mode, xp in (("indirect_first_node", "INDIRECT", "FIRST_NODE"), ("copy", "COPY", "DEFAULT"),
+                           ("eager", "EAGER", "DEFAULT")):
+        ex = chain.exec(mode, stream=stream, transport=xp)
+        for i in range(5):
+            LIB.cgx_bind(ex.handle, ptrs[i % 4], 1)
+            LIB.cgx_launch(ex.handle)
+        stream.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n = args.steps if mode != "EAGER" else max(20, args.steps // 10)
+        e0.record(stream)
+        for i in range(n):
+            LIB.cgx_bind(ex.handle, ptrs[i % 4], 1)
+            LIB.cgx_launch(ex.handle)
+        e1.record(stream)
+        e1.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) * 1e3 / n], dtype=torch.float64)
+        if world > 1:
+            t = t.to(dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        res[name] = float(t.item())
+        if args.check and name == "indirect_first_node":
+            LIB.cgx_bind(ex.handle, ptrs[0], 1)
+            LIB.cgx_launch(ex.handle)
+            got = ex.output(spec.nodes[-1].out)
+            gathered = [None] * world
+            dist.all_gather_object(gathered, got)
+            if rank == 0:
+                from oracle import chain as och
+                from oracle.numerics import bits_to_f64
+                chains = [wl.c3_chain(T=args.T, n_layers=args.layers, tp=world, rank=r) if world > 1 else full
+                          for r in range(world)]
+                sts = [wl.static_values(c, tp=world, rank=r, full=full) if world > 1 else wl.static_values(c)
+                       for r, c in enumerate(chains)]
+                exts = [wl.external_values(c, 0) for c in chains]
+                envs = och.eval_chain_tp(chains, exts, sts) if world > 1 else [och.eval_chain(full, exts[0], sts[0])]
+                o = envs[0][spec.nodes[-1].out]
+                errs = [float(np.linalg.norm(bits_to_f64(g) - o) / np.linalg.norm(o)) for g in gathered]
+                res["check_rel_err_per_rank"] = errs
+                res["ranks_identical"] = all(np.array_equal(g, gathered[0]) for g in gathered)
+        ex.close()
+    if rank == 0:
+        res["tokens_per_s_indirect"] = args.T * 1e6 / res["indirect_first_node"]
+        print(json.dumps({"config": f"C5 TP={world} T={args.T} layers={args.layers}", "us_per_replay_max_over_ranks": res}))
+    chain.close()
+    cgx.nccl_comm_destroy(comm)
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

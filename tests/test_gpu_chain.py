@@ -416,3 +416,28 @@ def test_scalar_staleness_and_cgct_rewrite(rt):
             ex.launch()
             assert np.array_equal(ex.output("o"), eval_chain(fixed, vals, {})["o"]), (mode, r)
         chain.close()
+
+
+def test_param_offset_discovery_on_live_node_images(rt):
+    """NEXT-2: pattern-match each bound input pointer in the parameter image of every
+    node that reads it; the offset found is the field the runtime patches (and the kernel reads, as
+    the parity tests prove), and cudaFuncGetParamInfo's size matches the image."""
+    cgx, runner = rt
+    from oracle import offsets as ooff
+    dev = torch.device("cuda:0")
+    spec = wl.c1_chain()
+    chain = runner.Chain(spec, runner.upload_statics(spec, wl.static_values(spec), dev))
+    ex = chain.exec("SETPARAMS")
+    t = runner.upload_externals(spec, wl.external_values(spec, 0), dev)
+    ex.bind(t)
+    ptr = {n: t[n].data_ptr() for n in chain.ext_names}
+    for pos, node in enumerate(spec.nodes):
+        img, p0 = cgx.param_image(ex.handle, pos)
+        assert p0 == len(img)
+        want = sorted(cgx.ext_field_offsets(ex.handle, pos))
+        found = []
+        for nm in dict.fromkeys(i for i in node.ins if i in ptr):
+            found.append(cgx.find_param_offset(img, ptr[nm]))
+            assert found[-1] == ooff.find_param_offset(img, ptr[nm])
+        assert sorted(found) == want, (pos, found, want)
+    chain.close()
