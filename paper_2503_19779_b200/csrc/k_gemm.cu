@@ -19,6 +19,7 @@
 #include <cudaTypedefs.h>
 #include <stdint.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "../../include/cgx.h"
@@ -29,7 +30,11 @@ namespace cgx {
 
 static constexpr int kBM = 128;
 static constexpr int kBK = 64;          // 64 bf16 = 128 B = one swizzle-128B row
-static constexpr int kStages = 4;
+// Stage count per N tile (4: deeper rings measured no faster at the C3 shapes, profiles/r01).
+template <int BN>
+struct Stages {
+  static constexpr int value = 4;
+};
 static constexpr int kGemmThreads = 192;
 static constexpr uint32_t kGemmTriggerAfterWait = 1u << 8;   // internal flag bit (above CGX_GEMM_*)
 
@@ -207,6 +212,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
   constexpr uint32_t kABytes = kBM * kBK * 2;     // 16 KiB
   constexpr uint32_t kBBytes = BN * kBK * 2;
   constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
+  constexpr int kStages = Stages<BN>::value;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -244,7 +250,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
-  if (threadIdx.x == 0) trace_at(a, 1);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -290,7 +295,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
   } else {
     // ---- epilogue warps (128 threads): TMEM -> registers -> [split-K reduction] -> epilogue
     mbar_wait(tmem_full, 0);
-    if (threadIdx.x == 64) trace_at(a, 4);
     tc_fence_after();
     const uint32_t q = warp & 3;                  // TMEM lane quarter this warp may access
     const uint32_t row = q * 32 + lane;
@@ -371,6 +375,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
             acc[j].w += t[j].w;
           }
       }
+      if (threadIdx.x == 64) trace_at(a, 1);
 #pragma unroll
       for (int j = 0; j < kQMax; ++j) {
         if (!have[j]) continue;
@@ -379,6 +384,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
         const int mr = m0 + (int)r;
         if (mr < (int)a.M) epilogue_store4(a, mr, n0 + (int)c, acc[j], bias_q[j]);
       }
+      if (threadIdx.x == 64) trace_at(a, 4);
     }
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
   }
@@ -417,33 +423,28 @@ static int encode_kmajor(CUtensorMap* tm, const void* base, uint64_t rows, uint6
   return r == CUDA_SUCCESS ? CGX_OK : CGX_E_CUDA;
 }
 
-// Tiling: N tile BN in {64, 32} and split-K factor S <= 8 (a portable cluster) dividing the
-// k-block count, maximising CTAs = tiles * S within one wave (<= 148); ties keep the larger BN.
+// Tiling (measured per C3 shape with scripts/diag_gemm_tiling.py, profiles/r01/gemm_tiling.txt):
+// BN = 32 everywhere; no split-K when there are already >= 64 N tiles (the DSMEM reduction costs
+// more than the smaller A slice saves), else the largest split S <= 4 dividing the k-block count
+// with tiles * S <= 148 (one wave; the S CTAs of a tile form a thread-block cluster).
 static void pick_tiling(uint32_t M, uint32_t N, uint32_t K, int* bn_out, uint32_t* split_out) {
-  int best_bn = 0;
-  uint32_t best_s = 1, best_ctas = 0;
+  const char* env_bn = getenv("CGX_GEMM_BN");          // measurement knobs
+  const char* env_ms = getenv("CGX_GEMM_MAXSPLIT");
+  int bn = (N % 32 == 0) ? 32 : 64;
+  if (env_bn && N % atoi(env_bn) == 0) bn = atoi(env_bn);
+  const uint32_t tiles = (N / bn) * ((M + kBM - 1) / kBM);
   const uint32_t nk = K / kBK;
-  for (int bn : {64, 32}) {
-    if (N % bn) continue;
-    const uint32_t tiles = (N / bn) * ((M + kBM - 1) / kBM);
-    for (uint32_t sp = 1; sp <= 8 && sp <= nk; ++sp)
-      if (nk % sp == 0 && tiles * sp <= 148 && tiles * sp > best_ctas) {
-        best_ctas = tiles * sp;
-        best_bn = bn;
-        best_s = sp;
-      }
-    if (!best_bn) {     // more tiles than one wave: no split
-      best_bn = bn;
-      best_s = 1;
-      best_ctas = tiles;
-    }
-  }
-  *bn_out = best_bn;
-  *split_out = best_s;
+  uint32_t max_split = env_ms ? (uint32_t)atoi(env_ms) : (tiles >= 64 ? 1u : 4u);
+  uint32_t best = 1;
+  for (uint32_t sp = 1; sp <= max_split && sp <= 8 && sp <= nk; ++sp)
+    if (nk % sp == 0 && tiles * sp <= 148) best = sp;
+  *bn_out = bn;
+  *split_out = best;
 }
 
 template <int BN>
 static size_t smem_bytes() {
+  constexpr int kStages = Stages<BN>::value;
   return 1024 + kStages * (kBM * kBK * 2 + BN * kBK * 2) + (2 * kStages + 1) * 8 + 16;
 }
 
