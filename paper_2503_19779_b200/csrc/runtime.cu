@@ -1203,7 +1203,12 @@ extern "C" int cgx_bind(cgx_exec* e, const void* const* ext, int n_ext) {
       } else {  // ROOT_MAPPED: replay number r reads ring slot r % ring
         if (!e->launched_since_bind) e->seq--;     // overwrite the not-yet-launched slot
         const uint64_t need = e->seq >= (uint64_t)e->ring ? e->seq - e->ring + 1 : 0;
-        while (*e->h_ack < need) { /* slot still owned by an in-flight replay */ }
+        if (*e->h_ack < need) {   // slot still owned by an in-flight replay: wait (bounded)
+          const double t_start = now_us();
+          while (*e->h_ack < need) {
+            if (now_us() - t_start > 10e6) return fail(CGX_E_CUDA, "bind: ROOT_MAPPED ring slot not released in 10 s");
+          }
+        }
         uint64_t* h = e->h_stage + (size_t)(e->seq % e->ring) * e->n_pad;
         volatile uint64_t* vh = h;
         for (int j = 0; j < N; ++j) vh[j] = reinterpret_cast<uint64_t>(ext[j]);
