@@ -36,7 +36,7 @@ METRIC = "per-replay rebinding µs and chain iters/s (graph+indirection vs copy 
 WORKLOAD = ("C2: 200-kernel fp32 elementwise/reduction chain, 64 external inputs of 1 KiB-4 MiB "
             "(37,743,616 B), batch-1 replay with fresh inputs every step")
 N_SETS = 8   # rotating input sets: 8 x 37.7 MB = 302 MB > 126 MB L2
-MAIN_TRANSPORT = "FIRST_NODE"   # INDIRECT pointer-table transport of the deployed arm
+MAIN_TRANSPORT = "H2D"   # INDIRECT pointer-table transport of the deployed arm (lowest Δ, r01 dataflow run)
 
 
 def parse():
@@ -321,12 +321,38 @@ def run_extras(args, torch, cgx, runner, wl, sm, spec, chain, stream, sets, set_
     LIB = cgx.LIB
 
     # ---------------- arms: per-replay device time and rebinding Δ
+    # Two bases. (1) "cold" (headline): N_SETS COPY execs, each holding one input set in its own
+    # placeholders, launched round-robin WITHOUT binding — a replay that reads as much L2-cold input
+    # as a rebinding replay does, with zero rebinding work. (2) "warm" (SURVEY §8(d) literal: same
+    # exec, same pointers): one exec relaunched on the same inputs, which stay in the 126 MB L2 —
+    # on B200 that base also credits the L2 residency of a repeated input, not only the rebinding.
     M = 2000
     arms = {}
     ex_copy = chain.exec("COPY", stream=stream)
     loop(ex_copy.handle, 20)
-    base = min(timed(ex_copy.handle, M, bind=False) for _ in range(3))   # graph, no rebinding
-    arms["graph_no_rebind"] = {"us_per_replay": base}
+    base_warm = min(timed(ex_copy.handle, M, bind=False) for _ in range(3))
+    cold = [chain.exec("COPY", stream=stream) for _ in range(N_SETS)]
+    for i, exc in enumerate(cold):
+        LIB.cgx_bind(exc.handle, set_ptrs[i], n_ext)
+        LIB.cgx_launch(exc.handle)
+    stream.synchronize()
+
+    def timed_rr(n):
+        e0_, e1_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        stream.synchronize()
+        with torch.cuda.stream(stream):
+            e0_.record(stream)
+            for i in range(n):
+                LIB.cgx_launch(cold[i % N_SETS].handle)
+            e1_.record(stream)
+        e1_.synchronize()
+        return e0_.elapsed_time(e1_) * 1e3 / n
+    timed_rr(50)
+    base = min(timed_rr(M) for _ in range(3))
+    for exc in cold:
+        exc.close()
+    arms["graph_no_rebind"] = {"us_per_replay": base, "base": f"cold: {N_SETS} COPY execs round-robin, no bind"}
+    arms["graph_no_rebind_warm"] = {"us_per_replay": base_warm, "base": "warm: same exec, same inputs"}
     for name, (mode, xp) in {"copy": ("COPY", "DEFAULT"), "indirect_h2d": ("INDIRECT", "H2D"),
                              "indirect_root_memcpy": ("INDIRECT", "ROOT_MEMCPY"),
                              "indirect_root_params": ("INDIRECT", "ROOT_PARAMS"),
@@ -347,9 +373,20 @@ def run_extras(args, torch, cgx, runner, wl, sm, spec, chain, stream, sets, set_
             host.append((time.perf_counter() - t0) * 1e6)
         stream.synchronize()
         arms[name] = {"us_per_replay": us, "rebind_delta_us": us - base,
+                      "rebind_delta_vs_warm_base_us": us - base_warm,
                       "host_bind_launch_us": statistics.median(host)}
         if ex is not ex_copy:
             ex.close()
+    # node synchronisation inside the replay: dataflow counters (deployed, AUTO) vs
+    # deferred PDL waits vs the plain PDL chain, same INDIRECT exec otherwise
+    sync_cmp = {}
+    for sm_ in ("AUTO", "DEFER", "CHAIN"):
+        ex = chain.exec("INDIRECT", stream=stream, transport=main_transport, sync=sm_)
+        loop(ex.handle, 20)
+        sync_cmp[sm_] = {"us_per_replay": min(timed(ex.handle, M) for _ in range(3)),
+                         "dataflow": ex.stats()["dataflow"], "n_deferred": ex.stats()["n_deferred"]}
+        ex.close()
+    out["sync_modes"] = sync_cmp
     ex_e = chain.exec("EAGER", stream=stream)
     loop(ex_e.handle, 3)
     us_e = min(timed(ex_e.handle, 100) for _ in range(3))
@@ -362,8 +399,11 @@ def run_extras(args, torch, cgx, runner, wl, sm, spec, chain, stream, sets, set_
     out["rebinding_us"] = {"copy": d_copy, "indirect": d_ind, "indirect_transport": best_ind,
                            "setparams": arms["setparams"]["rebind_delta_us"],
                            "copy_over_indirect": (d_copy / d_ind) if d_ind > 0 else None,
-                           "definition": "T_iter(bind+launch) - T_iter(graph launch, no rebinding), "
-                                         "device timeline, 2000 replays, best of 3"}
+                           "definition": "T_iter(bind+launch, fresh inputs from 8 rotating sets) - "
+                                         "T_iter(graph launch, no rebinding, equally L2-cold inputs), "
+                                         "device timeline, 2000 replays, best of 3 (DESIGN reading 14)",
+                           "vs_warm_base": {"copy": arms["copy"]["rebind_delta_vs_warm_base_us"],
+                                            "indirect": arms[best_ind]["rebind_delta_vs_warm_base_us"]}}
     g_floor, k_floor = cgx.dispatch_floor(sh, 2000)
     out["dispatch_floor"] = {"graph_launch_us": g_floor, "kernel_launch_us": k_floor,
                              "bind_launch_over_floor": arms[best_ind]["host_bind_launch_us"] / g_floor}

@@ -153,7 +153,14 @@ typedef struct {
                                1 = every bind, 2 = off (alignment and count are always checked) */
   int copy_impl;            /* GRAPH_COPY: 0 = multi-tensor LDG/STG kernel, 1 = cudaMemcpyAsync per
                                tensor, 2 = multi-tensor TMA bulk-copy kernel */
+  int sync_mode;            /* graph modes with PDL, how a node waits for its predecessors
+                               (DESIGN §5): CGX_SYNC_AUTO (0) = dataflow counters when every node
+                               supports them, else deferred waits; CGX_SYNC_DEFER (1) = deferred
+                               griddepcontrol.wait for nodes with no in-graph producer;
+                               CGX_SYNC_CHAIN (2) = griddepcontrol.wait in every node */
 } cgx_exec_opts;
+
+typedef enum { CGX_SYNC_AUTO = 0, CGX_SYNC_DEFER = 1, CGX_SYNC_CHAIN = 2 } cgx_sync_mode;
 
 typedef struct {
   uint64_t bytes_data_rebound;   /* last bind: data bytes copied into placeholders */
@@ -167,6 +174,8 @@ typedef struct {
   uint32_t n_ext;                /* N_ext of this exec */
   uint32_t kernels_per_replay;   /* library kernels per bind+launch (copy/root/chain) */
   uint32_t mode, transport;
+  uint32_t n_deferred;           /* nodes running with the deferred PDL wait */
+  uint32_t dataflow;             /* 1: nodes synchronise through dataflow counters */
 } cgx_stats_t;
 
 /* One segment's slow-path measurements, all microseconds. */
@@ -242,6 +251,11 @@ int cgx_debug_ext_field_offsets(const cgx_exec* e, int pos, uint64_t* offs, int 
  * [cta][8] ns stamps (entry, setup done, first stage landed, last MMA committed, accumulator ready,
  * split partial published, all splits arrived, exit); n_out = CTA count. */
 int cgx_debug_gemm_trace(cgx_exec* e, int pos, uint64_t* host_out, int cap, int* n_out);
+/* Diagnostics: replay timeline of an exec created with CGX_NODE_TRACE=1 in the environment (chain
+ * kernels only): host_out gets [launch][3] %globaltimer ns = (first CTA entry, last CTA past its
+ * input wait, last CTA exit) over the replays since the previous call, which then resets them.
+ * CGX_E_STATE when tracing is off. Synchronises the exec's stream. */
+int cgx_debug_node_trace(cgx_exec* e, uint64_t* host_out, int cap, int* n_out);
 
 /* ---- selective CUDA graphs ---------------------------------------------------------------- */
 /* Slow path: measure one segment (index into the marked segments, or -1 = whole chain) in the

@@ -28,6 +28,7 @@ GEMM_BIAS, GEMM_GELU, GEMM_RESIDUAL = 1, 2, 4
 MODE = {"EAGER": 0, "COPY": 1, "INDIRECT": 2, "SETPARAMS": 3, "STALE": 4}
 XPORT = {"DEFAULT": 0, "H2D": 1, "ROOT_MEMCPY": 2, "ROOT_PARAMS": 3, "ROOT_MAPPED": 4, "FIRST_NODE": 5, "H2D_PINGPONG": 6, "PRELUDE": 7}
 DECIDE = {0: "EAGER", 1: "GRAPH_COPY", 2: "GRAPH_INDIRECT"}
+SYNC = {"AUTO": 0, "DEFER": 1, "CHAIN": 2}
 MAX_PROFILE_KERNELS = 1024
 
 
@@ -41,7 +42,7 @@ class Attr(C.Structure):
 class ExecOpts(C.Structure):
     _fields_ = [("mode", C.c_int), ("transport", C.c_int), ("first_node", C.c_int),
                 ("n_nodes", C.c_int), ("no_pdl", C.c_int), ("validate", C.c_int),
-                ("copy_impl", C.c_int)]
+                ("copy_impl", C.c_int), ("sync_mode", C.c_int)]
 
 
 class Stats(C.Structure):
@@ -50,7 +51,8 @@ class Stats(C.Structure):
                 ("n_binds", C.c_uint64), ("n_launches", C.c_uint64),
                 ("n_setparam_calls", C.c_uint32), ("n_copy_tensors", C.c_uint32),
                 ("n_nodes", C.c_uint32), ("n_graph_nodes", C.c_uint32), ("n_ext", C.c_uint32),
-                ("kernels_per_replay", C.c_uint32), ("mode", C.c_uint32), ("transport", C.c_uint32)]
+                ("kernels_per_replay", C.c_uint32), ("mode", C.c_uint32), ("transport", C.c_uint32),
+                ("n_deferred", C.c_uint32), ("dataflow", C.c_uint32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -109,6 +111,7 @@ def _load():
         "cgx_debug_param_image": ([VP, I, VP, U64, P(U64), P(U64)], I),
         "cgx_debug_ext_field_offsets": ([VP, I, P(U64), I, P(I)], I),
         "cgx_debug_gemm_trace": ([VP, I, P(U64), I, P(I)], I),
+        "cgx_debug_node_trace": ([VP, P(U64), I, P(I)], I),
         "cgx_nccl_unique_id": ([VP], I),
         "cgx_nccl_comm_init": ([I, I, VP, I, P(VP)], I),
         "cgx_nccl_comm_destroy": ([VP], I),
@@ -127,7 +130,7 @@ EXPORTED = ("cgx_version", "cgx_last_error", "cgx_chain_create", "cgx_chain_add_
             "cgx_launch", "cgx_output", "cgx_stats", "cgx_debug_read_table",
             "cgx_debug_setparam_nodes", "cgx_exec_destroy", "cgx_profile", "cgx_select",
             "cgx_dispatch_floor", "cgx_fill_uniform_f32", "cgx_copy", "cgx_graph_floor", "cgx_kernel_times", "cgx_find_param_offset",
-            "cgx_debug_param_image", "cgx_debug_ext_field_offsets", "cgx_debug_gemm_trace", "cgx_nccl_unique_id",
+            "cgx_debug_param_image", "cgx_debug_ext_field_offsets", "cgx_debug_gemm_trace", "cgx_debug_node_trace", "cgx_nccl_unique_id",
             "cgx_nccl_comm_init", "cgx_nccl_comm_destroy")
 
 
@@ -180,8 +183,10 @@ def chain_destroy(chain: int):
 
 
 def exec_create(chain: int, mode: str, stream: int, transport: str = "DEFAULT", first_node: int = 0,
-                n_nodes: int = 0, no_pdl: bool = False, validate: int = 0, copy_impl: int = 0) -> int:
-    o = ExecOpts(MODE[mode], XPORT[transport], first_node, n_nodes, int(no_pdl), validate, copy_impl)
+                n_nodes: int = 0, no_pdl: bool = False, validate: int = 0, copy_impl: int = 0,
+                sync: str = "AUTO") -> int:
+    o = ExecOpts(MODE[mode], XPORT[transport], first_node, n_nodes, int(no_pdl), validate, copy_impl,
+                 SYNC[sync])
     out = C.c_void_p()
     _ck(LIB.cgx_exec_create_ex(chain, C.byref(o), stream, C.byref(out)), "cgx_exec_create_ex")
     return out.value
@@ -254,6 +259,14 @@ def gemm_trace(ex: int, pos: int) -> list:
     buf = (C.c_uint64 * (8 * 4096))()
     _ck(LIB.cgx_debug_gemm_trace(ex, pos, buf, 8 * 4096, C.byref(n)), "cgx_debug_gemm_trace")
     return [list(buf[8 * i: 8 * i + 8]) for i in range(n.value)]
+
+
+def node_trace(ex: int, n_launch: int) -> list:
+    """[(entry, ready, exit)] ns per launch position (exec created with CGX_NODE_TRACE=1)."""
+    n = C.c_int()
+    buf = (C.c_uint64 * (3 * n_launch))()
+    _ck(LIB.cgx_debug_node_trace(ex, buf, 3 * n_launch, C.byref(n)), "cgx_debug_node_trace")
+    return [tuple(buf[3 * i: 3 * i + 3]) for i in range(n.value)]
 
 
 def exec_destroy(ex: int):

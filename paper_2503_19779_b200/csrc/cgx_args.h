@@ -23,7 +23,17 @@ struct ElemArgs {
   float scalar;            // SCALE_IMM
   uint32_t pre;            // bit i: operand i may be loaded BEFORE griddepcontrol.wait (an
                            // EXTERNAL or STATIC slot, never written inside the graph)
+  // Dataflow mode (kFlagDataflow; runtime.cu set_dataflow): per-node completion counters replace
+  // griddepcontrol.wait, so a node waits for exactly the nodes it depends on.
+  uint32_t* df_done;       // per-launch CTA-completion counters of this exec (monotonic)
+  uint32_t* df_epoch;      // replay counter of this exec, bumped by its first node
+  uint32_t df_self;        // this launch's counter
+  uint32_t df_n;           // dependencies
+  uint32_t df_dep[4];      // their counters
+  uint32_t df_ctas[4];     // their CTA counts: dependency complete <=> done >= epoch * ctas
+  unsigned long long* trace;  // diagnostics (CGX_NODE_TRACE=1): [entry min, ready max, exit max] ns
 };
+static constexpr int kDfMaxDeps = 4;
 // PDL protocol (see runtime.cu, set_pdl_flags): every chain kernel triggers its dependents at
 // entry, so consecutive nodes' prologues cascade; only data nothing in the graph writes (inputs,
 // weights, the table under T1) is read before griddepcontrol.wait. The first consumer after a
@@ -31,6 +41,25 @@ struct ElemArgs {
 // start before the root has completed.
 static constexpr uint32_t kFlagTableAfterWait = 1u;
 static constexpr uint32_t kFlagTriggerAfterWait = 2u;
+// Deferred wait (runtime.cu, set_defer_flags): a node whose operands are all EXTERNAL/STATIC and
+// whose output no earlier node of the graph reads or writes has no data dependency on any
+// predecessor, so it computes and stores BEFORE griddepcontrol.wait and waits only before exiting.
+// The wait is kept (at the end) so "node k complete => nodes < k complete" stays transitive for the
+// later nodes that rely on it.
+static constexpr uint32_t kFlagDeferWait = 4u;
+// Dataflow (graph modes, every node a chain kernel): the early-trigger cascade keeps every node of
+// the replay launched in order (all CTAs of node k have started before node k+1 is launched), and
+// each node, instead of griddepcontrol.wait, spins (one thread, ld.acquire.gpu) until the CTA
+// counters of its RAW / WAR / WAW dependencies reach epoch x CTAs, and signals its own counter
+// (bar.sync, fence, atomic add) when done. Deadlock-free because a node only ever waits for
+// EARLIER nodes, whose CTAs are all resident or finished by the time it runs.
+static constexpr uint32_t kFlagDataflow = 8u;
+static constexpr uint32_t kFlagEpochBump = 16u;   // first node: CTA 0 bumps the epoch before it triggers
+// Dataflow refinements: a dependency on the IMMEDIATELY preceding node is taken with the hardware
+// griddepcontrol.wait (cheaper than a counter round trip); only nodes some later node spins on
+// signal their counter.
+static constexpr uint32_t kFlagDfPdlWait = 32u;
+static constexpr uint32_t kFlagDfSignal = 64u;
 
 // Multi-tensor copy (BASELINE north_star (1)). Static part lives in device
 // memory (per exec, written once at capture); the fresh sources travel by value in the params.

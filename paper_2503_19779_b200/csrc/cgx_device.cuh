@@ -28,6 +28,73 @@ __device__ __forceinline__ void tw_publish(const ArgsTW<Base, CAP>& A) {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 
+// Dataflow-mode synchronisation (kFlagDataflow, cgx_args.h).
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// First node, CTA 0, before it triggers: epoch += 1 (the only writer; later nodes read it after
+// their launch, which follows this CTA's trigger).
+__device__ __forceinline__ void df_bump(const ElemArgs& a) {
+  if (blockIdx.x == 0) {
+    if (threadIdx.x == 0) {
+      *a.df_epoch = *a.df_epoch + 1u;
+      __threadfence();
+    }
+    __syncthreads();
+  }
+}
+__device__ __forceinline__ void df_wait(const ElemArgs& a) {
+  if (a.df_n == 0) return;
+  if (threadIdx.x == 0) {
+    const uint32_t ep = ld_relaxed_u32(a.df_epoch);
+    for (uint32_t i = 0; i < a.df_n; ++i) {
+      const uint32_t target = ep * a.df_ctas[i];
+      const uint32_t* c = a.df_done + a.df_dep[i];
+      uint64_t spins = 0;
+      while ((int32_t)(ld_acquire_u32(c) - target) < 0) {
+        if (++spins > (1ull << 28)) __trap();    // a lost signal would hang the box: fail loudly
+      }
+    }
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ void df_signal(const ElemArgs& a) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(a.df_done + a.df_self, 1u);
+  }
+}
+
+// Plain (weak, L1-cached) 16-byte global load through an address that came from the pointer table
+// or a by-value param: without the explicit state space the compiler emits a generic LD.
+__device__ __forceinline__ float4 ld_global_f4(const float4* p) {
+  float4 v;
+  asm volatile("ld.global.v4.f32 {%0,%1,%2,%3}, [%4];\n" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p) : "memory");
+  return v;
+}
+
+// Replay timeline diagnostics (ElemArgs::trace): one thread per CTA stamps %globaltimer.
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void trace_at(const ElemArgs& a, int what) {
+  if (a.trace && threadIdx.x == 0) {
+    const unsigned long long t = gtimer();
+    if (what == 0) atomicMin(a.trace, t);
+    else atomicMax(a.trace + what, t);
+  }
+}
+
 // Pointer-table entry. Read-only path: the table never changes while a reader kernel runs (it is
 // written before the graph starts, by a root node the reader waits for, or by the T5 publisher
 // before it triggers the reader's launch), and L1/texture state is invalidated at every kernel

@@ -42,11 +42,31 @@ __device__ __forceinline__ void fetch_operands(const ElemArgs& a, const void*& p
 #define CGX_PROLOGUE(a, p0, p1)                                        \
   const void* p0;                                                      \
   const void* p1;                                                      \
+  if ((a).flags & kFlagEpochBump) df_bump(a);                          \
   if (!((a).flags & kFlagTriggerAfterWait)) pdl_trigger();             \
   if (!((a).flags & kFlagTableAfterWait)) fetch_operands((a), p0, p1); \
-  pdl_wait();                                                          \
+  sync_in(a);                                                          \
   if ((a).flags & kFlagTableAfterWait) fetch_operands((a), p0, p1);    \
   if ((a).flags & kFlagTriggerAfterWait) pdl_trigger();
+
+// The point where a node may start reading other nodes' outputs: griddepcontrol.wait (PDL chain),
+// nothing yet (deferred wait: at sync_out), or the dataflow counters (plus the PDL wait when the
+// node follows a root table-writer node, kFlagTableAfterWait).
+__device__ __forceinline__ void sync_in(const ElemArgs& a) {
+  if (a.flags & kFlagDataflow) {
+    if (a.flags & kFlagDfPdlWait) pdl_wait();
+    df_wait(a);
+  } else if (!(a.flags & kFlagDeferWait)) {
+    pdl_wait();
+  }
+  trace_at(a, 1);
+}
+// Every CTA (all threads) must reach this once, at the very end.
+__device__ __forceinline__ void sync_out(const ElemArgs& a) {
+  if (a.flags & kFlagDfSignal) df_signal(a);
+  else if (a.flags & kFlagDeferWait) pdl_wait();
+  trace_at(a, 2);
+}
 
 // ---------------------------------------------------------------------------- f32 elementwise
 // Operands whose `pre` bit is set (EXTERNAL / STATIC slots: never written inside the graph) are
@@ -54,9 +74,11 @@ __device__ __forceinline__ void fetch_operands(const ElemArgs& a, const void*& p
 template <int OP, int TW>
 __global__ void __launch_bounds__(kElemThreads) k_elem_f32(const __grid_constant__ ArgsTW<ElemArgs, TW> A) {
   const ElemArgs& a = A.a;
+  trace_at(a, 0);
   tw_publish(A);
   constexpr bool kBinary = (OP == OP_ADD || OP == OP_MUL);
   const bool late = a.flags & kFlagTableAfterWait;
+  if (a.flags & kFlagEpochBump) df_bump(a);
   if (!(a.flags & kFlagTriggerAfterWait)) pdl_trigger();
   const void* p0;
   const void* p1;
@@ -76,17 +98,17 @@ __global__ void __launch_bounds__(kElemThreads) k_elem_f32(const __grid_constant
 #pragma unroll
     for (int j = 0; j < kElemVec; ++j) {
       const uint64_t i = base + (uint64_t)j * kElemThreads;
-      if (i < n4) xv[j] = x[i];
+      if (i < n4) xv[j] = ld_global_f4(x + i);
     }
   }
   if (pre_y) {
 #pragma unroll
     for (int j = 0; j < kElemVec; ++j) {
       const uint64_t i = base + (uint64_t)j * kElemThreads;
-      if (i < n4) yv[j] = y[i];
+      if (i < n4) yv[j] = ld_global_f4(y + i);
     }
   }
-  pdl_wait();
+  sync_in(a);
   if (late) {
     fetch_operands(a, p0, p1);
     x = reinterpret_cast<const float4*>(p0);
@@ -98,14 +120,14 @@ __global__ void __launch_bounds__(kElemThreads) k_elem_f32(const __grid_constant
 #pragma unroll
     for (int j = 0; j < kElemVec; ++j) {
       const uint64_t i = base + (uint64_t)j * kElemThreads;
-      if (i < n4) xv[j] = x[i];
+      if (i < n4) xv[j] = ld_global_f4(x + i);
     }
   }
   if (kBinary && !pre_y) {
 #pragma unroll
     for (int j = 0; j < kElemVec; ++j) {
       const uint64_t i = base + (uint64_t)j * kElemThreads;
-      if (i < n4) yv[j] = y[i];
+      if (i < n4) yv[j] = ld_global_f4(y + i);
     }
   }
   float4* o = reinterpret_cast<float4*>(a.out);
@@ -131,6 +153,7 @@ __global__ void __launch_bounds__(kElemThreads) k_elem_f32(const __grid_constant
       reinterpret_cast<float*>(a.out)[t] = apply_f32<OP>(xs[t], yy, sval);
     }
   }
+  sync_out(a);
 }
 
 // ---------------------------------------------------------------------------- bf16 elementwise
@@ -144,6 +167,7 @@ __device__ __forceinline__ __nv_bfloat16 apply_bf16(__nv_bfloat16 x, __nv_bfloat
 template <int OP, int TW>
 __global__ void __launch_bounds__(kElemThreads) k_elem_bf16(const __grid_constant__ ArgsTW<ElemArgs, TW> A) {
   const ElemArgs& a = A.a;
+  trace_at(a, 0);
   tw_publish(A);
   CGX_PROLOGUE(a, p0, p1)
   const uint4* x = reinterpret_cast<const uint4*>(p0);
@@ -183,6 +207,7 @@ __global__ void __launch_bounds__(kElemThreads) k_elem_bf16(const __grid_constan
           apply_bf16<OP>(xs[t], (OP == OP_ADD || OP == OP_MUL) ? ys[t] : xs[t], a.scalar);
     }
   }
+  sync_out(a);
 }
 
 // ---------------------------------------------------------------------------- REDUCE_SUM f32
@@ -193,26 +218,42 @@ static constexpr int kReduceThreads = 256;
 template <int TW>
 __global__ void __launch_bounds__(kReduceThreads) k_reduce_sum_f32(const __grid_constant__ ArgsTW<ElemArgs, TW> A) {
   const ElemArgs& a = A.a;
+  trace_at(a, 0);
   tw_publish(A);
   CGX_PROLOGUE(a, p0, p1)
   (void)p1;
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t rows = a.n / a.cols;
   const uint64_t r = (uint64_t)blockIdx.x * (kReduceThreads / 32) + warp;
-  if (r >= rows) return;
-  const float4* row = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(p0) + r * a.cols);
-  const uint32_t c4 = a.cols >> 2;
-  double acc = 0.0;
-  for (uint32_t c = lane; c < c4; c += 32) {
-    const float4 v = row[c];
-    acc += (double)v.x;
-    acc += (double)v.y;
-    acc += (double)v.z;
-    acc += (double)v.w;
-  }
+  if (r < rows) {
+    const float4* row = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(p0) + r * a.cols);
+    const uint32_t c4 = a.cols >> 2;
+    double acc = 0.0;
+    uint32_t c = lane;
+    for (; c + 32 < c4; c += 64) {            // two loads in flight, same summation order
+      const float4 v = ld_global_f4(row + c);
+      const float4 u = ld_global_f4(row + c + 32);
+      acc += (double)v.x;
+      acc += (double)v.y;
+      acc += (double)v.z;
+      acc += (double)v.w;
+      acc += (double)u.x;
+      acc += (double)u.y;
+      acc += (double)u.z;
+      acc += (double)u.w;
+    }
+    if (c < c4) {
+      const float4 v = ld_global_f4(row + c);
+      acc += (double)v.x;
+      acc += (double)v.y;
+      acc += (double)v.z;
+      acc += (double)v.w;
+    }
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-  if (lane == 0) reinterpret_cast<float*>(a.out)[r] = __double2float_rn(acc);
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (lane == 0) reinterpret_cast<float*>(a.out)[r] = __double2float_rn(acc);
+  }
+  sync_out(a);
 }
 
 // ---------------------------------------------------------------------------- multi-tensor copy

@@ -381,6 +381,9 @@ struct cgx_exec {
   void* gemm_cnt = nullptr;
   size_t gemm_cnt_off = 0;        // next free counter bytes while building launches
   int t5_pub = 0;                 // T5: position of the table-publishing launch
+  unsigned long long* d_trace = nullptr;   // CGX_NODE_TRACE=1: [launch][3] ns stamps
+  uint32_t* df_mem = nullptr;     // dataflow: [launches] CTA-completion counters + [1] epoch
+  bool dataflow = false;
   // T3 / T4 root
   const void* root_fn = nullptr;
   AlignedBuf root_args;
@@ -615,6 +618,130 @@ static void set_prewait_masks(cgx_exec* e) {
     }
     argp<ElemArgs>(l)->pre = pre;
   }
+}
+
+// How nodes wait for their predecessors in graph modes with PDL (cgx_args.h).
+//
+// Dataflow (CGX_SYNC_AUTO, every node a chain kernel): node k waits, through per-launch CTA
+// counters, for exactly (a) the last earlier writer of each slot it reads (RAW), (b) the last
+// earlier writer of its output slot (WAW) and every earlier reader of that slot since then (WAR).
+// "Earlier" is within this graph only: a graph launch waits for the previous replay as a whole.
+// Waits compose transitively (a node signals only after its own waits returned), so these sets
+// suffice. More than kDfMaxDeps dependencies falls back to deferred waits.
+//
+// Deferred wait (CGX_SYNC_DEFER, or the fallback): inside one graph the early-trigger cascade
+// means node k's pre-wait part can overlap ANY earlier, not yet completed node of the same replay.
+// So node k may store before its griddepcontrol.wait iff it is an f32 elementwise node whose
+// operands are all read pre-wait (EXTERNAL/STATIC) and no earlier node of this graph reads or
+// writes its output slot; it still waits before exiting, which keeps "node k complete => nodes < k
+// complete" for the nodes after it.
+//
+// Eager mode keeps plain PDL waits: there the previous iteration's nodes are stream predecessors.
+static bool df_capable(const Node& n, cgx_dtype out_dt) {
+  if (n.op == CGX_OP_REDUCE_SUM) return true;
+  if (n.op <= CGX_OP_COPY) return true;                         // f32 and bf16 elementwise
+  return n.op == CGX_OP_SCALE_T && out_dt == CGX_F32;
+}
+
+static int set_sync_flags(cgx_exec* e) {
+  if (e->o.no_pdl || e->o.mode == CGX_MODE_EAGER || e->o.sync_mode == CGX_SYNC_CHAIN) return CGX_OK;
+  const size_t ns = e->c->slots.size(), nl = e->L.size();
+  if (e->o.sync_mode == CGX_SYNC_AUTO && nl > 0) {
+    bool ok = true;
+    for (auto& l : e->L) ok = ok && l.kind == LK_KERNEL && df_capable(e->c->nodes[l.node], e->c->slots[e->c->nodes[l.node].out].dtype);
+    std::vector<std::vector<uint32_t>> deps(nl);
+    if (ok) {
+      std::vector<int> last_w(ns, -1);
+      std::vector<std::vector<uint32_t>> readers(ns);   // readers since the last writer
+      for (size_t p = 0; p < nl && ok; ++p) {
+        const Node& n = e->c->nodes[e->L[p].node];
+        auto add = [&](int q) {
+          if (q < 0) return;
+          for (uint32_t d : deps[p]) if (d == (uint32_t)q) return;
+          deps[p].push_back((uint32_t)q);
+        };
+        for (int j = 0; j < n.n_in; ++j) add(last_w[n.in[j]]);
+        add(last_w[n.out]);
+        for (uint32_t r : readers[n.out]) if (r != p) add((int)r);
+        if (deps[p].size() > (size_t)kDfMaxDeps) ok = false;
+        for (int j = 0; j < n.n_in; ++j) readers[n.in[j]].push_back((uint32_t)p);
+        last_w[n.out] = (int)p;
+        readers[n.out].clear();
+      }
+    }
+    if (ok) {
+      cudaError_t ce = cudaMalloc(&e->df_mem, sizeof(uint32_t) * (nl + 1));
+      if (ce == cudaSuccess) ce = cudaMemset(e->df_mem, 0, sizeof(uint32_t) * (nl + 1));
+      if (ce != cudaSuccess) return cuda_fail(ce, "dataflow counters", __LINE__);
+      // transitive dependency closure (bitsets): a node whose closure is every earlier node takes
+      // its immediate predecessor through griddepcontrol.wait (measured: cheaper on a linear chain,
+      // C1); a node with independent earlier nodes spins on counters only, because a PDL wait
+      // also waits out the in-order retirement of the unrelated grids before it (measured: C2
+      // 175 us with counters vs 190 us with PDL waits on the immediate predecessor).
+      const size_t words = (nl + 63) / 64;
+      std::vector<std::vector<uint64_t>> clo(nl, std::vector<uint64_t>(words, 0));
+      std::vector<char> full(nl, 0);
+      for (size_t p = 0; p < nl; ++p) {
+        for (uint32_t d : deps[p]) {
+          clo[p][d / 64] |= 1ull << (d % 64);
+          for (size_t w = 0; w < words; ++w) clo[p][w] |= clo[d][w];
+        }
+        size_t cnt = 0;
+        for (size_t w = 0; w < words; ++w) cnt += (size_t)__builtin_popcountll(clo[p][w]);
+        full[p] = cnt == p;
+      }
+      std::vector<char> spun_on(nl, 0);
+      for (size_t p = 0; p < nl; ++p) {
+        ElemArgs* a = argp<ElemArgs>(e->L[p]);
+        a->df_done = e->df_mem;
+        a->df_epoch = e->df_mem + nl;
+        a->df_self = (uint32_t)p;
+        a->df_n = 0;
+        uint32_t f = kFlagDataflow;
+        // the first node after a root table-writer waits for the root through PDL
+        if (a->flags & kFlagTableAfterWait) f |= kFlagDfPdlWait;
+        for (uint32_t d : deps[p]) {
+          if (d + 1 == p && full[p]) {  // immediate predecessor of a chain node: hardware wait
+            f |= kFlagDfPdlWait;
+            continue;
+          }
+          const Launch& q = e->L[d];
+          a->df_dep[a->df_n] = d;
+          a->df_ctas[a->df_n] = q.grid.x * q.grid.y * q.grid.z;
+          ++a->df_n;
+          spun_on[d] = 1;
+        }
+        a->flags |= f;
+      }
+      bool any = false;
+      for (size_t p = 0; p < nl; ++p)
+        if (spun_on[p]) {
+          argp<ElemArgs>(e->L[p])->flags |= kFlagDfSignal;
+          any = true;
+        }
+      // the epoch (and its fence before node 0 triggers) is only needed when some node spins
+      if (any) argp<ElemArgs>(e->L[0])->flags |= kFlagEpochBump;
+      e->dataflow = true;
+      return CGX_OK;
+    }
+  }
+  std::vector<char> touched(ns, 0);
+  for (auto& l : e->L) {
+    const Node& node = e->c->nodes[l.node];
+    if (l.kind == LK_KERNEL) {
+      const bool elem = node.op <= CGX_OP_COPY || node.op == CGX_OP_SCALE_T;
+      const bool f32 = e->c->slots[node.out].dtype == CGX_F32;
+      if (elem && f32) {
+        const uint32_t need = (node.op == CGX_OP_ADD || node.op == CGX_OP_MUL || node.op == CGX_OP_SCALE_T) ? 3u : 1u;
+        ElemArgs* a = argp<ElemArgs>(l);
+        if ((a->pre & need) == need && !touched[node.out] && !(a->flags & (kFlagTableAfterWait | kFlagTriggerAfterWait)))
+          a->flags |= kFlagDeferWait;
+      }
+    }
+    for (int j = 0; j < node.n_in; ++j) touched[node.in[j]] = 1;
+    touched[node.out] = 1;
+  }
+  return CGX_OK;
 }
 
 static int issue(cgx_exec* e, Launch& l, cudaStream_t s) {
@@ -869,7 +996,8 @@ static int capture_graph(cgx_exec* e, int gi) {
         const Node& n = e->c->nodes[l.node];
         const uint32_t f = kFlagTableAfterWait | kFlagTriggerAfterWait;
         if (n.op == CGX_OP_LAYERNORM) argp<LnArgs>(l)->flags |= f;
-        else if (n.op <= CGX_OP_REDUCE_SUM || n.op == CGX_OP_SCALE_T) argp<ElemArgs>(l)->flags |= f;
+        else if (n.op <= CGX_OP_REDUCE_SUM || n.op == CGX_OP_SCALE_T)
+          argp<ElemArgs>(l)->flags = (argp<ElemArgs>(l)->flags | f | ((argp<ElemArgs>(l)->flags & kFlagDataflow) ? kFlagDfPdlWait : 0u)) & ~kFlagDeferWait;
         else return fail(CGX_E_UNSUPPORTED, "first node after the root table writer must be elementwise/LN");
       }
       if (root_is_copy) l.pdl = false;
@@ -896,6 +1024,8 @@ static void exec_free(cgx_exec* e) {
   if (e->ph_arena) cudaFree(e->ph_arena);
   if (e->gemm_ws) cudaFree(e->gemm_ws);
   if (e->gemm_cnt) cudaFree(e->gemm_cnt);
+  if (e->df_mem) cudaFree(e->df_mem);
+  if (e->d_trace) cudaFree(e->d_trace);
   if (e->d_desc) cudaFree(e->d_desc);
   if (e->d_chunk) cudaFree(e->d_chunk);
   if (e->d_table) cudaFree(e->d_table);
@@ -914,6 +1044,8 @@ static void exec_free(cgx_exec* e) {
   delete e;
 }
 
+static void node_trace_reset(cgx_exec* e);
+
 extern "C" int cgx_exec_create_ex(cgx_chain* c, const cgx_exec_opts* opts, void* stream, cgx_exec** out) {
   if (!c || !out) return fail(CGX_E_INVALID_ARG, "exec_create: NULL argument");
   cgx_exec_opts o{};
@@ -922,6 +1054,7 @@ extern "C" int cgx_exec_create_ex(cgx_chain* c, const cgx_exec_opts* opts, void*
   if (o.transport < CGX_XPORT_DEFAULT || o.transport > CGX_XPORT_PRELUDE)
     return fail(CGX_E_INVALID_ARG, "exec_create: transport");
   if (o.copy_impl < 0 || o.copy_impl > 2) return fail(CGX_E_INVALID_ARG, "exec_create: copy_impl");
+  if (o.sync_mode < CGX_SYNC_AUTO || o.sync_mode > CGX_SYNC_CHAIN) return fail(CGX_E_INVALID_ARG, "exec_create: sync_mode");
   const int K = (int)c->nodes.size();
   if (K == 0) return fail(CGX_E_STATE, "exec_create: empty chain");
   const int first = o.first_node, last = o.n_nodes ? o.first_node + o.n_nodes - 1 : K - 1;
@@ -967,6 +1100,16 @@ extern "C" int cgx_exec_create_ex(cgx_chain* c, const cgx_exec_opts* opts, void*
   for (int k = first; k <= last; ++k)
     if ((st = build_launch(e, k, e->L[k - first])) != CGX_OK) return bail(st);
   set_prewait_masks(e);
+  if ((st = set_sync_flags(e)) != CGX_OK) return bail(st);
+  if (const char* tv = getenv("CGX_NODE_TRACE"); tv && tv[0] == '1') {
+    const size_t nb = sizeof(unsigned long long) * 3 * e->L.size();
+    cudaError_t ce = cudaMalloc(&e->d_trace, nb);
+    if (ce != cudaSuccess) return bail(cuda_fail(ce, "node trace", __LINE__));
+    node_trace_reset(e);
+    for (size_t p = 0; p < e->L.size(); ++p)
+      if (e->L[p].kind == LK_KERNEL && df_capable(c->nodes[e->L[p].node], c->slots[c->nodes[e->L[p].node].out].dtype))
+        argp<ElemArgs>(e->L[p])->trace = e->d_trace + 3 * p;
+  }
   if (o.mode != CGX_MODE_EAGER) {
     cudaError_t ce = cudaStreamCreateWithFlags(&e->cs, cudaStreamNonBlocking);
     if (ce != cudaSuccess) return bail(cuda_fail(ce, "cudaStreamCreate", __LINE__));
@@ -1018,6 +1161,11 @@ extern "C" int cgx_exec_create_ex(cgx_chain* c, const cgx_exec_opts* opts, void*
   e->st.n_nodes = (uint32_t)e->L.size();
   e->st.n_ext = (uint32_t)n_ext;
   e->st.n_graph_nodes = e->graph_nodes;
+  e->st.n_deferred = 0;
+  for (auto& l : e->L)
+    if (l.kind == LK_KERNEL && (e->c->nodes[l.node].op <= CGX_OP_COPY || e->c->nodes[l.node].op == CGX_OP_SCALE_T))
+      e->st.n_deferred += (argp<ElemArgs>(l)->flags & kFlagDeferWait) ? 1u : 0u;
+  e->st.dataflow = e->dataflow ? 1u : 0u;
   e->st.mode = (uint32_t)o.mode;
   e->st.transport = o.mode == CGX_MODE_GRAPH_INDIRECT ? (uint32_t)eff_transport(o) : 0;
   e->st.kernels_per_replay = (uint32_t)kernels + (o.mode == CGX_MODE_GRAPH_COPY && o.copy_impl != 1 && !e->ext_read.empty()) +
@@ -1322,6 +1470,26 @@ extern "C" int cgx_debug_param_image(const cgx_exec* e, int pos, void* buf, uint
     CK(cudaFuncGetParamInfo(l.func, 0, &off, &sz));
     *param0_size_out = sz;
   }
+  return CGX_OK;
+}
+
+static void node_trace_reset(cgx_exec* e) {
+  std::vector<unsigned long long> h(3 * e->L.size(), 0);
+  for (size_t p = 0; p < e->L.size(); ++p) h[3 * p] = ~0ull;
+  cudaMemcpy(e->d_trace, h.data(), sizeof(unsigned long long) * h.size(), cudaMemcpyHostToDevice);
+}
+
+// Diagnostics (exec created with CGX_NODE_TRACE=1 in the environment): per launch position the
+// [first CTA entry, last CTA past its input wait, last CTA exit] %globaltimer ns of the replays
+// since the previous call (min / max over them), then reset. Synchronises the exec's stream.
+extern "C" int cgx_debug_node_trace(cgx_exec* e, uint64_t* host_out, int cap, int* n_out) {
+  if (!e || !n_out) return fail(CGX_E_INVALID_ARG, "node_trace: bad argument");
+  if (!e->d_trace) return fail(CGX_E_STATE, "node_trace: exec not created with CGX_NODE_TRACE=1");
+  CK(cudaStreamSynchronize(e->s));
+  const int n = (int)(3 * e->L.size());
+  if (host_out) CK(cudaMemcpy(host_out, e->d_trace, sizeof(uint64_t) * std::min(cap, n), cudaMemcpyDeviceToHost));
+  node_trace_reset(e);
+  *n_out = (int)e->L.size();
   return CGX_OK;
 }
 
