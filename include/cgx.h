@@ -134,10 +134,15 @@ typedef enum {
  *   PRELUDE      T7 (NEXT-1): the consumers are plain direct-pointer kernels (stand-ins for opaque
  *                    vendor kernels) captured as device-updatable nodes; a prelude root
  *                    node dereferences the table (one H2D per replay) and writes every pointer into
- *                    the consumers' parameter buffers with cudaGraphKernelNodeSetParam. */
+ *                    the consumers' parameter buffers with cudaGraphKernelNodeSetParam.
+ *   DEVICE       T8 (NEXT-4): as H2D for host binds, but the graph is instantiated for device
+ *                    launch, so cgx_device_loop can run many replays with no host work: a
+ *                    scheduler kernel copies replay i's pointer set into the table and
+ *                    tail-launches the chain graph, then itself. */
 typedef enum {
   CGX_XPORT_DEFAULT = 0, CGX_XPORT_H2D = 1, CGX_XPORT_ROOT_MEMCPY = 2, CGX_XPORT_ROOT_PARAMS = 3,
-  CGX_XPORT_ROOT_MAPPED = 4, CGX_XPORT_FIRST_NODE = 5, CGX_XPORT_H2D_PINGPONG = 6, CGX_XPORT_PRELUDE = 7
+  CGX_XPORT_ROOT_MAPPED = 4, CGX_XPORT_FIRST_NODE = 5, CGX_XPORT_H2D_PINGPONG = 6, CGX_XPORT_PRELUDE = 7,
+  CGX_XPORT_DEVICE = 8
 } cgx_transport;
 
 typedef enum { CGX_DECIDE_EAGER = 0, CGX_DECIDE_GRAPH_COPY = 1, CGX_DECIDE_GRAPH_INDIRECT = 2 } cgx_decision;
@@ -225,6 +230,15 @@ int cgx_exec_create_ex(cgx_chain* c, const cgx_exec_opts* opts, void* cuda_strea
 int cgx_bind(cgx_exec* e, const void* const* ext_dptrs, int n_ext);
 /* Per replay: cudaGraphLaunch (or K eager launches). CGX_E_STATE if never bound. */
 int cgx_launch(cgx_exec* e);
+/* NEXT-4: device-launched replays (INDIRECT exec with transport DEVICE). Enqueues on the exec's
+ * stream ONE host launch of a scheduler graph that runs n_replays replays on the device: replay i
+ * binds pointer set i % n_sets — d_ptr_sets is a caller-owned DEVICE array [n_sets][N_ext] of
+ * uint64 input addresses, each 16-B aligned, kept valid (with the buffers it points to) until the
+ * stream reaches the end of the loop — by copying it into the pointer table, then tail-launches
+ * the chain graph and itself (tail launches run in order, each after the previous completes).
+ * Returns immediately; the stream's next work starts after the last replay. n_replays = 0 is a
+ * no-op. CGX_E_STATE for other execs; CGX_E_NOT_ELIGIBLE when d_ptr_sets is not device memory. */
+int cgx_device_loop(cgx_exec* e, const void* d_ptr_sets, int n_sets, uint64_t n_replays);
 /* Library-owned device buffer of a slot (internal: shared per chain; external under COPY: the
  * placeholder). nbytes may be NULL. */
 int cgx_output(cgx_exec* e, int slot, void** dptr, uint64_t* nbytes);

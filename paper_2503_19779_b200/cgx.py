@@ -26,7 +26,8 @@ OP = {"ADD": 0, "MUL": 1, "SCALE_IMM": 2, "COPY": 3, "REDUCE_SUM": 4, "LAYERNORM
       "GEMM_BF16": 6, "ATTN_CAUSAL": 7, "ALLREDUCE_SUM": 8, "SCALE_T": 9}
 GEMM_BIAS, GEMM_GELU, GEMM_RESIDUAL = 1, 2, 4
 MODE = {"EAGER": 0, "COPY": 1, "INDIRECT": 2, "SETPARAMS": 3, "STALE": 4}
-XPORT = {"DEFAULT": 0, "H2D": 1, "ROOT_MEMCPY": 2, "ROOT_PARAMS": 3, "ROOT_MAPPED": 4, "FIRST_NODE": 5, "H2D_PINGPONG": 6, "PRELUDE": 7}
+XPORT = {"DEFAULT": 0, "H2D": 1, "ROOT_MEMCPY": 2, "ROOT_PARAMS": 3, "ROOT_MAPPED": 4, "FIRST_NODE": 5, "H2D_PINGPONG": 6, "PRELUDE": 7,
+         "DEVICE": 8}
 DECIDE = {0: "EAGER", 1: "GRAPH_COPY", 2: "GRAPH_INDIRECT"}
 SYNC = {"AUTO": 0, "DEFER": 1, "CHAIN": 2}
 MAX_PROFILE_KERNELS = 1024
@@ -112,6 +113,7 @@ def _load():
         "cgx_debug_ext_field_offsets": ([VP, I, P(U64), I, P(I)], I),
         "cgx_debug_gemm_trace": ([VP, I, P(U64), I, P(I)], I),
         "cgx_debug_node_trace": ([VP, P(U64), I, P(I)], I),
+        "cgx_device_loop": ([VP, VP, I, U64], I),
         "cgx_nccl_unique_id": ([VP], I),
         "cgx_nccl_comm_init": ([I, I, VP, I, P(VP)], I),
         "cgx_nccl_comm_destroy": ([VP], I),
@@ -130,7 +132,7 @@ EXPORTED = ("cgx_version", "cgx_last_error", "cgx_chain_create", "cgx_chain_add_
             "cgx_launch", "cgx_output", "cgx_stats", "cgx_debug_read_table",
             "cgx_debug_setparam_nodes", "cgx_exec_destroy", "cgx_profile", "cgx_select",
             "cgx_dispatch_floor", "cgx_fill_uniform_f32", "cgx_copy", "cgx_graph_floor", "cgx_kernel_times", "cgx_find_param_offset",
-            "cgx_debug_param_image", "cgx_debug_ext_field_offsets", "cgx_debug_gemm_trace", "cgx_debug_node_trace", "cgx_nccl_unique_id",
+            "cgx_debug_param_image", "cgx_debug_ext_field_offsets", "cgx_debug_gemm_trace", "cgx_debug_node_trace", "cgx_device_loop", "cgx_nccl_unique_id",
             "cgx_nccl_comm_init", "cgx_nccl_comm_destroy")
 
 
@@ -259,6 +261,10 @@ def gemm_trace(ex: int, pos: int) -> list:
     buf = (C.c_uint64 * (8 * 4096))()
     _ck(LIB.cgx_debug_gemm_trace(ex, pos, buf, 8 * 4096, C.byref(n)), "cgx_debug_gemm_trace")
     return [list(buf[8 * i: 8 * i + 8]) for i in range(n.value)]
+
+
+def device_loop(ex: int, d_ptr_sets: int, n_sets: int, n_replays: int) -> None:
+    _ck(LIB.cgx_device_loop(ex, d_ptr_sets, n_sets, n_replays), "cgx_device_loop")
 
 
 def node_trace(ex: int, n_launch: int) -> list:

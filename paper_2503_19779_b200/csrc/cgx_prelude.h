@@ -20,4 +20,15 @@ struct PreludeArgs {
 
 const void* kfn_prelude();
 
+// NEXT-4 device-side replay loop (k_prelude.cu, k_devloop)
+struct DevLoopArgs {
+  uint64_t* table;              // the exec's pointer table
+  const uint64_t* sets;         // [n_sets][n_ext] pointer sets (device)
+  unsigned long long* iter;     // replays started so far (device counter, reset per loop)
+  unsigned long long n_replays;
+  cudaGraphExec_t chain;        // device-launchable chain graph
+  uint32_t n_ext, n_sets;
+};
+const void* kfn_devloop();
+
 }  // namespace cgx

@@ -30,4 +30,30 @@ __global__ void k_prelude(const __grid_constant__ PreludeArgs a) {
 
 const void* kfn_prelude() { return (const void*)k_prelude; }
 
+// NEXT-4: one replay step of the device-side loop. Replay i = *iter: copy pointer set i % n_sets
+// into the table, fence, then tail-launch the chain graph and this scheduler's own graph. Tail
+// launches start after the launching graph completes and run one after another in enqueue order,
+// so the chain of replay i reads the table after this kernel wrote it, and the next scheduler
+// step (which overwrites the table) starts only after that chain has completed.
+__global__ void k_devloop(const __grid_constant__ DevLoopArgs a) {
+  __shared__ unsigned long long s_i;
+  if (threadIdx.x == 0) s_i = *a.iter;
+  __syncthreads();
+  const unsigned long long i = s_i;
+  if (i >= a.n_replays) return;
+  const uint64_t* src = a.sets + (size_t)(i % a.n_sets) * a.n_ext;
+  for (uint32_t j = threadIdx.x; j < a.n_ext; j += blockDim.x) a.table[j] = src[j];
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *a.iter = i + 1;
+    __threadfence();
+    if (cudaGraphLaunch(a.chain, cudaStreamGraphTailLaunch) != cudaSuccess) __trap();
+    if (i + 1 < a.n_replays && cudaGraphLaunch(cudaGetCurrentGraphExec(), cudaStreamGraphTailLaunch) != cudaSuccess)
+      __trap();
+  }
+}
+
+const void* kfn_devloop() { return (const void*)k_devloop; }
+
 }  // namespace cgx

@@ -383,6 +383,11 @@ struct cgx_exec {
   int t5_pub = 0;                 // T5: position of the table-publishing launch
   unsigned long long* d_trace = nullptr;   // CGX_NODE_TRACE=1: [launch][3] ns stamps
   uint32_t* df_mem = nullptr;     // dataflow: [launches] CTA-completion counters + [1] epoch
+  // T8 device loop: scheduler graph (one k_devloop node) + its replay counter
+  cudaGraph_t dl_g = nullptr;
+  cudaGraphExec_t dl_ge = nullptr;
+  cudaGraphNode_t dl_node = nullptr;
+  unsigned long long* dl_iter = nullptr;
   bool dataflow = false;
   // T3 / T4 root
   const void* root_fn = nullptr;
@@ -882,7 +887,8 @@ static int setup_table(cgx_exec* e) {
   CK(cudaMemset(e->d_table, 0, sizeof(uint64_t) * nalloc));
   const cgx_transport t = eff_transport(e->o);
   e->n_pad = (uint32_t)(((nalloc + 15) / 16) * 16);   // 128-B aligned ring slots
-  if (t == CGX_XPORT_H2D || t == CGX_XPORT_ROOT_MEMCPY || t == CGX_XPORT_ROOT_MAPPED || t == CGX_XPORT_PRELUDE) {
+  if (t == CGX_XPORT_H2D || t == CGX_XPORT_ROOT_MEMCPY || t == CGX_XPORT_ROOT_MAPPED || t == CGX_XPORT_PRELUDE ||
+      t == CGX_XPORT_DEVICE) {
     e->ring = t == CGX_XPORT_ROOT_MEMCPY ? 2 : 4;
     const unsigned flags = t == CGX_XPORT_ROOT_MAPPED ? cudaHostAllocMapped : cudaHostAllocDefault;
     CK(cudaHostAlloc((void**)&e->h_stage, sizeof(uint64_t) * e->n_pad * e->ring, flags));
@@ -1007,7 +1013,8 @@ static int capture_graph(cgx_exec* e, int gi) {
     if (l.kind == LK_KERNEL) CKS(last_captured_node(cs, &l.gnode[gi]));
   }
   CK(cudaStreamEndCapture(cs, &e->g[gi]));
-  CK(cudaGraphInstantiateWithFlags(&e->ge[gi], e->g[gi], 0));
+  const bool devl = e->o.mode == CGX_MODE_GRAPH_INDIRECT && t == CGX_XPORT_DEVICE;
+  CK(cudaGraphInstantiateWithFlags(&e->ge[gi], e->g[gi], devl ? cudaGraphInstantiateFlagDeviceLaunch : 0));
   CK(cudaGraphUpload(e->ge[gi], e->s));
   size_t nn = 0;
   CK(cudaGraphGetNodes(e->g[gi], nullptr, &nn));
@@ -1025,6 +1032,9 @@ static void exec_free(cgx_exec* e) {
   if (e->gemm_ws) cudaFree(e->gemm_ws);
   if (e->gemm_cnt) cudaFree(e->gemm_cnt);
   if (e->df_mem) cudaFree(e->df_mem);
+  if (e->dl_ge) cudaGraphExecDestroy(e->dl_ge);
+  if (e->dl_g) cudaGraphDestroy(e->dl_g);
+  if (e->dl_iter) cudaFree(e->dl_iter);
   if (e->d_trace) cudaFree(e->d_trace);
   if (e->d_desc) cudaFree(e->d_desc);
   if (e->d_chunk) cudaFree(e->d_chunk);
@@ -1051,7 +1061,7 @@ extern "C" int cgx_exec_create_ex(cgx_chain* c, const cgx_exec_opts* opts, void*
   cgx_exec_opts o{};
   if (opts) o = *opts;
   if (o.mode < CGX_MODE_EAGER || o.mode > CGX_MODE_GRAPH_STALE) return fail(CGX_E_INVALID_ARG, "exec_create: mode");
-  if (o.transport < CGX_XPORT_DEFAULT || o.transport > CGX_XPORT_PRELUDE)
+  if (o.transport < CGX_XPORT_DEFAULT || o.transport > CGX_XPORT_DEVICE)
     return fail(CGX_E_INVALID_ARG, "exec_create: transport");
   if (o.copy_impl < 0 || o.copy_impl > 2) return fail(CGX_E_INVALID_ARG, "exec_create: copy_impl");
   if (o.sync_mode < CGX_SYNC_AUTO || o.sync_mode > CGX_SYNC_CHAIN) return fail(CGX_E_INVALID_ARG, "exec_create: sync_mode");
@@ -1336,7 +1346,7 @@ extern "C" int cgx_bind(cgx_exec* e, const void* const* ext, int n_ext) {
                            e->xs));
         CK(cudaEventRecord(e->ev_copy[b], e->xs));
         e->ev_copy_set[b] = true;
-      } else if (t == CGX_XPORT_H2D || t == CGX_XPORT_PRELUDE) {
+      } else if (t == CGX_XPORT_H2D || t == CGX_XPORT_PRELUDE || t == CGX_XPORT_DEVICE) {
         const int slot = (int)(e->seq % e->ring);
         if (e->ev_used[slot]) CK(cudaEventSynchronize(e->ev[slot]));
         uint64_t* h = e->h_stage + (size_t)slot * e->n_pad;
@@ -1401,6 +1411,58 @@ extern "C" int cgx_launch(cgx_exec* e) {
     }
   }
   e->st.n_launches++;
+  e->launched_since_bind = true;
+  return CGX_OK;
+}
+
+extern "C" int cgx_device_loop(cgx_exec* e, const void* d_ptr_sets, int n_sets, uint64_t n_replays) {
+  if (!e) return fail(CGX_E_INVALID_ARG, "device_loop: exec is NULL");
+  if (e->o.mode != CGX_MODE_GRAPH_INDIRECT || eff_transport(e->o) != CGX_XPORT_DEVICE)
+    return fail(CGX_E_STATE, "device_loop: needs an INDIRECT exec with transport DEVICE");
+  if (n_replays == 0) return CGX_OK;
+  if (!d_ptr_sets || n_sets <= 0) return fail(CGX_E_INVALID_ARG, "device_loop: no pointer sets");
+  cudaPointerAttributes pa{};
+  if (cudaPointerGetAttributes(&pa, d_ptr_sets) != cudaSuccess || pa.type != cudaMemoryTypeDevice) {
+    cudaGetLastError();
+    return fail(CGX_E_NOT_ELIGIBLE, "device_loop: pointer sets must be device memory");
+  }
+  const uint32_t n_ext = (uint32_t)e->c->ext_slots.size();
+  DevLoopArgs a{};
+  a.table = e->d_table;
+  a.sets = static_cast<const uint64_t*>(d_ptr_sets);
+  a.n_replays = n_replays;
+  a.chain = e->ge[0];
+  a.n_ext = n_ext;
+  a.n_sets = (uint32_t)n_sets;
+  if (!e->dl_ge) {
+    CK(cudaMalloc(&e->dl_iter, sizeof(unsigned long long)));
+    a.iter = e->dl_iter;
+    CK(cudaStreamBeginCapture(e->cs, cudaStreamCaptureModeThreadLocal));
+    Launch r;
+    r.func = kfn_devloop();
+    r.grid = dim3(1);
+    r.block = dim3(128);
+    r.pdl = false;
+    r.args.reset(sizeof(DevLoopArgs));
+    memcpy(r.args.p, &a, sizeof(a));
+    CKS(issue(e, r, e->cs));
+    CKS(last_captured_node(e->cs, &e->dl_node));
+    CK(cudaStreamEndCapture(e->cs, &e->dl_g));
+    CK(cudaGraphInstantiateWithFlags(&e->dl_ge, e->dl_g, cudaGraphInstantiateFlagDeviceLaunch));
+    CK(cudaGraphUpload(e->dl_ge, e->s));
+  }
+  a.iter = e->dl_iter;
+  cudaKernelNodeParams kp{};
+  kp.func = const_cast<void*>(kfn_devloop());
+  kp.gridDim = dim3(1);
+  kp.blockDim = dim3(128);
+  void* argv[1] = {&a};
+  kp.kernelParams = argv;
+  CK(cudaGraphExecKernelNodeSetParams(e->dl_ge, e->dl_node, &kp));
+  CK(cudaMemsetAsync(e->dl_iter, 0, sizeof(unsigned long long), e->s));
+  CK(cudaGraphLaunch(e->dl_ge, e->s));
+  e->st.n_launches += n_replays;
+  e->bound = true;
   e->launched_since_bind = true;
   return CGX_OK;
 }
