@@ -349,8 +349,6 @@ def run_extras(args, torch, cgx, runner, wl, sm, spec, chain, stream, sets, set_
         return e0_.elapsed_time(e1_) * 1e3 / n
     timed_rr(50)
     base = min(timed_rr(M) for _ in range(3))
-    for exc in cold:
-        exc.close()
     arms["graph_no_rebind"] = {"us_per_replay": base, "base": f"cold: {N_SETS} COPY execs round-robin, no bind"}
     arms["graph_no_rebind_warm"] = {"us_per_replay": base_warm, "base": "warm: same exec, same inputs"}
     for name, (mode, xp) in {"copy": ("COPY", "DEFAULT"), "indirect_h2d": ("INDIRECT", "H2D"),
@@ -363,7 +361,15 @@ def run_extras(args, torch, cgx, runner, wl, sm, spec, chain, stream, sets, set_
                              "setparams": ("SETPARAMS", "DEFAULT")}.items():
         ex = ex_copy if mode == "COPY" else chain.exec(mode, stream=stream, transport=xp)
         loop(ex.handle, 20)
-        us = min(timed(ex.handle, M) for _ in range(3))
+        # base and arm interleaved, 5 pairs: the median pair difference cancels slow drift
+        pairs = []
+        for _ in range(5):
+            b_ = timed_rr(M // 2)
+            a_ = timed(ex.handle, M // 2)
+            pairs.append((a_, b_))
+        us = statistics.median(a_ for a_, _ in pairs)
+        delta = statistics.median(a_ - b_ for a_, b_ in pairs)
+        noise = statistics.pstdev(a_ - b_ for a_, b_ in pairs)
         host = []
         for i in range(200):
             stream.synchronize()
@@ -372,11 +378,13 @@ def run_extras(args, torch, cgx, runner, wl, sm, spec, chain, stream, sets, set_
             LIB.cgx_launch(ex.handle)
             host.append((time.perf_counter() - t0) * 1e6)
         stream.synchronize()
-        arms[name] = {"us_per_replay": us, "rebind_delta_us": us - base,
+        arms[name] = {"us_per_replay": us, "rebind_delta_us": delta, "rebind_delta_noise_us": noise,
                       "rebind_delta_vs_warm_base_us": us - base_warm,
                       "host_bind_launch_us": statistics.median(host)}
         if ex is not ex_copy:
             ex.close()
+    for exc in cold:
+        exc.close()
     # node synchronisation inside the replay: dataflow counters (deployed, AUTO) vs
     # deferred PDL waits vs the plain PDL chain, same INDIRECT exec otherwise
     sync_cmp = {}
@@ -387,6 +395,40 @@ def run_extras(args, torch, cgx, runner, wl, sm, spec, chain, stream, sets, set_
                          "dataflow": ex.stats()["dataflow"], "n_deferred": ex.stats()["n_deferred"]}
         ex.close()
     out["sync_modes"] = sync_cmp
+    # NEXT-4: device-launched replays (transport DEVICE): one host call runs M replays; the host
+    # thread's CPU time per replay vs the host-driven loop on the same exec
+    try:
+        exd = chain.exec("INDIRECT", stream=stream, transport="DEVICE")
+        tab = torch.tensor([[t.data_ptr() for t in ts] for ts in sets], dtype=torch.int64, device=dev)
+        loop(exd.handle, 20)
+        host_us = min(timed(exd.handle, M) for _ in range(3))
+        stream.synchronize()
+        c0 = time.process_time()
+        loop(exd.handle, M)
+        c_host = (time.process_time() - c0) * 1e6 / M
+        stream.synchronize()
+
+        def dl():
+            e0_, e1_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            stream.synchronize()
+            with torch.cuda.stream(stream):
+                e0_.record(stream)
+                c0_ = time.process_time()
+                cgx.device_loop(exd.handle, tab.data_ptr(), N_SETS, M)
+                c1_ = time.process_time()
+                e1_.record(stream)
+            e1_.synchronize()
+            return e0_.elapsed_time(e1_) * 1e3 / M, (c1_ - c0_) * 1e6 / M
+        dl()
+        dev_us, c_dev = min(dl() for _ in range(3))
+        out["device_loop"] = {"us_per_replay_device_loop": dev_us, "us_per_replay_host_loop_same_exec": host_us,
+                              "host_cpu_us_per_replay_device_loop": c_dev,
+                              "host_cpu_us_per_replay_host_loop": c_host,
+                              "note": "NEXT-4: cgx_device_loop (scheduler kernel binds set i and tail-launches "
+                                      "the chain graph); host CPU = process time of the issuing thread"}
+        exd.close()
+    except Exception as exn:  # noqa: BLE001
+        out["device_loop"] = {"error": str(exn)}
     ex_e = chain.exec("EAGER", stream=stream)
     loop(ex_e.handle, 3)
     us_e = min(timed(ex_e.handle, 100) for _ in range(3))
@@ -395,10 +437,17 @@ def run_extras(args, torch, cgx, runner, wl, sm, spec, chain, stream, sets, set_
     best_ind = min((k for k in arms if k.startswith("indirect")), key=lambda k: arms[k]["rebind_delta_us"])
     d_copy = arms["copy"]["rebind_delta_us"]
     d_ind = arms[best_ind]["rebind_delta_us"]
+    # a Δ within the pair-to-pair noise is unresolved: the ratio is then a lower bound, computed
+    # with Δ_indirect raised to that noise (reported, never a division by ~0)
+    ind_res = max(d_ind, arms[best_ind]["rebind_delta_noise_us"], 0.05)
     out["arms"] = arms
     out["rebinding_us"] = {"copy": d_copy, "indirect": d_ind, "indirect_transport": best_ind,
                            "setparams": arms["setparams"]["rebind_delta_us"],
-                           "copy_over_indirect": (d_copy / d_ind) if d_ind > 0 else None,
+                           "copy_over_indirect": d_copy / ind_res,
+                           "copy_over_indirect_is_lower_bound": ind_res > d_ind,
+                           "copy_over_indirect_h2d": d_copy / max(arms["indirect_h2d"]["rebind_delta_us"],
+                                                                  arms["indirect_h2d"]["rebind_delta_noise_us"], 0.05),
+                           "indirect_noise_us": arms[best_ind]["rebind_delta_noise_us"],
                            "definition": "T_iter(bind+launch, fresh inputs from 8 rotating sets) - "
                                          "T_iter(graph launch, no rebinding, equally L2-cold inputs), "
                                          "device timeline, 2000 replays, best of 3 (DESIGN reading 14)",

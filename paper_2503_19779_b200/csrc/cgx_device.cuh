@@ -58,19 +58,21 @@ __device__ __forceinline__ void df_wait(const ElemArgs& a) {
       const uint32_t target = ep * a.df_ctas[i];
       const uint32_t* c = a.df_done + a.df_dep[i];
       uint64_t spins = 0;
-      while ((int32_t)(ld_acquire_u32(c) - target) < 0) {
+      // poll with relaxed loads (no L1 invalidation per poll), then one acquire fence below
+      while ((int32_t)(ld_relaxed_u32(c) - target) < 0) {
         if (++spins > (1ull << 28)) __trap();    // a lost signal would hang the box: fail loudly
       }
     }
+    asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
   }
   __syncthreads();
 }
+// bar.sync orders every thread's stores before thread 0's release; a release reduction (cumulative
+// over what thread 0 has observed) publishes them together with the count.
 __device__ __forceinline__ void df_signal(const ElemArgs& a) {
   __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(a.df_done + a.df_self, 1u);
-  }
+  if (threadIdx.x == 0)
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" :: "l"(a.df_done + a.df_self) : "memory");
 }
 
 // Plain (weak, L1-cached) 16-byte global load through an address that came from the pointer table

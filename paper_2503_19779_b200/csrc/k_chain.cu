@@ -143,6 +143,30 @@ __global__ void __launch_bounds__(kElemThreads) k_elem_f32(const __grid_constant
       o[i] = r;
     }
   }
+  // further tiles when the grid is capped below the tile count (grid-stride over tiles)
+  for (uint64_t b2 = base + (uint64_t)gridDim.x * (kElemThreads * kElemVec); b2 < n4;
+       b2 += (uint64_t)gridDim.x * (kElemThreads * kElemVec)) {
+#pragma unroll
+    for (int j = 0; j < kElemVec; ++j) {
+      const uint64_t i = b2 + (uint64_t)j * kElemThreads;
+      if (i < n4) {
+        xv[j] = ld_global_f4(x + i);
+        if (kBinary) yv[j] = ld_global_f4(y + i);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kElemVec; ++j) {
+      const uint64_t i = b2 + (uint64_t)j * kElemThreads;
+      if (i < n4) {
+        float4 r;
+        r.x = apply_f32<OP>(xv[j].x, yv[j].x, sval);
+        r.y = apply_f32<OP>(xv[j].y, yv[j].y, sval);
+        r.z = apply_f32<OP>(xv[j].z, yv[j].z, sval);
+        r.w = apply_f32<OP>(xv[j].w, yv[j].w, sval);
+        o[i] = r;
+      }
+    }
+  }
   // scalar tail (n not a multiple of 4): block 0 only
   if (blockIdx.x == 0) {
     const uint64_t t = (n4 << 2) + threadIdx.x;
@@ -224,8 +248,8 @@ __global__ void __launch_bounds__(kReduceThreads) k_reduce_sum_f32(const __grid_
   (void)p1;
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t rows = a.n / a.cols;
-  const uint64_t r = (uint64_t)blockIdx.x * (kReduceThreads / 32) + warp;
-  if (r < rows) {
+  for (uint64_t r = (uint64_t)blockIdx.x * (kReduceThreads / 32) + warp; r < rows;
+       r += (uint64_t)gridDim.x * (kReduceThreads / 32)) {
     const float4* row = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(p0) + r * a.cols);
     const uint32_t c4 = a.cols >> 2;
     double acc = 0.0;

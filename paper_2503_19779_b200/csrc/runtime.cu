@@ -405,6 +405,28 @@ static cgx_transport eff_transport(const cgx_exec_opts& o) {
 template <typename T>
 static T* argp(Launch& l) { return reinterpret_cast<T*>(l.args.p); }
 
+// Upper bound on the CTAs of an f32 elementwise / reduction node (the kernels grid-stride beyond
+// it). Every CTA of node k must have started before node k+1 can launch, so wide grids slow the
+// PDL launch cascade (scripts/launch_microbench.cu: 0.59 us per kernel at 148 CTAs, 0.82 at 512,
+// 1.45 at 1184). A dataflow replay is bound by that cascade, so there the grid is capped at one
+// CTA per SM (measured C2: 189 us uncapped, 172 us at 148, flat down to 64, 185 us at 16); a
+// serial chain is bound by each node's latency and keeps the full-width grid (C2 CHAIN: 249 us
+// uncapped, 270 us at 148). Env CGX_CHAIN_MAX_CTAS overrides both (diagnostics).
+static uint64_t chain_grid_cap(bool dataflow = false) {
+  static const int env = [] {
+    const char* v = getenv("CGX_CHAIN_MAX_CTAS");
+    return v ? std::max(1, atoi(v)) : 0;
+  }();
+  if (env) return (uint64_t)env;
+  if (!dataflow) return 1ull << 20;
+  static const int sms = [] {
+    int d = 0, n = 0;
+    cudaGetDevice(&d);
+    return cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d) == cudaSuccess && n > 0 ? n : 148;
+  }();
+  return (uint64_t)sms;
+}
+
 // Build the launch record of one node. Operand addresses are resolved for `mode`:
 // EXTERNAL -> placeholder (COPY), table index (INDIRECT), or a patchable field (others).
 // T5 (FIRST_NODE): launches 0..t5_pub of an INDIRECT exec take their external operands by value
@@ -512,7 +534,7 @@ static int build_launch(cgx_exec* e, int k, Launch& l) {
       if (n.op == CGX_OP_REDUCE_SUM) {
         l.func = kfn_reduce_sum_f32(twc);
         l.block = dim3(256);
-        l.grid = dim3((unsigned)std::max<uint64_t>(1, ceil_div(n.attr.n / n.attr.cols, 8)));
+        l.grid = dim3((unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ceil_div(n.attr.n / n.attr.cols, 8), chain_grid_cap())));
       } else {
         const int opi = n.op == CGX_OP_ADD ? 0 : n.op == CGX_OP_MUL ? 1 : n.op == CGX_OP_SCALE_IMM ? 2
                         : n.op == CGX_OP_SCALE_T ? 4 : 3;
@@ -521,7 +543,8 @@ static int build_launch(cgx_exec* e, int k, Launch& l) {
         l.block = dim3(elem_block_threads());
         const uint64_t per_vec = dt == 0 ? 4 : 8;
         const uint64_t nv = n.attr.n / per_vec;
-        l.grid = dim3((unsigned)std::max<uint64_t>(1, ceil_div(nv, (uint64_t)elem_block_threads() * 4)));
+        const uint64_t tiles = ceil_div(nv, (uint64_t)elem_block_threads() * 4);
+        l.grid = dim3((unsigned)std::max<uint64_t>(1, dt == 0 ? std::min<uint64_t>(tiles, chain_grid_cap()) : tiles));
       }
       return CGX_OK;
     }
@@ -675,6 +698,12 @@ static int set_sync_flags(cgx_exec* e) {
       }
     }
     if (ok) {
+      // narrower grids for the launch-cascade-bound dataflow replay (chain_grid_cap)
+      for (auto& l : e->L) {
+        const Node& n = e->c->nodes[l.node];
+        const bool f32 = e->c->slots[n.out].dtype == CGX_F32;
+        if (n.op == CGX_OP_REDUCE_SUM || f32) l.grid.x = (unsigned)std::min<uint64_t>(l.grid.x, chain_grid_cap(true));
+      }
       cudaError_t ce = cudaMalloc(&e->df_mem, sizeof(uint32_t) * (nl + 1));
       if (ce == cudaSuccess) ce = cudaMemset(e->df_mem, 0, sizeof(uint32_t) * (nl + 1));
       if (ce != cudaSuccess) return cuda_fail(ce, "dataflow counters", __LINE__);

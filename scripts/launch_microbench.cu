@@ -22,6 +22,51 @@ __global__ void k_chain(const __grid_constant__ P<PB> p) {
   if (i < p.n) p.out[i] = p.out[i] * (0.5f + V) + 1.0f;
 }
 
+// In-flight depth of the PDL cascade: each kernel triggers at entry, then busy-waits `ns`.
+__global__ void k_sleep(unsigned long long ns) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do { asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); } while (t - t0 < ns);
+}
+
+static double run_sleep(int K, int grid, unsigned long long ns, int reps) {
+  cudaStream_t s;
+  CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  cudaGraph_t g;
+  CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeGlobal));
+  for (int k = 0; k < K; ++k) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(32);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, k_sleep, ns));
+  }
+  CK(cudaStreamEndCapture(s, &g));
+  cudaGraphExec_t ge;
+  CK(cudaGraphInstantiate(&ge, g, 0));
+  for (int i = 0; i < 5; ++i) CK(cudaGraphLaunch(ge, s));
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaStreamSynchronize(s));
+  CK(cudaEventRecord(e0, s));
+  for (int i = 0; i < reps; ++i) CK(cudaGraphLaunch(ge, s));
+  CK(cudaEventRecord(e1, s));
+  CK(cudaEventSynchronize(e1));
+  float ms;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaGraphExecDestroy(ge);
+  cudaGraphDestroy(g);
+  cudaStreamDestroy(s);
+  return ms * 1e3 / reps / K;
+}
+
 // nfn distinct kernel functions used round-robin (instruction-cache / function-switch cost)
 template <int PB>
 static double run(int K, int grid, int block, int wait, int reps, float* buf, int nfn = 1) {
@@ -74,6 +119,12 @@ int main() {
   CK(cudaMemset(buf, 0, 64 << 20));
   const int K = 200, reps = 200;
   printf("K=%d kernels per graph, us per kernel\n", K);
+  printf("PDL cascade depth: kernels trigger at entry then run for T us (no wait)\n%6s %8s %8s %10s\n", "grid", "T_us", "us/kern", "T/us_kern");
+  for (int grid : {1, 16})
+    for (unsigned long long ns : {0ull, 500ull, 1000ull, 2000ull, 4000ull, 8000ull, 16000ull}) {
+      const double u = run_sleep(K, grid, ns, 50);
+      printf("%6d %8.1f %8.3f %10.2f\n", grid, ns / 1e3, u, ns / 1e3 / u);
+    }
   printf("function switching (params 160 B, block 256):\n%6s %5s %8s %8s\n", "grid", "wait", "1 fn", "3 fns");
   for (int wait = 0; wait <= 1; ++wait)
     for (int grid : {1, 16, 256})
