@@ -562,6 +562,13 @@ def run_extras(args, torch, cgx, runner, wl, sm, spec, chain, stream, sets, set_
 
     dom_nodes = [n for n in spec.nodes if n.op == dom_op]
     us_l, by_l = sub_roofline(dom_nodes)
+    # the same measurement per lane size: the latency floor at small sizes vs HBM at 4 MiB
+    by_size = []
+    for nsz in sorted({n.attrs["n"] for n in dom_nodes}):
+        grp = [n for n in dom_nodes if n.attrs["n"] == nsz]
+        u_, b_ = sub_roofline(grp)
+        by_size.append({"bytes_per_launch": b_, "launches": len(grp), "us_per_launch": u_,
+                        "GBps": b_ / (u_ * 1e-6) / 1e9})
     big = [n for n in dom_nodes if n.attrs["n"] == (4 << 20) // 4]
     us_b, by_b = sub_roofline(big) if big else (None, None)
     achieved = by_l / (us_l * 1e-6) / 1e9
@@ -579,6 +586,7 @@ def run_extras(args, torch, cgx, runner, wl, sm, spec, chain, stream, sets, set_
                        "algorithmic_bytes_per_launch": by_l, "avg_launch_us": us_l,
                        "largest_lanes_4MiB": ({"avg_launch_us": us_b, "algorithmic_bytes_per_launch": by_b,
                                                "achieved_GBps": by_b / (us_b * 1e-6) / 1e9} if big else None),
+                       "by_lane_size": by_size,
                        "peak_source": peak_src,
                        "timing": "CUDA events on the replay stream around 200 replays of a graph holding "
                                  "only this kernel's launches (same shapes, INDIRECT operands, no PDL); "

@@ -3,6 +3,8 @@
   python scripts/ncu_targets.py replay   # one C2 INDIRECT (FIRST_NODE) replay: 200 kernels
   python scripts/ncu_targets.py copy     # one COPY-arm bind at the C4 1 GiB point (copy kernel)
   python scripts/ncu_targets.py gemm     # one C3 (T=128, 1 layer) INDIRECT replay (tcgen05 GEMMs)
+  python scripts/ncu_targets.py replay_nopdl  # one C2 INDIRECT replay captured without PDL (the
+                                              # roofline's sub-graph configuration)
 """
 import os
 import sys
@@ -44,7 +46,7 @@ def main():
         spec = wl.c2_chain()
         mode, xp = "INDIRECT", "FIRST_NODE"
     chain = runner.Chain(spec, runner.upload_statics(spec, wl.static_values(spec), dev))
-    ex = chain.exec(mode, transport=xp)
+    ex = chain.exec(mode, transport=xp, no_pdl=(what == "replay_nopdl"))
     ts = fill(spec, dev, sh)
     torch.cuda.synchronize()
     ex.bind_ptrs([t.data_ptr() for t in ts])
