@@ -262,8 +262,9 @@ int cgx_debug_param_image(const cgx_exec* e, int pos, void* buf, uint64_t cap, u
  * STALE execs, and the by-value first node of FIRST_NODE). */
 int cgx_debug_ext_field_offsets(const cgx_exec* e, int pos, uint64_t* offs, int cap, int* n_out);
 /* Diagnostics: run GEMM launch `pos` once alone with per-CTA %globaltimer tracing; host_out gets
- * [cta][8] ns stamps (entry, setup done, first stage landed, last MMA committed, accumulator ready,
- * split partial published, all splits arrived, exit); n_out = CTA count. */
+ * [cta][16] ns stamps (0 entry, 1 setup done, 2 first stage landed, 3 last MMA issued, 4 stores
+ * issued, 5 split partial pushed, 6 all splits arrived, 7 exit, 8 accumulator ready, 9 accumulator
+ * in registers, 10 staged; 0 = not reached); n_out = CTA count. */
 int cgx_debug_gemm_trace(cgx_exec* e, int pos, uint64_t* host_out, int cap, int* n_out);
 /* Diagnostics: replay timeline of an exec created with CGX_NODE_TRACE=1 in the environment (chain
  * kernels only): host_out gets [launch][3] %globaltimer ns = (first CTA entry, last CTA past its

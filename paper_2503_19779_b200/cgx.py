@@ -258,9 +258,9 @@ def ext_field_offsets(ex: int, pos: int) -> list:
 
 def gemm_trace(ex: int, pos: int) -> list:
     n = C.c_int()
-    buf = (C.c_uint64 * (8 * 4096))()
-    _ck(LIB.cgx_debug_gemm_trace(ex, pos, buf, 8 * 4096, C.byref(n)), "cgx_debug_gemm_trace")
-    return [list(buf[8 * i: 8 * i + 8]) for i in range(n.value)]
+    buf = (C.c_uint64 * (16 * 4096))()
+    _ck(LIB.cgx_debug_gemm_trace(ex, pos, buf, 16 * 4096, C.byref(n)), "cgx_debug_gemm_trace")
+    return [list(buf[16 * i: 16 * i + 16]) for i in range(n.value)]
 
 
 def device_loop(ex: int, d_ptr_sets: int, n_sets: int, n_replays: int) -> None:

@@ -19,7 +19,9 @@
 #include <cudaTypedefs.h>
 #include <stdint.h>
 
+#include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 #include "../../include/cgx.h"
@@ -30,11 +32,9 @@ namespace cgx {
 
 static constexpr int kBM = 128;
 static constexpr int kBK = 64;          // 64 bf16 = 128 B = one swizzle-128B row
-// Stage count per N tile (4: deeper rings measured no faster at the C3 shapes, profiles/r01).
-template <int BN>
-struct Stages {
-  static constexpr int value = 4;
-};
+// Operand ring depth: min(4, k-blocks per CTA) (deeper rings measured no faster at the C3 shapes,
+// profiles/r01); a shallow ring keeps split-K CTAs small enough for two per SM.
+static constexpr int kMaxStages = 4;
 static constexpr int kGemmThreads = 192;
 static constexpr uint32_t kGemmTriggerAfterWait = 1u << 8;   // internal flag bit (above CGX_GEMM_*)
 
@@ -48,6 +48,7 @@ struct alignas(64) GemmArgs {
   unsigned long long* cnt;    // per-tile monotonic arrival counters (split > 1)
   uint32_t M, N, K, flags;
   uint32_t split;             // K splits (gridDim.z)
+  uint32_t stages;            // operand ring depth (<= kMaxStages)
   unsigned long long* trace;  // optional per-CTA %globaltimer trace [cta][8] (diagnostics)
 };
 
@@ -115,16 +116,24 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+// TMEM load without the wait: callers batch several, then tmem_wait_regs() once.
+__device__ __forceinline__ void tmem_ld16_nw(uint32_t taddr, float* v) {
   uint32_t r[16];
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
         "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+// tcgen05.wait::ld, then pin every loaded register behind it (empty volatile asms keep their order
+// relative to the wait, so no use of v can be hoisted above it).
+template <int N>
+__device__ __forceinline__ void tmem_wait_regs(float* v) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < N; ++i) asm volatile("" : "+f"(v[i]));
 }
 
 __device__ __forceinline__ void trace_at(const GemmArgs& a, int slot) {
@@ -132,79 +141,51 @@ __device__ __forceinline__ void trace_at(const GemmArgs& a, int slot) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     const uint32_t cta = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-    a.trace[cta * 8 + slot] = t;
+    a.trace[cta * 16 + slot] = t;
   }
 }
 
+// tanh-approximate GELU with the hardware tanh (MUFU.TANH, max rel. error ~2^-11, far inside the
+// bf16 output rounding of 2^-8): libm tanhf made the FC1 epilogue ~2 us of ALU work per CTA.
+__device__ __forceinline__ float tanh_fast(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ float gelu_tanh(float x) {
   const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-  return 0.5f * x * (1.0f + tanhf(k0 * (x + k1 * x * x * x)));
+  return 0.5f * x * (1.0f + tanh_fast(k0 * (x + k1 * x * x * x)));
 }
 
 // ------------------------------------------------------------------ kernel
-// Split-K (gridDim.z = split, launched as thread-block clusters (1, 1, split)): CTA z accumulates
-// k-blocks [z*nk/split, (z+1)*nk/split) in TMEM, parks its fp32 partial tile in its own shared
-// memory, and after a cluster barrier reduces 1/split of the tile over DSMEM in fixed split order
-// (deterministic, no float atomics, no global workspace) before running the epilogue on it. At M = 128 every N tile re-reads the whole A panel, so without split-K the per-CTA
-// bytes (up to 128 x 3072 x 2 for FC2) bound the kernel; split-K spreads them over ~148 CTAs.
-__device__ __forceinline__ void epilogue_store(const GemmArgs& a, int m, int n, float* v) {
-  if (a.flags & CGX_GEMM_BIAS) {
-    const uint4* bp = reinterpret_cast<const uint4*>(a.bias + n);
-    const uint4 b0 = __ldg(bp), b1 = __ldg(bp + 1);
-    const __nv_bfloat16* bb0 = reinterpret_cast<const __nv_bfloat16*>(&b0);
-    const __nv_bfloat16* bb1 = reinterpret_cast<const __nv_bfloat16*>(&b1);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      v[i] += __bfloat162float(bb0[i]);
-      v[8 + i] += __bfloat162float(bb1[i]);
-    }
-  }
-  if (a.flags & CGX_GEMM_GELU) {
-#pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = gelu_tanh(v[i]);
-  }
-  if (a.flags & CGX_GEMM_RESIDUAL) {
-    const uint4* rp = reinterpret_cast<const uint4*>(a.residual + (size_t)m * a.N + n);
-    const uint4 r0 = rp[0], r1 = rp[1];
-    const __nv_bfloat16* rb0 = reinterpret_cast<const __nv_bfloat16*>(&r0);
-    const __nv_bfloat16* rb1 = reinterpret_cast<const __nv_bfloat16*>(&r1);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      v[i] += __bfloat162float(rb0[i]);
-      v[8 + i] += __bfloat162float(rb1[i]);
-    }
-  }
-  uint4 o[2];
-  __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(o);
-#pragma unroll
-  for (int i = 0; i < 16; ++i) ob[i] = __float2bfloat16_rn(v[i]);
-  uint4* op = reinterpret_cast<uint4*>(a.out + (size_t)m * a.N + n);
-  op[0] = o[0];
-  op[1] = o[1];
-}
+// Split-K (gridDim.z = S, launched as thread-block clusters (1, 1, S)): CTA z accumulates the
+// k-blocks [nk*z/S, nk*(z+1)/S) in TMEM. The output rows of the tile are partitioned over the S
+// CTAs (CTA o owns rows [ceil(128 o/S), ceil(128 (o+1)/S))). Each CTA stages its fp32 partial tile
+// in its (now idle) operand ring, then pushes every peer owner's row block into that owner's
+// receive slot z with ONE bulk shared::cta -> shared::cluster copy that completes bytes on the
+// owner's receive mbarrier (expect_tx armed at init). The owner sums the S slots of its rows in
+// fixed split order 0..S-1 (deterministic, no float atomics, no global workspace; its own slot is
+// read from its staging tile) and runs the epilogue. Cluster barriers: phase 0 publishes the
+// receive mbarriers' initialisation (armed at entry, waited just before the first push); phase 1
+// is arrived at as soon as a CTA's incoming copies are complete and waited on at exit, so no CTA
+// releases a staging tile a peer is still copying from. (Per-thread st.async pushes of 16 B each
+// measured slower for BN >= 64: the DSMEM transaction rate bounds them.)
+__host__ __device__ constexpr uint32_t split_row_lo(uint32_t z, uint32_t S) { return (128u * z + S - 1) / S; }
+__host__ __device__ constexpr uint32_t split_rows_max(uint32_t S) { return (128u + S - 1) / S; }
 
-__device__ __forceinline__ void epilogue_store4(const GemmArgs& a, int m, int n, float4 acc, uint2 bu) {
-  float v[4] = {acc.x, acc.y, acc.z, acc.w};
-  if (a.flags & CGX_GEMM_BIAS) {
-    const __nv_bfloat16* bb = reinterpret_cast<const __nv_bfloat16*>(&bu);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) v[i] += __bfloat162float(bb[i]);
-  }
-  if (a.flags & CGX_GEMM_GELU) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) v[i] = gelu_tanh(v[i]);
-  }
-  if (a.flags & CGX_GEMM_RESIDUAL) {
-    const uint2 ru = *reinterpret_cast<const uint2*>(a.residual + (size_t)m * a.N + n);
-    const __nv_bfloat16* rb = reinterpret_cast<const __nv_bfloat16*>(&ru);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) v[i] += __bfloat162float(rb[i]);
-  }
-  uint2 o;
-  __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(&o);
-#pragma unroll
-  for (int i = 0; i < 4; ++i) ob[i] = __float2bfloat16_rn(v[i]);
-  *reinterpret_cast<uint2*>(a.out + (size_t)m * a.N + n) = o;
+__device__ __forceinline__ void bulk_s2dsmem(uint32_t rdst, uint32_t src, uint32_t bytes, uint32_t rbar) {
+  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   rdst),
+               "r"(src), "r"(bytes), "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+__device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t cta) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(saddr), "r"(cta));
+  return r;
 }
 
 template <int BN>
@@ -212,15 +193,28 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
   constexpr uint32_t kABytes = kBM * kBK * 2;     // 16 KiB
   constexpr uint32_t kBBytes = BN * kBK * 2;
   constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
-  constexpr int kStages = Stages<BN>::value;
+  const int kStages = (int)a.stages;
+  constexpr uint32_t kRowF = BN + 4;              // partial-tile row stride (floats): 16-B aligned, bank-spread
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B alignment (SWIZZLE_128B) by offsetting the __shared__ array itself, so every derived
+  // pointer stays in the shared address space (LDS/STS; a uintptr_t round trip made them generic)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const uint32_t S = a.split;
+  const uint32_t z = blockIdx.z;                   // cluster (1,1,S) over gridDim.z == S: rank == z
+  const uint32_t rows_max = split_rows_max(S);
   uint8_t* sA = smem;
   uint8_t* sB = smem + kStages * kABytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + kStages * kBBytes);
+  // The operand ring doubles as the epilogue staging area once the MMAs are done: the fp32
+  // partial tile [128][kRowF] (split-K).
+  const uint32_t ring_bytes = kStages * (kABytes + kBBytes);
+  const uint32_t stage_bytes = S > 1 ? 128u * kRowF * 4u : 0u;
+  float* recv = reinterpret_cast<float*>(smem + (ring_bytes > stage_bytes ? ring_bytes : stage_bytes));  // [S][rows_max][kRowF]
+  float* sbias = recv + (S > 1 ? S * rows_max * kRowF : 0);                     // [BN] fp32 bias slice
+  uint64_t* full = reinterpret_cast<uint64_t*>(sbias + BN);
   uint64_t* empty = full + kStages;
   uint64_t* tmem_full = empty + kStages;
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* recv_full = tmem_full + 1;
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(recv_full + 1);
 
   if (threadIdx.x == 0) trace_at(a, 0);
   const bool late_trigger = a.flags & kGemmTriggerAfterWait;
@@ -228,8 +222,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n0 = blockIdx.x * BN;
   const int m0 = blockIdx.y * kBM;
-  const int kps = (int)(a.K / kBK / a.split);     // k-blocks per split
-  const int kbase = (int)blockIdx.z * kps;
+  const int nk = (int)(a.K / kBK);
+  const int kbase = (int)((uint32_t)nk * z / S);
+  const int kps = (int)((uint32_t)nk * (z + 1) / S) - kbase;   // k-blocks of this split (>= 1)
+  const uint32_t my_lo = split_row_lo(z, S), my_rows = split_row_lo(z + 1, S) - my_lo;
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&a.tmA);
@@ -239,6 +235,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
       mbar_init(&empty[s], 1);
     }
     mbar_init(tmem_full, 1);
+    if (S > 1) {
+      mbar_init(recv_full, 1);
+      // armed now, before the cluster barrier that lets peers push: one arrival + the peers' bytes
+      mbar_expect_tx(recv_full, (S - 1) * my_rows * kRowF * 4u);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 1) {   // TMEM allocation (whole warp), address published through shared memory
@@ -249,6 +250,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (threadIdx.x == 0) trace_at(a, 1);
+  if (S > 1) asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
   const uint32_t tmem = *s_tmem;
 
   if (warp == 0) {
@@ -293,100 +296,158 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
       trace_at(a, 3);
     }
   } else {
-    // ---- epilogue warps (128 threads): TMEM -> registers -> [split-K reduction] -> epilogue
-    mbar_wait(tmem_full, 0);
-    tc_fence_after();
+    // ---- epilogue warps (128 threads): TMEM -> registers -> [split-K push/reduce] -> epilogue.
+    // Everything the epilogue reads from global memory is fetched BEFORE the accumulator is ready:
+    // the bias slice (STATIC) into shared memory pre-wait, the residual (written by an earlier
+    // node) into registers right after this thread's own griddepcontrol.wait. The TMEM row is
+    // read with all tcgen05.ld in flight behind one wait. (Serial per-chunk global loads after
+    // the MMA cost ~0.5 us each, measured with the phase tracer.)
     const uint32_t q = warp & 3;                  // TMEM lane quarter this warp may access
     const uint32_t row = q * 32 + lane;
-    const int m = m0 + (int)row;
-    const bool live = m < (int)a.M;
-    if (a.split == 1) {
+    const uint32_t et = threadIdx.x - 64;          // epilogue thread 0..127
+    const bool has_bias = a.flags & CGX_GEMM_BIAS, has_res = a.flags & CGX_GEMM_RESIDUAL;
+    const bool gelu = a.flags & CGX_GEMM_GELU;
+    for (uint32_t i = et; i < (uint32_t)BN; i += 128u)
+      sbias[i] = has_bias ? __bfloat162float(a.bias[n0 + i]) : 0.f;
+    constexpr uint32_t kQRow = BN / 4;             // 4-column quads per tile row
+    constexpr int kQMax = BN / 8;                  // quads per thread in the split reduction (rows_max <= 64)
+    uint4 res_row[BN / 8];                         // S == 1: this thread's residual row (bf16 x 8 per uint4)
+    uint2 res_q[kQMax];                            // S > 1: the residual quads this thread outputs
+    if (has_res) {
+      pdl_wait();
+      if (S == 1) {
+        const int m = m0 + (int)row;
+        if (m < (int)a.M) {
+          const uint4* rp = reinterpret_cast<const uint4*>(a.residual + (size_t)m * a.N + n0);
 #pragma unroll
-      for (int c0 = 0; c0 < BN; c0 += 16) {
-        float v[16];
-        tmem_ld16(tmem + ((q * 32u) << 16) + (uint32_t)c0, v);
-        if (live) epilogue_store(a, m, n0 + c0, v);
+          for (int i = 0; i < BN / 8; ++i) res_row[i] = rp[i];
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < kQMax; ++j) {
+          const uint32_t qi = et + 128u * j;
+          if (qi < my_rows * kQRow) {
+            const int mr = m0 + (int)(my_lo + qi / kQRow);
+            if (mr < (int)a.M)
+              res_q[j] = *reinterpret_cast<const uint2*>(a.residual + (size_t)mr * a.N + n0 + 4 * (qi % kQRow));
+          }
+        }
       }
-    } else {
-      // split-K: park this split's fp32 partial tile in OWN shared memory (the operand ring is
-      // idle now): row-major [128][BN + 4] floats (padding keeps the 16-B column accesses of a
-      // quarter warp on distinct banks)
-      float* sP = reinterpret_cast<float*>(smem);
-#pragma unroll
-      for (int c0 = 0; c0 < BN; c0 += 16) {
-        float v[16];
-        tmem_ld16(tmem + ((q * 32u) << 16) + (uint32_t)c0, v);
-        float4* d = reinterpret_cast<float4*>(sP + row * (BN + 4) + c0);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) d[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-      }
-      if (threadIdx.x == 64) trace_at(a, 5);
     }
-  }
-  if (a.split > 1) {
-    // The S splits of a tile form one thread-block cluster (1, 1, S). After a cluster barrier
-    // every CTA reduces 1/S of the tile, reading the S partials from the CTAs' shared memory
-    // (DSMEM) in fixed split order 0..S-1 — deterministic, no global round trips or atomics —
-    // then runs the epilogue on it. A second barrier keeps every partial alive until all reads
-    // are done.
-    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-    if (threadIdx.x == 64) trace_at(a, 6);
-    if (warp >= 2) {
-      const uint32_t S = a.split;
-      const uint32_t my_rank = blockIdx.z;          // cluster (1,1,S) over gridDim.z == S
-      constexpr uint32_t kQuads = kBM * BN / 4;
-      const uint32_t q_lo = (uint32_t)((uint64_t)kQuads * my_rank / S);
-      const uint32_t q_hi = (uint32_t)((uint64_t)kQuads * (my_rank + 1) / S);
-      const uint32_t et = threadIdx.x - 64;          // epilogue thread 0..127
-      const uint32_t local = smem_u32(smem);
-      // this thread's quads: q_lo + et + 128 j, j < kQMax (<= BN/8 for any split >= 1)
-      constexpr int kQMax = BN / 8;
-      uint32_t offs[kQMax];
-      bool have[kQMax];
-      uint2 bias_q[kQMax];
-      float4 acc[kQMax];
+    asm volatile("bar.sync 1, 128;\n" ::: "memory");   // bias slice staged
+    mbar_wait(tmem_full, 0);
+    tc_fence_after();
+    if (threadIdx.x == 64) trace_at(a, 8);
+    float v[BN];
 #pragma unroll
-      for (int j = 0; j < kQMax; ++j) {
-        const uint32_t qi = q_lo + et + 128u * j;
-        have[j] = qi < q_hi;
-        const uint32_t r = qi / (BN / 4), c = 4 * (qi % (BN / 4));
-        offs[j] = (r * (BN + 4) + c) * 4;
-        acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-        bias_q[j] = make_uint2(0u, 0u);
-        if (have[j] && (a.flags & CGX_GEMM_BIAS)) bias_q[j] = __ldg(reinterpret_cast<const uint2*>(a.bias + n0 + c));
-      }
-      for (uint32_t z = 0; z < S; ++z) {            // fixed split order: deterministic sums
-        float4 t[kQMax];
+    for (int c0 = 0; c0 < BN; c0 += 16) tmem_ld16_nw(tmem + ((q * 32u) << 16) + (uint32_t)c0, v + c0);
+    tmem_wait_regs<BN>(v);
+    if (threadIdx.x == 64) trace_at(a, 9);
+    if (S == 1) {
+      // bias / GELU / residual in registers, 16-B stores straight from registers (measured faster
+      // than staging the tile and bulk-storing rows: the bulk store's read-completion wait is ~1 us)
+      const int m = m0 + (int)row;
+      if (m < (int)a.M) {
+        uint4* op = reinterpret_cast<uint4*>(a.out + (size_t)m * a.N + n0);
 #pragma unroll
-        for (int j = 0; j < kQMax; ++j) {           // all of this split's loads in flight at once
-          if (have[j]) {
-            uint32_t remote;
-            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(remote) : "r"(local + offs[j]), "r"(z));
-            asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];\n"
-                         : "=f"(t[j].x), "=f"(t[j].y), "=f"(t[j].z), "=f"(t[j].w) : "r"(remote));
+        for (int c8 = 0; c8 < BN / 8; ++c8) {
+          const float4 b0 = *reinterpret_cast<const float4*>(sbias + 8 * c8);
+          const float4 b1 = *reinterpret_cast<const float4*>(sbias + 8 * c8 + 4);
+          const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+          for (int i = 0; i < 8; ++i) v[8 * c8 + i] += bb[i];
+        }
+        if (gelu) {
+#pragma unroll
+          for (int i = 0; i < BN; ++i) v[i] = gelu_tanh(v[i]);
+        }
+        if (has_res) {
+#pragma unroll
+          for (int c8 = 0; c8 < BN / 8; ++c8) {
+            const __nv_bfloat16* rb = reinterpret_cast<const __nv_bfloat16*>(&res_row[c8]);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v[8 * c8 + i] += __bfloat162float(rb[i]);
           }
         }
 #pragma unroll
-        for (int j = 0; j < kQMax; ++j)
-          if (have[j]) {
-            acc[j].x += t[j].x;
-            acc[j].y += t[j].y;
-            acc[j].z += t[j].z;
-            acc[j].w += t[j].w;
-          }
+        for (int c8 = 0; c8 < BN / 8; ++c8) {
+          uint4 o;
+          __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(&o);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) ob[i] = __float2bfloat16_rn(v[8 * c8 + i]);
+          op[c8] = o;
+        }
       }
-      if (threadIdx.x == 64) trace_at(a, 1);
+      if (threadIdx.x == 64) trace_at(a, 4);
+    } else {
+      // stage this row of the partial tile locally, then one thread per peer owner pushes that
+      // owner's row block to its receive slot z with a single bulk DSMEM copy (complete_tx on
+      // the owner's receive barrier). Own rows are reduced straight from the staging tile.
+      float* stg = reinterpret_cast<float*>(smem);
+      {
+        float4* d4 = reinterpret_cast<float4*>(stg + row * kRowF);
+#pragma unroll
+        for (int i = 0; i < BN / 4; ++i) d4[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+      }
+      fence_proxy_async_smem();
+      if (threadIdx.x == 64) trace_at(a, 10);
+      asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");   // peers' receive barriers are armed
+      asm volatile("bar.sync 1, 128;\n" ::: "memory");                         // staging tile complete
+      if (et < S && et != z) {
+        const uint32_t o = et, lo = split_row_lo(o, S), n = split_row_lo(o + 1, S) - lo;
+        bulk_s2dsmem(mapa(smem_u32(recv + (size_t)z * rows_max * kRowF), o), smem_u32(stg + lo * kRowF),
+                     n * kRowF * 4u, mapa(smem_u32(recv_full), o));
+      }
+      if (threadIdx.x == 64) trace_at(a, 5);
+      mbar_wait(recv_full, 0);                            // every peer's rows have landed
+      // our incoming copies are complete (so the peers' staging reads are done): release them
+      asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+      if (threadIdx.x == 64) trace_at(a, 6);
+      const uint32_t nq = my_rows * kQRow;
 #pragma unroll
       for (int j = 0; j < kQMax; ++j) {
-        if (!have[j]) continue;
-        const uint32_t qi = q_lo + et + 128u * j;
-        const uint32_t r = qi / (BN / 4), c = 4 * (qi % (BN / 4));
-        const int mr = m0 + (int)r;
-        if (mr < (int)a.M) epilogue_store4(a, mr, n0 + (int)c, acc[j], bias_q[j]);
+        const uint32_t qi = et + 128u * j;
+        if (qi >= nq) break;
+        const uint32_t r = qi / kQRow, c = 4u * (qi % kQRow);
+        const int mr = m0 + (int)(my_lo + r);
+        const float* src = recv + (size_t)r * kRowF + c;
+        const float* own = stg + (size_t)(my_lo + r) * kRowF + c;
+        float4 acc = *reinterpret_cast<const float4*>(z == 0 ? own : src);
+        for (uint32_t zz = 1; zz < S; ++zz) {        // fixed split order: deterministic sums
+          const float4 t = *reinterpret_cast<const float4*>(zz == z ? own : src + (size_t)zz * rows_max * kRowF);
+          acc.x += t.x;
+          acc.y += t.y;
+          acc.z += t.z;
+          acc.w += t.w;
+        }
+        if (mr >= (int)a.M) continue;
+        float w[4] = {acc.x + sbias[c], acc.y + sbias[c + 1], acc.z + sbias[c + 2], acc.w + sbias[c + 3]};
+        if (gelu) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) w[i] = gelu_tanh(w[i]);
+        }
+        if (has_res) {
+          const __nv_bfloat16* rb = reinterpret_cast<const __nv_bfloat16*>(&res_q[j]);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) w[i] += __bfloat162float(rb[i]);
+        }
+        uint2 ov;
+        __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(&ov);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) ob[i] = __float2bfloat16_rn(w[i]);
+        *reinterpret_cast<uint2*>(a.out + (size_t)mr * a.N + n0 + c) = ov;
       }
       if (threadIdx.x == 64) trace_at(a, 4);
     }
-    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  }
+  if (S > 1) {
+    // phase 0 (receive barriers armed) for the non-epilogue warps; phase 1: no CTA exits before
+    // every peer has received the rows it copied out of this CTA's staging tile
+    if (warp < 2) {
+      asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+      asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+    }
+    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
   }
   tc_fence_before();
   __syncthreads();
@@ -423,29 +484,58 @@ static int encode_kmajor(CUtensorMap* tm, const void* base, uint64_t rows, uint6
   return r == CUDA_SUCCESS ? CGX_OK : CGX_E_CUDA;
 }
 
-// Tiling (measured per C3 shape with scripts/diag_gemm_tiling.py, profiles/r01/gemm_tiling.txt):
-// BN = 32 everywhere; no split-K when there are already >= 64 N tiles (the DSMEM reduction costs
-// more than the smaller A slice saves), else the largest split S <= 4 dividing the k-block count
-// with tiles * S <= 148 (one wave; the S CTAs of a tile form a thread-block cluster).
-static void pick_tiling(uint32_t M, uint32_t N, uint32_t K, int* bn_out, uint32_t* split_out) {
-  const char* env_bn = getenv("CGX_GEMM_BN");          // measurement knobs
-  const char* env_ms = getenv("CGX_GEMM_MAXSPLIT");
-  int bn = (N % 32 == 0) ? 32 : 64;
-  if (env_bn && N % atoi(env_bn) == 0) bn = atoi(env_bn);
-  const uint32_t tiles = (N / bn) * ((M + kBM - 1) / kBM);
-  const uint32_t nk = K / kBK;
-  uint32_t max_split = env_ms ? (uint32_t)atoi(env_ms) : (tiles >= 64 ? 1u : 4u);
-  uint32_t best = 1;
-  for (uint32_t sp = 1; sp <= max_split && sp <= 8 && sp <= nk; ++sp)
-    if (nk % sp == 0 && tiles * sp <= 148) best = sp;
-  *bn_out = bn;
-  *split_out = best;
+// Tiling. Every CTA of an M = 128 GEMM streams its A panel slice through its SM, so per-SM operand
+// ingress (k-blocks per CTA x (16 KiB of A + BN x 128 B of W)) and the serial latency chain (first
+// TMA, MMA, epilogue) bound it; split-K cuts the ingress S-fold at the price of the push
+// reduction. Rule measured on the deployed C3 replay (scripts/diag_c3_tiling.py,
+// profiles/r01/c3_tiling.txt: 562 -> 514 us per 12-layer replay): BN = 32, and the largest
+// S in {1, 2, 4, 8} with tiles x S <= 192 CTAs (up to two co-resident per SM) and >= 3 k-blocks
+// per split. CGX_GEMM_TILING / CGX_GEMM_BN / CGX_GEMM_SPLIT pin a tiling for measurement.
+static uint32_t split_rows_max_h(uint32_t S) { return (128u + S - 1) / S; }
+
+static size_t smem_bytes(int bn, uint32_t S, uint32_t stages) {
+  const size_t recv = S > 1 ? (size_t)S * split_rows_max_h(S) * (bn + 4) * 4 : 0;
+  size_t ring = stages * (size_t)(kBM * kBK * 2 + bn * kBK * 2);
+  const size_t stage = S > 1 ? (size_t)128 * (bn + 4) * 4 : 0;
+  if (stage > ring) ring = stage;
+  return 1024 + ring + recv + bn * 4 + (2 * stages + 2) * 8 + 16;
+}
+static uint32_t ring_stages(uint32_t nk, uint32_t S) {
+  const uint32_t kps = (nk + S - 1) / S;
+  return kps < (uint32_t)kMaxStages ? kps : (uint32_t)kMaxStages;
 }
 
-template <int BN>
-static size_t smem_bytes() {
-  constexpr int kStages = Stages<BN>::value;
-  return 1024 + kStages * (kBM * kBK * 2 + BN * kBK * 2) + (2 * kStages + 1) * 8 + 16;
+static void pick_tiling(uint32_t M, uint32_t N, uint32_t K, int* bn_out, uint32_t* split_out) {
+  // CGX_GEMM_TILING="NxK=BN/S,..." pins a tiling per shape (measurement knob)
+  if (const char* t = getenv("CGX_GEMM_TILING")) {
+    char key[32];
+    snprintf(key, sizeof key, "%ux%u=", N, K);
+    if (const char* p = strstr(t, key)) {
+      int bn = 0, sp = 0;
+      if (sscanf(p + strlen(key), "%d/%d", &bn, &sp) == 2 && (bn == 32 || bn == 64 || bn == 128) && N % bn == 0 &&
+          sp >= 1 && sp <= 16 && (uint32_t)sp <= K / kBK) {
+        *bn_out = bn;
+        *split_out = (uint32_t)sp;
+        return;
+      }
+    }
+  }
+  const char* env_bn = getenv("CGX_GEMM_BN");          // measurement knobs
+  const char* env_sp = getenv("CGX_GEMM_SPLIT");
+  const uint32_t nk = K / kBK;
+  int bn = 32;
+  if (env_bn && (atoi(env_bn) == 32 || atoi(env_bn) == 64 || atoi(env_bn) == 128) && N % atoi(env_bn) == 0)
+    bn = atoi(env_bn);
+  const uint32_t tiles = (N / bn) * ((M + kBM - 1) / kBM);
+  uint32_t sp = 1;
+  if (env_sp && atoi(env_sp) >= 1 && (uint32_t)atoi(env_sp) <= nk && atoi(env_sp) <= 16) {
+    sp = (uint32_t)atoi(env_sp);
+  } else {
+    for (uint32_t c = 2; c <= 8; c *= 2)
+      if (tiles * c <= 192 && nk >= 3 * c) sp = c;
+  }
+  *bn_out = bn;
+  *split_out = sp;
 }
 
 void decoder_gemm_plan(uint32_t, uint32_t, uint32_t, size_t* ws_bytes, size_t* cnt_bytes) {
@@ -458,10 +548,14 @@ template <int BN>
 static const void* setup_kernel() {
   static std::once_flag once;
   std::call_once(once, [] {
-    cudaFuncSetAttribute(k_gemm_bf16<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<BN>());
+    cudaFuncSetAttribute(k_gemm_bf16<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(k_gemm_bf16<BN>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   });
   return (const void*)k_gemm_bf16<BN>;
+}
+
+static const void* kernel_for(int bn) {
+  return bn == 128 ? setup_kernel<128>() : bn == 64 ? setup_kernel<64>() : setup_kernel<32>();
 }
 
 void decoder_gemm_set_trace(void* args, unsigned long long* trace) {
@@ -484,15 +578,11 @@ int decoder_gemm_build(uint32_t M, uint32_t N, uint32_t K, uint32_t flags, const
   uint32_t sp = 1;
   pick_tiling(M, N, K, &bn, &sp);
   *argbytes = sizeof(GemmArgs);
+  const uint32_t stages = ring_stages(K / kBK, sp);
   *grid = dim3(N / bn, (M + kBM - 1) / kBM, sp);
   *block = dim3(kGemmThreads);
-  if (bn == 64) {
-    *smem = smem_bytes<64>();
-    *func = setup_kernel<64>();
-  } else {
-    *smem = smem_bytes<32>();
-    *func = setup_kernel<32>();
-  }
+  *smem = smem_bytes(bn, sp, stages);
+  *func = kernel_for(bn);
   if (!args_out) return CGX_OK;
   if (get_encode() != CGX_OK) return CGX_E_CUDA;
   GemmArgs* g = static_cast<GemmArgs*>(args_out);
@@ -508,6 +598,7 @@ int decoder_gemm_build(uint32_t M, uint32_t N, uint32_t K, uint32_t flags, const
   g->K = K;
   g->flags = flags;
   g->split = sp;
+  g->stages = stages;
   g->trace = nullptr;
 
   return CGX_OK;

@@ -1585,16 +1585,17 @@ extern "C" int cgx_debug_node_trace(cgx_exec* e, uint64_t* host_out, int cap, in
 }
 
 // Diagnostics: launch GEMM node `pos` once, alone (no PDL), with per-CTA %globaltimer tracing;
-// host_out receives [cta][8] ns timestamps (entry, setup, first stage landed, last MMA committed,
-// accumulator ready, partial published, all splits arrived, exit).
+// host_out receives [cta][16] ns timestamps (0 entry, 1 setup done, 2 first stage landed, 3 last MMA
+// issued, 4 stores issued, 5 partial pushed, 6 all splits arrived, 7 exit, 8 accumulator ready,
+// 9 accumulator in registers, 10 staged).
 extern "C" int cgx_debug_gemm_trace(cgx_exec* e, int pos, uint64_t* host_out, int cap, int* n_out) {
   if (!e || pos < 0 || pos >= (int)e->L.size() || !n_out) return fail(CGX_E_INVALID_ARG, "gemm_trace: bad argument");
   Launch& l = e->L[pos];
   if (e->c->nodes[l.node].op != CGX_OP_GEMM_BF16) return fail(CGX_E_INVALID_ARG, "gemm_trace: not a GEMM node");
   const int ctas = (int)(l.grid.x * l.grid.y * l.grid.z);
   unsigned long long* d = nullptr;
-  CK(cudaMalloc(&d, sizeof(unsigned long long) * 8 * ctas));
-  CK(cudaMemset(d, 0, sizeof(unsigned long long) * 8 * ctas));
+  CK(cudaMalloc(&d, sizeof(unsigned long long) * 16 * ctas));
+  CK(cudaMemset(d, 0, sizeof(unsigned long long) * 16 * ctas));
   Launch t;
   t.func = l.func;
   t.grid = l.grid;
@@ -1609,7 +1610,7 @@ extern "C" int cgx_debug_gemm_trace(cgx_exec* e, int pos, uint64_t* host_out, in
   if (st == CGX_OK) {
     cudaError_t ce = cudaStreamSynchronize(e->s);
     if (ce == cudaSuccess && host_out)
-      ce = cudaMemcpy(host_out, d, sizeof(uint64_t) * std::min(cap, 8 * ctas), cudaMemcpyDeviceToHost);
+      ce = cudaMemcpy(host_out, d, sizeof(uint64_t) * std::min(cap, 16 * ctas), cudaMemcpyDeviceToHost);
     if (ce != cudaSuccess) st = cuda_fail(ce, "gemm_trace", __LINE__);
   }
   cudaFree(d);

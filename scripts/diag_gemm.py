@@ -13,7 +13,7 @@ chain = runner.Chain(spec, runner.upload_statics(spec, wl.static_values(spec), d
 ex = chain.exec("COPY")
 x = runner.host_to_device(wl.slot_values(spec, "x", 0), "bf16", dev)
 ex.bind({"x": x}); ex.launch(); torch.cuda.synchronize()
-names = ["entry", "reduced", "stage0", "mma_done", "stored", "published", "arrived", "exit"]
+names = ["entry", "setup", "stage0", "mma_issued", "stored", "pushed", "arrived", "exit", "acc_ready", "acc_regs", "staged"]
 for pos, node in enumerate(spec.nodes):
     if node.op != "GEMM_BF16":
         continue

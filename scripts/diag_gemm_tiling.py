@@ -25,7 +25,11 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
     print(json.dumps(out))
     chain.close()
 else:
-    for bn, ms in (("64", "8"), ("32", "8"), ("32", "1"), ("64", "1"), ("32", "2"), ("64", "2"), ("32", "4"), ("64", "4")):
-        env = dict(os.environ, CGX_GEMM_BN=bn, CGX_GEMM_MAXSPLIT=ms)
+    # default (model-picked) tiling first, then forced (BN, split) pairs
+    combos = [(None, None)] + [(bn, sp) for bn in ("32", "64", "128") for sp in ("1", "2", "3", "4", "6", "8")]
+    for bn, sp in combos:
+        env = dict(os.environ)
+        if bn:
+            env.update(CGX_GEMM_BN=bn, CGX_GEMM_SPLIT=sp)
         r = subprocess.run([sys.executable, __file__, "child"], env=env, capture_output=True, text=True)
-        print(f"BN={bn} maxsplit={ms}", (r.stdout.strip() or r.stderr[-1500:]), flush=True)
+        print(f"BN={bn or 'model'} split={sp or 'model'}", (r.stdout.strip() or r.stderr[-600:]), flush=True)
