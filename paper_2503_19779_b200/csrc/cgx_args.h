@@ -60,6 +60,13 @@ static constexpr uint32_t kFlagEpochBump = 16u;   // first node: CTA 0 bumps the
 // signal their counter.
 static constexpr uint32_t kFlagDfPdlWait = 32u;
 static constexpr uint32_t kFlagDfSignal = 64u;
+// Diagnostics only (env CGX_DEBUG_NOOP=1 / 2, scripts/diag_cadence_split.py): return right after
+// the trigger (pure launch cascade of the real kernels), or keep the synchronisation but skip the
+// memory work.
+static constexpr uint32_t kFlagDbgNoop = 1u << 12;
+static constexpr uint32_t kFlagDbgNoWork = 1u << 13;
+// LayerNorm: gamma and beta are STATIC slots (never written in the graph): load them pre-wait.
+static constexpr uint32_t kFlagLnParamsPre = 1u << 14;
 
 // Multi-tensor copy (BASELINE north_star (1)). Static part lives in device
 // memory (per exec, written once at capture); the fresh sources travel by value in the params.

@@ -44,6 +44,7 @@ __device__ __forceinline__ void fetch_operands(const ElemArgs& a, const void*& p
   const void* p1;                                                      \
   if ((a).flags & kFlagEpochBump) df_bump(a);                          \
   if (!((a).flags & kFlagTriggerAfterWait)) pdl_trigger();             \
+  if ((a).flags & kFlagDbgNoop) return;                                \
   if (!((a).flags & kFlagTableAfterWait)) fetch_operands((a), p0, p1); \
   sync_in(a);                                                          \
   if ((a).flags & kFlagTableAfterWait) fetch_operands((a), p0, p1);    \
@@ -80,6 +81,7 @@ __global__ void __launch_bounds__(kElemThreads) k_elem_f32(const __grid_constant
   const bool late = a.flags & kFlagTableAfterWait;
   if (a.flags & kFlagEpochBump) df_bump(a);
   if (!(a.flags & kFlagTriggerAfterWait)) pdl_trigger();
+  if (a.flags & kFlagDbgNoop) return;
   const void* p0;
   const void* p1;
   if (!late) fetch_operands(a, p0, p1);
@@ -109,6 +111,10 @@ __global__ void __launch_bounds__(kElemThreads) k_elem_f32(const __grid_constant
     }
   }
   sync_in(a);
+  if (a.flags & kFlagDbgNoWork) {
+    sync_out(a);
+    return;
+  }
   if (late) {
     fetch_operands(a, p0, p1);
     x = reinterpret_cast<const float4*>(p0);
@@ -247,7 +253,7 @@ __global__ void __launch_bounds__(kReduceThreads) k_reduce_sum_f32(const __grid_
   CGX_PROLOGUE(a, p0, p1)
   (void)p1;
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint64_t rows = a.n / a.cols;
+  const uint64_t rows = (a.flags & kFlagDbgNoWork) ? 0 : a.n / a.cols;
   for (uint64_t r = (uint64_t)blockIdx.x * (kReduceThreads / 32) + warp; r < rows;
        r += (uint64_t)gridDim.x * (kReduceThreads / 32)) {
     const float4* row = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(p0) + r * a.cols);

@@ -561,6 +561,8 @@ static int build_launch(cgx_exec* e, int k, Launch& l) {
       a->cols = n.attr.cols;
       a->eps = n.attr.eps;
       if (is_ext(n.in[1]) || is_ext(n.in[2])) return fail(CGX_E_UNSUPPORTED, "layernorm: external gamma/beta");
+      if (c->slots[n.in[1]].kind == CGX_SLOT_STATIC && c->slots[n.in[2]].kind == CGX_SLOT_STATIC)
+        a->flags |= kFlagLnParamsPre;
       if (is_ext(n.in[0])) {
         const int j = c->slots[n.in[0]].ext_j;
         if (indirect) {
@@ -1140,6 +1142,11 @@ extern "C" int cgx_exec_create_ex(cgx_chain* c, const cgx_exec_opts* opts, void*
     if ((st = build_launch(e, k, e->L[k - first])) != CGX_OK) return bail(st);
   set_prewait_masks(e);
   if ((st = set_sync_flags(e)) != CGX_OK) return bail(st);
+  if (const char* dv = getenv("CGX_DEBUG_NOOP"); dv && (dv[0] == '1' || dv[0] == '2') && o.mode != CGX_MODE_EAGER) {
+    for (size_t p = 0; p < e->L.size(); ++p)
+      if (e->L[p].kind == LK_KERNEL && df_capable(c->nodes[e->L[p].node], c->slots[c->nodes[e->L[p].node].out].dtype))
+        argp<ElemArgs>(e->L[p])->flags |= dv[0] == '1' ? kFlagDbgNoop : kFlagDbgNoWork;
+  }
   if (const char* tv = getenv("CGX_NODE_TRACE"); tv && tv[0] == '1') {
     const size_t nb = sizeof(unsigned long long) * 3 * e->L.size();
     cudaError_t ce = cudaMalloc(&e->d_trace, nb);
