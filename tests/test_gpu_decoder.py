@@ -89,6 +89,24 @@ def test_gemm_integer_exact(rt, M, N, K):
         assert np.array_equal(got["y"], bf16_bits(env["y"]))
 
 
+# Every split-K / N-tile path of the tcgen05 GEMM, pinned with CGX_GEMM_TILING (read per exec):
+# uneven k-block splits (nk % S != 0), uneven owner row blocks (128 % S != 0), BN = 32/64/128,
+# ragged M, two M tiles, bias + residual epilogue. Integer-mode operands make every fp32 partial
+# and the sum exact, so the single bf16 rounding makes the result bit-exact for ANY split order.
+@pytest.mark.parametrize("M,N,K,tiling", [
+    (128, 768, 768, "32/3"), (128, 768, 768, "64/5"), (128, 2304, 768, "128/6"),
+    (128, 768, 3072, "32/8"), (128, 768, 3072, "64/7"), (128, 3072, 768, "32/2"),
+    (77, 384, 192, "32/3"), (256, 128, 512, "64/2"), (128, 256, 768, "128/1"), (1, 768, 768, "32/4")])
+def test_gemm_split_tilings_integer_exact(rt, monkeypatch, M, N, K, tiling):
+    monkeypatch.setenv("CGX_GEMM_TILING", f"{N}x{K}={tiling}")
+    spec = _gemm_chain(M, N, K, residual=True)
+    st = wl.static_values(spec, mode="int")
+    outs = _run(rt, spec, "INDIRECT", 2, st, mode_vals="int")
+    for r, got in enumerate(outs):
+        env = eval_chain(spec, wl.external_values(spec, r, "int"), st)
+        assert np.array_equal(got["y"], bf16_bits(env["y"])), f"tiling {tiling}"
+
+
 def test_gemm_gelu_and_residual(rt):
     for gelu, res in ((True, False), (False, True), (True, True)):
         spec = _gemm_chain(128, 3072 if gelu else 768, 768, gelu=gelu, residual=res)
