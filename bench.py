@@ -656,35 +656,42 @@ def run_extras(args, torch, cgx, runner, wl, sm, spec, chain, stream, sets, set_
         host_arena.append(h)
     dev_arena = [torch.empty(tot, dtype=torch.uint8, device=dev) for _ in range(NB)]
     arena_ptrs = [cgx.ptr_array([d.data_ptr() + o for o in offs]) for d in dev_arena]
-    out_bytes = sum(s_.nbytes for s_ in outs)
-    host_out = [torch.empty(out_bytes, dtype=torch.uint8).pin_memory() for _ in range(NB)]
+    out_slots = [chain.slot[s_.name] for s_ in outs]
+    out_cap = sum((s_.nbytes + 15) // 16 * 16 for s_ in outs)
+    host_out = [torch.empty(out_cap, dtype=torch.uint8).pin_memory() for _ in range(NB)]
+    dev_out = [torch.empty(out_cap, dtype=torch.uint8, device=dev) for _ in range(NB)]
     ex2 = chain.exec("INDIRECT", stream=stream, transport=main_transport)
-    out_ptrs = [(cgx.output(ex2.handle, chain.slot[s_.name])[0], s_.nbytes) for s_ in outs]
-    cstream = torch.cuda.Stream(device=dev)
-    ev_h2d = [torch.cuda.Event() for _ in range(NB)]
+    out_bytes = cgx.output_gather(ex2.handle, out_slots, dev_out[0].data_ptr(), out_cap)
+    torch.cuda.synchronize(dev)
+    # the H2D of a step is split in two halves on two copy streams (one 37.7 MB copy measured
+    # 42-54 GB/s run to run, two concurrent halves a steady ~53.6 GB/s: scripts/diag_h2d.py)
+    cstreams = [torch.cuda.Stream(device=dev) for _ in range(2)]
+    half = (tot // 2) // 256 * 256
+    ev_h2d = [[torch.cuda.Event() for _ in range(2)] for _ in range(NB)]
     ev_free = [torch.cuda.Event() for _ in range(NB)]
     h2 = ex2.handle
 
     def issue_h2d(i):
         b = i % NB
-        if i >= NB:
-            cstream.wait_event(ev_free[b])     # step i - NB has released arena b
-        cgx.copy(dev_arena[b].data_ptr(), host_arena[b].data_ptr(), tot, cstream.cuda_stream)
-        ev_h2d[b].record(cstream)
+        for k, cs_ in enumerate(cstreams):
+            if i >= NB:
+                cs_.wait_event(ev_free[b])     # step i - NB has released arena b
+            lo, hi = (0, half) if k == 0 else (half, tot)
+            cgx.copy(dev_arena[b].data_ptr() + lo, host_arena[b].data_ptr() + lo, hi - lo, cs_.cuda_stream)
+            ev_h2d[b][k].record(cs_)
 
     def issue_compute(i):
         b = i % NB
-        stream.wait_event(ev_h2d[b])
+        for ev_ in ev_h2d[b]:
+            stream.wait_event(ev_)
         st_ = LIB.cgx_bind(h2, arena_ptrs[b], n_ext)
         if st_ == 0:
             st_ = LIB.cgx_launch(h2)
         if st_:
             raise cgx.CgxError(st_, "e2e", cgx.last_error())
-        off = 0
-        base_ptr = host_out[b].data_ptr()
-        for p_, nb in out_ptrs:
-            cgx.copy(base_ptr + off, p_, nb, sh)
-            off += nb
+        # the 64 results: packed on the device by one gather kernel, read with ONE D2H copy
+        cgx.output_gather(h2, out_slots, dev_out[b].data_ptr(), out_cap)
+        cgx.copy(host_out[b].data_ptr(), dev_out[b].data_ptr(), out_bytes, sh)
         ev_free[b].record(stream)
 
     def run_e2e(n):
@@ -713,9 +720,10 @@ def run_extras(args, torch, cgx, runner, wl, sm, spec, chain, stream, sets, set_
                   "d2h_bytes_per_step": out_bytes,
                   "h2d_GBps": sum(s_.nbytes for s_ in exts) * n_e2e / e2e_dt / 1e9,
                   "note": "public API (cgx_copy H2D of the step's 64 inputs from one pinned arena on a "
-                          "copy stream, cgx_bind + cgx_launch, cgx_copy D2H of the 64 final outputs, "
+                          "copy stream, cgx_bind + cgx_launch, cgx_output_gather of the 64 final "
+                          "outputs + ONE cgx_copy D2H, "
                           "host waits for every step's result); triple-buffered: the H2D of step "
-                          "i+2 overlaps replay i; PCIe Gen5 x16 H2D ceiling on this box ~54 GB/s "
+                          "i+2 (two halves on two copy streams) overlaps replay i; PCIe Gen5 x16 H2D ceiling on this box ~54 GB/s "
                           "(scripts/diag_h2d.py)"}
     ex2.close()
 

@@ -243,6 +243,13 @@ int cgx_device_loop(cgx_exec* e, const void* d_ptr_sets, int n_sets, uint64_t n_
  * placeholder). nbytes may be NULL. */
 int cgx_output(cgx_exec* e, int slot, void** dptr, uint64_t* nbytes);
 int cgx_stats(const cgx_exec* e, cgx_stats_t* out);
+/* Pack the library-owned output buffers of `slots` (as cgx_output resolves them, in the given
+ * order, each at a 16-byte-aligned offset) into the caller-owned DEVICE buffer `dst` (16-B aligned,
+ * `cap` bytes) with one kernel enqueued on the exec's stream, after the launch that wrote them;
+ * the caller then reads all results with ONE device-to-host copy. *nbytes_out = packed size
+ * (written even on CGX_E_SIZE_MISMATCH). At most 64 slots. Errors: CGX_E_INVALID_ARG (NULL, bad or
+ * non-library-owned slot, n > 64), CGX_E_SIZE_MISMATCH (cap too small), CGX_E_MISALIGNED, CGX_E_CUDA. */
+int cgx_output_gather(cgx_exec* e, const int* slots, int n, void* dst, uint64_t cap, uint64_t* nbytes_out);
 /* Parity hooks: the device pointer table (n entries, host copy; synchronises the stream) and the
  * node indices a SETPARAMS bind rewrites. */
 int cgx_debug_read_table(const cgx_exec* e, uint64_t* host_out, int n);

@@ -97,6 +97,7 @@ def _load():
         "cgx_bind": ([VP, P(VP), I], I),
         "cgx_launch": ([VP], I),
         "cgx_output": ([VP, I, P(VP), P(U64)], I),
+        "cgx_output_gather": ([VP, P(I), I, VP, U64, P(U64)], I),
         "cgx_stats": ([VP, P(Stats)], I),
         "cgx_debug_read_table": ([VP, P(U64), I], I),
         "cgx_debug_setparam_nodes": ([VP, P(I), I, P(I)], I),
@@ -129,7 +130,7 @@ LIB = _load()
 EXPORTED = ("cgx_version", "cgx_last_error", "cgx_chain_create", "cgx_chain_add_slot",
             "cgx_chain_add_node", "cgx_chain_mark_segment", "cgx_chain_set_nccl",
             "cgx_chain_destroy", "cgx_exec_create", "cgx_exec_create_ex", "cgx_bind",
-            "cgx_launch", "cgx_output", "cgx_stats", "cgx_debug_read_table",
+            "cgx_launch", "cgx_output", "cgx_output_gather", "cgx_stats", "cgx_debug_read_table",
             "cgx_debug_setparam_nodes", "cgx_exec_destroy", "cgx_profile", "cgx_select",
             "cgx_dispatch_floor", "cgx_fill_uniform_f32", "cgx_copy", "cgx_graph_floor", "cgx_kernel_times", "cgx_find_param_offset",
             "cgx_debug_param_image", "cgx_debug_ext_field_offsets", "cgx_debug_gemm_trace", "cgx_debug_node_trace", "cgx_device_loop", "cgx_nccl_unique_id",
@@ -211,6 +212,16 @@ def output(ex: int, slot: int):
     p, n = C.c_void_p(), C.c_uint64()
     _ck(LIB.cgx_output(ex, slot, C.byref(p), C.byref(n)), "cgx_output")
     return p.value, n.value
+
+
+def output_gather(ex: int, slots, dst_dptr: int, cap: int) -> int:
+    """Pack the output buffers of `slots` into the device buffer dst (16-B aligned offsets) on the
+    exec's stream; returns the packed byte count."""
+    arr = (C.c_int * max(1, len(slots)))(*slots)
+    nb = C.c_uint64()
+    _ck(LIB.cgx_output_gather(ex, arr, len(slots), C.c_void_p(dst_dptr), C.c_uint64(cap), C.byref(nb)),
+        "cgx_output_gather")
+    return nb.value
 
 
 def stats(ex: int) -> dict:

@@ -145,6 +145,14 @@ struct ArgsTW<Base, 0> {
 // capacity for the T5 first node (0 = plain kernel; else 8, 64 or 512 pointers).
 extern "C++" {
 namespace cgx {
+static constexpr int kGatherMax = 64;
+struct GatherArgs {
+  const void* src[kGatherMax];
+  void* dst[kGatherMax];
+  uint64_t nbytes[kGatherMax];
+  uint32_t n;
+};
+const void* kfn_gather();
 const void* kfn_elem(int op, int dtype, int tw = 0);   // ADD/MUL/SCALE_IMM/COPY f32|bf16
 const void* kfn_reduce_sum_f32(int tw = 0);
 int tw_cap(int n);                                // 8, 64, 512 (0 if n > 512)

@@ -464,6 +464,20 @@ __global__ void k_pdl_nop() {
   pdl_wait();
 }
 
+// Output gather (cgx_output_gather): CTA i copies source i (a library-owned output slot, 256-B
+// aligned) to its 16-B aligned offset of the caller's packed buffer: 16-B vectors, then the tail
+// bytes. One launch replaces one small device-to-host copy per output with a single one.
+__global__ void __launch_bounds__(256) k_gather(const __grid_constant__ GatherArgs a) {
+  const uint32_t i = blockIdx.x;
+  if (i >= a.n) return;
+  const uint8_t* src = static_cast<const uint8_t*>(a.src[i]);
+  uint8_t* dst = static_cast<uint8_t*>(a.dst[i]);
+  const uint64_t nb = a.nbytes[i], n16 = nb >> 4;
+  for (uint64_t j = threadIdx.x; j < n16; j += blockDim.x)
+    reinterpret_cast<uint4*>(dst)[j] = reinterpret_cast<const uint4*>(src)[j];
+  for (uint64_t j = (n16 << 4) + threadIdx.x; j < nb; j += blockDim.x) dst[j] = src[j];
+}
+
 struct FillArgs { float* out; uint64_t n; uint64_t base; };
 __global__ void k_fill_uniform_f32(const __grid_constant__ FillArgs a) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n;
@@ -543,6 +557,7 @@ const void* kfn_table_mapped() { return (const void*)k_table_mapped; }
 const void* kfn_empty() { return (const void*)k_empty; }
 const void* kfn_pdl_nop() { return (const void*)k_pdl_nop; }
 const void* kfn_fill_uniform_f32() { return (const void*)k_fill_uniform_f32; }
+const void* kfn_gather() { return (const void*)k_gather; }
 int elem_block_threads() { return kElemThreads; }
 
 }  // namespace cgx

@@ -501,8 +501,13 @@ static size_t smem_bytes(int bn, uint32_t S, uint32_t stages) {
   return 1024 + ring + recv + bn * 4 + (2 * stages + 2) * 8 + 16;
 }
 static uint32_t ring_stages(uint32_t nk, uint32_t S) {
+  static const uint32_t cap = [] {   // CGX_GEMM_STAGES: measurement knob (1..kMaxStages)
+    const char* v = getenv("CGX_GEMM_STAGES");
+    const int n = v ? atoi(v) : kMaxStages;
+    return (uint32_t)(n >= 1 && n <= kMaxStages ? n : kMaxStages);
+  }();
   const uint32_t kps = (nk + S - 1) / S;
-  return kps < (uint32_t)kMaxStages ? kps : (uint32_t)kMaxStages;
+  return kps < cap ? kps : cap;
 }
 
 static void pick_tiling(uint32_t M, uint32_t N, uint32_t K, int* bn_out, uint32_t* split_out) {

@@ -1516,6 +1516,31 @@ extern "C" int cgx_output(cgx_exec* e, int slot, void** dptr, uint64_t* nbytes) 
   return CGX_OK;
 }
 
+extern "C" int cgx_output_gather(cgx_exec* e, const int* slots, int n, void* dst, uint64_t cap, uint64_t* nbytes_out) {
+  if (!e || (n > 0 && (!slots || !dst)) || n < 0) return fail(CGX_E_INVALID_ARG, "output_gather: bad argument");
+  if (n > kGatherMax) return fail(CGX_E_INVALID_ARG, "output_gather: more than 64 slots");
+  GatherArgs ga{};
+  uint64_t off = 0;
+  for (int i = 0; i < n; ++i) {
+    void* p = nullptr;
+    uint64_t nb = 0;
+    int st = cgx_output(e, slots[i], &p, &nb);
+    if (st != CGX_OK) return st;
+    ga.src[i] = p;
+    ga.dst[i] = static_cast<uint8_t*>(dst) + off;
+    ga.nbytes[i] = nb;
+    off += (nb + 15) / 16 * 16;
+  }
+  ga.n = (uint32_t)n;
+  if (nbytes_out) *nbytes_out = off;
+  if (off > cap) return fail(CGX_E_SIZE_MISMATCH, "output_gather: destination smaller than the packed outputs");
+  if (reinterpret_cast<uintptr_t>(dst) % 16) return fail(CGX_E_MISALIGNED, "output_gather: destination not 16-B aligned");
+  if (n == 0) return CGX_OK;
+  void* argv[1] = {&ga};
+  CK(cudaLaunchKernel(kfn_gather(), dim3(n), dim3(256), argv, 0, e->s));
+  return CGX_OK;
+}
+
 extern "C" int cgx_stats(const cgx_exec* e, cgx_stats_t* out) {
   if (!e || !out) return fail(CGX_E_INVALID_ARG, "stats: NULL argument");
   *out = e->st;

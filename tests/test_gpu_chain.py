@@ -244,6 +244,36 @@ def test_output_must_be_internal(rt):
     cgx.chain_destroy(c)
 
 
+def test_output_gather_packs_outputs(rt):
+    """cgx_output_gather == the individual outputs, byte for byte, at 16-B aligned offsets."""
+    cgx, runner = rt
+    dev = torch.device("cuda:0")
+    spec = wl.c2_chain()
+    st = wl.static_values(spec)
+    chain = runner.Chain(spec, runner.upload_statics(spec, st, dev))
+    ex = chain.exec("INDIRECT", transport="FIRST_NODE")
+    t = runner.upload_externals(spec, wl.external_values(spec, 0), dev)
+    ex.bind(t)
+    ex.launch()
+    names = [s.name for s in spec.internals()][-72:]
+    slots = [chain.slot[n] for n in names]
+    buf = torch.zeros(64 << 20, dtype=torch.uint8, device=dev)
+    with pytest.raises(cgx.CgxError):
+        cgx.output_gather(ex.handle, slots[:64], buf.data_ptr(), 16)           # too small
+    with pytest.raises(cgx.CgxError):
+        cgx.output_gather(ex.handle, slots + slots, buf.data_ptr(), buf.numel())  # > 64 slots
+    nb = cgx.output_gather(ex.handle, slots[:64], buf.data_ptr(), buf.numel())
+    torch.cuda.synchronize()
+    host = buf[:nb].cpu().numpy()
+    off = 0
+    for n in names[:64]:
+        ref = ex.output(n).view(np.uint8)
+        assert np.array_equal(host[off:off + ref.size], ref), n
+        off += (ref.size + 15) // 16 * 16
+    assert off == nb
+    chain.close()
+
+
 def test_copy_placeholder_rebind_copies_nothing(rt):
     cgx, runner = rt
     dev = torch.device("cuda:0")
