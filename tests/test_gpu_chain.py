@@ -159,6 +159,44 @@ def test_c4_points(rt, size, window):
             assert stats[-1]["bytes_data_rebound"] == 3 * size
 
 
+def test_c4_1gib_window_copy_and_indirect(rt):
+    """BASELINE C4 at its largest point, in the launch configuration bench.py times: 3 inputs of
+    1 GiB (device generator, bit-exact with synth), window kernels. COPY placeholders must equal
+    the bound inputs byte for byte (compared on the device), and both arms' outputs must equal the
+    oracle, which evaluates the same chain on the 4096-element window (counter-based generator:
+    the window of a 1 GiB input IS the C1-sized input of the same slot and replay)."""
+    cgx, runner = rt
+    dev = torch.device("cuda:0")
+    S = 1 << 30
+    spec, ref_spec = wl.c4_chain(S, window_mode=True), wl.c1_chain()
+    st = wl.static_values(spec)
+    chain = runner.Chain(spec, runner.upload_statics(spec, st, dev))
+    sh = torch.cuda.current_stream().cuda_stream
+    scratch = torch.empty(S // 4, dtype=torch.float32, device=dev)
+    for mode in ("COPY", "INDIRECT"):
+        ex = chain.exec(mode)
+        for r in range(2):
+            ts = {}
+            for s_ in spec.externals():
+                t = torch.empty(s_.nelems, dtype=torch.float32, device=dev)
+                cgx.fill_uniform_f32(t.data_ptr(), s_.nelems, sm.SEED, sm.stream_id(spec.index(s_.name), r), sh)
+                ts[s_.name] = t
+            ex.bind(ts)
+            ex.launch()
+            env = eval_chain(ref_spec, wl.external_values(ref_spec, r), st)
+            assert np.array_equal(ex.output("out"), env["out"]), (mode, r)
+            if mode == "COPY":
+                assert ex.stats()["bytes_data_rebound"] == 3 * S
+                for s_ in spec.externals():
+                    p, nb = cgx.output(ex.handle, chain.slot[s_.name])
+                    assert nb == S
+                    cgx.copy(scratch.data_ptr(), p, nb, sh)
+                    assert torch.equal(scratch, ts[s_.name]), s_.name
+            del ts
+        ex.close()
+    chain.close()
+
+
 def _ragged_chain(n, cols):
     slots = [SlotSpec("x", "external", "f32", n), SlotSpec("y", "external", "f32", n + 7),
              SlotSpec("w", "static", "f32", n), SlotSpec("a", "internal", "f32", n),
