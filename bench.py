@@ -278,6 +278,11 @@ def main():
     value = world * args.steps / (max_ms / 1e3)
     stats_main = ex_main.stats()
 
+    e2e = None
+    if not args.no_extras:
+        if world > 1:
+            dist.barrier()
+        e2e = run_e2e_all(torch, cgx, wl, spec, chain, stream, dev, world)
     extras = {}
     if rank == 0 and not args.no_extras:
         extras = run_extras(args, torch, cgx, runner, wl, sm, spec, chain, stream, sets, set_ptrs,
@@ -303,10 +308,120 @@ def main():
         "wall_s_timed_region": wall,
     }
     line.update(extras)
+    if e2e is not None:
+        line["e2e"] = e2e
     print(json.dumps(line), flush=True)
     chain.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_e2e_all(torch, cgx, wl, spec, chain, stream, dev, world):
+    """End to end through the public API on EVERY rank at once (pinned H2D inputs + D2H results);
+    the whole-job value is all ranks' steps over the max-over-ranks elapsed time."""
+    LIB = cgx.LIB
+    sh = stream.cuda_stream
+    n_ext = len(spec.externals())
+    main_transport = MAIN_TRANSPORT
+    # ---------------- end to end through the public API (pinned H2D inputs + D2H result)
+    # Inputs live packed in one pinned host arena per step and are copied (two halves, two copy
+    # streams) into a triple-buffered device arena, overlapping the replays; the 64 final outputs
+    # are packed on the device (cgx_output_gather) and read back with one D2H copy, and the host
+    # waits for every step's results before the clock stops.
+    outs = final_outputs(spec)
+    exts = spec.externals()
+    offs, tot = [], 0
+    for s_ in exts:
+        offs.append(tot)
+        tot += (s_.nbytes + 255) // 256 * 256
+    NB = 3                                     # triple-buffered pinned/device arenas
+    host_arena = []
+    for r in range(NB):
+        vals = wl.external_values(spec, r % 2)
+        h = torch.zeros(tot, dtype=torch.uint8).pin_memory()
+        hv = h.numpy()
+        for s_, o in zip(exts, offs):
+            hv[o:o + s_.nbytes] = vals[s_.name].view("u1")
+        host_arena.append(h)
+    dev_arena = [torch.empty(tot, dtype=torch.uint8, device=dev) for _ in range(NB)]
+    arena_ptrs = [cgx.ptr_array([d.data_ptr() + o for o in offs]) for d in dev_arena]
+    out_slots = [chain.slot[s_.name] for s_ in outs]
+    out_cap = sum((s_.nbytes + 15) // 16 * 16 for s_ in outs)
+    host_out = [torch.empty(out_cap, dtype=torch.uint8).pin_memory() for _ in range(NB)]
+    dev_out = [torch.empty(out_cap, dtype=torch.uint8, device=dev) for _ in range(NB)]
+    ex2 = chain.exec("INDIRECT", stream=stream, transport=main_transport)
+    out_bytes = cgx.output_gather(ex2.handle, out_slots, dev_out[0].data_ptr(), out_cap)
+    torch.cuda.synchronize(dev)
+    # the H2D of a step is split in two halves on two copy streams (one 37.7 MB copy measured
+    # 42-54 GB/s run to run, two concurrent halves a steady ~53.6 GB/s: scripts/diag_h2d.py)
+    cstreams = [torch.cuda.Stream(device=dev) for _ in range(2)]
+    half = (tot // 2) // 256 * 256
+    ev_h2d = [[torch.cuda.Event() for _ in range(2)] for _ in range(NB)]
+    ev_free = [torch.cuda.Event() for _ in range(NB)]
+    h2 = ex2.handle
+
+    def issue_h2d(i):
+        b = i % NB
+        for k, cs_ in enumerate(cstreams):
+            if i >= NB:
+                cs_.wait_event(ev_free[b])     # step i - NB has released arena b
+            lo, hi = (0, half) if k == 0 else (half, tot)
+            cgx.copy(dev_arena[b].data_ptr() + lo, host_arena[b].data_ptr() + lo, hi - lo, cs_.cuda_stream)
+            ev_h2d[b][k].record(cs_)
+
+    def issue_compute(i):
+        b = i % NB
+        for ev_ in ev_h2d[b]:
+            stream.wait_event(ev_)
+        st_ = LIB.cgx_bind(h2, arena_ptrs[b], n_ext)
+        if st_ == 0:
+            st_ = LIB.cgx_launch(h2)
+        if st_:
+            raise cgx.CgxError(st_, "e2e", cgx.last_error())
+        # the 64 results: packed on the device by one gather kernel, read with ONE D2H copy
+        cgx.output_gather(h2, out_slots, dev_out[b].data_ptr(), out_cap)
+        cgx.copy(host_out[b].data_ptr(), dev_out[b].data_ptr(), out_bytes, sh)
+        ev_free[b].record(stream)
+
+    def run_e2e(n):
+        # step i: H2D of its inputs (issued two steps ahead on the copy stream), bind + replay,
+        # D2H of its 64 results; the host waits for step i-1's results after issuing step i, and
+        # for the last step's before the clock stops: every step's result reaches host memory
+        torch.cuda.synchronize(dev)
+        t0w = time.perf_counter()
+        for j in range(min(NB - 1, n)):
+            issue_h2d(j)
+        for i in range(n):
+            issue_compute(i)
+            if i + NB - 1 < n:
+                issue_h2d(i + NB - 1)
+            if i >= 1:
+                ev_free[(i - 1) % NB].synchronize()
+        ev_free[(n - 1) % NB].synchronize()
+        torch.cuda.synchronize(dev)
+        return time.perf_counter() - t0w
+
+    run_e2e(10)
+    n_e2e = 400
+    e2e_dt = run_e2e(n_e2e)
+    if world > 1:                               # whole job: every rank's steps / max over ranks
+        import torch.distributed as dist
+        tt = torch.tensor([e2e_dt], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_dt = float(tt.item()) / world
+    res = {"value": n_e2e / e2e_dt, "unit": "iters/s",
+                  "h2d_bytes_per_step": sum(s_.nbytes for s_ in exts),
+                  "d2h_bytes_per_step": out_bytes,
+                  "h2d_GBps": sum(s_.nbytes for s_ in exts) * n_e2e / e2e_dt / 1e9,
+                  "note": "public API (cgx_copy H2D of the step's 64 inputs from one pinned arena on a "
+                          "copy stream, cgx_bind + cgx_launch, cgx_output_gather of the 64 final "
+                          "outputs + ONE cgx_copy D2H, "
+                          "host waits for every step's result); triple-buffered: the H2D of step "
+                          "i+2 (two halves on two copy streams) overlaps replay i; PCIe Gen5 x16 H2D ceiling on this box ~54 GB/s "
+                          "(scripts/diag_h2d.py)"}
+    ex2.close()
+    return res
+
 
 
 def run_extras(args, torch, cgx, runner, wl, sm, spec, chain, stream, sets, set_ptrs, timed, loop,
@@ -530,12 +645,13 @@ def run_extras(args, torch, cgx, runner, wl, sm, spec, chain, stream, sets, set_
             return 2 * 4 * n
         return 4 * n + 4 * n // node.attrs.get("cols", 256)
 
-    def sub_roofline(nodes):
+    def sub_roofline(nodes, overlapped=False):
         used = {i for n in nodes for i in n.ins} | {n.out for n in nodes}
         slots = [s_ for s_ in spec.slots if s_.name in used]
         sub = _CS("dom", slots, nodes, [(0, len(nodes) - 1)])
         sch = runner.Chain(sub, {k_: v for k_, v in chain.statics.items() if k_ in used}, device=dev.index or 0)
-        exs = sch.exec("INDIRECT", stream=stream, transport="ROOT_PARAMS", no_pdl=True)
+        exs = sch.exec("INDIRECT", stream=stream, transport=MAIN_TRANSPORT if overlapped else "ROOT_PARAMS",
+                       no_pdl=not overlapped)
         idx = [spec.externals().index(s_) for s_ in sub.externals()]
         arrs = [cgx.ptr_array([set_ptrs[r][i] for i in idx]) for r in range(N_SETS)]
         nx = len(idx)
@@ -556,7 +672,8 @@ def run_extras(args, torch, cgx, runner, wl, sm, spec, chain, stream, sets, set_
         exs.close()
         sch.close()
         # the root writer node (1 CTA, ~the graph floor) is part of the span: subtract it
-        per_launch = max(1e-3, (best_ - cgx.graph_floor(sh, 1, False, 200)) / len(nodes))
+        root = 0.0 if overlapped else cgx.graph_floor(sh, 1, False, 200)   # FIRST_NODE has no root node
+        per_launch = max(1e-3, (best_ - root) / len(nodes))
         byts = sum(algo_bytes(n) for n in nodes) / len(nodes)
         return per_launch, byts
 
@@ -572,6 +689,9 @@ def run_extras(args, torch, cgx, runner, wl, sm, spec, chain, stream, sets, set_
     big = [n for n in dom_nodes if n.attrs["n"] == (4 << 20) // 4]
     us_b, by_b = sub_roofline(big) if big else (None, None)
     achieved = by_l / (us_l * 1e-6) / 1e9
+    # the same launches captured the way the replay deploys them (PDL early trigger, dataflow sync:
+    # the independent lanes overlap): throughput of this kernel class in the deployed regime
+    us_o, by_o = sub_roofline(dom_nodes, overlapped=True)
     kname = {"ADD": "k_elem_f32<0>", "MUL": "k_elem_f32<1>", "REDUCE_SUM": "k_reduce_sum_f32",
              "SCALE_IMM": "k_elem_f32<2>"}[dom_op]
     traffic = None
@@ -587,6 +707,11 @@ def run_extras(args, torch, cgx, runner, wl, sm, spec, chain, stream, sets, set_
                        "largest_lanes_4MiB": ({"avg_launch_us": us_b, "algorithmic_bytes_per_launch": by_b,
                                                "achieved_GBps": by_b / (us_b * 1e-6) / 1e9} if big else None),
                        "by_lane_size": by_size,
+                       "deployed_overlapped": {"us_per_launch": us_o, "GBps": by_o / (us_o * 1e-6) / 1e9,
+                                               "frac": by_o / (us_o * 1e-6) / 1e9 / hbm,
+                                               "note": "same launches in a PDL + dataflow sub-graph (how the "
+                                                       "replay runs them): span / launches; launches overlap, so "
+                                                       "this is class throughput, not a per-launch duration"},
                        "peak_source": peak_src,
                        "timing": "CUDA events on the replay stream around 200 replays of a graph holding "
                                  "only this kernel's launches (same shapes, INDIRECT operands, no PDL); "
@@ -633,99 +758,6 @@ def run_extras(args, torch, cgx, runner, wl, sm, spec, chain, stream, sets, set_
         torch.cuda.empty_cache()
     except Exception as exn:  # noqa: BLE001
         out["copy_kernel"] = {"error": str(exn)}
-
-    # ---------------- end to end through the public API (pinned H2D inputs + D2H result)
-    # Inputs live packed in one pinned host arena per step and are copied with ONE cudaMemcpyAsync
-    # into a double-buffered device arena on a copy stream, overlapping the previous step's replay;
-    # the 64 final outputs are read back into pinned host memory and the host waits for them
-    # before the step counts as done.
-    outs = final_outputs(spec)
-    exts = spec.externals()
-    offs, tot = [], 0
-    for s_ in exts:
-        offs.append(tot)
-        tot += (s_.nbytes + 255) // 256 * 256
-    NB = 3                                     # triple-buffered pinned/device arenas
-    host_arena = []
-    for r in range(NB):
-        vals = wl.external_values(spec, r % 2)
-        h = torch.zeros(tot, dtype=torch.uint8).pin_memory()
-        hv = h.numpy()
-        for s_, o in zip(exts, offs):
-            hv[o:o + s_.nbytes] = vals[s_.name].view("u1")
-        host_arena.append(h)
-    dev_arena = [torch.empty(tot, dtype=torch.uint8, device=dev) for _ in range(NB)]
-    arena_ptrs = [cgx.ptr_array([d.data_ptr() + o for o in offs]) for d in dev_arena]
-    out_slots = [chain.slot[s_.name] for s_ in outs]
-    out_cap = sum((s_.nbytes + 15) // 16 * 16 for s_ in outs)
-    host_out = [torch.empty(out_cap, dtype=torch.uint8).pin_memory() for _ in range(NB)]
-    dev_out = [torch.empty(out_cap, dtype=torch.uint8, device=dev) for _ in range(NB)]
-    ex2 = chain.exec("INDIRECT", stream=stream, transport=main_transport)
-    out_bytes = cgx.output_gather(ex2.handle, out_slots, dev_out[0].data_ptr(), out_cap)
-    torch.cuda.synchronize(dev)
-    # the H2D of a step is split in two halves on two copy streams (one 37.7 MB copy measured
-    # 42-54 GB/s run to run, two concurrent halves a steady ~53.6 GB/s: scripts/diag_h2d.py)
-    cstreams = [torch.cuda.Stream(device=dev) for _ in range(2)]
-    half = (tot // 2) // 256 * 256
-    ev_h2d = [[torch.cuda.Event() for _ in range(2)] for _ in range(NB)]
-    ev_free = [torch.cuda.Event() for _ in range(NB)]
-    h2 = ex2.handle
-
-    def issue_h2d(i):
-        b = i % NB
-        for k, cs_ in enumerate(cstreams):
-            if i >= NB:
-                cs_.wait_event(ev_free[b])     # step i - NB has released arena b
-            lo, hi = (0, half) if k == 0 else (half, tot)
-            cgx.copy(dev_arena[b].data_ptr() + lo, host_arena[b].data_ptr() + lo, hi - lo, cs_.cuda_stream)
-            ev_h2d[b][k].record(cs_)
-
-    def issue_compute(i):
-        b = i % NB
-        for ev_ in ev_h2d[b]:
-            stream.wait_event(ev_)
-        st_ = LIB.cgx_bind(h2, arena_ptrs[b], n_ext)
-        if st_ == 0:
-            st_ = LIB.cgx_launch(h2)
-        if st_:
-            raise cgx.CgxError(st_, "e2e", cgx.last_error())
-        # the 64 results: packed on the device by one gather kernel, read with ONE D2H copy
-        cgx.output_gather(h2, out_slots, dev_out[b].data_ptr(), out_cap)
-        cgx.copy(host_out[b].data_ptr(), dev_out[b].data_ptr(), out_bytes, sh)
-        ev_free[b].record(stream)
-
-    def run_e2e(n):
-        # step i: H2D of its inputs (issued two steps ahead on the copy stream), bind + replay,
-        # D2H of its 64 results; the host waits for step i-1's results after issuing step i, and
-        # for the last step's before the clock stops: every step's result reaches host memory
-        torch.cuda.synchronize(dev)
-        t0w = time.perf_counter()
-        for j in range(min(NB - 1, n)):
-            issue_h2d(j)
-        for i in range(n):
-            issue_compute(i)
-            if i + NB - 1 < n:
-                issue_h2d(i + NB - 1)
-            if i >= 1:
-                ev_free[(i - 1) % NB].synchronize()
-        ev_free[(n - 1) % NB].synchronize()
-        torch.cuda.synchronize(dev)
-        return time.perf_counter() - t0w
-
-    run_e2e(10)
-    n_e2e = 400
-    e2e_dt = run_e2e(n_e2e)
-    out["e2e"] = {"value": n_e2e / e2e_dt, "unit": "iters/s",
-                  "h2d_bytes_per_step": sum(s_.nbytes for s_ in exts),
-                  "d2h_bytes_per_step": out_bytes,
-                  "h2d_GBps": sum(s_.nbytes for s_ in exts) * n_e2e / e2e_dt / 1e9,
-                  "note": "public API (cgx_copy H2D of the step's 64 inputs from one pinned arena on a "
-                          "copy stream, cgx_bind + cgx_launch, cgx_output_gather of the 64 final "
-                          "outputs + ONE cgx_copy D2H, "
-                          "host waits for every step's result); triple-buffered: the H2D of step "
-                          "i+2 (two halves on two copy streams) overlaps replay i; PCIe Gen5 x16 H2D ceiling on this box ~54 GB/s "
-                          "(scripts/diag_h2d.py)"}
-    ex2.close()
 
     # ---------------- CPU oracle baseline (bounded sample)
     n, dt = run_oracle_replays(spec, args.cpu_budget_s)
