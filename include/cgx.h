@@ -158,14 +158,22 @@ typedef struct {
                                1 = every bind, 2 = off (alignment and count are always checked) */
   int copy_impl;            /* GRAPH_COPY: 0 = multi-tensor LDG/STG kernel, 1 = cudaMemcpyAsync per
                                tensor, 2 = multi-tensor TMA bulk-copy kernel */
-  int sync_mode;            /* graph modes with PDL, how a node waits for its predecessors
-                               (DESIGN §5): CGX_SYNC_AUTO (0) = dataflow counters when every node
-                               supports them, else deferred waits; CGX_SYNC_DEFER (1) = deferred
+  int sync_mode;            /* graph modes with PDL, how the captured nodes are ordered:
+                               CGX_SYNC_AUTO (0) = GRAPH, except DATAFLOW for the PRELUDE and
+                               DEVICE transports; CGX_SYNC_DEFER (1) = one serial stream, deferred
                                griddepcontrol.wait for nodes with no in-graph producer;
-                               CGX_SYNC_CHAIN (2) = griddepcontrol.wait in every node */
+                               CGX_SYNC_CHAIN (2) = one serial stream, griddepcontrol.wait in every
+                               node; CGX_SYNC_GRAPH (3) = the graph is captured as the chain's
+                               data-dependency DAG over `graph_streams` capture streams (PDL +
+                               griddepcontrol.wait inside a stream, graph edges across streams);
+                               CGX_SYNC_DATAFLOW (4) = one serial stream, per-node completion
+                               counters (deferred waits when a node cannot use them) */
+  int graph_streams;        /* CGX_SYNC_GRAPH: capture streams (0 = 16, at most 64) */
 } cgx_exec_opts;
 
-typedef enum { CGX_SYNC_AUTO = 0, CGX_SYNC_DEFER = 1, CGX_SYNC_CHAIN = 2 } cgx_sync_mode;
+typedef enum {
+  CGX_SYNC_AUTO = 0, CGX_SYNC_DEFER = 1, CGX_SYNC_CHAIN = 2, CGX_SYNC_GRAPH = 3, CGX_SYNC_DATAFLOW = 4
+} cgx_sync_mode;
 
 typedef struct {
   uint64_t bytes_data_rebound;   /* last bind: data bytes copied into placeholders */
@@ -181,6 +189,7 @@ typedef struct {
   uint32_t mode, transport;
   uint32_t n_deferred;           /* nodes running with the deferred PDL wait */
   uint32_t dataflow;             /* 1: nodes synchronise through dataflow counters */
+  uint32_t dag_streams;          /* CGX_SYNC_GRAPH: capture streams holding at least one node */
 } cgx_stats_t;
 
 /* One segment's slow-path measurements, all microseconds. */

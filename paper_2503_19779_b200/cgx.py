@@ -29,7 +29,7 @@ MODE = {"EAGER": 0, "COPY": 1, "INDIRECT": 2, "SETPARAMS": 3, "STALE": 4}
 XPORT = {"DEFAULT": 0, "H2D": 1, "ROOT_MEMCPY": 2, "ROOT_PARAMS": 3, "ROOT_MAPPED": 4, "FIRST_NODE": 5, "H2D_PINGPONG": 6, "PRELUDE": 7,
          "DEVICE": 8}
 DECIDE = {0: "EAGER", 1: "GRAPH_COPY", 2: "GRAPH_INDIRECT"}
-SYNC = {"AUTO": 0, "DEFER": 1, "CHAIN": 2}
+SYNC = {"AUTO": 0, "DEFER": 1, "CHAIN": 2, "GRAPH": 3, "DATAFLOW": 4}
 MAX_PROFILE_KERNELS = 1024
 
 
@@ -43,7 +43,7 @@ class Attr(C.Structure):
 class ExecOpts(C.Structure):
     _fields_ = [("mode", C.c_int), ("transport", C.c_int), ("first_node", C.c_int),
                 ("n_nodes", C.c_int), ("no_pdl", C.c_int), ("validate", C.c_int),
-                ("copy_impl", C.c_int), ("sync_mode", C.c_int)]
+                ("copy_impl", C.c_int), ("sync_mode", C.c_int), ("graph_streams", C.c_int)]
 
 
 class Stats(C.Structure):
@@ -53,7 +53,7 @@ class Stats(C.Structure):
                 ("n_setparam_calls", C.c_uint32), ("n_copy_tensors", C.c_uint32),
                 ("n_nodes", C.c_uint32), ("n_graph_nodes", C.c_uint32), ("n_ext", C.c_uint32),
                 ("kernels_per_replay", C.c_uint32), ("mode", C.c_uint32), ("transport", C.c_uint32),
-                ("n_deferred", C.c_uint32), ("dataflow", C.c_uint32)]
+                ("n_deferred", C.c_uint32), ("dataflow", C.c_uint32), ("dag_streams", C.c_uint32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -187,9 +187,9 @@ def chain_destroy(chain: int):
 
 def exec_create(chain: int, mode: str, stream: int, transport: str = "DEFAULT", first_node: int = 0,
                 n_nodes: int = 0, no_pdl: bool = False, validate: int = 0, copy_impl: int = 0,
-                sync: str = "AUTO") -> int:
+                sync: str = "AUTO", graph_streams: int = 0) -> int:
     o = ExecOpts(MODE[mode], XPORT[transport], first_node, n_nodes, int(no_pdl), validate, copy_impl,
-                 SYNC[sync])
+                 SYNC[sync], graph_streams)
     out = C.c_void_p()
     _ck(LIB.cgx_exec_create_ex(chain, C.byref(o), stream, C.byref(out)), "cgx_exec_create_ex")
     return out.value

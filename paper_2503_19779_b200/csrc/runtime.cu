@@ -389,6 +389,10 @@ struct cgx_exec {
   cudaGraphNode_t dl_node = nullptr;
   unsigned long long* dl_iter = nullptr;
   bool dataflow = false;
+  // CGX_SYNC_GRAPH: dependency-DAG capture streams and per-node completion events
+  std::vector<cudaStream_t> dag_s;
+  std::vector<cudaEvent_t> dag_ev;
+  uint32_t dag_used = 0;          // capture streams that received at least one node
   // T3 / T4 root
   const void* root_fn = nullptr;
   AlignedBuf root_args;
@@ -652,7 +656,7 @@ static void set_prewait_masks(cgx_exec* e) {
 
 // How nodes wait for their predecessors in graph modes with PDL (cgx_args.h).
 //
-// Dataflow (CGX_SYNC_AUTO, every node a chain kernel): node k waits, through per-launch CTA
+// Dataflow (CGX_SYNC_DATAFLOW, every node a chain kernel): node k waits, through per-launch CTA
 // counters, for exactly (a) the last earlier writer of each slot it reads (RAW), (b) the last
 // earlier writer of its output slot (WAW) and every earlier reader of that slot since then (WAR).
 // "Earlier" is within this graph only: a graph launch waits for the previous replay as a whole.
@@ -675,8 +679,19 @@ static bool df_capable(const Node& n, cgx_dtype out_dt) {
 
 static int set_sync_flags(cgx_exec* e) {
   if (e->o.no_pdl || e->o.mode == CGX_MODE_EAGER || e->o.sync_mode == CGX_SYNC_CHAIN) return CGX_OK;
+  if (e->o.sync_mode == CGX_SYNC_GRAPH) {
+    // concurrent branches: one CTA per SM for the f32 elementwise / reduction nodes as in the
+    // dataflow replay (C2 at 16 streams: 54.8 us capped vs 56.3 us full width, profiles/r01)
+    for (auto& l : e->L) {
+      if (l.kind != LK_KERNEL) continue;
+      const Node& n = e->c->nodes[l.node];
+      const bool f32 = e->c->slots[n.out].dtype == CGX_F32 && (n.op <= CGX_OP_COPY || n.op == CGX_OP_SCALE_T);
+      if (n.op == CGX_OP_REDUCE_SUM || f32) l.grid.x = (unsigned)std::min<uint64_t>(l.grid.x, chain_grid_cap(true));
+    }
+    return CGX_OK;
+  }
   const size_t ns = e->c->slots.size(), nl = e->L.size();
-  if (e->o.sync_mode == CGX_SYNC_AUTO && nl > 0) {
+  if (e->o.sync_mode == CGX_SYNC_DATAFLOW && nl > 0) {
     bool ok = true;
     for (auto& l : e->L) ok = ok && l.kind == LK_KERNEL && df_capable(e->c->nodes[l.node], e->c->slots[e->c->nodes[l.node].out].dtype);
     std::vector<std::vector<uint32_t>> deps(nl);
@@ -978,6 +993,103 @@ static int setup_table(cgx_exec* e) {
   return CGX_OK;
 }
 
+// CGX_SYNC_GRAPH: capture the chain as its data-dependency DAG instead of one serial stream.
+// Dependencies come from the slot accesses in chain order (RAW: last writer of every input; WAW:
+// last writer of the output; WAR: readers of the output since then). Nodes are spread over
+// `graph_streams` capture streams: a node joins the stream whose tail is its most recent
+// dependency (so that edge is a PDL edge), else an empty stream, else the stream with the oldest
+// tail; dependencies on other streams become graph edges (event record/wait during capture).
+// Inside a stream every kernel triggers at entry and griddepcontrol.wait's before it reads another
+// node's output or writes its own, so any incoming edge (programmatic or not) is honoured, and
+// in-stream order makes every earlier node of the stream an ancestor. The first kernel of a
+// stream is captured WITHOUT the PDL attribute: its edges from the fork (root table writer,
+// T5 publisher) are then full completion edges, so its pre-wait table fetch is safe. Independent
+// branches let the graph executor issue launches on several hardware queues at once instead of
+// one PDL cascade (scripts/dag_microbench.cu).
+static int capture_dag(cgx_exec* e, int gi, cudaStream_t cs, cgx_transport t) {
+  const bool indirect = e->o.mode == CGX_MODE_GRAPH_INDIRECT;
+  if (indirect && (t == CGX_XPORT_PRELUDE || t == CGX_XPORT_DEVICE))
+    return fail(CGX_E_UNSUPPORTED, "sync GRAPH: not with the PRELUDE / DEVICE transports");
+  const size_t nl = e->L.size(), ns = e->c->slots.size();
+  std::vector<std::vector<int>> deps(nl);
+  {
+    std::vector<int> last_w(ns, -1);
+    std::vector<std::vector<int>> readers(ns);
+    for (size_t p = 0; p < nl; ++p) {
+      const Node& n = e->c->nodes[e->L[p].node];
+      auto add = [&](int q) {
+        if (q < 0 || q == (int)p) return;
+        for (int d : deps[p]) if (d == q) return;
+        deps[p].push_back(q);
+      };
+      for (int j = 0; j < n.n_in; ++j) add(last_w[n.in[j]]);
+      add(last_w[n.out]);
+      for (int r : readers[n.out]) add(r);
+      for (int j = 0; j < n.n_in; ++j) readers[n.in[j]].push_back((int)p);
+      last_w[n.out] = (int)p;
+      readers[n.out].clear();
+    }
+  }
+  const int S = e->o.graph_streams ? e->o.graph_streams : 16;
+  if (e->dag_s.empty()) {
+    e->dag_s.assign((size_t)S + 0, nullptr);
+    for (auto& st : e->dag_s) CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    e->dag_ev.assign(nl + 1 + (size_t)S, nullptr);   // per node, fork, per-stream join
+    for (auto& ev : e->dag_ev) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  }
+  // T5: the by-value prefix up to the table publisher runs on the origin stream before the fork
+  const int pre = (indirect && t == CGX_XPORT_FIRST_NODE) ? e->t5_pub : -1;
+  for (int p = 0; p <= pre; ++p) {
+    Launch& l = e->L[p];
+    CKS(issue(e, l, cs));
+    if (l.kind == LK_KERNEL) CKS(last_captured_node(cs, &l.gnode[gi]));
+  }
+  cudaEvent_t fork = e->dag_ev[nl];
+  CK(cudaEventRecord(fork, cs));
+  for (auto& st : e->dag_s) CK(cudaStreamWaitEvent(st, fork, 0));
+  std::vector<int> stream_of(nl, -1), tail((size_t)S, -1);
+  std::vector<char> need_ev(nl, 0);
+  for (size_t p = 0; p < nl; ++p)
+    for (int d : deps[p]) need_ev[d] = 1;
+  for (int p = pre + 1; p < (int)nl; ++p) {
+    int best = -1, bestd = -1;
+    for (int d : deps[p])
+      if (stream_of[d] >= 0 && tail[stream_of[d]] == d && d > bestd) {
+        best = stream_of[d];
+        bestd = d;
+      }
+    if (best < 0) {
+      for (int k = 0; k < S && best < 0; ++k)
+        if (tail[k] < 0) best = k;
+      if (best < 0) {
+        best = 0;
+        for (int k = 1; k < S; ++k)
+          if (tail[k] < tail[best]) best = k;
+      }
+    }
+    cudaStream_t st = e->dag_s[best];
+    for (int d : deps[p])
+      if (d > pre && stream_of[d] != best) CK(cudaStreamWaitEvent(st, e->dag_ev[d], 0));
+    Launch& l = e->L[p];
+    const bool saved = l.pdl;
+    if (tail[best] < 0) l.pdl = false;
+    const int rc = issue(e, l, st);
+    l.pdl = saved;
+    CKS(rc);
+    if (l.kind == LK_KERNEL) CKS(last_captured_node(st, &l.gnode[gi]));
+    if (need_ev[p]) CK(cudaEventRecord(e->dag_ev[p], st));
+    stream_of[p] = best;
+    tail[best] = p;
+  }
+  e->dag_used = 0;
+  for (int k = 0; k < S; ++k) e->dag_used += tail[k] >= 0 ? 1u : 0u;
+  for (int k = 0; k < S; ++k) {
+    CK(cudaEventRecord(e->dag_ev[nl + 1 + k], e->dag_s[k]));
+    CK(cudaStreamWaitEvent(cs, e->dag_ev[nl + 1 + k], 0));
+  }
+  return CGX_OK;
+}
+
 static int capture_graph(cgx_exec* e, int gi) {
   cudaStream_t cs = e->cs;
   const cgx_transport t = eff_transport(e->o);
@@ -1025,6 +1137,9 @@ static int capture_graph(cgx_exec* e, int gi) {
       after_root = true;
     }
   }
+  if (e->o.sync_mode == CGX_SYNC_GRAPH) {
+    CKS(capture_dag(e, gi, cs, t));
+  } else {
   bool first_kernel = true;
   for (auto& l : e->L) {
     if (l.kind == LK_KERNEL && first_kernel && after_root) {
@@ -1042,6 +1157,7 @@ static int capture_graph(cgx_exec* e, int gi) {
     if (l.kind == LK_KERNEL) first_kernel = false;
     CKS(issue(e, l, cs));
     if (l.kind == LK_KERNEL) CKS(last_captured_node(cs, &l.gnode[gi]));
+  }
   }
   CK(cudaStreamEndCapture(cs, &e->g[gi]));
   const bool devl = e->o.mode == CGX_MODE_GRAPH_INDIRECT && t == CGX_XPORT_DEVICE;
@@ -1081,6 +1197,8 @@ static void exec_free(cgx_exec* e) {
   if (e->h_ack) cudaFreeHost((void*)e->h_ack);
   if (e->d_seq) cudaFree(e->d_seq);
   for (auto& v : e->ev) cudaEventDestroy(v);
+  for (auto& v : e->dag_ev) if (v) cudaEventDestroy(v);
+  for (auto& v : e->dag_s) if (v) cudaStreamDestroy(v);
   if (e->c) e->c->live_execs--;
   delete e;
 }
@@ -1095,7 +1213,8 @@ extern "C" int cgx_exec_create_ex(cgx_chain* c, const cgx_exec_opts* opts, void*
   if (o.transport < CGX_XPORT_DEFAULT || o.transport > CGX_XPORT_DEVICE)
     return fail(CGX_E_INVALID_ARG, "exec_create: transport");
   if (o.copy_impl < 0 || o.copy_impl > 2) return fail(CGX_E_INVALID_ARG, "exec_create: copy_impl");
-  if (o.sync_mode < CGX_SYNC_AUTO || o.sync_mode > CGX_SYNC_CHAIN) return fail(CGX_E_INVALID_ARG, "exec_create: sync_mode");
+  if (o.sync_mode < CGX_SYNC_AUTO || o.sync_mode > CGX_SYNC_DATAFLOW) return fail(CGX_E_INVALID_ARG, "exec_create: sync_mode");
+  if (o.graph_streams < 0 || o.graph_streams > 64) return fail(CGX_E_INVALID_ARG, "exec_create: graph_streams (0..64)");
   const int K = (int)c->nodes.size();
   if (K == 0) return fail(CGX_E_STATE, "exec_create: empty chain");
   const int first = o.first_node, last = o.n_nodes ? o.first_node + o.n_nodes - 1 : K - 1;
@@ -1106,6 +1225,14 @@ extern "C" int cgx_exec_create_ex(cgx_chain* c, const cgx_exec_opts* opts, void*
   e->c = c;
   c->live_execs++;
   e->o = o;
+  // AUTO: graph modes with PDL capture the chain's dependency DAG (CGX_SYNC_GRAPH) unless the
+  // transport relies on the serial protocol (PRELUDE, DEVICE); those keep the dataflow counters.
+  if (e->o.sync_mode == CGX_SYNC_AUTO) {
+    const cgx_transport t0 = eff_transport(e->o);
+    const bool dag_ok = e->o.mode != CGX_MODE_EAGER && !e->o.no_pdl &&
+                        !(e->o.mode == CGX_MODE_GRAPH_INDIRECT && (t0 == CGX_XPORT_PRELUDE || t0 == CGX_XPORT_DEVICE));
+    e->o.sync_mode = dag_ok ? CGX_SYNC_GRAPH : CGX_SYNC_DATAFLOW;
+  }
   e->s = static_cast<cudaStream_t>(stream);
   e->first = first;
   e->last = last;
@@ -1212,6 +1339,7 @@ extern "C" int cgx_exec_create_ex(cgx_chain* c, const cgx_exec_opts* opts, void*
     if (l.kind == LK_KERNEL && (e->c->nodes[l.node].op <= CGX_OP_COPY || e->c->nodes[l.node].op == CGX_OP_SCALE_T))
       e->st.n_deferred += (argp<ElemArgs>(l)->flags & kFlagDeferWait) ? 1u : 0u;
   e->st.dataflow = e->dataflow ? 1u : 0u;
+  e->st.dag_streams = e->dag_used;
   e->st.mode = (uint32_t)o.mode;
   e->st.transport = o.mode == CGX_MODE_GRAPH_INDIRECT ? (uint32_t)eff_transport(o) : 0;
   e->st.kernels_per_replay = (uint32_t)kernels + (o.mode == CGX_MODE_GRAPH_COPY && o.copy_impl != 1 && !e->ext_read.empty()) +

@@ -24,7 +24,8 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
     chain = runner.Chain(spec, runner.upload_statics(spec, wl.static_values(spec), dev))
     sets = [runner.upload_externals(spec, wl.external_values(spec, r), dev) for r in range(4)]
     stream = torch.cuda.current_stream()
-    ex = chain.exec("INDIRECT", stream=stream, transport="FIRST_NODE", sync=sys.argv[2])
+    ex = chain.exec("INDIRECT", stream=stream, transport=os.environ.get("XPORT", "FIRST_NODE"), sync=sys.argv[2],
+                    graph_streams=int(sys.argv[3]) if len(sys.argv) > 3 else 0)
     ptrs = [cgx.ptr_array([t[s.name].data_ptr() for s in spec.externals()]) for t in sets]
     n_ext = len(spec.externals())
     L = cgx.LIB
@@ -48,17 +49,29 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
     sys.exit(0)
 
 
-def run(env_extra, sync="AUTO"):
+def run(env_extra, sync="AUTO", streams=0):
     env = dict(os.environ, **env_extra)
-    r = subprocess.run([sys.executable, __file__, "child", sync], env=env, capture_output=True, text=True,
-                       timeout=240)
+    r = subprocess.run([sys.executable, __file__, "child", sync, str(streams)], env=env, capture_output=True,
+                       text=True, timeout=240)
     try:
         return json.loads(r.stdout.strip().splitlines()[-1])["us_per_replay"]
     except (IndexError, ValueError, KeyError):
         return r.stderr[-400:]
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "graph":
+    # dependency-DAG capture (sync GRAPH): capture streams x grid cap x transport
+    for xp in ("FIRST_NODE", "H2D", "ROOT_PARAMS"):
+        for streams in (2, 4, 8, 16, 32):
+            for cap in (None, "148"):
+                e = {"XPORT": xp}
+                if cap:
+                    e["CGX_CHAIN_MAX_CTAS"] = cap
+                key = f"sync=GRAPH xport={xp} streams={streams} cap={cap or 'default'}"
+                print(json.dumps({key: run(e, "GRAPH", streams)}), flush=True)
+    print(json.dumps({"sync=AUTO xport=FIRST_NODE": run({}, "AUTO")}), flush=True)
+    print(json.dumps({"sync=CHAIN xport=FIRST_NODE": run({}, "CHAIN")}), flush=True)
+elif __name__ == "__main__":
     out = {}
     for sync in ("AUTO",):
         for cap in (None, "16", "4"):

@@ -1,4 +1,4 @@
-"""Node synchronisation modes in graph replays: AUTO (dataflow counters), DEFER
+"""Node synchronisation modes in graph replays: DATAFLOW (per-node completion counters), DEFER
 (deferred griddepcontrol.wait for nodes with no in-graph producer) and CHAIN (plain PDL waits).
 Outputs must be bit-identical across modes, to EAGER and to the oracle, over many replays with
 fresh input addresses, including chains with write-after-read / write-after-write hazards."""
@@ -43,7 +43,7 @@ def _replays(rt, spec, mode, transport, n, sync, int_mode=False):
 @pytest.mark.parametrize("transport,want", [("FIRST_NODE", 64), ("H2D", 64), ("ROOT_PARAMS", 63)])
 def test_c2_sync_modes_bitexact(rt, transport, want):
     spec = wl.c2_chain()
-    a, sa, st = _replays(rt, spec, "INDIRECT", transport, 6, "AUTO")
+    a, sa, st = _replays(rt, spec, "INDIRECT", transport, 6, "DATAFLOW")
     b, sb, _ = _replays(rt, spec, "INDIRECT", transport, 6, "DEFER")
     c, sc, _ = _replays(rt, spec, "INDIRECT", transport, 6, "CHAIN")
     assert sa == (0, 1) and sb == (want, 0) and sc == (0, 0)
@@ -60,7 +60,7 @@ def test_c2_sync_modes_bitexact(rt, transport, want):
 @pytest.mark.parametrize("mode", ["COPY", "SETPARAMS", "EAGER", "STALE"])
 def test_c2_sync_other_modes(rt, mode):
     spec = wl.c2_chain(n_lanes=16)
-    a, sa, _ = _replays(rt, spec, mode, "DEFAULT", 4, "AUTO")
+    a, sa, _ = _replays(rt, spec, mode, "DEFAULT", 4, "DATAFLOW")
     b, sb, _ = _replays(rt, spec, mode, "DEFAULT", 4, "DEFER")
     c, _, _ = _replays(rt, spec, mode, "DEFAULT", 4, "CHAIN")
     graph = mode != "EAGER"                       # eager keeps the wait: previous iteration
@@ -86,7 +86,7 @@ def _war_chain(n):
 
 
 @pytest.mark.parametrize("n", [4096, 1 << 22])
-@pytest.mark.parametrize("sync,want", [("AUTO", (0, 1)), ("DEFER", (2, 0))])
+@pytest.mark.parametrize("sync,want", [("DATAFLOW", (0, 1)), ("DEFER", (2, 0))])
 def test_war_hazard(rt, n, sync, want):
     spec = _war_chain(n)
     outs, got, st = _replays(rt, spec, "INDIRECT", "FIRST_NODE", 8, sync)
@@ -112,14 +112,14 @@ def _fanin_chain(n, readers):
 @pytest.mark.parametrize("readers,df", [(3, 1), (6, 0)])
 def test_fanin_fallback(rt, readers, df):
     spec = _fanin_chain(1 << 16, readers)
-    outs, got, st = _replays(rt, spec, "INDIRECT", "FIRST_NODE", 4, "AUTO")
+    outs, got, st = _replays(rt, spec, "INDIRECT", "FIRST_NODE", 4, "DATAFLOW")
     assert got[1] == df
     env = eval_chain(spec, wl.external_values(spec, 3), st)
     for k in outs[3]:
         assert np.array_equal(outs[3][k], env[k]), k
 
 
-@pytest.mark.parametrize("sync", ["AUTO", "DEFER"])
+@pytest.mark.parametrize("sync", ["DATAFLOW", "DEFER"])
 def test_c2_sync_stress_rotating(rt, sync):
     """100 replays over 4 rotating input sets (integer mode: every value exact)."""
     cgx, runner = rt
