@@ -15,6 +15,8 @@ timeout 300 ncu --set full --import-source on --clock-control none --graph-profi
 timeout 240 python scripts/c4_sweep.py window full > gpurun_out/c4_final.log 2>&1
 timeout 120 python scripts/pi_sweep.py > gpurun_out/pi_sweep_final.log 2>&1
 [ -x scripts/launch_microbench ] && timeout 120 ./scripts/launch_microbench > gpurun_out/launch_microbench.txt 2>&1
+[ -x scripts/dag_microbench ] && timeout 120 ./scripts/dag_microbench > gpurun_out/dag_microbench.txt 2>&1
+timeout 600 python scripts/diag_cadence_split.py graph > gpurun_out/dag_sweep.txt 2>&1
 timeout 300 python scripts/diag_cadence_split.py > gpurun_out/cadence_split.txt 2>&1
 timeout 120 python scripts/diag_h2d.py > gpurun_out/h2d.txt 2>&1
 ls -la gpurun_out | tail -30
