@@ -1008,8 +1008,6 @@ static int setup_table(cgx_exec* e) {
 // one PDL cascade (scripts/dag_microbench.cu).
 static int capture_dag(cgx_exec* e, int gi, cudaStream_t cs, cgx_transport t) {
   const bool indirect = e->o.mode == CGX_MODE_GRAPH_INDIRECT;
-  if (indirect && (t == CGX_XPORT_PRELUDE || t == CGX_XPORT_DEVICE))
-    return fail(CGX_E_UNSUPPORTED, "sync GRAPH: not with the PRELUDE / DEVICE transports");
   const size_t nl = e->L.size(), ns = e->c->slots.size();
   std::vector<std::vector<int>> deps(nl);
   {
@@ -1039,18 +1037,8 @@ static int capture_dag(cgx_exec* e, int gi, cudaStream_t cs, cgx_transport t) {
   }
   // T5: the by-value prefix up to the table publisher runs on the origin stream before the fork
   const int pre = (indirect && t == CGX_XPORT_FIRST_NODE) ? e->t5_pub : -1;
-  for (int p = 0; p <= pre; ++p) {
-    Launch& l = e->L[p];
-    CKS(issue(e, l, cs));
-    if (l.kind == LK_KERNEL) CKS(last_captured_node(cs, &l.gnode[gi]));
-  }
-  cudaEvent_t fork = e->dag_ev[nl];
-  CK(cudaEventRecord(fork, cs));
-  for (auto& st : e->dag_s) CK(cudaStreamWaitEvent(st, fork, 0));
+  // stream assignment (pure pass)
   std::vector<int> stream_of(nl, -1), tail((size_t)S, -1);
-  std::vector<char> need_ev(nl, 0);
-  for (size_t p = 0; p < nl; ++p)
-    for (int d : deps[p]) need_ev[d] = 1;
   for (int p = pre + 1; p < (int)nl; ++p) {
     int best = -1, bestd = -1;
     for (int d : deps[p])
@@ -1067,22 +1055,55 @@ static int capture_dag(cgx_exec* e, int gi, cudaStream_t cs, cgx_transport t) {
           if (tail[k] < tail[best]) best = k;
       }
     }
-    cudaStream_t st = e->dag_s[best];
-    for (int d : deps[p])
-      if (d > pre && stream_of[d] != best) CK(cudaStreamWaitEvent(st, e->dag_ev[d], 0));
-    Launch& l = e->L[p];
-    const bool saved = l.pdl;
-    if (tail[best] < 0) l.pdl = false;
-    const int rc = issue(e, l, st);
-    l.pdl = saved;
-    CKS(rc);
-    if (l.kind == LK_KERNEL) CKS(last_captured_node(st, &l.gnode[gi]));
-    if (need_ev[p]) CK(cudaEventRecord(e->dag_ev[p], st));
     stream_of[p] = best;
     tail[best] = p;
   }
   e->dag_used = 0;
   for (int k = 0; k < S; ++k) e->dag_used += tail[k] >= 0 ? 1u : 0u;
+  if (e->dag_used <= 1) {
+    // a single branch (a linear chain such as C1 or the decoder): capture it on the origin stream
+    // without a fork (same graph, no multi-stream capture overhead on the host launch path); the
+    // first kernel after a root node still takes a full completion edge
+    bool first = true;
+    for (int p = 0; p < (int)nl; ++p) {
+      Launch& l = e->L[p];
+      const bool saved = l.pdl;
+      if (first && p > pre) l.pdl = false;
+      if (p > pre) first = false;
+      const int rc = issue(e, l, cs);
+      l.pdl = saved;
+      CKS(rc);
+      if (l.kind == LK_KERNEL) CKS(last_captured_node(cs, &l.gnode[gi]));
+    }
+    return CGX_OK;
+  }
+  for (int p = 0; p <= pre; ++p) {
+    Launch& l = e->L[p];
+    CKS(issue(e, l, cs));
+    if (l.kind == LK_KERNEL) CKS(last_captured_node(cs, &l.gnode[gi]));
+  }
+  cudaEvent_t fork = e->dag_ev[nl];
+  CK(cudaEventRecord(fork, cs));
+  for (auto& st : e->dag_s) CK(cudaStreamWaitEvent(st, fork, 0));
+  std::vector<char> need_ev(nl, 0), started((size_t)S, 0);
+  for (size_t p = 0; p < nl; ++p)
+    for (int d : deps[p]) need_ev[d] = 1;
+  for (int p = pre + 1; p < (int)nl; ++p) {
+    const int best = stream_of[p];
+    cudaStream_t st = e->dag_s[best];
+    for (int d : deps[p])
+      if (d > pre && stream_of[d] != best) CK(cudaStreamWaitEvent(st, e->dag_ev[d], 0));
+    Launch& l = e->L[p];
+    const bool saved = l.pdl;
+    if (!started[best]) l.pdl = false;
+    started[best] = 1;
+    const int rc = issue(e, l, st);
+    l.pdl = saved;
+    CKS(rc);
+    if (l.kind == LK_KERNEL) CKS(last_captured_node(st, &l.gnode[gi]));
+    if (need_ev[p]) CK(cudaEventRecord(e->dag_ev[p], st));
+  }
+
   for (int k = 0; k < S; ++k) {
     CK(cudaEventRecord(e->dag_ev[nl + 1 + k], e->dag_s[k]));
     CK(cudaStreamWaitEvent(cs, e->dag_ev[nl + 1 + k], 0));
@@ -1225,14 +1246,10 @@ extern "C" int cgx_exec_create_ex(cgx_chain* c, const cgx_exec_opts* opts, void*
   e->c = c;
   c->live_execs++;
   e->o = o;
-  // AUTO: graph modes with PDL capture the chain's dependency DAG (CGX_SYNC_GRAPH) unless the
-  // transport relies on the serial protocol (PRELUDE, DEVICE); those keep the dataflow counters.
-  if (e->o.sync_mode == CGX_SYNC_AUTO) {
-    const cgx_transport t0 = eff_transport(e->o);
-    const bool dag_ok = e->o.mode != CGX_MODE_EAGER && !e->o.no_pdl &&
-                        !(e->o.mode == CGX_MODE_GRAPH_INDIRECT && (t0 == CGX_XPORT_PRELUDE || t0 == CGX_XPORT_DEVICE));
-    e->o.sync_mode = dag_ok ? CGX_SYNC_GRAPH : CGX_SYNC_DATAFLOW;
-  }
+  // AUTO: graph modes with PDL capture the chain's dependency DAG (CGX_SYNC_GRAPH); without PDL
+  // (no_pdl) the serial capture with plain stream edges is kept.
+  if (e->o.sync_mode == CGX_SYNC_AUTO)
+    e->o.sync_mode = (e->o.mode != CGX_MODE_EAGER && !e->o.no_pdl) ? CGX_SYNC_GRAPH : CGX_SYNC_DATAFLOW;
   e->s = static_cast<cudaStream_t>(stream);
   e->first = first;
   e->last = last;
@@ -1311,6 +1328,11 @@ extern "C" int cgx_exec_create_ex(cgx_chain* c, const cgx_exec_opts* opts, void*
         }
         return bail(st);
       }
+    // the DAG's capture streams and events are not referenced by the instantiated graphs
+    for (auto& v : e->dag_ev) if (v) cudaEventDestroy(v);
+    for (auto& v : e->dag_s) if (v) cudaStreamDestroy(v);
+    e->dag_ev.clear();
+    e->dag_s.clear();
     if (t7) {
       // patch list: (device node handle, byte offset of the pointer field, pointer cell); the
       // offsets are the fields the runtime itself patches in SETPARAMS mode — the same ones the

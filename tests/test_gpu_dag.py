@@ -130,11 +130,29 @@ def test_c3_decoder_graph_sync_bitexact(rt):
 
 
 @pytest.mark.parametrize("transport", ["PRELUDE", "DEVICE"])
-def test_graph_sync_unsupported_transports(rt, transport):
+def test_graph_sync_prelude_and_device_transports(rt, transport):
+    """The opaque-kernel prelude (device-side param updates before the fork) and the device-launched
+    replay loop on the DAG capture: bit-identical to the serial dataflow capture and the oracle."""
     cgx, runner = rt
+    spec = wl.c2_chain(n_lanes=20)
+    if transport == "PRELUDE":
+        a, st = _replays(rt, spec, "INDIRECT", transport, 3, "GRAPH", int_mode=True)
+        c, _ = _replays(rt, spec, "INDIRECT", transport, 3, "DATAFLOW", int_mode=True)
+        for r in range(3):
+            env = eval_chain(spec, wl.external_values(spec, r, "int"), st)
+            for k in a[r]:
+                assert np.array_equal(a[r][k], c[r][k]) and np.array_equal(a[r][k], env[k]), (r, k)
+        return
     dev = torch.device("cuda:0")
-    spec = wl.c1_chain()
-    chain = runner.Chain(spec, runner.upload_statics(spec, wl.static_values(spec), dev))
-    with pytest.raises(cgx.CgxError):
-        chain.exec("INDIRECT", transport=transport, sync="GRAPH")
+    st = wl.static_values(spec, "int")
+    chain = runner.Chain(spec, runner.upload_statics(spec, st, dev))
+    ex = chain.exec("INDIRECT", transport="DEVICE", sync="GRAPH")
+    sets = [runner.upload_externals(spec, wl.external_values(spec, r, "int"), dev) for r in range(3)]
+    names = [s_.name for s_ in spec.externals()]
+    ptrs = torch.tensor([[t[n].data_ptr() for n in names] for t in sets], dtype=torch.int64, device=dev)
+    cgx.device_loop(ex.handle, ptrs.data_ptr(), 3, 5)      # replays 0..4 bind sets 0,1,2,0,1
+    torch.cuda.synchronize()
+    env = eval_chain(spec, wl.external_values(spec, 1, "int"), st)
+    for l in range(20):
+        assert np.array_equal(ex.output(f"r{l}"), env[f"r{l}"]), l
     chain.close()
