@@ -824,6 +824,18 @@ def bench_decoder(torch, cgx, runner, wl, stream, dev, peaks):
     exc.close()
     res["us_per_replay"] = arms
     res["tokens_per_s_indirect"] = T * 1e6 / arms["indirect_first_node"]
+    # the same decoder with the residual adds fused into the O-proj / FC2 GEMM epilogues (SURVEY
+    # §8(a) allows it): 84 kernels instead of 108
+    try:
+        fspec = wl.c3_chain(T=T, n_layers=L, fuse_residual=True)
+        fchain = runner.Chain(fspec, runner.upload_statics(fspec, wl.static_values(fspec), dev))
+        fex = fchain.exec("INDIRECT", stream=stream, transport="FIRST_NODE")
+        fus = timed(fex.handle, 300)
+        res["fused_residual"] = {"kernels_per_replay": len(fspec.nodes), "us_per_replay": fus,
+                                 "tokens_per_s": T * 1e6 / fus}
+        fchain.close()
+    except Exception as exn:  # noqa: BLE001
+        res["fused_residual"] = {"error": str(exn)}
     res["rebind_delta_us"] = {k: arms[k] - base for k in ("copy", "indirect_first_node", "indirect_root_params", "setparams")}
     bf16_peak = peaks.get("bf16_tflops", 1590.0)
     hbm = peaks.get("hbm_gbs", 6650.0)

@@ -25,6 +25,10 @@ int decoder_gemm_build(uint32_t M, uint32_t N, uint32_t K, uint32_t flags, const
                        size_t* argbytes, dim3* grid, dim3* block, size_t* smem, const void** func);
 // Make a built GEMM parameter block trigger its PDL dependents only after its wait (T5 node 2).
 void decoder_gemm_set_trigger_after_wait(void* args);
-// Diagnostics: per-CTA %globaltimer trace [cta][8] written by the kernel (nullptr = off).
+// An EXTERNAL residual under INDIRECT: the epilogue reads its base pointer from table[idx].
+void decoder_gemm_set_residual_table(void* args, const uint64_t* table, int32_t idx);
+// Byte offsets of the residual pointer field and its int32 table-index field (patch modes).
+size_t decoder_gemm_residual_field(size_t* tidx_off);
+// Diagnostics: per-CTA %globaltimer trace [cta][16] written by the kernel (nullptr = off).
 void decoder_gemm_set_trace(void* args, unsigned long long* trace);
 }  // namespace cgx

@@ -49,7 +49,9 @@ struct alignas(64) GemmArgs {
   uint32_t M, N, K, flags;
   uint32_t split;             // K splits (gridDim.z)
   uint32_t stages;            // operand ring depth (<= kMaxStages)
-  unsigned long long* trace;  // optional per-CTA %globaltimer trace [cta][8] (diagnostics)
+  unsigned long long* trace;  // optional per-CTA %globaltimer trace [cta][16] (diagnostics)
+  const uint64_t* table;      // INDIRECT: pointer table; residual = table[tres] when tres >= 0
+  int32_t tres;               // table index of an EXTERNAL residual (-1: `residual` is direct)
 };
 
 // ------------------------------------------------------------------ PTX wrappers
@@ -315,10 +317,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
     uint2 res_q[kQMax];                            // S > 1: the residual quads this thread outputs
     if (has_res) {
       pdl_wait();
+      // an EXTERNAL residual under INDIRECT comes from the pointer table (published before the
+      // graph's first consumer; read after this thread's wait)
+      const __nv_bfloat16* resp = a.tres >= 0 ? reinterpret_cast<const __nv_bfloat16*>(ld_table(a.table + a.tres))
+                                              : a.residual;
       if (S == 1) {
         const int m = m0 + (int)row;
         if (m < (int)a.M) {
-          const uint4* rp = reinterpret_cast<const uint4*>(a.residual + (size_t)m * a.N + n0);
+          const uint4* rp = reinterpret_cast<const uint4*>(resp + (size_t)m * a.N + n0);
 #pragma unroll
           for (int i = 0; i < BN / 8; ++i) res_row[i] = rp[i];
         }
@@ -329,7 +335,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
           if (qi < my_rows * kQRow) {
             const int mr = m0 + (int)(my_lo + qi / kQRow);
             if (mr < (int)a.M)
-              res_q[j] = *reinterpret_cast<const uint2*>(a.residual + (size_t)mr * a.N + n0 + 4 * (qi % kQRow));
+              res_q[j] = *reinterpret_cast<const uint2*>(resp + (size_t)mr * a.N + n0 + 4 * (qi % kQRow));
           }
         }
       }
@@ -563,6 +569,16 @@ static const void* kernel_for(int bn) {
   return bn == 128 ? setup_kernel<128>() : bn == 64 ? setup_kernel<64>() : setup_kernel<32>();
 }
 
+void decoder_gemm_set_residual_table(void* args, const uint64_t* table, int32_t idx) {
+  static_cast<GemmArgs*>(args)->table = table;
+  static_cast<GemmArgs*>(args)->tres = idx;
+  static_cast<GemmArgs*>(args)->residual = nullptr;
+}
+size_t decoder_gemm_residual_field(size_t* tidx_off) {
+  *tidx_off = offsetof(GemmArgs, tres);
+  return offsetof(GemmArgs, residual);
+}
+
 void decoder_gemm_set_trace(void* args, unsigned long long* trace) {
   static_cast<GemmArgs*>(args)->trace = trace;
 }
@@ -605,6 +621,8 @@ int decoder_gemm_build(uint32_t M, uint32_t N, uint32_t K, uint32_t flags, const
   g->split = sp;
   g->stages = stages;
   g->trace = nullptr;
+  g->table = nullptr;
+  g->tres = -1;
 
   return CGX_OK;
 }

@@ -581,11 +581,16 @@ static int build_launch(cgx_exec* e, int k, Launch& l) {
       return CGX_OK;
     }
     case CGX_OP_GEMM_BF16: {
-      for (int i = 0; i < n.n_in; ++i)
+      // EXTERNAL operands: A is read through a TMA tensor map (encoded at capture) and the weights
+      // and bias are STATIC by construction, so only the residual can be rebound; under INDIRECT
+      // the epilogue reads its base pointer from the table, in patch modes the pointer field is
+      // patched like any other, under COPY it is the placeholder
+      const bool res_ext = (n.attr.flags & CGX_GEMM_RESIDUAL) && is_ext(n.in[3]);
+      for (int i = 0; i < 3; ++i)
         if (is_ext(n.in[i])) {
-          if (indirect)
-            return fail(CGX_E_UNSUPPORTED, "gemm: an EXTERNAL operand of a GEMM needs the prelude path (NEXT-1)");
-          if (i != 0 && i != 3) return fail(CGX_E_UNSUPPORTED, "gemm: external weights");
+          if (i == 0 && !indirect && !patch) continue;                   // COPY: placeholder
+          return fail(CGX_E_UNSUPPORTED, i == 0 ? "gemm: an EXTERNAL A operand needs a rebuilt tensor map (COPY arm only)"
+                                                : "gemm: external weights/bias");
         }
       void* A = slot_ptr(n.in[0]);
       void* W = slot_ptr(n.in[1]);
@@ -604,8 +609,16 @@ static int build_launch(cgx_exec* e, int k, Launch& l) {
         e->gemm_cnt_off += c1;
       }
       l.cluster_z = l.grid.z;
-      if (patch && (is_ext(n.in[0]) || ((n.attr.flags & CGX_GEMM_RESIDUAL) && is_ext(n.in[3]))))
-        return fail(CGX_E_UNSUPPORTED, "gemm: external A/residual needs a rebuilt tensor map");
+      if (res_ext) {
+        const int j = c->slots[n.in[3]].ext_j;
+        if (indirect) {
+          decoder_gemm_set_residual_table(l.args.p, e->d_table, j);
+        } else if (patch) {
+          size_t tidx = 0;
+          const size_t off = decoder_gemm_residual_field(&tidx);
+          l.ext.push_back({off, tidx, j});
+        }
+      }
       return CGX_OK;
     }
     case CGX_OP_ATTN_CAUSAL: {
@@ -1117,11 +1130,16 @@ static int capture_graph(cgx_exec* e, int gi) {
   if (e->o.mode == CGX_MODE_GRAPH_INDIRECT && t == CGX_XPORT_H2D_PINGPONG) {
     // graph gi reads table gi: the `table` field is the first member of ElemArgs and LnArgs
     uint64_t* tab = gi == 0 ? e->d_table : e->d_table2;
-    for (auto& l : e->L)
+    for (auto& l : e->L) {
       if (l.kind == LK_KERNEL && (e->c->nodes[l.node].op <= CGX_OP_REDUCE_SUM ||
                                   e->c->nodes[l.node].op == CGX_OP_SCALE_T ||
                                   e->c->nodes[l.node].op == CGX_OP_LAYERNORM))
         memcpy(l.args.p, &tab, sizeof(tab));
+      const Node& gn = e->c->nodes[l.node];
+      if (l.kind == LK_KERNEL && gn.op == CGX_OP_GEMM_BF16 && (gn.attr.flags & CGX_GEMM_RESIDUAL) &&
+          e->c->slots[gn.in[3]].kind == CGX_SLOT_EXTERNAL)
+        decoder_gemm_set_residual_table(l.args.p, tab, e->c->slots[gn.in[3]].ext_j);
+    }
   }
   CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
   bool after_root = false;

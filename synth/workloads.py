@@ -159,7 +159,8 @@ def c2_chain(n_lanes: int = 64, scale_tail: int = 8, reduce_cols: int = 256) -> 
 GPT2 = dict(d=768, heads=12, head_dim=64, d_ff=3072, eps=1e-5)
 
 
-def c3_chain(T: int = 128, n_layers: int = 12, tp: int = 1, rank: int = 0) -> ChainSpec:
+def c3_chain(T: int = 128, n_layers: int = 12, tp: int = 1, rank: int = 0,
+             fuse_residual: bool = False) -> ChainSpec:
     """GPT-2-small-shaped decoder chain: per layer LN1, QKV GEMM+bias,
     causal attention, O-proj GEMM+bias, residual ADD, LN2, FC1 GEMM+bias+GELU, FC2 GEMM+bias,
     residual ADD. Only x is EXTERNAL; weights are STATIC (SURVEY ambiguity 4).
@@ -167,7 +168,12 @@ def c3_chain(T: int = 128, n_layers: int = 12, tp: int = 1, rank: int = 0) -> Ch
     With tp > 1 this is rank `rank`'s shard: QKV and FC1 column-sharded
     (heads / d_ff split p ways; at p=8 the 12 heads are padded to 16 with zero weights,
     SURVEY ambiguity 13), O-proj and FC2 row-sharded with their bias on rank 0 only, each
-    followed by ALLREDUCE_SUM. Shard weights are SLICES of the TP=1 weights (see tp_weight)."""
+    followed by ALLREDUCE_SUM. Shard weights are SLICES of the TP=1 weights (see tp_weight).
+
+    fuse_residual (tp == 1 only; SURVEY §8(a) "residual adds may be fused into the GEMM epilogue"):
+    the O-proj and FC2 GEMMs take the residual stream as a 4th input and write h1 / h2 directly,
+    7 nodes per layer instead of 9 (one bf16 rounding of A W^T + b + residual instead of two)."""
+    assert not (fuse_residual and tp > 1), "residual fusion needs the un-reduced sum (TP = 1)"
     d, hd, dff, eps = GPT2["d"], GPT2["head_dim"], GPT2["d_ff"], GPT2["eps"]
     H = GPT2["heads"]
     Hp = H if H % tp == 0 else ((H + tp - 1) // tp) * tp   # 12 -> 16 at tp=8
@@ -192,7 +198,27 @@ def c3_chain(T: int = 128, n_layers: int = 12, tp: int = 1, rank: int = 0) -> Ch
                   SlotSpec(p + "b_fc2", STATIC, "bf16", d, "bias")]
         for nm, n in (("a", T * d), ("qkv", T * 3 * hl * hd), ("att", T * hl * hd), ("o", T * d),
                       ("h1", T * d), ("a2", T * d), ("f", T * fl), ("g", T * d), ("h2", T * d)):
-            slots.append(SlotSpec(p + nm, INTERNAL, "bf16", n))
+            slots.append(SlotSpec(p + nm, INTERNAL, "bf16", n))   # (o, g stay when fused: same slot
+                                                                    # indices -> same seeded weights)
+        if fuse_residual:
+            nodes += [
+                NodeSpec("LAYERNORM", (h, p + "ln1_g", p + "ln1_b"), p + "a",
+                         {"rows": T, "cols": d, "eps": eps}),
+                NodeSpec("GEMM_BF16", (p + "a", p + "w_qkv", p + "b_qkv"), p + "qkv",
+                         {"M": T, "N": 3 * hl * hd, "K": d, "bias": True, "gelu": False}),
+                NodeSpec("ATTN_CAUSAL", (p + "qkv",), p + "att",
+                         {"T": T, "H": hl, "D": hd, "scale": 0.125}),
+                NodeSpec("GEMM_BF16", (p + "att", p + "w_o", p + "b_o", h), p + "h1",
+                         {"M": T, "N": d, "K": hl * hd, "bias": True, "gelu": False, "residual": True}),
+                NodeSpec("LAYERNORM", (p + "h1", p + "ln2_g", p + "ln2_b"), p + "a2",
+                         {"rows": T, "cols": d, "eps": eps}),
+                NodeSpec("GEMM_BF16", (p + "a2", p + "w_fc1", p + "b_fc1"), p + "f",
+                         {"M": T, "N": fl, "K": d, "bias": True, "gelu": True}),
+                NodeSpec("GEMM_BF16", (p + "f", p + "w_fc2", p + "b_fc2", p + "h1"), p + "h2",
+                         {"M": T, "N": d, "K": fl, "bias": True, "gelu": False, "residual": True}),
+            ]
+            h = p + "h2"
+            continue
         bias_ro = (rank == 0)
         nodes += [
             NodeSpec("LAYERNORM", (h, p + "ln1_g", p + "ln1_b"), p + "a",
@@ -222,6 +248,8 @@ def c3_chain(T: int = 128, n_layers: int = 12, tp: int = 1, rank: int = 0) -> Ch
         nodes.append(NodeSpec("ADD", (p + "h1", p + "g"), p + "h2", {"n": T * d}))
         h = p + "h2"
     name = f"C3_T{T}_L{n_layers}" if tp == 1 else f"C5_T{T}_L{n_layers}_tp{tp}_r{rank}"
+    if fuse_residual:
+        name += "_fused"
     return ChainSpec(name, slots, nodes, [(0, len(nodes) - 1)])
 
 

@@ -163,7 +163,8 @@ def _node_local_check(spec, st, ext, got):
         if node.op == "LAYERNORM":
             ref = ops.layernorm(env[node.ins[0]], env[node.ins[1]], env[node.ins[2]], a)
         elif node.op == "GEMM_BF16":
-            ref = ops.gemm_bf16(env[node.ins[0]], env[node.ins[1]], env[node.ins[2]], a)
+            res = env[node.ins[3]] if len(node.ins) > 3 else None
+            ref = ops.gemm_bf16(env[node.ins[0]], env[node.ins[1]], env[node.ins[2]], a, res)
         elif node.op == "ATTN_CAUSAL":
             ref = ops.attn_causal(env[node.ins[0]], a)
         elif node.op == "ADD":
@@ -193,6 +194,30 @@ def test_c3_decoder_chain(rt, n_layers):
         assert np.linalg.norm(g - o) / np.linalg.norm(o) <= 2e-2
         for mode in ("EAGER", "COPY", "SETPARAMS", "FIRST_NODE", "H2D_PINGPONG"):   # bit-identical across arms
             for k in got:
+                assert np.array_equal(res[mode][r][k], got[k]), (mode, k)
+
+
+@pytest.mark.parametrize("n_layers", [1, 12])
+def test_c3_fused_residual_chain(rt, n_layers):
+    """The decoder with the residual adds fused into the O-proj / FC2 epilogues (7 nodes per
+    layer): node-local and end-to-end parity, arms bit-identical."""
+    spec = wl.c3_chain(T=128, n_layers=n_layers, fuse_residual=True)
+    assert len(spec.nodes) == 7 * n_layers
+    st = wl.static_values(spec)
+    res = {mode: _run(rt, spec, mode, 2, st) for mode in ("EAGER", "COPY", "INDIRECT", "SETPARAMS")}
+    for xp in ("FIRST_NODE", "H2D", "H2D_PINGPONG"):          # layer 0's residual is the EXTERNAL x
+        res[xp] = _run(rt, spec, "INDIRECT", 2, st, transport=xp)
+    for r in range(2):
+        ext = wl.external_values(spec, r)
+        got = res["INDIRECT"][r]
+        written = {n.out for n in spec.nodes}
+        _node_local_check(spec, st, ext, got)
+        env = eval_chain(spec, ext, st)
+        last = spec.nodes[-1].out
+        g, o = bits_to_f64(got[last]), env[last]
+        assert np.linalg.norm(g - o) / np.linalg.norm(o) <= 2e-2
+        for mode in ("EAGER", "COPY", "SETPARAMS", "FIRST_NODE", "H2D", "H2D_PINGPONG"):
+            for k in written:
                 assert np.array_equal(res[mode][r][k], got[k]), (mode, k)
 
 

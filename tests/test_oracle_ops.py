@@ -201,3 +201,19 @@ def test_scale_t_is_scale_imm_with_a_device_scalar():
     a = sm.uniform_f32(sm.SEED, 30, 1000)
     assert np.array_equal(ops.scale_t(a, np.array([0.75], np.float32), {}),
                           ops.scale_imm(a, {"scalar": 0.75}))
+
+
+def test_c3_fused_residual_matches_unfused_within_bf16():
+    """residual adds may be fused into the GEMM epilogue. The fused chain (7 nodes per
+    layer) keeps the same seeded weights (same slot indices) and differs from the 9-node chain only
+    by the intermediate bf16 rounding of the GEMM output before the add: a few bf16 ulps."""
+    from oracle.chain import eval_chain
+    from synth import workloads as wl
+    f = wl.c3_chain(T=8, n_layers=2, fuse_residual=True)
+    u = wl.c3_chain(T=8, n_layers=2)
+    assert len(f.nodes) == 14 and len(u.nodes) == 18
+    ef = eval_chain(f, wl.external_values(f, 0), wl.static_values(f))
+    eu = eval_chain(u, wl.external_values(u, 0), wl.static_values(u))
+    a, b = ef["L1.h2"], eu["L1.h2"]
+    assert np.linalg.norm(a - b) / np.linalg.norm(b) < 1e-2
+    assert not np.array_equal(a, b)          # the fusion does change the rounding
