@@ -827,6 +827,35 @@ def bench_decoder(torch, cgx, runner, wl, stream, dev, peaks):
     exc.close()
     res["us_per_replay"] = arms
     res["tokens_per_s_indirect"] = T * 1e6 / arms["indirect_first_node"]
+    # the T = 1 decode variant (SURVEY §8(a) a7 "T=1 uses swap-AB or CUDA cores"): small-M GEMV path
+    try:
+        dspec = wl.c3_chain(T=1, n_layers=L)
+        dchain = runner.Chain(dspec, runner.upload_statics(dspec, wl.static_values(dspec), dev))
+        dxs = [runner.host_to_device(wl.slot_values(dspec, "x", r), "bf16", dev) for r in range(4)]
+        dptrs = [cgx.ptr_array([x.data_ptr()]) for x in dxs]
+        dex = dchain.exec("INDIRECT", stream=stream, transport="FIRST_NODE")
+        for i in range(20):
+            LIB.cgx_bind(dex.handle, dptrs[i % 4], 1)
+            LIB.cgx_launch(dex.handle)
+        best_d = 1e30
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            stream.synchronize()
+            e0.record(stream)
+            for i in range(300):
+                LIB.cgx_bind(dex.handle, dptrs[i % 4], 1)
+                LIB.cgx_launch(dex.handle)
+            e1.record(stream)
+            e1.synchronize()
+            best_d = min(best_d, e0.elapsed_time(e1) * 1e3 / 300)
+        res["decode_t1"] = {"kernels_per_replay": len(dspec.nodes), "us_per_replay": best_d,
+                            "tokens_per_s": 1e6 / best_d,
+                            "weight_GBps": 12 * 14.16e6 / (best_d * 1e-6) / 1e9,
+                            "note": "12 layers, T = 1: GEMM nodes on the small-M weight-stream path "
+                                    "(k_gemv_bf16); 170 MB of weights per replay"}
+        dchain.close()
+    except Exception as exn:  # noqa: BLE001
+        res["decode_t1"] = {"error": str(exn)}
     # the same decoder with the residual adds fused into the O-proj / FC2 GEMM epilogues (SURVEY
     # §8(a) allows it): 84 kernels instead of 108
     try:

@@ -52,6 +52,8 @@ struct alignas(64) GemmArgs {
   unsigned long long* trace;  // optional per-CTA %globaltimer trace [cta][16] (diagnostics)
   const uint64_t* table;      // INDIRECT: pointer table; residual = table[tres] when tres >= 0
   int32_t tres;               // table index of an EXTERNAL residual (-1: `residual` is direct)
+  const __nv_bfloat16* a_ptr; // small-M path (k_gemv_bf16): A and W by plain pointers
+  const __nv_bfloat16* w_ptr;
 };
 
 // ------------------------------------------------------------------ PTX wrappers
@@ -464,6 +466,96 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
   }
 }
 
+// ------------------------------------------------------------------ small-M path (decode, T <= 8)
+// At M <= 4 (the C3 T = 1 decode variant) a 128-row UMMA tile wastes 127/128 of the tensor core and
+// still pays the TMA/TMEM latency chain, while the node is a pure weight stream (N x K x 2 bytes).
+// One warp per kEvRows output columns: the warp streams those W rows (STATIC) into registers
+// BEFORE griddepcontrol.wait — the whole weight matrix is in flight while the predecessor drains —
+// then loads the M activation rows (L2), forms M dot products per row in fp32 (fixed lane order +
+// fixed shuffle tree: deterministic) and lane 0 applies bias / GELU / residual and rounds once.
+static constexpr int kGvWarps = 8;
+static constexpr int kGvMaxM = 4;    // decode replays measured faster than tcgen05 up to T = 4, not at 8
+static constexpr int kGvMaxKV = 12;          // 16-B vectors per lane per row: K <= 12 * 256 = 3072
+
+__device__ __forceinline__ float bf16lo(uint32_t u) { return __uint_as_float(u << 16); }
+__device__ __forceinline__ float bf16hi(uint32_t u) { return __uint_as_float(u & 0xffff0000u); }
+
+template <int R, int kGvKV>
+__global__ void __launch_bounds__(kGvWarps * 32) k_gemv_bf16(const __grid_constant__ GemmArgs a) {
+  const bool late_trigger = a.flags & kGemmTriggerAfterWait;
+  if (!late_trigger) pdl_trigger();
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t n0 = (blockIdx.x * kGvWarps + warp) * R;     // this warp's first output column
+  const uint32_t kv = a.K / 8;                                  // 16-B vectors per row
+  // ---- W rows n0 .. n0+R-1 (STATIC): all loads in flight before the wait
+  uint4 w[R][kGvKV];
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int i = 0; i < kGvKV; ++i) {
+      const uint32_t v = lane + 32u * i;
+      if (n0 + r < a.N && v < kv) w[r][i] = __ldg(reinterpret_cast<const uint4*>(a.w_ptr + (size_t)(n0 + r) * a.K) + v);
+    }
+  pdl_wait();
+  if (late_trigger) pdl_trigger();
+  float acc[R][kGvMaxM];
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int m = 0; m < kGvMaxM; ++m) acc[r][m] = 0.f;
+  for (uint32_t m = 0; m < a.M; ++m) {
+    uint4 x[kGvKV];
+    const uint4* ar = reinterpret_cast<const uint4*>(a.a_ptr + (size_t)m * a.K);
+#pragma unroll
+    for (int i = 0; i < kGvKV; ++i) {
+      const uint32_t v = lane + 32u * i;
+      if (v < kv) x[i] = ar[v];
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+      for (int i = 0; i < kGvKV; ++i) {
+        if (lane + 32u * i < kv) {
+          const uint32_t* xp = reinterpret_cast<const uint32_t*>(&x[i]);
+          const uint32_t* wp = reinterpret_cast<const uint32_t*>(&w[r][i]);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            s0 = fmaf(bf16lo(xp[q]), bf16lo(wp[q]), s0);
+            s1 = fmaf(bf16hi(xp[q]), bf16hi(wp[q]), s1);
+          }
+        }
+      }
+      float t = s0 + s1;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+#pragma unroll
+      for (int mm = 0; mm < kGvMaxM; ++mm)
+        if (mm == (int)m) acc[r][mm] = t;
+    }
+  }
+  if (lane != 0) return;
+  const bool has_bias = a.flags & CGX_GEMM_BIAS, gelu = a.flags & CGX_GEMM_GELU;
+  const bool has_res = a.flags & CGX_GEMM_RESIDUAL;
+  const __nv_bfloat16* resp = !has_res ? nullptr
+                              : a.tres >= 0 ? reinterpret_cast<const __nv_bfloat16*>(ld_table(a.table + a.tres))
+                                            : a.residual;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const uint32_t n = n0 + r;
+    if (n >= a.N) break;
+    const float b = has_bias ? __bfloat162float(a.bias[n]) : 0.f;
+#pragma unroll
+    for (int m = 0; m < kGvMaxM; ++m) {
+      if (m >= (int)a.M) break;
+      float v = acc[r][m] + b;
+      if (gelu) v = gelu_tanh(v);
+      if (has_res) v += __bfloat162float(resp[(size_t)m * a.N + n]);
+      a.out[(size_t)m * a.N + n] = __float2bfloat16_rn(v);
+    }
+  }
+}
+
 // ------------------------------------------------------------------ host side
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 static std::once_flag g_encode_once;
@@ -587,14 +679,46 @@ void decoder_gemm_set_trigger_after_wait(void* args) {
   static_cast<GemmArgs*>(args)->flags |= kGemmTriggerAfterWait;
 }
 
+static bool gemv_shape(uint32_t M, uint32_t N, uint32_t K) {
+  const char* ngv = getenv("CGX_GEMM_NO_GEMV");         // measurement / test knob: force tcgen05
+  return !(ngv && ngv[0] == '1') && M >= 1 && M <= (uint32_t)kGvMaxM && N >= 1 && K >= 8 && K % 8 == 0 &&
+         K <= (uint32_t)kGvMaxKV * 256;
+}
+
 bool decoder_gemm_supported(uint32_t M, uint32_t N, uint32_t K) {
-  return M >= 1 && K >= kBK && K % kBK == 0 && (N % 32 == 0);
+  return gemv_shape(M, N, K) || (M >= 1 && K >= kBK && K % kBK == 0 && (N % 32 == 0));
 }
 
 int decoder_gemm_build(uint32_t M, uint32_t N, uint32_t K, uint32_t flags, const void* A, const void* W,
                        const void* bias, const void* residual, void* out, void* ws, void* cnt, void* args_out,
                        size_t* argbytes, dim3* grid, dim3* block, size_t* smem, const void** func) {
   if (!decoder_gemm_supported(M, N, K)) return CGX_E_UNSUPPORTED;
+  if (gemv_shape(M, N, K)) {
+    // small-M (decode) path: one output column per warp (more warps in flight beat more rows per
+    // warp at these sizes), per-lane vector count picked from K
+    const int R = 1;
+    *argbytes = sizeof(GemmArgs);
+    *grid = dim3((N + kGvWarps * R - 1) / (kGvWarps * R));
+    *block = dim3(kGvWarps * 32);
+    *smem = 0;
+    *func = K <= 768 ? (const void*)k_gemv_bf16<1, 3> : K <= 1536 ? (const void*)k_gemv_bf16<1, 6>
+                                                                   : (const void*)k_gemv_bf16<1, 12>;
+    if (!args_out) return CGX_OK;
+    GemmArgs* g = static_cast<GemmArgs*>(args_out);
+    memset(g, 0, sizeof(GemmArgs));
+    g->a_ptr = static_cast<const __nv_bfloat16*>(A);
+    g->w_ptr = static_cast<const __nv_bfloat16*>(W);
+    g->bias = static_cast<const __nv_bfloat16*>(bias);
+    g->residual = static_cast<const __nv_bfloat16*>(residual);
+    g->out = static_cast<__nv_bfloat16*>(out);
+    g->M = M;
+    g->N = N;
+    g->K = K;
+    g->flags = flags;
+    g->split = 1;
+    g->tres = -1;
+    return CGX_OK;
+  }
   int bn = 0;
   uint32_t sp = 1;
   pick_tiling(M, N, K, &bn, &sp);
@@ -623,7 +747,8 @@ int decoder_gemm_build(uint32_t M, uint32_t N, uint32_t K, uint32_t flags, const
   g->trace = nullptr;
   g->table = nullptr;
   g->tres = -1;
-
+  g->a_ptr = static_cast<const __nv_bfloat16*>(A);
+  g->w_ptr = static_cast<const __nv_bfloat16*>(W);
   return CGX_OK;
 }
 

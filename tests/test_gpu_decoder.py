@@ -107,6 +107,32 @@ def test_gemm_split_tilings_integer_exact(rt, monkeypatch, M, N, K, tiling):
         assert np.array_equal(got["y"], bf16_bits(env["y"])), f"tiling {tiling}"
 
 
+# Small-M (decode) path k_gemv_bf16 (M <= 4; M = 5, 8 exercise the tcgen05 kernel) and, with CGX_GEMM_NO_GEMV=1, the tcgen05 kernel at
+# the same shapes; every epilogue; integer mode makes both bit-exact against the oracle.
+@pytest.mark.parametrize("M", [1, 2, 5, 8])
+@pytest.mark.parametrize("N,K,gelu,res", [(2304, 768, False, False), (768, 3072, False, True),
+                                          (3072, 768, True, False), (768, 768, False, True), (96, 1032, False, False)])
+@pytest.mark.parametrize("gemv", [True, False])
+def test_gemm_small_m_paths(rt, monkeypatch, M, N, K, gelu, res, gemv):
+    if not gemv:
+        if K % 64:
+            pytest.skip("tcgen05 path needs K % 64 == 0")
+        monkeypatch.setenv("CGX_GEMM_NO_GEMV", "1")
+    spec = _gemm_chain(M, N, K, gelu=gelu, residual=res)
+    if gelu:
+        st = wl.static_values(spec)
+        outs = _run(rt, spec, "INDIRECT", 2, st)
+        for r, got in enumerate(outs):
+            env = eval_chain(spec, wl.external_values(spec, r), st)
+            _close(got["y"], env["y"], f"gemm M={M} gemv={gemv}")
+        return
+    st = wl.static_values(spec, mode="int")
+    outs = _run(rt, spec, "INDIRECT", 2, st, mode_vals="int")
+    for r, got in enumerate(outs):
+        env = eval_chain(spec, wl.external_values(spec, r, "int"), st)
+        assert np.array_equal(got["y"], bf16_bits(env["y"])), (M, N, K, gemv)
+
+
 def test_gemm_gelu_and_residual(rt):
     for gelu, res in ((True, False), (False, True), (True, True)):
         spec = _gemm_chain(128, 3072 if gelu else 768, 768, gelu=gelu, residual=res)
