@@ -114,9 +114,9 @@ def test_gemm_split_tilings_integer_exact(rt, monkeypatch, M, N, K, tiling):
                                           (3072, 768, True, False), (768, 768, False, True), (96, 1032, False, False)])
 @pytest.mark.parametrize("gemv", [True, False])
 def test_gemm_small_m_paths(rt, monkeypatch, M, N, K, gelu, res, gemv):
+    if (not gemv or M > 4) and K % 64:
+        pytest.skip("the tcgen05 kernel needs K % 64 == 0 (the GEMV path covers M <= 4)")
     if not gemv:
-        if K % 64:
-            pytest.skip("tcgen05 path needs K % 64 == 0")
         monkeypatch.setenv("CGX_GEMM_NO_GEMV", "1")
     spec = _gemm_chain(M, N, K, gelu=gelu, residual=res)
     if gelu:
