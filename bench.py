@@ -152,6 +152,54 @@ def run_oracle_replays(spec, budget_s: float, max_replays: int = 1000):
     return n, dt
 
 
+def run_oracle_timings():
+    """SURVEY §8(d) 'Oracle timing' column: the CPU oracle, one thread, on bounded samples of the
+    other configs (C2's is `cpu_baseline`). Seconds of wall time."""
+    from threadpoolctl import threadpool_limits
+
+    from oracle import capture as ocap
+    from oracle.chain import eval_chain, eval_chain_tp
+    from synth import workloads as wl
+    out = {}
+    with threadpool_limits(limits=1):
+        # C1: 10 replays x {COPY, INDIRECT, SETPARAMS} plus the STALE control
+        spec = wl.c1_chain()
+        t0 = time.perf_counter()
+        for mode in ("COPY", "INDIRECT", "SETPARAMS", "STALE"):
+            mem = ocap.Memory()
+            saddr = ocap.load_statics(spec, mem, wl.static_values(spec))
+            inputs = [ocap.load_inputs(spec, mem, wl.external_values(spec, r)) for r in range(10)]
+            ex = ocap.CapturedExec(spec, mode, mem, saddr, inputs[0] if mode == "STALE" else None)
+            for r in range(10):
+                if mode != "STALE":
+                    ex.bind(inputs[r])
+                ex.replay()
+        out["C1_10_replays_x4_arms_s"] = time.perf_counter() - t0
+        # C3: one step of the 12-layer decoder (f64 NumPy)
+        spec = wl.c3_chain(T=128, n_layers=12)
+        st, ext = wl.static_values(spec), wl.external_values(spec, 0)
+        t0 = time.perf_counter()
+        eval_chain(spec, ext, st)
+        out["C3_one_step_12_layers_s"] = time.perf_counter() - t0
+        # C4: the window chain at every sweep point up to 64 MiB (the kernels read the window)
+        t0 = time.perf_counter()
+        for S in [1024 * 4 ** k for k in range(9)]:
+            spec = wl.c4_chain(S, window_mode=True)
+            eval_chain(spec, wl.external_values(spec, 0), wl.static_values(spec))
+        out["C4_window_points_to_64MiB_s"] = time.perf_counter() - t0
+        # C5: TP = 2 lockstep ranks (partials + their reduction), 1 layer
+        full = wl.c3_chain(T=128, n_layers=1)
+        chains = [wl.c3_chain(T=128, n_layers=1, tp=2, rank=r) for r in range(2)]
+        stats = [wl.static_values(c, tp=2, rank=r, full=full) for r, c in enumerate(chains)]
+        exts = [wl.external_values(c, 0) for c in chains]
+        t0 = time.perf_counter()
+        eval_chain_tp(chains, exts, stats)
+        out["C5_tp2_one_layer_s"] = time.perf_counter() - t0
+    out["cores"] = 1
+    out["host"] = cpu_info()
+    return out
+
+
 # ------------------------------------------------------------------------------- reference arm
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
@@ -775,7 +823,11 @@ def run_extras(args, torch, cgx, runner, wl, sm, spec, chain, stream, sets, set_
     except Exception as exn:  # noqa: BLE001
         out["copy_kernel"] = {"error": str(exn)}
 
-    # ---------------- CPU oracle baseline (bounded sample)
+    # ---------------- CPU oracle baseline (bounded sample) and the other configs' oracle timings
+    try:
+        out["oracle_timings"] = run_oracle_timings()
+    except Exception as exn:  # noqa: BLE001
+        out["oracle_timings"] = {"error": str(exn)}
     n, dt = run_oracle_replays(spec, args.cpu_budget_s)
     out["cpu_baseline"] = {"value": n / dt, "unit": "iters/s", "cores": 1, "kind": "oracle",
                            "sample": f"{n} C2 replays (INDIRECT bind + replay, NumPy f32/f64, "
