@@ -317,6 +317,24 @@ int cgx_copy(void* dst, const void* src, uint64_t nbytes, void* cuda_stream);
 int cgx_fill_uniform_f32(void* dptr, uint64_t n, uint64_t seed, uint64_t stream_id, void* cuda_stream);
 
 /* ---- NCCL bootstrap (ncclComm_t for ALLREDUCE_SUM; caller owns it) ------------------------- */
+/* Tensor-parallel all-reduce over peer memory (replaces ncclAllReduce for the
+ * chain's ALLREDUCE_SUM nodes once set). Every rank owns one region of cgx_peer_buffer_bytes()
+ * bytes of device memory, 256-B aligned and ZERO-FILLED before any exec of the chain is created;
+ * `bases[r]` is rank r's region as mapped in THIS process (cudaIpc via cgx_ipc_open across
+ * processes, or the plain pointer when ranks share a device). An ALLREDUCE_SUM node then runs a
+ * one-shot kernel: each rank pushes its partial into slot `rank` of every region (P2P stores over
+ * NVLink), publishes a per-CTA generation flag with sys-scope release, waits for every source, and
+ * sums the slots in fixed rank order (bit-identical results on all ranks). Requirements: n % 8 == 0,
+ * n <= max_elems, world <= 8, <= 64 ALLREDUCE_SUM nodes, every rank creates its execs and replays in
+ * the same order, and each ALLREDUCE_SUM depends (through the data flow) on the previous one.
+ * Call before the chain's first exec. Errors: CGX_E_INVALID_ARG, CGX_E_MISALIGNED, CGX_E_STATE. */
+int cgx_peer_buffer_bytes(int world, uint64_t max_elems, uint64_t* bytes);
+int cgx_chain_set_peers(cgx_chain* c, int rank, int world, void* const* bases, uint64_t max_elems);
+/* CUDA IPC helpers for the multi-process case: a device allocation's 64-byte handle, and mapping /
+ * unmapping a peer's allocation in this process. */
+int cgx_ipc_handle(void* dptr, void* handle_out /* 64 bytes */);
+int cgx_ipc_open(const void* handle /* 64 bytes */, void** dptr_out);
+int cgx_ipc_close(void* dptr);
 int cgx_nccl_unique_id(void* id_out /* 128 bytes */);
 int cgx_nccl_comm_init(int nranks, int rank, const void* id /* 128 bytes */, int device, void** comm_out);
 int cgx_nccl_comm_destroy(void* comm);

@@ -118,6 +118,11 @@ def _load():
         "cgx_nccl_unique_id": ([VP], I),
         "cgx_nccl_comm_init": ([I, I, VP, I, P(VP)], I),
         "cgx_nccl_comm_destroy": ([VP], I),
+        "cgx_peer_buffer_bytes": ([I, U64, P(U64)], I),
+        "cgx_chain_set_peers": ([VP, I, I, P(VP), U64], I),
+        "cgx_ipc_handle": ([VP, VP], I),
+        "cgx_ipc_open": ([VP, P(VP)], I),
+        "cgx_ipc_close": ([VP], I),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -134,7 +139,8 @@ EXPORTED = ("cgx_version", "cgx_last_error", "cgx_chain_create", "cgx_chain_add_
             "cgx_debug_setparam_nodes", "cgx_exec_destroy", "cgx_profile", "cgx_select",
             "cgx_dispatch_floor", "cgx_fill_uniform_f32", "cgx_copy", "cgx_graph_floor", "cgx_kernel_times", "cgx_find_param_offset",
             "cgx_debug_param_image", "cgx_debug_ext_field_offsets", "cgx_debug_gemm_trace", "cgx_debug_node_trace", "cgx_device_loop", "cgx_nccl_unique_id",
-            "cgx_nccl_comm_init", "cgx_nccl_comm_destroy")
+            "cgx_nccl_comm_init", "cgx_nccl_comm_destroy", "cgx_peer_buffer_bytes", "cgx_chain_set_peers",
+            "cgx_ipc_handle", "cgx_ipc_open", "cgx_ipc_close")
 
 
 def _ck(status: int, fn: str):
@@ -348,3 +354,30 @@ def nccl_comm_init(nranks: int, rank: int, uid: bytes, device: int) -> int:
 
 def nccl_comm_destroy(comm: int):
     _ck(LIB.cgx_nccl_comm_destroy(comm), "cgx_nccl_comm_destroy")
+
+
+def peer_buffer_bytes(world: int, max_elems: int) -> int:
+    b = C.c_uint64()
+    _ck(LIB.cgx_peer_buffer_bytes(world, max_elems, C.byref(b)), "cgx_peer_buffer_bytes")
+    return b.value
+
+
+def chain_set_peers(chain: int, rank: int, world: int, bases, max_elems: int) -> None:
+    arr = (C.c_void_p * world)(*bases)
+    _ck(LIB.cgx_chain_set_peers(chain, rank, world, arr, max_elems), "cgx_chain_set_peers")
+
+
+def ipc_handle(dptr: int) -> bytes:
+    buf = C.create_string_buffer(64)
+    _ck(LIB.cgx_ipc_handle(C.c_void_p(dptr), buf), "cgx_ipc_handle")
+    return buf.raw
+
+
+def ipc_open(handle: bytes) -> int:
+    p = C.c_void_p()
+    _ck(LIB.cgx_ipc_open(C.create_string_buffer(handle, 64), C.byref(p)), "cgx_ipc_open")
+    return p.value
+
+
+def ipc_close(dptr: int) -> None:
+    _ck(LIB.cgx_ipc_close(C.c_void_p(dptr)), "cgx_ipc_close")

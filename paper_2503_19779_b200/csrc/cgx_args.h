@@ -5,6 +5,7 @@
 // each pointer argument with a pointer-to-pointer").
 #pragma once
 #include <stdint.h>
+#include <cuda_bf16.h>
 
 namespace cgx {
 
@@ -145,6 +146,22 @@ struct ArgsTW<Base, 0> {
 // capacity for the T5 first node (0 = plain kernel; else 8, 64 or 512 pointers).
 extern "C++" {
 namespace cgx {
+// Peer all-reduce (k_allreduce_peer, cgx_chain_set_peers): per-rank region = receive data
+// [2 parity][world][slot_elems] bf16, then flags [kArMaxNodes][kArMaxWorld][kArMaxCtas] uint32.
+static constexpr int kArMaxWorld = 8;
+static constexpr int kArMaxCtas = 64;
+static constexpr int kArMaxNodes = 64;
+struct PeerArArgs {
+  const __nv_bfloat16* in;
+  __nv_bfloat16* out;
+  uint64_t n;                          // elements (multiple of 8)
+  uint64_t slot_elems;                 // elements per receive slot
+  uint32_t rank, world, ar_index, n_ar, flags;
+  uint32_t* counters;                  // chain-owned [kArMaxNodes][kArMaxCtas] generations
+  __nv_bfloat16* recv[kArMaxWorld];    // every rank's receive data (mapped in this process)
+  uint32_t* flags_of[kArMaxWorld];     // every rank's flag array
+};
+const void* kfn_allreduce_peer();
 static constexpr int kGatherMax = 64;
 struct GatherArgs {
   const void* src[kGatherMax];

@@ -478,6 +478,87 @@ __global__ void __launch_bounds__(256) k_gather(const __grid_constant__ GatherAr
   for (uint64_t j = (n16 << 4) + threadIdx.x; j < nb; j += blockDim.x) dst[j] = src[j];
 }
 
+// ---------------------------------------------------------------------------- peer all-reduce
+// One-shot bf16 sum across `world` ranks over peer memory (NVLink P2P stores on an NVSwitch box;
+// plain device memory when the ranks share one GPU): CTA c owns vectors [c*nv/C, (c+1)*nv/C).
+//  1. push: copy this rank's chunk into slot `rank` (parity buffer) of EVERY rank's receive
+//     region, itself included;
+//  2. publish: bar.sync, then one thread: sys-scope fence and st.release.sys of the generation g
+//     into flag[ar][rank][c] of every rank;
+//  3. wait until flag[ar][s][c] == g in its own region for every source s (ld.acquire.sys polls,
+//     bounded: a lost peer traps instead of hanging), then fence + bar.sync;
+//  4. sum the world slots in fixed rank order 0..world-1 in fp32 and round once: every rank
+//     computes bit-identical results.
+// g = ++counter[ar][c] (chain-owned, the same sequence on every rank); the receive buffer parity is
+// the global AR sequence number ((g-1)*n_ar + ar) & 1, so consecutive all-reduces alternate
+// buffers. Reuse of a parity buffer two all-reduces later is safe because every all-reduce of the
+// chain depends (through the data flow) on the previous one: a writer reaching AR s+2 has received
+// every peer's AR s+1 push, which each peer sends only after its AR s has completed.
+// PDL: this kernel triggers its dependents only once every source has arrived (after step 3), so
+// no successor sits resident on the SMs while the all-reduce spins for its peers (a desynchronised
+// rank, or ranks sharing one GPU as in the tests, could otherwise starve the peers it waits for).
+__global__ void __launch_bounds__(256) k_allreduce_peer(const __grid_constant__ PeerArArgs a) {
+  pdl_wait();
+  __shared__ uint32_t s_g;
+  const uint32_t c = blockIdx.x, C = gridDim.x;
+  const uint64_t nv = a.n / 8;
+  const uint64_t lo = nv * c / C, hi = nv * (c + 1) / C;
+  if (threadIdx.x == 0) {
+    const uint32_t g = a.counters[a.ar_index * kArMaxCtas + c] + 1;
+    a.counters[a.ar_index * kArMaxCtas + c] = g;
+    s_g = g;
+  }
+  __syncthreads();
+  const uint32_t g = s_g;
+  const uint32_t par = (uint32_t)(((uint64_t)(g - 1) * a.n_ar + a.ar_index) & 1u);
+  const uint4* in = reinterpret_cast<const uint4*>(a.in);
+  // 1. push
+  for (uint64_t v = lo + threadIdx.x; v < hi; v += blockDim.x) {
+    const uint4 x = in[v];
+    for (uint32_t p = 0; p < a.world; ++p)
+      reinterpret_cast<uint4*>(a.recv[p] + ((uint64_t)par * a.world + a.rank) * a.slot_elems)[v] = x;
+  }
+  __syncthreads();
+  // 2. publish
+  if (threadIdx.x == 0) {
+    asm volatile("fence.acq_rel.sys;\n" ::: "memory");
+    for (uint32_t p = 0; p < a.world; ++p) {
+      uint32_t* f = a.flags_of[p] + ((uint64_t)a.ar_index * kArMaxWorld + a.rank) * kArMaxCtas + c;
+      asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(f), "r"(g) : "memory");
+    }
+    // 3. wait for every source
+    for (uint32_t s2 = 0; s2 < a.world; ++s2) {
+      const uint32_t* f = a.flags_of[a.rank] + ((uint64_t)a.ar_index * kArMaxWorld + s2) * kArMaxCtas + c;
+      uint64_t spins = 0;
+      for (;;) {
+        uint32_t v;
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];\n" : "=r"(v) : "l"(f) : "memory");
+        if (v == g) break;
+        if (++spins > (1ull << 28)) __trap();
+      }
+    }
+    asm volatile("fence.acq_rel.sys;\n" ::: "memory");
+  }
+  __syncthreads();
+  pdl_trigger();
+  // 4. fixed-order sum
+  const __nv_bfloat16* mine = a.recv[a.rank] + (uint64_t)par * a.world * a.slot_elems;
+  for (uint64_t v = lo + threadIdx.x; v < hi; v += blockDim.x) {
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (uint32_t s2 = 0; s2 < a.world; ++s2) {
+      const uint4 x = reinterpret_cast<const uint4*>(mine + (uint64_t)s2 * a.slot_elems)[v];
+      const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&x);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] += __bfloat162float(b[e]);
+    }
+    uint4 o;
+    __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(&o);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) ob[e] = __float2bfloat16_rn(acc[e]);
+    reinterpret_cast<uint4*>(a.out)[v] = o;
+  }
+}
+
 struct FillArgs { float* out; uint64_t n; uint64_t base; };
 __global__ void k_fill_uniform_f32(const __grid_constant__ FillArgs a) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n;
@@ -558,6 +639,7 @@ const void* kfn_empty() { return (const void*)k_empty; }
 const void* kfn_pdl_nop() { return (const void*)k_pdl_nop; }
 const void* kfn_fill_uniform_f32() { return (const void*)k_fill_uniform_f32; }
 const void* kfn_gather() { return (const void*)k_gather; }
+const void* kfn_allreduce_peer() { return (const void*)k_allreduce_peer; }
 int elem_block_threads() { return kElemThreads; }
 
 }  // namespace cgx

@@ -128,6 +128,11 @@ struct cgx_chain {
   std::vector<std::pair<int, int>> segments;
   std::vector<int> ext_slots;   // j -> slot
   void* nccl = nullptr;
+  // peer all-reduce (cgx_chain_set_peers): rank, world, every rank's region, generation counters
+  int peer_rank = -1, peer_world = 0;
+  uint64_t peer_max_elems = 0;
+  std::vector<void*> peer_base;
+  uint32_t* peer_counters = nullptr;
   void* arena = nullptr;        // internal buffers
   bool allocated = false;
   int live_execs = 0;
@@ -267,6 +272,60 @@ extern "C" int cgx_chain_set_nccl(cgx_chain* c, void* comm) {
   return CGX_OK;
 }
 
+// Peer all-reduce region of one rank: receive data [2][world][slot] bf16 (slots 256-B aligned),
+// then the flag array [kArMaxNodes][kArMaxWorld][kArMaxCtas] uint32.
+static uint64_t peer_slot_elems(uint64_t max_elems) { return (max_elems + 127) / 128 * 128; }
+static uint64_t peer_flag_offset(int world, uint64_t max_elems) {
+  return 2ull * (uint64_t)world * peer_slot_elems(max_elems) * 2;
+}
+
+extern "C" int cgx_peer_buffer_bytes(int world, uint64_t max_elems, uint64_t* bytes) {
+  if (world < 1 || world > kArMaxWorld || !bytes) return fail(CGX_E_INVALID_ARG, "peer_buffer_bytes: world 1..8");
+  *bytes = peer_flag_offset(world, max_elems) + sizeof(uint32_t) * kArMaxNodes * kArMaxWorld * kArMaxCtas;
+  return CGX_OK;
+}
+
+extern "C" int cgx_chain_set_peers(cgx_chain* c, int rank, int world, void* const* bases, uint64_t max_elems) {
+  if (!c || !bases || world < 1 || world > kArMaxWorld || rank < 0 || rank >= world || max_elems == 0)
+    return fail(CGX_E_INVALID_ARG, "set_peers: bad argument");
+  if (c->allocated) return fail(CGX_E_STATE, "set_peers: chain already captured");
+  for (int r = 0; r < world; ++r) {
+    if (!bases[r]) return fail(CGX_E_INVALID_ARG, "set_peers: NULL region");
+    if (reinterpret_cast<uintptr_t>(bases[r]) % 256) return fail(CGX_E_MISALIGNED, "set_peers: region not 256-B aligned");
+  }
+  CK(cudaSetDevice(c->device));
+  if (!c->peer_counters) {
+    CK(cudaMalloc(&c->peer_counters, sizeof(uint32_t) * kArMaxNodes * kArMaxCtas));
+    CK(cudaMemset(c->peer_counters, 0, sizeof(uint32_t) * kArMaxNodes * kArMaxCtas));
+  }
+  c->peer_rank = rank;
+  c->peer_world = world;
+  c->peer_max_elems = max_elems;
+  c->peer_base.assign(bases, bases + world);
+  return CGX_OK;
+}
+
+// CUDA IPC (multi-process TP): export a device allocation's handle (64 bytes) / map a peer's.
+extern "C" int cgx_ipc_handle(void* dptr, void* handle_out) {
+  if (!dptr || !handle_out) return fail(CGX_E_INVALID_ARG, "ipc_handle: NULL");
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, dptr));
+  memcpy(handle_out, &h, sizeof(h));
+  return CGX_OK;
+}
+extern "C" int cgx_ipc_open(const void* handle, void** dptr_out) {
+  if (!handle || !dptr_out) return fail(CGX_E_INVALID_ARG, "ipc_open: NULL");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  CK(cudaIpcOpenMemHandle(dptr_out, h, cudaIpcMemLazyEnablePeerAccess));
+  return CGX_OK;
+}
+extern "C" int cgx_ipc_close(void* dptr) {
+  if (!dptr) return CGX_OK;
+  CK(cudaIpcCloseMemHandle(dptr));
+  return CGX_OK;
+}
+
 static int chain_allocate(cgx_chain* c) {
   if (c->allocated) return CGX_OK;
   CK(cudaSetDevice(c->device));
@@ -291,6 +350,7 @@ extern "C" int cgx_chain_destroy(cgx_chain* c) {
   if (!c) return CGX_OK;
   if (c->live_execs) return fail(CGX_E_STATE, "chain_destroy: execs still alive");
   if (c->arena) cudaFree(c->arena);
+  if (c->peer_counters) cudaFree(c->peer_counters);
   delete c;
   return CGX_OK;
 }
@@ -637,6 +697,39 @@ static int build_launch(cgx_exec* e, int k, Launch& l) {
     }
     case CGX_OP_ALLREDUCE_SUM: {
       if (is_ext(n.in[0])) return fail(CGX_E_UNSUPPORTED, "allreduce: external input");
+      if (c->peer_world > 0) {
+        // one-shot all-reduce over peer memory (k_allreduce_peer)
+        if (n.attr.n % 8 || n.attr.n > c->peer_max_elems)
+          return fail(CGX_E_UNSUPPORTED, "allreduce (peer): n must be a multiple of 8 and <= max_elems");
+        int ar_index = 0, n_ar = 0;
+        for (size_t q = 0; q < c->nodes.size(); ++q)
+          if (c->nodes[q].op == CGX_OP_ALLREDUCE_SUM) {
+            if ((int)q < k) ++ar_index;
+            ++n_ar;
+          }
+        if (n_ar > kArMaxNodes) return fail(CGX_E_UNSUPPORTED, "allreduce (peer): more than 64 nodes");
+        l.args.reset(sizeof(PeerArArgs));
+        PeerArArgs* a = argp<PeerArArgs>(l);
+        a->in = static_cast<const __nv_bfloat16*>(slot_ptr(n.in[0]));
+        a->out = static_cast<__nv_bfloat16*>(slot_ptr(n.out));
+        a->n = n.attr.n;
+        a->slot_elems = peer_slot_elems(c->peer_max_elems);
+        a->rank = (uint32_t)c->peer_rank;
+        a->world = (uint32_t)c->peer_world;
+        a->ar_index = (uint32_t)ar_index;
+        a->n_ar = (uint32_t)n_ar;
+        a->counters = c->peer_counters;
+        for (int r = 0; r < c->peer_world; ++r) {
+          a->recv[r] = static_cast<__nv_bfloat16*>(c->peer_base[r]);
+          a->flags_of[r] = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(c->peer_base[r]) +
+                                                      peer_flag_offset(c->peer_world, c->peer_max_elems));
+        }
+        const uint64_t nv = n.attr.n / 8;
+        l.grid = dim3((unsigned)std::max<uint64_t>(1, std::min<uint64_t>(kArMaxCtas, ceil_div(nv, 256))));
+        l.block = dim3(256);
+        l.func = kfn_allreduce_peer();
+        return CGX_OK;
+      }
       if (!c->nccl) return fail(CGX_E_STATE, "allreduce: no NCCL communicator (cgx_chain_set_nccl)");
       l.kind = LK_NCCL;
       l.nc_in = slot_ptr(n.in[0]);

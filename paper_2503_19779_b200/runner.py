@@ -59,7 +59,10 @@ def device_to_host(t: torch.Tensor, dtype: str) -> np.ndarray:
 class Chain:
     """A cgx chain built from `spec`, holding its static device tensors alive."""
 
-    def __init__(self, spec, statics: dict, device: int = 0, nccl_comm: int | None = None):
+    def __init__(self, spec, statics: dict, device: int = 0, nccl_comm: int | None = None,
+                 peers: tuple | None = None):
+        """peers = (rank, world, [region base per rank], max_elems): ALLREDUCE_SUM nodes run the
+        peer-memory one-shot all-reduce instead of NCCL (cgx_chain_set_peers)."""
         self.spec = spec
         self.device = device
         self.handle = cgx.chain_create(device)
@@ -76,6 +79,8 @@ class Chain:
             cgx.chain_mark_segment(self.handle, f, l)
         if nccl_comm is not None:
             cgx.chain_set_nccl(self.handle, nccl_comm)
+        if peers is not None:
+            cgx.chain_set_peers(self.handle, *peers)
         self.ext_names = [s.name for s in spec.slots if s.kind == "external"]
         self.execs = []
 

@@ -1,0 +1,119 @@
+"""Peer-memory one-shot all-reduce (cgx_chain_set_peers, k_allreduce_peer).
+
+This box has one GPU, so the ranks are emulated inside one process on one device: each rank is its
+own chain (its TP shard of the decoder) with its own region, every rank's region is passed to every
+chain as its "peer" pointer, and the ranks' graphs are launched on separate streams so their
+all-reduce kernels run concurrently and meet through the flags exactly as they would over NVLink
+(the kernel code path — remote stores, sys-scope release/acquire flags, fixed-order sums — is the
+same; only the link differs). Results must be bit-identical across ranks and match the lockstep
+TP oracle (integer mode: exact; uniform values: the decoder tolerance)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+from oracle.chain import eval_chain, eval_chain_tp  # noqa: E402
+from oracle.numerics import bf16_bits, bits_to_f64  # noqa: E402
+from synth import workloads as wl  # noqa: E402
+from synth.workloads import ChainSpec, NodeSpec, SlotSpec  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def rt():
+    from paper_2503_19779_b200 import build
+    build.build()
+    from paper_2503_19779_b200 import cgx, runner
+    return cgx, runner
+
+
+def _regions(cgx, world, max_elems, dev):
+    nb = cgx.peer_buffer_bytes(world, max_elems)
+    return [torch.zeros(nb + 256, dtype=torch.uint8, device=dev) for _ in range(world)]
+
+
+def _base(t):
+    return (t.data_ptr() + 255) // 256 * 256
+
+
+def _ar_spec(n):
+    slots = [SlotSpec("x", "external", "bf16", n), SlotSpec("a", "internal", "bf16", n),
+             SlotSpec("s", "internal", "bf16", n), SlotSpec("y", "internal", "bf16", n),
+             SlotSpec("s2", "internal", "bf16", n)]
+    nodes = [NodeSpec("COPY", ("x",), "a", {"n": n}), NodeSpec("ALLREDUCE_SUM", ("a",), "s", {"n": n}),
+             NodeSpec("ADD", ("s", "a"), "y", {"n": n}), NodeSpec("ALLREDUCE_SUM", ("y",), "s2", {"n": n})]
+    return ChainSpec("ar", slots, nodes, [(0, 3)])
+
+
+def _run_ranks(rt, specs, statics, exts_per_replay, world, max_elems, mode="INDIRECT", transport="DEFAULT"):
+    cgx, runner = rt
+    dev = torch.device("cuda:0")
+    regs = _regions(cgx, world, max_elems, dev)
+    bases = [_base(t) for t in regs]
+    chains = [runner.Chain(specs[r], runner.upload_statics(specs[r], statics[r], dev),
+                           peers=(r, world, bases, max_elems)) for r in range(world)]
+    streams = [torch.cuda.Stream(device=dev) for _ in range(world)]
+    exs = [chains[r].exec(mode, stream=streams[r], transport=transport) for r in range(world)]
+    outs, keep = [], []
+    for ext in exts_per_replay:
+        ts = [runner.upload_externals(specs[r], ext[r], dev) for r in range(world)]
+        keep.append(ts)
+        torch.cuda.synchronize()
+        for r in range(world):
+            exs[r].bind(ts[r])
+        for r in range(world):                      # all ranks' replays in flight together
+            exs[r].launch()
+        torch.cuda.synchronize()
+        outs.append([{s.name: exs[r].output(s.name) for s in specs[r].internals()} for r in range(world)])
+    for ch in chains:
+        ch.close()
+    return outs
+
+
+@pytest.mark.parametrize("world", [1, 2, 4])
+@pytest.mark.parametrize("n", [8, 4096, 98304])
+def test_allreduce_integer_exact(rt, world, n):
+    spec = _ar_spec(n)
+    specs = [spec] * world
+    exts = [[{"x": wl.slot_values(spec, "x", 10 * rep + r, "int")} for r in range(world)] for rep in range(5)]
+    outs = _run_ranks(rt, specs, [{}] * world, exts, world, max(n, 4096))
+    for rep in range(5):
+        parts = [bits_to_f64(exts[rep][r]["x"]) for r in range(world)]
+        s = sum(parts)
+        y = [s + p for p in parts]
+        s2 = sum(y)
+        for r in range(world):
+            assert np.array_equal(outs[rep][r]["s"], bf16_bits(s)), (rep, r)
+            assert np.array_equal(outs[rep][r]["s2"], bf16_bits(s2)), (rep, r)
+
+
+@pytest.mark.parametrize("tp", [2, 4])
+@pytest.mark.parametrize("mode,transport", [("INDIRECT", "FIRST_NODE"), ("COPY", "DEFAULT"), ("EAGER", "DEFAULT")])
+def test_tp_decoder_peer_allreduce(rt, tp, mode, transport):
+    """C5 (TP decoder, 2 layers, T=128) with the peer all-reduce: every rank's output identical, and
+    equal to the lockstep TP oracle within the decoder tolerance."""
+    full = wl.c3_chain(T=128, n_layers=2)
+    specs = [wl.c3_chain(T=128, n_layers=2, tp=tp, rank=r) for r in range(tp)]
+    statics = [wl.static_values(specs[r], tp=tp, rank=r, full=full) for r in range(tp)]
+    exts = [[wl.external_values(specs[r], rep) for r in range(tp)] for rep in range(3)]
+    outs = _run_ranks(rt, specs, statics, exts, tp, 128 * 768, mode, transport)
+    last = specs[0].nodes[-1].out
+    for rep in range(3):
+        for r in range(1, tp):
+            assert np.array_equal(outs[rep][r][last], outs[rep][0][last]), (rep, r)
+        ref = eval_chain_tp(specs, exts[rep], statics)[0][last]
+        g = bits_to_f64(outs[rep][0][last])
+        assert np.linalg.norm(g - ref) / np.linalg.norm(ref) <= 2e-2
+        tp1 = eval_chain(full, wl.external_values(full, rep), wl.static_values(full))[last]
+        assert np.linalg.norm(g - tp1) / np.linalg.norm(tp1) <= 2e-2
+
+
+def test_set_peers_errors(rt):
+    cgx, runner = rt
+    spec = _ar_spec(4096)
+    ch = runner.Chain(spec, {}, 0)
+    with pytest.raises(cgx.CgxError):
+        cgx.chain_set_peers(ch.handle, 2, 2, [256, 512], 4096)          # rank out of range
+    with pytest.raises(cgx.CgxError):
+        cgx.chain_set_peers(ch.handle, 0, 2, [256 + 16, 512], 4096)     # misaligned region
+    ch.close()
