@@ -23,3 +23,38 @@ def nccl_bootstrap(device: int, group=None) -> int:
     import torch.distributed as dist
     uid = broadcast_unique_id(group)
     return cgx.nccl_comm_init(dist.get_world_size(group), dist.get_rank(group), uid, device)
+
+
+class PeerRegions:
+    """Multi-process setup of the peer-memory all-reduce (cgx_chain_set_peers): every rank zero-fills
+    one region of cgx_peer_buffer_bytes() on its own GPU, exports its CUDA IPC handle, gathers every
+    rank's handle through the torch process group and maps the peers' regions into this process
+    (cgx_ipc_open; peer access over NVLink). `bases` is then the per-rank pointer list the chain
+    takes. Keep the object alive as long as the chain; close() unmaps the peers' regions."""
+
+    def __init__(self, world: int, rank: int, max_elems: int, device, group=None):
+        import torch
+        import torch.distributed as dist
+        self.own = torch.zeros(cgx.peer_buffer_bytes(world, max_elems) + 256, dtype=torch.uint8, device=device)
+        base = (self.own.data_ptr() + 255) // 256 * 256
+        torch.cuda.synchronize(device)
+        handle = cgx.ipc_handle(self.own.data_ptr())          # handles map allocation bases
+        gathered = [None] * world
+        dist.all_gather_object(gathered, (handle, base - self.own.data_ptr()), group=group)
+        self.opened, self.bases = [], []
+        for r, (h, off) in enumerate(gathered):
+            if r == rank:
+                self.bases.append(base)
+            else:
+                p = cgx.ipc_open(h)
+                self.opened.append(p)
+                self.bases.append(p + off)
+        self.world, self.rank, self.max_elems = world, rank, max_elems
+
+    def peers(self) -> tuple:
+        return (self.rank, self.world, self.bases, self.max_elems)
+
+    def close(self):
+        for p in self.opened:
+            cgx.ipc_close(p)
+        self.opened = []

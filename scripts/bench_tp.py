@@ -23,6 +23,9 @@ def main():
     ap.add_argument("--T", type=int, default=128)
     ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--check", action="store_true")
+    ap.add_argument("--allreduce", choices=("nccl", "peer"), default="nccl",
+                    help="ALLREDUCE_SUM nodes: captured ncclAllReduce, or the peer-memory one-shot "
+                         "kernel over CUDA IPC-mapped regions (tp.PeerRegions)")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -31,8 +34,14 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # CGX_TP_DEVICE pins every rank to one GPU (functional runs of the peer path on a 1-GPU box:
+    # the ranks' kernels then time-share the device, so the timings mean nothing)
+    if os.environ.get("CGX_TP_DEVICE") is not None:
+        local = int(os.environ["CGX_TP_DEVICE"])
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl" if world > 1 else "gloo", device_id=torch.device("cuda", local) if world > 1 else None)
+    use_nccl_pg = world > 1 and args.allreduce == "nccl"
+    dist.init_process_group("nccl" if use_nccl_pg else "gloo",
+                            device_id=torch.device("cuda", local) if use_nccl_pg else None)
     from paper_2503_19779_b200 import build
     if rank == 0:
         build.build()
@@ -41,11 +50,13 @@ def main():
     from synth import workloads as wl
 
     dev = torch.device("cuda", local)
-    comm = tp.nccl_bootstrap(local)
+    comm = tp.nccl_bootstrap(local) if args.allreduce == "nccl" else None
     full = wl.c3_chain(T=args.T, n_layers=args.layers)
     spec = wl.c3_chain(T=args.T, n_layers=args.layers, tp=world, rank=rank) if world > 1 else full
     st = wl.static_values(spec, tp=world, rank=rank, full=full) if world > 1 else wl.static_values(spec)
-    chain = runner.Chain(spec, runner.upload_statics(spec, st, dev), device=local, nccl_comm=comm)
+    regions = tp.PeerRegions(world, rank, args.T * 768, dev) if args.allreduce == "peer" else None
+    chain = runner.Chain(spec, runner.upload_statics(spec, st, dev), device=local, nccl_comm=comm,
+                         peers=regions.peers() if regions else None)
     stream = torch.cuda.Stream(device=dev)
     xs = [runner.host_to_device(wl.slot_values(spec, "x", r), "bf16", dev) for r in range(4)]
     ptrs = [cgx.ptr_array([x.data_ptr()]) for x in xs]
@@ -69,7 +80,8 @@ def main():
         e1.synchronize()
         t = torch.tensor([e0.elapsed_time(e1) * 1e3 / n], dtype=torch.float64)
         if world > 1:
-            t = t.to(dev)
+            if use_nccl_pg:
+                t = t.to(dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         res[name] = float(t.item())
         if args.check and name == "indirect_first_node":
@@ -94,9 +106,14 @@ def main():
         ex.close()
     if rank == 0:
         res["tokens_per_s_indirect"] = args.T * 1e6 / res["indirect_first_node"]
-        print(json.dumps({"config": f"C5 TP={world} T={args.T} layers={args.layers}", "us_per_replay_max_over_ranks": res}))
+        print(json.dumps({"config": f"C5 TP={world} T={args.T} layers={args.layers} allreduce={args.allreduce}",
+                          "us_per_replay_max_over_ranks": res}))
     chain.close()
-    cgx.nccl_comm_destroy(comm)
+    if comm is not None:
+        cgx.nccl_comm_destroy(comm)
+    if regions is not None:
+        dist.barrier()                  # no rank unmaps a region a peer may still write
+        regions.close()
     dist.destroy_process_group()
 
 

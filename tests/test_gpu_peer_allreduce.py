@@ -117,3 +117,29 @@ def test_set_peers_errors(rt):
     with pytest.raises(cgx.CgxError):
         cgx.chain_set_peers(ch.handle, 0, 2, [256 + 16, 512], 4096)     # misaligned region
     ch.close()
+
+
+def test_multiprocess_ipc_peer_allreduce(rt):
+    """Two processes (torchrun) on this one GPU: regions exchanged as CUDA IPC handles through a
+    gloo process group (tp.PeerRegions), TP=2 decoder layer with the peer all-reduce. The ranks
+    time-share the device, so only the results are checked: identical across ranks, oracle error
+    within the decoder tolerance."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ, CGX_TP_DEVICE="0")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port),
+                        os.path.join(root, "scripts", "bench_tp.py"), "--allreduce", "peer", "--layers", "1",
+                        "--steps", "5", "--check"], env=env, capture_output=True, text=True, timeout=280)
+    line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert r.returncode == 0 and line, r.stdout[-2000:] + r.stderr[-2000:]
+    res = json.loads(line[-1])["us_per_replay_max_over_ranks"]
+    assert res["ranks_identical"]
+    assert max(res["check_rel_err_per_rank"]) <= 2e-2
