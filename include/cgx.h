@@ -90,6 +90,9 @@ typedef enum {
 #define CGX_GEMM_BIAS 1u
 #define CGX_GEMM_GELU 2u        /* tanh-approximate GELU after the bias */
 #define CGX_GEMM_RESIDUAL 4u    /* + in_slots[3] after the activation */
+#define CGX_GEMM_ALLREDUCE 8u   /* row-parallel TP: the epilogue sums the bf16 output tile over the
+                                   chain's peer ranks (cgx_chain_set_peers) before storing it — the
+                                   GEMM and its all-reduce in ONE kernel; tcgen05 path only */
 
 typedef struct {
   uint64_t n;          /* elementwise/reduce: elements processed (0 = whole first input) */

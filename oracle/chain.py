@@ -81,6 +81,14 @@ def eval_chain_tp(chains: list, ext: list, static: list) -> list:
             for env in envs:
                 env[nodes[0].out] = red.copy()
             continue
+        if nodes[0].op == "GEMM_BF16" and nodes[0].attrs.get("allreduce"):
+            # the GEMM with its all-reduce fused: each rank's bf16 output tile, then ALLREDUCE_SUM
+            parts = [eval_node(c, node, env, lambda name, c=c: c.slot(name).dtype)
+                     for c, env, node in zip(chains, envs, nodes)]
+            red = ops.allreduce_sum(parts)
+            for env in envs:
+                env[nodes[0].out] = red.copy()
+            continue
         for c, env, node in zip(chains, envs, nodes):
             env[node.out] = eval_node(c, node, env, lambda name, c=c: c.slot(name).dtype)
     return envs

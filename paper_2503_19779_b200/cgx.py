@@ -24,7 +24,7 @@ F32, BF16 = 0, 1
 SLOT_EXTERNAL, SLOT_STATIC, SLOT_INTERNAL = 0, 1, 2
 OP = {"ADD": 0, "MUL": 1, "SCALE_IMM": 2, "COPY": 3, "REDUCE_SUM": 4, "LAYERNORM": 5,
       "GEMM_BF16": 6, "ATTN_CAUSAL": 7, "ALLREDUCE_SUM": 8, "SCALE_T": 9}
-GEMM_BIAS, GEMM_GELU, GEMM_RESIDUAL = 1, 2, 4
+GEMM_BIAS, GEMM_GELU, GEMM_RESIDUAL, GEMM_ALLREDUCE = 1, 2, 4, 8
 MODE = {"EAGER": 0, "COPY": 1, "INDIRECT": 2, "SETPARAMS": 3, "STALE": 4}
 XPORT = {"DEFAULT": 0, "H2D": 1, "ROOT_MEMCPY": 2, "ROOT_PARAMS": 3, "ROOT_MAPPED": 4, "FIRST_NODE": 5, "H2D_PINGPONG": 6, "PRELUDE": 7,
          "DEVICE": 8}

@@ -149,7 +149,7 @@ namespace cgx {
 // Peer all-reduce (k_allreduce_peer, cgx_chain_set_peers): per-rank region = receive data
 // [2 parity][world][slot_elems] bf16, then flags [kArMaxNodes][kArMaxWorld][kArMaxCtas] uint32.
 static constexpr int kArMaxWorld = 8;
-static constexpr int kArMaxCtas = 64;
+static constexpr int kArMaxCtas = 256;
 static constexpr int kArMaxNodes = 64;
 struct PeerArArgs {
   const __nv_bfloat16* in;

@@ -25,6 +25,10 @@ int decoder_gemm_build(uint32_t M, uint32_t N, uint32_t K, uint32_t flags, const
                        size_t* argbytes, dim3* grid, dim3* block, size_t* smem, const void** func);
 // Make a built GEMM parameter block trigger its PDL dependents only after its wait (T5 node 2).
 void decoder_gemm_set_trigger_after_wait(void* args);
+// CGX_GEMM_ALLREDUCE: the epilogue's peer all-reduce (regions as for k_allreduce_peer).
+void decoder_gemm_set_allreduce(void* args, uint32_t rank, uint32_t world, uint32_t ar_index, uint32_t n_ar,
+                                uint64_t slot_elems, uint32_t* counters, void* const* recv, uint32_t* const* flags);
+uint32_t decoder_gemm_ctas(const void* args, dim3 grid);
 // An EXTERNAL residual under INDIRECT: the epilogue reads its base pointer from table[idx].
 void decoder_gemm_set_residual_table(void* args, const uint64_t* table, int32_t idx);
 // Byte offsets of the residual pointer field and its int32 table-index field (patch modes).

@@ -25,6 +25,7 @@
 #include <mutex>
 
 #include "../../include/cgx.h"
+#include "cgx_args.h"
 #include "cgx_decoder.h"
 #include "cgx_device.cuh"
 
@@ -54,6 +55,13 @@ struct alignas(64) GemmArgs {
   int32_t tres;               // table index of an EXTERNAL residual (-1: `residual` is direct)
   const __nv_bfloat16* a_ptr; // small-M path (k_gemv_bf16): A and W by plain pointers
   const __nv_bfloat16* w_ptr;
+  // CGX_GEMM_ALLREDUCE: the epilogue's peer all-reduce (same protocol and regions as
+  // k_allreduce_peer, flags indexed by this GEMM's CTA)
+  uint32_t ar_rank, ar_world, ar_index, ar_nar;
+  uint64_t ar_slot;
+  uint32_t* ar_counters;
+  __nv_bfloat16* ar_recv[kArMaxWorld];
+  uint32_t* ar_flags[kArMaxWorld];
 };
 
 // ------------------------------------------------------------------ PTX wrappers
@@ -192,6 +200,35 @@ __device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t cta) {
   return r;
 }
 
+// ---- CGX_GEMM_ALLREDUCE epilogue helpers (protocol of k_allreduce_peer, k_chain.cu)
+__device__ __forceinline__ __nv_bfloat16* ar_slot_ptr(const GemmArgs& a, uint32_t region, uint32_t par, uint32_t src) {
+  return a.ar_recv[region] + ((uint64_t)par * a.ar_world + src) * a.ar_slot;
+}
+// Epilogue threads only (named barrier 1): publish this CTA's generation to every rank, wait for
+// every source's, with sys-scope release / acquire.
+__device__ __forceinline__ void ar_publish_wait(const GemmArgs& a, uint32_t cta, uint32_t g, uint32_t et) {
+  asm volatile("bar.sync 1, 128;\n" ::: "memory");
+  if (et == 0) {
+    asm volatile("fence.acq_rel.sys;\n" ::: "memory");
+    for (uint32_t p = 0; p < a.ar_world; ++p) {
+      uint32_t* f = a.ar_flags[p] + ((uint64_t)a.ar_index * kArMaxWorld + a.ar_rank) * kArMaxCtas + cta;
+      asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(f), "r"(g) : "memory");
+    }
+    for (uint32_t s2 = 0; s2 < a.ar_world; ++s2) {
+      const uint32_t* f = a.ar_flags[a.ar_rank] + ((uint64_t)a.ar_index * kArMaxWorld + s2) * kArMaxCtas + cta;
+      uint64_t spins = 0;
+      for (;;) {
+        uint32_t v;
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];\n" : "=r"(v) : "l"(f) : "memory");
+        if (v == g) break;
+        if (++spins > (1ull << 28)) __trap();
+      }
+    }
+    asm volatile("fence.acq_rel.sys;\n" ::: "memory");
+  }
+  asm volatile("bar.sync 1, 128;\n" ::: "memory");
+}
+
 template <int BN>
 __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_constant__ GemmArgs a) {
   constexpr uint32_t kABytes = kBM * kBK * 2;     // 16 KiB
@@ -221,8 +258,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(recv_full + 1);
 
   if (threadIdx.x == 0) trace_at(a, 0);
-  const bool late_trigger = a.flags & kGemmTriggerAfterWait;
-  if (!late_trigger) pdl_trigger();   // dependents may start their prologues (they read our output after their wait)
+  // an all-reducing GEMM never triggers early: no successor may sit resident while it waits for
+  // its peers (dependents then launch at its completion)
+  const bool ar = a.flags & CGX_GEMM_ALLREDUCE;
+  const bool late_trigger = (a.flags & kGemmTriggerAfterWait) && !ar;
+  if (!late_trigger && !ar) pdl_trigger();   // dependents may start their prologues (they read our output after their wait)
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n0 = blockIdx.x * BN;
   const int m0 = blockIdx.y * kBM;
@@ -313,6 +353,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
     const bool gelu = a.flags & CGX_GEMM_GELU;
     for (uint32_t i = et; i < (uint32_t)BN; i += 128u)
       sbias[i] = has_bias ? __bfloat162float(a.bias[n0 + i]) : 0.f;
+    const uint32_t cta_lin = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    uint32_t& s_ar_g = s_tmem[1];                  // dynamic smem word after the TMEM address
+    if (ar && et == 0) {
+      const uint32_t g = a.ar_counters[a.ar_index * kArMaxCtas + cta_lin] + 1;
+      a.ar_counters[a.ar_index * kArMaxCtas + cta_lin] = g;
+      s_ar_g = g;
+    }
     constexpr uint32_t kQRow = BN / 4;             // 4-column quads per tile row
     constexpr int kQMax = BN / 8;                  // quads per thread in the split reduction (rows_max <= 64)
     uint4 res_row[BN / 8];                         // S == 1: this thread's residual row (bf16 x 8 per uint4)
@@ -383,7 +430,36 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
           __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(&o);
 #pragma unroll
           for (int i = 0; i < 8; ++i) ob[i] = __float2bfloat16_rn(v[8 * c8 + i]);
-          op[c8] = o;
+          if (!ar) {
+            op[c8] = o;
+          } else {                                 // this rank's bf16 tile row -> slot `rank` everywhere
+            const uint32_t par = (uint32_t)(((uint64_t)(s_ar_g - 1) * a.ar_nar + a.ar_index) & 1u);
+            for (uint32_t p = 0; p < a.ar_world; ++p)
+              reinterpret_cast<uint4*>(ar_slot_ptr(a, p, par, a.ar_rank) + (size_t)m * a.N + n0)[c8] = o;
+          }
+        }
+      }
+      if (ar) {
+        const uint32_t g = s_ar_g;
+        const uint32_t par = (uint32_t)(((uint64_t)(g - 1) * a.ar_nar + a.ar_index) & 1u);
+        ar_publish_wait(a, cta_lin, g, et);
+        if (m < (int)a.M) {                       // fixed rank order, fp32, one rounding
+          uint4* op = reinterpret_cast<uint4*>(a.out + (size_t)m * a.N + n0);
+#pragma unroll
+          for (int c8 = 0; c8 < BN / 8; ++c8) {
+            float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            for (uint32_t s2 = 0; s2 < a.ar_world; ++s2) {
+              const uint4 x = reinterpret_cast<const uint4*>(ar_slot_ptr(a, a.ar_rank, par, s2) + (size_t)m * a.N + n0)[c8];
+              const __nv_bfloat16* xb = reinterpret_cast<const __nv_bfloat16*>(&x);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) acc[i] += __bfloat162float(xb[i]);
+            }
+            uint4 o;
+            __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(&o);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) ob[i] = __float2bfloat16_rn(acc[i]);
+            op[c8] = o;
+          }
         }
       }
       if (threadIdx.x == 64) trace_at(a, 4);
@@ -443,7 +519,38 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
         __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(&ov);
 #pragma unroll
         for (int i = 0; i < 4; ++i) ob[i] = __float2bfloat16_rn(w[i]);
-        *reinterpret_cast<uint2*>(a.out + (size_t)mr * a.N + n0 + c) = ov;
+        if (!ar) {
+          *reinterpret_cast<uint2*>(a.out + (size_t)mr * a.N + n0 + c) = ov;
+        } else {                                   // this rank's bf16 quad -> slot `rank` everywhere
+          const uint32_t par = (uint32_t)(((uint64_t)(s_ar_g - 1) * a.ar_nar + a.ar_index) & 1u);
+          for (uint32_t p = 0; p < a.ar_world; ++p)
+            *reinterpret_cast<uint2*>(ar_slot_ptr(a, p, par, a.ar_rank) + (size_t)mr * a.N + n0 + c) = ov;
+        }
+      }
+      if (ar) {
+        const uint32_t g = s_ar_g;
+        const uint32_t par = (uint32_t)(((uint64_t)(g - 1) * a.ar_nar + a.ar_index) & 1u);
+        ar_publish_wait(a, cta_lin, g, et);
+#pragma unroll
+        for (int j = 0; j < kQMax; ++j) {          // fixed rank order, fp32, one rounding
+          const uint32_t qi = et + 128u * j;
+          if (qi >= nq) break;
+          const uint32_t r = qi / kQRow, c = 4u * (qi % kQRow);
+          const int mr = m0 + (int)(my_lo + r);
+          if (mr >= (int)a.M) continue;
+          float acc[4] = {0.f, 0.f, 0.f, 0.f};
+          for (uint32_t s2 = 0; s2 < a.ar_world; ++s2) {
+            const uint2 x = *reinterpret_cast<const uint2*>(ar_slot_ptr(a, a.ar_rank, par, s2) + (size_t)mr * a.N + n0 + c);
+            const __nv_bfloat16* xb = reinterpret_cast<const __nv_bfloat16*>(&x);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) acc[i] += __bfloat162float(xb[i]);
+          }
+          uint2 ov;
+          __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(&ov);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) ob[i] = __float2bfloat16_rn(acc[i]);
+          *reinterpret_cast<uint2*>(a.out + (size_t)mr * a.N + n0 + c) = ov;
+        }
       }
       if (threadIdx.x == 64) trace_at(a, 4);
     }
@@ -651,7 +758,8 @@ template <int BN>
 static const void* setup_kernel() {
   static std::once_flag once;
   std::call_once(once, [] {
-    cudaFuncSetAttribute(k_gemm_bf16<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    // headroom below the 227 KiB per-block limit for the kernel's static shared memory
+    cudaFuncSetAttribute(k_gemm_bf16<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     cudaFuncSetAttribute(k_gemm_bf16<BN>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   });
   return (const void*)k_gemm_bf16<BN>;
@@ -659,6 +767,26 @@ static const void* setup_kernel() {
 
 static const void* kernel_for(int bn) {
   return bn == 128 ? setup_kernel<128>() : bn == 64 ? setup_kernel<64>() : setup_kernel<32>();
+}
+
+void decoder_gemm_set_allreduce(void* args, uint32_t rank, uint32_t world, uint32_t ar_index, uint32_t n_ar,
+                                uint64_t slot_elems, uint32_t* counters, void* const* recv, uint32_t* const* flags) {
+  GemmArgs* g = static_cast<GemmArgs*>(args);
+  g->ar_rank = rank;
+  g->ar_world = world;
+  g->ar_index = ar_index;
+  g->ar_nar = n_ar;
+  g->ar_slot = slot_elems;
+  g->ar_counters = counters;
+  for (uint32_t r = 0; r < world && r < (uint32_t)kArMaxWorld; ++r) {
+    g->ar_recv[r] = static_cast<__nv_bfloat16*>(recv[r]);
+    g->ar_flags[r] = flags[r];
+  }
+}
+
+uint32_t decoder_gemm_ctas(const void* args, dim3 grid) {
+  (void)args;
+  return grid.x * grid.y * grid.z;
 }
 
 void decoder_gemm_set_residual_table(void* args, const uint64_t* table, int32_t idx) {
@@ -693,7 +821,7 @@ int decoder_gemm_build(uint32_t M, uint32_t N, uint32_t K, uint32_t flags, const
                        const void* bias, const void* residual, void* out, void* ws, void* cnt, void* args_out,
                        size_t* argbytes, dim3* grid, dim3* block, size_t* smem, const void** func) {
   if (!decoder_gemm_supported(M, N, K)) return CGX_E_UNSUPPORTED;
-  if (gemv_shape(M, N, K)) {
+  if (gemv_shape(M, N, K) && !(flags & CGX_GEMM_ALLREDUCE)) {
     // small-M (decode) path: one output column per warp (more warps in flight beat more rows per
     // warp at these sizes), per-lane vector count picked from K
     const int R = 1;

@@ -279,6 +279,21 @@ static uint64_t peer_flag_offset(int world, uint64_t max_elems) {
   return 2ull * (uint64_t)world * peer_slot_elems(max_elems) * 2;
 }
 
+// Position of node k among the chain's all-reduces (ALLREDUCE_SUM nodes and GEMMs with the fused
+// all-reduce), and their total: the generation / parity sequence every rank shares.
+static void ar_position(const cgx_chain* c, int k, int* index, int* total) {
+  int i = 0, t = 0;
+  for (size_t q = 0; q < c->nodes.size(); ++q) {
+    const Node& n = c->nodes[q];
+    if (n.op == CGX_OP_ALLREDUCE_SUM || (n.op == CGX_OP_GEMM_BF16 && (n.attr.flags & CGX_GEMM_ALLREDUCE))) {
+      if ((int)q < k) ++i;
+      ++t;
+    }
+  }
+  *index = i;
+  *total = t;
+}
+
 extern "C" int cgx_peer_buffer_bytes(int world, uint64_t max_elems, uint64_t* bytes) {
   if (world < 1 || world > kArMaxWorld || !bytes) return fail(CGX_E_INVALID_ARG, "peer_buffer_bytes: world 1..8");
   *bytes = peer_flag_offset(world, max_elems) + sizeof(uint32_t) * kArMaxNodes * kArMaxWorld * kArMaxCtas;
@@ -669,6 +684,26 @@ static int build_launch(cgx_exec* e, int k, Launch& l) {
         e->gemm_cnt_off += c1;
       }
       l.cluster_z = l.grid.z;
+      if (n.attr.flags & CGX_GEMM_ALLREDUCE) {
+        if (c->peer_world <= 0) return fail(CGX_E_STATE, "gemm allreduce: no peers (cgx_chain_set_peers)");
+        if ((uint64_t)n.attr.M * n.attr.N > c->peer_max_elems || n.attr.N % 8)
+          return fail(CGX_E_UNSUPPORTED, "gemm allreduce: M*N <= max_elems and N % 8 == 0");
+        if (l.grid.x * l.grid.y * l.grid.z > (unsigned)kArMaxCtas)
+          return fail(CGX_E_UNSUPPORTED, "gemm allreduce: more than 256 CTAs");
+        int ar_index = 0, n_ar = 0;
+        ar_position(c, k, &ar_index, &n_ar);
+        if (n_ar > kArMaxNodes) return fail(CGX_E_UNSUPPORTED, "gemm allreduce: more than 64 all-reduces");
+        std::vector<void*> recv(c->peer_world);
+        std::vector<uint32_t*> flg(c->peer_world);
+        for (int r = 0; r < c->peer_world; ++r) {
+          recv[r] = c->peer_base[r];
+          flg[r] = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(c->peer_base[r]) +
+                                               peer_flag_offset(c->peer_world, c->peer_max_elems));
+        }
+        decoder_gemm_set_allreduce(l.args.p, (uint32_t)c->peer_rank, (uint32_t)c->peer_world, (uint32_t)ar_index,
+                                   (uint32_t)n_ar, peer_slot_elems(c->peer_max_elems), c->peer_counters,
+                                   recv.data(), flg.data());
+      }
       if (res_ext) {
         const int j = c->slots[n.in[3]].ext_j;
         if (indirect) {
@@ -702,11 +737,7 @@ static int build_launch(cgx_exec* e, int k, Launch& l) {
         if (n.attr.n % 8 || n.attr.n > c->peer_max_elems)
           return fail(CGX_E_UNSUPPORTED, "allreduce (peer): n must be a multiple of 8 and <= max_elems");
         int ar_index = 0, n_ar = 0;
-        for (size_t q = 0; q < c->nodes.size(); ++q)
-          if (c->nodes[q].op == CGX_OP_ALLREDUCE_SUM) {
-            if ((int)q < k) ++ar_index;
-            ++n_ar;
-          }
+        ar_position(c, k, &ar_index, &n_ar);
         if (n_ar > kArMaxNodes) return fail(CGX_E_UNSUPPORTED, "allreduce (peer): more than 64 nodes");
         l.args.reset(sizeof(PeerArArgs));
         PeerArArgs* a = argp<PeerArArgs>(l);
@@ -941,7 +972,16 @@ static int issue(cgx_exec* e, Launch& l, cudaStream_t s) {
     cfg.numAttrs = na;
   }
   void* argv[1] = {l.args.p};
-  CK(cudaLaunchKernelExC(&cfg, l.func, argv));
+  const cudaError_t le = cudaLaunchKernelExC(&cfg, l.func, argv);
+  if (le != cudaSuccess) {
+    cudaGetLastError();
+    return fail(CGX_E_CUDA, std::string("launch of node ") + std::to_string(l.node) + " (op " +
+                                std::to_string((int)e->c->nodes[l.node].op) + ", grid " + std::to_string(l.grid.x) + "x" +
+                                std::to_string(l.grid.y) + "x" + std::to_string(l.grid.z) + ", block " +
+                                std::to_string(l.block.x) + ", smem " + std::to_string(l.smem) + ", cluster " +
+                                std::to_string(l.cluster_z) + ", params " + std::to_string(l.args.n) + " B): " +
+                                cudaGetErrorString(le));
+  }
   if (du >= 0) l.dev_node = attr[du].val.deviceUpdatableKernelNode.devNode;
   return CGX_OK;
 }

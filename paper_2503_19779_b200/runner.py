@@ -37,6 +37,8 @@ def make_attr(op: str, attrs: dict) -> cgx.Attr:
         f |= cgx.GEMM_GELU
     if attrs.get("residual"):
         f |= cgx.GEMM_RESIDUAL
+    if attrs.get("allreduce"):
+        f |= cgx.GEMM_ALLREDUCE
     a.flags = f
     return a
 

@@ -160,7 +160,7 @@ GPT2 = dict(d=768, heads=12, head_dim=64, d_ff=3072, eps=1e-5)
 
 
 def c3_chain(T: int = 128, n_layers: int = 12, tp: int = 1, rank: int = 0,
-             fuse_residual: bool = False) -> ChainSpec:
+             fuse_residual: bool = False, fuse_allreduce: bool = False) -> ChainSpec:
     """GPT-2-small-shaped decoder chain: per layer LN1, QKV GEMM+bias,
     causal attention, O-proj GEMM+bias, residual ADD, LN2, FC1 GEMM+bias+GELU, FC2 GEMM+bias,
     residual ADD. Only x is EXTERNAL; weights are STATIC (SURVEY ambiguity 4).
@@ -174,6 +174,9 @@ def c3_chain(T: int = 128, n_layers: int = 12, tp: int = 1, rank: int = 0,
     the O-proj and FC2 GEMMs take the residual stream as a 4th input and write h1 / h2 directly,
     7 nodes per layer instead of 9 (one bf16 rounding of A W^T + b + residual instead of two)."""
     assert not (fuse_residual and tp > 1), "residual fusion needs the un-reduced sum (TP = 1)"
+    # fuse_allreduce (tp > 1, NEXT-4): the O-proj / FC2 GEMMs carry "allreduce" (their epilogue sums
+    # the output tile over the ranks through peer memory) instead of separate ALLREDUCE_SUM nodes
+    fuse_ar = fuse_allreduce and tp > 1
     d, hd, dff, eps = GPT2["d"], GPT2["head_dim"], GPT2["d_ff"], GPT2["eps"]
     H = GPT2["heads"]
     Hp = H if H % tp == 0 else ((H + tp - 1) // tp) * tp   # 12 -> 16 at tp=8
@@ -229,9 +232,9 @@ def c3_chain(T: int = 128, n_layers: int = 12, tp: int = 1, rank: int = 0,
                      {"T": T, "H": hl, "D": hd, "scale": 0.125}),
             NodeSpec("GEMM_BF16", (p + "att", p + "w_o", p + "b_o"), p + "o",
                      {"M": T, "N": d, "K": hl * hd, "bias": bias_ro if tp > 1 else True,
-                      "gelu": False}),
+                      "gelu": False, "allreduce": fuse_ar}),
         ]
-        if tp > 1:
+        if tp > 1 and not fuse_ar:
             nodes.append(NodeSpec("ALLREDUCE_SUM", (p + "o",), p + "o", {"n": T * d}))
         nodes += [
             NodeSpec("ADD", (h, p + "o"), p + "h1", {"n": T * d}),
@@ -241,15 +244,17 @@ def c3_chain(T: int = 128, n_layers: int = 12, tp: int = 1, rank: int = 0,
                      {"M": T, "N": fl, "K": d, "bias": True, "gelu": True}),
             NodeSpec("GEMM_BF16", (p + "f", p + "w_fc2", p + "b_fc2"), p + "g",
                      {"M": T, "N": d, "K": fl, "bias": bias_ro if tp > 1 else True,
-                      "gelu": False}),
+                      "gelu": False, "allreduce": fuse_ar}),
         ]
-        if tp > 1:
+        if tp > 1 and not fuse_ar:
             nodes.append(NodeSpec("ALLREDUCE_SUM", (p + "g",), p + "g", {"n": T * d}))
         nodes.append(NodeSpec("ADD", (p + "h1", p + "g"), p + "h2", {"n": T * d}))
         h = p + "h2"
     name = f"C3_T{T}_L{n_layers}" if tp == 1 else f"C5_T{T}_L{n_layers}_tp{tp}_r{rank}"
     if fuse_residual:
         name += "_fused"
+    if fuse_ar:
+        name += "_arfused"
     return ChainSpec(name, slots, nodes, [(0, len(nodes) - 1)])
 
 

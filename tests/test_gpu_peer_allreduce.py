@@ -143,3 +143,31 @@ def test_multiprocess_ipc_peer_allreduce(rt):
     res = json.loads(line[-1])["us_per_replay_max_over_ranks"]
     assert res["ranks_identical"]
     assert max(res["check_rel_err_per_rank"]) <= 2e-2
+
+
+@pytest.mark.parametrize("tp", [2, 4])
+@pytest.mark.parametrize("mode,transport", [("INDIRECT", "FIRST_NODE"), ("SETPARAMS", "DEFAULT"), ("EAGER", "DEFAULT")])
+def test_tp_decoder_gemm_fused_allreduce(rt, monkeypatch, tp, mode, transport):
+    """The row-parallel GEMMs (O-proj, FC2) with the all-reduce fused into their epilogue
+    (CGX_GEMM_ALLREDUCE: one kernel computes the partial tile, pushes it to every rank and sums):
+    bit-identical to the chain with separate peer ALLREDUCE_SUM nodes, identical across ranks,
+    and within the decoder tolerance of the TP oracle. Small row-parallel tilings keep every
+    virtual rank's all-reducing GEMM resident on the one shared GPU."""
+    k_o, k_f = 768 // tp, 3072 // tp
+    monkeypatch.setenv("CGX_GEMM_TILING", f"768x{k_o}=32/{1 if tp == 4 else 2},768x{k_f}=32/2")
+    full = wl.c3_chain(T=128, n_layers=2)
+    specs_f = [wl.c3_chain(T=128, n_layers=2, tp=tp, rank=r, fuse_allreduce=True) for r in range(tp)]
+    specs_u = [wl.c3_chain(T=128, n_layers=2, tp=tp, rank=r) for r in range(tp)]
+    assert len(specs_f[0].nodes) + 4 == len(specs_u[0].nodes)
+    statics = [wl.static_values(specs_u[r], tp=tp, rank=r, full=full) for r in range(tp)]
+    exts = [[wl.external_values(specs_u[r], rep) for r in range(tp)] for rep in range(3)]
+    outs_f = _run_ranks(rt, specs_f, statics, exts, tp, 128 * 768, mode, transport)
+    outs_u = _run_ranks(rt, specs_u, statics, exts, tp, 128 * 768, mode, transport)
+    last = specs_f[0].nodes[-1].out
+    for rep in range(3):
+        for r in range(tp):
+            assert np.array_equal(outs_f[rep][r][last], outs_u[rep][r][last]), (rep, r)
+            assert np.array_equal(outs_f[rep][r][last], outs_f[rep][0][last]), (rep, r)
+        ref = eval_chain_tp(specs_f, exts[rep], statics)[0][last]
+        g = bits_to_f64(outs_f[rep][0][last])
+        assert np.linalg.norm(g - ref) / np.linalg.norm(ref) <= 2e-2
