@@ -23,9 +23,10 @@ def main():
     ap.add_argument("--T", type=int, default=128)
     ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--check", action="store_true")
-    ap.add_argument("--allreduce", choices=("nccl", "peer"), default="nccl",
-                    help="ALLREDUCE_SUM nodes: captured ncclAllReduce, or the peer-memory one-shot "
-                         "kernel over CUDA IPC-mapped regions (tp.PeerRegions)")
+    ap.add_argument("--allreduce", choices=("nccl", "peer", "fused"), default="nccl",
+                    help="ALLREDUCE_SUM nodes: captured ncclAllReduce, the peer-memory one-shot kernel "
+                         "over CUDA IPC-mapped regions (tp.PeerRegions), or that all-reduce fused into "
+                         "the row-parallel GEMM epilogues (CGX_GEMM_ALLREDUCE)")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -39,7 +40,7 @@ def main():
     if os.environ.get("CGX_TP_DEVICE") is not None:
         local = int(os.environ["CGX_TP_DEVICE"])
     torch.cuda.set_device(local)
-    use_nccl_pg = world > 1 and args.allreduce == "nccl"
+    use_nccl_pg = world > 1 and args.allreduce == "nccl"   # peer modes: gloo carries the IPC handles
     dist.init_process_group("nccl" if use_nccl_pg else "gloo",
                             device_id=torch.device("cuda", local) if use_nccl_pg else None)
     from paper_2503_19779_b200 import build
@@ -52,9 +53,10 @@ def main():
     dev = torch.device("cuda", local)
     comm = tp.nccl_bootstrap(local) if args.allreduce == "nccl" else None
     full = wl.c3_chain(T=args.T, n_layers=args.layers)
-    spec = wl.c3_chain(T=args.T, n_layers=args.layers, tp=world, rank=rank) if world > 1 else full
+    spec = (wl.c3_chain(T=args.T, n_layers=args.layers, tp=world, rank=rank,
+                        fuse_allreduce=args.allreduce == "fused") if world > 1 else full)
     st = wl.static_values(spec, tp=world, rank=rank, full=full) if world > 1 else wl.static_values(spec)
-    regions = tp.PeerRegions(world, rank, args.T * 768, dev) if args.allreduce == "peer" else None
+    regions = tp.PeerRegions(world, rank, args.T * 768, dev) if args.allreduce != "nccl" else None
     chain = runner.Chain(spec, runner.upload_statics(spec, st, dev), device=local, nccl_comm=comm,
                          peers=regions.peers() if regions else None)
     stream = torch.cuda.Stream(device=dev)

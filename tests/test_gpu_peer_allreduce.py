@@ -119,7 +119,8 @@ def test_set_peers_errors(rt):
     ch.close()
 
 
-def test_multiprocess_ipc_peer_allreduce(rt):
+@pytest.mark.parametrize("allreduce", ["peer", "fused"])
+def test_multiprocess_ipc_peer_allreduce(rt, allreduce):
     """Two processes (torchrun) on this one GPU: regions exchanged as CUDA IPC handles through a
     gloo process group (tp.PeerRegions), TP=2 decoder layer with the peer all-reduce. The ranks
     time-share the device, so only the results are checked: identical across ranks, oracle error
@@ -136,7 +137,7 @@ def test_multiprocess_ipc_peer_allreduce(rt):
     env = dict(os.environ, CGX_TP_DEVICE="0")
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
                         "--master-addr", "127.0.0.1", "--master-port", str(port),
-                        os.path.join(root, "scripts", "bench_tp.py"), "--allreduce", "peer", "--layers", "1",
+                        os.path.join(root, "scripts", "bench_tp.py"), "--allreduce", allreduce, "--layers", "1",
                         "--steps", "5", "--check"], env=env, capture_output=True, text=True, timeout=280)
     line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
     assert r.returncode == 0 and line, r.stdout[-2000:] + r.stderr[-2000:]
