@@ -84,7 +84,11 @@ typedef enum { CGX_SLOT_EXTERNAL = 0, CGX_SLOT_STATIC = 1, CGX_SLOT_INTERNAL = 2
 typedef enum {
   CGX_OP_ADD = 0, CGX_OP_MUL = 1, CGX_OP_SCALE_IMM = 2, CGX_OP_COPY = 3, CGX_OP_REDUCE_SUM = 4,
   CGX_OP_LAYERNORM = 5, CGX_OP_GEMM_BF16 = 6, CGX_OP_ATTN_CAUSAL = 7, CGX_OP_ALLREDUCE_SUM = 8,
-  CGX_OP_SCALE_T = 9
+  CGX_OP_SCALE_T = 9,
+  /* training-shaped chain, bf16, one rounding each: a - b; a + scalar * b;
+     tanh-GELU(a); a * GELU'(b) (a = upstream gradient, b = pre-activation); out[c,r] = in[r,c] for
+     a [n / cols, cols] matrix */
+  CGX_OP_SUB = 10, CGX_OP_AXPY = 11, CGX_OP_GELU = 12, CGX_OP_GELU_BWD = 13, CGX_OP_TRANSPOSE = 14
 } cgx_op;
 
 #define CGX_GEMM_BIAS 1u

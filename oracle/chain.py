@@ -44,20 +44,35 @@ def eval_node(chain, node, env, dtype_of):
         return ops.gemm_bf16(env[ins[0]], env[ins[1]], env[ins[2]], at, residual=res)
     if op == "ATTN_CAUSAL":
         return ops.attn_causal(env[ins[0]], at)
+    if op == "SUB":
+        return ops.sub(env[ins[0]], env[ins[1]], at, dt)
+    if op == "AXPY":
+        return ops.axpy(env[ins[0]], env[ins[1]], at, dt)
+    if op == "GELU":
+        return ops.gelu(env[ins[0]], at, dt)
+    if op == "GELU_BWD":
+        return ops.gelu_bwd(env[ins[0]], env[ins[1]], at, dt)
+    if op == "TRANSPOSE":
+        return ops.transpose(env[ins[0]], at, dt)
     raise ValueError(f"eval_node: op {op} needs the multi-rank evaluator")
 
 
-def eval_chain(chain, ext: dict, static: dict) -> dict:
+def eval_chain(chain, ext: dict, static: dict, state: dict | None = None, nodes: tuple | None = None) -> dict:
     """Eager evaluation: returns name -> value for every slot after running all nodes once.
-    `ext` / `static` map slot names to values as produced by synth (uint16 for bf16)."""
+    `ext` / `static` map slot names to values as produced by synth (uint16 for bf16).
+    `state`: values of INTERNAL slots carried over from a previous step (the training chain's
+    weights, updated in place every replay); `nodes`: an inclusive node range (first, last)."""
     env = {}
+    for name, v in (state or {}).items():
+        env[name] = np.array(v, copy=True)
     for s in chain.slots:
         if s.kind == "external":
             env[s.name] = to_host(s, ext[s.name])
         elif s.kind == "static":
             env[s.name] = to_host(s, static[s.name])
     dtype_of = lambda name: chain.slot(name).dtype  # noqa: E731
-    for node in chain.nodes:
+    first, last = nodes if nodes is not None else (0, len(chain.nodes) - 1)
+    for node in chain.nodes[first:last + 1]:
         env[node.out] = eval_node(chain, node, env, dtype_of)
     return env
 

@@ -60,6 +60,48 @@ def copy(a, attrs, dtype="f32"):
     return a[:_n(a, attrs)].copy()
 
 
+# ------------------------------------------------------------------ training-shaped chain (NEXT-4)
+
+def sub(a, b, attrs, dtype="bf16"):
+    """SUB(a,b)[i] = a[i] - b[i], one rounding (bf16)."""
+    n = _n(a, attrs)
+    return bf16_rne(a[:n].astype(np.float64) - b[:n].astype(np.float64))
+
+
+def axpy(a, b, attrs, dtype="bf16"):
+    """AXPY(a,b)[i] = a[i] + c * b[i], c = attrs['scalar'] as fp32 (the SGD step W - lr * dW with
+    c = -lr), one rounding (bf16)."""
+    n = _n(a, attrs)
+    c = float(np.float32(attrs["scalar"]))
+    return bf16_rne(a[:n].astype(np.float64) + c * b[:n].astype(np.float64))
+
+
+def gelu_grad(x):
+    """d/dx of the tanh-approximate GELU 0.5 x (1 + tanh(u)), u = k0 (x + k1 x^3):
+    0.5 (1 + tanh u) + 0.5 x (1 - tanh^2 u) k0 (1 + 3 k1 x^2)."""
+    k0, k1 = math.sqrt(2.0 / math.pi), 0.044715
+    t = np.tanh(k0 * (x + k1 * x ** 3))
+    return 0.5 * (1.0 + t) + 0.5 * x * (1.0 - t * t) * k0 * (1.0 + 3.0 * k1 * x * x)
+
+
+def gelu(a, attrs, dtype="bf16"):
+    """GELU(a)[i] (tanh approximation), one rounding (bf16)."""
+    n = _n(a, attrs)
+    return bf16_rne(gelu_tanh(a[:n].astype(np.float64)))
+
+
+def gelu_bwd(dy, x, attrs, dtype="bf16"):
+    """GELU_BWD(dy, x)[i] = dy[i] * GELU'(x[i]) (chain rule through the activation), one rounding."""
+    n = _n(dy, attrs)
+    return bf16_rne(dy[:n].astype(np.float64) * gelu_grad(x[:n].astype(np.float64)))
+
+
+def transpose(a, attrs, dtype="bf16"):
+    """TRANSPOSE: out[c, r] = in[r, c] for in = [n / cols, cols] row-major (exact copy)."""
+    n, cols = _n(a, attrs), int(attrs["cols"])
+    return a[:n].reshape(n // cols, cols).T.reshape(-1).copy()
+
+
 def reduce_sum(a, attrs, dtype="f32"):
     """REDUCE_SUM(a)[r] = sum_c a[r, c] over rows of `cols`, f64 accumulate, one fp32 rounding
     (SURVEY §8(a) a6, §8(c) O1)."""

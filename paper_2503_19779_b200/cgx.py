@@ -23,7 +23,8 @@ E_INVALID_ARG, E_STATE, E_NOT_ELIGIBLE, E_MISSING_INPUT, E_SIZE_MISMATCH, E_MISA
 F32, BF16 = 0, 1
 SLOT_EXTERNAL, SLOT_STATIC, SLOT_INTERNAL = 0, 1, 2
 OP = {"ADD": 0, "MUL": 1, "SCALE_IMM": 2, "COPY": 3, "REDUCE_SUM": 4, "LAYERNORM": 5,
-      "GEMM_BF16": 6, "ATTN_CAUSAL": 7, "ALLREDUCE_SUM": 8, "SCALE_T": 9}
+      "GEMM_BF16": 6, "ATTN_CAUSAL": 7, "ALLREDUCE_SUM": 8, "SCALE_T": 9, "SUB": 10, "AXPY": 11,
+      "GELU": 12, "GELU_BWD": 13, "TRANSPOSE": 14}
 GEMM_BIAS, GEMM_GELU, GEMM_RESIDUAL, GEMM_ALLREDUCE = 1, 2, 4, 8
 MODE = {"EAGER": 0, "COPY": 1, "INDIRECT": 2, "SETPARAMS": 3, "STALE": 4}
 XPORT = {"DEFAULT": 0, "H2D": 1, "ROOT_MEMCPY": 2, "ROOT_PARAMS": 3, "ROOT_MAPPED": 4, "FIRST_NODE": 5, "H2D_PINGPONG": 6, "PRELUDE": 7,

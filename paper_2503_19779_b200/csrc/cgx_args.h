@@ -170,6 +170,7 @@ struct GatherArgs {
   uint32_t n;
 };
 const void* kfn_gather();
+const void* kfn_transpose_bf16(int tw = 0);
 const void* kfn_elem(int op, int dtype, int tw = 0);   // ADD/MUL/SCALE_IMM/COPY f32|bf16
 const void* kfn_reduce_sum_f32(int tw = 0);
 int tw_cap(int n);                                // 8, 64, 512 (0 if n > 512)

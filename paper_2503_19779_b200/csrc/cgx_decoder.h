@@ -23,6 +23,8 @@ void decoder_gemm_plan(uint32_t M, uint32_t N, uint32_t K, size_t* ws_bytes, siz
 int decoder_gemm_build(uint32_t M, uint32_t N, uint32_t K, uint32_t flags, const void* A, const void* W,
                        const void* bias, const void* residual, void* out, void* ws, void* cnt, void* args_out,
                        size_t* argbytes, dim3* grid, dim3* block, size_t* smem, const void** func);
+// W / bias written inside the graph: load them only after griddepcontrol.wait.
+void decoder_gemm_set_w_after_wait(void* args);
 // Make a built GEMM parameter block trigger its PDL dependents only after its wait (T5 node 2).
 void decoder_gemm_set_trigger_after_wait(void* args);
 // CGX_GEMM_ALLREDUCE: the epilogue's peer all-reduce (regions as for k_allreduce_peer).

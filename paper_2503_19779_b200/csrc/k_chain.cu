@@ -20,14 +20,35 @@ namespace cgx {
 static constexpr int kElemThreads = 256;
 static constexpr int kElemVec = 4;     // 16-B vectors per thread per operand (loads in flight)
 
-enum { OP_ADD = 0, OP_MUL = 1, OP_SCALE = 2, OP_COPY = 3, OP_SCALE_T = 4 };
+enum { OP_ADD = 0, OP_MUL = 1, OP_SCALE = 2, OP_COPY = 3, OP_SCALE_T = 4,
+       // training-shaped chain (bf16): a - b, a + s*b, GELU(a), dy * GELU'(x)
+       OP_SUB = 5, OP_AXPY = 6, OP_GELU = 7, OP_GELU_BWD = 8 };
+
+// tanh-approximate GELU and its derivative in fp32 with libm tanhf (SURVEY ambiguity 11)
+__device__ __forceinline__ float gelu_f(float x) {
+  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+  return 0.5f * x * (1.0f + tanhf(k0 * (x + k1 * x * x * x)));
+}
+__device__ __forceinline__ float gelu_grad_f(float x) {
+  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+  const float t = tanhf(k0 * (x + k1 * x * x * x));
+  return 0.5f * (1.0f + t) + 0.5f * x * (1.0f - t * t) * k0 * (1.0f + 3.0f * k1 * x * x);
+}
 
 template <int OP>
 __device__ __forceinline__ float apply_f32(float x, float y, float s) {
   if (OP == OP_ADD) return __fadd_rn(x, y);
   if (OP == OP_MUL) return __fmul_rn(x, y);
   if (OP == OP_SCALE || OP == OP_SCALE_T) return __fmul_rn(x, s);
+  if (OP == OP_SUB) return __fsub_rn(x, y);
+  if (OP == OP_AXPY) return __fmaf_rn(s, y, x);          // x + s*y, one fp32 rounding
+  if (OP == OP_GELU) return gelu_f(x);
+  if (OP == OP_GELU_BWD) return __fmul_rn(x, gelu_grad_f(y));   // x = dy, y = pre-activation
   return x;
+}
+template <int OP>
+__host__ __device__ constexpr bool elem_binary() {
+  return OP == OP_ADD || OP == OP_MUL || OP == OP_SUB || OP == OP_AXPY || OP == OP_GELU_BWD;
 }
 
 __device__ __forceinline__ void fetch_operands(const ElemArgs& a, const void*& p0, const void*& p1) {
@@ -211,7 +232,7 @@ __global__ void __launch_bounds__(kElemThreads) k_elem_bf16(const __grid_constan
     const uint64_t i = base + (uint64_t)j * kElemThreads;
     if (i < n8) {
       xv[j] = x[i];
-      if (OP == OP_ADD || OP == OP_MUL) yv[j] = y[i];
+      if (elem_binary<OP>()) yv[j] = y[i];
     }
   }
 #pragma unroll
@@ -224,7 +245,7 @@ __global__ void __launch_bounds__(kElemThreads) k_elem_bf16(const __grid_constan
       __nv_bfloat16* rb = reinterpret_cast<__nv_bfloat16*>(&r);
 #pragma unroll
       for (int e = 0; e < 8; ++e)
-        rb[e] = apply_bf16<OP>(xb[e], (OP == OP_ADD || OP == OP_MUL) ? yb[e] : xb[e], a.scalar);
+        rb[e] = apply_bf16<OP>(xb[e], elem_binary<OP>() ? yb[e] : xb[e], a.scalar);
       o[i] = r;
     }
   }
@@ -234,8 +255,44 @@ __global__ void __launch_bounds__(kElemThreads) k_elem_bf16(const __grid_constan
       const __nv_bfloat16* xs = reinterpret_cast<const __nv_bfloat16*>(p0);
       const __nv_bfloat16* ys = reinterpret_cast<const __nv_bfloat16*>(p1);
       reinterpret_cast<__nv_bfloat16*>(a.out)[t] =
-          apply_bf16<OP>(xs[t], (OP == OP_ADD || OP == OP_MUL) ? ys[t] : xs[t], a.scalar);
+          apply_bf16<OP>(xs[t], elem_binary<OP>() ? ys[t] : xs[t], a.scalar);
     }
+  }
+  sync_out(a);
+}
+
+// ---------------------------------------------------------------------------- TRANSPOSE bf16
+// out[c, r] = in[r, c] for a [rows, cols] bf16 matrix (rows = n / cols): 32 x 32 tiles staged in
+// shared memory (33-column padding: conflict-free column reads), 8 rows per warp pass. A pure copy:
+// bit-exact. Used by the training-shaped chain to feed transposed operands to the K-major GEMM.
+static constexpr int kTrTile = 32;
+template <int TW>
+__global__ void __launch_bounds__(256) k_transpose_bf16(const __grid_constant__ ArgsTW<ElemArgs, TW> A) {
+  const ElemArgs& a = A.a;
+  trace_at(a, 0);
+  tw_publish(A);
+  CGX_PROLOGUE(a, p0, p1)
+  (void)p1;
+  __shared__ __nv_bfloat16 tile[kTrTile][kTrTile + 1];
+  const uint32_t cols = a.cols, rows = (uint32_t)(a.n / a.cols);
+  const __nv_bfloat16* in = reinterpret_cast<const __nv_bfloat16*>(p0);
+  __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(a.out);
+  const uint32_t tx = threadIdx.x & 31, ty = threadIdx.x >> 5;      // 32 x 8 threads
+  const uint32_t tiles_c = (cols + kTrTile - 1) / kTrTile, tiles_r = (rows + kTrTile - 1) / kTrTile;
+  for (uint32_t t = blockIdx.x; t < tiles_c * tiles_r; t += gridDim.x) {
+    const uint32_t r0 = (t / tiles_c) * kTrTile, c0 = (t % tiles_c) * kTrTile;
+#pragma unroll
+    for (uint32_t k = 0; k < kTrTile; k += 8) {
+      const uint32_t r = r0 + ty + k, c = c0 + tx;
+      if (r < rows && c < cols) tile[ty + k][tx] = in[(size_t)r * cols + c];
+    }
+    __syncthreads();
+#pragma unroll
+    for (uint32_t k = 0; k < kTrTile; k += 8) {
+      const uint32_t c = c0 + ty + k, r = r0 + tx;                  // out row c, out col r
+      if (c < cols && r < rows) out[(size_t)c * rows + r] = tile[tx][ty + k];
+    }
+    __syncthreads();
   }
   sync_out(a);
 }
@@ -585,6 +642,10 @@ static const void* elem_fn(int op, int dtype) {
       case OP_MUL: return (const void*)k_elem_bf16<OP_MUL, TW>;
       case OP_SCALE: return (const void*)k_elem_bf16<OP_SCALE, TW>;
       case OP_COPY: return (const void*)k_elem_bf16<OP_COPY, TW>;
+      case OP_SUB: return (const void*)k_elem_bf16<OP_SUB, TW>;
+      case OP_AXPY: return (const void*)k_elem_bf16<OP_AXPY, TW>;
+      case OP_GELU: return (const void*)k_elem_bf16<OP_GELU, TW>;
+      case OP_GELU_BWD: return (const void*)k_elem_bf16<OP_GELU_BWD, TW>;
     }
   }
   return nullptr;
@@ -595,6 +656,15 @@ const void* kfn_elem(int op, int dtype, int tw) {
     case 8: return elem_fn<8>(op, dtype);
     case 64: return elem_fn<64>(op, dtype);
     case 512: return elem_fn<512>(op, dtype);
+  }
+  return nullptr;
+}
+const void* kfn_transpose_bf16(int tw) {
+  switch (tw) {
+    case 0: return (const void*)k_transpose_bf16<0>;
+    case 8: return (const void*)k_transpose_bf16<8>;
+    case 64: return (const void*)k_transpose_bf16<64>;
+    case 512: return (const void*)k_transpose_bf16<512>;
   }
   return nullptr;
 }

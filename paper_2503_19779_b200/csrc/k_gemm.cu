@@ -38,6 +38,9 @@ static constexpr int kBK = 64;          // 64 bf16 = 128 B = one swizzle-128B ro
 static constexpr int kMaxStages = 4;
 static constexpr int kGemmThreads = 192;
 static constexpr uint32_t kGemmTriggerAfterWait = 1u << 8;   // internal flag bit (above CGX_GEMM_*)
+// W (and bias) written by an earlier node of the graph (training chain: transposed activations,
+// updated weights): no pre-wait weight prefetch / loads
+static constexpr uint32_t kGemmWAfterWait = 1u << 11;
 
 struct alignas(64) GemmArgs {
   CUtensorMap tmA;            // A [M, K] bf16, box {64, 128}
@@ -301,13 +304,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
   if (warp == 0) {
     if (lane == 0) {
       // ---- TMA producer. Weights first (independent of the predecessor), then wait, then A.
+      const bool w_late = a.flags & kGemmWAfterWait;
+      if (w_late) pdl_wait();
       for (int i = 0; i < kps; ++i) tma_prefetch_l2(&a.tmB, (kbase + i) * kBK, n0);
       const int pre = kps < kStages ? kps : kStages;
       for (int i = 0; i < pre; ++i) {
         mbar_expect_tx(&full[i], kABytes + kBBytes);
         tma_load_2d(sB + i * kBBytes, &a.tmB, &full[i], (kbase + i) * kBK, n0);
       }
-      pdl_wait();
+      if (!w_late) pdl_wait();
       if (late_trigger) pdl_trigger();
       for (int i = 0; i < pre; ++i) tma_load_2d(sA + i * kABytes, &a.tmA, &full[i], (kbase + i) * kBK, m0);
       for (int i = pre; i < kps; ++i) {
@@ -351,6 +356,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
     const uint32_t et = threadIdx.x - 64;          // epilogue thread 0..127
     const bool has_bias = a.flags & CGX_GEMM_BIAS, has_res = a.flags & CGX_GEMM_RESIDUAL;
     const bool gelu = a.flags & CGX_GEMM_GELU;
+    if (has_bias && (a.flags & kGemmWAfterWait)) pdl_wait();
     for (uint32_t i = et; i < (uint32_t)BN; i += 128u)
       sbias[i] = has_bias ? __bfloat162float(a.bias[n0 + i]) : 0.f;
     const uint32_t cta_lin = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
@@ -595,15 +601,17 @@ __global__ void __launch_bounds__(kGvWarps * 32) k_gemv_bf16(const __grid_consta
   const uint32_t n0 = (blockIdx.x * kGvWarps + warp) * R;     // this warp's first output column
   const uint32_t kv = a.K / 8;                                  // 16-B vectors per row
   // ---- W rows n0 .. n0+R-1 (STATIC): all loads in flight before the wait
+  const bool w_late = a.flags & kGemmWAfterWait;
+  if (w_late) pdl_wait();
   uint4 w[R][kGvKV];
 #pragma unroll
   for (int r = 0; r < R; ++r)
 #pragma unroll
     for (int i = 0; i < kGvKV; ++i) {
       const uint32_t v = lane + 32u * i;
-      if (n0 + r < a.N && v < kv) w[r][i] = __ldg(reinterpret_cast<const uint4*>(a.w_ptr + (size_t)(n0 + r) * a.K) + v);
+      if (n0 + r < a.N && v < kv) w[r][i] = *(reinterpret_cast<const uint4*>(a.w_ptr + (size_t)(n0 + r) * a.K) + v);
     }
-  pdl_wait();
+  if (!w_late) pdl_wait();
   if (late_trigger) pdl_trigger();
   float acc[R][kGvMaxM];
 #pragma unroll
@@ -801,6 +809,10 @@ size_t decoder_gemm_residual_field(size_t* tidx_off) {
 
 void decoder_gemm_set_trace(void* args, unsigned long long* trace) {
   static_cast<GemmArgs*>(args)->trace = trace;
+}
+
+void decoder_gemm_set_w_after_wait(void* args) {
+  static_cast<GemmArgs*>(args)->flags |= kGemmWAfterWait;
 }
 
 void decoder_gemm_set_trigger_after_wait(void* args) {

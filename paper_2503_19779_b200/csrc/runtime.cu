@@ -140,6 +140,19 @@ struct cgx_chain {
 
 static size_t dtype_size(cgx_dtype d) { return d == CGX_F32 ? 4 : 2; }
 
+// Op families. Elementwise kernels (k_elem_f32 / k_elem_bf16); everything that takes the ElemArgs
+// parameter block (elementwise, REDUCE_SUM, TRANSPOSE): table-indexed operands, dataflow flags.
+static bool is_elemwise(cgx_op op) {
+  return op == CGX_OP_ADD || op == CGX_OP_MUL || op == CGX_OP_SCALE_IMM || op == CGX_OP_COPY || op == CGX_OP_SCALE_T ||
+         op == CGX_OP_SUB || op == CGX_OP_AXPY || op == CGX_OP_GELU || op == CGX_OP_GELU_BWD;
+}
+static bool uses_elem_args(cgx_op op) {
+  return is_elemwise(op) || op == CGX_OP_REDUCE_SUM || op == CGX_OP_TRANSPOSE;
+}
+static bool elem_binary(cgx_op op) {
+  return op == CGX_OP_ADD || op == CGX_OP_MUL || op == CGX_OP_SUB || op == CGX_OP_AXPY || op == CGX_OP_GELU_BWD;
+}
+
 extern "C" int cgx_chain_create(int device, cgx_chain** out) {
   if (!out) return fail(CGX_E_INVALID_ARG, "cgx_chain_create: out is NULL");
   int n = 0;
@@ -178,11 +191,17 @@ static int check_node(const cgx_chain* c, const Node& n) {
   const cgx_attr& a = n.attr;
   auto need = [&](bool ok, const char* m) { return ok ? CGX_OK : fail(CGX_E_SIZE_MISMATCH, m); };
   switch (n.op) {
+    case CGX_OP_SUB:
+    case CGX_OP_AXPY:
+    case CGX_OP_GELU:
+    case CGX_OP_GELU_BWD:
+      if (o.dtype != CGX_BF16) return fail(CGX_E_UNSUPPORTED, "sub/axpy/gelu/gelu_bwd: bf16 only");
+      [[fallthrough]];
     case CGX_OP_ADD:
     case CGX_OP_MUL:
     case CGX_OP_SCALE_IMM:
     case CGX_OP_COPY: {
-      int nin = (n.op == CGX_OP_ADD || n.op == CGX_OP_MUL) ? 2 : 1;
+      int nin = elem_binary(n.op) ? 2 : 1;
       if (n.n_in != nin) return fail(CGX_E_INVALID_ARG, "elementwise: wrong number of inputs");
       for (int i = 0; i < nin; ++i) {
         if (S(i).dtype != o.dtype) return fail(CGX_E_UNSUPPORTED, "elementwise: mixed dtypes");
@@ -190,6 +209,11 @@ static int check_node(const cgx_chain* c, const Node& n) {
       }
       return need(o.nelems >= a.n, "elementwise: output shorter than attr.n");
     }
+    case CGX_OP_TRANSPOSE:
+      if (n.n_in != 1) return fail(CGX_E_INVALID_ARG, "transpose: one input");
+      if (S(0).dtype != CGX_BF16 || o.dtype != CGX_BF16) return fail(CGX_E_UNSUPPORTED, "transpose: bf16 only");
+      CKS(need(a.cols > 0 && a.n % a.cols == 0, "transpose: n must be rows x cols"));
+      return need(S(0).nelems >= a.n && o.nelems >= a.n, "transpose: shape");
     case CGX_OP_SCALE_T:
       if (n.n_in != 2) return fail(CGX_E_INVALID_ARG, "scale_t: inputs a, s");
       if (S(0).dtype != CGX_F32 || S(1).dtype != CGX_F32 || o.dtype != CGX_F32)
@@ -249,8 +273,7 @@ extern "C" int cgx_chain_add_node(cgx_chain* c, cgx_op op, const int* in_slots, 
   }
   if (c->slots[out_slot].kind != CGX_SLOT_INTERNAL)
     return fail(CGX_E_NOT_ELIGIBLE, "add_node: output must be an INTERNAL slot (no writes to inputs/weights)");
-  if ((op == CGX_OP_ADD || op == CGX_OP_MUL || op == CGX_OP_SCALE_IMM || op == CGX_OP_COPY ||
-       op == CGX_OP_REDUCE_SUM || op == CGX_OP_ALLREDUCE_SUM || op == CGX_OP_SCALE_T) && n.attr.n == 0 && n_in > 0)
+  if ((uses_elem_args(op) || op == CGX_OP_ALLREDUCE_SUM) && n.attr.n == 0 && n_in > 0)
     n.attr.n = c->slots[n.in[0]].nelems;
   if (op == CGX_OP_REDUCE_SUM && n.attr.cols == 0) n.attr.cols = 256;
   CKS(check_node(c, n));
@@ -518,7 +541,7 @@ static bool t5_byvalue(const cgx_exec* e, int pos) {
           eff_transport(e->o) == CGX_XPORT_PRELUDE);
 }
 static bool tw_capable(cgx_op op) {
-  return op <= CGX_OP_REDUCE_SUM || op == CGX_OP_LAYERNORM || op == CGX_OP_SCALE_T;
+  return uses_elem_args(op) || op == CGX_OP_LAYERNORM;
 }
 
 template <typename Base>
@@ -578,7 +601,7 @@ static int build_launch(cgx_exec* e, int k, Launch& l) {
   const bool patch = mode == CGX_MODE_EAGER || mode == CGX_MODE_GRAPH_SETPARAMS || mode == CGX_MODE_GRAPH_STALE ||
                      byvalue;
   const int twc = tw ? tw_cap((int)c->ext_slots.size()) : 0;
-  if (tw && (twc == 0 || !(n.op <= CGX_OP_REDUCE_SUM || n.op == CGX_OP_LAYERNORM || n.op == CGX_OP_SCALE_T)))
+  if (tw && (twc == 0 || !(uses_elem_args(n.op) || n.op == CGX_OP_LAYERNORM)))
     return fail(CGX_E_UNSUPPORTED, "FIRST_NODE transport: first node must be elementwise/reduce/LN, <= 512 externals");
 
   switch (n.op) {
@@ -587,6 +610,11 @@ static int build_launch(cgx_exec* e, int k, Launch& l) {
     case CGX_OP_SCALE_IMM:
     case CGX_OP_COPY:
     case CGX_OP_SCALE_T:
+    case CGX_OP_SUB:
+    case CGX_OP_AXPY:
+    case CGX_OP_GELU:
+    case CGX_OP_GELU_BWD:
+    case CGX_OP_TRANSPOSE:
     case CGX_OP_REDUCE_SUM: {
       make_args<ElemArgs>(e, l, tw);
       ElemArgs* a = argp<ElemArgs>(l);
@@ -610,13 +638,20 @@ static int build_launch(cgx_exec* e, int k, Launch& l) {
           }
         }
       }
-      if (n.op == CGX_OP_REDUCE_SUM) {
+      if (n.op == CGX_OP_TRANSPOSE) {
+        l.func = kfn_transpose_bf16(twc);
+        l.block = dim3(256);
+        const uint64_t rows = n.attr.n / n.attr.cols;
+        const uint64_t tiles = ceil_div(rows, 32) * ceil_div((uint64_t)n.attr.cols, 32);
+        l.grid = dim3((unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tiles, 148ull * 8)));
+      } else if (n.op == CGX_OP_REDUCE_SUM) {
         l.func = kfn_reduce_sum_f32(twc);
         l.block = dim3(256);
         l.grid = dim3((unsigned)std::max<uint64_t>(1, std::min<uint64_t>(ceil_div(n.attr.n / n.attr.cols, 8), chain_grid_cap())));
       } else {
         const int opi = n.op == CGX_OP_ADD ? 0 : n.op == CGX_OP_MUL ? 1 : n.op == CGX_OP_SCALE_IMM ? 2
-                        : n.op == CGX_OP_SCALE_T ? 4 : 3;
+                        : n.op == CGX_OP_SCALE_T ? 4 : n.op == CGX_OP_SUB ? 5 : n.op == CGX_OP_AXPY ? 6
+                        : n.op == CGX_OP_GELU ? 7 : n.op == CGX_OP_GELU_BWD ? 8 : 3;
         const int dt = c->slots[n.out].dtype == CGX_F32 ? 0 : 1;
         l.func = kfn_elem(opi, dt, twc);
         l.block = dim3(elem_block_threads());
@@ -684,6 +719,14 @@ static int build_launch(cgx_exec* e, int k, Launch& l) {
         e->gemm_cnt_off += c1;
       }
       l.cluster_z = l.grid.z;
+      // the weight / bias operands are prefetched before griddepcontrol.wait unless a node of the
+      // chain writes them (training chain: transposed activations, in-place weight updates)
+      {
+        bool written = false;
+        for (const Node& q : c->nodes)
+          if (q.out == n.in[1] || q.out == n.in[2]) written = true;
+        if (written) decoder_gemm_set_w_after_wait(l.args.p);
+      }
       if (n.attr.flags & CGX_GEMM_ALLREDUCE) {
         if (c->peer_world <= 0) return fail(CGX_E_STATE, "gemm allreduce: no peers (cgx_chain_set_peers)");
         if ((uint64_t)n.attr.M * n.attr.N > c->peer_max_elems || n.attr.N % 8)
@@ -781,7 +824,7 @@ static void set_prewait_masks(cgx_exec* e) {
   for (auto& l : e->L) {
     if (l.kind != LK_KERNEL) continue;
     const Node& node = e->c->nodes[l.node];
-    if (node.op > CGX_OP_REDUCE_SUM && node.op != CGX_OP_SCALE_T) continue;
+    if (!uses_elem_args(node.op)) continue;
     uint32_t pre = 0;
     for (int j = 0; j < node.n_in && j < 2; ++j) {
       const cgx_slot_kind k = e->c->slots[node.in[j]].kind;
@@ -809,8 +852,8 @@ static void set_prewait_masks(cgx_exec* e) {
 //
 // Eager mode keeps plain PDL waits: there the previous iteration's nodes are stream predecessors.
 static bool df_capable(const Node& n, cgx_dtype out_dt) {
-  if (n.op == CGX_OP_REDUCE_SUM) return true;
-  if (n.op <= CGX_OP_COPY) return true;                         // f32 and bf16 elementwise
+  if (n.op == CGX_OP_REDUCE_SUM || n.op == CGX_OP_TRANSPOSE) return true;
+  if (is_elemwise(n.op) && n.op != CGX_OP_SCALE_T) return true;   // f32 and bf16 elementwise
   return n.op == CGX_OP_SCALE_T && out_dt == CGX_F32;
 }
 
@@ -1264,8 +1307,7 @@ static int capture_graph(cgx_exec* e, int gi) {
     // graph gi reads table gi: the `table` field is the first member of ElemArgs and LnArgs
     uint64_t* tab = gi == 0 ? e->d_table : e->d_table2;
     for (auto& l : e->L) {
-      if (l.kind == LK_KERNEL && (e->c->nodes[l.node].op <= CGX_OP_REDUCE_SUM ||
-                                  e->c->nodes[l.node].op == CGX_OP_SCALE_T ||
+      if (l.kind == LK_KERNEL && (uses_elem_args(e->c->nodes[l.node].op) ||
                                   e->c->nodes[l.node].op == CGX_OP_LAYERNORM))
         memcpy(l.args.p, &tab, sizeof(tab));
       const Node& gn = e->c->nodes[l.node];
@@ -1320,7 +1362,7 @@ static int capture_graph(cgx_exec* e, int gi) {
         const Node& n = e->c->nodes[l.node];
         const uint32_t f = kFlagTableAfterWait | kFlagTriggerAfterWait;
         if (n.op == CGX_OP_LAYERNORM) argp<LnArgs>(l)->flags |= f;
-        else if (n.op <= CGX_OP_REDUCE_SUM || n.op == CGX_OP_SCALE_T)
+        else if (uses_elem_args(n.op))
           argp<ElemArgs>(l)->flags = (argp<ElemArgs>(l)->flags | f | ((argp<ElemArgs>(l)->flags & kFlagDataflow) ? kFlagDfPdlWait : 0u)) & ~kFlagDeferWait;
         else return fail(CGX_E_UNSUPPORTED, "first node after the root table writer must be elementwise/LN");
       }
@@ -1509,7 +1551,7 @@ extern "C" int cgx_exec_create_ex(cgx_chain* c, const cgx_exec_opts* opts, void*
   e->st.n_graph_nodes = e->graph_nodes;
   e->st.n_deferred = 0;
   for (auto& l : e->L)
-    if (l.kind == LK_KERNEL && (e->c->nodes[l.node].op <= CGX_OP_COPY || e->c->nodes[l.node].op == CGX_OP_SCALE_T))
+    if (l.kind == LK_KERNEL && is_elemwise(e->c->nodes[l.node].op))
       e->st.n_deferred += (argp<ElemArgs>(l)->flags & kFlagDeferWait) ? 1u : 0u;
   e->st.dataflow = e->dataflow ? 1u : 0u;
   e->st.dag_streams = e->dag_used;

@@ -258,6 +258,78 @@ def c3_chain(T: int = 128, n_layers: int = 12, tp: int = 1, rank: int = 0,
     return ChainSpec(name, slots, nodes, [(0, len(nodes) - 1)])
 
 
+# ----------------------------------------------------------------------------- training-shaped (NEXT-4)
+
+def mlp_train_chain(T: int = 128, d: int = 768, dff: int = 3072, n_blocks: int = 6,
+                    lr: float = 0.5) -> ChainSpec:
+    """A training step of a stack of GPT-2-shaped MLP blocks (SURVEY §8(f) NEXT-4 "training-shaped
+    (fwd+bwd) chain", P:L694 DGPT2-T), bf16, batch T tokens, no biases, MSE loss:
+
+      forward per block l (a_0 = X, staged by a COPY node):  pre_l = a_l W1_l^T;  h_l = GELU(pre_l);  a_{l+1} = h_l W2_l^T
+      loss gradient:                  dy = (a_L - target) * 2 / (T d)
+      backward per block (l = L-1..0), with dy the gradient w.r.t. a_{l+1}:
+        dW2 = dy^T h_l;  dh = dy W2;  dpre = dh * GELU'(pre_l);  dW1 = dpre^T a_l;  da = dpre W1 (l > 0)
+      update:                         W <- W - lr dW (in place)
+
+    Every product is a K-major GEMM (out = A B^T): the transposed operands (dy^T, h^T, W2^T, ...)
+    come from TRANSPOSE nodes. The weights are INTERNAL slots updated in place every replay; nodes
+    [0, 2 n_blocks) form an init segment that copies the STATIC initial weights into them (run once),
+    the rest is the training step (segment 1) with X and target EXTERNAL, fresh every step."""
+    slots = [SlotSpec("X", EXTERNAL, "bf16", T * d), SlotSpec("target", EXTERNAL, "bf16", T * d),
+             SlotSpec("zb_dff", STATIC, "bf16", dff, "zero"), SlotSpec("zb_d", STATIC, "bf16", d, "zero")]
+    nodes = []
+    for l in range(n_blocks):
+        p = f"B{l}."
+        slots += [SlotSpec(p + "W1_0", STATIC, "bf16", dff * d, "weight"),
+                  SlotSpec(p + "W2_0", STATIC, "bf16", d * dff, "weight"),
+                  SlotSpec(p + "W1", INTERNAL, "bf16", dff * d), SlotSpec(p + "W2", INTERNAL, "bf16", d * dff)]
+        nodes += [NodeSpec("COPY", (p + "W1_0",), p + "W1", {"n": dff * d}),
+                  NodeSpec("COPY", (p + "W2_0",), p + "W2", {"n": d * dff})]
+    n_init = len(nodes)
+    g = lambda M, N, K: {"M": M, "N": N, "K": K, "bias": False, "gelu": False}  # noqa: E731
+    # the step's input is staged by one COPY node (a GEMM reads its A operand through a TMA tensor
+    # map encoded at capture, so it cannot take a rebindable EXTERNAL pointer)
+    slots.append(SlotSpec("x_in", INTERNAL, "bf16", T * d))
+    nodes.append(NodeSpec("COPY", ("X",), "x_in", {"n": T * d}))
+    a = "x_in"
+    acts = []
+    for l in range(n_blocks):
+        p = f"B{l}."
+        for nm, n in (("pre", T * dff), ("h", T * dff), ("y", T * d)):
+            slots.append(SlotSpec(p + nm, INTERNAL, "bf16", n))
+        nodes += [NodeSpec("GEMM_BF16", (a, p + "W1", "zb_dff"), p + "pre", g(T, dff, d)),
+                  NodeSpec("GELU", (p + "pre",), p + "h", {"n": T * dff}),
+                  NodeSpec("GEMM_BF16", (p + "h", p + "W2", "zb_d"), p + "y", g(T, d, dff))]
+        acts.append(a)
+        a = p + "y"
+    slots += [SlotSpec("r", INTERNAL, "bf16", T * d), SlotSpec("dyL", INTERNAL, "bf16", T * d)]
+    nodes += [NodeSpec("SUB", (a, "target"), "r", {"n": T * d}),
+              NodeSpec("SCALE_IMM", ("r",), "dyL", {"n": T * d, "scalar": 2.0 / (T * d)})]
+    dy = "dyL"
+    for l in reversed(range(n_blocks)):
+        p = f"B{l}."
+        for nm, n in (("dyT", d * T), ("hT", dff * T), ("dW2", d * dff), ("W2T", dff * d), ("dh", T * dff),
+                      ("dpre", T * dff), ("dpreT", dff * T), ("aT", d * T), ("dW1", dff * d),
+                      ("W1T", d * dff), ("da", T * d)):
+            slots.append(SlotSpec(p + nm, INTERNAL, "bf16", n))
+        nodes += [NodeSpec("TRANSPOSE", (dy,), p + "dyT", {"n": T * d, "cols": d}),
+                  NodeSpec("TRANSPOSE", (p + "h",), p + "hT", {"n": T * dff, "cols": dff}),
+                  NodeSpec("GEMM_BF16", (p + "dyT", p + "hT", "zb_dff"), p + "dW2", g(d, dff, T)),
+                  NodeSpec("TRANSPOSE", (p + "W2",), p + "W2T", {"n": d * dff, "cols": dff}),
+                  NodeSpec("GEMM_BF16", (dy, p + "W2T", "zb_dff"), p + "dh", g(T, dff, d)),
+                  NodeSpec("GELU_BWD", (p + "dh", p + "pre"), p + "dpre", {"n": T * dff}),
+                  NodeSpec("TRANSPOSE", (p + "dpre",), p + "dpreT", {"n": T * dff, "cols": dff}),
+                  NodeSpec("TRANSPOSE", (acts[l],), p + "aT", {"n": T * d, "cols": d}),
+                  NodeSpec("GEMM_BF16", (p + "dpreT", p + "aT", "zb_d"), p + "dW1", g(dff, d, T))]
+        if l > 0:
+            nodes += [NodeSpec("TRANSPOSE", (p + "W1",), p + "W1T", {"n": dff * d, "cols": d}),
+                      NodeSpec("GEMM_BF16", (p + "dpre", p + "W1T", "zb_d"), p + "da", g(T, d, dff))]
+            dy = p + "da"
+        nodes += [NodeSpec("AXPY", (p + "W2", p + "dW2"), p + "W2", {"n": d * dff, "scalar": -lr}),
+                  NodeSpec("AXPY", (p + "W1", p + "dW1"), p + "W1", {"n": dff * d, "scalar": -lr})]
+    return ChainSpec(f"MLPT_T{T}_B{n_blocks}", slots, nodes, [(0, n_init - 1), (n_init, len(nodes) - 1)])
+
+
 def tp_weight(full: ChainSpec, name: str, tp: int, rank: int, values: np.ndarray) -> np.ndarray:
     """Slice the TP=1 value array of weight slot `name` (bf16 bits) into rank `rank`'s shard.
 
