@@ -787,6 +787,11 @@ def run_extras(args, torch, cgx, runner, wl, sm, spec, chain, stream, sets, set_
         out["decoder_c3"] = bench_decoder(torch, cgx, runner, wl, stream, dev, peaks)
     except Exception as exn:  # noqa: BLE001
         out["decoder_c3"] = {"error": str(exn)}
+    # ---------------- NEXT-4: training-shaped chain (fwd + bwd + SGD of 6 GPT-2 MLP blocks)
+    try:
+        out["training_chain"] = bench_training(torch, cgx, runner, wl, stream, dev)
+    except Exception as exn:  # noqa: BLE001
+        out["training_chain"] = {"error": str(exn)}
 
     # ---------------- copy kernel at the C4 1 GiB point (HBM roofline target >= 80%)
     try:
@@ -834,6 +839,55 @@ def run_extras(args, torch, cgx, runner, wl, sm, spec, chain, stream, sets, set_
                                      f"threadpoolctl 1 thread) on {os.cpu_count()}-core host "
                                      f"{cpu_info()}"}
     return out
+
+
+def bench_training(torch, cgx, runner, wl, stream, dev):
+    """Training-shaped chain: one step = forward + loss gradient + backward +
+    in-place SGD of 6 GPT-2-shaped MLP blocks (T=128, bf16), fresh X / target every step. Per arm:
+    µs per step and the rebinding Δ against the same exec without binding."""
+    spec = wl.mlp_train_chain(n_blocks=6)
+    chain = runner.Chain(spec, runner.upload_statics(spec, wl.static_values(spec), dev))
+    f0, l0 = spec.segments[0]
+    f1, l1 = spec.segments[1]
+    sets = [runner.upload_externals(spec, wl.external_values(spec, r), dev) for r in range(4)]
+    ptrs = [cgx.ptr_array([t[n].data_ptr() for n in chain.ext_names]) for t in sets]
+    LIB = cgx.LIB
+    init = chain.exec("EAGER", stream=stream, first_node=f0, n_nodes=l0 - f0 + 1)
+    LIB.cgx_bind(init.handle, ptrs[0], 2)
+    LIB.cgx_launch(init.handle)
+
+    def timed(h, n, bind=True):
+        best = 1e30
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            stream.synchronize()
+            e0.record(stream)
+            for i in range(n):
+                if bind:
+                    LIB.cgx_bind(h, ptrs[i % 4], 2)
+                LIB.cgx_launch(h)
+            e1.record(stream)
+            e1.synchronize()
+            best = min(best, e0.elapsed_time(e1) * 1e3 / n)
+        return best
+    res = {"workload": "6 GPT-2 MLP blocks (d 768, d_ff 3072, T 128, bf16): forward, MSE gradient, backward "
+                       "(TRANSPOSE + tcgen05 GEMMs + GELU_BWD), in-place SGD; fresh X / target per step",
+           "kernels_per_step": l1 - f1 + 1, "us_per_step": {}, "rebind_delta_us": {}}
+    for name, mode, xp in (("indirect_root_params", "INDIRECT", "ROOT_PARAMS"), ("copy", "COPY", "DEFAULT"),
+                           ("setparams", "SETPARAMS", "DEFAULT"), ("eager", "EAGER", "DEFAULT")):
+        ex = chain.exec(mode, stream=stream, transport=xp, first_node=f1, n_nodes=l1 - f1 + 1)
+        for i in range(5):
+            LIB.cgx_bind(ex.handle, ptrs[i % 4], 2)
+            LIB.cgx_launch(ex.handle)
+        n = 100 if mode != "EAGER" else 30
+        us = timed(ex.handle, n)
+        res["us_per_step"][name] = us
+        if mode != "EAGER":
+            res["rebind_delta_us"][name] = us - timed(ex.handle, n, bind=False)
+        ex.close()
+    res["steps_per_s_indirect"] = 1e6 / res["us_per_step"]["indirect_root_params"]
+    chain.close()
+    return res
 
 
 def bench_decoder(torch, cgx, runner, wl, stream, dev, peaks):
