@@ -1224,8 +1224,15 @@ static int capture_dag(cgx_exec* e, int gi, cudaStream_t cs, cgx_transport t) {
     e->dag_ev.assign(nl + 1 + (size_t)S, nullptr);   // per node, fork, per-stream join
     for (auto& ev : e->dag_ev) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   }
-  // T5: the by-value prefix up to the table publisher runs on the origin stream before the fork
-  const int pre = (indirect && t == CGX_XPORT_FIRST_NODE) ? e->t5_pub : -1;
+  // T5: the by-value prefix up to the table publisher runs on the origin stream before the fork.
+  // Without a root node (COPY / SETPARAMS / STALE, the H2D and DEVICE transports) the first node
+  // is the prefix: a graph whose branches fork from one completed node replays faster than one
+  // with many entry nodes (training chain: 345 vs 378-389 us per step; C2 COPY: 2.7 us),
+  // measured with scripts/diag_training_arms.py.
+  const bool has_root = indirect && (t == CGX_XPORT_ROOT_MEMCPY || t == CGX_XPORT_ROOT_PARAMS ||
+                                     t == CGX_XPORT_ROOT_MAPPED || t == CGX_XPORT_PRELUDE);
+  int pre = (indirect && t == CGX_XPORT_FIRST_NODE) ? e->t5_pub : -1;
+  if (!has_root && pre < 0 && nl > 1) pre = 0;
   // stream assignment (pure pass)
   std::vector<int> stream_of(nl, -1), tail((size_t)S, -1);
   for (int p = pre + 1; p < (int)nl; ++p) {
