@@ -236,12 +236,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    # one host core per rank ("host thread pinned to a core; one process per GPU")
-    try:
-        cpus = sorted(os.sched_getaffinity(0))
-        os.sched_setaffinity(0, {cpus[(2 * local + 1) % len(cpus)]})
-    except (AttributeError, OSError):
-        pass
+    # (the host thread is not pinned: the clock sampler's nvidia-smi subprocess and the CPU oracle
+    # would inherit a one-core affinity and compete with the launch loop on that core)
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
