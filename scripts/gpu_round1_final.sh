@@ -21,5 +21,7 @@ timeout 300 python scripts/diag_cadence_split.py > gpurun_out/cadence_split.txt 
 timeout 120 python scripts/diag_h2d.py > gpurun_out/h2d.txt 2>&1
 timeout 300 python scripts/diag_decode.py > gpurun_out/decode.txt 2>&1
 timeout 300 python scripts/diag_devloop.py > gpurun_out/devloop.txt 2>&1
+timeout 300 python scripts/diag_training_arms.py > gpurun_out/training_arms.txt 2>&1
+timeout 300 python scripts/diag_concurrent_graphs.py > gpurun_out/concurrent_graphs.txt 2>&1
 timeout 200 ncu --graph-profiling graph --clock-control none --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sector_hit_rate.pct --csv python scripts/ncu_targets.py replay > gpurun_out/ncu_graph_replay.csv 2>&1
 ls -la gpurun_out | tail -30
