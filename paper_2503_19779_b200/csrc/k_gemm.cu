@@ -8,11 +8,16 @@
 // issuer, warps 2..5 = epilogue (warp w reads TMEM lane quarter w % 4).
 // Operands are K-major, staged by TMA with the 128-byte swizzle into a STAGES-deep mbarrier ring.
 //
-// Programmatic dependent launch: W is a STATIC slot (weights never written by the chain), so the
+// Programmatic dependent launch: when W is a STATIC slot (weights never written by the chain) the
 // producer prefetches this CTA's whole W slab into L2 and issues the first stages' W tiles BEFORE
-// griddepcontrol.wait; only the A tiles (the predecessor's output) wait. At the C3 shapes the
-// GEMMs are weight-streaming bound (M = 128: ~128 FLOP/B, below the ~210 FLOP/B ridge), so
+// griddepcontrol.wait; only the A tiles (the predecessor's output) wait (kGemmWAfterWait moves the
+// W loads behind the wait when a node writes W: the training chain). At the C3 shapes the GEMMs are
+// weight-streaming / latency bound (M = 128: ~128 FLOP/B, below the ~210 FLOP/B ridge), so
 // overlapping the weight fetch with the previous node's tail is the main lever.
+//
+// Also here: split-K over a thread-block cluster with bulk-DSMEM pushes (below), the fused
+// tensor-parallel all-reduce epilogue (CGX_GEMM_ALLREDUCE), and the small-M (decode) path
+// k_gemv_bf16.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
