@@ -237,7 +237,7 @@ __device__ __forceinline__ void ar_publish_wait(const GemmArgs& a, uint32_t cta,
   asm volatile("bar.sync 1, 128;\n" ::: "memory");
 }
 
-template <int BN>
+template <int BN, bool AR>
 __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_constant__ GemmArgs a) {
   constexpr uint32_t kABytes = kBM * kBK * 2;     // 16 KiB
   constexpr uint32_t kBBytes = BN * kBK * 2;
@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
   if (threadIdx.x == 0) trace_at(a, 0);
   // an all-reducing GEMM never triggers early: no successor may sit resident while it waits for
   // its peers (dependents then launch at its completion)
-  const bool ar = a.flags & CGX_GEMM_ALLREDUCE;
+  constexpr bool ar = AR;                        // CGX_GEMM_ALLREDUCE instantiation
   const bool late_trigger = (a.flags & kGemmTriggerAfterWait) && !ar;
   if (!late_trigger && !ar) pdl_trigger();   // dependents may start their prologues (they read our output after their wait)
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -767,19 +767,21 @@ void decoder_gemm_plan(uint32_t, uint32_t, uint32_t, size_t* ws_bytes, size_t* c
   *cnt_bytes = 0;
 }
 
-template <int BN>
+template <int BN, bool AR>
 static const void* setup_kernel() {
   static std::once_flag once;
   std::call_once(once, [] {
     // headroom below the 227 KiB per-block limit for the kernel's static shared memory
-    cudaFuncSetAttribute(k_gemm_bf16<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    cudaFuncSetAttribute(k_gemm_bf16<BN>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(k_gemm_bf16<BN, AR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(k_gemm_bf16<BN, AR>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   });
-  return (const void*)k_gemm_bf16<BN>;
+  return (const void*)k_gemm_bf16<BN, AR>;
 }
 
-static const void* kernel_for(int bn) {
-  return bn == 128 ? setup_kernel<128>() : bn == 64 ? setup_kernel<64>() : setup_kernel<32>();
+// the fused all-reduce epilogue is a separate instantiation: the plain kernel keeps its code
+static const void* kernel_for(int bn, bool ar = false) {
+  if (ar) return bn == 128 ? setup_kernel<128, true>() : bn == 64 ? setup_kernel<64, true>() : setup_kernel<32, true>();
+  return bn == 128 ? setup_kernel<128, false>() : bn == 64 ? setup_kernel<64, false>() : setup_kernel<32, false>();
 }
 
 void decoder_gemm_set_allreduce(void* args, uint32_t rank, uint32_t world, uint32_t ar_index, uint32_t n_ar,
@@ -872,7 +874,7 @@ int decoder_gemm_build(uint32_t M, uint32_t N, uint32_t K, uint32_t flags, const
   *grid = dim3(N / bn, (M + kBM - 1) / kBM, sp);
   *block = dim3(kGemmThreads);
   *smem = smem_bytes(bn, sp, stages);
-  *func = kernel_for(bn);
+  *func = kernel_for(bn, (flags & CGX_GEMM_ALLREDUCE) != 0);
   if (!args_out) return CGX_OK;
   if (get_encode() != CGX_OK) return CGX_E_CUDA;
   GemmArgs* g = static_cast<GemmArgs*>(args_out);
