@@ -238,9 +238,17 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     # (the host thread is not pinned: the clock sampler's nvidia-smi subprocess and the CPU oracle
     # would inherit a one-core affinity and compete with the launch loop on that core)
+    # functional checks of the multi-rank path on a one-GPU box (never a measurement):
+    # CGX_BENCH_DEVICE pins every rank to one device, CGX_BENCH_PG=gloo avoids NCCL's one-rank-per-GPU rule
+    if os.environ.get("CGX_BENCH_DEVICE") is not None:
+        local = int(os.environ["CGX_BENCH_DEVICE"])
     torch.cuda.set_device(local)
+    pg_gloo = os.environ.get("CGX_BENCH_PG") == "gloo"
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if pg_gloo:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     from paper_2503_19779_b200 import build
     if rank == 0:
@@ -321,7 +329,7 @@ def main():
         dist.barrier()
     clk = clocks.stop() if clocks else None
     el_ms = e0.elapsed_time(e1)
-    t = torch.tensor([el_ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([el_ms], dtype=torch.float64, device="cpu" if pg_gloo else dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     max_ms = float(t.item())
@@ -456,7 +464,8 @@ def run_e2e_all(torch, cgx, wl, spec, chain, stream, dev, world):
     e2e_dt = run_e2e(n_e2e)
     if world > 1:                               # whole job: every rank's steps / max over ranks
         import torch.distributed as dist
-        tt = torch.tensor([e2e_dt], dtype=torch.float64, device=dev)
+        tt = torch.tensor([e2e_dt], dtype=torch.float64,
+                          device="cpu" if os.environ.get("CGX_BENCH_PG") == "gloo" else dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_dt = float(tt.item()) / world
     res = {"value": n_e2e / e2e_dt, "unit": "iters/s",
