@@ -63,3 +63,15 @@ def test_product_and_oracle_are_independent():
                 if f.endswith((".py", ".cu", ".h", ".cuh", ".cpp")):
                     txt = open(os.path.join(dirpath, f)).read()
                     assert not re.search(rf"^\s*(from|import)\s+{forbidden}\b", txt, re.M), (f, forbidden)
+
+
+def test_peer_buffer_bytes_host_only():
+    """cgx_peer_buffer_bytes is pure host arithmetic: receive data [2][world][slot] bf16 (slots
+    rounded up to 128 elements) followed by the flag array [64][8][256] uint32."""
+    from paper_2503_19779_b200 import cgx
+    for world, n in ((1, 8), (2, 98304), (8, 1000)):
+        slot = (n + 127) // 128 * 128
+        assert cgx.peer_buffer_bytes(world, n) == 2 * world * slot * 2 + 4 * 64 * 8 * 256
+    for bad in (0, 9):
+        with pytest.raises(cgx.CgxError):
+            cgx.peer_buffer_bytes(bad, 1024)
