@@ -706,7 +706,8 @@ static int encode_kmajor(CUtensorMap* tm, const void* base, uint64_t rows, uint6
 // ingress (k-blocks per CTA x (16 KiB of A + BN x 128 B of W)) and the serial latency chain (first
 // TMA, MMA, epilogue) bound it; split-K cuts the ingress S-fold at the price of the push
 // reduction. Rule measured on the deployed C3 replay (scripts/diag_c3_tiling.py,
-// profiles/r01/c3_tiling.txt: 562 -> 514 us per 12-layer replay): BN = 32, and the largest
+// profiles/r01/c3_tiling.txt: 562 -> 514 us per 12-layer replay): BN = 32 (64 for M >= 1024 with
+// K >= 512, profiles/r01/gemm_large.txt), and the largest
 // S in {1, 2, 4, 8} with tiles x S <= 192 CTAs (up to two co-resident per SM) and >= 3 k-blocks
 // per split. CGX_GEMM_TILING / CGX_GEMM_BN / CGX_GEMM_SPLIT pin a tiling for measurement.
 static uint32_t split_rows_max_h(uint32_t S) { return (128u + S - 1) / S; }
@@ -746,7 +747,9 @@ static void pick_tiling(uint32_t M, uint32_t N, uint32_t K, int* bn_out, uint32_
   const char* env_bn = getenv("CGX_GEMM_BN");          // measurement knobs
   const char* env_sp = getenv("CGX_GEMM_SPLIT");
   const uint32_t nk = K / kBK;
-  int bn = 32;
+  // large, compute-bound shapes (many M tiles and a long K) take BN = 64: two CTAs per SM overlap one
+  // tile's epilogue with the other's mainloop (gemm_large.txt: 753 vs 422 TFLOP/s at BN = 32)
+  int bn = (M >= 1024 && K >= 512 && N % 64 == 0) ? 64 : 32;
   if (env_bn && (atoi(env_bn) == 32 || atoi(env_bn) == 64 || atoi(env_bn) == 128) && N % atoi(env_bn) == 0)
     bn = atoi(env_bn);
   const uint32_t tiles = (N / bn) * ((M + kBM - 1) / kBM);
