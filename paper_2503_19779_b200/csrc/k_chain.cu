@@ -688,12 +688,8 @@ const void* kfn_copy_bulk(int cap) {
   if (cap <= 8) f = (const void*)k_copy_bulk<8>;
   else if (cap <= 64) f = (const void*)k_copy_bulk<64>;
   else f = (const void*)k_copy_bulk<1024>;
-  static bool set[3] = {false, false, false};
-  const int i = cap <= 8 ? 0 : cap <= 64 ? 1 : 2;
-  if (!set[i]) {
-    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkStages * kBulkChunk);
-    set[i] = true;
-  }
+  // per call (build time, cheap): function attributes belong to the current device's context
+  cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkStages * kBulkChunk);
   return f;
 }
 size_t copy_bulk_smem() { return (size_t)kBulkStages * kBulkChunk; }

@@ -351,11 +351,8 @@ void decoder_attn_launch_dims(uint32_t T, uint32_t H, uint32_t D, dim3* grid, di
   const uint32_t warps = (T + kAttnKChunk - 1) / kAttnKChunk;   // one warp per 32-key chunk of the longest range
   *block = dim3(32 * (warps < 1 ? 1 : warps > (uint32_t)kAttnMaxWarps ? kAttnMaxWarps : warps));
   *smem = attn_smem_bytes(T);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_attention, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)attn_smem_bytes(kAttnMaxT));
-    attr_set = true;
-  }
+  // per call (build time, cheap): function attributes belong to the current device's context
+  cudaFuncSetAttribute(k_attention, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)attn_smem_bytes(kAttnMaxT));
 }
 
 }  // namespace cgx

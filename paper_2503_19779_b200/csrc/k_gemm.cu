@@ -772,12 +772,10 @@ void decoder_gemm_plan(uint32_t, uint32_t, uint32_t, size_t* ws_bytes, size_t* c
 
 template <int BN, bool AR>
 static const void* setup_kernel() {
-  static std::once_flag once;
-  std::call_once(once, [] {
-    // headroom below the 227 KiB per-block limit for the kernel's static shared memory
-    cudaFuncSetAttribute(k_gemm_bf16<BN, AR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    cudaFuncSetAttribute(k_gemm_bf16<BN, AR>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  });
+  // per call (exec build time, cheap): function attributes belong to the current device's context.
+  // Headroom below the 227 KiB per-block limit for the kernel's static shared memory.
+  cudaFuncSetAttribute(k_gemm_bf16<BN, AR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  cudaFuncSetAttribute(k_gemm_bf16<BN, AR>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   return (const void*)k_gemm_bf16<BN, AR>;
 }
 
