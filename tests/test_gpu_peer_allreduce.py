@@ -154,8 +154,13 @@ def test_tp_decoder_gemm_fused_allreduce(rt, monkeypatch, tp, mode, transport):
     bit-identical to the chain with separate peer ALLREDUCE_SUM nodes, identical across ranks,
     and within the decoder tolerance of the TP oracle. Small row-parallel tilings keep every
     virtual rank's all-reducing GEMM resident on the one shared GPU."""
-    k_o, k_f = 768 // tp, 3072 // tp
-    monkeypatch.setenv("CGX_GEMM_TILING", f"768x{k_o}=32/{1 if tp == 4 else 2},768x{k_f}=32/2")
+    # every GEMM of every virtual rank on an unsplit BN = 32 tiling (<= 48 CTAs each): the ranks share
+    # ONE GPU here, and an all-reducing GEMM spins until every rank's GEMM for the same tile has
+    # arrived, so all of them must be able to be resident at once (on an NVSwitch box each rank has
+    # its own GPU). Larger footprints can starve a rank and trip the bounded spin.
+    hl, fl = 12 // tp, 3072 // tp
+    shapes = {(3 * hl * 64, 768), (768, hl * 64), (fl, 768), (768, fl)}
+    monkeypatch.setenv("CGX_GEMM_TILING", ",".join(f"{n}x{k}=32/1" for n, k in shapes))
     full = wl.c3_chain(T=128, n_layers=2)
     specs_f = [wl.c3_chain(T=128, n_layers=2, tp=tp, rank=r, fuse_allreduce=True) for r in range(tp)]
     specs_u = [wl.c3_chain(T=128, n_layers=2, tp=tp, rank=r) for r in range(tp)]
