@@ -75,3 +75,17 @@ def test_peer_buffer_bytes_host_only():
     for bad in (0, 9):
         with pytest.raises(cgx.CgxError):
             cgx.peer_buffer_bytes(bad, 1024)
+
+
+def test_bench_reference_arm_contract_on_cpu():
+    """bench.py --impl reference (the oracle timed on host cores) prints the contract's JSON line."""
+    import json
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--steps", "2",
+                        "--warmup", "3"], capture_output=True, text=True, timeout=240, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    assert d["impl"] == "reference" and d["steps"] == 2 and d["warmup"] == 3 and d["value"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "oracle"
+    assert d["unit"] == "iters/s" and d["higher_is_better"] is True
