@@ -1233,14 +1233,68 @@ static int capture_dag(cgx_exec* e, int gi, cudaStream_t cs, cgx_transport t) {
                                      t == CGX_XPORT_ROOT_MAPPED || t == CGX_XPORT_PRELUDE);
   int pre = (indirect && t == CGX_XPORT_FIRST_NODE) ? e->t5_pub : -1;
   if (!has_root && pre < 0 && nl > 1) pre = 0;
-  // stream assignment (pure pass)
+  // issue order: a topological order of the post-prefix nodes. Default: chain order.
+  // CGX_DAG_ORDER=priority: longest remaining path first (list scheduling; weight per node = one
+  // launch + its slot bytes at HBM rate); CGX_DAG_ORDER=level: by dependency depth (all first
+  // nodes of every branch, then all second nodes, ...). Any topological order gives the same
+  // results (every RAW/WAR/WAW hazard is an edge); chain order replays fastest on C2 and the
+  // training chain (scripts/diag_dag_order.py, profiles/r01/dag_order.json).
+  std::vector<int> order;
+  order.reserve(nl);
+  {
+    const char* ov = getenv("CGX_DAG_ORDER");
+    const int how = !ov ? 0 : ov[0] == 'p' ? 1 : ov[0] == 'l' ? 2 : 0;
+    std::vector<double> prio(nl, 0.0);
+    std::vector<std::vector<int>> succ(nl);
+    std::vector<int> indeg(nl, 0);
+    for (int p = pre + 1; p < (int)nl; ++p)
+      for (int d : deps[p])
+        if (d > pre) {
+          succ[d].push_back(p);
+          ++indeg[p];
+        }
+    for (int p = (int)nl - 1; p > pre; --p) {
+      const Node& n = e->c->nodes[e->L[p].node];
+      double bytes = (double)e->c->slots[n.out].nbytes;
+      for (int j = 0; j < n.n_in; ++j) bytes += (double)e->c->slots[n.in[j]].nbytes;
+      double m = 0.0;
+      for (int q : succ[p]) m = std::max(m, prio[q]);
+      prio[p] = 1.0 + bytes / (2.0 * 1024 * 1024) + m;
+    }
+    std::vector<int> level(nl, 0);
+    for (int p = pre + 1; p < (int)nl; ++p)
+      for (int d : deps[p])
+        if (d > pre) level[p] = std::max(level[p], level[d] + 1);
+    std::vector<int> ready;
+    for (int p = pre + 1; p < (int)nl; ++p)
+      if (indeg[p] == 0) ready.push_back(p);
+    while (!ready.empty()) {
+      size_t bi = 0;
+      for (size_t i = 1; i < ready.size(); ++i) {
+        const int a = ready[i], b = ready[bi];
+        const bool better = how == 1 ? (prio[a] > prio[b] || (prio[a] == prio[b] && a < b))
+                          : how == 2 ? (level[a] < level[b] || (level[a] == level[b] && a < b))
+                                     : a < b;
+        if (better) bi = i;
+      }
+      const int p = ready[bi];
+      ready[bi] = ready.back();
+      ready.pop_back();
+      order.push_back(p);
+      for (int q : succ[p])
+        if (--indeg[q] == 0) ready.push_back(q);
+    }
+  }
+  std::vector<int> pos(nl, -1);
+  for (size_t i = 0; i < order.size(); ++i) pos[order[i]] = (int)i;
+  // stream assignment (pure pass, in issue order; tails hold issue positions' nodes)
   std::vector<int> stream_of(nl, -1), tail((size_t)S, -1);
-  for (int p = pre + 1; p < (int)nl; ++p) {
+  for (int p : order) {
     int best = -1, bestd = -1;
     for (int d : deps[p])
-      if (stream_of[d] >= 0 && tail[stream_of[d]] == d && d > bestd) {
+      if (stream_of[d] >= 0 && tail[stream_of[d]] == d && pos[d] > bestd) {
         best = stream_of[d];
-        bestd = d;
+        bestd = pos[d];
       }
     if (best < 0) {
       for (int k = 0; k < S && best < 0; ++k)
@@ -1248,7 +1302,7 @@ static int capture_dag(cgx_exec* e, int gi, cudaStream_t cs, cgx_transport t) {
       if (best < 0) {
         best = 0;
         for (int k = 1; k < S; ++k)
-          if (tail[k] < tail[best]) best = k;
+          if (pos[tail[k]] < pos[tail[best]]) best = k;
       }
     }
     stream_of[p] = best;
@@ -1284,7 +1338,7 @@ static int capture_dag(cgx_exec* e, int gi, cudaStream_t cs, cgx_transport t) {
   std::vector<char> need_ev(nl, 0), started((size_t)S, 0);
   for (size_t p = 0; p < nl; ++p)
     for (int d : deps[p]) need_ev[d] = 1;
-  for (int p = pre + 1; p < (int)nl; ++p) {
+  for (int p : order) {
     const int best = stream_of[p];
     cudaStream_t st = e->dag_s[best];
     for (int d : deps[p])

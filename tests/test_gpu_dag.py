@@ -156,3 +156,15 @@ def test_graph_sync_prelude_and_device_transports(rt, transport):
     for l in range(20):
         assert np.array_equal(ex.output(f"r{l}"), env[f"r{l}"]), l
     chain.close()
+
+
+@pytest.mark.parametrize("order", ["priority", "level"])
+def test_graph_sync_issue_orders(rt, order, monkeypatch):
+    """Any topological issue order (CGX_DAG_ORDER, read at capture) gives the oracle's results."""
+    monkeypatch.setenv("CGX_DAG_ORDER", order)
+    for spec in (wl.c2_chain(n_lanes=24), _hazard_chain(4096)):
+        a, st = _replays(rt, spec, "INDIRECT", "FIRST_NODE", 3, "GRAPH", int_mode=True)
+        for r in (0, 2):
+            env = eval_chain(spec, wl.external_values(spec, r, "int"), st)
+            for k in a[r]:
+                assert np.array_equal(a[r][k], env[k]), (order, r, k)
