@@ -1576,7 +1576,7 @@ extern "C" int cgx_exec_create_ex(cgx_chain* c, const cgx_exec_opts* opts, void*
       if ((st = capture_graph(e, gi)) != CGX_OK) {
         cudaStreamCaptureStatus cst;
         if (cudaStreamIsCapturing(e->cs, &cst) == cudaSuccess && cst != cudaStreamCaptureStatusNone) {
-          cudaGraph_t junk;
+          cudaGraph_t junk = nullptr;
           cudaStreamEndCapture(e->cs, &junk);
           if (junk) cudaGraphDestroy(junk);
         }
@@ -1885,8 +1885,15 @@ extern "C" int cgx_device_loop(cgx_exec* e, const void* d_ptr_sets, int n_sets, 
     r.pdl = false;
     r.args.reset(sizeof(DevLoopArgs));
     memcpy(r.args.p, &a, sizeof(a));
-    CKS(issue(e, r, e->cs));
-    CKS(last_captured_node(e->cs, &e->dl_node));
+    int st = issue(e, r, e->cs);
+    if (st == CGX_OK) st = last_captured_node(e->cs, &e->dl_node);
+    if (st != CGX_OK) {
+      // leave the exec's capture stream usable: close the capture, drop the partial graph
+      cudaGraph_t junk = nullptr;
+      cudaStreamEndCapture(e->cs, &junk);
+      if (junk) cudaGraphDestroy(junk);
+      return st;
+    }
     CK(cudaStreamEndCapture(e->cs, &e->dl_g));
     CK(cudaGraphInstantiateWithFlags(&e->dl_ge, e->dl_g, cudaGraphInstantiateFlagDeviceLaunch));
     CK(cudaGraphUpload(e->dl_ge, e->s));
@@ -2270,38 +2277,48 @@ double median(std::vector<double> v) {
 // event-record node between consecutive launches (no PDL overlap in this copy), median over reps.
 static int kernel_times(cgx_exec* e, int reps, std::vector<double>* out) {
   const int K = (int)e->L.size();
-  cudaStream_t cs;
-  CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-  std::vector<cudaEvent_t> ev(K + 1);
-  for (auto& v : ev) CK(cudaEventCreate(&v));
-  CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-  CK(cudaEventRecordWithFlags(ev[0], cs, cudaEventRecordExternal));
-  for (int k = 0; k < K; ++k) {
+  // every resource is released on every return path (errors included)
+  struct Res {
+    cudaStream_t cs = nullptr;
+    std::vector<cudaEvent_t> ev;
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t ge = nullptr;
+    ~Res() {
+      if (ge) cudaGraphExecDestroy(ge);
+      if (g) cudaGraphDestroy(g);
+      for (auto& v : ev) if (v) cudaEventDestroy(v);
+      if (cs) cudaStreamDestroy(cs);
+    }
+  } r;
+  CK(cudaStreamCreateWithFlags(&r.cs, cudaStreamNonBlocking));
+  r.ev.assign(K + 1, nullptr);
+  for (auto& v : r.ev) CK(cudaEventCreate(&v));
+  CK(cudaStreamBeginCapture(r.cs, cudaStreamCaptureModeThreadLocal));
+  int st = CGX_OK;
+  cudaError_t ce = cudaEventRecordWithFlags(r.ev[0], r.cs, cudaEventRecordExternal);
+  if (ce != cudaSuccess) st = cuda_fail(ce, "kernel_times: event record", __LINE__);
+  for (int k = 0; k < K && st == CGX_OK; ++k) {
     Launch& l = e->L[k];
     const bool pdl = l.pdl;
     l.pdl = false;
-    const int st = issue(e, l, cs);
+    st = issue(e, l, r.cs);
     l.pdl = pdl;
-    if (st != CGX_OK) {
-      cudaGraph_t junk;
-      cudaStreamEndCapture(cs, &junk);
-      if (junk) cudaGraphDestroy(junk);
-      return st;
-    }
-    CK(cudaEventRecordWithFlags(ev[k + 1], cs, cudaEventRecordExternal));
+    if (st != CGX_OK) break;
+    ce = cudaEventRecordWithFlags(r.ev[k + 1], r.cs, cudaEventRecordExternal);
+    if (ce != cudaSuccess) st = cuda_fail(ce, "kernel_times: event record", __LINE__);
   }
-  cudaGraph_t g;
-  cudaGraphExec_t ge;
-  CK(cudaStreamEndCapture(cs, &g));
-  CK(cudaGraphInstantiateWithFlags(&ge, g, 0));
+  ce = cudaStreamEndCapture(r.cs, &r.g);
+  CKS(st);
+  CK(ce);
+  CK(cudaGraphInstantiateWithFlags(&r.ge, r.g, 0));
   std::vector<std::vector<double>> dk(K);
-  for (int r = 0; r < reps + 2; ++r) {
-    CK(cudaGraphLaunch(ge, e->s));
+  for (int it = 0; it < reps + 2; ++it) {
+    CK(cudaGraphLaunch(r.ge, e->s));
     CK(cudaStreamSynchronize(e->s));
-    if (r < 2) continue;
+    if (it < 2) continue;
     for (int k = 0; k < K; ++k) {
       float ms = 0;
-      CK(cudaEventElapsedTime(&ms, ev[k], ev[k + 1]));
+      CK(cudaEventElapsedTime(&ms, r.ev[k], r.ev[k + 1]));
       dk[k].push_back(ms * 1e3);
     }
   }
@@ -2313,10 +2330,6 @@ static int kernel_times(cgx_exec* e, int reps, std::vector<double>* out) {
     for (double v : dk[k]) sacc += v;
     (*out)[k] = dk[k].empty() ? 0.0 : sacc / dk[k].size();
   }
-  cudaGraphExecDestroy(ge);
-  cudaGraphDestroy(g);
-  for (auto& v : ev) cudaEventDestroy(v);
-  cudaStreamDestroy(cs);
   return CGX_OK;
 }
 
