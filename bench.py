@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=200)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-extras", action="store_true", help="only the timed hot-path loop")
+    ap.add_argument("--graph-streams", type=int, default=0,
+                    help="DAG capture streams of the deployed exec (0: measured choice, cgx_tune_graph_streams)")
     ap.add_argument("--cpu-budget-s", type=float, default=15.0)
     return ap.parse_args()
 
@@ -303,7 +305,16 @@ def main():
         return e0.elapsed_time(e1) * 1e3 / n
 
     main_arm = ("INDIRECT", MAIN_TRANSPORT)
-    ex_main = chain.exec(main_arm[0], stream=stream, transport=main_arm[1], validate=0)
+    # slow path (like the selector's profiling): the DAG capture's stream count is
+    # measured on this workload's inputs and the fastest deployed (cgx_tune_graph_streams)
+    tune_us = None
+    if args.graph_streams:
+        best_streams = args.graph_streams
+    else:
+        best_streams, tune_us = cgx.tune_graph_streams(
+            chain.handle, main_arm[0], stream.cuda_stream, [[t.data_ptr() for t in ts] for ts in sets],
+            candidates=(8, 12, 14, 16, 20, 24, 32), reps=100, transport=main_arm[1])
+    ex_main = chain.exec(main_arm[0], stream=stream, transport=main_arm[1], validate=0, graph_streams=best_streams)
     h = ex_main.handle
     loop(h, max(3, args.warmup))
     stream.synchronize()
@@ -359,6 +370,9 @@ def main():
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": WORKLOAD, "arm": f"GRAPH_INDIRECT (pointer table, {MAIN_TRANSPORT} transport)",
                    "kernels_per_replay": stats_main["kernels_per_replay"],
+                   "graph_streams": best_streams,
+                   "graph_streams_tuning_us": ({str(k): round(v, 2) for k, v in tune_us.items()} if tune_us
+                                               else "fixed by --graph-streams"),
                    "l2": f"rotating {N_SETS} input sets ({N_SETS * 37743616 / 1e6:.0f} MB > 126 MB L2)",
                    "parallelism": f"independent replicas x{world}"},
         "gpu_launches": args.steps * stats_main["kernels_per_replay"],

@@ -306,6 +306,19 @@ int cgx_profile(cgx_chain* c, int segment, const void* const* ext_dptrs, int n_e
  * optional) receives the three estimates/totals used. */
 int cgx_select(const cgx_profile_t* prof, int n_segments, cgx_decision* out, double* est_out);
 
+/* Slow path (measure candidates with the real inputs, deploy one): choose the
+ * dependency-DAG capture's stream count. For each candidates[i] (1..64) an exec with *opts
+ * (mode must be a graph mode; sync_mode forced to CGX_SYNC_GRAPH, graph_streams = candidates[i])
+ * is created on cuda_stream, replayed reps times (bind + launch each, cycling over the n_sets
+ * input sets of ext_sets: n_sets x n_ext DEVICE pointers, row-major, same order as cgx_bind),
+ * timed with CUDA events (best of three trials) and destroyed. *best_out = the fastest count;
+ * us_out (n_cand doubles, optional) = µs per replay of each candidate. The chain must be ready
+ * for exec creation (statics set). Errors: CGX_E_INVALID_ARG on bad arguments or an EAGER mode;
+ * any exec-create / bind / launch / CUDA error is returned as is (the candidate exec is freed). */
+int cgx_tune_graph_streams(cgx_chain* c, const cgx_exec_opts* opts, void* cuda_stream,
+                           const void* const* ext_sets, int n_sets, int n_ext, const int* candidates,
+                           int n_cand, int reps, int* best_out, double* us_out);
+
 /* ---- measurement helpers ------------------------------------------------------------------ */
 /* Single-dispatch floor: median host µs of cudaGraphLaunch of a 1-node
  * empty-kernel graph and of cudaLaunchKernel of an empty kernel on cuda_stream. */

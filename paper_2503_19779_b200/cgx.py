@@ -124,6 +124,7 @@ def _load():
         "cgx_ipc_handle": ([VP, VP], I),
         "cgx_ipc_open": ([VP, P(VP)], I),
         "cgx_ipc_close": ([VP], I),
+        "cgx_tune_graph_streams": ([VP, P(ExecOpts), VP, VP, I, I, P(C.c_int), I, I, P(C.c_int), P(C.c_double)], I),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -141,7 +142,7 @@ EXPORTED = ("cgx_version", "cgx_last_error", "cgx_chain_create", "cgx_chain_add_
             "cgx_dispatch_floor", "cgx_fill_uniform_f32", "cgx_copy", "cgx_graph_floor", "cgx_kernel_times", "cgx_find_param_offset",
             "cgx_debug_param_image", "cgx_debug_ext_field_offsets", "cgx_debug_gemm_trace", "cgx_debug_node_trace", "cgx_device_loop", "cgx_nccl_unique_id",
             "cgx_nccl_comm_init", "cgx_nccl_comm_destroy", "cgx_peer_buffer_bytes", "cgx_chain_set_peers",
-            "cgx_ipc_handle", "cgx_ipc_open", "cgx_ipc_close")
+            "cgx_ipc_handle", "cgx_ipc_open", "cgx_ipc_close", "cgx_tune_graph_streams")
 
 
 def _ck(status: int, fn: str):
@@ -200,6 +201,23 @@ def exec_create(chain: int, mode: str, stream: int, transport: str = "DEFAULT", 
     out = C.c_void_p()
     _ck(LIB.cgx_exec_create_ex(chain, C.byref(o), stream, C.byref(out)), "cgx_exec_create_ex")
     return out.value
+
+
+def tune_graph_streams(chain: int, mode: str, stream: int, ext_sets, candidates=(8, 12, 14, 16, 20, 24, 32),
+                       reps: int = 100, transport: str = "DEFAULT", **kw) -> tuple:
+    """Slow-path stream-count choice for the DAG capture (cgx_tune_graph_streams): ext_sets is a
+    list of input sets (each a list of device pointers in cgx_bind order). Returns
+    (best_count, {count: us_per_replay})."""
+    n_sets, n_ext = len(ext_sets), len(ext_sets[0]) if ext_sets else 0
+    flat = ptr_array([p for row in ext_sets for p in row])
+    o = ExecOpts(MODE[mode], XPORT[transport], kw.get("first_node", 0), kw.get("n_nodes", 0),
+                 int(kw.get("no_pdl", False)), kw.get("validate", 0), kw.get("copy_impl", 0), SYNC["GRAPH"], 0)
+    cand = (C.c_int * len(candidates))(*candidates)
+    us = (C.c_double * len(candidates))()
+    best = C.c_int()
+    _ck(LIB.cgx_tune_graph_streams(chain, C.byref(o), stream, flat, n_sets, n_ext, cand, len(candidates), reps,
+                                   C.byref(best), us), "cgx_tune_graph_streams")
+    return best.value, {int(c_): us[i] for i, c_ in enumerate(candidates)}
 
 
 def ptr_array(ptrs):

@@ -2157,6 +2157,75 @@ extern "C" int cgx_profile(cgx_chain* c, int segment, const void* const* ext, in
   return cgx_profile_impl(c, segment, ext, n_ext, reps, stream, out);
 }
 
+// Slow-path choice of the DAG capture's stream count (candidates are measured with the
+// real inputs, then one is deployed). The replay rate of a dependency-DAG graph depends on how
+// its branches fall onto capture streams in a way no static rule captured (C2: 14 streams
+// 53.3 us, 16 -> 54.9, 12 -> 61.6, 20 -> 57.2; profiles/r01/dag_assign.txt), so each candidate
+// exec is built, replayed `reps` times over the given input sets (bind + launch per replay, CUDA
+// events on the stream), and the fastest count is returned. Nothing is kept.
+extern "C" int cgx_tune_graph_streams(cgx_chain* c, const cgx_exec_opts* opts, void* stream,
+                                      const void* const* ext_sets, int n_sets, int n_ext,
+                                      const int* candidates, int n_cand, int reps, int* best_out,
+                                      double* us_out) {
+  if (!c || !opts || !ext_sets || n_sets <= 0 || n_ext < 0 || !candidates || n_cand <= 0 || reps <= 0 ||
+      !best_out)
+    return fail(CGX_E_INVALID_ARG, "tune_graph_streams: bad argument");
+  if (opts->mode == CGX_MODE_EAGER) return fail(CGX_E_INVALID_ARG, "tune_graph_streams: graph modes only");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  struct Ev {
+    cudaEvent_t* a;
+    cudaEvent_t* b;
+    ~Ev() {
+      if (*a) cudaEventDestroy(*a);
+      if (*b) cudaEventDestroy(*b);
+    }
+  } ev_guard{&e0, &e1};
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  double best_us = 1e300;
+  int best = -1;
+  for (int ci = 0; ci < n_cand; ++ci) {
+    cgx_exec_opts o = *opts;
+    o.sync_mode = CGX_SYNC_GRAPH;
+    o.graph_streams = candidates[ci];
+    cgx_exec* e = nullptr;
+    CKS(cgx_exec_create_ex(c, &o, stream, &e));
+    int st = CGX_OK;
+    auto run = [&](int n) {
+      for (int i = 0; i < n && st == CGX_OK; ++i) {
+        st = cgx_bind(e, ext_sets + (size_t)(i % n_sets) * n_ext, n_ext);
+        if (st == CGX_OK) st = cgx_launch(e);
+      }
+    };
+    run(std::max(5, reps / 4));                       // warm-up (instantiation upload, L2)
+    float ms = 0.f, ms_min = 1e30f;
+    for (int t = 0; t < 3 && st == CGX_OK; ++t) {   // best of three trials
+      cudaError_t ce = cudaStreamSynchronize(s);
+      if (ce == cudaSuccess) ce = cudaEventRecord(e0, s);
+      if (ce != cudaSuccess) st = cuda_fail(ce, "tune_graph_streams", __LINE__);
+      run(reps);
+      if (st == CGX_OK) {
+        ce = cudaEventRecord(e1, s);
+        if (ce == cudaSuccess) ce = cudaEventSynchronize(e1);
+        if (ce == cudaSuccess) ce = cudaEventElapsedTime(&ms, e0, e1);
+        if (ce != cudaSuccess) st = cuda_fail(ce, "tune_graph_streams", __LINE__);
+        ms_min = std::min(ms_min, ms);
+      }
+    }
+    cgx_exec_destroy(e);
+    CKS(st);
+    const double us = (double)ms_min * 1e3 / reps;
+    if (us_out) us_out[ci] = us;
+    if (us < best_us) {
+      best_us = us;
+      best = candidates[ci];
+    }
+  }
+  *best_out = best;
+  return CGX_OK;
+}
+
 // ============================================================================ helpers
 extern "C" int cgx_dispatch_floor(void* stream, int reps, double* g_us, double* k_us) {
   if (reps <= 0 || !g_us || !k_us) return fail(CGX_E_INVALID_ARG, "dispatch_floor: bad argument");

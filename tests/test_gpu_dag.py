@@ -168,3 +168,29 @@ def test_graph_sync_issue_orders(rt, order, monkeypatch):
             env = eval_chain(spec, wl.external_values(spec, r, "int"), st)
             for k in a[r]:
                 assert np.array_equal(a[r][k], env[k]), (order, r, k)
+
+
+def test_tune_graph_streams(rt):
+    """cgx_tune_graph_streams (slow path): measures each candidate stream count on the given
+    inputs and returns the fastest; the exec deployed with it is bit-exact; EAGER is rejected."""
+    cgx, runner = rt
+    dev = torch.device("cuda:0")
+    spec = wl.c2_chain(n_lanes=24)
+    st = wl.static_values(spec, "int")
+    chain = runner.Chain(spec, runner.upload_statics(spec, st, dev))
+    sets = [runner.upload_externals(spec, wl.external_values(spec, r, "int"), dev) for r in range(2)]
+    ptrs = [[t[n].data_ptr() for n in chain.ext_names] for t in sets]
+    stream = torch.cuda.current_stream()
+    best, us = cgx.tune_graph_streams(chain.handle, "INDIRECT", stream.cuda_stream, ptrs, candidates=(2, 8, 16),
+                                      reps=20, transport="ROOT_PARAMS")
+    assert best in (2, 8, 16) and set(us) == {2, 8, 16}
+    assert all(v > 0 for v in us.values()) and us[best] == min(us.values())
+    with pytest.raises(cgx.CgxError):
+        cgx.tune_graph_streams(chain.handle, "EAGER", stream.cuda_stream, ptrs, candidates=(2,), reps=2)
+    ex = chain.exec("INDIRECT", transport="ROOT_PARAMS", graph_streams=best)
+    ex.bind(sets[1])
+    ex.launch()
+    env = eval_chain(spec, wl.external_values(spec, 1, "int"), st)
+    for l in range(24):
+        assert np.array_equal(ex.output(f"r{l}"), env[f"r{l}"]), l
+    chain.close()
