@@ -501,6 +501,7 @@ def run_extras(args, torch, cgx, runner, wl, sm, spec, chain, stream, sets, set_
                ex_main, dev):
     sh = stream.cuda_stream
     main_transport = MAIN_TRANSPORT
+    deployed_streams = ex_main.stats()["dag_streams"] or 16   # the main exec's DAG capture streams
     out = {}
     peaks = measured_peaks()
     hbm = peaks.get("hbm_gbs", 6650.0)
@@ -737,7 +738,7 @@ def run_extras(args, torch, cgx, runner, wl, sm, spec, chain, stream, sets, set_
         sub = _CS("dom", slots, nodes, [(0, len(nodes) - 1)])
         sch = runner.Chain(sub, {k_: v for k_, v in chain.statics.items() if k_ in used}, device=dev.index or 0)
         exs = sch.exec("INDIRECT", stream=stream, transport=MAIN_TRANSPORT if overlapped else "ROOT_PARAMS",
-                       no_pdl=not overlapped)
+                       no_pdl=not overlapped, graph_streams=deployed_streams if overlapped else 0)
         idx = [spec.externals().index(s_) for s_ in sub.externals()]
         arrs = [cgx.ptr_array([set_ptrs[r][i] for i in idx]) for r in range(N_SETS)]
         nx = len(idx)
@@ -794,7 +795,7 @@ def run_extras(args, torch, cgx, runner, wl, sm, spec, chain, stream, sets, set_
                        "algorithmic_bytes_per_launch": by_o, "avg_launch_us": us_o,
                        "timing": "CUDA events on the replay stream around 200 replays of a graph holding "
                                  "only this kernel's 64 launches, captured the way the replay deploys them "
-                                 "(dependency DAG over 16 streams, PDL, INDIRECT operands): span / launches. "
+                                 f"(dependency DAG over the deployed {deployed_streams} streams, PDL, INDIRECT operands): span / launches. "
                                  "Independent launches overlap, so this is the kernel's sustained per-launch "
                                  "time in the deployed regime (class throughput), not one launch's duration",
                        "serial_no_pdl": {"avg_launch_us": us_l, "achieved_GBps": achieved, "frac": achieved / hbm,
