@@ -899,9 +899,17 @@ def bench_training(torch, cgx, runner, wl, stream, dev):
     res = {"workload": "6 GPT-2 MLP blocks (d 768, d_ff 3072, T 128, bf16): forward, MSE gradient, backward "
                        "(TRANSPOSE + tcgen05 GEMMs + GELU_BWD), in-place SGD; fresh X / target per step",
            "kernels_per_step": l1 - f1 + 1, "us_per_step": {}, "rebind_delta_us": {}}
+    # slow path: the DAG capture's stream count measured on this chain (as for C2)
+    best_s, tune = cgx.tune_graph_streams(chain.handle, "INDIRECT", stream.cuda_stream,
+                                          [[t[n].data_ptr() for n in chain.ext_names] for t in sets],
+                                          candidates=(8, 12, 16, 20, 24, 32), reps=30, transport="ROOT_PARAMS",
+                                          first_node=f1, n_nodes=l1 - f1 + 1)
+    res["graph_streams"] = best_s
+    res["graph_streams_tuning_us"] = {str(k): round(v, 1) for k, v in tune.items()}
     for name, mode, xp in (("indirect_root_params", "INDIRECT", "ROOT_PARAMS"), ("copy", "COPY", "DEFAULT"),
                            ("setparams", "SETPARAMS", "DEFAULT"), ("eager", "EAGER", "DEFAULT")):
-        ex = chain.exec(mode, stream=stream, transport=xp, first_node=f1, n_nodes=l1 - f1 + 1)
+        ex = chain.exec(mode, stream=stream, transport=xp, first_node=f1, n_nodes=l1 - f1 + 1,
+                        graph_streams=best_s if mode != "EAGER" else 0)
         for i in range(5):
             LIB.cgx_bind(ex.handle, ptrs[i % 4], 2)
             LIB.cgx_launch(ex.handle)
