@@ -89,3 +89,25 @@ def test_bench_reference_arm_contract_on_cpu():
     assert d["impl"] == "reference" and d["steps"] == 2 and d["warmup"] == 3 and d["value"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["kind"] == "oracle"
     assert d["unit"] == "iters/s" and d["higher_is_better"] is True
+
+
+def test_tune_graph_streams_argument_checks_on_cpu(lib):
+    """cgx_tune_graph_streams rejects bad arguments before touching the device (include/cgx.h)."""
+    import ctypes as C
+    c = lib
+    opts = c.ExecOpts(c.MODE["INDIRECT"], c.XPORT["ROOT_PARAMS"], 0, 0, 0, 0, 0, c.SYNC["GRAPH"], 0)
+    cand = (C.c_int * 1)(16)
+    best = C.c_int()
+    sets = c.ptr_array([0])
+    # NULL chain, no candidates, zero reps: all CGX_E_INVALID_ARG with a message
+    assert c.LIB.cgx_tune_graph_streams(None, C.byref(opts), None, sets, 1, 1, cand, 1, 10, C.byref(best),
+                                        None) == c.E_INVALID_ARG
+    assert "tune_graph_streams" in c.last_error()
+    fake_chain = C.c_void_p(0x1000)   # never dereferenced: the checks below fail first
+    assert c.LIB.cgx_tune_graph_streams(fake_chain, C.byref(opts), None, sets, 1, 1, cand, 0, 10, C.byref(best),
+                                        None) == c.E_INVALID_ARG
+    assert c.LIB.cgx_tune_graph_streams(fake_chain, C.byref(opts), None, sets, 1, 1, cand, 1, 0, C.byref(best),
+                                        None) == c.E_INVALID_ARG
+    eager = c.ExecOpts(c.MODE["EAGER"], 0, 0, 0, 0, 0, 0, 0, 0)
+    assert c.LIB.cgx_tune_graph_streams(fake_chain, C.byref(eager), None, sets, 1, 1, cand, 1, 10, C.byref(best),
+                                        None) == c.E_INVALID_ARG
