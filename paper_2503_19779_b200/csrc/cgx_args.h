@@ -185,5 +185,6 @@ const void* kfn_empty();
 const void* kfn_pdl_nop();
 const void* kfn_fill_uniform_f32();
 int elem_block_threads();
+int elem_tile_vecs();      // 16-B vectors per thread per operand in one elementwise tile
 }  // namespace cgx
 }

@@ -18,7 +18,10 @@
 namespace cgx {
 
 static constexpr int kElemThreads = 256;
-static constexpr int kElemVec = 4;     // 16-B vectors per thread per operand (loads in flight)
+#ifndef CGX_ELEM_VEC
+#define CGX_ELEM_VEC 4
+#endif
+static constexpr int kElemVec = CGX_ELEM_VEC;   // 16-B vectors per thread per operand (loads in flight)
 
 enum { OP_ADD = 0, OP_MUL = 1, OP_SCALE = 2, OP_COPY = 3, OP_SCALE_T = 4,
        // training-shaped chain (bf16): a - b, a + s*b, GELU(a), dy * GELU'(x)
@@ -707,5 +710,6 @@ const void* kfn_fill_uniform_f32() { return (const void*)k_fill_uniform_f32; }
 const void* kfn_gather() { return (const void*)k_gather; }
 const void* kfn_allreduce_peer() { return (const void*)k_allreduce_peer; }
 int elem_block_threads() { return kElemThreads; }
+int elem_tile_vecs() { return kElemVec; }
 
 }  // namespace cgx

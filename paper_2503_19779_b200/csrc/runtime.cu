@@ -657,7 +657,7 @@ static int build_launch(cgx_exec* e, int k, Launch& l) {
         l.block = dim3(elem_block_threads());
         const uint64_t per_vec = dt == 0 ? 4 : 8;
         const uint64_t nv = n.attr.n / per_vec;
-        const uint64_t tiles = ceil_div(nv, (uint64_t)elem_block_threads() * 4);
+        const uint64_t tiles = ceil_div(nv, (uint64_t)elem_block_threads() * elem_tile_vecs());
         l.grid = dim3((unsigned)std::max<uint64_t>(1, dt == 0 ? std::min<uint64_t>(tiles, chain_grid_cap()) : tiles));
       }
       return CGX_OK;
