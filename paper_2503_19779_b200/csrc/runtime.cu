@@ -417,6 +417,7 @@ struct Launch {
   cudaGraphNode_t gnode[2] = {nullptr, nullptr};
   unsigned cluster_z = 1;                 // thread-block cluster (1, 1, z) (split-K GEMM)
   bool dev_updatable = false;             // T7: consumer patched by the prelude node
+  int prio = 0;                           // launch priority (0 = default; CGX_DAG_PRIO experiment)
   cudaGraphDeviceNode_t dev_node = nullptr;
   // NCCL
   const void* nc_in = nullptr;
@@ -987,8 +988,13 @@ static int issue(cgx_exec* e, Launch& l, cudaStream_t s) {
   cfg.blockDim = l.block;
   cfg.dynamicSmemBytes = l.smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[3];
+  cudaLaunchAttribute attr[4];
   unsigned na = 0;
+  if (l.prio) {
+    attr[na].id = cudaLaunchAttributePriority;
+    attr[na].val.priority = l.prio;
+    ++na;
+  }
   if (l.cluster_z > 1) {
     attr[na].id = cudaLaunchAttributeClusterDimension;
     attr[na].val.clusterDim.x = 1;
@@ -1291,6 +1297,15 @@ static int capture_dag(cgx_exec* e, int gi, cudaStream_t cs, cgx_transport t) {
   }
   std::vector<int> pos(nl, -1);
   for (size_t i = 0; i < order.size(); ++i) pos[order[i]] = (int)i;
+  // CGX_DAG_PRIO=<MiB> (experiment): nodes moving at least that many slot bytes get the device's
+  // greatest launch priority (the graph is instantiated with cudaGraphInstantiateFlagUseNodePriority)
+  if (const char* pv = getenv("CGX_DAG_PRIO")) {
+    int least = 0, greatest = 0;
+    cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    const double thr = atof(pv) * 1024.0 * 1024.0;
+    for (int p = pre + 1; p < (int)nl; ++p)
+      e->L[p].prio = (node_cost[p] - 1.0) * 2.0 * 1024 * 1024 >= thr ? greatest : 0;
+  }
   // stream assignment (pure pass, in issue order; tails hold issue positions' nodes). A node
   // continues the stream whose tail is its latest dependency; a node that starts a new branch goes
   // to an empty stream, else the one with the oldest tail. CGX_DAG_ASSIGN=load: the least-loaded
@@ -1455,7 +1470,8 @@ static int capture_graph(cgx_exec* e, int gi) {
   }
   CK(cudaStreamEndCapture(cs, &e->g[gi]));
   const bool devl = e->o.mode == CGX_MODE_GRAPH_INDIRECT && t == CGX_XPORT_DEVICE;
-  CK(cudaGraphInstantiateWithFlags(&e->ge[gi], e->g[gi], devl ? cudaGraphInstantiateFlagDeviceLaunch : 0));
+  const unsigned long long prio_flag = getenv("CGX_DAG_PRIO") ? cudaGraphInstantiateFlagUseNodePriority : 0ull;
+  CK(cudaGraphInstantiateWithFlags(&e->ge[gi], e->g[gi], (devl ? cudaGraphInstantiateFlagDeviceLaunch : 0ull) | prio_flag));
   CK(cudaGraphUpload(e->ge[gi], e->s));
   size_t nn = 0;
   CK(cudaGraphGetNodes(e->g[gi], nullptr, &nn));
