@@ -226,11 +226,30 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------------------------- launcher
+def self_launch(args) -> int | None:
+    """`python bench.py --gpus N` outside torchrun (WORLD_SIZE unset, N > 1): start N ranks of this
+    script with torch.distributed.run on 127.0.0.1 (one process per GPU) and return their exit
+    code; rank 0 prints the JSON line. Under torchrun (WORLD_SIZE set) nothing happens."""
+    if args.gpus <= 1 or os.environ.get("WORLD_SIZE") is not None:
+        return None
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
+
+
 # ------------------------------------------------------------------------------- ours
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    rc = self_launch(args)
+    if rc is not None:
+        sys.exit(rc)
 
     import torch
     import torch.distributed as dist
@@ -352,6 +371,11 @@ def main():
         if world > 1:
             dist.barrier()
         e2e = run_e2e_all(torch, cgx, wl, spec, chain, stream, dev, world)
+    # C5 (BASELINE configs[4]): the TP = N decoder step with captured all-reduces, every rank
+    c5 = None
+    if world > 1 and not args.no_extras:
+        dist.barrier()
+        c5 = bench_tp_leg(torch, dist, cgx, runner, wl, dev, local, rank, world, pg_gloo)
     extras = {}
     if rank == 0 and not args.no_extras:
         extras = run_extras(args, torch, cgx, runner, wl, sm, spec, chain, stream, sets, set_ptrs,
@@ -382,10 +406,84 @@ def main():
     line.update(extras)
     if e2e is not None:
         line["e2e"] = e2e
+    if c5 is not None:
+        line["c5_tp"] = c5
     print(json.dumps(line), flush=True)
     chain.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def bench_tp_leg(torch, dist, cgx, runner, wl, dev, local, rank, world, pg_gloo):
+    """C5: the GPT-2-small decoder (12 layers, T = 128) Megatron-sharded
+    TP = world ways, one process per GPU, replayed as each rank's captured graph with a fresh
+    (replicated) x bound every step. Variants: ALLREDUCE_SUM as a captured ncclAllReduce (NVLink /
+    NVSwitch), and the row-parallel GEMMs with the peer all-reduce fused into their epilogue over
+    CUDA-IPC-mapped regions. µs per replay = device time on each rank's stream, MAX over ranks;
+    tokens/s = T / that. Never fatal: a failing variant is reported as its error string."""
+    from paper_2503_19779_b200 import tp
+    T, L = 128, 12
+    out = {"tp": world, "workload": f"C5: GPT-2-small decoder, {L} layers, T={T}, bf16, TP={world} "
+                                     "(column-parallel QKV/FC1, row-parallel O/FC2, 2 all-reduces per layer)"}
+    full = wl.c3_chain(T=T, n_layers=L)
+    stream = torch.cuda.Stream(device=dev)
+
+    def max_over_ranks(v):
+        t = torch.tensor([v], dtype=torch.float64, device="cpu" if pg_gloo else dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for name, kind in (("nccl", "nccl"), ("peer_fused", "fused")):
+        comm = regions = chain = None
+        res = {}
+        try:
+            spec = wl.c3_chain(T=T, n_layers=L, tp=world, rank=rank, fuse_allreduce=kind == "fused")
+            st = wl.static_values(wl.c3_chain(T=T, n_layers=L, tp=world, rank=rank), tp=world, rank=rank, full=full)
+            if kind == "nccl":
+                if pg_gloo:
+                    raise RuntimeError("NCCL ranks need one GPU each (CGX_BENCH_PG=gloo run)")
+                comm = tp.nccl_bootstrap(local)
+            else:
+                regions = tp.PeerRegions(world, rank, T * 768, dev, max_allreduces=2 * L)
+            chain = runner.Chain(spec, runner.upload_statics(spec, st, dev), device=local, nccl_comm=comm,
+                                 peers=regions.peers() if regions else None)
+            xs = [runner.host_to_device(wl.slot_values(spec, "x", r), "bf16", dev) for r in range(4)]
+            ptrs = [cgx.ptr_array([x.data_ptr()]) for x in xs]
+            ex = chain.exec("INDIRECT", stream=stream, transport="FIRST_NODE")
+            n = 200
+            for i in range(10):
+                cgx.bind(ex.handle, [xs[i % 4].data_ptr()])
+                cgx.launch(ex.handle)
+            stream.synchronize()
+            best = 1e30
+            for _ in range(3):
+                dist.barrier()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for i in range(n):
+                    if cgx.LIB.cgx_bind(ex.handle, ptrs[i % 4], 1) or cgx.LIB.cgx_launch(ex.handle):
+                        raise cgx.CgxError(1, "bind/launch", cgx.last_error())
+                e1.record(stream)
+                e1.synchronize()
+                best = min(best, max_over_ranks(e0.elapsed_time(e1) * 1e3 / n))
+            res = {"us_per_replay_max_over_ranks": best, "tokens_per_s": T * 1e6 / best,
+                   "kernels_per_replay": ex.stats()["kernels_per_replay"]}
+            ex.close()
+        except Exception as exn:  # noqa: BLE001
+            res = {"error": f"{type(exn).__name__}: {exn}"[:400]}
+        finally:
+            if chain is not None:
+                chain.close()
+            try:
+                dist.barrier()
+            except Exception:  # noqa: BLE001
+                pass
+            if comm is not None:
+                cgx.nccl_comm_destroy(comm)
+            if regions is not None:
+                regions.close()
+        out[name] = res
+    return out
 
 
 def run_e2e_all(torch, cgx, wl, spec, chain, stream, dev, world):

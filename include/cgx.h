@@ -10,7 +10,9 @@
  * (P:Lnnn = line of the paper's LaTeX source, PAPER.md; S:Lnnn = SPEC.md.)
  *
  * Conventions
- *  - Every function returns an int status (cgx_status) and never aborts. On a non-OK status
+ *  - Every function returns an int status (cgx_status) and never aborts; kernels never trap (a
+ *    device-side wait that times out, bound 10 s or env CGX_SPIN_TIMEOUT_MS, is reported through
+ *    CGX_E_DEVICE at the exec's next cgx_launch). On a non-OK status
  *    cgx_last_error() returns a thread-local human-readable message (CUDA/NCCL errors carry the
  *    library's own message). Out-parameters are written only on CGX_OK.
  *  - All pointers to tensor data are DEVICE pointers of the chain's device (plain addresses, no
@@ -57,7 +59,11 @@ typedef enum {
   CGX_E_OFFSET_NOT_FOUND = 8, /* param-offset discovery: no match (NEXT-2) */
   CGX_E_OFFSET_AMBIGUOUS = 9, /* param-offset discovery: >= 2 matches (NEXT-2) */
   CGX_E_CUDA = 10,            /* CUDA runtime error; message in cgx_last_error() */
-  CGX_E_NCCL = 11             /* NCCL error; message in cgx_last_error() */
+  CGX_E_NCCL = 11,            /* NCCL error; message in cgx_last_error() */
+  CGX_E_DEVICE = 12           /* a kernel of an earlier replay of this exec reported a device-side
+                                 failure instead of trapping (a peer all-reduce or dataflow spin
+                                 timed out, a device-side graph launch failed; cgx_stats
+                                 device_error has the bits). Sticky for the exec. */
 } cgx_status;
 
 typedef enum { CGX_F32 = 0, CGX_BF16 = 1 } cgx_dtype;
@@ -166,8 +172,9 @@ typedef struct {
   int copy_impl;            /* GRAPH_COPY: 0 = multi-tensor LDG/STG kernel, 1 = cudaMemcpyAsync per
                                tensor, 2 = multi-tensor TMA bulk-copy kernel */
   int sync_mode;            /* graph modes with PDL, how the captured nodes are ordered:
-                               CGX_SYNC_AUTO (0) = GRAPH, except DATAFLOW for the PRELUDE and
-                               DEVICE transports; CGX_SYNC_DEFER (1) = one serial stream, deferred
+                               CGX_SYNC_AUTO (0) = GRAPH for every graph mode with PDL (all
+                               transports, PRELUDE and DEVICE included); EAGER and no_pdl execs
+                               keep their serial stream order; CGX_SYNC_DEFER (1) = one serial stream, deferred
                                griddepcontrol.wait for nodes with no in-graph producer;
                                CGX_SYNC_CHAIN (2) = one serial stream, griddepcontrol.wait in every
                                node; CGX_SYNC_GRAPH (3) = the graph is captured as the chain's
@@ -197,6 +204,8 @@ typedef struct {
   uint32_t n_deferred;           /* nodes running with the deferred PDL wait */
   uint32_t dataflow;             /* 1: nodes synchronise through dataflow counters */
   uint32_t dag_streams;          /* CGX_SYNC_GRAPH: capture streams holding at least one node */
+  uint32_t device_error;         /* device-side failure bits seen so far (0 = none; CGX_E_DEVICE):
+                                    1 dataflow timeout, 2 lost peer, 4 device launch failed */
 } cgx_stats_t;
 
 /* One segment's slow-path measurements, all microseconds. */
@@ -344,12 +353,22 @@ int cgx_fill_uniform_f32(void* dptr, uint64_t n, uint64_t seed, uint64_t stream_
  * processes, or the plain pointer when ranks share a device). An ALLREDUCE_SUM node then runs a
  * one-shot kernel: each rank pushes its partial into slot `rank` of every region (P2P stores over
  * NVLink), publishes a per-CTA generation flag with sys-scope release, waits for every source, and
- * sums the slots in fixed rank order (bit-identical results on all ranks). Requirements: n % 8 == 0,
- * n <= max_elems, world <= 8, <= 64 ALLREDUCE_SUM nodes, every rank creates its execs and replays in
- * the same order, and each ALLREDUCE_SUM depends (through the data flow) on the previous one.
- * Call before the chain's first exec. Errors: CGX_E_INVALID_ARG, CGX_E_MISALIGNED, CGX_E_STATE. */
-int cgx_peer_buffer_bytes(int world, uint64_t max_elems, uint64_t* bytes);
-int cgx_chain_set_peers(cgx_chain* c, int rank, int world, void* const* bases, uint64_t max_elems);
+ * sums the slots in fixed rank order (bit-identical results on all ranks). Region layout: receive
+ * data [max_allreduces][2 parity][world][slot] bf16, then flags [max_allreduces][8][256] uint32 —
+ * every all-reduce node (ALLREDUCE_SUM or a GEMM with CGX_GEMM_ALLREDUCE) owns two parity buffers,
+ * so any exec may hold any subset of the chain's all-reduces. Requirements: n % 8 == 0,
+ * n <= max_elems, world <= 8, the chain's all-reduces <= max_allreduces (1..64), and every rank
+ * launches the same all-reduces in the same order (captured graphs order each all-reduce after the
+ * previous one). Call before the chain's first exec. Errors: CGX_E_INVALID_ARG,
+ * CGX_E_MISALIGNED, CGX_E_STATE; exec creation returns CGX_E_UNSUPPORTED past max_allreduces. */
+int cgx_peer_buffer_bytes(int world, uint64_t max_elems, int max_allreduces, uint64_t* bytes);
+int cgx_chain_set_peers(cgx_chain* c, int rank, int world, void* const* bases, uint64_t max_elems,
+                        int max_allreduces);
+/* A dedicated zero-filled device allocation (cudaMalloc + memset, synchronised) and its release:
+ * use it for peer regions, so the CUDA IPC handle (which maps the whole allocation) maps exactly
+ * the region at offset 0 in the peer process. */
+int cgx_device_alloc(int device, uint64_t bytes, void** dptr_out);
+int cgx_device_free(void* dptr);
 /* CUDA IPC helpers for the multi-process case: a device allocation's 64-byte handle, and mapping /
  * unmapping a peer's allocation in this process. */
 int cgx_ipc_handle(void* dptr, void* handle_out /* 64 bytes */);

@@ -17,9 +17,9 @@ OK = 0
 STATUS = {0: "CGX_OK", 1: "CGX_E_INVALID_ARG", 2: "CGX_E_STATE", 3: "CGX_E_NOT_ELIGIBLE",
           4: "CGX_E_MISSING_INPUT", 5: "CGX_E_SIZE_MISMATCH", 6: "CGX_E_MISALIGNED",
           7: "CGX_E_UNSUPPORTED", 8: "CGX_E_OFFSET_NOT_FOUND", 9: "CGX_E_OFFSET_AMBIGUOUS",
-          10: "CGX_E_CUDA", 11: "CGX_E_NCCL"}
+          10: "CGX_E_CUDA", 11: "CGX_E_NCCL", 12: "CGX_E_DEVICE"}
 E_INVALID_ARG, E_STATE, E_NOT_ELIGIBLE, E_MISSING_INPUT, E_SIZE_MISMATCH, E_MISALIGNED, \
-    E_UNSUPPORTED, E_OFFSET_NOT_FOUND, E_OFFSET_AMBIGUOUS, E_CUDA, E_NCCL = range(1, 12)
+    E_UNSUPPORTED, E_OFFSET_NOT_FOUND, E_OFFSET_AMBIGUOUS, E_CUDA, E_NCCL, E_DEVICE = range(1, 13)
 F32, BF16 = 0, 1
 SLOT_EXTERNAL, SLOT_STATIC, SLOT_INTERNAL = 0, 1, 2
 OP = {"ADD": 0, "MUL": 1, "SCALE_IMM": 2, "COPY": 3, "REDUCE_SUM": 4, "LAYERNORM": 5,
@@ -54,7 +54,8 @@ class Stats(C.Structure):
                 ("n_setparam_calls", C.c_uint32), ("n_copy_tensors", C.c_uint32),
                 ("n_nodes", C.c_uint32), ("n_graph_nodes", C.c_uint32), ("n_ext", C.c_uint32),
                 ("kernels_per_replay", C.c_uint32), ("mode", C.c_uint32), ("transport", C.c_uint32),
-                ("n_deferred", C.c_uint32), ("dataflow", C.c_uint32), ("dag_streams", C.c_uint32)]
+                ("n_deferred", C.c_uint32), ("dataflow", C.c_uint32), ("dag_streams", C.c_uint32),
+                ("device_error", C.c_uint32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -119,8 +120,9 @@ def _load():
         "cgx_nccl_unique_id": ([VP], I),
         "cgx_nccl_comm_init": ([I, I, VP, I, P(VP)], I),
         "cgx_nccl_comm_destroy": ([VP], I),
-        "cgx_peer_buffer_bytes": ([I, U64, P(U64)], I),
-        "cgx_chain_set_peers": ([VP, I, I, P(VP), U64], I),
+        "cgx_peer_buffer_bytes": ([I, U64, I, P(U64)], I),
+        "cgx_chain_set_peers": ([VP, I, I, P(VP), U64, I], I),
+        "cgx_device_alloc": ([I, U64, P(VP)], I), "cgx_device_free": ([VP], I),
         "cgx_ipc_handle": ([VP, VP], I),
         "cgx_ipc_open": ([VP, P(VP)], I),
         "cgx_ipc_close": ([VP], I),
@@ -142,6 +144,7 @@ EXPORTED = ("cgx_version", "cgx_last_error", "cgx_chain_create", "cgx_chain_add_
             "cgx_dispatch_floor", "cgx_fill_uniform_f32", "cgx_copy", "cgx_graph_floor", "cgx_kernel_times", "cgx_find_param_offset",
             "cgx_debug_param_image", "cgx_debug_ext_field_offsets", "cgx_debug_gemm_trace", "cgx_debug_node_trace", "cgx_device_loop", "cgx_nccl_unique_id",
             "cgx_nccl_comm_init", "cgx_nccl_comm_destroy", "cgx_peer_buffer_bytes", "cgx_chain_set_peers",
+            "cgx_device_alloc", "cgx_device_free",
             "cgx_ipc_handle", "cgx_ipc_open", "cgx_ipc_close", "cgx_tune_graph_streams")
 
 
@@ -375,15 +378,26 @@ def nccl_comm_destroy(comm: int):
     _ck(LIB.cgx_nccl_comm_destroy(comm), "cgx_nccl_comm_destroy")
 
 
-def peer_buffer_bytes(world: int, max_elems: int) -> int:
+def peer_buffer_bytes(world: int, max_elems: int, max_allreduces: int = 64) -> int:
     b = C.c_uint64()
-    _ck(LIB.cgx_peer_buffer_bytes(world, max_elems, C.byref(b)), "cgx_peer_buffer_bytes")
+    _ck(LIB.cgx_peer_buffer_bytes(world, max_elems, max_allreduces, C.byref(b)), "cgx_peer_buffer_bytes")
     return b.value
 
 
-def chain_set_peers(chain: int, rank: int, world: int, bases, max_elems: int) -> None:
+def chain_set_peers(chain: int, rank: int, world: int, bases, max_elems: int, max_allreduces: int = 64) -> None:
     arr = (C.c_void_p * world)(*bases)
-    _ck(LIB.cgx_chain_set_peers(chain, rank, world, arr, max_elems), "cgx_chain_set_peers")
+    _ck(LIB.cgx_chain_set_peers(chain, rank, world, arr, max_elems, max_allreduces), "cgx_chain_set_peers")
+
+
+def device_alloc(device: int, nbytes: int) -> int:
+    """Dedicated zero-filled cudaMalloc allocation (peer regions: IPC maps it at offset 0)."""
+    p = C.c_void_p()
+    _ck(LIB.cgx_device_alloc(device, nbytes, C.byref(p)), "cgx_device_alloc")
+    return p.value
+
+
+def device_free(dptr: int) -> None:
+    _ck(LIB.cgx_device_free(C.c_void_p(dptr)), "cgx_device_free")
 
 
 def ipc_handle(dptr: int) -> bytes:

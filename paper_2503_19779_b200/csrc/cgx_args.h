@@ -9,6 +9,19 @@
 
 namespace cgx {
 
+// Device-side failure reporting (include/cgx.h CGX_E_DEVICE): kernels that spin on another agent
+// (dataflow counters, peer all-reduce flags) or launch work from the device never trap. On a
+// timeout (%globaltimer, timeout_ns) or a failed device launch they store a code into the exec's
+// status word (mapped pinned host memory, sys-scope release store), stop waiting and finish; the
+// host sees the word at the exec's next cgx_launch, which returns CGX_E_DEVICE from then on.
+struct DevStatus {
+  uint32_t* word;          // device alias of the exec's mapped host status word (nullptr = none)
+  uint64_t timeout_ns;     // spin bound
+};
+static constexpr uint32_t kDevErrDataflow = 1u;     // dataflow counter never reached its target
+static constexpr uint32_t kDevErrPeer = 2u;         // peer all-reduce: a source never published
+static constexpr uint32_t kDevErrDevLaunch = 4u;    // device-side cudaGraphLaunch failed
+
 // Operand fetch rule ("de-references these pointers-to-pointers before performing
 // any computation"): operand i reads `ptr[i]` when tidx[i] < 0, else `table[tidx[i]]`; the load
 // happens once at kernel start into a register (warp-uniform address, one request per warp).
@@ -33,6 +46,7 @@ struct ElemArgs {
   uint32_t df_dep[4];      // their counters
   uint32_t df_ctas[4];     // their CTA counts: dependency complete <=> done >= epoch * ctas
   unsigned long long* trace;  // diagnostics (CGX_NODE_TRACE=1): [entry min, ready max, exit max] ns
+  DevStatus st;            // dataflow spin bound / failure report
 };
 static constexpr int kDfMaxDeps = 4;
 // PDL protocol (see runtime.cu, set_pdl_flags): every chain kernel triggers its dependents at
@@ -160,6 +174,7 @@ struct PeerArArgs {
   uint32_t* counters;                  // chain-owned [kArMaxNodes][kArMaxCtas] generations
   __nv_bfloat16* recv[kArMaxWorld];    // every rank's receive data (mapped in this process)
   uint32_t* flags_of[kArMaxWorld];     // every rank's flag array
+  DevStatus st;                        // spin bound / lost-peer report
 };
 const void* kfn_allreduce_peer();
 static constexpr int kGatherMax = 64;

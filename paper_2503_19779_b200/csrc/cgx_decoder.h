@@ -5,7 +5,8 @@
 #include <stdint.h>
 
 namespace cgx {
-// LayerNorm: one warp per row, registers hold the row (cols <= 2048, cols % 8 == 0).
+// LayerNorm: one warp per row, registers hold the row (cols <= kLnMaxCols, cols % 8 == 0).
+static constexpr uint32_t kLnMaxCols = 2048;
 const void* kfn_layernorm(int tw = 0);
 void decoder_ln_launch_dims(uint32_t rows, uint32_t cols, dim3* grid, dim3* block);
 
@@ -35,6 +36,8 @@ uint32_t decoder_gemm_ctas(const void* args, dim3 grid);
 void decoder_gemm_set_residual_table(void* args, const uint64_t* table, int32_t idx);
 // Byte offsets of the residual pointer field and its int32 table-index field (patch modes).
 size_t decoder_gemm_residual_field(size_t* tidx_off);
+// Spin bound / failure word for the fused all-reduce epilogue (DevStatus, cgx_args.h).
+void decoder_gemm_set_status(void* args, uint32_t* word, uint64_t timeout_ns);
 // Diagnostics: per-CTA %globaltimer trace [cta][16] written by the kernel (nullptr = off).
 void decoder_gemm_set_trace(void* args, unsigned long long* trace);
 }  // namespace cgx

@@ -28,6 +28,17 @@ __device__ __forceinline__ void tw_publish(const ArgsTW<Base, CAP>& A) {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 
+__device__ __forceinline__ unsigned long long gtimer();
+// Bounded spin (DevStatus, cgx_args.h): call once per poll with the poll start time; every 1024
+// polls the elapsed %globaltimer is checked. On expiry the failure code is stored (sys-scope
+// release: the word is mapped host memory) and true is returned, so the caller stops waiting.
+__device__ __forceinline__ bool spin_expired(const DevStatus& s, unsigned long long t0, uint64_t& spins, uint32_t code) {
+  if ((++spins & 1023u) != 0) return false;
+  if (gtimer() - t0 < s.timeout_ns) return false;
+  if (s.word) asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(s.word), "r"(code) : "memory");
+  return true;
+}
+
 // Dataflow-mode synchronisation (kFlagDataflow, cgx_args.h).
 __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
   uint32_t v;
@@ -58,9 +69,11 @@ __device__ __forceinline__ void df_wait(const ElemArgs& a) {
       const uint32_t target = ep * a.df_ctas[i];
       const uint32_t* c = a.df_done + a.df_dep[i];
       uint64_t spins = 0;
-      // poll with relaxed loads (no L1 invalidation per poll), then one acquire fence below
+      const unsigned long long t0 = gtimer();
+      // poll with relaxed loads (no L1 invalidation per poll), then one acquire fence below; a
+      // lost signal is reported through the exec's status word instead of hanging or trapping
       while ((int32_t)(ld_relaxed_u32(c) - target) < 0) {
-        if (++spins > (1ull << 28)) __trap();    // a lost signal would hang the box: fail loudly
+        if (spin_expired(a.st, t0, spins, kDevErrDataflow)) break;
       }
     }
     asm volatile("fence.acq_rel.gpu;\n" ::: "memory");

@@ -28,6 +28,7 @@ struct DevLoopArgs {
   unsigned long long n_replays;
   cudaGraphExec_t chain;        // device-launchable chain graph
   uint32_t n_ext, n_sets;
+  uint32_t* status;             // exec status word (mapped host memory): kDevErrDevLaunch
 };
 const void* kfn_devloop();
 

@@ -546,14 +546,15 @@ __global__ void __launch_bounds__(256) k_gather(const __grid_constant__ GatherAr
 //  2. publish: bar.sync, then one thread: sys-scope fence and st.release.sys of the generation g
 //     into flag[ar][rank][c] of every rank;
 //  3. wait until flag[ar][s][c] == g in its own region for every source s (ld.acquire.sys polls,
-//     bounded: a lost peer traps instead of hanging), then fence + bar.sync;
+//     bounded: a lost peer is reported through the exec's status word, DevStatus, instead of
+//     hanging), then fence + bar.sync;
 //  4. sum the world slots in fixed rank order 0..world-1 in fp32 and round once: every rank
 //     computes bit-identical results.
-// g = ++counter[ar][c] (chain-owned, the same sequence on every rank); the receive buffer parity is
-// the global AR sequence number ((g-1)*n_ar + ar) & 1, so consecutive all-reduces alternate
-// buffers. Reuse of a parity buffer two all-reduces later is safe because every all-reduce of the
-// chain depends (through the data flow) on the previous one: a writer reaching AR s+2 has received
-// every peer's AR s+1 push, which each peer sends only after its AR s has completed.
+// g = ++counter[ar][c] (chain-owned, the same sequence on every rank). Every all-reduce node owns
+// two receive buffers (recv[] points at this node's [2][world][slot] block); generation g uses
+// parity (g - 1) & 1. A writer reaches generation g + 2 of this node only after it received every
+// peer's generation g + 1 flag, which each peer publishes only after it finished reading
+// generation g: reuse is safe whatever other all-reduces (or execs) run in between.
 // PDL: this kernel triggers its dependents only once every source has arrived (after step 3), so
 // no successor sits resident on the SMs while the all-reduce spins for its peers (a desynchronised
 // rank, or ranks sharing one GPU as in the tests, could otherwise starve the peers it waits for).
@@ -570,7 +571,7 @@ __global__ void __launch_bounds__(256) k_allreduce_peer(const __grid_constant__ 
   }
   __syncthreads();
   const uint32_t g = s_g;
-  const uint32_t par = (uint32_t)(((uint64_t)(g - 1) * a.n_ar + a.ar_index) & 1u);
+  const uint32_t par = (g - 1u) & 1u;
   const uint4* in = reinterpret_cast<const uint4*>(a.in);
   // 1. push
   for (uint64_t v = lo + threadIdx.x; v < hi; v += blockDim.x) {
@@ -590,11 +591,12 @@ __global__ void __launch_bounds__(256) k_allreduce_peer(const __grid_constant__ 
     for (uint32_t s2 = 0; s2 < a.world; ++s2) {
       const uint32_t* f = a.flags_of[a.rank] + ((uint64_t)a.ar_index * kArMaxWorld + s2) * kArMaxCtas + c;
       uint64_t spins = 0;
+      const unsigned long long t0 = gtimer();
       for (;;) {
         uint32_t v;
         asm volatile("ld.acquire.sys.global.u32 %0, [%1];\n" : "=r"(v) : "l"(f) : "memory");
         if (v == g) break;
-        if (++spins > (1ull << 28)) __trap();
+        if (spin_expired(a.st, t0, spins, kDevErrPeer)) break;   // lost peer: reported, no trap
       }
     }
     asm volatile("fence.acq_rel.sys;\n" ::: "memory");

@@ -26,6 +26,7 @@ __device__ __forceinline__ float warp_max(float v) {
 // ---------------------------------------------------------------------------- LayerNorm
 static constexpr int kLnWarps = 4;
 static constexpr int kLnMaxVec = 8;    // 8 x 16 B per lane -> cols <= 2048
+static_assert(kLnMaxVec * 8 * 32 == (int)kLnMaxCols, "k_layernorm row capacity");
 
 template <int TW>
 __global__ void __launch_bounds__(kLnWarps * 32) k_layernorm(const __grid_constant__ ArgsTW<LnArgs, TW> A) {

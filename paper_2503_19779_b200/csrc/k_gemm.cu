@@ -70,6 +70,7 @@ struct alignas(64) GemmArgs {
   uint32_t* ar_counters;
   __nv_bfloat16* ar_recv[kArMaxWorld];
   uint32_t* ar_flags[kArMaxWorld];
+  DevStatus st;               // spin bound / lost-peer report (CGX_GEMM_ALLREDUCE)
 };
 
 // ------------------------------------------------------------------ PTX wrappers
@@ -225,11 +226,12 @@ __device__ __forceinline__ void ar_publish_wait(const GemmArgs& a, uint32_t cta,
     for (uint32_t s2 = 0; s2 < a.ar_world; ++s2) {
       const uint32_t* f = a.ar_flags[a.ar_rank] + ((uint64_t)a.ar_index * kArMaxWorld + s2) * kArMaxCtas + cta;
       uint64_t spins = 0;
+      const unsigned long long t0 = gtimer();
       for (;;) {
         uint32_t v;
         asm volatile("ld.acquire.sys.global.u32 %0, [%1];\n" : "=r"(v) : "l"(f) : "memory");
         if (v == g) break;
-        if (++spins > (1ull << 28)) __trap();
+        if (spin_expired(a.st, t0, spins, kDevErrPeer)) break;   // lost peer: reported, no trap
       }
     }
     asm volatile("fence.acq_rel.sys;\n" ::: "memory");
@@ -444,7 +446,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
           if (!ar) {
             op[c8] = o;
           } else {                                 // this rank's bf16 tile row -> slot `rank` everywhere
-            const uint32_t par = (uint32_t)(((uint64_t)(s_ar_g - 1) * a.ar_nar + a.ar_index) & 1u);
+            const uint32_t par = (s_ar_g - 1u) & 1u;
             for (uint32_t p = 0; p < a.ar_world; ++p)
               reinterpret_cast<uint4*>(ar_slot_ptr(a, p, par, a.ar_rank) + (size_t)m * a.N + n0)[c8] = o;
           }
@@ -452,7 +454,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
       }
       if (ar) {
         const uint32_t g = s_ar_g;
-        const uint32_t par = (uint32_t)(((uint64_t)(g - 1) * a.ar_nar + a.ar_index) & 1u);
+        const uint32_t par = (g - 1u) & 1u;
         ar_publish_wait(a, cta_lin, g, et);
         if (m < (int)a.M) {                       // fixed rank order, fp32, one rounding
           uint4* op = reinterpret_cast<uint4*>(a.out + (size_t)m * a.N + n0);
@@ -533,14 +535,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
         if (!ar) {
           *reinterpret_cast<uint2*>(a.out + (size_t)mr * a.N + n0 + c) = ov;
         } else {                                   // this rank's bf16 quad -> slot `rank` everywhere
-          const uint32_t par = (uint32_t)(((uint64_t)(s_ar_g - 1) * a.ar_nar + a.ar_index) & 1u);
+          const uint32_t par = (s_ar_g - 1u) & 1u;
           for (uint32_t p = 0; p < a.ar_world; ++p)
             *reinterpret_cast<uint2*>(ar_slot_ptr(a, p, par, a.ar_rank) + (size_t)mr * a.N + n0 + c) = ov;
         }
       }
       if (ar) {
         const uint32_t g = s_ar_g;
-        const uint32_t par = (uint32_t)(((uint64_t)(g - 1) * a.ar_nar + a.ar_index) & 1u);
+        const uint32_t par = (g - 1u) & 1u;
         ar_publish_wait(a, cta_lin, g, et);
 #pragma unroll
         for (int j = 0; j < kQMax; ++j) {          // fixed rank order, fp32, one rounding
@@ -813,6 +815,10 @@ void decoder_gemm_set_residual_table(void* args, const uint64_t* table, int32_t 
 size_t decoder_gemm_residual_field(size_t* tidx_off) {
   *tidx_off = offsetof(GemmArgs, tres);
   return offsetof(GemmArgs, residual);
+}
+
+void decoder_gemm_set_status(void* args, uint32_t* word, uint64_t timeout_ns) {
+  static_cast<GemmArgs*>(args)->st = DevStatus{word, timeout_ns};
 }
 
 void decoder_gemm_set_trace(void* args, unsigned long long* trace) {

@@ -48,9 +48,13 @@ __global__ void k_devloop(const __grid_constant__ DevLoopArgs a) {
   if (threadIdx.x == 0) {
     *a.iter = i + 1;
     __threadfence();
-    if (cudaGraphLaunch(a.chain, cudaStreamGraphTailLaunch) != cudaSuccess) __trap();
-    if (i + 1 < a.n_replays && cudaGraphLaunch(cudaGetCurrentGraphExec(), cudaStreamGraphTailLaunch) != cudaSuccess)
-      __trap();
+    // a failed device launch ends the loop and is reported through the exec's status word (the
+    // host's next cgx_launch returns CGX_E_DEVICE) instead of trapping the context
+    bool ok = cudaGraphLaunch(a.chain, cudaStreamGraphTailLaunch) == cudaSuccess;
+    if (ok && i + 1 < a.n_replays)
+      ok = cudaGraphLaunch(cudaGetCurrentGraphExec(), cudaStreamGraphTailLaunch) == cudaSuccess;
+    if (!ok && a.status)
+      asm volatile("st.release.sys.global.u32 [%0], %1;\n" ::"l"(a.status), "r"(kDevErrDevLaunch) : "memory");
   }
 }
 

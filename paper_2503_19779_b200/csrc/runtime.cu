@@ -131,6 +131,7 @@ struct cgx_chain {
   // peer all-reduce (cgx_chain_set_peers): rank, world, every rank's region, generation counters
   int peer_rank = -1, peer_world = 0;
   uint64_t peer_max_elems = 0;
+  int peer_max_ar = 0;          // all-reduce nodes the regions have receive buffers for
   std::vector<void*> peer_base;
   uint32_t* peer_counters = nullptr;
   void* arena = nullptr;        // internal buffers
@@ -231,7 +232,9 @@ static int check_node(const cgx_chain* c, const Node& n) {
       for (int i = 0; i < 3; ++i)
         if (S(i).dtype != CGX_BF16) return fail(CGX_E_UNSUPPORTED, "layernorm: bf16 only");
       if (o.dtype != CGX_BF16) return fail(CGX_E_UNSUPPORTED, "layernorm: bf16 only");
-      CKS(need(a.rows > 0 && a.cols > 0 && a.cols % 8 == 0 && a.cols <= 8192, "layernorm: cols % 8, <= 8192"));
+      CKS(need(a.rows > 0 && a.cols > 0 && a.cols % 8 == 0, "layernorm: rows, cols > 0 and cols % 8 == 0"));
+      // k_layernorm keeps the row in registers: 8 x 16 B per lane x 32 lanes = 2048 bf16 columns
+      if (a.cols > kLnMaxCols) return fail(CGX_E_UNSUPPORTED, "layernorm: cols > 2048 (row held in one warp's registers)");
       CKS(need(S(0).nelems >= (uint64_t)a.rows * a.cols && o.nelems >= (uint64_t)a.rows * a.cols, "layernorm: shape"));
       return need(S(1).nelems >= a.cols && S(2).nelems >= a.cols, "layernorm: gamma/beta shape");
     case CGX_OP_GEMM_BF16: {
@@ -246,6 +249,7 @@ static int check_node(const cgx_chain* c, const Node& n) {
     }
     case CGX_OP_ATTN_CAUSAL:
       if (n.n_in != 1) return fail(CGX_E_INVALID_ARG, "attention: one input qkv");
+      if (S(0).dtype != CGX_BF16 || o.dtype != CGX_BF16) return fail(CGX_E_UNSUPPORTED, "attention: bf16 qkv and output only");
       CKS(need(S(0).nelems >= (uint64_t)a.T * 3 * a.H * a.D && o.nelems >= (uint64_t)a.T * a.H * a.D, "attention: shape"));
       return decoder_attn_supported(a.T, a.H, a.D) ? CGX_OK : fail(CGX_E_UNSUPPORTED, "attention: shape");
     case CGX_OP_ALLREDUCE_SUM:
@@ -295,11 +299,21 @@ extern "C" int cgx_chain_set_nccl(cgx_chain* c, void* comm) {
   return CGX_OK;
 }
 
-// Peer all-reduce region of one rank: receive data [2][world][slot] bf16 (slots 256-B aligned),
-// then the flag array [kArMaxNodes][kArMaxWorld][kArMaxCtas] uint32.
+// Peer all-reduce region of one rank: receive data [max_ar][2 parity][world][slot] bf16 (slots
+// 256-B aligned), then the flag array [max_ar][kArMaxWorld][kArMaxCtas] uint32. Every all-reduce
+// node owns its two parity buffers, so buffer reuse never depends on which other all-reduces an
+// exec runs or in which order execs are launched (node i's parity-p buffer is rewritten at its
+// generation g + 2, after every rank has published generation g + 1, i.e. finished reading g).
 static uint64_t peer_slot_elems(uint64_t max_elems) { return (max_elems + 127) / 128 * 128; }
-static uint64_t peer_flag_offset(int world, uint64_t max_elems) {
-  return 2ull * (uint64_t)world * peer_slot_elems(max_elems) * 2;
+static uint64_t peer_node_elems(int world, uint64_t max_elems) {
+  return 2ull * (uint64_t)world * peer_slot_elems(max_elems);
+}
+static uint64_t peer_flag_offset(int world, uint64_t max_elems, int max_ar) {
+  return (uint64_t)max_ar * peer_node_elems(world, max_elems) * 2;
+}
+
+static bool is_allreduce(const Node& n) {
+  return n.op == CGX_OP_ALLREDUCE_SUM || (n.op == CGX_OP_GEMM_BF16 && (n.attr.flags & CGX_GEMM_ALLREDUCE));
 }
 
 // Position of node k among the chain's all-reduces (ALLREDUCE_SUM nodes and GEMMs with the fused
@@ -308,7 +322,7 @@ static void ar_position(const cgx_chain* c, int k, int* index, int* total) {
   int i = 0, t = 0;
   for (size_t q = 0; q < c->nodes.size(); ++q) {
     const Node& n = c->nodes[q];
-    if (n.op == CGX_OP_ALLREDUCE_SUM || (n.op == CGX_OP_GEMM_BF16 && (n.attr.flags & CGX_GEMM_ALLREDUCE))) {
+    if (is_allreduce(n)) {
       if ((int)q < k) ++i;
       ++t;
     }
@@ -317,14 +331,19 @@ static void ar_position(const cgx_chain* c, int k, int* index, int* total) {
   *total = t;
 }
 
-extern "C" int cgx_peer_buffer_bytes(int world, uint64_t max_elems, uint64_t* bytes) {
+extern "C" int cgx_peer_buffer_bytes(int world, uint64_t max_elems, int max_allreduces, uint64_t* bytes) {
   if (world < 1 || world > kArMaxWorld || !bytes) return fail(CGX_E_INVALID_ARG, "peer_buffer_bytes: world 1..8");
-  *bytes = peer_flag_offset(world, max_elems) + sizeof(uint32_t) * kArMaxNodes * kArMaxWorld * kArMaxCtas;
+  if (max_allreduces < 1 || max_allreduces > kArMaxNodes)
+    return fail(CGX_E_INVALID_ARG, "peer_buffer_bytes: max_allreduces 1..64");
+  *bytes = peer_flag_offset(world, max_elems, max_allreduces) +
+           sizeof(uint32_t) * (uint64_t)max_allreduces * kArMaxWorld * kArMaxCtas;
   return CGX_OK;
 }
 
-extern "C" int cgx_chain_set_peers(cgx_chain* c, int rank, int world, void* const* bases, uint64_t max_elems) {
-  if (!c || !bases || world < 1 || world > kArMaxWorld || rank < 0 || rank >= world || max_elems == 0)
+extern "C" int cgx_chain_set_peers(cgx_chain* c, int rank, int world, void* const* bases, uint64_t max_elems,
+                                   int max_allreduces) {
+  if (!c || !bases || world < 1 || world > kArMaxWorld || rank < 0 || rank >= world || max_elems == 0 ||
+      max_allreduces < 1 || max_allreduces > kArMaxNodes)
     return fail(CGX_E_INVALID_ARG, "set_peers: bad argument");
   if (c->allocated) return fail(CGX_E_STATE, "set_peers: chain already captured");
   for (int r = 0; r < world; ++r) {
@@ -339,7 +358,30 @@ extern "C" int cgx_chain_set_peers(cgx_chain* c, int rank, int world, void* cons
   c->peer_rank = rank;
   c->peer_world = world;
   c->peer_max_elems = max_elems;
+  c->peer_max_ar = max_allreduces;
   c->peer_base.assign(bases, bases + world);
+  return CGX_OK;
+}
+
+// Dedicated zero-filled device allocation (peer regions): its CUDA IPC handle maps exactly this
+// buffer at offset 0 in a peer process (a sub-allocation of a caching allocator would not).
+extern "C" int cgx_device_alloc(int device, uint64_t bytes, void** dptr_out) {
+  if (!dptr_out || bytes == 0) return fail(CGX_E_INVALID_ARG, "device_alloc: bad argument");
+  CK(cudaSetDevice(device));
+  void* p = nullptr;
+  CK(cudaMalloc(&p, bytes));
+  const cudaError_t ce = cudaMemset(p, 0, bytes);
+  if (ce != cudaSuccess) {
+    cudaFree(p);
+    return cuda_fail(ce, "device_alloc memset", __LINE__);
+  }
+  CK(cudaDeviceSynchronize());
+  *dptr_out = p;
+  return CGX_OK;
+}
+extern "C" int cgx_device_free(void* dptr) {
+  if (!dptr) return CGX_OK;
+  CK(cudaFree(dptr));
   return CGX_OK;
 }
 
@@ -499,7 +541,21 @@ struct cgx_exec {
   unsigned long long* d_seq = nullptr;
   volatile unsigned long long* h_ack = nullptr;
   unsigned long long* d_ack = nullptr;
+  // device-side failure word (DevStatus, cgx_args.h): mapped pinned host memory written by spinning
+  // / device-launching kernels instead of trapping; checked by every cgx_launch
+  volatile uint32_t* h_status = nullptr;
+  uint32_t* d_status = nullptr;
+  uint64_t spin_timeout_ns = 0;
 };
+
+static DevStatus dev_status(const cgx_exec* e) { return DevStatus{e->d_status, e->spin_timeout_ns}; }
+
+// Spin bound of the kernels that wait on another agent: 10 s, or CGX_SPIN_TIMEOUT_MS (tests).
+static uint64_t spin_timeout_ns() {
+  const char* v = getenv("CGX_SPIN_TIMEOUT_MS");
+  const long long ms = v ? atoll(v) : 0;
+  return (uint64_t)(ms > 0 ? ms : 10000) * 1000000ull;
+}
 
 static cgx_transport eff_transport(const cgx_exec_opts& o) {
   return o.transport == CGX_XPORT_DEFAULT ? CGX_XPORT_ROOT_PARAMS : o.transport;
@@ -736,17 +792,20 @@ static int build_launch(cgx_exec* e, int k, Launch& l) {
           return fail(CGX_E_UNSUPPORTED, "gemm allreduce: more than 256 CTAs");
         int ar_index = 0, n_ar = 0;
         ar_position(c, k, &ar_index, &n_ar);
-        if (n_ar > kArMaxNodes) return fail(CGX_E_UNSUPPORTED, "gemm allreduce: more than 64 all-reduces");
+        if (n_ar > c->peer_max_ar)
+          return fail(CGX_E_UNSUPPORTED, "gemm allreduce: more all-reduces than the peer regions hold (max_allreduces)");
         std::vector<void*> recv(c->peer_world);
         std::vector<uint32_t*> flg(c->peer_world);
-        for (int r = 0; r < c->peer_world; ++r) {
-          recv[r] = c->peer_base[r];
+        for (int r = 0; r < c->peer_world; ++r) {   // this node's [2][world][slot] receive buffers
+          recv[r] = static_cast<__nv_bfloat16*>(c->peer_base[r]) +
+                    (uint64_t)ar_index * peer_node_elems(c->peer_world, c->peer_max_elems);
           flg[r] = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(c->peer_base[r]) +
-                                               peer_flag_offset(c->peer_world, c->peer_max_elems));
+                                               peer_flag_offset(c->peer_world, c->peer_max_elems, c->peer_max_ar));
         }
         decoder_gemm_set_allreduce(l.args.p, (uint32_t)c->peer_rank, (uint32_t)c->peer_world, (uint32_t)ar_index,
                                    (uint32_t)n_ar, peer_slot_elems(c->peer_max_elems), c->peer_counters,
                                    recv.data(), flg.data());
+        decoder_gemm_set_status(l.args.p, e->d_status, e->spin_timeout_ns);
       }
       if (res_ext) {
         const int j = c->slots[n.in[3]].ext_j;
@@ -782,7 +841,8 @@ static int build_launch(cgx_exec* e, int k, Launch& l) {
           return fail(CGX_E_UNSUPPORTED, "allreduce (peer): n must be a multiple of 8 and <= max_elems");
         int ar_index = 0, n_ar = 0;
         ar_position(c, k, &ar_index, &n_ar);
-        if (n_ar > kArMaxNodes) return fail(CGX_E_UNSUPPORTED, "allreduce (peer): more than 64 nodes");
+        if (n_ar > c->peer_max_ar)
+          return fail(CGX_E_UNSUPPORTED, "allreduce (peer): more all-reduces than the peer regions hold (max_allreduces)");
         l.args.reset(sizeof(PeerArArgs));
         PeerArArgs* a = argp<PeerArArgs>(l);
         a->in = static_cast<const __nv_bfloat16*>(slot_ptr(n.in[0]));
@@ -794,11 +854,13 @@ static int build_launch(cgx_exec* e, int k, Launch& l) {
         a->ar_index = (uint32_t)ar_index;
         a->n_ar = (uint32_t)n_ar;
         a->counters = c->peer_counters;
-        for (int r = 0; r < c->peer_world; ++r) {
-          a->recv[r] = static_cast<__nv_bfloat16*>(c->peer_base[r]);
+        for (int r = 0; r < c->peer_world; ++r) {   // this node's [2][world][slot] receive buffers
+          a->recv[r] = static_cast<__nv_bfloat16*>(c->peer_base[r]) +
+                       (uint64_t)ar_index * peer_node_elems(c->peer_world, c->peer_max_elems);
           a->flags_of[r] = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(c->peer_base[r]) +
-                                                      peer_flag_offset(c->peer_world, c->peer_max_elems));
+                                                      peer_flag_offset(c->peer_world, c->peer_max_elems, c->peer_max_ar));
         }
+        a->st = dev_status(e);
         const uint64_t nv = n.attr.n / 8;
         l.grid = dim3((unsigned)std::max<uint64_t>(1, std::min<uint64_t>(kArMaxCtas, ceil_div(nv, 256))));
         l.block = dim3(256);
@@ -925,6 +987,7 @@ static int set_sync_flags(cgx_exec* e) {
       std::vector<char> spun_on(nl, 0);
       for (size_t p = 0; p < nl; ++p) {
         ElemArgs* a = argp<ElemArgs>(e->L[p]);
+        a->st = dev_status(e);
         a->df_done = e->df_mem;
         a->df_epoch = e->df_mem + nl;
         a->df_self = (uint32_t)p;
@@ -1208,6 +1271,7 @@ static int capture_dag(cgx_exec* e, int gi, cudaStream_t cs, cgx_transport t) {
   {
     std::vector<int> last_w(ns, -1);
     std::vector<std::vector<int>> readers(ns);
+    int last_ar = -1;
     for (size_t p = 0; p < nl; ++p) {
       const Node& n = e->c->nodes[e->L[p].node];
       auto add = [&](int q) {
@@ -1218,6 +1282,13 @@ static int capture_dag(cgx_exec* e, int gi, cudaStream_t cs, cgx_transport t) {
       for (int j = 0; j < n.n_in; ++j) add(last_w[n.in[j]]);
       add(last_w[n.out]);
       for (int r : readers[n.out]) add(r);
+      // collectives run one at a time, in chain order, on every rank: an artificial edge from the
+      // previous all-reduce (NCCL forbids concurrent collectives on one communicator; the peer
+      // protocol's spinning kernels must not compete for SMs with each other)
+      if (is_allreduce(n)) {
+        add(last_ar);
+        last_ar = (int)p;
+      }
       for (int j = 0; j < n.n_in; ++j) readers[n.in[j]].push_back((int)p);
       last_w[n.out] = (int)p;
       readers[n.out].clear();
@@ -1505,6 +1576,7 @@ static void exec_free(cgx_exec* e) {
   }
   if (e->h_stage) cudaFreeHost(e->h_stage);
   if (e->h_ack) cudaFreeHost((void*)e->h_ack);
+  if (e->h_status) cudaFreeHost((void*)e->h_status);
   if (e->d_seq) cudaFree(e->d_seq);
   for (auto& v : e->ev) cudaEventDestroy(v);
   for (auto& v : e->dag_ev) if (v) cudaEventDestroy(v);
@@ -1552,6 +1624,16 @@ extern "C" int cgx_exec_create_ex(cgx_chain* c, const cgx_exec_opts* opts, void*
     if (read[j]) e->ext_read.push_back(j);
   auto bail = [&](int st) { exec_free(e); return st; };
   int st;
+  {
+    uint32_t* hs = nullptr;
+    cudaError_t ce = cudaHostAlloc((void**)&hs, 64, cudaHostAllocMapped);
+    if (ce != cudaSuccess) return bail(cuda_fail(ce, "status word", __LINE__));
+    *hs = 0;
+    e->h_status = hs;
+    ce = cudaHostGetDevicePointer((void**)&e->d_status, hs, 0);
+    if (ce != cudaSuccess) return bail(cuda_fail(ce, "status word", __LINE__));
+    e->spin_timeout_ns = spin_timeout_ns();
+  }
   if (o.mode == CGX_MODE_GRAPH_COPY && (st = setup_copy(e)) != CGX_OK) return bail(st);
   if (o.mode == CGX_MODE_GRAPH_INDIRECT && (st = setup_table(e)) != CGX_OK) return bail(st);
   {
@@ -1859,9 +1941,22 @@ extern "C" int cgx_bind(cgx_exec* e, const void* const* ext, int n_ext) {
   return CGX_OK;
 }
 
+// A kernel of an earlier replay reported a device-side failure (DevStatus): sticky, the exec's
+// outputs are no longer trustworthy.
+static int check_device_status(const cgx_exec* e) {
+  const uint32_t w = e->h_status ? *e->h_status : 0u;
+  if (!w) return CGX_OK;
+  std::string m = "device-side failure reported by an earlier replay of this exec:";
+  if (w & kDevErrPeer) m += " peer all-reduce timed out waiting for a rank (lost peer);";
+  if (w & kDevErrDataflow) m += " dataflow dependency counter never reached its target;";
+  if (w & kDevErrDevLaunch) m += " device-side cudaGraphLaunch failed;";
+  return fail(CGX_E_DEVICE, m);
+}
+
 extern "C" int cgx_launch(cgx_exec* e) {
   if (!e) return fail(CGX_E_INVALID_ARG, "launch: exec is NULL");
   if (!e->bound) return fail(CGX_E_STATE, "launch: exec was never bound (cgx_bind first)");
+  CKS(check_device_status(e));
   if (e->o.mode == CGX_MODE_EAGER) {
     for (auto& l : e->L) CKS(issue(e, l, e->s));
   } else {
@@ -1909,6 +2004,8 @@ extern "C" int cgx_device_loop(cgx_exec* e, const void* d_ptr_sets, int n_sets, 
   a.chain = e->ge[0];
   a.n_ext = n_ext;
   a.n_sets = (uint32_t)n_sets;
+  a.status = e->d_status;
+  CKS(check_device_status(e));
   if (!e->dl_ge) {
     CK(cudaMalloc(&e->dl_iter, sizeof(unsigned long long)));
     a.iter = e->dl_iter;
@@ -1990,6 +2087,7 @@ extern "C" int cgx_output_gather(cgx_exec* e, const int* slots, int n, void* dst
 extern "C" int cgx_stats(const cgx_exec* e, cgx_stats_t* out) {
   if (!e || !out) return fail(CGX_E_INVALID_ARG, "stats: NULL argument");
   *out = e->st;
+  out->device_error = e->h_status ? *e->h_status : 0u;
   return CGX_OK;
 }
 
@@ -2187,6 +2285,9 @@ extern "C" int cgx_tune_graph_streams(cgx_chain* c, const cgx_exec_opts* opts, v
       !best_out)
     return fail(CGX_E_INVALID_ARG, "tune_graph_streams: bad argument");
   if (opts->mode == CGX_MODE_EAGER) return fail(CGX_E_INVALID_ARG, "tune_graph_streams: graph modes only");
+  for (int ci = 0; ci < n_cand; ++ci)   // every candidate is checked before any is timed
+    if (candidates[ci] < 1 || candidates[ci] > 64)
+      return fail(CGX_E_INVALID_ARG, "tune_graph_streams: every candidate stream count must be in 1..64");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   struct Ev {

@@ -26,35 +26,40 @@ def nccl_bootstrap(device: int, group=None) -> int:
 
 
 class PeerRegions:
-    """Multi-process setup of the peer-memory all-reduce (cgx_chain_set_peers): every rank zero-fills
-    one region of cgx_peer_buffer_bytes() on its own GPU, exports its CUDA IPC handle, gathers every
-    rank's handle through the torch process group and maps the peers' regions into this process
-    (cgx_ipc_open; peer access over NVLink). `bases` is then the per-rank pointer list the chain
-    takes. Keep the object alive as long as the chain; close() unmaps the peers' regions."""
+    """Multi-process setup of the peer-memory all-reduce (cgx_chain_set_peers): every rank owns one
+    zero-filled region of cgx_peer_buffer_bytes() in a DEDICATED allocation on its own GPU
+    (cgx_device_alloc: the CUDA IPC handle maps a whole allocation, so a sub-allocation of torch's
+    caching allocator would land at the wrong offset in the peer), exports its IPC handle, gathers
+    every rank's handle through the torch process group and maps the peers' regions into this
+    process (cgx_ipc_open; peer access over NVLink). `bases` is then the per-rank pointer list the
+    chain takes. Keep the object alive as long as the chain; close() unmaps and frees."""
 
-    def __init__(self, world: int, rank: int, max_elems: int, device, group=None):
+    def __init__(self, world: int, rank: int, max_elems: int, device, group=None, max_allreduces: int = 64):
         import torch
         import torch.distributed as dist
-        self.own = torch.zeros(cgx.peer_buffer_bytes(world, max_elems) + 256, dtype=torch.uint8, device=device)
-        base = (self.own.data_ptr() + 255) // 256 * 256
-        torch.cuda.synchronize(device)
-        handle = cgx.ipc_handle(self.own.data_ptr())          # handles map allocation bases
+        dev = torch.device(device)
+        self.own = cgx.device_alloc(dev.index if dev.index is not None else torch.cuda.current_device(),
+                                    cgx.peer_buffer_bytes(world, max_elems, max_allreduces))
+        handle = cgx.ipc_handle(self.own)
         gathered = [None] * world
-        dist.all_gather_object(gathered, (handle, base - self.own.data_ptr()), group=group)
+        dist.all_gather_object(gathered, handle, group=group)
         self.opened, self.bases = [], []
-        for r, (h, off) in enumerate(gathered):
+        for r, h in enumerate(gathered):
             if r == rank:
-                self.bases.append(base)
+                self.bases.append(self.own)
             else:
                 p = cgx.ipc_open(h)
                 self.opened.append(p)
-                self.bases.append(p + off)
-        self.world, self.rank, self.max_elems = world, rank, max_elems
+                self.bases.append(p)
+        self.world, self.rank, self.max_elems, self.max_allreduces = world, rank, max_elems, max_allreduces
 
     def peers(self) -> tuple:
-        return (self.rank, self.world, self.bases, self.max_elems)
+        return (self.rank, self.world, self.bases, self.max_elems, self.max_allreduces)
 
     def close(self):
         for p in self.opened:
             cgx.ipc_close(p)
         self.opened = []
+        if self.own:
+            cgx.device_free(self.own)
+            self.own = 0

@@ -23,6 +23,8 @@ def main():
     ap.add_argument("--T", type=int, default=128)
     ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--check", action="store_true")
+    ap.add_argument("--dump", default="", help="directory: every rank saves the GPU value of every INTERNAL "
+                    "slot after one INDIRECT replay with input set 0 (rank{r}.npz) for node-local parity")
     ap.add_argument("--allreduce", choices=("nccl", "peer", "fused"), default="nccl",
                     help="ALLREDUCE_SUM nodes: captured ncclAllReduce, the peer-memory one-shot kernel "
                          "over CUDA IPC-mapped regions (tp.PeerRegions), or that all-reduce fused into "
@@ -86,6 +88,12 @@ def main():
                 t = t.to(dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         res[name] = float(t.item())
+        if args.dump and name == "indirect_first_node":
+            LIB.cgx_bind(ex.handle, ptrs[0], 1)
+            LIB.cgx_launch(ex.handle)
+            os.makedirs(args.dump, exist_ok=True)
+            np.savez(os.path.join(args.dump, f"rank{rank}.npz"),
+                     **{s.name: ex.output(s.name) for s in spec.internals()})
         if args.check and name == "indirect_first_node":
             LIB.cgx_bind(ex.handle, ptrs[0], 1)
             LIB.cgx_launch(ex.handle)

@@ -66,15 +66,20 @@ def test_product_and_oracle_are_independent():
 
 
 def test_peer_buffer_bytes_host_only():
-    """cgx_peer_buffer_bytes is pure host arithmetic: receive data [2][world][slot] bf16 (slots
-    rounded up to 128 elements) followed by the flag array [64][8][256] uint32."""
+    """cgx_peer_buffer_bytes is pure host arithmetic: receive data [max_ar][2][world][slot] bf16
+    (slots rounded up to 128 elements: every all-reduce node owns two parity buffers) followed by
+    the flag array [max_ar][8][256] uint32."""
     from paper_2503_19779_b200 import cgx
-    for world, n in ((1, 8), (2, 98304), (8, 1000)):
+    for world, n, nar in ((1, 8, 1), (2, 98304, 24), (8, 1000, 64)):
         slot = (n + 127) // 128 * 128
-        assert cgx.peer_buffer_bytes(world, n) == 2 * world * slot * 2 + 4 * 64 * 8 * 256
+        assert cgx.peer_buffer_bytes(world, n, nar) == nar * 2 * world * slot * 2 + 4 * nar * 8 * 256
+    assert cgx.peer_buffer_bytes(2, 8) == cgx.peer_buffer_bytes(2, 8, 64)
     for bad in (0, 9):
         with pytest.raises(cgx.CgxError):
             cgx.peer_buffer_bytes(bad, 1024)
+    for bad_ar in (0, 65):
+        with pytest.raises(cgx.CgxError):
+            cgx.peer_buffer_bytes(2, 1024, bad_ar)
 
 
 def test_bench_reference_arm_contract_on_cpu():
@@ -111,3 +116,19 @@ def test_tune_graph_streams_argument_checks_on_cpu(lib):
     eager = c.ExecOpts(c.MODE["EAGER"], 0, 0, 0, 0, 0, 0, 0, 0)
     assert c.LIB.cgx_tune_graph_streams(fake_chain, C.byref(eager), None, sets, 1, 1, cand, 1, 10, C.byref(best),
                                         None) == c.E_INVALID_ARG
+
+
+def test_tune_graph_streams_rejects_out_of_range_candidates_on_cpu(lib):
+    """Every candidate stream count is validated (1..64) before any candidate is built or timed
+    (0 used to build the default 16 streams and could be returned as the best)."""
+    import ctypes as C
+    c = lib
+    opts = c.ExecOpts(c.MODE["INDIRECT"], c.XPORT["ROOT_PARAMS"], 0, 0, 0, 0, 0, c.SYNC["GRAPH"], 0)
+    best = C.c_int(-7)
+    sets = c.ptr_array([0])
+    fake_chain = C.c_void_p(0x1000)   # never dereferenced: the candidate check fails first
+    for bad in ((16, 0), (65,), (8, 16, -1)):
+        cand = (C.c_int * len(bad))(*bad)
+        assert c.LIB.cgx_tune_graph_streams(fake_chain, C.byref(opts), None, sets, 1, 1, cand, len(bad), 10,
+                                            C.byref(best), None) == c.E_INVALID_ARG
+        assert "1..64" in c.last_error() and best.value == -7

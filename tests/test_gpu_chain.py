@@ -14,6 +14,7 @@ from oracle import capture as ocap  # noqa: E402
 from oracle.chain import eval_chain  # noqa: E402
 from synth import splitmix as sm  # noqa: E402
 from synth import workloads as wl  # noqa: E402
+from reduce_bounds import assert_output  # noqa: E402
 from synth.workloads import ChainSpec, NodeSpec, SlotSpec  # noqa: E402
 
 ARMS = [("EAGER", "DEFAULT"), ("COPY", "DEFAULT"), ("SETPARAMS", "DEFAULT"),
@@ -434,12 +435,7 @@ def test_indirect_stress_rotating_inputs(rt, transport):
         for i, d in snap.items():
             for nm, buf in d.items():
                 got = buf.cpu().numpy().view(np.float32)
-                o = ref[i % 3][nm]
-                prod = [n for n in spec.nodes if n.out == nm][0]
-                if prod.op == "REDUCE_SUM" or (prod.op == "SCALE_IMM" and nm.startswith("s")):
-                    assert np.allclose(got, o, rtol=1e-5, atol=1e-3), (transport, i, nm)
-                else:
-                    assert np.array_equal(got, o), (transport, i, nm)
+                assert_output(spec, ref[i % 3], nm, got, (transport, i))
         chain.close()
 
 

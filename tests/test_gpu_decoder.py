@@ -283,3 +283,35 @@ def test_c3_t1_decode_shape(rt):
     outs = _run(rt, spec, "INDIRECT", 1, st)
     ext = wl.external_values(spec, 0)
     _node_local_check(spec, st, ext, outs[0])
+
+
+def test_layernorm_row_capacity(rt):
+    """k_layernorm holds a row in one warp's registers (2048 bf16 columns): cols = 2048 runs and
+    matches the oracle; cols = 2056 (and the 4096 of a wider model) is rejected at add_node with
+    CGX_E_UNSUPPORTED instead of silently normalising a partial row."""
+    cgx, runner = rt
+    for cols, ok in ((2048, True), (2056, False), (4096, False)):
+        rows = 8
+        slots = [SlotSpec("x", "external", "bf16", rows * cols), SlotSpec("g", "static", "bf16", cols, "gamma"),
+                 SlotSpec("b", "static", "bf16", cols, "bias"), SlotSpec("ln", "internal", "bf16", rows * cols)]
+        nodes = [NodeSpec("LAYERNORM", ("x", "g", "b"), "ln", {"rows": rows, "cols": cols, "eps": 1e-5})]
+        spec = ChainSpec("ln_wide", slots, nodes, [(0, 0)])
+        st = wl.static_values(spec)
+        if not ok:
+            with pytest.raises(cgx.CgxError) as ei:
+                runner.Chain(spec, runner.upload_statics(spec, st, torch.device("cuda:0")))
+            assert ei.value.status == cgx.E_UNSUPPORTED
+            continue
+        outs = _run(rt, spec, "INDIRECT", 1, st)
+        env = eval_chain(spec, wl.external_values(spec, 0), st)
+        _close(outs[0]["ln"], env["ln"], f"layernorm cols={cols}")
+
+
+def test_attention_rejects_f32_slots(rt):
+    cgx, runner = rt
+    T, H, D = 16, 2, 64
+    slots = [SlotSpec("q", "external", "f32", T * 3 * H * D), SlotSpec("att", "internal", "bf16", T * H * D)]
+    nodes = [NodeSpec("ATTN_CAUSAL", ("q",), "att", {"T": T, "H": H, "D": D, "scale": 0.125})]
+    with pytest.raises(cgx.CgxError) as ei:
+        runner.Chain(ChainSpec("attn_f32", slots, nodes, [(0, 0)]), {})
+    assert ei.value.status == cgx.E_UNSUPPORTED

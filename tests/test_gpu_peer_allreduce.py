@@ -17,6 +17,7 @@ from oracle.chain import eval_chain, eval_chain_tp  # noqa: E402
 from oracle.numerics import bf16_bits, bits_to_f64  # noqa: E402
 from synth import workloads as wl  # noqa: E402
 from synth.workloads import ChainSpec, NodeSpec, SlotSpec  # noqa: E402
+from tp_check import check_tp_node_local  # noqa: E402
 
 
 @pytest.fixture(scope="module")
@@ -101,6 +102,9 @@ def test_tp_decoder_peer_allreduce(rt, tp, mode, transport):
     for rep in range(3):
         for r in range(1, tp):
             assert np.array_equal(outs[rep][r][last], outs[rep][0][last]), (rep, r)
+        # every node of every rank, element-wise, from the GPU's own node inputs (shard GEMMs included)
+        assert check_tp_node_local(specs, statics, exts[rep], outs[rep], f"tp{tp} {mode} rep {rep}") == \
+            tp * len(specs[0].nodes)
         ref = eval_chain_tp(specs, exts[rep], statics)[0][last]
         g = bits_to_f64(outs[rep][0][last])
         assert np.linalg.norm(g - ref) / np.linalg.norm(ref) <= 2e-2
@@ -119,12 +123,9 @@ def test_set_peers_errors(rt):
     ch.close()
 
 
-@pytest.mark.parametrize("allreduce", ["peer", "fused"])
-def test_multiprocess_ipc_peer_allreduce(rt, allreduce):
-    """Two processes (torchrun) on this one GPU: regions exchanged as CUDA IPC handles through a
-    gloo process group (tp.PeerRegions), TP=2 decoder layer with the peer all-reduce. The ranks
-    time-share the device, so only the results are checked: identical across ranks, oracle error
-    within the decoder tolerance."""
+def _torchrun_tp(tp, allreduce, layers, tmp_path, one_gpu):
+    """Run scripts/bench_tp.py under torchrun with `tp` ranks (each on its own GPU, or all on GPU 0
+    when one_gpu), dump every rank's internals and check them node-local against the oracle."""
     import json
     import os
     import socket
@@ -134,16 +135,53 @@ def test_multiprocess_ipc_peer_allreduce(rt, allreduce):
     with socket.socket() as sk:
         sk.bind(("127.0.0.1", 0))
         port = sk.getsockname()[1]
-    env = dict(os.environ, CGX_TP_DEVICE="0")
-    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+    env = dict(os.environ)
+    if one_gpu:
+        env["CGX_TP_DEVICE"] = "0"
+    dump = str(tmp_path / f"tp{tp}_{allreduce}")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(tp),
                         "--master-addr", "127.0.0.1", "--master-port", str(port),
-                        os.path.join(root, "scripts", "bench_tp.py"), "--allreduce", allreduce, "--layers", "1",
-                        "--steps", "5", "--check"], env=env, capture_output=True, text=True, timeout=280)
+                        os.path.join(root, "scripts", "bench_tp.py"), "--allreduce", allreduce, "--layers",
+                        str(layers), "--steps", "5", "--check", "--dump", dump],
+                       env=env, capture_output=True, text=True, timeout=400)
     line = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
     assert r.returncode == 0 and line, r.stdout[-2000:] + r.stderr[-2000:]
     res = json.loads(line[-1])["us_per_replay_max_over_ranks"]
     assert res["ranks_identical"]
     assert max(res["check_rel_err_per_rank"]) <= 2e-2
+    full = wl.c3_chain(T=128, n_layers=layers)
+    specs = [wl.c3_chain(T=128, n_layers=layers, tp=tp, rank=k, fuse_allreduce=allreduce == "fused")
+             for k in range(tp)]
+    statics = [wl.static_values(wl.c3_chain(T=128, n_layers=layers, tp=tp, rank=k), tp=tp, rank=k, full=full)
+               for k in range(tp)]
+    exts = [wl.external_values(specs[k], 0) for k in range(tp)]
+    gots = []
+    for k in range(tp):
+        z = np.load(os.path.join(dump, f"rank{k}.npz"))
+        gots.append({nm: z[nm] for nm in z.files})
+    assert check_tp_node_local(specs, statics, exts, gots, f"torchrun tp{tp} {allreduce}") == tp * len(specs[0].nodes)
+    return res
+
+
+@pytest.mark.parametrize("allreduce", ["peer", "fused"])
+def test_multiprocess_ipc_peer_allreduce(rt, allreduce, tmp_path):
+    """Two processes (torchrun) on this one GPU: regions exchanged as CUDA IPC handles through a
+    gloo process group (tp.PeerRegions, dedicated allocations), TP=2 decoder layer with the peer
+    all-reduce. The ranks time-share the device, so only the results are checked: every node of
+    every rank element-wise against the oracle fed that rank's GPU inputs, ranks identical."""
+    _torchrun_tp(2, allreduce, 1, tmp_path, one_gpu=True)
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="needs >= 2 GPUs (NCCL ranks on separate devices)")
+@pytest.mark.parametrize("tp", [2, 4, 8])
+@pytest.mark.parametrize("allreduce", ["nccl", "peer", "fused"])
+def test_multigpu_tp_chain(rt, tp, allreduce, tmp_path):
+    """C5 on real ranks: TP = 2/4/8 decoder (2 layers, T = 128), one
+    process per GPU, ALLREDUCE_SUM as a captured ncclAllReduce over NVLink (or the peer / fused
+    peer all-reduce over IPC-mapped regions); node-local element-wise parity on every rank."""
+    if torch.cuda.device_count() < tp:
+        pytest.skip(f"needs {tp} GPUs")
+    _torchrun_tp(tp, allreduce, 2, tmp_path, one_gpu=False)
 
 
 @pytest.mark.parametrize("tp", [2, 4])
@@ -174,6 +212,36 @@ def test_tp_decoder_gemm_fused_allreduce(rt, monkeypatch, tp, mode, transport):
         for r in range(tp):
             assert np.array_equal(outs_f[rep][r][last], outs_u[rep][r][last]), (rep, r)
             assert np.array_equal(outs_f[rep][r][last], outs_f[rep][0][last]), (rep, r)
+        check_tp_node_local(specs_f, statics, exts[rep], outs_f[rep], f"tp{tp} fused {mode} rep {rep}")
         ref = eval_chain_tp(specs_f, exts[rep], statics)[0][last]
         g = bits_to_f64(outs_f[rep][0][last])
         assert np.linalg.norm(g - ref) / np.linalg.norm(ref) <= 2e-2
+
+
+def test_lost_peer_reports_device_error(rt, monkeypatch):
+    """A rank whose peer never arrives must not hang or trap the context: the
+    spinning all-reduce gives up after the spin bound (CGX_SPIN_TIMEOUT_MS), stores kDevErrPeer in
+    the exec's status word, and the exec's next cgx_launch returns CGX_E_DEVICE (sticky); the CUDA
+    context stays usable for other work."""
+    cgx, runner = rt
+    monkeypatch.setenv("CGX_SPIN_TIMEOUT_MS", "300")
+    n = 4096
+    dev = torch.device("cuda:0")
+    regs = _regions(cgx, 2, n, dev)
+    spec = _ar_spec(n)
+    chain = runner.Chain(spec, {}, peers=(0, 2, [_base(t) for t in regs], n))   # rank 1 never runs
+    ex = chain.exec("INDIRECT")
+    x = runner.upload_externals(spec, wl.external_values(spec, 0), dev)
+    ex.bind(x)
+    ex.launch()                                  # returns at once; the kernel gives up after ~0.3 s
+    torch.cuda.synchronize()
+    assert ex.stats()["device_error"] == 2
+    ex.bind(x)
+    with pytest.raises(cgx.CgxError) as ei:
+        ex.launch()
+    assert ei.value.status == cgx.E_DEVICE and "lost peer" in str(ei.value)
+    with pytest.raises(cgx.CgxError):
+        ex.launch()                              # sticky
+    chain.close()
+    y = torch.ones(16, device=dev) * 2           # the context is still healthy
+    assert float(y.sum().item()) == 32.0
