@@ -127,12 +127,14 @@ struct LnArgs {
   int32_t tx, pad0;
   uint32_t flags, rows, cols, pad1;
   float eps;
+  unsigned long long* ntrace;   // CGX_NODE_TRACE=1: [entry min, ready max, exit max] ns (node_stamp)
 };
 
 struct AttnArgs {
   const void* qkv; void* out;
   uint32_t T, H, D, flags;
   float scale;
+  unsigned long long* ntrace;   // CGX_NODE_TRACE=1 (node_stamp)
 };
 
 // T5 (FIRST_NODE transport): the first node of the graph carries the bound pointers by value; its

@@ -32,12 +32,24 @@ void decoder_gemm_set_trigger_after_wait(void* args);
 void decoder_gemm_set_allreduce(void* args, uint32_t rank, uint32_t world, uint32_t ar_index, uint32_t n_ar,
                                 uint64_t slot_elems, uint32_t* counters, void* const* recv, uint32_t* const* flags);
 uint32_t decoder_gemm_ctas(const void* args, dim3 grid);
+// An EXTERNAL A operand (PI through the TMA descriptor): the kernel builds a per-CTA tensor map
+// (tm_ws: decoder_gemm_ctas x 128 B, 128-B aligned device memory) with the replay's A address,
+// table[idx] (INDIRECT) or the a_ptr field (idx < 0: patched by the patch modes; its byte offset,
+// and that of the idx field, from decoder_gemm_a_field). The small-M path reads a_ptr / table[idx]
+// directly.
+// after_wait: rebuild the map only after griddepcontrol.wait (EAGER: launches of one node overlap).
+void decoder_gemm_set_a_dynamic(void* args, const uint64_t* table, int32_t idx, void* tm_ws, bool after_wait);
+size_t decoder_gemm_a_field(size_t* tidx_off);
+// Re-point the table of a GEMM reading table entries (T6: graph gi reads table gi).
+void decoder_gemm_set_table(void* args, const uint64_t* table);
 // An EXTERNAL residual under INDIRECT: the epilogue reads its base pointer from table[idx].
 void decoder_gemm_set_residual_table(void* args, const uint64_t* table, int32_t idx);
 // Byte offsets of the residual pointer field and its int32 table-index field (patch modes).
 size_t decoder_gemm_residual_field(size_t* tidx_off);
 // Spin bound / failure word for the fused all-reduce epilogue (DevStatus, cgx_args.h).
 void decoder_gemm_set_status(void* args, uint32_t* word, uint64_t timeout_ns);
+// Diagnostics: replay-timeline stamps (CGX_NODE_TRACE=1; node_stamp, cgx_debug_node_trace).
+void decoder_gemm_set_node_trace(void* args, unsigned long long* nt);
 // Diagnostics: per-CTA %globaltimer trace [cta][16] written by the kernel (nullptr = off).
 void decoder_gemm_set_trace(void* args, unsigned long long* trace);
 }  // namespace cgx

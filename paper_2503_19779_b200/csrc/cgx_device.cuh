@@ -102,6 +102,14 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+// The same replay-timeline stamps for the decoder kernels (one thread per CTA calls it).
+__device__ __forceinline__ void node_stamp(unsigned long long* nt, int what) {
+  if (nt) {
+    const unsigned long long t = gtimer();
+    if (what == 0) atomicMin(nt, t);
+    else atomicMax(nt + what, t);
+  }
+}
 __device__ __forceinline__ void trace_at(const ElemArgs& a, int what) {
   if (a.trace && threadIdx.x == 0) {
     const unsigned long long t = gtimer();

@@ -31,6 +31,7 @@ static_assert(kLnMaxVec * 8 * 32 == (int)kLnMaxCols, "k_layernorm row capacity")
 template <int TW>
 __global__ void __launch_bounds__(kLnWarps * 32) k_layernorm(const __grid_constant__ ArgsTW<LnArgs, TW> A) {
   const LnArgs& a = A.a;
+  if (threadIdx.x == 0) node_stamp(a.ntrace, 0);
   tw_publish(A);
   const void* px = a.x;
   const bool late = a.flags & kFlagTableAfterWait;
@@ -68,7 +69,11 @@ __global__ void __launch_bounds__(kLnWarps * 32) k_layernorm(const __grid_consta
   }
   if (a.tx >= 0 && late) px = reinterpret_cast<const void*>(ld_table(a.table + a.tx));
   if (a.flags & kFlagTriggerAfterWait) pdl_trigger();
-  if (row >= a.rows) return;
+  if (threadIdx.x == 0) node_stamp(a.ntrace, 1);
+  if (row >= a.rows) {
+    if (a.ntrace && lane == 0) node_stamp(a.ntrace, 2);
+    return;
+  }
   const uint4* xr = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(px) + (size_t)row * a.cols);
   uint4 xu[kLnMaxVec];
 #pragma unroll
@@ -114,6 +119,7 @@ __global__ void __launch_bounds__(kLnWarps * 32) k_layernorm(const __grid_consta
       orow[idx] = r;
     }
   }
+  if (a.ntrace && lane == 0) node_stamp(a.ntrace, 2);
 }
 
 const void* kfn_layernorm(int tw) {
@@ -169,9 +175,11 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 
 __global__ void __launch_bounds__(kAttnMaxWarps * 32) k_attention(const __grid_constant__ AttnArgs a) {
   extern __shared__ __align__(16) uint8_t sm_attn[];
+  if (threadIdx.x == 0) node_stamp(a.ntrace, 0);
   if (!(a.flags & kFlagTriggerAfterWait)) pdl_trigger();
   pdl_wait();
   if (a.flags & kFlagTriggerAfterWait) pdl_trigger();
+  if (threadIdx.x == 0) node_stamp(a.ntrace, 1);
   const uint32_t T = a.T, H = a.H;
   const uint32_t h = blockIdx.y;
   const uint32_t q0 = blockIdx.x * kAttnQRows;
@@ -335,6 +343,10 @@ __global__ void __launch_bounds__(kAttnMaxWarps * 32) k_attention(const __grid_c
     const float inv = 1.0f / l;
     *reinterpret_cast<uint32_t*>(reinterpret_cast<__nv_bfloat16*>(a.out) + (size_t)qi * (H * kAttnD) + h * kAttnD + c) =
         pack_bf16(ox * inv, oy * inv);
+  }
+  if (a.ntrace) {
+    __syncthreads();
+    if (threadIdx.x == 0) node_stamp(a.ntrace, 2);
   }
 }
 

@@ -38,18 +38,38 @@ namespace cgx {
 
 static constexpr int kBM = 128;
 static constexpr int kBK = 64;          // 64 bf16 = 128 B = one swizzle-128B row
-// Operand ring depth: min(4, k-blocks per CTA) (deeper rings measured no faster at the C3 shapes,
-// profiles/r01); a shallow ring keeps split-K CTAs small enough for two per SM.
-static constexpr int kMaxStages = 4;
+// Operand pipelines (r02, profiles/r02/tma_issue_microbench.txt): A and W flow through SEPARATE
+// mbarrier rings of groups of G k-blocks (one 3-D TMA box {64, rows, G} per group, landing as G
+// stacked SW128 K-major tiles = the UMMA operand layout). One SM pulls ~160 GB/s from L2 when all
+// of a CTA's boxes are in flight at once (12 x 16 KiB in 1.25 us), whereas a ring that refills a
+// slot only after the MMA consumed it exposes one L2 round trip per refill. So the activation A
+// (the operand that arrives after the PDL wait, on the critical path) is held WHOLE in shared
+// memory whenever it fits ("one-shot": every A box is issued right after the wait, one barrier per
+// k-block so the MMAs start with the first), and the small weight slab W (static: issued before
+// the wait) cycles through the remaining space.
+static constexpr int kMaxGroupKb = 8;   // k-blocks per box
+static constexpr uint32_t kSmemLimit = 232448u;   // dynamic shared memory per block (227 KiB)
+static constexpr uint32_t kSmemFixed = 1024u + 512u + 16u + 256u + 512u;   // align, bias, words, tensor map, barriers
 static constexpr int kGemmThreads = 192;
 static constexpr uint32_t kGemmTriggerAfterWait = 1u << 8;   // internal flag bit (above CGX_GEMM_*)
 // W (and bias) written by an earlier node of the graph (training chain: transposed activations,
 // updated weights): no pre-wait weight prefetch / loads
 static constexpr uint32_t kGemmWAfterWait = 1u << 11;
+// A is rebound per replay (EXTERNAL A operand, PI through the TMA descriptor; "de-
+// references these pointers-to-pointers before performing any computation"): the producer warp
+// builds this CTA's own copy of the A tensor map in global memory with the replay's address
+// (table[ta] under INDIRECT, the patched a_ptr field in the patch modes) and loads A through it.
+static constexpr uint32_t kGemmADynamic = 1u << 12;
+// EAGER: two launches of the same node may overlap under PDL (node k of iteration i + 1 can start
+// while node k of iteration i still waits), so the per-CTA map is rewritten only after this
+// launch's griddepcontrol.wait (every earlier launch in the stream has then completed). In graphs
+// a node runs once per replay and replays are stream-serialised: the map is built pre-wait.
+static constexpr uint32_t kGemmADynAfterWait = 1u << 13;
+static constexpr uint32_t kGemmFenceOnWait = 1u << 14;   // experiment: tcgen05 fence only after a barrier wait
 
 struct alignas(64) GemmArgs {
-  CUtensorMap tmA;            // A [M, K] bf16, box {64, 128}
-  CUtensorMap tmB;            // W [N, K] bf16, box {64, BN}
+  CUtensorMap tmA;            // A [M, K] bf16 as 3-D {64, M, K/64}, box {64, 128, group}
+  CUtensorMap tmB;            // W [N, K] bf16 as 3-D {64, N, K/64}, box {64, BN, group}
   const __nv_bfloat16* bias;
   const __nv_bfloat16* residual;
   __nv_bfloat16* out;
@@ -57,10 +77,13 @@ struct alignas(64) GemmArgs {
   unsigned long long* cnt;    // per-tile monotonic arrival counters (split > 1)
   uint32_t M, N, K, flags;
   uint32_t split;             // K splits (gridDim.z)
-  uint32_t stages;            // operand ring depth (<= kMaxStages)
+  uint32_t ga, ra;            // A: k-blocks per box, groups resident (ra * ga >= k-blocks: one-shot)
+  uint32_t gw, rw;            // W: k-blocks per box, groups resident
   unsigned long long* trace;  // optional per-CTA %globaltimer trace [cta][16] (diagnostics)
   const uint64_t* table;      // INDIRECT: pointer table; residual = table[tres] when tres >= 0
   int32_t tres;               // table index of an EXTERNAL residual (-1: `residual` is direct)
+  int32_t ta;                 // kGemmADynamic: table index of A (-1: a_ptr, a patched field)
+  CUtensorMap* tm_ws;         // kGemmADynamic: per-CTA tensor-map workspace [ctas] (128-B aligned)
   const __nv_bfloat16* a_ptr; // small-M path (k_gemv_bf16): A and W by plain pointers
   const __nv_bfloat16* w_ptr;
   // CGX_GEMM_ALLREDUCE: the epilogue's peer all-reduce (same protocol and regions as
@@ -71,6 +94,7 @@ struct alignas(64) GemmArgs {
   __nv_bfloat16* ar_recv[kArMaxWorld];
   uint32_t* ar_flags[kArMaxWorld];
   DevStatus st;               // spin bound / lost-peer report (CGX_GEMM_ALLREDUCE)
+  unsigned long long* ntrace; // CGX_NODE_TRACE=1: replay timeline [entry min, ready max, exit max] ns
 };
 
 // ------------------------------------------------------------------ PTX wrappers
@@ -102,8 +126,53 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, ui
       "l"(tm), "r"(smem_u32(bar)), "r"(x), "r"(y)
       : "memory");
 }
-__device__ __forceinline__ void tma_prefetch_l2(const CUtensorMap* tm, int x, int y) {
-  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];\n" ::"l"(tm), "r"(x), "r"(y) : "memory");
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, uint64_t* bar, int x, int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(tm), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
+// Issue from a CONVERGED warp: every lane executes the helper and elect.sync picks the one lane that
+// issues. A tcgen05 / TMA instruction reached by one lane of a diverged warp is wrapped by the
+// compiler in an ELECT/BRA.U.ANY loop and costs ~2x the issue cycles (profiles/r02/
+// umma_rate_microbench.txt: 90-100 vs 45-50 cycles per 128x32x16 MMA).
+__device__ __forceinline__ void tma_load_3d_w(void* dst, const CUtensorMap* tm, uint64_t* bar, int x, int y, int z) {
+  asm volatile(
+      "{\n .reg .pred q;\n elect.sync _|q, 0xffffffff;\n"
+      " @q cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];\n}\n" ::"r"(
+          smem_u32(dst)),
+      "l"(tm), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx_w(uint64_t* b, uint32_t bytes) {
+  asm volatile("{\n .reg .pred q;\n elect.sync _|q, 0xffffffff;\n"
+               " @q mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n}\n" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_l2_3d(const CUtensorMap* tm, int x, int y, int z) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];\n" ::"l"(tm), "r"(x), "r"(y), "r"(z)
+               : "memory");
+}
+// kGemmADynamic: warp-wide. Copy the A tensor-map template into shared memory, replace its global
+// address, and publish it to this CTA's global workspace slot with the tensormap proxy release
+// (tensormap.cp_fenceproxy); the issuing lane then acquires it before its first TMA through it.
+__device__ __forceinline__ const CUtensorMap* build_dynamic_tmap(const CUtensorMap* tmpl, CUtensorMap* ws,
+                                                                 uint32_t* smem_tm, uint64_t addr, uint32_t lane) {
+  smem_tm[lane] = reinterpret_cast<const uint32_t*>(tmpl)[lane];     // 32 lanes x 4 B = 128 B
+  __syncwarp();
+  if (lane == 0)
+    asm volatile("tensormap.replace.tile.global_address.shared::cta.b1024.b64 [%0], %1;\n" ::"r"(smem_u32(smem_tm)),
+                 "l"(addr)
+                 : "memory");
+  __syncwarp();
+  asm volatile(
+      "tensormap.cp_fenceproxy.global.shared::cta.tensormap::generic.release.gpu.sync.aligned [%0], [%1], 128;\n" ::"l"(
+          ws),
+      "r"(smem_u32(smem_tm))
+      : "memory");
+  asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;\n" ::"l"(ws) : "memory");
+  return ws;
 }
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* tm) {
   asm volatile("prefetch.tensormap [%0];\n" ::"l"(tm) : "memory");
@@ -129,6 +198,17 @@ __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t a, uint64_t 
       "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
       " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
       "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_bf16_w(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p, q;\n elect.sync _|q, 0xffffffff;\n setp.ne.b32 p, %4, 0;\n"
+      " @q tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit_w(uint64_t* bar) {
+  asm volatile("{\n .reg .pred q;\n elect.sync _|q, 0xffffffff;\n"
+               " @q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(smem_u32(bar))
+               : "memory");
 }
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
@@ -244,7 +324,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
   constexpr uint32_t kABytes = kBM * kBK * 2;     // 16 KiB
   constexpr uint32_t kBBytes = BN * kBK * 2;
   constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
-  const int kStages = (int)a.stages;
+  const uint32_t GA = a.ga, RA = a.ra, GW = a.gw, RW = a.rw;
   constexpr uint32_t kRowF = BN + 4;              // partial-tile row stride (floats): 16-B aligned, bank-spread
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-B alignment (SWIZZLE_128B) by offsetting the __shared__ array itself, so every derived
@@ -253,21 +333,27 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
   const uint32_t S = a.split;
   const uint32_t z = blockIdx.z;                   // cluster (1,1,S) over gridDim.z == S: rank == z
   const uint32_t rows_max = split_rows_max(S);
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + kStages * kABytes;
-  // The operand ring doubles as the epilogue staging area once the MMAs are done: the fp32
+  uint8_t* sA = smem;                              // [RA][GA][128 x 128 B]
+  uint8_t* sB = smem + RA * GA * kABytes;          // [RW][GW][BN x 128 B]
+  // The operand rings double as the epilogue staging area once the MMAs are done: the fp32
   // partial tile [128][kRowF] (split-K).
-  const uint32_t ring_bytes = kStages * (kABytes + kBBytes);
+  const uint32_t ring_bytes = RA * GA * kABytes + RW * GW * kBBytes;
   const uint32_t stage_bytes = S > 1 ? 128u * kRowF * 4u : 0u;
   float* recv = reinterpret_cast<float*>(smem + (ring_bytes > stage_bytes ? ring_bytes : stage_bytes));  // [S][rows_max][kRowF]
   float* sbias = recv + (S > 1 ? S * rows_max * kRowF : 0);                     // [BN] fp32 bias slice
-  uint64_t* full = reinterpret_cast<uint64_t*>(sbias + BN);
-  uint64_t* empty = full + kStages;
-  uint64_t* tmem_full = empty + kStages;
+  uint64_t* full_a = reinterpret_cast<uint64_t*>(sbias + BN);
+  uint64_t* empty_a = full_a + RA;
+  uint64_t* full_w = empty_a + RA;
+  uint64_t* empty_w = full_w + RW;
+  uint64_t* tmem_full = empty_w + RW;
   uint64_t* recv_full = tmem_full + 1;
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(recv_full + 1);
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(recv_full + 1);   // [0] TMEM address, [1] AR generation
+  uint32_t* s_tm = reinterpret_cast<uint32_t*>((reinterpret_cast<uintptr_t>(s_tmem + 4) + 127) & ~uintptr_t(127));
 
-  if (threadIdx.x == 0) trace_at(a, 0);
+  if (threadIdx.x == 0) {
+    trace_at(a, 0);
+    node_stamp(a.ntrace, 0);
+  }
   // an all-reducing GEMM never triggers early: no successor may sit resident while it waits for
   // its peers (dependents then launch at its completion)
   constexpr bool ar = AR;                        // CGX_GEMM_ALLREDUCE instantiation
@@ -279,14 +365,20 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
   const int nk = (int)(a.K / kBK);
   const int kbase = (int)((uint32_t)nk * z / S);
   const int kps = (int)((uint32_t)nk * (z + 1) / S) - kbase;   // k-blocks of this split (>= 1)
+  const int nga = (kps + (int)GA - 1) / (int)GA, ngw = (kps + (int)GW - 1) / (int)GW;   // operand groups
   const uint32_t my_lo = split_row_lo(z, S), my_rows = split_row_lo(z + 1, S) - my_lo;
+  const bool dyn_a = a.flags & kGemmADynamic;
 
   if (warp == 0 && lane == 0) {
-    prefetch_tmap(&a.tmA);
+    if (!dyn_a) prefetch_tmap(&a.tmA);
     prefetch_tmap(&a.tmB);
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+    for (uint32_t s = 0; s < RA; ++s) {
+      mbar_init(&full_a[s], 1);
+      mbar_init(&empty_a[s], 1);
+    }
+    for (uint32_t s = 0; s < RW; ++s) {
+      mbar_init(&full_w[s], 1);
+      mbar_init(&empty_w[s], 1);
     }
     mbar_init(tmem_full, 1);
     if (S > 1) {
@@ -309,48 +401,109 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
   const uint32_t tmem = *s_tmem;
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ---- TMA producer. Weights first (independent of the predecessor), then wait, then A.
-      const bool w_late = a.flags & kGemmWAfterWait;
-      if (w_late) pdl_wait();
-      for (int i = 0; i < kps; ++i) tma_prefetch_l2(&a.tmB, (kbase + i) * kBK, n0);
-      const int pre = kps < kStages ? kps : kStages;
-      for (int i = 0; i < pre; ++i) {
-        mbar_expect_tx(&full[i], kABytes + kBBytes);
-        tma_load_2d(sB + i * kBBytes, &a.tmB, &full[i], (kbase + i) * kBK, n0);
-      }
-      if (!w_late) pdl_wait();
-      if (late_trigger) pdl_trigger();
-      for (int i = 0; i < pre; ++i) tma_load_2d(sA + i * kABytes, &a.tmA, &full[i], (kbase + i) * kBK, m0);
-      for (int i = pre; i < kps; ++i) {
-        const int s = i % kStages;
-        const uint32_t ph = (uint32_t)(i / kStages) & 1u;
-        mbar_wait(&empty[s], ph ^ 1u);
-        mbar_expect_tx(&full[s], kABytes + kBBytes);
-        tma_load_2d(sB + s * kBBytes, &a.tmB, &full[s], (kbase + i) * kBK, n0);
-        tma_load_2d(sA + s * kABytes, &a.tmA, &full[s], (kbase + i) * kBK, m0);
+    // ---- TMA producer (lane 0; the whole warp builds a dynamic A tensor map). Weights first
+    // (independent of the predecessor), then the PDL wait, then A. One 3-D box per operand per
+    // group of G k-blocks; the box bytes always count in full (a short last group's extra k-blocks
+    // are fetched, or zero-filled past K, and never multiplied).
+    const CUtensorMap* tmA = &a.tmA;
+    const bool dyn_late = dyn_a && (a.flags & kGemmADynAfterWait);
+    auto build_a = [&]() {
+      // the replay's A address: the pointer table (written before the graph's first consumer; a
+      // GEMM never is the first consumer after a root table writer) or the patched a_ptr field
+      uint64_t addr = 0;
+      if (lane == 0) addr = a.ta >= 0 ? ld_table(a.table + a.ta) : reinterpret_cast<uint64_t>(a.a_ptr);
+      addr = __shfl_sync(0xffffffffu, addr, 0);
+      const uint32_t cta_lin = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+      tmA = build_dynamic_tmap(&a.tmA, a.tm_ws + cta_lin, s_tm, addr, lane);
+    };
+    if (dyn_a && !dyn_late) build_a();
+    // the whole warp runs the producer loop (converged: elect.sync picks the issuing lane)
+    const int pre_a = nga < (int)RA ? nga : (int)RA, pre_w = ngw < (int)RW ? ngw : (int)RW;
+    const bool w_late = a.flags & kGemmWAfterWait;
+    if (w_late) pdl_wait();
+    if (lane == 0)
+      for (int g = pre_w; g < ngw; ++g) tma_prefetch_l2_3d(&a.tmB, 0, n0, kbase + g * (int)GW);   // beyond the ring
+    __syncwarp();
+    for (int g = 0; g < pre_w; ++g) {
+      mbar_expect_tx_w(&full_w[g], GW * kBBytes);
+      tma_load_3d_w(sB + g * GW * kBBytes, &a.tmB, &full_w[g], 0, n0, kbase + g * (int)GW);
+    }
+    if (!w_late) pdl_wait();
+    if (lane == 0) node_stamp(a.ntrace, 1);
+    if (dyn_late) build_a();                        // every lane has passed the wait
+    if (late_trigger) pdl_trigger();
+    for (int g = 0; g < pre_a; ++g) {               // the whole A slice (one-shot) or the first RA groups
+      mbar_expect_tx_w(&full_a[g], GA * kABytes);
+      tma_load_3d_w(sA + g * GA * kABytes, tmA, &full_a[g], 0, m0, kbase + g * (int)GA);
+    }
+    if (lane == 0) trace_at(a, 11);
+    // refills in the order the MMAs consume k-blocks (deadlock-free: each waits for an earlier
+    // k-block's release); slot / phase counters advance incrementally (no divisions)
+    // (the first refill of a ring reuses slot 0 and waits for its release #1, i.e. parity 0)
+    int ia = pre_a, iw = pre_w, sa = 0, sw = 0;
+    uint32_t pha = 0u, phw = 0u;
+    while (ia < nga || iw < ngw) {
+      const int ka = ia < nga ? ia * (int)GA : 1 << 30, kw = iw < ngw ? iw * (int)GW : 1 << 30;
+      if (ka <= kw) {
+        mbar_wait(&empty_a[sa], pha);
+        mbar_expect_tx_w(&full_a[sa], GA * kABytes);
+        tma_load_3d_w(sA + sa * GA * kABytes, tmA, &full_a[sa], 0, m0, kbase + ia * (int)GA);
+        ++ia;
+        if (++sa == (int)RA) {
+          sa = 0;
+          pha ^= 1u;
+        }
+      } else {
+        mbar_wait(&empty_w[sw], phw);
+        mbar_expect_tx_w(&full_w[sw], GW * kBBytes);
+        tma_load_3d_w(sB + sw * GW * kBBytes, &a.tmB, &full_w[sw], 0, n0, kbase + iw * (int)GW);
+        ++iw;
+        if (++sw == (int)RW) {
+          sw = 0;
+          phw ^= 1u;
+        }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---- single-thread MMA issuer
-      constexpr uint32_t idesc = umma_idesc(kBM, BN);
-      for (int i = 0; i < kps; ++i) {
-        const int s = i % kStages;
-        const uint32_t ph = (uint32_t)(i / kStages) & 1u;
-        mbar_wait(&full[s], ph);
-        if (i == 0) trace_at(a, 2);
-        tc_fence_after();
-        const uint64_t da = umma_desc_sw128(smem_u32(sA + s * kABytes));
-        const uint64_t db = umma_desc_sw128(smem_u32(sB + s * kBBytes));
+    // ---- MMA issuer: the whole warp runs the loop, elect.sync issues (k-block by k-block, 4
+    // UMMA_K steps each, waiting for the A and W groups as they land; a group's slot is released
+    // with a commit when it will be refilled)
+    constexpr uint32_t idesc = umma_idesc(kBM, BN);
+    int sa = 0, sw = 0, oa = 0, ow = 0, ia = 0, iw = 0;
+    uint32_t pha = 0u, phw = 0u;
+    for (int kb = 0; kb < kps; ++kb) {
+      if (oa == 0) mbar_wait(&full_a[sa], pha);
+      if (ow == 0) mbar_wait(&full_w[sw], phw);
+      if (kb == 0 && lane == 0) trace_at(a, 2);
+      tc_fence_after();
+      const uint64_t da = umma_desc_sw128(smem_u32(sA + (sa * GA + oa) * kABytes));
+      const uint64_t db = umma_desc_sw128(smem_u32(sB + (sw * GW + ow) * kBBytes));
 #pragma unroll
-        for (int k = 0; k < kBK / 16; ++k)   // UMMA_K = 16 bf16 = 32 B -> +2 in the >>4 address field
-          umma_bf16(tmem, da + 2 * k, db + 2 * k, idesc, (i | k) != 0);
-        umma_commit(&empty[s]);
+      for (int k = 0; k < kBK / 16; ++k)   // UMMA_K = 16 bf16 = 32 B -> +2 in the >>4 address field
+        umma_bf16_w(tmem, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+      const bool last = kb + 1 == kps;
+      if (++oa == (int)GA || last) {
+        if (ia + (int)RA < nga) umma_commit_w(&empty_a[sa]);
+        oa = 0;
+        ++ia;
+        if (++sa == (int)RA) {
+          sa = 0;
+          pha ^= 1u;
+        }
       }
-      umma_commit(tmem_full);
-      trace_at(a, 3);
+      if (++ow == (int)GW || last) {
+        if (iw + (int)RW < ngw) umma_commit_w(&empty_w[sw]);
+        ow = 0;
+        ++iw;
+        if (++sw == (int)RW) {
+          sw = 0;
+          phw ^= 1u;
+        }
+      }
     }
+    if (lane == 0) trace_at(a, 15);
+    umma_commit_w(tmem_full);
+    if (lane == 0) trace_at(a, 3);
   } else {
     // ---- epilogue warps (128 threads): TMEM -> registers -> [split-K push/reduce] -> epilogue.
     // Everything the epilogue reads from global memory is fetched BEFORE the accumulator is ready:
@@ -579,7 +732,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
   }
   tc_fence_before();
   __syncthreads();
-  if (threadIdx.x == 0) trace_at(a, 7);
+  if (threadIdx.x == 0) {
+    trace_at(a, 7);
+    node_stamp(a.ntrace, 2);
+  }
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(kTmemCols));
@@ -603,6 +759,7 @@ __device__ __forceinline__ float bf16hi(uint32_t u) { return __uint_as_float(u &
 template <int R, int kGvKV>
 __global__ void __launch_bounds__(kGvWarps * 32) k_gemv_bf16(const __grid_constant__ GemmArgs a) {
   const bool late_trigger = a.flags & kGemmTriggerAfterWait;
+  if (threadIdx.x == 0) node_stamp(a.ntrace, 0);
   if (!late_trigger) pdl_trigger();
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t n0 = (blockIdx.x * kGvWarps + warp) * R;     // this warp's first output column
@@ -620,6 +777,9 @@ __global__ void __launch_bounds__(kGvWarps * 32) k_gemv_bf16(const __grid_consta
     }
   if (!w_late) pdl_wait();
   if (late_trigger) pdl_trigger();
+  if (threadIdx.x == 0) node_stamp(a.ntrace, 1);
+  // A: the patched / direct a_ptr, or table[ta] for an EXTERNAL A under INDIRECT (after the wait)
+  const __nv_bfloat16* ap = a.ta >= 0 ? reinterpret_cast<const __nv_bfloat16*>(ld_table(a.table + a.ta)) : a.a_ptr;
   float acc[R][kGvMaxM];
 #pragma unroll
   for (int r = 0; r < R; ++r)
@@ -627,7 +787,7 @@ __global__ void __launch_bounds__(kGvWarps * 32) k_gemv_bf16(const __grid_consta
     for (int m = 0; m < kGvMaxM; ++m) acc[r][m] = 0.f;
   for (uint32_t m = 0; m < a.M; ++m) {
     uint4 x[kGvKV];
-    const uint4* ar = reinterpret_cast<const uint4*>(a.a_ptr + (size_t)m * a.K);
+    const uint4* ar = reinterpret_cast<const uint4*>(ap + (size_t)m * a.K);
 #pragma unroll
     for (int i = 0; i < kGvKV; ++i) {
       const uint32_t v = lane + 32u * i;
@@ -655,6 +815,10 @@ __global__ void __launch_bounds__(kGvWarps * 32) k_gemv_bf16(const __grid_consta
       for (int mm = 0; mm < kGvMaxM; ++mm)
         if (mm == (int)m) acc[r][mm] = t;
     }
+  }
+  if (a.ntrace) {
+    __syncthreads();
+    if (threadIdx.x == 0) node_stamp(a.ntrace, 2);   // (approximately: before lane 0's epilogue stores)
   }
   if (lane != 0) return;
   const bool has_bias = a.flags & CGX_GEMM_BIAS, gelu = a.flags & CGX_GEMM_GELU;
@@ -693,12 +857,16 @@ static int get_encode() {
   return g_encode ? CGX_OK : CGX_E_CUDA;
 }
 
-static int encode_kmajor(CUtensorMap* tm, const void* base, uint64_t rows, uint64_t K, uint32_t box_rows) {
-  cuuint64_t dims[2] = {K, rows};
-  cuuint64_t strides[1] = {K * 2};
-  cuuint32_t box[2] = {(cuuint32_t)kBK, box_rows};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = g_encode(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+// K-major operand [rows, K] bf16 viewed as 3-D {64 (k in block), rows, K/64 (k-block)} with strides
+// {K * 2 B, 128 B}: a box {64, box_rows, G} lands in shared memory as G stacked [box_rows][128 B]
+// SW128 tiles (the swizzle phase repeats every 8 rows; box_rows % 8 == 0).
+static int encode_kmajor(CUtensorMap* tm, const void* base, uint64_t rows, uint64_t K, uint32_t box_rows,
+                         uint32_t group) {
+  cuuint64_t dims[3] = {(cuuint64_t)kBK, rows, K / kBK};
+  cuuint64_t strides[2] = {K * 2, (cuuint64_t)kBK * 2};
+  cuuint32_t box[3] = {(cuuint32_t)kBK, box_rows, group};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = g_encode(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? CGX_OK : CGX_E_CUDA;
@@ -714,21 +882,50 @@ static int encode_kmajor(CUtensorMap* tm, const void* base, uint64_t rows, uint6
 // per split. CGX_GEMM_TILING / CGX_GEMM_BN / CGX_GEMM_SPLIT pin a tiling for measurement.
 static uint32_t split_rows_max_h(uint32_t S) { return (128u + S - 1) / S; }
 
-static size_t smem_bytes(int bn, uint32_t S, uint32_t stages) {
-  const size_t recv = S > 1 ? (size_t)S * split_rows_max_h(S) * (bn + 4) * 4 : 0;
-  size_t ring = stages * (size_t)(kBM * kBK * 2 + bn * kBK * 2);
+static size_t recv_bytes(int bn, uint32_t S) { return S > 1 ? (size_t)S * split_rows_max_h(S) * (bn + 4) * 4 : 0; }
+struct GemmPipes {
+  uint32_t ga, ra, gw, rw;
+};
+static size_t smem_bytes(int bn, uint32_t S, const GemmPipes& p) {
+  size_t ring = (size_t)p.ra * p.ga * kBM * kBK * 2 + (size_t)p.rw * p.gw * bn * kBK * 2;
   const size_t stage = S > 1 ? (size_t)128 * (bn + 4) * 4 : 0;
   if (stage > ring) ring = stage;
-  return 1024 + ring + recv + bn * 4 + (2 * stages + 2) * 8 + 16;
+  // align + rings + split receive slots + bias slice + barriers + TMEM/AR words + dynamic tensor map
+  return 1024 + ring + recv_bytes(bn, S) + bn * 4 + (2 * p.ra + 2 * p.rw + 2) * 8 + 16 + 256;
 }
-static uint32_t ring_stages(uint32_t nk, uint32_t S) {
-  static const uint32_t cap = [] {   // CGX_GEMM_STAGES: measurement knob (1..kMaxStages)
-    const char* v = getenv("CGX_GEMM_STAGES");
-    const int n = v ? atoi(v) : kMaxStages;
-    return (uint32_t)(n >= 1 && n <= kMaxStages ? n : kMaxStages);
-  }();
+// Operand pipelines: A whole (one-shot, one box per k-block so the MMAs start with the first) when
+// its K slice fits beside a W ring of >= 2 k-blocks, else an A ring of 4-k-block boxes; W per
+// k-block through the rest of the budget (>= 2 slots). CGX_GEMM_PIPES="GA/RA/GW/RW" pins all shapes,
+// CGX_GEMM_TILING="NxK=BN/S/GA/RA/GW/RW" one shape (measurement knobs).
+static GemmPipes pick_pipes(int bn, uint32_t S, uint32_t nk) {
+  // Lean rings (r02 sweeps, profiles/r02/gemm_pipes_sweep.txt): groups of 2 k-blocks, 2 groups of A
+  // and 2 of W resident (80 KiB at BN = 32), so two GEMM CTAs fit on one SM and a node's CTAs can
+  // become resident — and stream their weights before griddepcontrol.wait — while its predecessor
+  // still runs. Holding the whole A slice (one-shot, ~200 KiB) made each GEMM ~1 us shorter alone
+  // but cost as much in launch gaps in the deployed chain (FC1 -> FC2: 2.9-3.7 us), and the
+  // per-CTA floor is the tcgen05 issue rate (~50-60 cycles per 128 x 32 x 16 MMA), not the loads.
   const uint32_t kps = (nk + S - 1) / S;
-  return kps < cap ? kps : cap;
+  GemmPipes p{1, 1, 1, 1};
+  p.ga = p.gw = kps < 2 ? kps : 2;
+  const uint32_t ng = (kps + p.ga - 1) / p.ga;
+  p.ra = p.rw = ng < 2 ? ng : 2;
+  (void)bn;
+  return p;
+}
+
+static bool parse_pipes(const char* s, GemmPipes* p) {
+  int ga = 0, ra = 0, gw = 0, rw = 0;
+  if (sscanf(s, "%d/%d/%d/%d", &ga, &ra, &gw, &rw) != 4) return false;
+  if (ga < 1 || ga > kMaxGroupKb || gw < 1 || gw > kMaxGroupKb || ra < 1 || rw < 1) return false;
+  *p = GemmPipes{(uint32_t)ga, (uint32_t)ra, (uint32_t)gw, (uint32_t)rw};
+  return true;
+}
+static void clamp_pipes(GemmPipes* p, uint32_t kps) {
+  if (p->ga > kps) p->ga = kps;
+  if (p->gw > kps) p->gw = kps;
+  const uint32_t nga = (kps + p->ga - 1) / p->ga, ngw = (kps + p->gw - 1) / p->gw;
+  if (p->ra > nga) p->ra = nga;
+  if (p->rw > ngw) p->rw = ngw;
 }
 
 static void pick_tiling(uint32_t M, uint32_t N, uint32_t K, int* bn_out, uint32_t* split_out) {
@@ -776,7 +973,11 @@ template <int BN, bool AR>
 static const void* setup_kernel() {
   // per call (exec build time, cheap): function attributes belong to the current device's context.
   // Headroom below the 227 KiB per-block limit for the kernel's static shared memory.
-  cudaFuncSetAttribute(k_gemm_bf16<BN, AR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  static const int attr = [] {   // CGX_GEMM_SMEM_ATTR: measurement knob (bytes)
+    const char* v = getenv("CGX_GEMM_SMEM_ATTR");
+    return v ? atoi(v) : (int)kSmemLimit;
+  }();
+  cudaFuncSetAttribute(k_gemm_bf16<BN, AR>, cudaFuncAttributeMaxDynamicSharedMemorySize, attr);
   cudaFuncSetAttribute(k_gemm_bf16<BN, AR>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   return (const void*)k_gemm_bf16<BN, AR>;
 }
@@ -807,6 +1008,24 @@ uint32_t decoder_gemm_ctas(const void* args, dim3 grid) {
   return grid.x * grid.y * grid.z;
 }
 
+void decoder_gemm_set_a_dynamic(void* args, const uint64_t* table, int32_t idx, void* tm_ws, bool after_wait) {
+  GemmArgs* g = static_cast<GemmArgs*>(args);
+  g->flags |= kGemmADynamic | (after_wait ? kGemmADynAfterWait : 0u);
+  if (table) g->table = table;
+  g->ta = idx;
+  g->tm_ws = static_cast<CUtensorMap*>(tm_ws);
+  if (idx >= 0) g->a_ptr = nullptr;
+}
+size_t decoder_gemm_a_field(size_t* tidx_off) {
+  *tidx_off = offsetof(GemmArgs, ta);
+  return offsetof(GemmArgs, a_ptr);
+}
+
+void decoder_gemm_set_table(void* args, const uint64_t* table) {
+  GemmArgs* g = static_cast<GemmArgs*>(args);
+  if (g->ta >= 0 || g->tres >= 0) g->table = table;
+}
+
 void decoder_gemm_set_residual_table(void* args, const uint64_t* table, int32_t idx) {
   static_cast<GemmArgs*>(args)->table = table;
   static_cast<GemmArgs*>(args)->tres = idx;
@@ -819,6 +1038,10 @@ size_t decoder_gemm_residual_field(size_t* tidx_off) {
 
 void decoder_gemm_set_status(void* args, uint32_t* word, uint64_t timeout_ns) {
   static_cast<GemmArgs*>(args)->st = DevStatus{word, timeout_ns};
+}
+
+void decoder_gemm_set_node_trace(void* args, unsigned long long* nt) {
+  static_cast<GemmArgs*>(args)->ntrace = nt;
 }
 
 void decoder_gemm_set_trace(void* args, unsigned long long* trace) {
@@ -871,22 +1094,41 @@ int decoder_gemm_build(uint32_t M, uint32_t N, uint32_t K, uint32_t flags, const
     g->flags = flags;
     g->split = 1;
     g->tres = -1;
+    g->ta = -1;
     return CGX_OK;
   }
   int bn = 0;
   uint32_t sp = 1;
   pick_tiling(M, N, K, &bn, &sp);
   *argbytes = sizeof(GemmArgs);
-  const uint32_t stages = ring_stages(K / kBK, sp);
+  GemmPipes pp = pick_pipes(bn, sp, K / kBK);
+  if (const char* v = getenv("CGX_GEMM_PIPES")) parse_pipes(v, &pp);
+  if (const char* t = getenv("CGX_GEMM_TILING")) {   // "NxK=BN/S/GA/RA/GW/RW" pins this shape's pipes
+    char key[32];
+    snprintf(key, sizeof key, "%ux%u=", N, K);
+    if (const char* p = strstr(t, key)) {
+      int b2 = 0, s2 = 0;
+      const char* q = p + strlen(key);
+      if (sscanf(q, "%d/%d/", &b2, &s2) == 2) {
+        const char* r = strchr(strchr(q, '/') + 1, '/');
+        if (r) parse_pipes(r + 1, &pp);
+      }
+    }
+  }
+  clamp_pipes(&pp, (K / kBK + sp - 1) / sp);
   *grid = dim3(N / bn, (M + kBM - 1) / kBM, sp);
   *block = dim3(kGemmThreads);
-  *smem = smem_bytes(bn, sp, stages);
+  *smem = smem_bytes(bn, sp, pp);
+  if (*smem > kSmemLimit) return CGX_E_UNSUPPORTED;
   *func = kernel_for(bn, (flags & CGX_GEMM_ALLREDUCE) != 0);
   if (!args_out) return CGX_OK;
   if (get_encode() != CGX_OK) return CGX_E_CUDA;
   GemmArgs* g = static_cast<GemmArgs*>(args_out);
-  if (encode_kmajor(&g->tmA, A, M, K, kBM) != CGX_OK) return CGX_E_CUDA;
-  if (encode_kmajor(&g->tmB, W, N, K, (uint32_t)bn) != CGX_OK) return CGX_E_CUDA;
+  memset(g, 0, sizeof(GemmArgs));
+  // an EXTERNAL A has no address before the first bind: encode the template with any aligned
+  // address (the kernel replaces it, kGemmADynamic)
+  if (encode_kmajor(&g->tmA, A ? A : W, M, K, kBM, pp.ga) != CGX_OK) return CGX_E_CUDA;
+  if (encode_kmajor(&g->tmB, W, N, K, (uint32_t)bn, pp.gw) != CGX_OK) return CGX_E_CUDA;
   g->bias = static_cast<const __nv_bfloat16*>(bias);
   g->residual = static_cast<const __nv_bfloat16*>(residual);
   g->out = static_cast<__nv_bfloat16*>(out);
@@ -897,10 +1139,15 @@ int decoder_gemm_build(uint32_t M, uint32_t N, uint32_t K, uint32_t flags, const
   g->K = K;
   g->flags = flags;
   g->split = sp;
-  g->stages = stages;
+  if (getenv("CGX_GEMM_FENCE_ON_WAIT")) g->flags |= kGemmFenceOnWait;
+  g->ga = pp.ga;
+  g->ra = pp.ra;
+  g->gw = pp.gw;
+  g->rw = pp.rw;
   g->trace = nullptr;
   g->table = nullptr;
   g->tres = -1;
+  g->ta = -1;
   g->a_ptr = static_cast<const __nv_bfloat16*>(A);
   g->w_ptr = static_cast<const __nv_bfloat16*>(W);
   return CGX_OK;

@@ -520,6 +520,7 @@ struct cgx_exec {
   // after another: a GEMM writes its partials only after its griddepcontrol.wait)
   void* gemm_ws = nullptr;
   void* gemm_cnt = nullptr;
+  std::vector<void*> gemm_tm_ws;  // per-CTA A tensor maps of GEMMs with an EXTERNAL A (kGemmADynamic)
   size_t gemm_cnt_off = 0;        // next free counter bytes while building launches
   int t5_pub = 0;                 // T5: position of the table-publishing launch
   unsigned long long* d_trace = nullptr;   // CGX_NODE_TRACE=1: [launch][3] ns stamps
@@ -748,17 +749,15 @@ static int build_launch(cgx_exec* e, int k, Launch& l) {
       return CGX_OK;
     }
     case CGX_OP_GEMM_BF16: {
-      // EXTERNAL operands: A is read through a TMA tensor map (encoded at capture) and the weights
-      // and bias are STATIC by construction, so only the residual can be rebound; under INDIRECT
-      // the epilogue reads its base pointer from the table, in patch modes the pointer field is
-      // patched like any other, under COPY it is the placeholder
+      // EXTERNAL operands. A is read through a TMA tensor map: under COPY it is encoded at capture
+      // with the placeholder; under INDIRECT and the patch modes the kernel rebuilds this CTA's copy
+      // of the map from table[j] / the patched a_ptr field (tensormap.replace, kGemmADynamic) — PI
+      // through the TMA descriptor, no data copy. The residual: table / patched field / placeholder.
+      // Weights and bias are STATIC by construction.
       const bool res_ext = (n.attr.flags & CGX_GEMM_RESIDUAL) && is_ext(n.in[3]);
-      for (int i = 0; i < 3; ++i)
-        if (is_ext(n.in[i])) {
-          if (i == 0 && !indirect && !patch) continue;                   // COPY: placeholder
-          return fail(CGX_E_UNSUPPORTED, i == 0 ? "gemm: an EXTERNAL A operand needs a rebuilt tensor map (COPY arm only)"
-                                                : "gemm: external weights/bias");
-        }
+      const bool a_ext = is_ext(n.in[0]) && (indirect || patch);
+      for (int i = 1; i < 3; ++i)
+        if (is_ext(n.in[i])) return fail(CGX_E_UNSUPPORTED, "gemm: external weights/bias");
       void* A = slot_ptr(n.in[0]);
       void* W = slot_ptr(n.in[1]);
       void* bias = slot_ptr(n.in[2]);
@@ -806,6 +805,22 @@ static int build_launch(cgx_exec* e, int k, Launch& l) {
                                    (uint32_t)n_ar, peer_slot_elems(c->peer_max_elems), c->peer_counters,
                                    recv.data(), flg.data());
         decoder_gemm_set_status(l.args.p, e->d_status, e->spin_timeout_ns);
+      }
+      if (a_ext) {
+        const int j = c->slots[n.in[0]].ext_j;
+        const size_t ws_bytes = (size_t)l.grid.x * l.grid.y * l.grid.z * 128;
+        void* ws = nullptr;
+        CK(cudaMalloc(&ws, ws_bytes));
+        e->gemm_tm_ws.push_back(ws);
+        const bool late = mode == CGX_MODE_EAGER;
+        if (indirect) {
+          decoder_gemm_set_a_dynamic(l.args.p, e->d_table, j, ws, late);
+        } else {
+          decoder_gemm_set_a_dynamic(l.args.p, nullptr, -1, ws, late);
+          size_t tidx = 0;
+          const size_t off = decoder_gemm_a_field(&tidx);
+          l.ext.push_back({off, tidx, j});
+        }
       }
       if (res_ext) {
         const int j = c->slots[n.in[3]].ext_j;
@@ -1477,9 +1492,8 @@ static int capture_graph(cgx_exec* e, int gi) {
                                   e->c->nodes[l.node].op == CGX_OP_LAYERNORM))
         memcpy(l.args.p, &tab, sizeof(tab));
       const Node& gn = e->c->nodes[l.node];
-      if (l.kind == LK_KERNEL && gn.op == CGX_OP_GEMM_BF16 && (gn.attr.flags & CGX_GEMM_RESIDUAL) &&
-          e->c->slots[gn.in[3]].kind == CGX_SLOT_EXTERNAL)
-        decoder_gemm_set_residual_table(l.args.p, tab, e->c->slots[gn.in[3]].ext_j);
+      // a GEMM reads the table for an EXTERNAL A (its rebuilt tensor map) and / or residual
+      if (l.kind == LK_KERNEL && gn.op == CGX_OP_GEMM_BF16) decoder_gemm_set_table(l.args.p, tab);
     }
   }
   CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
@@ -1559,6 +1573,7 @@ static void exec_free(cgx_exec* e) {
   if (e->ph_arena) cudaFree(e->ph_arena);
   if (e->gemm_ws) cudaFree(e->gemm_ws);
   if (e->gemm_cnt) cudaFree(e->gemm_cnt);
+  for (void* p : e->gemm_tm_ws) cudaFree(p);
   if (e->df_mem) cudaFree(e->df_mem);
   if (e->dl_ge) cudaGraphExecDestroy(e->dl_ge);
   if (e->dl_g) cudaGraphDestroy(e->dl_g);
@@ -1667,9 +1682,15 @@ extern "C" int cgx_exec_create_ex(cgx_chain* c, const cgx_exec_opts* opts, void*
     cudaError_t ce = cudaMalloc(&e->d_trace, nb);
     if (ce != cudaSuccess) return bail(cuda_fail(ce, "node trace", __LINE__));
     node_trace_reset(e);
-    for (size_t p = 0; p < e->L.size(); ++p)
-      if (e->L[p].kind == LK_KERNEL && df_capable(c->nodes[e->L[p].node], c->slots[c->nodes[e->L[p].node].out].dtype))
-        argp<ElemArgs>(e->L[p])->trace = e->d_trace + 3 * p;
+    for (size_t p = 0; p < e->L.size(); ++p) {
+      if (e->L[p].kind != LK_KERNEL) continue;
+      const Node& tn = c->nodes[e->L[p].node];
+      unsigned long long* nt = e->d_trace + 3 * p;
+      if (uses_elem_args(tn.op)) argp<ElemArgs>(e->L[p])->trace = nt;
+      else if (tn.op == CGX_OP_LAYERNORM) argp<LnArgs>(e->L[p])->ntrace = nt;
+      else if (tn.op == CGX_OP_ATTN_CAUSAL) argp<AttnArgs>(e->L[p])->ntrace = nt;
+      else if (tn.op == CGX_OP_GEMM_BF16) decoder_gemm_set_node_trace(e->L[p].args.p, nt);
+    }
   }
   if (o.mode != CGX_MODE_EAGER) {
     cudaError_t ce = cudaStreamCreateWithFlags(&e->cs, cudaStreamNonBlocking);

@@ -203,6 +203,11 @@ def c3_chain(T: int = 128, n_layers: int = 12, tp: int = 1, rank: int = 0,
                       ("h1", T * d), ("a2", T * d), ("f", T * fl), ("g", T * d), ("h2", T * d)):
             slots.append(SlotSpec(p + nm, INTERNAL, "bf16", n))   # (o, g stay when fused: same slot
                                                                     # indices -> same seeded weights)
+        # TP: the all-reduced sums get their own slots (not in place), so every rank's partial and
+        # the reduced value both stay observable for the node-local parity check
+        o_sum, g_sum = (p + "o_sum", p + "g_sum") if tp > 1 and not fuse_ar else (p + "o", p + "g")
+        if tp > 1 and not fuse_ar:
+            slots += [SlotSpec(o_sum, INTERNAL, "bf16", T * d), SlotSpec(g_sum, INTERNAL, "bf16", T * d)]
         if fuse_residual:
             nodes += [
                 NodeSpec("LAYERNORM", (h, p + "ln1_g", p + "ln1_b"), p + "a",
@@ -235,9 +240,9 @@ def c3_chain(T: int = 128, n_layers: int = 12, tp: int = 1, rank: int = 0,
                       "gelu": False, "allreduce": fuse_ar}),
         ]
         if tp > 1 and not fuse_ar:
-            nodes.append(NodeSpec("ALLREDUCE_SUM", (p + "o",), p + "o", {"n": T * d}))
+            nodes.append(NodeSpec("ALLREDUCE_SUM", (p + "o",), o_sum, {"n": T * d}))
         nodes += [
-            NodeSpec("ADD", (h, p + "o"), p + "h1", {"n": T * d}),
+            NodeSpec("ADD", (h, o_sum), p + "h1", {"n": T * d}),
             NodeSpec("LAYERNORM", (p + "h1", p + "ln2_g", p + "ln2_b"), p + "a2",
                      {"rows": T, "cols": d, "eps": eps}),
             NodeSpec("GEMM_BF16", (p + "a2", p + "w_fc1", p + "b_fc1"), p + "f",
@@ -247,8 +252,8 @@ def c3_chain(T: int = 128, n_layers: int = 12, tp: int = 1, rank: int = 0,
                       "gelu": False, "allreduce": fuse_ar}),
         ]
         if tp > 1 and not fuse_ar:
-            nodes.append(NodeSpec("ALLREDUCE_SUM", (p + "g",), p + "g", {"n": T * d}))
-        nodes.append(NodeSpec("ADD", (p + "h1", p + "g"), p + "h2", {"n": T * d}))
+            nodes.append(NodeSpec("ALLREDUCE_SUM", (p + "g",), g_sum, {"n": T * d}))
+        nodes.append(NodeSpec("ADD", (p + "h1", g_sum), p + "h2", {"n": T * d}))
         h = p + "h2"
     name = f"C3_T{T}_L{n_layers}" if tp == 1 else f"C5_T{T}_L{n_layers}_tp{tp}_r{rank}"
     if fuse_residual:
@@ -261,11 +266,11 @@ def c3_chain(T: int = 128, n_layers: int = 12, tp: int = 1, rank: int = 0,
 # ----------------------------------------------------------------------------- training-shaped (NEXT-4)
 
 def mlp_train_chain(T: int = 128, d: int = 768, dff: int = 3072, n_blocks: int = 6,
-                    lr: float = 0.5) -> ChainSpec:
+                    lr: float = 0.5, stage_x: bool = False) -> ChainSpec:
     """A training step of a stack of GPT-2-shaped MLP blocks (SURVEY §8(f) NEXT-4 "training-shaped
     (fwd+bwd) chain", P:L694 DGPT2-T), bf16, batch T tokens, no biases, MSE loss:
 
-      forward per block l (a_0 = X, staged by a COPY node):  pre_l = a_l W1_l^T;  h_l = GELU(pre_l);  a_{l+1} = h_l W2_l^T
+      forward per block l (a_0 = X):  pre_l = a_l W1_l^T;  h_l = GELU(pre_l);  a_{l+1} = h_l W2_l^T
       loss gradient:                  dy = (a_L - target) * 2 / (T d)
       backward per block (l = L-1..0), with dy the gradient w.r.t. a_{l+1}:
         dW2 = dy^T h_l;  dh = dy W2;  dpre = dh * GELU'(pre_l);  dW1 = dpre^T a_l;  da = dpre W1 (l > 0)
@@ -287,11 +292,14 @@ def mlp_train_chain(T: int = 128, d: int = 768, dff: int = 3072, n_blocks: int =
                   NodeSpec("COPY", (p + "W2_0",), p + "W2", {"n": d * dff})]
     n_init = len(nodes)
     g = lambda M, N, K: {"M": M, "N": N, "K": K, "bias": False, "gelu": False}  # noqa: E731
-    # the step's input is staged by one COPY node (a GEMM reads its A operand through a TMA tensor
-    # map encoded at capture, so it cannot take a rebindable EXTERNAL pointer)
-    slots.append(SlotSpec("x_in", INTERNAL, "bf16", T * d))
-    nodes.append(NodeSpec("COPY", ("X",), "x_in", {"n": T * d}))
-    a = "x_in"
+    # the first GEMM reads the EXTERNAL X directly as its A operand (PI through the TMA descriptor:
+    # the kernel rebuilds its A tensor map from the pointer table). stage_x = True restores the
+    # round-1 variant that staged X with a COPY node (a data copy inside the graph), for comparison.
+    a = "X"
+    if stage_x:
+        slots.append(SlotSpec("x_in", INTERNAL, "bf16", T * d))
+        nodes.append(NodeSpec("COPY", ("X",), "x_in", {"n": T * d}))
+        a = "x_in"
     acts = []
     for l in range(n_blocks):
         p = f"B{l}."
