@@ -935,13 +935,76 @@ static bool df_capable(const Node& n, cgx_dtype out_dt) {
   return n.op == CGX_OP_SCALE_T && out_dt == CGX_F32;
 }
 
+// The chain's data-dependency DAG over the exec's launches, from the slot accesses in chain order
+// (RAW: last writer of every input; WAW: last writer of the output; WAR: readers of the output
+// since then), plus an artificial edge between consecutive collectives (they run one at a time,
+// in chain order, on every rank: NCCL forbids concurrent collectives on one communicator, and the
+// peer protocol's spinning kernels must not compete for SMs with each other).
+static std::vector<std::vector<int>> chain_deps(const cgx_exec* e) {
+  const size_t nl = e->L.size(), ns = e->c->slots.size();
+  std::vector<std::vector<int>> deps(nl);
+  std::vector<int> last_w(ns, -1);
+  std::vector<std::vector<int>> readers(ns);
+  int last_ar = -1;
+  for (size_t p = 0; p < nl; ++p) {
+    const Node& n = e->c->nodes[e->L[p].node];
+    auto add = [&](int q) {
+      if (q < 0 || q == (int)p) return;
+      for (int d : deps[p]) if (d == q) return;
+      deps[p].push_back(q);
+    };
+    for (int j = 0; j < n.n_in; ++j) add(last_w[n.in[j]]);
+    add(last_w[n.out]);
+    for (int r : readers[n.out]) add(r);
+    if (is_allreduce(n)) {
+      add(last_ar);
+      last_ar = (int)p;
+    }
+    for (int j = 0; j < n.n_in; ++j) readers[n.in[j]].push_back((int)p);
+    last_w[n.out] = (int)p;
+    readers[n.out].clear();
+  }
+  return deps;
+}
+
+// concurrent[p] = some other launch is neither an ancestor nor a descendant of p in the DAG
+// (transitive closure over bitsets; a linear chain has none).
+static std::vector<char> concurrent_nodes(const cgx_exec* e) {
+  const size_t nl = e->L.size(), w = (nl + 63) / 64;
+  const auto deps = chain_deps(e);
+  std::vector<uint64_t> anc(nl * w, 0);   // anc[p] includes p itself
+  for (size_t p = 0; p < nl; ++p) {
+    uint64_t* a = &anc[p * w];
+    a[p / 64] |= 1ull << (p % 64);
+    for (int d : deps[p])
+      for (size_t k = 0; k < w; ++k) a[k] |= anc[(size_t)d * w + k];
+  }
+  // related[p] = ancestors(p) ∪ descendants(p); descendants via q ∈ desc(p) ⇔ p ∈ anc(q)
+  std::vector<uint64_t> rel(anc);
+  for (size_t q = 0; q < nl; ++q)
+    for (size_t p = 0; p < q; ++p)
+      if (anc[q * w + p / 64] >> (p % 64) & 1) rel[p * w + q / 64] |= 1ull << (q % 64);
+  std::vector<char> conc(nl, 0);
+  for (size_t p = 0; p < nl; ++p) {
+    size_t cnt = 0;
+    for (size_t k = 0; k < w; ++k) cnt += (size_t)__builtin_popcountll(rel[p * w + k]);
+    conc[p] = cnt < nl;
+  }
+  return conc;
+}
+
 static int set_sync_flags(cgx_exec* e) {
   if (e->o.no_pdl || e->o.mode == CGX_MODE_EAGER || e->o.sync_mode == CGX_SYNC_CHAIN) return CGX_OK;
   if (e->o.sync_mode == CGX_SYNC_GRAPH) {
-    // concurrent branches: one CTA per SM for the f32 elementwise / reduction nodes as in the
-    // dataflow replay (C2 at 16 streams: 54.8 us capped vs 56.3 us full width, profiles/r01)
-    for (auto& l : e->L) {
-      if (l.kind != LK_KERNEL) continue;
+    // Nodes that can run concurrently with another node of the DAG (neither its ancestor nor its
+    // descendant): one CTA per SM for the f32 elementwise / reduction kernels, as in the dataflow
+    // replay (C2 at 16 streams: 54.8 us capped vs 56.3 us full width, profiles/r01). A node that
+    // runs alone (every other node is ordered with it: C1/C4 are linear chains) keeps the same
+    // full-width grid as EAGER — capping it cost up to 1.5x at >= 4 MiB (profiles/r01/c4_sweep.json).
+    const std::vector<char> conc = concurrent_nodes(e);
+    for (size_t p = 0; p < e->L.size(); ++p) {
+      auto& l = e->L[p];
+      if (l.kind != LK_KERNEL || !conc[p]) continue;
       const Node& n = e->c->nodes[l.node];
       const bool f32 = e->c->slots[n.out].dtype == CGX_F32 && (n.op <= CGX_OP_COPY || n.op == CGX_OP_SCALE_T);
       if (n.op == CGX_OP_REDUCE_SUM || f32) l.grid.x = (unsigned)std::min<uint64_t>(l.grid.x, chain_grid_cap(true));
@@ -1281,34 +1344,8 @@ static int setup_table(cgx_exec* e) {
 // one PDL cascade (scripts/dag_microbench.cu).
 static int capture_dag(cgx_exec* e, int gi, cudaStream_t cs, cgx_transport t) {
   const bool indirect = e->o.mode == CGX_MODE_GRAPH_INDIRECT;
-  const size_t nl = e->L.size(), ns = e->c->slots.size();
-  std::vector<std::vector<int>> deps(nl);
-  {
-    std::vector<int> last_w(ns, -1);
-    std::vector<std::vector<int>> readers(ns);
-    int last_ar = -1;
-    for (size_t p = 0; p < nl; ++p) {
-      const Node& n = e->c->nodes[e->L[p].node];
-      auto add = [&](int q) {
-        if (q < 0 || q == (int)p) return;
-        for (int d : deps[p]) if (d == q) return;
-        deps[p].push_back(q);
-      };
-      for (int j = 0; j < n.n_in; ++j) add(last_w[n.in[j]]);
-      add(last_w[n.out]);
-      for (int r : readers[n.out]) add(r);
-      // collectives run one at a time, in chain order, on every rank: an artificial edge from the
-      // previous all-reduce (NCCL forbids concurrent collectives on one communicator; the peer
-      // protocol's spinning kernels must not compete for SMs with each other)
-      if (is_allreduce(n)) {
-        add(last_ar);
-        last_ar = (int)p;
-      }
-      for (int j = 0; j < n.n_in; ++j) readers[n.in[j]].push_back((int)p);
-      last_w[n.out] = (int)p;
-      readers[n.out].clear();
-    }
-  }
+  const size_t nl = e->L.size();
+  const std::vector<std::vector<int>> deps = chain_deps(e);
   const int S = e->o.graph_streams ? e->o.graph_streams : 16;
   if (e->dag_s.empty()) {
     e->dag_s.assign((size_t)S + 0, nullptr);
