@@ -183,6 +183,14 @@ typedef struct {
                                CGX_SYNC_DATAFLOW (4) = one serial stream, per-node completion
                                counters (deferred waits when a node cannot use them) */
   int graph_streams;        /* CGX_SYNC_GRAPH: capture streams (0 = 16, at most 64) */
+  int megakernel;           /* 1 = run the node range as ONE persistent launch (one CTA per SM,
+                               grid barriers between stages) instead of one kernel per
+                               node. Every node must be LAYERNORM, GEMM_BF16 (no ALLREDUCE, A not
+                               EXTERNAL, W STATIC), ATTN_CAUSAL or a bf16 ADD, with at most 8
+                               EXTERNAL operands; otherwise exec creation fails with
+                               CGX_E_UNSUPPORTED. Not with the FIRST_NODE transport or SYNC_DATAFLOW.
+                               Every node's output slot is written as in the per-node exec, and the
+                               rebinding semantics of every mode are unchanged. 0 = off (default) */
 } cgx_exec_opts;
 
 typedef enum {
@@ -303,6 +311,13 @@ int cgx_debug_gemm_trace(cgx_exec* e, int pos, uint64_t* host_out, int cap, int*
  * input wait, last CTA exit) over the replays since the previous call, which then resets them.
  * CGX_E_STATE when tracing is off. Synchronises the exec's stream. */
 int cgx_debug_node_trace(cgx_exec* e, uint64_t* host_out, int cap, int* n_out);
+/* Diagnostics: per-stage, per-CTA timeline of a megakernel exec (opts.megakernel = 1) created with
+ * CGX_MEGA_TRACE=1: host_out gets [stage][cta][8] %globaltimer ns of the last replay (0 = start
+ * after the stage's barrier, 1 = end, 2-6 = phase marks of the stage kind, 7 = barrier arrival;
+ * unset marks are 0). Returns the entry count (stages x CTAs x 8; host_out == NULL:
+ * only the count), or a negative cgx_status (CGX_E_STATE: not a megakernel exec). Synchronises the
+ * exec's stream. */
+int cgx_debug_mega_trace(cgx_exec* e, uint64_t* host_out, int cap);
 
 /* ---- selective CUDA graphs ---------------------------------------------------------------- */
 /* Slow path: measure one segment (index into the marked segments, or -1 = whole chain) in the

@@ -44,7 +44,8 @@ class Attr(C.Structure):
 class ExecOpts(C.Structure):
     _fields_ = [("mode", C.c_int), ("transport", C.c_int), ("first_node", C.c_int),
                 ("n_nodes", C.c_int), ("no_pdl", C.c_int), ("validate", C.c_int),
-                ("copy_impl", C.c_int), ("sync_mode", C.c_int), ("graph_streams", C.c_int)]
+                ("copy_impl", C.c_int), ("sync_mode", C.c_int), ("graph_streams", C.c_int),
+                ("megakernel", C.c_int)]
 
 
 class Stats(C.Structure):
@@ -116,6 +117,7 @@ def _load():
         "cgx_debug_ext_field_offsets": ([VP, I, P(U64), I, P(I)], I),
         "cgx_debug_gemm_trace": ([VP, I, P(U64), I, P(I)], I),
         "cgx_debug_node_trace": ([VP, P(U64), I, P(I)], I),
+        "cgx_debug_mega_trace": ([VP, P(U64), I], I),
         "cgx_device_loop": ([VP, VP, I, U64], I),
         "cgx_nccl_unique_id": ([VP], I),
         "cgx_nccl_comm_init": ([I, I, VP, I, P(VP)], I),
@@ -142,7 +144,7 @@ EXPORTED = ("cgx_version", "cgx_last_error", "cgx_chain_create", "cgx_chain_add_
             "cgx_launch", "cgx_output", "cgx_output_gather", "cgx_stats", "cgx_debug_read_table",
             "cgx_debug_setparam_nodes", "cgx_exec_destroy", "cgx_profile", "cgx_select",
             "cgx_dispatch_floor", "cgx_fill_uniform_f32", "cgx_copy", "cgx_graph_floor", "cgx_kernel_times", "cgx_find_param_offset",
-            "cgx_debug_param_image", "cgx_debug_ext_field_offsets", "cgx_debug_gemm_trace", "cgx_debug_node_trace", "cgx_device_loop", "cgx_nccl_unique_id",
+            "cgx_debug_param_image", "cgx_debug_ext_field_offsets", "cgx_debug_gemm_trace", "cgx_debug_node_trace", "cgx_debug_mega_trace", "cgx_device_loop", "cgx_nccl_unique_id",
             "cgx_nccl_comm_init", "cgx_nccl_comm_destroy", "cgx_peer_buffer_bytes", "cgx_chain_set_peers",
             "cgx_device_alloc", "cgx_device_free",
             "cgx_ipc_handle", "cgx_ipc_open", "cgx_ipc_close", "cgx_tune_graph_streams")
@@ -198,9 +200,9 @@ def chain_destroy(chain: int):
 
 def exec_create(chain: int, mode: str, stream: int, transport: str = "DEFAULT", first_node: int = 0,
                 n_nodes: int = 0, no_pdl: bool = False, validate: int = 0, copy_impl: int = 0,
-                sync: str = "AUTO", graph_streams: int = 0) -> int:
+                sync: str = "AUTO", graph_streams: int = 0, megakernel: bool = False) -> int:
     o = ExecOpts(MODE[mode], XPORT[transport], first_node, n_nodes, int(no_pdl), validate, copy_impl,
-                 SYNC[sync], graph_streams)
+                 SYNC[sync], graph_streams, int(megakernel))
     out = C.c_void_p()
     _ck(LIB.cgx_exec_create_ex(chain, C.byref(o), stream, C.byref(out)), "cgx_exec_create_ex")
     return out.value
@@ -214,7 +216,8 @@ def tune_graph_streams(chain: int, mode: str, stream: int, ext_sets, candidates=
     n_sets, n_ext = len(ext_sets), len(ext_sets[0]) if ext_sets else 0
     flat = ptr_array([p for row in ext_sets for p in row])
     o = ExecOpts(MODE[mode], XPORT[transport], kw.get("first_node", 0), kw.get("n_nodes", 0),
-                 int(kw.get("no_pdl", False)), kw.get("validate", 0), kw.get("copy_impl", 0), SYNC["GRAPH"], 0)
+                 int(kw.get("no_pdl", False)), kw.get("validate", 0), kw.get("copy_impl", 0), SYNC["GRAPH"], 0,
+                 int(kw.get("megakernel", False)))
     cand = (C.c_int * len(candidates))(*candidates)
     us = (C.c_double * len(candidates))()
     best = C.c_int()

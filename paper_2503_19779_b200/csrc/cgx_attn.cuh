@@ -1,0 +1,221 @@
+// Causal attention tile on the warp-level bf16 tensor cores (mma.sync), shared by the per-node
+// kernel (k_decoder.cu k_attention) and the persistent decoder executor (k_mega.cu).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+namespace cgx {
+
+// ---------------------------------------------------------------------------- causal attention
+// softmax(Q K^T * scale + causal mask) V per head, bf16 in/out, on the warp-level bf16 tensor-core
+// MMA (mma.sync m16n8k16, fp32 accumulate): at T = 128, D = 64 a head is 2 x 0.5 MFLOP, far too
+// small for tcgen05 tiles, and the node is latency-bound (one L2 round trip for Q/K/V, a few
+// dozen MMAs, one store).
+// CTA = (16 query rows, 1 head); warp w owns keys [32 w, 32 w + 32) of the causal range (split-KV
+// inside the CTA, FlashDecoding-style): S_w = Q K_w^T (16 MMAs), row max / exp / row sum on the
+// accumulator fragments, O_w = P_w V_w (16 MMAs, P re-used from the S fragments as bf16 A
+// operands), then the warps' (m_w, l_w, O_w) are merged in fixed warp order through shared memory
+// (deterministic). K and V rows are staged in shared memory (padded rows: conflict-free ldmatrix),
+// Q fragments are loaded straight from global memory into registers, all loads in flight at once.
+static constexpr int kAttnQRows = 16;
+static constexpr int kAttnKChunk = 32;
+static constexpr int kAttnMaxT = 256;
+static constexpr int kAttnMaxWarps = kAttnMaxT / kAttnKChunk;   // 8
+static constexpr int kAttnD = 64;
+static constexpr int kKVRowB = kAttnD * 2 + 16;                   // padded smem row (bytes)
+
+__device__ __forceinline__ void mma_bf16_16816(float* c, const uint32_t* a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};\n"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void ldsm_x2(uint32_t addr, uint32_t& r0, uint32_t& r1) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];\n" : "=r"(r0), "=r"(r1) : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x2_trans(uint32_t addr, uint32_t& r0, uint32_t& r1) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0,%1}, [%2];\n" : "=r"(r0), "=r"(r1) : "r"(addr));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&v);
+}
+
+// One attention tile: query rows [16 qblock, 16 qblock + 16) of head h, with blockDim.x threads
+// (>= one warp per 32-key chunk of the causal range; extra warps only help with the loads).
+// Shared by k_attention (one tile per CTA) and the persistent decoder executor (k_mega.cu).
+__device__ __forceinline__ void attn_tile(const __nv_bfloat16* qkv_in, __nv_bfloat16* out, uint32_t T, uint32_t H,
+                                          float scale, uint32_t qblock, uint32_t h, uint8_t* smem) {
+  const uint32_t q0 = qblock * kAttnQRows;
+  const uint32_t kend = min(T, q0 + kAttnQRows);                 // keys [0, kend) are visible to the block
+  const uint32_t nchunk = (kend + kAttnKChunk - 1) / kAttnKChunk;
+  const uint32_t row_el = 3 * H * kAttnD;                         // qkv row length (elements)
+  const __nv_bfloat16* qkv = qkv_in;
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t g = lane >> 2, t4 = lane & 3;
+  const uint32_t cap_rows = (T + kAttnKChunk - 1) / kAttnKChunk * kAttnKChunk;   // sized per T (host agrees)
+  uint8_t* sK = smem;                                          // [cap_rows][kKVRowB]
+  uint8_t* sV = sK + cap_rows * kKVRowB;
+  float* sO = reinterpret_cast<float*>(sV + cap_rows * kKVRowB);  // [warps][16][64]
+  float* sML = sO + (cap_rows / kAttnKChunk) * kAttnQRows * kAttnD; // [warps][16][2]
+
+  // ---- loads: Q fragments (registers), K/V rows [0, nchunk*32) -> smem (zero beyond kend)
+  uint32_t qa[4][4];
+  {
+    const uint32_t r0 = q0 + g, r1 = q0 + g + 8;
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      const uint32_t c = h * kAttnD + 16 * kk + 2 * t4;
+      qa[kk][0] = r0 < T ? *reinterpret_cast<const uint32_t*>(qkv + (size_t)r0 * row_el + c) : 0u;
+      qa[kk][1] = r1 < T ? *reinterpret_cast<const uint32_t*>(qkv + (size_t)r1 * row_el + c) : 0u;
+      qa[kk][2] = r0 < T ? *reinterpret_cast<const uint32_t*>(qkv + (size_t)r0 * row_el + c + 8) : 0u;
+      qa[kk][3] = r1 < T ? *reinterpret_cast<const uint32_t*>(qkv + (size_t)r1 * row_el + c + 8) : 0u;
+    }
+  }
+  {
+    const uint32_t nrow = nchunk * kAttnKChunk, nvec = nrow * 8;   // 16-B vectors per matrix
+    constexpr int kPer = kAttnMaxT * 8 * 2 / (kAttnMaxWarps * 32);  // <= 16 per thread
+    uint4 buf[kPer];
+#pragma unroll
+    for (int r = 0; r < kPer; ++r) {
+      const uint32_t idx = threadIdx.x + r * blockDim.x;
+      buf[r] = make_uint4(0u, 0u, 0u, 0u);
+      if (idx < 2 * nvec) {
+        const uint32_t which = idx >= nvec, v = idx - which * nvec, j = v >> 3, c = v & 7;
+        if (j < kend)
+          buf[r] = *reinterpret_cast<const uint4*>(qkv + (size_t)j * row_el + (1 + which) * H * kAttnD + h * kAttnD + 8 * c);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < kPer; ++r) {
+      const uint32_t idx = threadIdx.x + r * blockDim.x;
+      if (idx < 2 * nvec) {
+        const uint32_t which = idx >= nvec, v = idx - which * nvec, j = v >> 3, c = v & 7;
+        *reinterpret_cast<uint4*>((which ? sV : sK) + j * kKVRowB + 16 * c) = buf[r];
+      }
+    }
+  }
+  __syncthreads();
+
+  if (warp < nchunk) {
+    const uint32_t k0 = warp * kAttnKChunk;
+    // ---- S = Q K^T over this warp's 32 keys: 4 n-tiles of 8 keys x 4 k-steps of 16 dims
+    float sacc[4][4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      sacc[j][0] = sacc[j][1] = sacc[j][2] = sacc[j][3] = 0.f;
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        // matrices: keys k0+8j..+8 x dims 16kk..+8 and 16kk+8..+16 (lanes 0-7 / 8-15 give rows)
+        const uint32_t rr = k0 + 8 * j + (lane & 7);
+        const uint32_t addr = (uint32_t)__cvta_generic_to_shared(sK + rr * kKVRowB + (16 * kk + ((lane >> 3) & 1) * 8) * 2);
+        uint32_t b0, b1;
+        ldsm_x2(addr, b0, b1);
+        mma_bf16_16816(sacc[j], qa[kk], b0, b1);
+      }
+    }
+    // ---- scale, causal mask, row max / exp / row sum (rows g and g+8 of the 16; quad-reduced)
+    const uint32_t qi0 = q0 + g, qi1 = q0 + g + 8;
+    float m0 = -INFINITY, m1 = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint32_t key = k0 + 8 * j + 2 * t4 + (e & 1);
+        const uint32_t qi = e < 2 ? qi0 : qi1;
+        float v = sacc[j][e] * scale;
+        if (key > qi || key >= T) v = -INFINITY;
+        sacc[j][e] = v;
+        if (e < 2) m0 = fmaxf(m0, v);
+        else m1 = fmaxf(m1, v);
+      }
+#pragma unroll
+    for (int o = 1; o <= 2; o <<= 1) {
+      m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, o));
+      m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, o));
+    }
+    // rows past T (ragged tail) have no visible key: keep them finite, they are never stored
+    const float mm0 = m0 == -INFINITY ? 0.f : m0, mm1 = m1 == -INFINITY ? 0.f : m1;
+    float l0 = 0.f, l1 = 0.f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      sacc[j][0] = __expf(sacc[j][0] - mm0);
+      sacc[j][1] = __expf(sacc[j][1] - mm0);
+      sacc[j][2] = __expf(sacc[j][2] - mm1);
+      sacc[j][3] = __expf(sacc[j][3] - mm1);
+      l0 += sacc[j][0] + sacc[j][1];
+      l1 += sacc[j][2] + sacc[j][3];
+    }
+#pragma unroll
+    for (int o = 1; o <= 2; o <<= 1) {
+      l0 += __shfl_xor_sync(0xffffffffu, l0, o);
+      l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+    }
+    // ---- O = P V: 2 k-steps of 16 keys x 8 n-tiles of 8 dims; P fragments from the S accumulators
+    float oacc[8][4];
+#pragma unroll
+    for (int n = 0; n < 8; ++n) oacc[n][0] = oacc[n][1] = oacc[n][2] = oacc[n][3] = 0.f;
+#pragma unroll
+    for (int kk = 0; kk < 2; ++kk) {
+      uint32_t pa[4];
+      pa[0] = pack_bf16(sacc[2 * kk][0], sacc[2 * kk][1]);
+      pa[1] = pack_bf16(sacc[2 * kk][2], sacc[2 * kk][3]);
+      pa[2] = pack_bf16(sacc[2 * kk + 1][0], sacc[2 * kk + 1][1]);
+      pa[3] = pack_bf16(sacc[2 * kk + 1][2], sacc[2 * kk + 1][3]);
+#pragma unroll
+      for (int n = 0; n < 8; ++n) {
+        // matrices: keys k0+16kk..+8 and +8..+16 x dims 8n..+8, transposed
+        const uint32_t rr = k0 + 16 * kk + (lane & 7) + ((lane >> 3) & 1) * 8;
+        const uint32_t addr = (uint32_t)__cvta_generic_to_shared(sV + rr * kKVRowB + 8 * n * 2);
+        uint32_t b0, b1;
+        ldsm_x2_trans(addr, b0, b1);
+        mma_bf16_16816(oacc[n], pa, b0, b1);
+      }
+    }
+    // ---- publish this warp's partial (m, l, O) for the merge
+    float* o = sO + warp * kAttnQRows * kAttnD;
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+      const uint32_t c = 8 * n + 2 * t4;
+      *reinterpret_cast<float2*>(o + g * kAttnD + c) = make_float2(oacc[n][0], oacc[n][1]);
+      *reinterpret_cast<float2*>(o + (g + 8) * kAttnD + c) = make_float2(oacc[n][2], oacc[n][3]);
+    }
+    if (t4 == 0) {
+      sML[(warp * kAttnQRows + g) * 2 + 0] = m0;
+      sML[(warp * kAttnQRows + g) * 2 + 1] = l0;
+      sML[(warp * kAttnQRows + g + 8) * 2 + 0] = m1;
+      sML[(warp * kAttnQRows + g + 8) * 2 + 1] = l1;
+    }
+  }
+  __syncthreads();
+  // ---- merge the warps' partials in fixed order: out = sum_w e^{m_w - m} O_w / sum_w e^{m_w - m} l_w
+  for (uint32_t idx = threadIdx.x; idx < kAttnQRows * kAttnD / 2; idx += blockDim.x) {
+    const uint32_t r = idx / (kAttnD / 2), c = 2 * (idx % (kAttnD / 2));
+    const uint32_t qi = q0 + r;
+    if (qi >= T) continue;
+    float m = -INFINITY;
+    for (uint32_t w = 0; w < nchunk; ++w) m = fmaxf(m, sML[(w * kAttnQRows + r) * 2]);
+    float l = 0.f, ox = 0.f, oy = 0.f;
+    for (uint32_t w = 0; w < nchunk; ++w) {
+      const float mw = sML[(w * kAttnQRows + r) * 2];
+      const float f = mw == -INFINITY ? 0.f : __expf(mw - m);
+      l += f * sML[(w * kAttnQRows + r) * 2 + 1];
+      const float2 ov = *reinterpret_cast<const float2*>(sO + (w * kAttnQRows + r) * kAttnD + c);
+      ox += f * ov.x;
+      oy += f * ov.y;
+    }
+    const float inv = 1.0f / l;
+    *reinterpret_cast<uint32_t*>(out + (size_t)qi * (H * kAttnD) + h * kAttnD + c) =
+        pack_bf16(ox * inv, oy * inv);
+  }
+}
+
+static inline size_t attn_smem_bytes(uint32_t T) {
+  const size_t rows = (T + kAttnKChunk - 1) / kAttnKChunk * kAttnKChunk, warps = rows / kAttnKChunk;
+  return 2 * rows * kKVRowB + warps * kAttnQRows * kAttnD * 4 + warps * kAttnQRows * 2 * 4;
+}
+
+}  // namespace cgx

@@ -52,4 +52,7 @@ void decoder_gemm_set_status(void* args, uint32_t* word, uint64_t timeout_ns);
 void decoder_gemm_set_node_trace(void* args, unsigned long long* nt);
 // Diagnostics: per-CTA %globaltimer trace [cta][16] written by the kernel (nullptr = off).
 void decoder_gemm_set_trace(void* args, unsigned long long* trace);
+// 3-D K-major bf16 operand map {64, rows, K/64}, box {64, box_rows, group}, SW128 (the layout both
+// tcgen05 kernels stage: G stacked [box_rows][128 B] tiles), written to tm (128 B, 64-B aligned).
+int decoder_encode_kmajor(void* tm, const void* base, uint64_t rows, uint64_t K, uint32_t box_rows, uint32_t group);
 }  // namespace cgx

@@ -24,12 +24,14 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <unordered_map>
 #include <unordered_set>
 #include <vector>
 
 #include "../../include/cgx.h"
 #include "cgx_args.h"
 #include "cgx_decoder.h"
+#include "cgx_mega.h"
 #include "cgx_prelude.h"
 
 using namespace cgx;
@@ -460,6 +462,8 @@ struct Launch {
   unsigned cluster_z = 1;                 // thread-block cluster (1, 1, z) (split-K GEMM)
   bool dev_updatable = false;             // T7: consumer patched by the prelude node
   int prio = 0;                           // launch priority (0 = default; CGX_DAG_PRIO experiment)
+  bool coop = false;                      // cooperative launch (co-resident grid: the megakernel)
+  bool mega = false;                      // the persistent decoder executor (args = MegaArgs)
   cudaGraphDeviceNode_t dev_node = nullptr;
   // NCCL
   const void* nc_in = nullptr;
@@ -547,6 +551,12 @@ struct cgx_exec {
   volatile uint32_t* h_status = nullptr;
   uint32_t* d_status = nullptr;
   uint64_t spin_timeout_ns = 0;
+  // megakernel (cgx_mega.h): one device blob = stages | row ops | tensor maps | split-K workspace |
+  // grid-barrier counter | stage trace
+  bool mega = false;
+  void* mega_mem = nullptr;
+  unsigned long long* mega_strace = nullptr;
+  uint32_t mega_stages = 0, mega_ctas = 0;
 };
 
 static DevStatus dev_status(const cgx_exec* e) { return DevStatus{e->d_status, e->spin_timeout_ns}; }
@@ -898,7 +908,7 @@ static int build_launch(cgx_exec* e, int k, Launch& l) {
 // griddepcontrol.wait: EXTERNAL inputs (bound before the replay; COPY placeholders are written by
 // the copy kernel, which fully precedes the graph) and STATIC weights.
 static void set_prewait_masks(cgx_exec* e) {
-  if (e->o.no_pdl) return;
+  if (e->o.no_pdl || e->mega) return;
   for (auto& l : e->L) {
     if (l.kind != LK_KERNEL) continue;
     const Node& node = e->c->nodes[l.node];
@@ -994,6 +1004,7 @@ static std::vector<char> concurrent_nodes(const cgx_exec* e) {
 }
 
 static int set_sync_flags(cgx_exec* e) {
+  if (e->mega) return CGX_OK;   // one launch: nothing to order
   if (e->o.no_pdl || e->o.mode == CGX_MODE_EAGER || e->o.sync_mode == CGX_SYNC_CHAIN) return CGX_OK;
   if (e->o.sync_mode == CGX_SYNC_GRAPH) {
     // Nodes that can run concurrently with another node of the DAG (neither its ancestor nor its
@@ -1129,8 +1140,13 @@ static int issue(cgx_exec* e, Launch& l, cudaStream_t s) {
   cfg.blockDim = l.block;
   cfg.dynamicSmemBytes = l.smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[4];
+  cudaLaunchAttribute attr[5];
   unsigned na = 0;
+  if (l.coop) {
+    attr[na].id = cudaLaunchAttributeCooperative;
+    attr[na].val.cooperative = 1;
+    ++na;
+  }
   if (l.prio) {
     attr[na].id = cudaLaunchAttributePriority;
     attr[na].val.priority = l.prio;
@@ -1525,6 +1541,10 @@ static int capture_graph(cgx_exec* e, int gi) {
     // graph gi reads table gi: the `table` field is the first member of ElemArgs and LnArgs
     uint64_t* tab = gi == 0 ? e->d_table : e->d_table2;
     for (auto& l : e->L) {
+      if (l.mega) {
+        argp<MegaArgs>(l)->table = tab;
+        continue;
+      }
       if (l.kind == LK_KERNEL && (uses_elem_args(e->c->nodes[l.node].op) ||
                                   e->c->nodes[l.node].op == CGX_OP_LAYERNORM))
         memcpy(l.args.p, &tab, sizeof(tab));
@@ -1575,7 +1595,7 @@ static int capture_graph(cgx_exec* e, int gi) {
   for (auto& l : e->L) {
     if (l.kind == LK_KERNEL && first_kernel && after_root) {
       // the first consumer after a root node fetches table entries after its wait
-      if (e->o.mode == CGX_MODE_GRAPH_INDIRECT) {
+      if (e->o.mode == CGX_MODE_GRAPH_INDIRECT && !l.mega) {   // (the megakernel reads it after its wait)
         const Node& n = e->c->nodes[l.node];
         const uint32_t f = kFlagTableAfterWait | kFlagTriggerAfterWait;
         if (n.op == CGX_OP_LAYERNORM) argp<LnArgs>(l)->flags |= f;
@@ -1616,6 +1636,7 @@ static void exec_free(cgx_exec* e) {
   if (e->dl_g) cudaGraphDestroy(e->dl_g);
   if (e->dl_iter) cudaFree(e->dl_iter);
   if (e->d_trace) cudaFree(e->d_trace);
+  if (e->mega_mem) cudaFree(e->mega_mem);
   if (e->d_desc) cudaFree(e->d_desc);
   if (e->d_chunk) cudaFree(e->d_chunk);
   if (e->d_table) cudaFree(e->d_table);
@@ -1639,6 +1660,372 @@ static void exec_free(cgx_exec* e) {
 
 static void node_trace_reset(cgx_exec* e);
 
+// ---------------------------------------------------------------- megakernel (cgx_mega.h)
+
+// Compile the exec's node range into the stages of ONE persistent launch:
+//  * LAYERNORM and bf16 ADD become row ops of a ROW stage (consecutive ones with the same row
+//    shape share a stage: row r is handled by CTA r % G in every ROW stage);
+//  * a GEMM is one GEMM stage. When the next node is a row op over its output (or the GEMM ends
+//    the range, or its weight slice cannot be staged unsplit) it runs DEFERRED: K split S ways into
+//    tasks that store fp32 partials, and the next ROW stage opens with a fixup op that sums them in
+//    split order and applies the epilogue (bias, GELU, residual, one bf16 rounding). Otherwise S = 1
+//    and the epilogue is applied in the GEMM stage;
+//  * ATTN_CAUSAL is one ATTN stage.
+// Every stage after the first starts with a grid barrier (each stage reads the previous one's
+// output, and consecutive stages partition the work differently).
+static int build_mega(cgx_exec* e) {
+  cgx_chain* c = e->c;
+  const cgx_mode mode = e->o.mode;
+  const cgx_transport t = eff_transport(e->o);
+  if (mode == CGX_MODE_GRAPH_INDIRECT && t == CGX_XPORT_FIRST_NODE)
+    return fail(CGX_E_UNSUPPORTED, "megakernel: the FIRST_NODE transport needs an elementwise first node");
+  // INDIRECT reads externals through the table; PRELUDE patches the by-value ext_ptr fields like
+  // the patch modes do; COPY binds the placeholders by address
+  const bool indirect = mode == CGX_MODE_GRAPH_INDIRECT && t != CGX_XPORT_PRELUDE;
+  int dev = 0, G = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&G, cudaDevAttrMultiProcessorCount, dev));
+  if (const char* gv = getenv("CGX_MEGA_CTAS")) G = std::max(1, std::min(G, atoi(gv)));   // diagnostics
+  std::vector<MegaStage> stages;
+  std::vector<MegaRowOp> ops;
+  std::vector<int> ext_of(c->ext_slots.size(), -1), ext_js;
+  bool ext_overflow = false;
+  auto ref = [&](int si) -> MegaRef {
+    const Slot& s = c->slots[si];
+    MegaRef r{nullptr, -1, -1};
+    if (s.kind == CGX_SLOT_STATIC) r.p = s.static_ptr;
+    else if (s.kind == CGX_SLOT_INTERNAL) r.p = s.buf;
+    else if (mode == CGX_MODE_GRAPH_COPY) r.p = e->ph[s.ext_j];
+    else {
+      if (ext_of[s.ext_j] < 0) {
+        if ((int)ext_js.size() == kMegaMaxExt) ext_overflow = true;
+        else {
+          ext_of[s.ext_j] = (int)ext_js.size();
+          ext_js.push_back(s.ext_j);
+        }
+      }
+      r.ext = ext_of[s.ext_j];
+    }
+    return r;
+  };
+  auto bf16 = [&](int si) { return c->slots[si].dtype == CGX_BF16; };
+  int cur_row = -1, pending = -1, pending_node = -1, next_reg = 0;
+  int reg_slot[kMegaMaxRegs];
+  std::unordered_map<int, int> reg_of;
+  size_t ws_floats = 0;
+  auto new_stage = [&](uint32_t kind, int node) -> int {
+    MegaStage st{};
+    st.kind = kind;
+    st.barrier = stages.empty() ? 0u : 1u;
+    st.node = (uint32_t)node;
+    st.next_gemm = -1;
+    stages.push_back(st);
+    cur_row = -1;
+    return (int)stages.size() - 1;
+  };
+  auto row_ref = [&](int si) -> MegaRef {
+    auto it = reg_of.find(si);
+    if (it != reg_of.end()) return MegaRef{nullptr, -1, it->second};
+    return ref(si);
+  };
+  auto alloc_reg = [&](int si) -> int32_t {
+    const int r = next_reg++ % kMegaMaxRegs;
+    if (reg_slot[r] >= 0) reg_of.erase(reg_slot[r]);
+    reg_slot[r] = si;
+    reg_of[si] = r;
+    return r;
+  };
+  std::string why;
+  auto open_row = [&](uint32_t rows, uint32_t cols, int node) -> bool {
+    const bool same = cur_row >= 0 && stages[cur_row].rows == rows && stages[cur_row].cols == cols;
+    if (same && stages[cur_row].n_ops < kMegaMaxRowOps) return true;
+    if (cols > kMegaMaxCols || cols % 8 || rows == 0) {
+      why = "row shape " + std::to_string(rows) + "x" + std::to_string(cols) + " (cols <= 2048, % 8)";
+      return false;
+    }
+    const int si = new_stage(kMegaRow, node);
+    // a full ROW stage continues without a barrier: same rows on the same CTAs, same columns on
+    // the same threads, so every value it reads was written by the reading thread itself
+    if (same) stages[si].barrier = 0;
+    cur_row = si;
+    stages[si].rows = rows;
+    stages[si].cols = cols;
+    stages[si].op0 = (uint32_t)ops.size();
+    reg_of.clear();
+    for (int& r : reg_slot) r = -1;
+    next_reg = 0;
+    if (pending >= 0) {   // the deferred GEMM's epilogue opens this stage
+      const MegaStage& g = stages[pending];
+      if (g.M != rows || g.N != cols) {
+        why = "deferred GEMM output shape";
+        return false;
+      }
+      const Node& gn = c->nodes[pending_node];
+      MegaRowOp op{};
+      op.kind = kRowFixup;
+      op.node = (uint32_t)pending_node;
+      op.flags = g.flags & (CGX_GEMM_BIAS | CGX_GEMM_GELU | CGX_GEMM_RESIDUAL);
+      op.S = g.split;
+      op.a = op.b = MegaRef{nullptr, -1, -1};
+      op.c = (g.flags & CGX_GEMM_BIAS) ? ref(gn.in[2]) : MegaRef{nullptr, -1, -1};
+      op.d = (g.flags & CGX_GEMM_RESIDUAL) ? ref(gn.in[3]) : MegaRef{nullptr, -1, -1};
+      op.ws = nullptr;   // set once the workspace is allocated
+      op.out = c->slots[gn.out].buf;
+      op.out_reg = alloc_reg(gn.out);
+      ops.push_back(op);
+      stages[si].n_ops++;
+      pending = -1;
+    }
+    return true;
+  };
+  auto flush_pending = [&](int node) -> bool {
+    if (pending < 0) return true;
+    return open_row(stages[pending].M, stages[pending].N, node);
+  };
+  int gemm_count = 0;
+  for (int k = e->first; k <= e->last; ++k) {
+    const Node& n = c->nodes[k];
+    const std::string at = "megakernel: node " + std::to_string(k) + ": ";
+    if (!bf16(n.out)) return fail(CGX_E_UNSUPPORTED, at + "output must be bf16");
+    switch (n.op) {
+      case CGX_OP_LAYERNORM: {
+        if (!bf16(n.in[0]) || !bf16(n.in[1]) || !bf16(n.in[2])) return fail(CGX_E_UNSUPPORTED, at + "LN operands must be bf16");
+        const uint32_t rows = n.attr.rows, cols = n.attr.cols;
+        if (pending >= 0 && (stages[pending].M != rows || stages[pending].N != cols) && !flush_pending(k))
+          return fail(CGX_E_UNSUPPORTED, at + why);
+        if (!open_row(rows, cols, k)) return fail(CGX_E_UNSUPPORTED, at + why);
+        MegaRowOp op{};
+        op.kind = kRowLn;
+        op.node = (uint32_t)k;
+        op.a = row_ref(n.in[0]);
+        op.b = MegaRef{nullptr, -1, -1};
+        op.c = ref(n.in[1]);
+        op.d = ref(n.in[2]);
+        op.out = c->slots[n.out].buf;
+        op.eps = n.attr.eps;
+        op.out_reg = alloc_reg(n.out);
+        ops.push_back(op);
+        stages[cur_row].n_ops++;
+        break;
+      }
+      case CGX_OP_ADD: {
+        if (!bf16(n.in[0]) || !bf16(n.in[1])) return fail(CGX_E_UNSUPPORTED, at + "ADD operands must be bf16");
+        const uint64_t ne = n.attr.n;
+        uint32_t rows = 0, cols = 0;
+        if (pending >= 0 && (uint64_t)stages[pending].M * stages[pending].N == ne) {
+          rows = stages[pending].M;
+          cols = stages[pending].N;
+        } else if (cur_row >= 0 && (uint64_t)stages[cur_row].rows * stages[cur_row].cols == ne) {
+          rows = stages[cur_row].rows;
+          cols = stages[cur_row].cols;
+        } else {
+          for (uint32_t cc = kMegaMaxCols; cc >= 8; cc -= 8)
+            if (ne % cc == 0) {
+              cols = cc;
+              break;
+            }
+          rows = cols ? (uint32_t)(ne / cols) : 0;
+        }
+        if (pending >= 0 && (stages[pending].M != rows || stages[pending].N != cols) && !flush_pending(k))
+          return fail(CGX_E_UNSUPPORTED, at + why);
+        if (!open_row(rows, cols, k)) return fail(CGX_E_UNSUPPORTED, at + why);
+        MegaRowOp op{};
+        op.kind = kRowAdd;
+        op.node = (uint32_t)k;
+        op.a = row_ref(n.in[0]);
+        op.b = row_ref(n.in[1]);
+        op.c = op.d = MegaRef{nullptr, -1, -1};
+        op.out = c->slots[n.out].buf;
+        op.out_reg = alloc_reg(n.out);
+        ops.push_back(op);
+        stages[cur_row].n_ops++;
+        break;
+      }
+      case CGX_OP_GEMM_BF16: {
+        if (!flush_pending(k)) return fail(CGX_E_UNSUPPORTED, at + why);
+        const uint32_t M = n.attr.M, N = n.attr.N, K = n.attr.K, fl = n.attr.flags;
+        if (fl & CGX_GEMM_ALLREDUCE) return fail(CGX_E_UNSUPPORTED, at + "GEMM with a fused all-reduce");
+        if (K % 64 || N % 16 || M == 0) return fail(CGX_E_UNSUPPORTED, at + "GEMM shape (K % 64, N % 16)");
+        if (c->slots[n.in[0]].kind == CGX_SLOT_EXTERNAL) return fail(CGX_E_UNSUPPORTED, at + "EXTERNAL A operand");
+        if (c->slots[n.in[1]].kind != CGX_SLOT_STATIC) return fail(CGX_E_UNSUPPORTED, at + "W must be STATIC");
+        const uint32_t kb = K / 64, m_tiles = (M + 127) / 128;
+        auto w_fits = [&](uint32_t bn, uint32_t kps) { return (uint64_t)bn * kps * 128u <= kMegaWBytes; };
+        // direct (unsplit) tiling: the widest N tile whose whole-K weight slice fits one W buffer
+        uint32_t bn_direct = 0;
+        for (uint32_t bn : {64u, 32u, 16u})
+          if (N % bn == 0 && w_fits(bn, kb)) {
+            bn_direct = bn;
+            break;
+          }
+        bool next_row = false;
+        if (k < e->last) {
+          const Node& nx = c->nodes[k + 1];
+          if (nx.op == CGX_OP_LAYERNORM || nx.op == CGX_OP_ADD)
+            for (int i = 0; i < nx.n_in; ++i) next_row = next_row || nx.in[i] == n.out;
+        }
+        const bool deferred = next_row || k == e->last || bn_direct == 0;
+        const int si = new_stage(kMegaGemm, k);
+        MegaStage& g = stages[si];
+        g.M = M;
+        g.N = N;
+        g.K = K;
+        g.flags = fl & (CGX_GEMM_BIAS | CGX_GEMM_GELU | CGX_GEMM_RESIDUAL);
+        g.m_tiles = m_tiles;
+        g.deferred = deferred ? 1u : 0u;
+        if (deferred) {
+          // widest N tile, then the most K splits (<= 16) that keep tasks <= G and the slice staged
+          g.bn = N % 64 == 0 ? 64u : N % 32 == 0 ? 32u : 16u;
+          g.split = 0;
+          for (uint32_t sp = std::min<uint32_t>(kMegaMaxSplit, kb); sp >= 1; --sp)
+            if (kb % sp == 0 && (uint64_t)m_tiles * (N / g.bn) * sp <= (uint64_t)G && w_fits(g.bn, kb / sp)) {
+              g.split = sp;
+              break;
+            }
+          if (g.split == 0)
+            for (uint32_t sp = 1; sp <= std::min<uint32_t>(kMegaMaxSplit, kb); ++sp)   // more tasks than CTAs
+              if (kb % sp == 0 && w_fits(g.bn, kb / sp)) {
+                g.split = sp;
+                break;
+              }
+          if (g.split == 0) return fail(CGX_E_UNSUPPORTED, at + "no K split stages the weight slice");
+          ws_floats = std::max<size_t>(ws_floats, (size_t)g.split * M * N);
+          pending = si;
+          pending_node = k;
+        } else {
+          g.bn = bn_direct;
+          g.split = 1;
+        }
+        g.n_tiles = N / g.bn;
+        g.kps = kb / g.split;
+        g.ga = g.kps % 4 == 0 ? 4u : g.kps % 2 == 0 ? 2u : 1u;
+        g.w_buf = (uint32_t)(gemm_count++ % 2);
+        g.bias = (fl & CGX_GEMM_BIAS) ? ref(n.in[2]) : MegaRef{nullptr, -1, -1};
+        g.res = (fl & CGX_GEMM_RESIDUAL) ? ref(n.in[3]) : MegaRef{nullptr, -1, -1};
+        g.out = c->slots[n.out].buf;
+        break;
+      }
+      case CGX_OP_ATTN_CAUSAL: {
+        if (!flush_pending(k)) return fail(CGX_E_UNSUPPORTED, at + why);
+        if (!bf16(n.in[0])) return fail(CGX_E_UNSUPPORTED, at + "attention operands must be bf16");
+        if (n.attr.D != 64 || n.attr.T > 256) return fail(CGX_E_UNSUPPORTED, at + "attention (D == 64, T <= 256)");
+        const int si = new_stage(kMegaAttn, k);
+        stages[si].T = n.attr.T;
+        stages[si].H = n.attr.H;
+        stages[si].scale = n.attr.scalar;
+        stages[si].qkv = ref(n.in[0]);
+        stages[si].aout = c->slots[n.out].buf;
+        break;
+      }
+      default:
+        return fail(CGX_E_UNSUPPORTED, at + "op not supported by the megakernel");
+    }
+  }
+  if (!flush_pending(e->last)) return fail(CGX_E_UNSUPPORTED, "megakernel: " + why);
+  if (ext_overflow) return fail(CGX_E_UNSUPPORTED, "megakernel: more than 8 EXTERNAL operands");
+  for (size_t i = 0; i + 1 < stages.size(); ++i) stages[i].bar_next = stages[i + 1].barrier;
+  for (auto& op : ops) {   // operands fetched from memory (not a register of the stage), per column
+    const MegaRef* r = &op.a;
+    auto present = [](const MegaRef& x) { return x.p != nullptr || x.ext >= 0 || x.reg >= 0; };
+    op.pf = op.col = 0;
+    for (uint32_t x = 0; x < 4; ++x)
+      if (present(r[x]) && r[x].reg < 0) op.pf |= 1u << x;
+    if (op.kind == kRowLn) op.col = 0xCu;                  // gamma, beta
+    else if (op.kind == kRowFixup) op.col = 0x4u;          // bias
+  }
+  int first_gemm = -1, prev = -1;
+  for (int i = 0; i < (int)stages.size(); ++i)
+    if (stages[i].kind == kMegaGemm) {
+      if (prev >= 0) stages[prev].next_gemm = i;
+      else first_gemm = i;
+      prev = i;
+    }
+  // device blob: stage records | tensor maps (2 per GEMM stage) | ws | barrier words | stage trace
+  auto al = [](size_t v, size_t a) { return (v + a - 1) / a * a; };
+  const size_t o_st = 0;
+  const size_t o_tm = al(o_st + (size_t)kMegaRec * stages.size(), 128);
+  const size_t o_ws = al(o_tm + 128 * 2 * stages.size(), 256);
+  const size_t o_bar = al(o_ws + sizeof(float) * ws_floats, 256);
+  const size_t o_tr = o_bar + 8192;   // per-CTA words [0, 256), spread counters, go word
+  const size_t total = o_tr + sizeof(unsigned long long) * 8 * stages.size() * G;
+  CK(cudaMalloc(&e->mega_mem, total));
+  uint8_t* d = static_cast<uint8_t*>(e->mega_mem);
+  std::vector<uint8_t> h(o_bar, 0);
+  for (size_t i = 0; i < stages.size(); ++i) {
+    MegaStage& g = stages[i];
+    if (g.kind != kMegaGemm) continue;
+    const Node& gn = c->nodes[g.node];
+    uint8_t* tma = h.data() + o_tm + 256 * i;
+    if (decoder_encode_kmajor(tma, c->slots[gn.in[0]].buf, g.M, g.K, 128, g.ga) != CGX_OK ||
+        decoder_encode_kmajor(tma + 128, c->slots[gn.in[1]].static_ptr, g.N, g.K, g.bn, g.kps) != CGX_OK)
+      return fail(CGX_E_CUDA, "megakernel: cuTensorMapEncodeTiled failed (node " + std::to_string(g.node) + ")");
+    g.tmA = reinterpret_cast<uint64_t>(d + o_tm + 256 * i);
+    g.tmW = g.tmA + 128;
+    g.ws = g.deferred ? reinterpret_cast<float*>(d + o_ws) : nullptr;
+  }
+  for (auto& op : ops)
+    if (op.kind == kRowFixup) op.ws = reinterpret_cast<const float*>(d + o_ws);
+  for (size_t i = 0; i < stages.size(); ++i) {
+    uint8_t* rec = h.data() + o_st + (size_t)kMegaRec * i;
+    memcpy(rec, &stages[i], sizeof(MegaStage));
+    if (stages[i].kind == kMegaRow)
+      for (uint32_t k = 0; k < stages[i].n_ops; ++k)
+        memcpy(rec + kMegaDescStage + sizeof(MegaRowOp) * k, &ops[stages[i].op0 + k], sizeof(MegaRowOp));
+  }
+  CK(cudaMemcpy(d, h.data(), h.size(), cudaMemcpyHostToDevice));
+  CK(cudaMemset(d + o_bar, 0, total - o_bar));
+  e->mega = true;
+  e->mega_strace = reinterpret_cast<unsigned long long*>(d + o_tr);
+  e->mega_ctas = (uint32_t)G;
+  e->mega_stages = (uint32_t)stages.size();
+  Launch l;
+  l.kind = LK_KERNEL;
+  l.node = e->first;
+  l.func = kfn_mega();
+  l.grid = dim3((unsigned)G);
+  l.block = dim3(kMegaThreads);
+  l.smem = mega_smem_bytes();
+  l.pdl = !e->o.no_pdl;
+  l.coop = getenv("CGX_MEGA_NOCOOP") == nullptr;
+  l.mega = true;
+  l.args.reset(sizeof(MegaArgs));
+  MegaArgs* a = argp<MegaArgs>(l);
+  a->recs = d + o_st;
+  a->n_stages = (uint32_t)stages.size();
+  a->G = (uint32_t)G;
+  a->first_gemm = first_gemm;
+  a->table = indirect ? e->d_table : nullptr;
+  a->n_ext = (uint32_t)ext_js.size();
+  for (int i = 0; i < kMegaMaxExt; ++i) {
+    a->ext_ptr[i] = nullptr;
+    a->ext_t[i] = -1;
+  }
+  for (size_t i = 0; i < ext_js.size(); ++i) {
+    if (indirect) {
+      a->ext_t[i] = ext_js[i];
+    } else {
+      a->ext_ptr[i] = e->cur[ext_js[i]];
+      l.ext.push_back({offsetof(MegaArgs, ext_ptr) + sizeof(void*) * i, offsetof(MegaArgs, ext_t) + sizeof(int32_t) * i,
+                       ext_js[i]});
+    }
+  }
+  a->flags = reinterpret_cast<uint32_t*>(d + o_bar);
+  {
+    const char* bm = getenv("CGX_MEGA_BAR");      // measurement knobs: barrier variant / poll back-off
+    const char* bs = getenv("CGX_MEGA_BAR_NS");
+    a->bar_mode = bm ? (uint32_t)atoi(bm) : 3u;
+    a->bar_sleep_ns = bs ? (uint32_t)atoi(bs) : 0u;
+    a->null_work = getenv("CGX_MEGA_NULL") ? 1u : 0u;
+    a->dbg = getenv("CGX_MEGA_DBG") ? (uint32_t)atoi(getenv("CGX_MEGA_DBG")) : 0u;
+  }
+  a->st = dev_status(e);
+  a->ntrace = nullptr;
+  const char* tv = getenv("CGX_MEGA_TRACE");
+  a->strace = (tv && tv[0] == '1') ? e->mega_strace : nullptr;
+  e->L.clear();
+  e->L.push_back(std::move(l));
+  return CGX_OK;
+}
+
 extern "C" int cgx_exec_create_ex(cgx_chain* c, const cgx_exec_opts* opts, void* stream, cgx_exec** out) {
   if (!c || !out) return fail(CGX_E_INVALID_ARG, "exec_create: NULL argument");
   cgx_exec_opts o{};
@@ -1649,6 +2036,7 @@ extern "C" int cgx_exec_create_ex(cgx_chain* c, const cgx_exec_opts* opts, void*
   if (o.copy_impl < 0 || o.copy_impl > 2) return fail(CGX_E_INVALID_ARG, "exec_create: copy_impl");
   if (o.sync_mode < CGX_SYNC_AUTO || o.sync_mode > CGX_SYNC_DATAFLOW) return fail(CGX_E_INVALID_ARG, "exec_create: sync_mode");
   if (o.graph_streams < 0 || o.graph_streams > 64) return fail(CGX_E_INVALID_ARG, "exec_create: graph_streams (0..64)");
+  if (o.megakernel < 0 || o.megakernel > 1) return fail(CGX_E_INVALID_ARG, "exec_create: megakernel (0 or 1)");
   const int K = (int)c->nodes.size();
   if (K == 0) return fail(CGX_E_STATE, "exec_create: empty chain");
   const int first = o.first_node, last = o.n_nodes ? o.first_node + o.n_nodes - 1 : K - 1;
@@ -1703,10 +2091,14 @@ extern "C" int cgx_exec_create_ex(cgx_chain* c, const cgx_exec_opts* opts, void*
     if (ce == cudaSuccess && cnt) ce = cudaMemset(e->gemm_cnt, 0, cnt);
     if (ce != cudaSuccess) return bail(cuda_fail(ce, "gemm workspace", __LINE__));
   }
-  e->L.resize(last - first + 1);
-  e->t5_pub = (last > first && tw_capable(c->nodes[first + 1].op)) ? 1 : 0;
-  for (int k = first; k <= last; ++k)
-    if ((st = build_launch(e, k, e->L[k - first])) != CGX_OK) return bail(st);
+  if (o.megakernel) {
+    if ((st = build_mega(e)) != CGX_OK) return bail(st);
+  } else {
+    e->L.resize(last - first + 1);
+    e->t5_pub = (last > first && tw_capable(c->nodes[first + 1].op)) ? 1 : 0;
+    for (int k = first; k <= last; ++k)
+      if ((st = build_launch(e, k, e->L[k - first])) != CGX_OK) return bail(st);
+  }
   set_prewait_masks(e);
   if ((st = set_sync_flags(e)) != CGX_OK) return bail(st);
   if (const char* dv = getenv("CGX_DEBUG_NOOP"); dv && (dv[0] == '1' || dv[0] == '2') && o.mode != CGX_MODE_EAGER) {
@@ -1723,7 +2115,8 @@ extern "C" int cgx_exec_create_ex(cgx_chain* c, const cgx_exec_opts* opts, void*
       if (e->L[p].kind != LK_KERNEL) continue;
       const Node& tn = c->nodes[e->L[p].node];
       unsigned long long* nt = e->d_trace + 3 * p;
-      if (uses_elem_args(tn.op)) argp<ElemArgs>(e->L[p])->trace = nt;
+      if (e->L[p].mega) argp<MegaArgs>(e->L[p])->ntrace = nt;
+      else if (uses_elem_args(tn.op)) argp<ElemArgs>(e->L[p])->trace = nt;
       else if (tn.op == CGX_OP_LAYERNORM) argp<LnArgs>(e->L[p])->ntrace = nt;
       else if (tn.op == CGX_OP_ATTN_CAUSAL) argp<AttnArgs>(e->L[p])->ntrace = nt;
       else if (tn.op == CGX_OP_GEMM_BF16) decoder_gemm_set_node_trace(e->L[p].args.p, nt);
@@ -1787,7 +2180,7 @@ extern "C" int cgx_exec_create_ex(cgx_chain* c, const cgx_exec_opts* opts, void*
   e->st.n_graph_nodes = e->graph_nodes;
   e->st.n_deferred = 0;
   for (auto& l : e->L)
-    if (l.kind == LK_KERNEL && is_elemwise(e->c->nodes[l.node].op))
+    if (l.kind == LK_KERNEL && !l.mega && is_elemwise(e->c->nodes[l.node].op))
       e->st.n_deferred += (argp<ElemArgs>(l)->flags & kFlagDeferWait) ? 1u : 0u;
   e->st.dataflow = e->dataflow ? 1u : 0u;
   e->st.dag_streams = e->dag_used;
@@ -2216,6 +2609,19 @@ extern "C" int cgx_debug_node_trace(cgx_exec* e, uint64_t* host_out, int cap, in
   node_trace_reset(e);
   *n_out = (int)e->L.size();
   return CGX_OK;
+}
+
+// Diagnostics (megakernel exec created with CGX_MEGA_TRACE=1): [stage][cta][8] %globaltimer ns of
+// the last replay (0 start after the stage's barrier, 1 end, 2-6 phase marks, 7 barrier arrival;
+// k_mega.cu mtrace). Returns the entry count (host_out == NULL: only the count) or a negative status.
+extern "C" int cgx_debug_mega_trace(cgx_exec* e, uint64_t* host_out, int cap) {
+  if (!e) return fail(CGX_E_INVALID_ARG, "mega_trace: exec is NULL");
+  if (!e->mega) return fail(CGX_E_STATE, "mega_trace: not a megakernel exec");
+  const int n = (int)(8 * e->mega_stages * e->mega_ctas);
+  if (!host_out) return n;
+  CK(cudaStreamSynchronize(e->s));
+  CK(cudaMemcpy(host_out, e->mega_strace, sizeof(uint64_t) * std::min(cap, n), cudaMemcpyDeviceToHost));
+  return n;
 }
 
 // Diagnostics: launch GEMM node `pos` once, alone (no PDL), with per-CTA %globaltimer tracing;
