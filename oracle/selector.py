@@ -15,6 +15,20 @@ Estimates (IEEE double, left-to-right, same order as the C library so decisions 
   t_copy = t_graph + c_copy;  t_ind = t_graph + c_ind
 Decision: argmin over [t_eager, t_copy, t_ind] scanned in that order with strict '<', so ties go
 EAGER > COPY > INDIRECT (ambiguity 8). INDIRECT drops out when unavailable.
+
+Model 1 (p["model"] == 1): the replay the runtime actually deploys is the chain's dependency DAG
+(DESIGN §5), not a serial sequence, so t_graph = G + sum(delta + d_k) no longer describes it (fitting
+delta to a DAG replay gave negative values). Its replay is a list schedule of the DAG in
+chain (issue) order:
+            issue_k = (k + 1) * delta                   (the graph executor's issue interval)
+            start_k = max(issue_k, max_{j in deps(k)} fin_j + lam)   (lam: dependency latency)
+            fin_k   = start_k + g_k                     (g_k: the node's work time in that replay)
+            S       = max_k fin_k
+            t_graph = max(G, S) + F
+        with max(G, S) because back-to-back replays overlap the host launch of replay i+1 with
+        the device work of replay i (the two-resource reasoning of the eager recurrence, S:L404,
+        applied to whole replays; DESIGN §3 reading 15). For a linear chain with lam == delta and
+        G == 0 this is exactly the serial form sum_k (delta + g_k) + F (pinned in the tests).
 """
 from __future__ import annotations
 
@@ -40,9 +54,31 @@ def t_graph(G: float, delta: float, d, F: float = 0.0) -> float:
     return s + F
 
 
+def t_graph_dag(G: float, delta: float, lam: float, g, deps, F: float = 0.0) -> float:
+    """Model 1: list schedule of the dependency DAG (module docstring). deps[k] lists the indices
+    j < k the k-th node depends on. Same operation order as the C library (bit-exact)."""
+    fin = []
+    S = 0.0
+    for k, gk in enumerate(g):
+        start = (k + 1) * delta
+        for j in deps[k]:
+            c = fin[j] + lam
+            if c > start:
+                start = c
+        f = start + gk
+        fin.append(f)
+        if f > S:
+            S = f
+    return (G if G > S else S) + F
+
+
 def estimates(p: dict) -> tuple:
-    """(t_eager, t_copy, t_ind) from a profile dict with keys L, G, delta, d, c_copy, c_ind [, F]."""
-    tg = t_graph(p["G"], p["delta"], p["d"], p.get("F", 0.0))
+    """(t_eager, t_copy, t_ind) from a profile dict with keys L, G, delta, d, c_copy, c_ind [, F];
+    model 1 also lam, g, deps."""
+    if p.get("model", 0) == 1:
+        tg = t_graph_dag(p["G"], p["delta"], p["lam"], p["g"], p["deps"], p.get("F", 0.0))
+    else:
+        tg = t_graph(p["G"], p["delta"], p["d"], p.get("F", 0.0))
     return t_eager(p["L"], p["d"]), tg + p["c_copy"], tg + p["c_ind"]
 
 

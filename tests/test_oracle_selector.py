@@ -115,3 +115,73 @@ def test_estimate_path_matches_manual_sums():
     assert te == 9.0 + 3.0                       # issue_3 = 9, GPU idle before each start
     assert tc == 4.0 + 1.75 + 2.75 + 3.25 + 2.0
     assert ti == 4.0 + 1.75 + 2.75 + 3.25 + 0.5
+
+
+# ---- model 1: the dependency-DAG replay (oracle/selector.py t_graph_dag)
+
+def _paths_ending(deps, k):
+    """Every path p_1 -> ... -> p_m = k of the DAG (brute force, tiny DAGs)."""
+    if not deps[k]:
+        return [[k]]
+    out = [[k]]
+    for j in deps[k]:
+        out += [p + [k] for p in _paths_ending(deps, j)]
+    return out
+
+
+def _span_by_paths(delta, lam, g, deps):
+    """Closed form of the list schedule: fin_k = max over paths ending at k of
+    issue_{p_1} + sum_i g_{p_i} + (m - 1) lam (each max in the recurrence picks the issue time or
+    one predecessor), S = max_k fin_k. Independent of the recurrence's code path."""
+    best = 0.0
+    for k in range(len(g)):
+        for p in _paths_ending(deps, k):
+            v = (p[0] + 1) * delta + sum(g[i] for i in p) + (len(p) - 1) * lam
+            best = max(best, v)
+    return best
+
+
+def _random_dag(rnd, K):
+    return [sorted(rnd.sample(range(k), rnd.randint(0, min(k, 3)))) if k else [] for k in range(K)]
+
+
+def test_dag_model_equals_path_enumeration():
+    rnd = random.Random(7)
+    for _ in range(400):
+        K = rnd.randint(1, 7)
+        deps = _random_dag(rnd, K)
+        g = [rnd.uniform(0, 10) for _ in range(K)]
+        delta, lam = rnd.uniform(0, 3), rnd.uniform(0, 3)
+        S = _span_by_paths(delta, lam, g, deps)
+        assert abs(sel.t_graph_dag(0.0, delta, lam, g, deps) - S) <= 1e-9 * max(1.0, S)
+        G = rnd.uniform(0, 40)
+        assert abs(sel.t_graph_dag(G, delta, lam, g, deps, F=1.5) - (max(G, S) + 1.5)) <= 1e-9 * max(1.0, S)
+
+
+def test_dag_model_linear_chain_is_the_serial_form():
+    # a linear chain with lam == delta and no host bound: sum_k (delta + g_k) + F, the serial
+    # replay form of S:L413 (with G = 0); S:L417's example numbers
+    g = [10.0, 10.0]
+    assert sel.t_graph_dag(0.0, 0.5, 0.5, g, [[], [0]], F=2.0) == sel.t_graph(0.0, 0.5, g, F=2.0) == 23.0
+    rnd = random.Random(3)
+    for _ in range(100):
+        K = rnd.randint(1, 40)
+        g = [rnd.uniform(0, 5) for _ in range(K)]
+        d = rnd.uniform(0, 2)
+        chain = [[]] + [[k - 1] for k in range(1, K)]
+        assert abs(sel.t_graph_dag(0.0, d, d, g, chain) - sel.t_graph(0.0, d, g)) <= 1e-9 * K * 10
+
+
+def test_dag_model_independent_nodes_are_issue_bound():
+    # no dependencies: every node starts at its issue time; the span is max_k (k+1) delta + g_k
+    g = [5.0, 0.1, 0.1, 0.1]
+    assert sel.t_graph_dag(0.0, 1.0, 9.0, g, [[], [], [], []]) == 6.0
+    assert sel.t_graph_dag(0.0, 1.0, 9.0, [0.1, 0.1, 0.1, 5.0], [[], [], [], []]) == 9.0
+
+
+def test_dag_estimates_dispatch():
+    p = _prof(L=3.0, G=4.0, delta=0.25, d=[1.5, 2.5, 3.0], c_copy=2.0, c_ind=0.5,
+              model=1, lam=1.0, g=[1.0, 2.0, 3.0], deps=[[], [0], [0]])
+    te, tc, ti = sel.estimates(p)
+    S = max(0.25 + 1.0, 1.25 + 1.0 + 2.0, 1.25 + 1.0 + 3.0)
+    assert te == 12.0 and tc == max(4.0, S) + 2.0 and ti == max(4.0, S) + 0.5
