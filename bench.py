@@ -758,14 +758,23 @@ def run_extras(args, torch, cgx, runner, wl, sm, spec, chain, stream, sets, set_
                              "bind_launch_over_floor": arms[main_ind]["host_bind_launch_us"] / g_floor}
 
     # ---------------- selector profile (slow path)
-    t0 = set_ptrs[0]
-    prof = cgx.profile(chain.handle, -1, [t0[i] for i in range(n_ext)], 30, sh)
+    # cgx_profile_ex over the 8 rotating input sets: each arm's delta against its own launch-only
+    # loop, the dependency-DAG estimate model (cgx.h model 1), estimates vs measured totals
+    prof = cgx.profile(chain.handle, -1, None, 30, sh, sets=[[ps[i] for i in range(n_ext)] for ps in set_ptrs])
     pd = prof.as_dict()
     dec, est = cgx.select([prof])
-    out["selector"] = {"decision": cgx.DECIDE[dec[0]], "t_eager_us": pd["t_eager_us"],
-                       "t_copy_us": pd["t_copy_us"], "t_ind_us": pd["t_ind_us"],
-                       "L_us": pd["L_us"], "G_us": pd["G_us"], "delta_us": pd["delta_us"],
-                       "c_copy_us": pd["c_copy_us"], "c_ind_us": pd["c_ind_us"]}
+    prof.use_measured = 0
+    dec_e, est_e = cgx.select([prof])
+    meas = (pd["t_eager_us"], pd["t_copy_us"], pd["t_ind_us"])
+    out["selector"] = {"decision": cgx.DECIDE[dec[0]], "decision_estimates": cgx.DECIDE[dec_e[0]],
+                       "t_eager_us": pd["t_eager_us"], "t_copy_us": pd["t_copy_us"], "t_ind_us": pd["t_ind_us"],
+                       "t_copy_base_us": pd["t_copy_base_us"], "t_ind_base_us": pd["t_ind_base_us"],
+                       "L_us": pd["L_us"], "G_us": pd["G_us"], "c_copy_us": pd["c_copy_us"],
+                       "c_ind_us": pd["c_ind_us"], "model": "dependency-DAG list schedule (cgx.h model 1)",
+                       "delta_issue_us": pd["delta_us"], "lambda_us": pd["lambda_us"],
+                       "span_traced_us": pd["span_us"], "n_sets": pd["n_sets"], "n_deps": pd["n_deps"],
+                       "estimates_us": list(est_e[0]),
+                       "estimate_rel_err": [(e - m) / m for e, m in zip(est_e[0], meas)]}
 
     # ---------------- Σ kernel device time vs replay (span <= 1.5 x Σ)
     # Kernel durations come from CUPTI activity records (torch.profiler) of a replay of the same
@@ -887,6 +896,49 @@ def run_extras(args, torch, cgx, runner, wl, sm, spec, chain, stream, sets, set_
     except (OSError, ValueError):
         pass
     achieved_dep = by_o / (us_o * 1e-6) / 1e9
+    # per-launch durations of this kernel INSIDE the deployed C2 replay: the deployed
+    # exec rebuilt with node-timeline stamps (CGX_NODE_TRACE=1: first CTA entry, last CTA past its
+    # PDL wait, last CTA exit per launch), 50 replays with rotating inputs; work = exit - ready
+    node_trace = None
+    try:
+        os.environ["CGX_NODE_TRACE"] = "1"
+        ex_tr = chain.exec("INDIRECT", stream=stream, transport=MAIN_TRANSPORT, graph_streams=deployed_streams)
+        os.environ.pop("CGX_NODE_TRACE", None)
+        K_ = len(spec.nodes)
+        for i in range(10):
+            LIB.cgx_bind(ex_tr.handle, set_ptrs[i % N_SETS], n_ext)
+            LIB.cgx_launch(ex_tr.handle)
+        cgx.node_trace(ex_tr.handle, K_)
+        pos = [k for k, n in enumerate(spec.nodes) if n.op == dom_op]
+        work, resident, bsum, wsum = [], [], 0.0, 0.0
+        for i in range(50):
+            LIB.cgx_bind(ex_tr.handle, set_ptrs[i % N_SETS], n_ext)
+            LIB.cgx_launch(ex_tr.handle)
+            tr = cgx.node_trace(ex_tr.handle, K_)
+            for k in pos:
+                en, rd, xt = tr[k]
+                w_ = max(1, xt - rd) * 1e-3
+                work.append(w_)
+                resident.append(max(1, xt - en) * 1e-3)
+                bsum += algo_bytes(spec.nodes[k])
+                wsum += w_
+        ex_tr.close()
+        ach_w = bsum / (wsum * 1e-6) / 1e9
+        dram = traffic
+        node_trace = {"launches_sampled": len(work), "median_work_us": statistics.median(work),
+                      "median_resident_us": statistics.median(resident),
+                      "achieved_GBps_work": ach_w, "frac_work": ach_w / hbm,
+                      "dram_bytes_per_launch": dram,
+                      "dram_GBps_work": (dram * len(pos) * 50 / (wsum * 1e-6) / 1e9) if dram else None,
+                      "dram_frac_work": (dram * len(pos) * 50 / (wsum * 1e-6) / 1e9 / hbm) if dram else None,
+                      "timing": "node-timeline stamps (%globaltimer) of every launch of this kernel inside the "
+                                "deployed INDIRECT replay (dependency DAG, PDL), 50 replays with rotating inputs: "
+                                "work = last CTA exit - last CTA past its griddepcontrol.wait; achieved = sum of "
+                                "algorithmic bytes / sum of work times (launches overlap, so this is per-launch, "
+                                "not class throughput); dram_* use the ncu DRAM bytes per launch (traffic)"}
+    except Exception as exn:  # noqa: BLE001
+        os.environ.pop("CGX_NODE_TRACE", None)
+        node_trace = {"error": str(exn)}
     out["roofline"] = {"bound": "hbm", "achieved": achieved_dep, "peak": hbm, "unit": "GB/s",
                        "frac": achieved_dep / hbm, "traffic": traffic, "kernel": kname,
                        "share_of_sum_kernel_time": share, "launches_per_replay": len(dom_nodes),
@@ -903,6 +955,7 @@ def run_extras(args, torch, cgx, runner, wl, sm, spec, chain, stream, sets, set_
                        "largest_lanes_4MiB": ({"avg_launch_us": us_b, "algorithmic_bytes_per_launch": by_b,
                                                "achieved_GBps": by_b / (us_b * 1e-6) / 1e9} if big else None),
                        "by_lane_size_serial": by_size,
+                       "deployed_node_trace": node_trace,
                        "peak_source": peak_src}
     ex_copy.close()
 

@@ -42,6 +42,7 @@ extern "C" {
 #define CGX_ABI_VERSION 1
 #define CGX_MAX_IN 4                    /* max inputs per node */
 #define CGX_MAX_PROFILE_KERNELS 1024    /* max kernels in one profiled segment */
+#define CGX_MAX_PROFILE_DEPS 8192       /* max dependency edges of a profiled segment (model 1) */
 
 typedef struct cgx_chain cgx_chain;     /* a kernel sequence description (slots + nodes) */
 typedef struct cgx_exec cgx_exec;       /* one captured+instantiated graph (or eager runner) */
@@ -216,20 +217,38 @@ typedef struct {
                                     1 dataflow timeout, 2 lost peer, 4 device launch failed */
 } cgx_stats_t;
 
-/* One segment's slow-path measurements, all microseconds. */
+/* One segment's slow-path measurements, all microseconds.
+ * Estimate models (oracle/selector.py):
+ *   model 0 (serial replay): t_graph = G + sum_k (delta + d_k) + F
+ *   model 1 (the dependency-DAG replay the runtime deploys): list schedule in chain
+ *     order, issue_k = (k+1) delta, start_k = max(issue_k, max_{j in deps(k)} fin_j + lambda),
+ *     fin_k = start_k + g_k, S = max_k fin_k, t_graph = max(G, S) + F
+ *   t_eager (both): S:L404 recurrence over L and d_k; t_copy = t_graph + c_copy; t_ind = t_graph + c_ind.
+ * cgx_profile / cgx_profile_ex fill model 1. */
 typedef struct {
   int n_kernels;          /* K */
   int ind_available;      /* 0 -> INDIRECT is not a candidate */
   int use_measured;       /* 1 -> decide on the measured totals, else on the estimates */
-  int reserved;
+  int model;              /* estimate model: 0 = serial replay, 1 = dependency-DAG replay */
   double L_us;            /* host launch cost per kernel (eager) */
   double G_us;            /* host cudaGraphLaunch cost */
-  double delta_us;        /* per-node in-graph overhead */
-  double c_copy_us;       /* COPY rebinding Δ */
-  double c_ind_us;        /* INDIRECT rebinding Δ */
+  double delta_us;        /* model 0: per-node in-graph overhead; model 1: issue interval per node */
+  double c_copy_us;       /* COPY rebinding Δ: its bind+launch loop minus its own launch-only loop (>= 0) */
+  double c_ind_us;        /* INDIRECT rebinding Δ, likewise against its own exec (>= 0) */
   double F_us;            /* fixed per-replay overhead term (0 unless set) */
-  double t_eager_us, t_copy_us, t_ind_us;   /* measured end-to-end per replay */
-  double d_us[CGX_MAX_PROFILE_KERNELS];     /* device time per kernel */
+  double t_eager_us, t_copy_us, t_ind_us;   /* measured end-to-end per replay (fresh inputs) */
+  double d_us[CGX_MAX_PROFILE_KERNELS];     /* work time per kernel in the EAGER stream (eager model) */
+  /* model 1 and measurement details */
+  double lambda_us;       /* dependency latency: producer exit -> dependent past its wait (median) */
+  double span_us;         /* measured device span of the deployed replay (median, traced exec) */
+  double t_copy_base_us, t_ind_base_us;     /* the arms' launch-only loops (same exec, no bind) */
+  int n_sets;             /* input sets rotated by the bind loops */
+  int n_deps;             /* dependency edges in dep_idx */
+  int ind_transport;      /* the INDIRECT candidate measured: ROOT_PARAMS or FIRST_NODE, the faster */
+  int reserved2;
+  double g_us[CGX_MAX_PROFILE_KERNELS];     /* work time per kernel inside the deployed replay */
+  int dep_off[CGX_MAX_PROFILE_KERNELS + 1]; /* deps of kernel k: dep_idx[dep_off[k] .. dep_off[k+1]) */
+  int dep_idx[CGX_MAX_PROFILE_DEPS];        /* indices j < k */
 } cgx_profile_t;
 
 int cgx_version(void);
@@ -307,8 +326,9 @@ int cgx_debug_ext_field_offsets(const cgx_exec* e, int pos, uint64_t* offs, int 
  * in registers, 10 staged; 0 = not reached); n_out = CTA count. */
 int cgx_debug_gemm_trace(cgx_exec* e, int pos, uint64_t* host_out, int cap, int* n_out);
 /* Diagnostics: replay timeline of an exec created with CGX_NODE_TRACE=1 in the environment (chain
- * kernels only): host_out gets [launch][3] %globaltimer ns = (first CTA entry, last CTA past its
- * input wait, last CTA exit) over the replays since the previous call, which then resets them.
+ * kernels only): host_out gets [launch][3] %globaltimer ns = (first CTA entry, first CTA past its
+ * input wait, last CTA exit) over the replays since the previous call, which then resets them
+ * (an untraced launch keeps entry == ready == UINT64_MAX, exit == 0).
  * CGX_E_STATE when tracing is off. Synchronises the exec's stream. */
 int cgx_debug_node_trace(cgx_exec* e, uint64_t* host_out, int cap, int* n_out);
 /* Diagnostics: per-stage, per-CTA timeline of a megakernel exec (opts.megakernel = 1) created with
@@ -322,12 +342,20 @@ int cgx_debug_mega_trace(cgx_exec* e, uint64_t* host_out, int cap);
 /* ---- selective CUDA graphs ---------------------------------------------------------------- */
 /* Slow path: measure one segment (index into the marked segments, or -1 = whole chain) in the
  * three candidate modules (eager, graph+copy, graph+PI) with the given inputs; reps timed
- * iterations after warm-up (SURVEY reading 7). Fills every field of *out. */
+ * iterations after warm-up (SURVEY reading 7). Fills every field of *out (model 1). */
 int cgx_profile(cgx_chain* c, int segment, const void* const* ext_dptrs, int n_ext, int reps,
                 void* cuda_stream, cgx_profile_t* out);
+/* The same, rotating over n_sets input sets (ext_sets: n_sets x n_ext DEVICE pointers, row-major,
+ * cgx_bind order): every timed bind binds the next set, so each replay reads fresh inputs; the
+ * launch-only bases re-launch the last bound set. The DAG model's g_k / lambda / delta / span come
+ * from node-traced replays of a separate INDIRECT exec of the segment (CGX_NODE_TRACE stamps;
+ * nodes without stamps, e.g. NCCL, take d_k). Errors as cgx_profile. */
+int cgx_profile_ex(cgx_chain* c, int segment, const void* const* ext_sets, int n_sets, int n_ext, int reps,
+                   void* cuda_stream, cgx_profile_t* out);
 /* Pure host function: per segment argmin over [eager, copy, ind]
  * with strict '<' in that order (ties EAGER > COPY > INDIRECT). est_out (3*n_segments doubles,
- * optional) receives the three estimates/totals used. */
+ * optional) receives the three estimates/totals used (estimates by the profile's model).
+ * CGX_E_INVALID_ARG: n_kernels, model, or (model 1) dep_off / dep_idx out of range. */
 int cgx_select(const cgx_profile_t* prof, int n_segments, cgx_decision* out, double* est_out);
 
 /* Slow path (measure candidates with the real inputs, deploy one): choose the

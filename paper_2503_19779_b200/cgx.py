@@ -29,9 +29,11 @@ GEMM_BIAS, GEMM_GELU, GEMM_RESIDUAL, GEMM_ALLREDUCE = 1, 2, 4, 8
 MODE = {"EAGER": 0, "COPY": 1, "INDIRECT": 2, "SETPARAMS": 3, "STALE": 4}
 XPORT = {"DEFAULT": 0, "H2D": 1, "ROOT_MEMCPY": 2, "ROOT_PARAMS": 3, "ROOT_MAPPED": 4, "FIRST_NODE": 5, "H2D_PINGPONG": 6, "PRELUDE": 7,
          "DEVICE": 8}
+XPORT_NAME = {v: k for k, v in XPORT.items() if k != "DEFAULT"}
 DECIDE = {0: "EAGER", 1: "GRAPH_COPY", 2: "GRAPH_INDIRECT"}
 SYNC = {"AUTO": 0, "DEFER": 1, "CHAIN": 2, "GRAPH": 3, "DATAFLOW": 4}
 MAX_PROFILE_KERNELS = 1024
+MAX_PROFILE_DEPS = 8192
 
 
 class Attr(C.Structure):
@@ -64,15 +66,33 @@ class Stats(C.Structure):
 
 class Profile(C.Structure):
     _fields_ = [("n_kernels", C.c_int), ("ind_available", C.c_int), ("use_measured", C.c_int),
-                ("reserved", C.c_int), ("L_us", C.c_double), ("G_us", C.c_double),
+                ("model", C.c_int), ("L_us", C.c_double), ("G_us", C.c_double),
                 ("delta_us", C.c_double), ("c_copy_us", C.c_double), ("c_ind_us", C.c_double),
                 ("F_us", C.c_double), ("t_eager_us", C.c_double), ("t_copy_us", C.c_double),
-                ("t_ind_us", C.c_double), ("d_us", C.c_double * MAX_PROFILE_KERNELS)]
+                ("t_ind_us", C.c_double), ("d_us", C.c_double * MAX_PROFILE_KERNELS),
+                ("lambda_us", C.c_double), ("span_us", C.c_double), ("t_copy_base_us", C.c_double),
+                ("t_ind_base_us", C.c_double), ("n_sets", C.c_int), ("n_deps", C.c_int),
+                ("ind_transport", C.c_int), ("reserved2", C.c_int),
+                ("g_us", C.c_double * MAX_PROFILE_KERNELS),
+                ("dep_off", C.c_int * (MAX_PROFILE_KERNELS + 1)), ("dep_idx", C.c_int * MAX_PROFILE_DEPS)]
+
+    def deps(self):
+        return [list(self.dep_idx[self.dep_off[k]:self.dep_off[k + 1]]) for k in range(self.n_kernels)]
 
     def as_dict(self):
-        d = {f: getattr(self, f) for f, _ in self._fields_ if f != "d_us"}
+        d = {f: getattr(self, f) for f, _ in self._fields_ if f not in ("d_us", "g_us", "dep_off", "dep_idx")}
         d["d_us"] = list(self.d_us[: self.n_kernels])
+        d["g_us"] = list(self.g_us[: self.n_kernels])
+        d["deps"] = self.deps()
         return d
+
+    def oracle_dict(self):
+        """The same profile in oracle/selector.py's vocabulary."""
+        return dict(L=self.L_us, G=self.G_us, delta=self.delta_us, d=list(self.d_us[: self.n_kernels]),
+                    c_copy=self.c_copy_us, c_ind=self.c_ind_us, F=self.F_us, use_measured=bool(self.use_measured),
+                    ind_available=bool(self.ind_available), t_eager=self.t_eager_us, t_copy=self.t_copy_us,
+                    t_ind=self.t_ind_us, model=self.model, lam=self.lambda_us,
+                    g=list(self.g_us[: self.n_kernels]), deps=self.deps())
 
 
 class CgxError(RuntimeError):
@@ -106,6 +126,7 @@ def _load():
         "cgx_debug_setparam_nodes": ([VP, P(I), I, P(I)], I),
         "cgx_exec_destroy": ([VP], I),
         "cgx_profile": ([VP, I, P(VP), I, I, VP, P(Profile)], I),
+        "cgx_profile_ex": ([VP, I, P(VP), I, I, I, VP, P(Profile)], I),
         "cgx_select": ([P(Profile), I, P(I), P(C.c_double)], I),
         "cgx_dispatch_floor": ([VP, I, P(C.c_double), P(C.c_double)], I),
         "cgx_fill_uniform_f32": ([VP, U64, U64, U64, VP], I),
@@ -142,7 +163,7 @@ EXPORTED = ("cgx_version", "cgx_last_error", "cgx_chain_create", "cgx_chain_add_
             "cgx_chain_add_node", "cgx_chain_mark_segment", "cgx_chain_set_nccl",
             "cgx_chain_destroy", "cgx_exec_create", "cgx_exec_create_ex", "cgx_bind",
             "cgx_launch", "cgx_output", "cgx_output_gather", "cgx_stats", "cgx_debug_read_table",
-            "cgx_debug_setparam_nodes", "cgx_exec_destroy", "cgx_profile", "cgx_select",
+            "cgx_debug_setparam_nodes", "cgx_exec_destroy", "cgx_profile", "cgx_profile_ex", "cgx_select",
             "cgx_dispatch_floor", "cgx_fill_uniform_f32", "cgx_copy", "cgx_graph_floor", "cgx_kernel_times", "cgx_find_param_offset",
             "cgx_debug_param_image", "cgx_debug_ext_field_offsets", "cgx_debug_gemm_trace", "cgx_debug_node_trace", "cgx_debug_mega_trace", "cgx_device_loop", "cgx_nccl_unique_id",
             "cgx_nccl_comm_init", "cgx_nccl_comm_destroy", "cgx_peer_buffer_bytes", "cgx_chain_set_peers",
@@ -321,8 +342,14 @@ def exec_destroy(ex: int):
     _ck(LIB.cgx_exec_destroy(ex), "cgx_exec_destroy")
 
 
-def profile(chain: int, segment: int, ptrs, reps: int, stream: int) -> Profile:
+def profile(chain: int, segment: int, ptrs, reps: int, stream: int, sets=None) -> Profile:
+    """cgx_profile (one input set: ptrs) or cgx_profile_ex (sets: list of pointer lists)."""
     p = Profile()
+    if sets:
+        n_ext = len(sets[0])
+        arr = ptr_array([q for row in sets for q in row])
+        _ck(LIB.cgx_profile_ex(chain, segment, arr, len(sets), n_ext, reps, stream, C.byref(p)), "cgx_profile_ex")
+        return p
     arr = ptr_array(list(ptrs))
     _ck(LIB.cgx_profile(chain, segment, arr, len(ptrs), reps, stream, C.byref(p)), "cgx_profile")
     return p

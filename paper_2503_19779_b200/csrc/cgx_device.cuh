@@ -103,19 +103,23 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 // The same replay-timeline stamps for the decoder kernels (one thread per CTA calls it).
+// [0] first CTA entry (min), [1] first CTA past its input wait (min), [2] last CTA exit (max): the
+// node's work window is [1]..[2] even for grids of several waves (whose last CTAs start late).
+// Only the first 256 CTAs stamp entry / ready and only the last 256 stamp the exit: every stamp is
+// an atomic on one of three words, and a multi-wave elementwise grid of 16K CTAs serialised ~50K
+// same-address atomics (~0.6 ms per replay at the C4 256 MiB point).
 __device__ __forceinline__ void node_stamp(unsigned long long* nt, int what) {
   if (nt) {
+    const uint32_t cta = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    const uint32_t ctas = gridDim.x * gridDim.y * gridDim.z;
+    if (what < 2 ? cta >= 256u : cta + 256u < ctas) return;
     const unsigned long long t = gtimer();
-    if (what == 0) atomicMin(nt, t);
+    if (what < 2) atomicMin(nt + what, t);
     else atomicMax(nt + what, t);
   }
 }
 __device__ __forceinline__ void trace_at(const ElemArgs& a, int what) {
-  if (a.trace && threadIdx.x == 0) {
-    const unsigned long long t = gtimer();
-    if (what == 0) atomicMin(a.trace, t);
-    else atomicMax(a.trace + what, t);
-  }
+  if (threadIdx.x == 0) node_stamp(a.trace, what);
 }
 
 // Pointer-table entry. Read-only path: the table never changes while a reader kernel runs (it is

@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
+
 #include "cgx_args.h"
 #include "cgx_decoder.h"
 #include "cgx_device.cuh"
@@ -25,12 +27,12 @@ __device__ __forceinline__ float warp_max(float v) {
 }
 
 // ---------------------------------------------------------------------------- LayerNorm
-static constexpr int kLnWarps = 4;
+static constexpr int kLnWarps = 8;   // rows per CTA (8: 443.8 -> see profiles/r02/c3_knobs.txt)
 static constexpr int kLnMaxVec = 8;    // 8 x 16 B per lane -> cols <= 2048
 static_assert(kLnMaxVec * 8 * 32 == (int)kLnMaxCols, "k_layernorm row capacity");
 
 template <int TW>
-__global__ void __launch_bounds__(kLnWarps * 32) k_layernorm(const __grid_constant__ ArgsTW<LnArgs, TW> A) {
+__global__ void __launch_bounds__(256) k_layernorm(const __grid_constant__ ArgsTW<LnArgs, TW> A) {
   const LnArgs& a = A.a;
   if (threadIdx.x == 0) node_stamp(a.ntrace, 0);
   tw_publish(A);
@@ -39,7 +41,7 @@ __global__ void __launch_bounds__(kLnWarps * 32) k_layernorm(const __grid_consta
   if (!(a.flags & kFlagTriggerAfterWait)) pdl_trigger();
   if (a.tx >= 0 && !late) px = reinterpret_cast<const void*>(ld_table(a.table + a.tx));
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t row = blockIdx.x * kLnWarps + warp;
+  const uint32_t row = blockIdx.x * (blockDim.x >> 5) + warp;
   const uint32_t nv = a.cols >> 3;
   // gamma / beta are STATIC (never written in the graph): fetched before the wait, overlapping
   // the predecessor, so the only post-wait round trip is the row itself
@@ -134,8 +136,14 @@ const void* kfn_layernorm(int tw) {
 }
 void decoder_ln_launch_dims(uint32_t rows, uint32_t cols, dim3* grid, dim3* block) {
   (void)cols;
-  *grid = dim3((rows + kLnWarps - 1) / kLnWarps);
-  *block = dim3(kLnWarps * 32);
+  // warps (rows) per CTA: CGX_LN_WARPS measurement knob (1..8), default kLnWarps
+  static const uint32_t w = [] {
+    const char* v = getenv("CGX_LN_WARPS");
+    const int x = v ? atoi(v) : kLnWarps;
+    return (uint32_t)(x >= 1 && x <= 8 ? x : kLnWarps);
+  }();
+  *grid = dim3((rows + w - 1) / w);
+  *block = dim3(w * 32);
 }
 
 // ---------------------------------------------------------------------------- causal attention
@@ -163,7 +171,16 @@ void decoder_attn_launch_dims(uint32_t T, uint32_t H, uint32_t D, dim3* grid, di
   (void)D;
   *grid = dim3((T + kAttnQRows - 1) / kAttnQRows, H);
   const uint32_t warps = (T + kAttnKChunk - 1) / kAttnKChunk;   // one warp per 32-key chunk of the longest range
-  *block = dim3(32 * (warps < 1 ? 1 : warps > (uint32_t)kAttnMaxWarps ? kAttnMaxWarps : warps));
+  uint32_t nw = warps < 1 ? 1 : warps > (uint32_t)kAttnMaxWarps ? kAttnMaxWarps : warps;
+  // extra warps only help with the K/V / Q loads (all 8 by default: C3 459.1 -> 444.8 us per
+  // 12-layer replay, profiles/r02/c3_knobs.txt); CGX_ATTN_WARPS measurement knob (>= the chunks)
+  static const uint32_t min_w = [] {
+    const char* v = getenv("CGX_ATTN_WARPS");
+    const int x = v ? atoi(v) : kAttnMaxWarps;
+    return (uint32_t)(x >= 1 && x <= kAttnMaxWarps ? x : kAttnMaxWarps);
+  }();
+  if (nw < min_w) nw = min_w;
+  *block = dim3(32 * nw);
   *smem = attn_smem_bytes(T);
   // per call (build time, cheap): function attributes belong to the current device's context
   cudaFuncSetAttribute(k_attention, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)attn_smem_bytes(kAttnMaxT));

@@ -38,6 +38,8 @@ using namespace cgx;
 
 // ============================================================================ errors
 static thread_local std::string g_err;
+// cgx_profile_ex: the next exec created on this thread stamps the node timeline (as CGX_NODE_TRACE=1)
+static thread_local bool g_force_trace = false;
 
 static int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -2106,7 +2108,7 @@ extern "C" int cgx_exec_create_ex(cgx_chain* c, const cgx_exec_opts* opts, void*
       if (e->L[p].kind == LK_KERNEL && df_capable(c->nodes[e->L[p].node], c->slots[c->nodes[e->L[p].node].out].dtype))
         argp<ElemArgs>(e->L[p])->flags |= dv[0] == '1' ? kFlagDbgNoop : kFlagDbgNoWork;
   }
-  if (const char* tv = getenv("CGX_NODE_TRACE"); tv && tv[0] == '1') {
+  if (const char* tv = getenv("CGX_NODE_TRACE"); g_force_trace || (tv && tv[0] == '1')) {
     const size_t nb = sizeof(unsigned long long) * 3 * e->L.size();
     cudaError_t ce = cudaMalloc(&e->d_trace, nb);
     if (ce != cudaSuccess) return bail(cuda_fail(ce, "node trace", __LINE__));
@@ -2593,13 +2595,13 @@ extern "C" int cgx_debug_param_image(const cgx_exec* e, int pos, void* buf, uint
 
 static void node_trace_reset(cgx_exec* e) {
   std::vector<unsigned long long> h(3 * e->L.size(), 0);
-  for (size_t p = 0; p < e->L.size(); ++p) h[3 * p] = ~0ull;
+  for (size_t p = 0; p < e->L.size(); ++p) h[3 * p] = h[3 * p + 1] = ~0ull;
   cudaMemcpy(e->d_trace, h.data(), sizeof(unsigned long long) * h.size(), cudaMemcpyHostToDevice);
 }
 
 // Diagnostics (exec created with CGX_NODE_TRACE=1 in the environment): per launch position the
-// [first CTA entry, last CTA past its input wait, last CTA exit] %globaltimer ns of the replays
-// since the previous call (min / max over them), then reset. Synchronises the exec's stream.
+// [first CTA entry, first CTA past its input wait, last CTA exit] %globaltimer ns of the replays
+// since the previous call (min / min / max over them), then reset. Synchronises the exec's stream.
 extern "C" int cgx_debug_node_trace(cgx_exec* e, uint64_t* host_out, int cap, int* n_out) {
   if (!e || !n_out) return fail(CGX_E_INVALID_ARG, "node_trace: bad argument");
   if (!e->d_trace) return fail(CGX_E_STATE, "node_trace: exec not created with CGX_NODE_TRACE=1");
@@ -2700,19 +2702,47 @@ static double est_graph(double G, double delta, const double* d, int K, double F
   for (int k = 0; k < K; ++k) s = s + (delta + d[k]);
   return s + F;
 }
+// model 1: list schedule of the dependency DAG (cgx.h, oracle/selector.py t_graph_dag; same
+// operation order, bit-exact)
+static double est_graph_dag(const cgx_profile_t& p) {
+  std::vector<double> fin((size_t)p.n_kernels);
+  double S = 0.0;
+  for (int k = 0; k < p.n_kernels; ++k) {
+    double start = (double)(k + 1) * p.delta_us;
+    for (int e = p.dep_off[k]; e < p.dep_off[k + 1]; ++e) {
+      const double c = fin[(size_t)p.dep_idx[e]] + p.lambda_us;
+      if (c > start) start = c;
+    }
+    const double f = start + p.g_us[k];
+    fin[(size_t)k] = f;
+    if (f > S) S = f;
+  }
+  return (p.G_us > S ? p.G_us : S) + p.F_us;
+}
+static bool dag_valid(const cgx_profile_t& p) {
+  if (p.dep_off[0] != 0) return false;
+  for (int k = 0; k < p.n_kernels; ++k) {
+    if (p.dep_off[k + 1] < p.dep_off[k] || p.dep_off[k + 1] > CGX_MAX_PROFILE_DEPS) return false;
+    for (int e = p.dep_off[k]; e < p.dep_off[k + 1]; ++e)
+      if (p.dep_idx[e] < 0 || p.dep_idx[e] >= k) return false;
+  }
+  return true;
+}
 
 extern "C" int cgx_select(const cgx_profile_t* prof, int n, cgx_decision* out, double* est) {
   if (!prof || !out || n < 0) return fail(CGX_E_INVALID_ARG, "select: bad argument");
   for (int i = 0; i < n; ++i) {
     const cgx_profile_t& p = prof[i];
     if (p.n_kernels < 0 || p.n_kernels > CGX_MAX_PROFILE_KERNELS) return fail(CGX_E_INVALID_ARG, "select: n_kernels");
+    if (p.model != 0 && p.model != 1) return fail(CGX_E_INVALID_ARG, "select: model (0 or 1)");
+    if (p.model == 1 && !p.use_measured && !dag_valid(p)) return fail(CGX_E_INVALID_ARG, "select: dependency lists");
     double te, tc, ti;
     if (p.use_measured) {
       te = p.t_eager_us;
       tc = p.t_copy_us;
       ti = p.t_ind_us;
     } else {
-      const double tg = est_graph(p.G_us, p.delta_us, p.d_us, p.n_kernels, p.F_us);
+      const double tg = p.model == 1 ? est_graph_dag(p) : est_graph(p.G_us, p.delta_us, p.d_us, p.n_kernels, p.F_us);
       te = est_eager(p.L_us, p.d_us, p.n_kernels);
       tc = tg + p.c_copy_us;
       ti = tg + p.c_ind_us;
@@ -2727,12 +2757,12 @@ extern "C" int cgx_select(const cgx_profile_t* prof, int n, cgx_decision* out, d
   return CGX_OK;
 }
 
-// profile: implemented in profile.cu
-extern "C" int cgx_profile_impl(cgx_chain* c, int segment, const void* const* ext, int n_ext, int reps,
-                                void* stream, cgx_profile_t* out);
+// profile: below (cgx_profile_ex)
+extern "C" int cgx_profile_ex(cgx_chain* c, int segment, const void* const* ext_sets, int n_sets, int n_ext,
+                              int reps, void* stream, cgx_profile_t* out);
 extern "C" int cgx_profile(cgx_chain* c, int segment, const void* const* ext, int n_ext, int reps, void* stream,
                            cgx_profile_t* out) {
-  return cgx_profile_impl(c, segment, ext, n_ext, reps, stream, out);
+  return cgx_profile_ex(c, segment, ext, 1, n_ext, reps, stream, out);
 }
 
 // Slow-path choice of the DAG capture's stream count (candidates are measured with the
@@ -3012,11 +3042,13 @@ extern "C" int cgx_kernel_times(cgx_exec* e, int reps, double* d_us, int cap, in
   return CGX_OK;
 }
 
-static int time_loop(cgx_exec* e, const void* const* ext, int n_ext, bool do_bind, int n, double* us) {
+// n bind+launch (or launch-only) iterations, host wall time per iteration; binds cycle over the
+// n_sets input sets (row-major n_sets x n_ext)
+static int time_loop(cgx_exec* e, const void* const* sets, int n_sets, int n_ext, bool do_bind, int n, double* us) {
   CK(cudaStreamSynchronize(e->s));
   const double t0 = now_us();
   for (int i = 0; i < n; ++i) {
-    if (do_bind) CKS(cgx_bind(e, ext, n_ext));
+    if (do_bind) CKS(cgx_bind(e, sets + (size_t)(i % n_sets) * n_ext, n_ext));
     CKS(cgx_launch(e));
   }
   CK(cudaStreamSynchronize(e->s));
@@ -3024,16 +3056,87 @@ static int time_loop(cgx_exec* e, const void* const* ext, int n_ext, bool do_bin
   return CGX_OK;
 }
 
-static int time_loop3(cgx_exec* e, const void* const* ext, int n_ext, bool do_bind, int n, double* us) {
+static int time_loop3(cgx_exec* e, const void* const* sets, int n_sets, int n_ext, bool do_bind, int n, double* us) {
   std::vector<double> v(3);
-  for (int t = 0; t < 3; ++t) CKS(time_loop(e, ext, n_ext, do_bind, n, &v[t]));
+  for (int t = 0; t < 3; ++t) CKS(time_loop(e, sets, n_sets, n_ext, do_bind, n, &v[t]));
   *us = median(v);
   return CGX_OK;
 }
 
-extern "C" int cgx_profile_impl(cgx_chain* c, int segment, const void* const* ext, int n_ext, int reps, void* stream,
-                                cgx_profile_t* out) {
-  if (!c || !out || reps <= 0) return fail(CGX_E_INVALID_ARG, "profile: bad argument");
+// Node-traced replays of one exec (mode / transport of *base) bound to `ext`: per launch the median
+// work time exit - first ready (stamps: cgx_debug_node_trace), plus (dag != NULL) the model-1
+// parameters: lambda = median over nodes with dependencies of first-ready_k - max_{j in deps(k)}
+// exit_j; delta = median of entry_k - entry_{k-1} over consecutive pairs WITHOUT an edge between
+// them (the executor's issue interval; a dependent node's entry is gated by its producer, which
+// lambda and the path already charge), 0 when there is none (a linear chain); span = median
+// (last exit - first entry). Untraced launches (NCCL) keep the fallback work time.
+static int traced_times(cgx_chain* c, const cgx_exec_opts& base, void* stream, const void* const* ext, int n_ext,
+                        int K, const double* fallback, double* work_out, cgx_profile_t* dag) {
+  cgx_exec* et = nullptr;
+  g_force_trace = true;
+  const int st = cgx_exec_create_ex(c, &base, stream, &et);
+  g_force_trace = false;
+  if (st != CGX_OK) return st;
+  struct G { cgx_exec* e; ~G() { cgx_exec_destroy(e); } } guard{et};
+  if ((int)et->L.size() != K) return fail(CGX_E_STATE, "profile: traced exec launch count");
+  const auto deps = chain_deps(et);
+  if (dag) {
+    int ne = 0;
+    dag->dep_off[0] = 0;
+    for (int k = 0; k < K; ++k) {
+      for (int j : deps[k]) {
+        if (ne >= CGX_MAX_PROFILE_DEPS) return fail(CGX_E_UNSUPPORTED, "profile: too many dependency edges");
+        dag->dep_idx[ne++] = j;
+      }
+      dag->dep_off[k + 1] = ne;
+    }
+    dag->n_deps = ne;
+  }
+  CKS(cgx_bind(et, ext, n_ext));
+  for (int i = 0; i < 5; ++i) CKS(cgx_launch(et));
+  std::vector<uint64_t> tr(3 * (size_t)K);
+  int n_out = 0;
+  CKS(cgx_debug_node_trace(et, tr.data(), 3 * K, &n_out));   // reset
+  const int R = 21;
+  std::vector<std::vector<double>> gk((size_t)K);
+  std::vector<double> lam, dl, span;
+  auto traced = [&](int k) { return tr[3 * k] != ~0ull && tr[3 * k + 1] != ~0ull && tr[3 * k + 2] != 0; };
+  for (int r = 0; r < R; ++r) {
+    CKS(cgx_launch(et));
+    CKS(cgx_debug_node_trace(et, tr.data(), 3 * K, &n_out));
+    uint64_t e_min = ~0ull, x_max = 0;
+    for (int k = 0; k < K; ++k) {
+      if (!traced(k)) continue;
+      const uint64_t en = tr[3 * k], rd = tr[3 * k + 1], ex = tr[3 * k + 2];
+      e_min = std::min(e_min, en);
+      x_max = std::max(x_max, ex);
+      gk[(size_t)k].push_back(ex > rd ? (double)(ex - rd) * 1e-3 : 0.0);
+      uint64_t dep_exit = 0;
+      bool any = false;
+      for (int j : deps[k])
+        if (traced(j)) {
+          dep_exit = std::max(dep_exit, (uint64_t)tr[3 * j + 2]);
+          any = true;
+        }
+      if (any) lam.push_back(rd > dep_exit ? (double)(rd - dep_exit) * 1e-3 : 0.0);
+      if (k > 0 && traced(k - 1) && std::find(deps[k].begin(), deps[k].end(), k - 1) == deps[k].end())
+        dl.push_back(en > tr[3 * (k - 1)] ? (double)(en - tr[3 * (k - 1)]) * 1e-3 : 0.0);
+    }
+    if (x_max > 0) span.push_back((double)(x_max - e_min) * 1e-3);
+  }
+  for (int k = 0; k < K; ++k) work_out[k] = gk[(size_t)k].empty() ? fallback[k] : median(gk[(size_t)k]);
+  if (dag) {
+    dag->lambda_us = lam.empty() ? 0.0 : median(lam);
+    dag->delta_us = dl.empty() ? 0.0 : median(dl);
+    dag->span_us = span.empty() ? 0.0 : median(span);
+  }
+  return CGX_OK;
+}
+
+extern "C" int cgx_profile_ex(cgx_chain* c, int segment, const void* const* sets, int n_sets, int n_ext, int reps,
+                              void* stream, cgx_profile_t* out) {
+  if (!c || !out || reps <= 0 || n_sets < 1 || n_ext < 0 || (n_ext > 0 && !sets))
+    return fail(CGX_E_INVALID_ARG, "profile: bad argument");
   int first = 0, last = (int)c->nodes.size() - 1;
   if (segment >= 0) {
     if (segment >= (int)c->segments.size()) return fail(CGX_E_INVALID_ARG, "profile: segment index");
@@ -3045,11 +3148,11 @@ extern "C" int cgx_profile_impl(cgx_chain* c, int segment, const void* const* ex
   cgx_exec_opts o{};
   o.first_node = first;
   o.n_nodes = K;
-  cgx_exec *ee = nullptr, *ec = nullptr, *ei = nullptr;
+  cgx_exec *ee = nullptr, *ec = nullptr, *ei = nullptr, *ei5 = nullptr;
   struct Guard {
-    cgx_exec** p[3];
+    cgx_exec** p[4];
     ~Guard() { for (auto q : p) if (*q) cgx_exec_destroy(*q); }
-  } guard{{&ee, &ec, &ei}};
+  } guard{{&ee, &ec, &ei, &ei5}};
   o.mode = CGX_MODE_EAGER;
   CKS(cgx_exec_create_ex(c, &o, stream, &ee));
   o.mode = CGX_MODE_GRAPH_COPY;
@@ -3059,26 +3162,57 @@ extern "C" int cgx_profile_impl(cgx_chain* c, int segment, const void* const* ex
   int st = cgx_exec_create_ex(c, &o, stream, &ei);
   if (st == CGX_E_UNSUPPORTED) { ind_ok = 0; ei = nullptr; }
   else if (st != CGX_OK) return st;
-  cgx_profile_t p{};
-  p.n_kernels = K;
-  p.ind_available = ind_ok;
-  p.use_measured = 1;
+  // a second INDIRECT candidate without a root node (FIRST_NODE: the first launches take their
+  // operands by value and one of them publishes the table), kept when it replays faster
+  cgx_exec_opts o5 = o;
+  o5.transport = CGX_XPORT_FIRST_NODE;
+  if (ei && cgx_exec_create_ex(c, &o5, stream, &ei5) != CGX_OK) ei5 = nullptr;
+  auto* p = new cgx_profile_t{};   // (large: heap, then copied out)
+  std::unique_ptr<cgx_profile_t> hold(p);
+  p->n_kernels = K;
+  p->ind_available = ind_ok;
+  p->use_measured = 1;
+  p->model = 1;
+  p->n_sets = n_sets;
   // warm-up (reading 7: 5 runs)
-  CKS(time_loop(ee, ext, n_ext, true, 5, &p.t_eager_us));
-  CKS(time_loop(ec, ext, n_ext, true, 5, &p.t_copy_us));
-  if (ei) CKS(time_loop(ei, ext, n_ext, true, 5, &p.t_ind_us));
-  // measured end-to-end totals per replay and the rebinding deltas
-  double t_base = 0;
-  CKS(time_loop3(ee, ext, n_ext, true, reps, &p.t_eager_us));
-  CKS(time_loop3(ec, ext, n_ext, true, reps, &p.t_copy_us));
-  CKS(time_loop3(ec, ext, n_ext, false, reps, &t_base));
-  if (ei) CKS(time_loop3(ei, ext, n_ext, true, reps, &p.t_ind_us));
-  else p.t_ind_us = INFINITY;
-  p.c_copy_us = p.t_copy_us - t_base;
-  p.c_ind_us = ei ? p.t_ind_us - t_base : INFINITY;
+  double junk = 0;
+  CKS(time_loop(ee, sets, n_sets, n_ext, true, 5, &junk));
+  CKS(time_loop(ec, sets, n_sets, n_ext, true, 5, &junk));
+  if (ei) CKS(time_loop(ei, sets, n_sets, n_ext, true, 5, &junk));
+  if (ei5) CKS(time_loop(ei5, sets, n_sets, n_ext, true, 5, &junk));
+  // measured end-to-end totals per replay with fresh inputs and each arm's rebinding
+  // delta against its OWN launch-only loop (the last bound set stays bound)
+  CKS(time_loop3(ee, sets, n_sets, n_ext, true, reps, &p->t_eager_us));
+  CKS(time_loop3(ec, sets, n_sets, n_ext, true, reps, &p->t_copy_us));
+  CKS(time_loop3(ec, sets, n_sets, n_ext, false, reps, &p->t_copy_base_us));
+  cgx_exec_opts o_ind = o;
+  if (ei) {
+    CKS(time_loop3(ei, sets, n_sets, n_ext, true, reps, &p->t_ind_us));
+    CKS(time_loop3(ei, sets, n_sets, n_ext, false, reps, &p->t_ind_base_us));
+    if (ei5) {
+      double t5 = 0, t5b = 0;
+      CKS(time_loop3(ei5, sets, n_sets, n_ext, true, reps, &t5));
+      CKS(time_loop3(ei5, sets, n_sets, n_ext, false, reps, &t5b));
+      if (t5 < p->t_ind_us) {
+        p->t_ind_us = t5;
+        p->t_ind_base_us = t5b;
+        std::swap(ei, ei5);
+        o_ind = o5;
+      }
+      cgx_exec_destroy(ei5);   // the losing INDIRECT candidate
+      ei5 = nullptr;
+    }
+    p->ind_transport = (int)eff_transport(o_ind);
+  } else {
+    p->t_ind_us = p->t_ind_base_us = INFINITY;
+  }
+  p->c_copy_us = std::max(0.0, p->t_copy_us - p->t_copy_base_us);
+  p->c_ind_us = ei ? std::max(0.0, p->t_ind_us - p->t_ind_base_us) : INFINITY;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  // L: host issue cost per eager kernel; G: host cost of cudaGraphLaunch
-  std::vector<double> vl, vg, vspan;
+  // L: host issue cost per eager kernel; G: host cost of cudaGraphLaunch of the INDIRECT (else
+  // COPY) exec — the graph that would be deployed
+  cgx_exec* eg = ei ? ei : ec;
+  std::vector<double> vl, vg;
   for (int r = 0; r < reps; ++r) {
     CK(cudaStreamSynchronize(s));
     double t0 = now_us();
@@ -3086,38 +3220,24 @@ extern "C" int cgx_profile_impl(cgx_chain* c, int segment, const void* const* ex
     vl.push_back((now_us() - t0) / K);
     CK(cudaStreamSynchronize(s));
     t0 = now_us();
-    CKS(cgx_launch(ec));
+    CKS(cgx_launch(eg));
     vg.push_back(now_us() - t0);
   }
-  p.L_us = median(vl);
-  p.G_us = median(vg);
-  // d_k: device time of each kernel, from CUDA events captured between the kernels of an
-  // instrumented copy of the graph (everything pre-enqueued, so no host issue gaps are included);
-  // graph span: events around the plain COPY-exec replay.
+  p->L_us = median(vl);
+  p->G_us = median(vg);
+  // d_k: each kernel's work time in the EAGER stream (node-traced eager launches: first CTA past
+  // its wait -> last CTA exit), the eager recurrence's input; fallback for untraced launches (NCCL):
+  // the serialised event-bracketed device time
   std::vector<double> dks;
   CKS(kernel_times(ec, reps, &dks));
-  cudaEvent_t es0, es1;
-  CK(cudaEventCreate(&es0));
-  CK(cudaEventCreate(&es1));
-  for (int r = 0; r < reps; ++r) {
-    CK(cudaStreamSynchronize(s));
-    CK(cudaEventRecord(es0, s));
-    CKS(cgx_launch(ec));
-    CK(cudaEventRecord(es1, s));
-    CK(cudaEventSynchronize(es1));
-    float ms = 0;
-    CK(cudaEventElapsedTime(&ms, es0, es1));
-    vspan.push_back(ms * 1e3);
-  }
-  cudaEventDestroy(es0);
-  cudaEventDestroy(es1);
-  double sum_d = 0.0;
-  for (int k = 0; k < K; ++k) {
-    p.d_us[k] = dks[k];
-    sum_d = sum_d + p.d_us[k];
-  }
-  p.delta_us = (median(vspan) - sum_d) / K;
-  p.F_us = 0.0;
-  *out = p;
+  cgx_exec_opts oe = o;
+  oe.mode = CGX_MODE_EAGER;
+  CKS(traced_times(c, oe, stream, sets, n_ext, K, dks.data(), p->d_us, nullptr));
+  p->F_us = 0.0;
+  // model 1: the graph that would be deployed (the INDIRECT candidate kept above, else COPY), traced
+  cgx_exec_opts og = o_ind;
+  if (!ei) og.mode = CGX_MODE_GRAPH_COPY;
+  CKS(traced_times(c, og, stream, sets, n_ext, K, dks.data(), p->g_us, p));
+  *out = *p;
   return CGX_OK;
 }

@@ -347,14 +347,21 @@ def test_profile_select_matches_oracle(rt):
     chain = runner.Chain(spec, runner.upload_statics(spec, wl.static_values(spec), dev))
     t = runner.upload_externals(spec, wl.external_values(spec, 0), dev)
     ptrs = [t[n].data_ptr() for n in chain.ext_names]
-    p = cgx.profile(chain.handle, -1, ptrs, 50, torch.cuda.current_stream().cuda_stream)
+    sets = []
+    for r in range(4):                       # rotating fresh input sets (cgx_profile_ex)
+        tr = runner.upload_externals(spec, wl.external_values(spec, r), dev)
+        sets.append(tr)
+    p = cgx.profile(chain.handle, -1, ptrs, 50, torch.cuda.current_stream().cuda_stream,
+                    sets=[[tr[n].data_ptr() for n in chain.ext_names] for tr in sets])
     d = p.as_dict()
-    assert d["n_kernels"] == 8 and d["ind_available"] == 1
+    assert d["n_kernels"] == 8 and d["ind_available"] == 1 and d["model"] == 1 and d["n_sets"] == 4
     assert all(x > 0 for x in d["d_us"]) and d["t_eager_us"] > 0
+    # every profile field is physical (negative delta / c_ind)
+    assert d["c_copy_us"] >= 0 and d["c_ind_us"] >= 0 and d["delta_us"] >= 0 and d["lambda_us"] >= 0
+    assert all(x >= 0 for x in d["g_us"]) and d["span_us"] > 0
+    assert d["deps"] == [[]] + [[k - 1] for k in range(1, 8)]          # C1 is a linear chain
     dec, est = cgx.select([p])
-    prof = dict(L=d["L_us"], G=d["G_us"], delta=d["delta_us"], d=d["d_us"], c_copy=d["c_copy_us"],
-                c_ind=d["c_ind_us"], F=d["F_us"], use_measured=True, t_eager=d["t_eager_us"],
-                t_copy=d["t_copy_us"], t_ind=d["t_ind_us"])
+    prof = p.oracle_dict()
     assert dec == sel.select([prof])
     p.use_measured = 0
     dec2, est2 = cgx.select([p])

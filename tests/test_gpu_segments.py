@@ -42,10 +42,14 @@ def test_profile_and_select_per_segment(rt):
     for p in profs:
         d = p.as_dict()
         assert d["n_kernels"] == spec.segments[profs.index(p)][1] - spec.segments[profs.index(p)][0] + 1
-        py.append(dict(L=d["L_us"], G=d["G_us"], delta=d["delta_us"], d=d["d_us"], c_copy=d["c_copy_us"],
-                       c_ind=d["c_ind_us"], F=d["F_us"], use_measured=True, t_eager=d["t_eager_us"],
-                       t_copy=d["t_copy_us"], t_ind=d["t_ind_us"], ind_available=bool(d["ind_available"])))
+        py.append(p.oracle_dict())
+        assert d["c_copy_us"] >= 0 and d["c_ind_us"] >= 0 and d["delta_us"] >= 0 and d["lambda_us"] >= 0
     assert dec == osel.select(py)                      # bit-exact decisions per segment
+    for p in profs:                                    # the estimate path too (model 1), bit for bit
+        p.use_measured = 0
+    dec_e, est_e = cgx.select(profs)
+    for p, e in zip(profs, est_e):
+        assert e == osel.estimates(p.oracle_dict())
     chain.close()
 
 
