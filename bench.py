@@ -1115,6 +1115,14 @@ def bench_decoder(torch, cgx, runner, wl, stream, dev, peaks):
         arms[name] = timed(ex.handle, 300 if mode != "EAGER" else 50)
         if ex is not exc:
             ex.close()
+    # the same chain as ONE persistent launch (exec option megakernel): measured beside
+    # the per-node graph, not deployed (it replays slower: grid barriers ~1.8 us x 84 stages)
+    try:
+        exm = chain.exec("INDIRECT", stream=stream, megakernel=True)
+        arms["megakernel_indirect"] = timed(exm.handle, 300)
+        exm.close()
+    except Exception as exn:  # noqa: BLE001
+        arms["megakernel_indirect"] = str(exn)
     exc.close()
     res["us_per_replay"] = arms
     res["tokens_per_s_indirect"] = T * 1e6 / arms["indirect_first_node"]

@@ -3066,10 +3066,11 @@ static int time_loop3(cgx_exec* e, const void* const* sets, int n_sets, int n_ex
 // Node-traced replays of one exec (mode / transport of *base) bound to `ext`: per launch the median
 // work time exit - first ready (stamps: cgx_debug_node_trace), plus (dag != NULL) the model-1
 // parameters: lambda = median over nodes with dependencies of first-ready_k - max_{j in deps(k)}
-// exit_j; delta = median of entry_k - entry_{k-1} over consecutive pairs WITHOUT an edge between
-// them (the executor's issue interval; a dependent node's entry is gated by its producer, which
-// lambda and the path already charge), 0 when there is none (a linear chain); span = median
-// (last exit - first entry). Untraced launches (NCCL) keep the fallback work time.
+// exit_j; delta = the executor's issue interval = median over replays of (last entry - first
+// entry) / (K - 1) when the DAG has consecutive launches WITHOUT an edge between them (the
+// executor issues them back to back over its streams; their entries are not in chain order), and
+// 0 for a linear chain (every entry is gated by its producer, which lambda and the path already
+// charge); span = median (last exit - first entry). Untraced launches (NCCL) keep the fallback.
 static int traced_times(cgx_chain* c, const cgx_exec_opts& base, void* stream, const void* const* ext, int n_ext,
                         int K, const double* fallback, double* work_out, cgx_profile_t* dag) {
   cgx_exec* et = nullptr;
@@ -3101,10 +3102,14 @@ static int traced_times(cgx_chain* c, const cgx_exec_opts& base, void* stream, c
   std::vector<std::vector<double>> gk((size_t)K);
   std::vector<double> lam, dl, span;
   auto traced = [&](int k) { return tr[3 * k] != ~0ull && tr[3 * k + 1] != ~0ull && tr[3 * k + 2] != 0; };
+  bool independent = false;   // some consecutive pair of launches has no edge between them
+  for (int k = 1; k < K && !independent; ++k)
+    independent = std::find(deps[k].begin(), deps[k].end(), k - 1) == deps[k].end();
   for (int r = 0; r < R; ++r) {
     CKS(cgx_launch(et));
     CKS(cgx_debug_node_trace(et, tr.data(), 3 * K, &n_out));
-    uint64_t e_min = ~0ull, x_max = 0;
+    uint64_t e_min = ~0ull, e_max = 0, x_max = 0;
+    int n_tr = 0;
     for (int k = 0; k < K; ++k) {
       if (!traced(k)) continue;
       const uint64_t en = tr[3 * k], rd = tr[3 * k + 1], ex = tr[3 * k + 2];
@@ -3119,9 +3124,10 @@ static int traced_times(cgx_chain* c, const cgx_exec_opts& base, void* stream, c
           any = true;
         }
       if (any) lam.push_back(rd > dep_exit ? (double)(rd - dep_exit) * 1e-3 : 0.0);
-      if (k > 0 && traced(k - 1) && std::find(deps[k].begin(), deps[k].end(), k - 1) == deps[k].end())
-        dl.push_back(en > tr[3 * (k - 1)] ? (double)(en - tr[3 * (k - 1)]) * 1e-3 : 0.0);
+      e_max = std::max(e_max, en);
+      ++n_tr;
     }
+    if (independent && n_tr > 1) dl.push_back((double)(e_max - e_min) * 1e-3 / (n_tr - 1));
     if (x_max > 0) span.push_back((double)(x_max - e_min) * 1e-3);
   }
   for (int k = 0; k < K; ++k) work_out[k] = gk[(size_t)k].empty() ? fallback[k] : median(gk[(size_t)k]);
