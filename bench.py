@@ -1209,6 +1209,43 @@ def bench_decoder(torch, cgx, runner, wl, stream, dev, peaks):
                        "bound": "latency (M = 128: weight-streaming roofline 14.2 MB/layer at HBM speed "
                                 "is ~2.2 us/layer; each GEMM node runs ~5-8 us)",
                        "timing": "CUPTI kernel durations, no-PDL capture of the same chain"}
+    # the same GEMM nodes timed INSIDE the deployed replay (node-timeline stamps, 20 replays):
+    # work = last CTA exit - first CTA past its griddepcontrol.wait (the per-node hand-over gap is
+    # reported separately: first ready - the previous node's last exit)
+    try:
+        os.environ["CGX_NODE_TRACE"] = "1"
+        ext_ = chain.exec("INDIRECT", stream=stream, transport="FIRST_NODE")
+        os.environ.pop("CGX_NODE_TRACE", None)
+        K_ = len(spec.nodes)
+        for i in range(10):
+            LIB.cgx_bind(ext_.handle, ptrs[i % 4], 1)
+            LIB.cgx_launch(ext_.handle)
+        cgx.node_trace(ext_.handle, K_)
+        per_op = {}
+        for i in range(20):
+            LIB.cgx_bind(ext_.handle, ptrs[i % 4], 1)
+            LIB.cgx_launch(ext_.handle)
+            tr = cgx.node_trace(ext_.handle, K_)
+            for k, n in enumerate(spec.nodes):
+                key = n.op if n.op != "GEMM_BF16" else f"GEMM {n.attrs['N']}x{n.attrs['K']}"
+                d_ = per_op.setdefault(key, {"work": [], "gap": []})
+                d_["work"].append((tr[k][2] - tr[k][1]) * 1e-3)
+                if k > 0:
+                    d_["gap"].append((tr[k][1] - tr[k - 1][2]) * 1e-3)
+        ext_.close()
+        g_work = sum(statistics.median(v["work"]) * sum(1 for n in spec.nodes if n.op == "GEMM_BF16" and
+                     f"GEMM {n.attrs['N']}x{n.attrs['K']}" == k_) for k_, v in per_op.items() if k_.startswith("GEMM"))
+        res["deployed_node_trace"] = {
+            "per_op_median_us": {k_: {"work": statistics.median(v["work"]),
+                                      "gap": statistics.median(v["gap"]) if v["gap"] else None}
+                                 for k_, v in per_op.items()},
+            "gemm_work_sum_us": g_work, "gemm_weight_GBps_work": wb / (g_work * 1e-6) / 1e9,
+            "gemm_frac_of_hbm_work": wb / (g_work * 1e-6) / 1e9 / hbm,
+            "timing": "node-timeline stamps inside the deployed INDIRECT replay (FIRST_NODE), 20 replays; "
+                      "work = last CTA exit - first CTA past its wait, gap = first ready - previous exit"}
+    except Exception as exn:  # noqa: BLE001
+        os.environ.pop("CGX_NODE_TRACE", None)
+        res["deployed_node_trace"] = {"error": str(exn)}
     chain.close()
     return res
 
