@@ -1115,6 +1115,15 @@ def bench_decoder(torch, cgx, runner, wl, stream, dev, peaks):
         arms[name] = timed(ex.handle, 300 if mode != "EAGER" else 50)
         if ex is not exc:
             ex.close()
+    # capture-time ADD -> LAYERNORM fusion (cgx_exec_opts.fuse): 85 launches for the
+    # 108 nodes, every node output still written (bit-identical, test_c3_fused_add_layernorm)
+    for name, xp in (("indirect_first_node_fused_add_ln", "FIRST_NODE"), ("indirect_root_params_fused_add_ln", "ROOT_PARAMS")):
+        try:
+            exf = chain.exec("INDIRECT", stream=stream, transport=xp, fuse=cgx.FUSE_ADD_LN)
+            arms[name] = timed(exf.handle, 300)
+            exf.close()
+        except Exception as exn:  # noqa: BLE001
+            arms[name] = str(exn)
     # the same chain as ONE persistent launch (exec option megakernel): measured beside
     # the per-node graph, not deployed (it replays slower: grid barriers ~1.8 us x 84 stages)
     try:

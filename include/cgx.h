@@ -192,7 +192,13 @@ typedef struct {
                                CGX_E_UNSUPPORTED. Not with the FIRST_NODE transport or SYNC_DATAFLOW.
                                Every node's output slot is written as in the per-node exec, and the
                                rebinding semantics of every mode are unchanged. 0 = off (default) */
+  int fuse;                 /* capture-time fusions (bit mask, 0 = none): CGX_FUSE_ADD_LN runs a
+                               bf16 ADD and the LAYERNORM that normalises its output as ONE launch
+                               (both output slots written, bit-identical to the two kernels); the
+                               exec then has fewer launches than nodes (cgx_stats n_nodes counts
+                               nodes, kernels_per_replay launches) */
 } cgx_exec_opts;
+#define CGX_FUSE_ADD_LN 1
 
 typedef enum {
   CGX_SYNC_AUTO = 0, CGX_SYNC_DEFER = 1, CGX_SYNC_CHAIN = 2, CGX_SYNC_GRAPH = 3, CGX_SYNC_DATAFLOW = 4

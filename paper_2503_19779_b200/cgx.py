@@ -34,6 +34,7 @@ DECIDE = {0: "EAGER", 1: "GRAPH_COPY", 2: "GRAPH_INDIRECT"}
 SYNC = {"AUTO": 0, "DEFER": 1, "CHAIN": 2, "GRAPH": 3, "DATAFLOW": 4}
 MAX_PROFILE_KERNELS = 1024
 MAX_PROFILE_DEPS = 8192
+FUSE_ADD_LN = 1
 
 
 class Attr(C.Structure):
@@ -47,7 +48,7 @@ class ExecOpts(C.Structure):
     _fields_ = [("mode", C.c_int), ("transport", C.c_int), ("first_node", C.c_int),
                 ("n_nodes", C.c_int), ("no_pdl", C.c_int), ("validate", C.c_int),
                 ("copy_impl", C.c_int), ("sync_mode", C.c_int), ("graph_streams", C.c_int),
-                ("megakernel", C.c_int)]
+                ("megakernel", C.c_int), ("fuse", C.c_int)]
 
 
 class Stats(C.Structure):
@@ -221,9 +222,10 @@ def chain_destroy(chain: int):
 
 def exec_create(chain: int, mode: str, stream: int, transport: str = "DEFAULT", first_node: int = 0,
                 n_nodes: int = 0, no_pdl: bool = False, validate: int = 0, copy_impl: int = 0,
-                sync: str = "AUTO", graph_streams: int = 0, megakernel: bool = False) -> int:
+                sync: str = "AUTO", graph_streams: int = 0, megakernel: bool = False, fuse: int = 0) -> int:
+    """fuse: bit mask of capture-time fusions (FUSE_ADD_LN)."""
     o = ExecOpts(MODE[mode], XPORT[transport], first_node, n_nodes, int(no_pdl), validate, copy_impl,
-                 SYNC[sync], graph_streams, int(megakernel))
+                 SYNC[sync], graph_streams, int(megakernel), int(fuse))
     out = C.c_void_p()
     _ck(LIB.cgx_exec_create_ex(chain, C.byref(o), stream, C.byref(out)), "cgx_exec_create_ex")
     return out.value

@@ -127,7 +127,13 @@ struct LnArgs {
   int32_t tx, pad0;
   uint32_t flags, rows, cols, pad1;
   float eps;
-  unsigned long long* ntrace;   // CGX_NODE_TRACE=1: [entry min, ready max, exit max] ns (node_stamp)
+  unsigned long long* ntrace;   // CGX_NODE_TRACE=1: [entry, ready, exit] ns (node_stamp)
+  // ADD -> LAYERNORM fused at capture (cgx_exec_opts.fuse & CGX_FUSE_ADD_LN, k_layernorm<TW, true>):
+  // the LN input is h = bf16(x + add_b), written to add_out (the ADD node's slot) and normalised
+  // from registers. x / tx are then the ADD's first operand.
+  const void* add_b;
+  void* add_out;
+  int32_t tb, pad2;             // table index of an EXTERNAL add_b (-1: direct pointer)
 };
 
 struct AttnArgs {

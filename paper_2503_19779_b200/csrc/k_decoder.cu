@@ -31,7 +31,10 @@ static constexpr int kLnWarps = 8;   // rows per CTA (8: 443.8 -> see profiles/r
 static constexpr int kLnMaxVec = 8;    // 8 x 16 B per lane -> cols <= 2048
 static_assert(kLnMaxVec * 8 * 32 == (int)kLnMaxCols, "k_layernorm row capacity");
 
-template <int TW>
+// ADD: the fused ADD -> LAYERNORM pair (LnArgs::add_b / add_out): h = bf16(x + add_b) is stored to
+// the ADD's slot and normalised from registers — the same values and the same reduction order as
+// the unfused LN reading h back, so both paths are bit-identical.
+template <int TW, bool ADD>
 __global__ void __launch_bounds__(256) k_layernorm(const __grid_constant__ ArgsTW<LnArgs, TW> A) {
   const LnArgs& a = A.a;
   if (threadIdx.x == 0) node_stamp(a.ntrace, 0);
@@ -71,6 +74,8 @@ __global__ void __launch_bounds__(256) k_layernorm(const __grid_constant__ ArgsT
     }
   }
   if (a.tx >= 0 && late) px = reinterpret_cast<const void*>(ld_table(a.table + a.tx));
+  const void* pb = a.add_b;
+  if (ADD && a.tb >= 0) pb = reinterpret_cast<const void*>(ld_table(a.table + a.tb));
   if (a.flags & kFlagTriggerAfterWait) pdl_trigger();
   if (threadIdx.x == 0) node_stamp(a.ntrace, 1);
   if (row >= a.rows) {
@@ -82,6 +87,23 @@ __global__ void __launch_bounds__(256) k_layernorm(const __grid_constant__ ArgsT
 #pragma unroll
   for (int i = 0; i < kLnMaxVec; ++i)
     if (lane + i * 32 < nv) xu[i] = xr[lane + i * 32];
+  if constexpr (ADD) {   // h = bf16(x + b) (k_elem_bf16 ADD: fp32 sum, one rounding), stored
+    const uint4* br2 = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(pb) + (size_t)row * a.cols);
+    uint4* hr = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.add_out) + (size_t)row * a.cols);
+    uint4 yu[kLnMaxVec];
+#pragma unroll
+    for (int i = 0; i < kLnMaxVec; ++i)
+      if (lane + i * 32 < nv) yu[i] = br2[lane + i * 32];
+#pragma unroll
+    for (int i = 0; i < kLnMaxVec; ++i)
+      if (lane + i * 32 < nv) {
+        __nv_bfloat16* xb = reinterpret_cast<__nv_bfloat16*>(&xu[i]);
+        const __nv_bfloat16* yb = reinterpret_cast<const __nv_bfloat16*>(&yu[i]);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) xb[e] = __float2bfloat16_rn(__bfloat162float(xb[e]) + __bfloat162float(yb[e]));
+        hr[lane + i * 32] = xu[i];
+      }
+  }
   float v[kLnMaxVec][8];
   float s = 0.f;
 #pragma unroll
@@ -125,12 +147,13 @@ __global__ void __launch_bounds__(256) k_layernorm(const __grid_constant__ ArgsT
   if (a.ntrace && lane == 0) node_stamp(a.ntrace, 2);
 }
 
-const void* kfn_layernorm(int tw) {
+const void* kfn_layernorm(int tw, bool add) {
+  if (add) return tw == 0 ? (const void*)k_layernorm<0, true> : nullptr;
   switch (tw) {
-    case 0: return (const void*)k_layernorm<0>;
-    case 8: return (const void*)k_layernorm<8>;
-    case 64: return (const void*)k_layernorm<64>;
-    case 512: return (const void*)k_layernorm<512>;
+    case 0: return (const void*)k_layernorm<0, false>;
+    case 8: return (const void*)k_layernorm<8, false>;
+    case 64: return (const void*)k_layernorm<64, false>;
+    case 512: return (const void*)k_layernorm<512, false>;
   }
   return nullptr;
 }

@@ -466,6 +466,7 @@ struct Launch {
   int prio = 0;                           // launch priority (0 = default; CGX_DAG_PRIO experiment)
   bool coop = false;                      // cooperative launch (co-resident grid: the megakernel)
   bool mega = false;                      // the persistent decoder executor (args = MegaArgs)
+  int fused_add = -1;                     // CGX_FUSE_ADD_LN: the ADD node this LAYERNORM launch also runs
   cudaGraphDeviceNode_t dev_node = nullptr;
   // NCCL
   const void* nc_in = nullptr;
@@ -650,7 +651,7 @@ static void make_args(cgx_exec* e, Launch& l, bool tw) {
   l.tw_ptr_off = ptr_off;
 }
 
-static int build_launch(cgx_exec* e, int k, Launch& l) {
+static int build_launch(cgx_exec* e, int k, Launch& l, int add_k = -1) {
   cgx_chain* c = e->c;
   const Node& n = c->nodes[k];
   const cgx_mode mode = e->o.mode;
@@ -756,8 +757,32 @@ static int build_launch(cgx_exec* e, int k, Launch& l) {
           l.ext.push_back({offsetof(LnArgs, x), offsetof(LnArgs, tx), j});
         }
       }
+      if (add_k >= 0) {   // the fused ADD -> LAYERNORM pair: x = ADD.in[0], add_b = ADD.in[1]
+        const Node& an = c->nodes[add_k];
+        a->x = slot_ptr(an.in[0]);
+        a->tx = -1;
+        a->add_b = slot_ptr(an.in[1]);
+        a->tb = -1;
+        a->add_out = slot_ptr(an.out);
+        const int opnd[2] = {an.in[0], an.in[1]};
+        const size_t foff[2] = {offsetof(LnArgs, x), offsetof(LnArgs, add_b)};
+        const size_t toff[2] = {offsetof(LnArgs, tx), offsetof(LnArgs, tb)};
+        int32_t* tix[2] = {&a->tx, &a->tb};
+        const void** pix[2] = {&a->x, &a->add_b};
+        for (int i = 0; i < 2; ++i)
+          if (is_ext(opnd[i])) {
+            const int j = c->slots[opnd[i]].ext_j;
+            if (indirect) {
+              *pix[i] = nullptr;
+              *tix[i] = j;
+            } else if (patch) {
+              l.ext.push_back({foff[i], toff[i], j});
+            }
+          }
+        l.fused_add = add_k;
+      }
       decoder_ln_launch_dims(n.attr.rows, n.attr.cols, &l.grid, &l.block);
-      l.func = kfn_layernorm(twc);
+      l.func = kfn_layernorm(twc, add_k >= 0);
       return CGX_OK;
     }
     case CGX_OP_GEMM_BF16: {
@@ -959,22 +984,27 @@ static std::vector<std::vector<int>> chain_deps(const cgx_exec* e) {
   std::vector<std::vector<int>> readers(ns);
   int last_ar = -1;
   for (size_t p = 0; p < nl; ++p) {
-    const Node& n = e->c->nodes[e->L[p].node];
     auto add = [&](int q) {
       if (q < 0 || q == (int)p) return;
       for (int d : deps[p]) if (d == q) return;
       deps[p].push_back(q);
     };
-    for (int j = 0; j < n.n_in; ++j) add(last_w[n.in[j]]);
-    add(last_w[n.out]);
-    for (int r : readers[n.out]) add(r);
-    if (is_allreduce(n)) {
-      add(last_ar);
-      last_ar = (int)p;
+    // a fused ADD -> LAYERNORM launch performs both nodes' accesses, the ADD's first
+    for (int part = 0; part < 2; ++part) {
+      const int ni = part == 0 ? e->L[p].fused_add : e->L[p].node;
+      if (ni < 0) continue;
+      const Node& n = e->c->nodes[ni];
+      for (int j = 0; j < n.n_in; ++j) add(last_w[n.in[j]]);
+      add(last_w[n.out]);
+      for (int r : readers[n.out]) add(r);
+      if (is_allreduce(n)) {
+        add(last_ar);
+        last_ar = (int)p;
+      }
+      for (int j = 0; j < n.n_in; ++j) readers[n.in[j]].push_back((int)p);
+      last_w[n.out] = (int)p;
+      readers[n.out].clear();
     }
-    for (int j = 0; j < n.n_in; ++j) readers[n.in[j]].push_back((int)p);
-    last_w[n.out] = (int)p;
-    readers[n.out].clear();
   }
   return deps;
 }
@@ -1662,6 +1692,20 @@ static void exec_free(cgx_exec* e) {
 
 static void node_trace_reset(cgx_exec* e);
 
+// CGX_FUSE_ADD_LN: node k is a bf16 ADD whose output the next node, a LAYERNORM over the same
+// rows x cols, normalises; not the first two nodes of the range (the FIRST_NODE transport's
+// by-value prefix keeps one launch per node there)
+static bool fusable_add_ln(const cgx_exec* e, int k) {
+  const cgx_chain* c = e->c;
+  if (k >= e->last || k <= e->first + 1) return false;
+  const Node& a = c->nodes[k];
+  const Node& l = c->nodes[k + 1];
+  if (a.op != CGX_OP_ADD || l.op != CGX_OP_LAYERNORM || l.in[0] != a.out) return false;
+  if (c->slots[a.out].dtype != CGX_BF16 || c->slots[a.in[0]].dtype != CGX_BF16 || c->slots[a.in[1]].dtype != CGX_BF16)
+    return false;
+  return a.attr.n == (uint64_t)l.attr.rows * l.attr.cols && l.attr.cols <= kLnMaxCols && l.attr.cols % 8 == 0;
+}
+
 // ---------------------------------------------------------------- megakernel (cgx_mega.h)
 
 // Compile the exec's node range into the stages of ONE persistent launch:
@@ -2039,6 +2083,7 @@ extern "C" int cgx_exec_create_ex(cgx_chain* c, const cgx_exec_opts* opts, void*
   if (o.sync_mode < CGX_SYNC_AUTO || o.sync_mode > CGX_SYNC_DATAFLOW) return fail(CGX_E_INVALID_ARG, "exec_create: sync_mode");
   if (o.graph_streams < 0 || o.graph_streams > 64) return fail(CGX_E_INVALID_ARG, "exec_create: graph_streams (0..64)");
   if (o.megakernel < 0 || o.megakernel > 1) return fail(CGX_E_INVALID_ARG, "exec_create: megakernel (0 or 1)");
+  if (o.fuse & ~CGX_FUSE_ADD_LN) return fail(CGX_E_INVALID_ARG, "exec_create: fuse (unknown bits)");
   const int K = (int)c->nodes.size();
   if (K == 0) return fail(CGX_E_STATE, "exec_create: empty chain");
   const int first = o.first_node, last = o.n_nodes ? o.first_node + o.n_nodes - 1 : K - 1;
@@ -2096,10 +2141,17 @@ extern "C" int cgx_exec_create_ex(cgx_chain* c, const cgx_exec_opts* opts, void*
   if (o.megakernel) {
     if ((st = build_mega(e)) != CGX_OK) return bail(st);
   } else {
-    e->L.resize(last - first + 1);
     e->t5_pub = (last > first && tw_capable(c->nodes[first + 1].op)) ? 1 : 0;
-    for (int k = first; k <= last; ++k)
-      if ((st = build_launch(e, k, e->L[k - first])) != CGX_OK) return bail(st);
+    e->L.reserve((size_t)(last - first + 1));
+    for (int k = first; k <= last; ++k) {
+      e->L.emplace_back();
+      if ((o.fuse & CGX_FUSE_ADD_LN) && fusable_add_ln(e, k)) {
+        if ((st = build_launch(e, k + 1, e->L.back(), k)) != CGX_OK) return bail(st);
+        ++k;
+      } else if ((st = build_launch(e, k, e->L.back())) != CGX_OK) {
+        return bail(st);
+      }
+    }
   }
   set_prewait_masks(e);
   if ((st = set_sync_flags(e)) != CGX_OK) return bail(st);
@@ -2177,7 +2229,7 @@ extern "C" int cgx_exec_create_ex(cgx_chain* c, const cgx_exec_opts* opts, void*
   }
   int kernels = 0;
   for (auto& l : e->L) kernels += l.kind == LK_KERNEL;
-  e->st.n_nodes = (uint32_t)e->L.size();
+  e->st.n_nodes = (uint32_t)(last - first + 1);
   e->st.n_ext = (uint32_t)n_ext;
   e->st.n_graph_nodes = e->graph_nodes;
   e->st.n_deferred = 0;

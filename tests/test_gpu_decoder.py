@@ -365,3 +365,39 @@ def test_training_chain_has_no_data_copy(rt):
     f1, l1 = spec.segments[1]
     assert all(n.op != "COPY" for n in spec.nodes[f1:l1 + 1])
     assert spec.nodes[f1].op == "GEMM_BF16" and spec.nodes[f1].ins[0] == "X"
+
+
+@pytest.mark.parametrize("n_layers", [1, 12])
+def test_c3_fused_add_layernorm(rt, n_layers):
+    """Capture-time ADD -> LAYERNORM fusion (cgx_exec_opts.fuse = CGX_FUSE_ADD_LN): one launch per
+    pair, both slots written; every node output bit-identical to the unfused exec of the same arm,
+    across the rebinding arms, and node-local against the oracle."""
+    cgx, runner = rt
+    spec = wl.c3_chain(T=128, n_layers=n_layers)
+    st = wl.static_values(spec)
+    dev = torch.device("cuda:0")
+    pairs = sum(1 for k in range(2, len(spec.nodes) - 1)
+                if spec.nodes[k].op == "ADD" and spec.nodes[k + 1].op == "LAYERNORM")
+    arms = [("INDIRECT", "ROOT_PARAMS"), ("INDIRECT", "FIRST_NODE"), ("INDIRECT", "H2D_PINGPONG"),
+            ("INDIRECT", "PRELUDE"), ("COPY", "DEFAULT"), ("SETPARAMS", "DEFAULT"), ("EAGER", "DEFAULT")]
+    for mode, xp in arms:
+        chain = runner.Chain(spec, runner.upload_statics(spec, st, dev))
+        ex_f = chain.exec(mode, transport=xp, fuse=cgx.FUSE_ADD_LN)
+        ex_u = chain.exec(mode, transport=xp)
+        sf, su = ex_f.stats(), ex_u.stats()
+        assert sf["n_nodes"] == su["n_nodes"] == len(spec.nodes)
+        assert su["kernels_per_replay"] - sf["kernels_per_replay"] == pairs
+        for r in range(2):
+            t = runner.upload_externals(spec, wl.external_values(spec, r), dev)
+            got = {}
+            for ex in (ex_f, ex_u):
+                ex.bind(t)
+                ex.launch()
+                got[ex is ex_f] = {n.out: ex.output(n.out) for n in spec.nodes}
+            for k in got[True]:
+                assert np.array_equal(got[True][k], got[False][k]), (mode, xp, k)
+            if mode == "INDIRECT" and xp == "ROOT_PARAMS":
+                _node_local_check(spec, st, wl.external_values(spec, r),
+                                  {s.name: (got[True][s.name] if s.name in got[True] else None)
+                                   for s in spec.internals()})
+        chain.close()
