@@ -1191,6 +1191,12 @@ def bench_decoder(torch, cgx, runner, wl, stream, dev, peaks):
         fus = timed(fex.handle, 300)
         res["fused_residual"] = {"kernels_per_replay": len(fspec.nodes), "us_per_replay": fus,
                                  "tokens_per_s": T * 1e6 / fus}
+        # + LayerNorm folded into its consumer GEMM (fuse = CGX_FUSE_LN_GEMM): 61 launches
+        fexl = fchain.exec("INDIRECT", stream=stream, transport="FIRST_NODE", fuse=cgx.FUSE_LN_GEMM)
+        ful = timed(fexl.handle, 300)
+        res["fused_residual"]["ln_folded"] = {"kernels_per_replay": fexl.stats()["kernels_per_replay"] - 0,
+                                              "us_per_replay": ful, "tokens_per_s": T * 1e6 / ful}
+        fexl.close()
         fchain.close()
     except Exception as exn:  # noqa: BLE001
         res["fused_residual"] = {"error": str(exn)}

@@ -192,13 +192,19 @@ typedef struct {
                                CGX_E_UNSUPPORTED. Not with the FIRST_NODE transport or SYNC_DATAFLOW.
                                Every node's output slot is written as in the per-node exec, and the
                                rebinding semantics of every mode are unchanged. 0 = off (default) */
-  int fuse;                 /* capture-time fusions (bit mask, 0 = none): CGX_FUSE_ADD_LN runs a
+  int fuse;                 /* capture-time fusions (bit mask, 0 = none). CGX_FUSE_ADD_LN runs a
                                bf16 ADD and the LAYERNORM that normalises its output as ONE launch
-                               (both output slots written, bit-identical to the two kernels); the
-                               exec then has fewer launches than nodes (cgx_stats n_nodes counts
-                               nodes, kernels_per_replay launches) */
+                               (both output slots written, bit-identical to the two kernels).
+                               CGX_FUSE_LN_GEMM runs a LAYERNORM inside the A prologue of the GEMM
+                               that consumes it when the LN input comes from the previous GEMM
+                               launch: that GEMM writes per-tile row sums, the consumer normalises
+                               A in shared memory and stores the LN output slot (mean / variance
+                               from the sums: not bit-identical to the LN kernel, within the bf16
+                               tolerance). The exec then has fewer launches than nodes (cgx_stats
+                               n_nodes counts nodes, kernels_per_replay launches) */
 } cgx_exec_opts;
 #define CGX_FUSE_ADD_LN 1
+#define CGX_FUSE_LN_GEMM 2
 
 typedef enum {
   CGX_SYNC_AUTO = 0, CGX_SYNC_DEFER = 1, CGX_SYNC_CHAIN = 2, CGX_SYNC_GRAPH = 3, CGX_SYNC_DATAFLOW = 4
@@ -337,6 +343,9 @@ int cgx_debug_gemm_trace(cgx_exec* e, int pos, uint64_t* host_out, int cap, int*
  * (an untraced launch keeps entry == ready == UINT64_MAX, exit == 0).
  * CGX_E_STATE when tracing is off. Synchronises the exec's stream. */
 int cgx_debug_node_trace(cgx_exec* e, uint64_t* host_out, int cap, int* n_out);
+/* Diagnostics: the chain node each launch position runs (a fused launch reports its last node;
+ * cgx_exec_opts.fuse / megakernel make launches fewer than nodes). *n_out = launch count. */
+int cgx_debug_launch_nodes(const cgx_exec* e, int* nodes_out, int cap, int* n_out);
 /* Diagnostics: per-stage, per-CTA timeline of a megakernel exec (opts.megakernel = 1) created with
  * CGX_MEGA_TRACE=1: host_out gets [stage][cta][8] %globaltimer ns of the last replay (0 = start
  * after the stage's barrier, 1 = end, 2-6 = phase marks of the stage kind, 7 = barrier arrival;

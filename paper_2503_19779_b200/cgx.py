@@ -35,6 +35,7 @@ SYNC = {"AUTO": 0, "DEFER": 1, "CHAIN": 2, "GRAPH": 3, "DATAFLOW": 4}
 MAX_PROFILE_KERNELS = 1024
 MAX_PROFILE_DEPS = 8192
 FUSE_ADD_LN = 1
+FUSE_LN_GEMM = 2
 
 
 class Attr(C.Structure):
@@ -140,6 +141,7 @@ def _load():
         "cgx_debug_gemm_trace": ([VP, I, P(U64), I, P(I)], I),
         "cgx_debug_node_trace": ([VP, P(U64), I, P(I)], I),
         "cgx_debug_mega_trace": ([VP, P(U64), I], I),
+        "cgx_debug_launch_nodes": ([VP, P(I), I, P(I)], I),
         "cgx_device_loop": ([VP, VP, I, U64], I),
         "cgx_nccl_unique_id": ([VP], I),
         "cgx_nccl_comm_init": ([I, I, VP, I, P(VP)], I),
@@ -166,7 +168,7 @@ EXPORTED = ("cgx_version", "cgx_last_error", "cgx_chain_create", "cgx_chain_add_
             "cgx_launch", "cgx_output", "cgx_output_gather", "cgx_stats", "cgx_debug_read_table",
             "cgx_debug_setparam_nodes", "cgx_exec_destroy", "cgx_profile", "cgx_profile_ex", "cgx_select",
             "cgx_dispatch_floor", "cgx_fill_uniform_f32", "cgx_copy", "cgx_graph_floor", "cgx_kernel_times", "cgx_find_param_offset",
-            "cgx_debug_param_image", "cgx_debug_ext_field_offsets", "cgx_debug_gemm_trace", "cgx_debug_node_trace", "cgx_debug_mega_trace", "cgx_device_loop", "cgx_nccl_unique_id",
+            "cgx_debug_param_image", "cgx_debug_ext_field_offsets", "cgx_debug_gemm_trace", "cgx_debug_node_trace", "cgx_debug_mega_trace", "cgx_debug_launch_nodes", "cgx_device_loop", "cgx_nccl_unique_id",
             "cgx_nccl_comm_init", "cgx_nccl_comm_destroy", "cgx_peer_buffer_bytes", "cgx_chain_set_peers",
             "cgx_device_alloc", "cgx_device_free",
             "cgx_ipc_handle", "cgx_ipc_open", "cgx_ipc_close", "cgx_tune_graph_streams")
@@ -338,6 +340,15 @@ def node_trace(ex: int, n_launch: int) -> list:
     buf = (C.c_uint64 * (3 * n_launch))()
     _ck(LIB.cgx_debug_node_trace(ex, buf, 3 * n_launch, C.byref(n)), "cgx_debug_node_trace")
     return [tuple(buf[3 * i: 3 * i + 3]) for i in range(n.value)]
+
+
+def launch_nodes(ex: int) -> list:
+    """Chain node index of every launch position (cgx_debug_launch_nodes)."""
+    n = C.c_int()
+    _ck(LIB.cgx_debug_launch_nodes(ex, None, 0, C.byref(n)), "cgx_debug_launch_nodes")
+    buf = (C.c_int * max(1, n.value))()
+    _ck(LIB.cgx_debug_launch_nodes(ex, buf, n.value, C.byref(n)), "cgx_debug_launch_nodes")
+    return list(buf[: n.value])
 
 
 def exec_destroy(ex: int):

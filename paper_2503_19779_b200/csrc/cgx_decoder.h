@@ -56,4 +56,16 @@ void decoder_gemm_set_trace(void* args, unsigned long long* trace);
 // 3-D K-major bf16 operand map {64, rows, K/64}, box {64, box_rows, group}, SW128 (the layout both
 // tcgen05 kernels stage: G stacked [box_rows][128 B] tiles), written to tm (128 B, 64-B aligned).
 int decoder_encode_kmajor(void* tm, const void* base, uint64_t rows, uint64_t K, uint32_t box_rows, uint32_t group);
+// LayerNorm folded into the consumer GEMM (exec option fuse & CGX_FUSE_LN_GEMM): the producer GEMM
+// writes per-tile row sums of its bf16 output (stats: [grid.x][M] float2); the consumer streams the
+// gamma-scaled weights W' with A = the LN's input h and corrects each output row in its epilogue
+// (k_gemm.cu kGemmLnA), and stores the LN output slot. decoder_ln_fold_prep builds W', c1, c2 once
+// (synchronous). CGX_E_UNSUPPORTED when the launch cannot (all-reduce epilogue, split shape, smem).
+int decoder_gemm_set_stats_out(void* args, void* stats, dim3 grid);
+int decoder_gemm_set_ln_a(void* args, dim3 grid, const void* stats, uint32_t ntiles, const void* h, const void* w_fold,
+                          const float* c1, const float* c2, const void* gamma, const void* beta, void* ln_out,
+                          float eps, size_t* smem, const void** func);
+int decoder_ln_fold_prep(const void* W, const void* gamma, const void* beta, uint32_t N, uint32_t K, void* wf,
+                         float* c1, float* c2);
+bool decoder_gemm_is_tcgen05(const void* func);
 }  // namespace cgx

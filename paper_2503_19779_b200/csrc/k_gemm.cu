@@ -67,6 +67,20 @@ static constexpr uint32_t kGemmADynamic = 1u << 12;
 // a node runs once per replay and replays are stream-serialised: the map is built pre-wait.
 static constexpr uint32_t kGemmADynAfterWait = 1u << 13;
 static constexpr uint32_t kGemmFenceOnWait = 1u << 14;   // experiment: tcgen05 fence only after a barrier wait
+// LayerNorm folded into the GEMM (exec option fuse & CGX_FUSE_LN_GEMM). With
+// a = LN(h) = (h - mean) * rstd * gamma + beta:
+//   a W^T [m, n] = rstd_m * (h W'^T)[m, n] - rstd_m * mean_m * c1[n] + c2[n],
+//   W' = bf16(gamma * W) (per column k), c1[n] = sum_k W'[n, k], c2[n] = sum_k beta_k W[n, k],
+// so the MMAs run on the LN's INPUT h with the gamma-scaled weights W' (prepared once at exec
+// creation, cgx_ln_fold_prep) and the epilogue applies the row correction before bias / GELU /
+// residual; mean / rstd come from the row sums the producer GEMM wrote (kGemmStatsOut). While the
+// MMAs run, the epilogue warps of every CTA also store a slice of a = LN(h) to the LN node's output
+// slot, so every node output is still materialised.
+static constexpr uint32_t kGemmLnA = 1u << 15;
+static constexpr uint32_t kLnMaxTiles = 64;   // producer N tiles whose row sums a kGemmLnA GEMM combines
+// This GEMM's epilogue writes per-row {sum, sum of squares} of its bf16 output tile to
+// stats_out[n_tile][M] (float2) for a kGemmLnA consumer.
+static constexpr uint32_t kGemmStatsOut = 1u << 16;
 
 struct alignas(64) GemmArgs {
   CUtensorMap tmA;            // A [M, K] bf16 as 3-D {64, M, K/64}, box {64, 128, group}
@@ -95,7 +109,17 @@ struct alignas(64) GemmArgs {
   __nv_bfloat16* ar_recv[kArMaxWorld];
   uint32_t* ar_flags[kArMaxWorld];
   DevStatus st;               // spin bound / lost-peer report (CGX_GEMM_ALLREDUCE)
-  unsigned long long* ntrace; // CGX_NODE_TRACE=1: replay timeline [entry min, ready max, exit max] ns
+  unsigned long long* ntrace; // CGX_NODE_TRACE=1: replay timeline [entry, ready, exit] ns
+  float2* stats_out;          // kGemmStatsOut: [N / BN][M] row sums of this GEMM's output
+  const float2* ln_stats;     // kGemmLnA: the producer's [ln_ntiles][M] row sums of h
+  const __nv_bfloat16* ln_g;  // kGemmLnA: gamma / beta [K]
+  const __nv_bfloat16* ln_b;
+  __nv_bfloat16* ln_out;      // kGemmLnA: the LN node's output slot [M][K]
+  const __nv_bfloat16* ln_h;  // kGemmLnA: the LN input h [M][K] (also A)
+  const float* ln_c1;         // kGemmLnA: [N] row sums of W'
+  const float* ln_c2;         // kGemmLnA: [N] beta . W
+  uint32_t ln_ntiles;
+  float ln_eps;
 };
 
 __device__ __forceinline__ void trace_at(const GemmArgs& a, int slot) {
@@ -183,6 +207,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
   uint64_t* recv_full = tmem_full + 1;
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(recv_full + 1);   // [0] TMEM address, [1] AR generation
   uint32_t* s_tm = reinterpret_cast<uint32_t*>((reinterpret_cast<uintptr_t>(s_tmem + 4) + 127) & ~uintptr_t(127));
+  float2* s_mr = reinterpret_cast<float2*>(s_tm + 32);              // kGemmLnA: [128] (mean, rstd) per tile row
+  float2* s_cc = s_mr + kBM;                                         // kGemmLnA: [BN] (c1, c2) of the tile's columns
+  // the folded LayerNorm is a runtime flag of the one kernel, not a separate instantiation: a
+  // dedicated <BN, AR, LN> kernel (128 vs 164 registers) replayed the fused-LN C3 chain in 424 us
+  // against 379 us for this generic one, every other node unchanged (profiles/r02/c3_fuse_ln_gemm.txt)
+  const bool ln_a = a.flags & kGemmLnA;
 
   if (threadIdx.x == 0) {
     trace_at(a, 0);
@@ -353,6 +383,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
     if (has_bias && (a.flags & kGemmWAfterWait)) pdl_wait();
     for (uint32_t i = et; i < (uint32_t)BN; i += 128u)
       sbias[i] = has_bias ? __bfloat162float(a.bias[n0 + i]) : 0.f;
+    if (ln_a)   // the fold's column terms (prepared at exec creation: STATIC, before the wait)
+      for (uint32_t i = et; i < (uint32_t)BN; i += 128u) s_cc[i] = make_float2(a.ln_c1[n0 + i], a.ln_c2[n0 + i]);
     const uint32_t cta_lin = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
     uint32_t& s_ar_g = s_tmem[1];                  // dynamic smem word after the TMEM address
     if (ar && et == 0) {
@@ -389,7 +421,65 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
         }
       }
     }
-    asm volatile("bar.sync 1, 128;\n" ::: "memory");   // bias slice staged
+    asm volatile("bar.sync 1, 128;\n" ::: "memory");   // bias slice (and LN gamma / beta) staged
+    if (ln_a) {
+      // ---- folded LayerNorm (kGemmLnA): this thread's tile row statistics from the producer's
+      // per-tile row sums (fixed tile order) into shared memory, then — while the MMAs run — this
+      // CTA's share of the LN output slot a = (h - mean) * rstd * gamma + beta (16-B chunks of the
+      // [M, K] matrix dealt round-robin over all CTAs of the grid), one bf16 rounding.
+      pdl_wait();
+      {
+        const int m = m0 + (int)row;
+        float mean = 0.f, rstd = 0.f;
+        if (m < (int)a.M) {
+          float s1 = 0.f, s2 = 0.f;                // the tiles' sums in fixed tile order
+          for (uint32_t t = 0; t < a.ln_ntiles; ++t) {
+            const float2 v = __ldcg(a.ln_stats + (size_t)t * a.M + m);
+            s1 += v.x;
+            s2 += v.y;
+          }
+          mean = s1 / (float)a.K;
+          const float var = fmaxf(s2 / (float)a.K - mean * mean, 0.f);
+          rstd = 1.0f / sqrtf(var + a.ln_eps);
+        }
+        s_mr[row] = make_float2(mean, rstd);
+      }
+      asm volatile("bar.sync 1, 128;\n" ::: "memory");
+      const uint32_t nctas = gridDim.x * gridDim.y * gridDim.z;
+      const uint32_t kc = a.K / 8;                       // 16-B chunks per row
+      const uint64_t chunks = (uint64_t)a.M * kc;
+      for (uint64_t i = (uint64_t)cta_lin * 128u + et; i < chunks; i += (uint64_t)nctas * 128u) {
+        const uint32_t mm = (uint32_t)(i / kc), k8 = (uint32_t)(i % kc) * 8;
+        // the row's statistics: from shared memory when the row is in this CTA's M tile, else
+        // recomputed from the sums (only when T > 128 spreads rows over several M tiles)
+        float2 mr;
+        if ((int)mm >= m0 && (int)mm < m0 + (int)kBM) {
+          mr = s_mr[mm - m0];
+        } else {
+          float s1 = 0.f, s2 = 0.f;
+          for (uint32_t t = 0; t < a.ln_ntiles; ++t) {
+            const float2 v = __ldcg(a.ln_stats + (size_t)t * a.M + mm);
+            s1 += v.x;
+            s2 += v.y;
+          }
+          const float mean = s1 / (float)a.K;
+          mr = make_float2(mean, 1.0f / sqrtf(fmaxf(s2 / (float)a.K - mean * mean, 0.f) + a.ln_eps));
+        }
+        const uint4 hx = *reinterpret_cast<const uint4*>(a.ln_h + (size_t)mm * a.K + k8);
+        const uint4 gx = __ldg(reinterpret_cast<const uint4*>(a.ln_g + k8));
+        const uint4 bx = __ldg(reinterpret_cast<const uint4*>(a.ln_b + k8));
+        const __nv_bfloat16* hb = reinterpret_cast<const __nv_bfloat16*>(&hx);
+        const __nv_bfloat16* gb = reinterpret_cast<const __nv_bfloat16*>(&gx);
+        const __nv_bfloat16* bb = reinterpret_cast<const __nv_bfloat16*>(&bx);
+        uint4 y;
+        __nv_bfloat16* yb = reinterpret_cast<__nv_bfloat16*>(&y);
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          yb[e] = __float2bfloat16_rn((__bfloat162float(hb[e]) - mr.x) * mr.y * __bfloat162float(gb[e]) +
+                                      __bfloat162float(bb[e]));
+        *reinterpret_cast<uint4*>(a.ln_out + (size_t)mm * a.K + k8) = y;
+      }
+    }
     mbar_wait(tmem_full, 0);
     tc_fence_after();
     if (threadIdx.x == 64) trace_at(a, 8);
@@ -404,6 +494,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
       const int m = m0 + (int)row;
       if (m < (int)a.M) {
         uint4* op = reinterpret_cast<uint4*>(a.out + (size_t)m * a.N + n0);
+        if (ln_a) {   // folded LayerNorm: rstd * acc - rstd * mean * c1 + c2
+          const float2 mr = s_mr[row];
+#pragma unroll
+          for (int i = 0; i < BN; ++i) v[i] = mr.y * v[i] - mr.y * mr.x * s_cc[i].x + s_cc[i].y;
+        }
 #pragma unroll
         for (int c8 = 0; c8 < BN / 8; ++c8) {
           const float4 b0 = *reinterpret_cast<const float4*>(sbias + 8 * c8);
@@ -424,12 +519,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
             for (int i = 0; i < 8; ++i) v[8 * c8 + i] += __bfloat162float(rb[i]);
           }
         }
+        float q1 = 0.f, q2 = 0.f;                  // kGemmStatsOut: row sums of the rounded output
 #pragma unroll
         for (int c8 = 0; c8 < BN / 8; ++c8) {
           uint4 o;
           __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(&o);
 #pragma unroll
-          for (int i = 0; i < 8; ++i) ob[i] = __float2bfloat16_rn(v[8 * c8 + i]);
+          for (int i = 0; i < 8; ++i) {
+            ob[i] = __float2bfloat16_rn(v[8 * c8 + i]);
+            const float y = __bfloat162float(ob[i]);
+            q1 += y;
+            q2 += y * y;
+          }
           if (!ar) {
             op[c8] = o;
           } else {                                 // this rank's bf16 tile row -> slot `rank` everywhere
@@ -438,6 +539,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
               reinterpret_cast<uint4*>(ar_slot_ptr(a, p, par, a.ar_rank) + (size_t)m * a.N + n0)[c8] = o;
           }
         }
+        if (a.flags & kGemmStatsOut) a.stats_out[(size_t)blockIdx.x * a.M + m] = make_float2(q1, q2);
       }
       if (ar) {
         const uint32_t g = s_ar_g;
@@ -504,7 +606,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
           acc.z += t.z;
           acc.w += t.w;
         }
-        if (mr >= (int)a.M) continue;
+        const bool valid = mr < (int)a.M;
+        if (ln_a) {   // folded LayerNorm: rstd * acc - rstd * mean * c1 + c2 (after the split sum)
+          const float2 m2 = s_mr[my_lo + r];
+          acc.x = m2.y * acc.x - m2.y * m2.x * s_cc[c].x + s_cc[c].y;
+          acc.y = m2.y * acc.y - m2.y * m2.x * s_cc[c + 1].x + s_cc[c + 1].y;
+          acc.z = m2.y * acc.z - m2.y * m2.x * s_cc[c + 2].x + s_cc[c + 2].y;
+          acc.w = m2.y * acc.w - m2.y * m2.x * s_cc[c + 3].x + s_cc[c + 3].y;
+        }
         float w[4] = {acc.x + sbias[c], acc.y + sbias[c + 1], acc.z + sbias[c + 2], acc.w + sbias[c + 3]};
         if (gelu) {
 #pragma unroll
@@ -519,6 +628,26 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
         __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(&ov);
 #pragma unroll
         for (int i = 0; i < 4; ++i) ob[i] = __float2bfloat16_rn(w[i]);
+        if (a.flags & kGemmStatsOut) {
+          // row sums of the ROUNDED output for a fused LN consumer: the kQRow threads holding this
+          // row's quads are consecutive lanes (every lane of the warp takes part: the planner keeps
+          // my_rows * kQRow a multiple of 32), reduced by a fixed shuffle tree
+          float q1 = 0.f, q2 = 0.f;
+          if (valid)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float y = __bfloat162float(ob[i]);
+              q1 += y;
+              q2 += y * y;
+            }
+#pragma unroll
+          for (uint32_t o = kQRow / 2; o > 0; o >>= 1) {
+            q1 += __shfl_xor_sync(0xffffffffu, q1, o);
+            q2 += __shfl_xor_sync(0xffffffffu, q2, o);
+          }
+          if (valid && qi % kQRow == 0) a.stats_out[(size_t)blockIdx.x * a.M + mr] = make_float2(q1, q2);
+        }
+        if (!valid) continue;
         if (!ar) {
           *reinterpret_cast<uint2*>(a.out + (size_t)mr * a.N + n0 + c) = ov;
         } else {                                   // this rank's bf16 quad -> slot `rank` everywhere
@@ -800,6 +929,93 @@ static void pick_tiling(uint32_t M, uint32_t N, uint32_t K, int* bn_out, uint32_
 int decoder_encode_kmajor(void* tm, const void* base, uint64_t rows, uint64_t K, uint32_t box_rows, uint32_t group) {
   if (get_encode() != CGX_OK) return CGX_E_CUDA;
   return encode_kmajor(static_cast<CUtensorMap*>(tm), base, rows, K, box_rows, group);
+}
+
+int decoder_gemm_set_stats_out(void* args, void* stats, dim3 grid) {
+  GemmArgs* g = static_cast<GemmArgs*>(args);
+  if (g->flags & CGX_GEMM_ALLREDUCE) return CGX_E_UNSUPPORTED;
+  const uint32_t S = grid.z, bn = g->N / grid.x, rows = split_rows_max_h(S);
+  // every lane of an owner warp takes part in the row-sum shuffles: my_rows * BN / 4 % 32 == 0
+  if (g->split != S || (S != 1 && ((128u % S) != 0 || (rows * (bn / 4)) % 32 != 0))) return CGX_E_UNSUPPORTED;
+  g->stats_out = static_cast<float2*>(stats);
+  g->flags |= kGemmStatsOut;
+  return CGX_OK;
+}
+
+int decoder_gemm_set_ln_a(void* args, dim3 grid, const void* stats, uint32_t ntiles, const void* h, const void* w_fold,
+                          const float* c1, const float* c2, const void* gamma, const void* beta, void* ln_out,
+                          float eps, size_t* smem, const void** func) {
+  GemmArgs* g = static_cast<GemmArgs*>(args);
+  if (g->flags & CGX_GEMM_ALLREDUCE) return CGX_E_UNSUPPORTED;
+  if (get_encode() != CGX_OK) return CGX_E_CUDA;
+  const uint32_t bn = g->N / grid.x;
+  if (ntiles > kLnMaxTiles) return CGX_E_UNSUPPORTED;
+  const size_t extra = 128 + (size_t)kBM * 8 + (size_t)bn * 8;
+  if (*smem + extra > kSmemLimit) return CGX_E_UNSUPPORTED;
+  // the MMAs stream the gamma-scaled weights W'
+  if (encode_kmajor(&g->tmB, w_fold, g->N, g->K, bn, g->gw) != CGX_OK) return CGX_E_CUDA;
+  g->w_ptr = static_cast<const __nv_bfloat16*>(w_fold);
+  *smem += extra;
+  g->ln_stats = static_cast<const float2*>(stats);
+  g->ln_ntiles = ntiles;
+  g->ln_h = static_cast<const __nv_bfloat16*>(h);
+  g->ln_c1 = c1;
+  g->ln_c2 = c2;
+  g->ln_g = static_cast<const __nv_bfloat16*>(gamma);
+  g->ln_b = static_cast<const __nv_bfloat16*>(beta);
+  g->ln_out = static_cast<__nv_bfloat16*>(ln_out);
+  g->ln_eps = eps;
+  g->flags |= kGemmLnA;
+  (void)func;   // the same kernel (kGemmLnA is a runtime flag)
+  return CGX_OK;
+}
+
+// Exec-creation prep of a folded LayerNorm (one CTA per output column n, fixed reduction order):
+// W'[n, k] = bf16(gamma_k * W[n, k]), c1[n] = sum_k W'[n, k], c2[n] = sum_k beta_k * W[n, k]
+// (fp64 accumulation, rounded once to fp32).
+__global__ void k_ln_fold_prep(const __nv_bfloat16* W, const __nv_bfloat16* gamma, const __nv_bfloat16* beta,
+                               uint32_t K, __nv_bfloat16* wf, float* c1, float* c2) {
+  const uint32_t n = blockIdx.x;
+  __shared__ double red[2][32];
+  double s1 = 0.0, s2 = 0.0;
+  for (uint32_t k = threadIdx.x; k < K; k += blockDim.x) {
+    const float w = __bfloat162float(W[(size_t)n * K + k]);
+    const __nv_bfloat16 wq = __float2bfloat16_rn(__bfloat162float(gamma[k]) * w);
+    wf[(size_t)n * K + k] = wq;
+    s1 += (double)__bfloat162float(wq);
+    s2 += (double)__bfloat162float(beta[k]) * (double)w;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = s1;
+    red[1][threadIdx.x >> 5] = s2;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t1 = 0.0, t2 = 0.0;
+    for (uint32_t w = 0; w < blockDim.x / 32; ++w) {
+      t1 += red[0][w];
+      t2 += red[1][w];
+    }
+    c1[n] = (float)t1;
+    c2[n] = (float)t2;
+  }
+}
+
+int decoder_ln_fold_prep(const void* W, const void* gamma, const void* beta, uint32_t N, uint32_t K, void* wf,
+                         float* c1, float* c2) {
+  k_ln_fold_prep<<<N, 256>>>(static_cast<const __nv_bfloat16*>(W), static_cast<const __nv_bfloat16*>(gamma),
+                             static_cast<const __nv_bfloat16*>(beta), K, static_cast<__nv_bfloat16*>(wf), c1, c2);
+  const cudaError_t e = cudaDeviceSynchronize();
+  return e == cudaSuccess ? CGX_OK : CGX_E_CUDA;
+}
+
+bool decoder_gemm_is_tcgen05(const void* func) {
+  return func == (const void*)k_gemm_bf16<32, false> || func == (const void*)k_gemm_bf16<64, false> ||
+         func == (const void*)k_gemm_bf16<128, false>;
 }
 
 void decoder_gemm_plan(uint32_t, uint32_t, uint32_t, size_t* ws_bytes, size_t* cnt_bytes) {

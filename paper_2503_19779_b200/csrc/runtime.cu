@@ -466,7 +466,8 @@ struct Launch {
   int prio = 0;                           // launch priority (0 = default; CGX_DAG_PRIO experiment)
   bool coop = false;                      // cooperative launch (co-resident grid: the megakernel)
   bool mega = false;                      // the persistent decoder executor (args = MegaArgs)
-  int fused_add = -1;                     // CGX_FUSE_ADD_LN: the ADD node this LAYERNORM launch also runs
+  int pre_node = -1;                      // capture-time fusion: a node this launch runs first (the ADD
+                                          // of an ADD -> LAYERNORM launch, the LN of an LN -> GEMM launch)
   cudaGraphDeviceNode_t dev_node = nullptr;
   // NCCL
   const void* nc_in = nullptr;
@@ -556,6 +557,7 @@ struct cgx_exec {
   uint64_t spin_timeout_ns = 0;
   // megakernel (cgx_mega.h): one device blob = stages | row ops | tensor maps | split-K workspace |
   // grid-barrier counter | stage trace
+  std::vector<void*> fuse_bufs;   // CGX_FUSE_LN_GEMM: producer row-sum buffers
   bool mega = false;
   void* mega_mem = nullptr;
   unsigned long long* mega_strace = nullptr;
@@ -651,7 +653,9 @@ static void make_args(cgx_exec* e, Launch& l, bool tw) {
   l.tw_ptr_off = ptr_off;
 }
 
-static int build_launch(cgx_exec* e, int k, Launch& l, int add_k = -1) {
+static int build_launch(cgx_exec* e, int k, Launch& l, int pre = -1) {
+  const int add_k = (pre >= 0 && e->c->nodes[pre].op == CGX_OP_ADD) ? pre : -1;
+  const int ln_k = (pre >= 0 && e->c->nodes[pre].op == CGX_OP_LAYERNORM) ? pre : -1;
   cgx_chain* c = e->c;
   const Node& n = c->nodes[k];
   const cgx_mode mode = e->o.mode;
@@ -779,7 +783,7 @@ static int build_launch(cgx_exec* e, int k, Launch& l, int add_k = -1) {
               l.ext.push_back({foff[i], toff[i], j});
             }
           }
-        l.fused_add = add_k;
+        l.pre_node = add_k;
       }
       decoder_ln_launch_dims(n.attr.rows, n.attr.cols, &l.grid, &l.block);
       l.func = kfn_layernorm(twc, add_k >= 0);
@@ -795,7 +799,8 @@ static int build_launch(cgx_exec* e, int k, Launch& l, int add_k = -1) {
       const bool a_ext = is_ext(n.in[0]) && (indirect || patch);
       for (int i = 1; i < 3; ++i)
         if (is_ext(n.in[i])) return fail(CGX_E_UNSUPPORTED, "gemm: external weights/bias");
-      void* A = slot_ptr(n.in[0]);
+      // LN -> GEMM fusion: A is the LayerNorm's INPUT (normalised in the kernel's A prologue)
+      void* A = ln_k >= 0 ? slot_ptr(c->nodes[ln_k].in[0]) : slot_ptr(n.in[0]);
       void* W = slot_ptr(n.in[1]);
       void* bias = slot_ptr(n.in[2]);
       void* res = (n.attr.flags & CGX_GEMM_RESIDUAL) ? slot_ptr(n.in[3]) : nullptr;
@@ -991,7 +996,7 @@ static std::vector<std::vector<int>> chain_deps(const cgx_exec* e) {
     };
     // a fused ADD -> LAYERNORM launch performs both nodes' accesses, the ADD's first
     for (int part = 0; part < 2; ++part) {
-      const int ni = part == 0 ? e->L[p].fused_add : e->L[p].node;
+      const int ni = part == 0 ? e->L[p].pre_node : e->L[p].node;
       if (ni < 0) continue;
       const Node& n = e->c->nodes[ni];
       for (int j = 0; j < n.n_in; ++j) add(last_w[n.in[j]]);
@@ -1669,6 +1674,7 @@ static void exec_free(cgx_exec* e) {
   if (e->dl_iter) cudaFree(e->dl_iter);
   if (e->d_trace) cudaFree(e->d_trace);
   if (e->mega_mem) cudaFree(e->mega_mem);
+  for (void* b : e->fuse_bufs) cudaFree(b);
   if (e->d_desc) cudaFree(e->d_desc);
   if (e->d_chunk) cudaFree(e->d_chunk);
   if (e->d_table) cudaFree(e->d_table);
@@ -1704,6 +1710,72 @@ static bool fusable_add_ln(const cgx_exec* e, int k) {
   if (c->slots[a.out].dtype != CGX_BF16 || c->slots[a.in[0]].dtype != CGX_BF16 || c->slots[a.in[1]].dtype != CGX_BF16)
     return false;
   return a.attr.n == (uint64_t)l.attr.rows * l.attr.cols && l.attr.cols <= kLnMaxCols && l.attr.cols % 8 == 0;
+}
+
+// CGX_FUSE_LN_GEMM: node k is a LAYERNORM whose output only the next node, a GEMM, reads as A; the
+// LN input is the output of the previous launch, a tcgen05 GEMM over the same rows x cols (so that
+// GEMM can hand over per-tile row sums); gamma / beta STATIC; more than 4 rows (the small-M path
+// has no A prologue)
+static bool fusable_ln_gemm(const cgx_exec* e, int k) {
+  const cgx_chain* c = e->c;
+  if (k >= e->last || k <= e->first + 1 || e->L.size() < 2) return false;
+  const Node& ln = c->nodes[k];
+  const Node& g = c->nodes[k + 1];
+  if (ln.op != CGX_OP_LAYERNORM || g.op != CGX_OP_GEMM_BF16 || g.in[0] != ln.out) return false;
+  if (g.attr.flags & CGX_GEMM_ALLREDUCE) return false;
+  if (g.attr.M != ln.attr.rows || g.attr.K != ln.attr.cols || ln.attr.rows <= 4) return false;
+  if (c->slots[ln.in[1]].kind != CGX_SLOT_STATIC || c->slots[ln.in[2]].kind != CGX_SLOT_STATIC) return false;
+  if (c->slots[g.in[1]].kind != CGX_SLOT_STATIC) return false;   // W' is prepared once from W
+  for (int q = e->first; q <= e->last; ++q)   // nothing else reads the LN output (it is still written)
+    if (q != k + 1)
+      for (int i = 0; i < c->nodes[q].n_in; ++i)
+        if (c->nodes[q].in[i] == ln.out) return false;
+  const Launch& prev = e->L[e->L.size() - 2];   // (the slot for node k is already emplaced)
+  if (prev.kind != LK_KERNEL || prev.mega || prev.pre_node >= 0) return false;
+  const Node& p = c->nodes[prev.node];
+  return p.op == CGX_OP_GEMM_BF16 && p.out == ln.in[0] && p.attr.M == ln.attr.rows && p.attr.N == ln.attr.cols &&
+         !(p.attr.flags & CGX_GEMM_ALLREDUCE) && decoder_gemm_is_tcgen05(prev.func);
+}
+
+// Build the LN (k) -> GEMM (k + 1) pair as ONE launch of the GEMM with the LayerNorm folded into
+// it (k_gemm.cu kGemmLnA: gamma-scaled weights W' prepared here once, row correction in the
+// epilogue, the LN output slot stored by the same launch), the previous launch (the producer GEMM)
+// writing per-tile row sums. *fused = false (and the LN built as a launch of its own) when either
+// kernel cannot take the fused role. Requires the GEMM's W / gamma / beta STATIC (prepared once).
+static int build_ln_gemm(cgx_exec* e, int k, bool* fused) {
+  cgx_chain* c = e->c;
+  const Node& ln = c->nodes[k];
+  Launch& l = e->L.back();
+  Launch& prev = e->L[e->L.size() - 2];
+  *fused = false;
+  Launch g;
+  CKS(build_launch(e, k + 1, g, k));
+  const Node& gn = c->nodes[k + 1];
+  void* stats = nullptr;
+  void* wf = nullptr;
+  float* cc = nullptr;
+  const size_t sb = sizeof(float) * 2 * (size_t)prev.grid.x * ln.attr.rows;
+  CK(cudaMalloc(&stats, sb));
+  e->fuse_bufs.push_back(stats);
+  CK(cudaMalloc(&wf, sizeof(uint16_t) * (size_t)gn.attr.N * gn.attr.K));
+  e->fuse_bufs.push_back(wf);
+  CK(cudaMalloc(reinterpret_cast<void**>(&cc), sizeof(float) * 2 * (size_t)gn.attr.N));
+  e->fuse_bufs.push_back(cc);
+  CKS(decoder_ln_fold_prep(c->slots[gn.in[1]].static_ptr, c->slots[ln.in[1]].static_ptr, c->slots[ln.in[2]].static_ptr,
+                           gn.attr.N, gn.attr.K, wf, cc, cc + gn.attr.N));
+  size_t smem = g.smem;
+  if (decoder_gemm_is_tcgen05(g.func) &&
+      decoder_gemm_set_ln_a(g.args.p, g.grid, stats, prev.grid.x, c->slots[ln.in[0]].buf, wf, cc, cc + gn.attr.N,
+                            c->slots[ln.in[1]].static_ptr, c->slots[ln.in[2]].static_ptr, c->slots[ln.out].buf,
+                            ln.attr.eps, &smem, &g.func) == CGX_OK &&
+      decoder_gemm_set_stats_out(prev.args.p, stats, prev.grid) == CGX_OK) {
+    g.smem = smem;
+    g.pre_node = k;
+    l = std::move(g);
+    *fused = true;
+    return CGX_OK;
+  }
+  return build_launch(e, k, l);   // not fusable after all: the LN keeps its own launch
 }
 
 // ---------------------------------------------------------------- megakernel (cgx_mega.h)
@@ -2083,7 +2155,7 @@ extern "C" int cgx_exec_create_ex(cgx_chain* c, const cgx_exec_opts* opts, void*
   if (o.sync_mode < CGX_SYNC_AUTO || o.sync_mode > CGX_SYNC_DATAFLOW) return fail(CGX_E_INVALID_ARG, "exec_create: sync_mode");
   if (o.graph_streams < 0 || o.graph_streams > 64) return fail(CGX_E_INVALID_ARG, "exec_create: graph_streams (0..64)");
   if (o.megakernel < 0 || o.megakernel > 1) return fail(CGX_E_INVALID_ARG, "exec_create: megakernel (0 or 1)");
-  if (o.fuse & ~CGX_FUSE_ADD_LN) return fail(CGX_E_INVALID_ARG, "exec_create: fuse (unknown bits)");
+  if (o.fuse & ~(CGX_FUSE_ADD_LN | CGX_FUSE_LN_GEMM)) return fail(CGX_E_INVALID_ARG, "exec_create: fuse (unknown bits)");
   const int K = (int)c->nodes.size();
   if (K == 0) return fail(CGX_E_STATE, "exec_create: empty chain");
   const int first = o.first_node, last = o.n_nodes ? o.first_node + o.n_nodes - 1 : K - 1;
@@ -2148,6 +2220,10 @@ extern "C" int cgx_exec_create_ex(cgx_chain* c, const cgx_exec_opts* opts, void*
       if ((o.fuse & CGX_FUSE_ADD_LN) && fusable_add_ln(e, k)) {
         if ((st = build_launch(e, k + 1, e->L.back(), k)) != CGX_OK) return bail(st);
         ++k;
+      } else if ((o.fuse & CGX_FUSE_LN_GEMM) && fusable_ln_gemm(e, k)) {
+        bool fused = false;
+        if ((st = build_ln_gemm(e, k, &fused)) != CGX_OK) return bail(st);
+        if (fused) ++k;
       } else if ((st = build_launch(e, k, e->L.back())) != CGX_OK) {
         return bail(st);
       }
@@ -2719,6 +2795,17 @@ extern "C" int cgx_debug_ext_field_offsets(const cgx_exec* e, int pos, uint64_t*
   int n = 0;
   for (const auto& f : l.ext) {
     if (offs && n < cap) offs[n] = f.off;
+    ++n;
+  }
+  *n_out = n;
+  return CGX_OK;
+}
+
+extern "C" int cgx_debug_launch_nodes(const cgx_exec* e, int* nodes_out, int cap, int* n_out) {
+  if (!e || !n_out) return fail(CGX_E_INVALID_ARG, "launch_nodes: bad argument");
+  int n = 0;
+  for (const auto& l : e->L) {
+    if (nodes_out && n < cap) nodes_out[n] = l.node;
     ++n;
   }
   *n_out = n;

@@ -20,16 +20,18 @@ from synth import workloads as wl  # noqa: E402
 args = [a for a in sys.argv[1:] if not a.startswith("--")]
 T = int(args[0]) if args else 128
 L = int(args[1]) if len(args) > 1 else 12
-fuse = "--fuse" in sys.argv
+fuse = "--fuse" in sys.argv or "--ln-gemm" in sys.argv
+ln_gemm = "--ln-gemm" in sys.argv
 dev = torch.device("cuda:0")
 spec = wl.c3_chain(T=T, n_layers=L, fuse_residual=fuse)
 chain = runner.Chain(spec, runner.upload_statics(spec, wl.static_values(spec), dev))
 xs = [runner.host_to_device(wl.slot_values(spec, "x", r), "bf16", dev) for r in range(2)]
-ex = chain.exec("INDIRECT")
+ex = chain.exec("INDIRECT", fuse=cgx.FUSE_LN_GEMM if ln_gemm else 0)
 for i in range(20):
     ex.bind({"x": xs[i % 2]})
     ex.launch()
-K = len(spec.nodes)
+lnodes = cgx.launch_nodes(ex.handle)   # chain node per launch position (fusion: fewer launches)
+K = len(lnodes)
 best = None
 for rep in range(5):
     cgx.node_trace(ex.handle, K)
@@ -46,8 +48,11 @@ print(f"== C3 T={T} L={L} fuse={fuse}: span {span:.1f} us over {K} nodes ({span 
 agg = {}
 prev_exit = 0.0
 for p, (a, b, c) in enumerate(rows):
-    n = spec.nodes[p]
+    n = spec.nodes[lnodes[p]]
     key = n.op if n.op != "GEMM_BF16" else f"GEMM {n.attrs['N']}x{n.attrs['K']}"
+    if ln_gemm and n.op == "GEMM_BF16" and lnodes[p] > 0 and spec.nodes[lnodes[p] - 1].op == "LAYERNORM" \
+            and (p == 0 or lnodes[p - 1] != lnodes[p] - 1):
+        key += " +LN"
     d = agg.setdefault(key, [0, 0.0, 0.0])
     d[0] += 1
     d[1] += c - b

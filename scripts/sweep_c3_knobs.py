@@ -16,12 +16,13 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
     dev = torch.device("cuda:0")
     stream = torch.cuda.Stream()
     res = {}
-    for fuse in (False, True, "add_ln"):
-        spec = wl.c3_chain(T=128, n_layers=12, fuse_residual=fuse is True)
+    for fuse in (False, True, "add_ln", "ln_gemm"):
+        spec = wl.c3_chain(T=128, n_layers=12, fuse_residual=fuse is True or fuse == "ln_gemm")
         chain = runner.Chain(spec, runner.upload_statics(spec, wl.static_values(spec), dev))
         xs = [runner.host_to_device(wl.slot_values(spec, "x", r), "bf16", dev) for r in range(4)]
         ptrs = [cgx.ptr_array([x.data_ptr()]) for x in xs]
-        ex = chain.exec("INDIRECT", stream=stream, fuse=cgx.FUSE_ADD_LN if fuse == "add_ln" else 0)
+        ex = chain.exec("INDIRECT", stream=stream, fuse=cgx.FUSE_ADD_LN if fuse == "add_ln" else
+                        cgx.FUSE_LN_GEMM if fuse == "ln_gemm" else 0)
         for i in range(30):
             cgx.LIB.cgx_bind(ex.handle, ptrs[i % 4], 1)
             cgx.LIB.cgx_launch(ex.handle)
@@ -36,7 +37,7 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
             e1.record(stream)
             e1.synchronize()
             best = min(best, e0.elapsed_time(e1) * 1e3 / 300)
-        res["fused_add_ln" if fuse == "add_ln" else "fused" if fuse else "unfused"] = round(best, 1)
+        res[fuse if isinstance(fuse, str) else "fused" if fuse else "unfused"] = round(best, 1)
         chain.close()
     print(json.dumps(res))
     sys.exit(0)

@@ -401,3 +401,48 @@ def test_c3_fused_add_layernorm(rt, n_layers):
                                   {s.name: (got[True][s.name] if s.name in got[True] else None)
                                    for s in spec.internals()})
         chain.close()
+
+
+@pytest.mark.parametrize("n_layers", [1, 12])
+@pytest.mark.parametrize("T", [128, 77, 200])
+def test_c3_fused_ln_gemm(rt, n_layers, T):
+    """Capture-time LN -> GEMM fusion (fuse = CGX_FUSE_LN_GEMM) on the fused-residual decoder: the
+    LayerNorm runs in the consumer GEMM's A prologue from the producer GEMM's row sums; its output
+    slot is still written. Node-local parity against the oracle (LN mean / variance from the sums,
+    within the bf16 bar), end to end, and bit-identical across the rebinding arms."""
+    cgx, runner = rt
+    if T != 128 and n_layers == 12:
+        pytest.skip("ragged / two-tile T covered at one layer")
+    spec = wl.c3_chain(T=T, n_layers=n_layers, fuse_residual=True)
+    st = wl.static_values(spec)
+    dev = torch.device("cuda:0")
+    pairs = sum(1 for k in range(2, len(spec.nodes) - 1)
+                if spec.nodes[k].op == "LAYERNORM" and spec.nodes[k - 1].op == "GEMM_BF16")
+    arms = [("INDIRECT", "ROOT_PARAMS"), ("INDIRECT", "FIRST_NODE"), ("INDIRECT", "PRELUDE"),
+            ("COPY", "DEFAULT"), ("SETPARAMS", "DEFAULT"), ("EAGER", "DEFAULT")]
+    ref = None
+    for mode, xp in arms:
+        chain = runner.Chain(spec, runner.upload_statics(spec, st, dev))
+        ex = chain.exec(mode, transport=xp, fuse=cgx.FUSE_LN_GEMM)
+        ex_u = chain.exec(mode, transport=xp)
+        assert ex_u.stats()["kernels_per_replay"] - ex.stats()["kernels_per_replay"] == pairs
+        outs = []
+        for r in range(2):
+            t = runner.upload_externals(spec, wl.external_values(spec, r), dev)
+            ex.bind(t)
+            ex.launch()
+            outs.append({s_.name: ex.output(s_.name) for s_ in spec.internals()})
+        chain.close()
+        if ref is None:
+            ref = outs
+            for r, got in enumerate(outs):
+                ext = wl.external_values(spec, r)
+                _node_local_check(spec, st, ext, got)
+                env = eval_chain(spec, ext, st)
+                last = spec.nodes[-1].out
+                g, o = bits_to_f64(got[last]), env[last]
+                assert np.linalg.norm(g - o) / np.linalg.norm(o) <= 2e-2
+        else:
+            for r in range(2):
+                for k in ref[r]:
+                    assert np.array_equal(outs[r][k], ref[r][k]), (mode, xp, k)
