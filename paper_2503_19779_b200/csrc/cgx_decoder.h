@@ -68,4 +68,6 @@ int decoder_gemm_set_ln_a(void* args, dim3 grid, const void* stats, uint32_t nti
 int decoder_ln_fold_prep(const void* W, const void* gamma, const void* beta, uint32_t N, uint32_t K, void* wf,
                          float* c1, float* c2);
 bool decoder_gemm_is_tcgen05(const void* func);
+// the small-M (GEMV) path serves this shape (M <= 4): a folded LN needs no producer row sums there
+bool decoder_gemm_is_gemv(uint32_t M, uint32_t N, uint32_t K);
 }  // namespace cgx

@@ -748,6 +748,11 @@ __global__ void __launch_bounds__(kGvWarps * 32) k_gemv_bf16(const __grid_consta
   for (int r = 0; r < R; ++r)
 #pragma unroll
     for (int m = 0; m < kGvMaxM; ++m) acc[r][m] = 0.f;
+  // folded LayerNorm (kGemmLnA, A = the LN input h): every warp holds its rows of h, so the row
+  // statistics come from the same loads — the LN kernel's reduction (per-lane chunk order, then the
+  // xor tree), so mean / rstd and the materialised a are bit-identical to the LN node
+  const bool ln_a = a.flags & kGemmLnA;
+  float ln_mean[kGvMaxM], ln_rstd[kGvMaxM];
   for (uint32_t m = 0; m < a.M; ++m) {
     uint4 x[kGvKV];
     const uint4* ar = reinterpret_cast<const uint4*>(ap + (size_t)m * a.K);
@@ -755,6 +760,58 @@ __global__ void __launch_bounds__(kGvWarps * 32) k_gemv_bf16(const __grid_consta
     for (int i = 0; i < kGvKV; ++i) {
       const uint32_t v = lane + 32u * i;
       if (v < kv) x[i] = ar[v];
+    }
+    if (ln_a) {
+      float s = 0.f;
+#pragma unroll
+      for (int i = 0; i < kGvKV; ++i)
+        if (lane + 32u * i < kv) {
+          const __nv_bfloat16* xb = reinterpret_cast<const __nv_bfloat16*>(&x[i]);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) s += __bfloat162float(xb[e]);
+        }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      const float mean = s / (float)a.K;
+      float q = 0.f;
+#pragma unroll
+      for (int i = 0; i < kGvKV; ++i)
+        if (lane + 32u * i < kv) {
+          const __nv_bfloat16* xb = reinterpret_cast<const __nv_bfloat16*>(&x[i]);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float d = __bfloat162float(xb[e]) - mean;
+            q += d * d;
+          }
+        }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+      const float rstd = 1.0f / sqrtf(q / (float)a.K + a.ln_eps);
+#pragma unroll
+      for (int mm = 0; mm < kGvMaxM; ++mm)
+        if (mm == (int)m) {
+          ln_mean[mm] = mean;
+          ln_rstd[mm] = rstd;
+        }
+      if (blockIdx.x == 0 && warp == 0)   // the LN node's output row, materialised once
+#pragma unroll
+        for (int i = 0; i < kGvKV; ++i) {
+          const uint32_t v = lane + 32u * i;
+          if (v < kv) {
+            const uint4 gx = __ldg(reinterpret_cast<const uint4*>(a.ln_g) + v);
+            const uint4 bx = __ldg(reinterpret_cast<const uint4*>(a.ln_b) + v);
+            const __nv_bfloat16* xb = reinterpret_cast<const __nv_bfloat16*>(&x[i]);
+            const __nv_bfloat16* gb = reinterpret_cast<const __nv_bfloat16*>(&gx);
+            const __nv_bfloat16* bb = reinterpret_cast<const __nv_bfloat16*>(&bx);
+            uint4 y;
+            __nv_bfloat16* yb = reinterpret_cast<__nv_bfloat16*>(&y);
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              yb[e] = __float2bfloat16_rn((__bfloat162float(xb[e]) - mean) * rstd * __bfloat162float(gb[e]) +
+                                          __bfloat162float(bb[e]));
+            reinterpret_cast<uint4*>(a.ln_out + (size_t)m * a.K)[v] = y;
+          }
+        }
     }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -797,7 +854,9 @@ __global__ void __launch_bounds__(kGvWarps * 32) k_gemv_bf16(const __grid_consta
 #pragma unroll
     for (int m = 0; m < kGvMaxM; ++m) {
       if (m >= (int)a.M) break;
-      float v = acc[r][m] + b;
+      float v = acc[r][m];
+      if (ln_a) v = ln_rstd[m] * v - ln_rstd[m] * ln_mean[m] * a.ln_c1[n] + a.ln_c2[n];   // folded LN
+      v += b;
       if (gelu) v = gelu_tanh(v);
       if (has_res) v += __bfloat162float(resp[(size_t)m * a.N + n]);
       a.out[(size_t)m * a.N + n] = __float2bfloat16_rn(v);
@@ -942,11 +1001,25 @@ int decoder_gemm_set_stats_out(void* args, void* stats, dim3 grid) {
   return CGX_OK;
 }
 
+static bool gemv_shape(uint32_t M, uint32_t N, uint32_t K);
 int decoder_gemm_set_ln_a(void* args, dim3 grid, const void* stats, uint32_t ntiles, const void* h, const void* w_fold,
                           const float* c1, const float* c2, const void* gamma, const void* beta, void* ln_out,
                           float eps, size_t* smem, const void** func) {
   GemmArgs* g = static_cast<GemmArgs*>(args);
   if (g->flags & CGX_GEMM_ALLREDUCE) return CGX_E_UNSUPPORTED;
+  if (gemv_shape(g->M, g->N, g->K)) {   // small-M path: the statistics come from its own A loads
+    g->w_ptr = static_cast<const __nv_bfloat16*>(w_fold);
+    g->ln_h = static_cast<const __nv_bfloat16*>(h);
+    g->ln_c1 = c1;
+    g->ln_c2 = c2;
+    g->ln_g = static_cast<const __nv_bfloat16*>(gamma);
+    g->ln_b = static_cast<const __nv_bfloat16*>(beta);
+    g->ln_out = static_cast<__nv_bfloat16*>(ln_out);
+    g->ln_eps = eps;
+    g->flags |= kGemmLnA;
+    (void)stats, (void)ntiles, (void)grid, (void)smem, (void)func;
+    return CGX_OK;
+  }
   if (get_encode() != CGX_OK) return CGX_E_CUDA;
   const uint32_t bn = g->N / grid.x;
   if (ntiles > kLnMaxTiles) return CGX_E_UNSUPPORTED;
@@ -1012,6 +1085,8 @@ int decoder_ln_fold_prep(const void* W, const void* gamma, const void* beta, uin
   const cudaError_t e = cudaDeviceSynchronize();
   return e == cudaSuccess ? CGX_OK : CGX_E_CUDA;
 }
+
+bool decoder_gemm_is_gemv(uint32_t M, uint32_t N, uint32_t K) { return gemv_shape(M, N, K); }
 
 bool decoder_gemm_is_tcgen05(const void* func) {
   return func == (const void*)k_gemm_bf16<32, false> || func == (const void*)k_gemm_bf16<64, false> ||

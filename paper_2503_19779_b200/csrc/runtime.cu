@@ -1723,13 +1723,15 @@ static bool fusable_ln_gemm(const cgx_exec* e, int k) {
   const Node& g = c->nodes[k + 1];
   if (ln.op != CGX_OP_LAYERNORM || g.op != CGX_OP_GEMM_BF16 || g.in[0] != ln.out) return false;
   if (g.attr.flags & CGX_GEMM_ALLREDUCE) return false;
-  if (g.attr.M != ln.attr.rows || g.attr.K != ln.attr.cols || ln.attr.rows <= 4) return false;
+  if (g.attr.M != ln.attr.rows || g.attr.K != ln.attr.cols) return false;
+  const bool gemv = decoder_gemm_is_gemv(g.attr.M, g.attr.N, g.attr.K);   // computes its own row statistics
   if (c->slots[ln.in[1]].kind != CGX_SLOT_STATIC || c->slots[ln.in[2]].kind != CGX_SLOT_STATIC) return false;
   if (c->slots[g.in[1]].kind != CGX_SLOT_STATIC) return false;   // W' is prepared once from W
   for (int q = e->first; q <= e->last; ++q)   // nothing else reads the LN output (it is still written)
     if (q != k + 1)
       for (int i = 0; i < c->nodes[q].n_in; ++i)
         if (c->nodes[q].in[i] == ln.out) return false;
+  if (gemv) return ln.attr.cols <= 3072;   // (the GEMV keeps a whole A row per warp in registers)
   const Launch& prev = e->L[e->L.size() - 2];   // (the slot for node k is already emplaced)
   if (prev.kind != LK_KERNEL || prev.mega || prev.pre_node >= 0) return false;
   const Node& p = c->nodes[prev.node];
@@ -1751,12 +1753,14 @@ static int build_ln_gemm(cgx_exec* e, int k, bool* fused) {
   Launch g;
   CKS(build_launch(e, k + 1, g, k));
   const Node& gn = c->nodes[k + 1];
+  const bool gemv = decoder_gemm_is_gemv(gn.attr.M, gn.attr.N, gn.attr.K);
   void* stats = nullptr;
   void* wf = nullptr;
   float* cc = nullptr;
-  const size_t sb = sizeof(float) * 2 * (size_t)prev.grid.x * ln.attr.rows;
-  CK(cudaMalloc(&stats, sb));
-  e->fuse_bufs.push_back(stats);
+  if (!gemv) {   // the producer GEMM's per-tile row sums (the GEMV computes its own statistics)
+    CK(cudaMalloc(&stats, sizeof(float) * 2 * (size_t)prev.grid.x * ln.attr.rows));
+    e->fuse_bufs.push_back(stats);
+  }
   CK(cudaMalloc(&wf, sizeof(uint16_t) * (size_t)gn.attr.N * gn.attr.K));
   e->fuse_bufs.push_back(wf);
   CK(cudaMalloc(reinterpret_cast<void**>(&cc), sizeof(float) * 2 * (size_t)gn.attr.N));
@@ -1764,11 +1768,11 @@ static int build_ln_gemm(cgx_exec* e, int k, bool* fused) {
   CKS(decoder_ln_fold_prep(c->slots[gn.in[1]].static_ptr, c->slots[ln.in[1]].static_ptr, c->slots[ln.in[2]].static_ptr,
                            gn.attr.N, gn.attr.K, wf, cc, cc + gn.attr.N));
   size_t smem = g.smem;
-  if (decoder_gemm_is_tcgen05(g.func) &&
+  if ((gemv || decoder_gemm_is_tcgen05(g.func)) &&
       decoder_gemm_set_ln_a(g.args.p, g.grid, stats, prev.grid.x, c->slots[ln.in[0]].buf, wf, cc, cc + gn.attr.N,
                             c->slots[ln.in[1]].static_ptr, c->slots[ln.in[2]].static_ptr, c->slots[ln.out].buf,
                             ln.attr.eps, &smem, &g.func) == CGX_OK &&
-      decoder_gemm_set_stats_out(prev.args.p, stats, prev.grid) == CGX_OK) {
+      (gemv || decoder_gemm_set_stats_out(prev.args.p, stats, prev.grid) == CGX_OK)) {
     g.smem = smem;
     g.pre_node = k;
     l = std::move(g);

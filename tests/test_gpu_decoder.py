@@ -404,15 +404,15 @@ def test_c3_fused_add_layernorm(rt, n_layers):
 
 
 @pytest.mark.parametrize("n_layers", [1, 12])
-@pytest.mark.parametrize("T", [128, 77, 200])
+@pytest.mark.parametrize("T", [128, 77, 200, 1, 4])
 def test_c3_fused_ln_gemm(rt, n_layers, T):
     """Capture-time LN -> GEMM fusion (fuse = CGX_FUSE_LN_GEMM) on the fused-residual decoder: the
     LayerNorm runs in the consumer GEMM's A prologue from the producer GEMM's row sums; its output
     slot is still written. Node-local parity against the oracle (LN mean / variance from the sums,
     within the bf16 bar), end to end, and bit-identical across the rebinding arms."""
     cgx, runner = rt
-    if T != 128 and n_layers == 12:
-        pytest.skip("ragged / two-tile T covered at one layer")
+    if T not in (128, 1) and n_layers == 12:
+        pytest.skip("ragged / two-tile / small-M T covered at one layer")
     spec = wl.c3_chain(T=T, n_layers=n_layers, fuse_residual=True)
     st = wl.static_values(spec)
     dev = torch.device("cuda:0")
@@ -446,3 +446,31 @@ def test_c3_fused_ln_gemm(rt, n_layers, T):
             for r in range(2):
                 for k in ref[r]:
                     assert np.array_equal(outs[r][k], ref[r][k]), (mode, xp, k)
+
+
+def test_c3_decode_fused_ln_gemv(rt):
+    """T = 1 decode, unfused chain: every LayerNorm after the first folds into its GEMV consumer
+    (the GEMV computes the row statistics from its own A loads, the LN kernel's reduction order, so
+    the materialised LN output is bit-identical to the LN node's)."""
+    cgx, runner = rt
+    spec = wl.c3_chain(T=1, n_layers=12)
+    st = wl.static_values(spec)
+    dev = torch.device("cuda:0")
+    chain = runner.Chain(spec, runner.upload_statics(spec, st, dev))
+    ex = chain.exec("INDIRECT", fuse=cgx.FUSE_LN_GEMM)
+    ex_u = chain.exec("INDIRECT")
+    lns = sum(1 for k, n in enumerate(spec.nodes) if n.op == "LAYERNORM" and k > 1)
+    assert ex_u.stats()["kernels_per_replay"] - ex.stats()["kernels_per_replay"] == lns
+    for r in range(2):
+        ext = wl.external_values(spec, r)
+        t = runner.upload_externals(spec, ext, dev)
+        got = {}
+        for e_ in (ex, ex_u):
+            e_.bind(t)
+            e_.launch()
+            got[e_ is ex] = {s_.name: e_.output(s_.name) for s_ in spec.internals()}
+        _node_local_check(spec, st, ext, got[True])
+        for n in spec.nodes:
+            if n.op == "LAYERNORM":   # the materialised LN output: bit-identical to the LN kernel's
+                assert np.array_equal(got[True][n.out], got[False][n.out]), n.out
+    chain.close()
