@@ -470,7 +470,8 @@ def test_c3_decode_fused_ln_gemv(rt):
             e_.launch()
             got[e_ is ex] = {s_.name: e_.output(s_.name) for s_ in spec.internals()}
         _node_local_check(spec, st, ext, got[True])
-        for n in spec.nodes:
-            if n.op == "LAYERNORM":   # the materialised LN output: bit-identical to the LN kernel's
-                assert np.array_equal(got[True][n.out], got[False][n.out]), n.out
+        # the first folded LN (layer 0's LN2) sees the same input in both execs: its materialised
+        # output is bit-identical to the LN kernel's (later ones follow GEMVs on the folded weights)
+        first = next(n for k, n in enumerate(spec.nodes) if n.op == "LAYERNORM" and k > 1)
+        assert np.array_equal(got[True][first.out], got[False][first.out]), first.out
     chain.close()
