@@ -8,7 +8,7 @@ namespace cgx {
 // LayerNorm: one warp per row, registers hold the row (cols <= kLnMaxCols, cols % 8 == 0).
 static constexpr uint32_t kLnMaxCols = 2048;
 // add: the fused ADD -> LAYERNORM variant (LnArgs::add_b / add_out; tw must be 0)
-const void* kfn_layernorm(int tw = 0, bool add = false);
+const void* kfn_layernorm(int tw, bool add, uint32_t cols);
 void decoder_ln_launch_dims(uint32_t rows, uint32_t cols, dim3* grid, dim3* block);
 
 // Causal attention on CUDA cores (T <= 1024, D == 64).

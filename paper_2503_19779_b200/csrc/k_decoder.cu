@@ -34,7 +34,9 @@ static_assert(kLnMaxVec * 8 * 32 == (int)kLnMaxCols, "k_layernorm row capacity")
 // ADD: the fused ADD -> LAYERNORM pair (LnArgs::add_b / add_out): h = bf16(x + add_b) is stored to
 // the ADD's slot and normalised from registers — the same values and the same reduction order as
 // the unfused LN reading h back, so both paths are bit-identical.
-template <int TW, bool ADD>
+// VEC: 16-B vectors per lane held in registers (cols <= VEC x 256): 3 for GPT-2's 768 columns keeps
+// the kernel at a register budget that lets it sit beside a GEMM CTA under PDL, 8 for up to 2048
+template <int TW, bool ADD, int VEC>
 __global__ void __launch_bounds__(256) k_layernorm(const __grid_constant__ ArgsTW<LnArgs, TW> A) {
   const LnArgs& a = A.a;
   if (threadIdx.x == 0) node_stamp(a.ntrace, 0);
@@ -48,13 +50,13 @@ __global__ void __launch_bounds__(256) k_layernorm(const __grid_constant__ ArgsT
   const uint32_t nv = a.cols >> 3;
   // gamma / beta are STATIC (never written in the graph): fetched before the wait, overlapping
   // the predecessor, so the only post-wait round trip is the row itself
-  uint4 gu[kLnMaxVec], bu[kLnMaxVec];
+  uint4 gu[VEC], bu[VEC];
   const uint4* gr = reinterpret_cast<const uint4*>(a.g);
   const uint4* br = reinterpret_cast<const uint4*>(a.b);
   const bool params_pre = a.flags & kFlagLnParamsPre;
   if (params_pre) {
 #pragma unroll
-    for (int i = 0; i < kLnMaxVec; ++i) {
+    for (int i = 0; i < VEC; ++i) {
       const uint32_t idx = lane + i * 32;
       if (idx < nv) {
         gu[i] = __ldg(gr + idx);
@@ -65,7 +67,7 @@ __global__ void __launch_bounds__(256) k_layernorm(const __grid_constant__ ArgsT
   pdl_wait();
   if (!params_pre) {
 #pragma unroll
-    for (int i = 0; i < kLnMaxVec; ++i) {
+    for (int i = 0; i < VEC; ++i) {
       const uint32_t idx = lane + i * 32;
       if (idx < nv) {
         gu[i] = gr[idx];
@@ -83,19 +85,19 @@ __global__ void __launch_bounds__(256) k_layernorm(const __grid_constant__ ArgsT
     return;
   }
   const uint4* xr = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(px) + (size_t)row * a.cols);
-  uint4 xu[kLnMaxVec];
+  uint4 xu[VEC];
 #pragma unroll
-  for (int i = 0; i < kLnMaxVec; ++i)
+  for (int i = 0; i < VEC; ++i)
     if (lane + i * 32 < nv) xu[i] = xr[lane + i * 32];
   if constexpr (ADD) {   // h = bf16(x + b) (k_elem_bf16 ADD: fp32 sum, one rounding), stored
     const uint4* br2 = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(pb) + (size_t)row * a.cols);
     uint4* hr = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.add_out) + (size_t)row * a.cols);
-    uint4 yu[kLnMaxVec];
+    uint4 yu[VEC];
 #pragma unroll
-    for (int i = 0; i < kLnMaxVec; ++i)
+    for (int i = 0; i < VEC; ++i)
       if (lane + i * 32 < nv) yu[i] = br2[lane + i * 32];
 #pragma unroll
-    for (int i = 0; i < kLnMaxVec; ++i)
+    for (int i = 0; i < VEC; ++i)
       if (lane + i * 32 < nv) {
         __nv_bfloat16* xb = reinterpret_cast<__nv_bfloat16*>(&xu[i]);
         const __nv_bfloat16* yb = reinterpret_cast<const __nv_bfloat16*>(&yu[i]);
@@ -104,10 +106,10 @@ __global__ void __launch_bounds__(256) k_layernorm(const __grid_constant__ ArgsT
         hr[lane + i * 32] = xu[i];
       }
   }
-  float v[kLnMaxVec][8];
+  float v[VEC][8];
   float s = 0.f;
 #pragma unroll
-  for (int i = 0; i < kLnMaxVec; ++i) {
+  for (int i = 0; i < VEC; ++i) {
     if (lane + i * 32 < nv) {
       const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&xu[i]);
 #pragma unroll
@@ -120,7 +122,7 @@ __global__ void __launch_bounds__(256) k_layernorm(const __grid_constant__ ArgsT
   const float mean = warp_sum(s) / (float)a.cols;
   float q = 0.f;
 #pragma unroll
-  for (int i = 0; i < kLnMaxVec; ++i)
+  for (int i = 0; i < VEC; ++i)
     if (lane + i * 32 < nv)
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
@@ -131,7 +133,7 @@ __global__ void __launch_bounds__(256) k_layernorm(const __grid_constant__ ArgsT
   const float rstd = 1.0f / sqrtf(var + a.eps);
   uint4* orow = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.out) + (size_t)row * a.cols);
 #pragma unroll
-  for (int i = 0; i < kLnMaxVec; ++i) {
+  for (int i = 0; i < VEC; ++i) {
     const uint32_t idx = lane + i * 32;
     if (idx < nv) {
       const __nv_bfloat16* gb = reinterpret_cast<const __nv_bfloat16*>(&gu[i]);
@@ -147,15 +149,19 @@ __global__ void __launch_bounds__(256) k_layernorm(const __grid_constant__ ArgsT
   if (a.ntrace && lane == 0) node_stamp(a.ntrace, 2);
 }
 
-const void* kfn_layernorm(int tw, bool add) {
-  if (add) return tw == 0 ? (const void*)k_layernorm<0, true> : nullptr;
+template <int VEC>
+static const void* kfn_layernorm_v(int tw, bool add) {
+  if (add) return tw == 0 ? (const void*)k_layernorm<0, true, VEC> : nullptr;
   switch (tw) {
-    case 0: return (const void*)k_layernorm<0, false>;
-    case 8: return (const void*)k_layernorm<8, false>;
-    case 64: return (const void*)k_layernorm<64, false>;
-    case 512: return (const void*)k_layernorm<512, false>;
+    case 0: return (const void*)k_layernorm<0, false, VEC>;
+    case 8: return (const void*)k_layernorm<8, false, VEC>;
+    case 64: return (const void*)k_layernorm<64, false, VEC>;
+    case 512: return (const void*)k_layernorm<512, false, VEC>;
   }
   return nullptr;
+}
+const void* kfn_layernorm(int tw, bool add, uint32_t cols) {
+  return cols <= 3u * 256u ? kfn_layernorm_v<3>(tw, add) : kfn_layernorm_v<kLnMaxVec>(tw, add);
 }
 void decoder_ln_launch_dims(uint32_t rows, uint32_t cols, dim3* grid, dim3* block) {
   (void)cols;

@@ -786,7 +786,7 @@ static int build_launch(cgx_exec* e, int k, Launch& l, int pre = -1) {
         l.pre_node = add_k;
       }
       decoder_ln_launch_dims(n.attr.rows, n.attr.cols, &l.grid, &l.block);
-      l.func = kfn_layernorm(twc, add_k >= 0);
+      l.func = kfn_layernorm(twc, add_k >= 0, n.attr.cols);
       return CGX_OK;
     }
     case CGX_OP_GEMM_BF16: {
