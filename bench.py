@@ -1201,6 +1201,8 @@ def bench_decoder(torch, cgx, runner, wl, stream, dev, peaks):
         ful = timed(fexl.handle, 300)
         res["fused_residual"]["ln_folded"] = {"kernels_per_replay": fexl.stats()["kernels_per_replay"] - 0,
                                               "us_per_replay": ful, "tokens_per_s": T * 1e6 / ful}
+        res["best"] = {"arm": "fused residual + LayerNorm folded into its consumer GEMM (INDIRECT, FIRST_NODE)",
+                       "us_per_replay": ful, "tokens_per_s": T * 1e6 / ful}
         fexl.close()
         fchain.close()
     except Exception as exn:  # noqa: BLE001
