@@ -174,8 +174,9 @@ def test_attention_lengths(rt, T):
     _close(outs[0]["att"], env["att"], f"attention T={T}")
 
 
-def _node_local_check(spec, st, ext, got):
-    """Feed every node the GPU's own inputs and compare its output (no error compounding)."""
+def _node_local_check(spec, st, ext, got, one_rank=False):
+    """Feed every node the GPU's own inputs and compare its output (no error compounding).
+    one_rank: ALLREDUCE_SUM nodes ran over a one-rank communicator (the identity)."""
     env = {}
     for s in spec.slots:
         if s.kind == "external":
@@ -195,6 +196,8 @@ def _node_local_check(spec, st, ext, got):
             ref = ops.attn_causal(env[node.ins[0]], a)
         elif node.op == "ADD":
             ref = ops.add(env[node.ins[0]], env[node.ins[1]], a, "bf16")
+        elif node.op == "ALLREDUCE_SUM" and one_rank:
+            ref = env[node.ins[0]]                     # the sum over a single rank
         else:
             raise AssertionError(node.op)
         _close(got[node.out], ref, f"{node.out} ({node.op})")
@@ -475,3 +478,37 @@ def test_c3_decode_fused_ln_gemv(rt):
         first = next(n for k, n in enumerate(spec.nodes) if n.op == "LAYERNORM" and k > 1)
         assert np.array_equal(got[True][first.out], got[False][first.out]), first.out
     chain.close()
+
+
+@pytest.mark.parametrize("tp", [2, 4, 8])
+def test_tp_shard_shapes_single_rank(rt, tp):
+    """Rank 0's tensor-parallel shard of the decoder (TP = 2 / 4 / 8: column-split QKV / FC1,
+    row-split O / FC2, 12 heads padded to 16 at TP = 8) run on this GPU with a ONE-rank NCCL
+    communicator, so every kernel shape of the TP chains is exercised here (the all-reduces are then
+    the identity); node-local parity against the oracle, INDIRECT and EAGER bit-identical."""
+    cgx, runner = rt
+    from paper_2503_19779_b200 import cgx as c
+    full = wl.c3_chain(T=128, n_layers=2)
+    spec = wl.c3_chain(T=128, n_layers=2, tp=tp, rank=0)
+    st = wl.static_values(spec, tp=tp, rank=0, full=full)
+    dev = torch.device("cuda:0")
+    comm = c.nccl_comm_init(1, 0, c.nccl_unique_id(), 0)
+    try:
+        res = {}
+        for mode in ("INDIRECT", "EAGER"):
+            chain = runner.Chain(spec, runner.upload_statics(spec, st, dev), nccl_comm=comm)
+            ex = chain.exec(mode)
+            outs = []
+            for r in range(2):
+                t = runner.upload_externals(spec, wl.external_values(spec, r), dev)
+                ex.bind(t)
+                ex.launch()
+                outs.append({s_.name: ex.output(s_.name) for s_ in spec.internals()})
+            res[mode] = outs
+            chain.close()
+        for r in range(2):
+            _node_local_check(spec, st, wl.external_values(spec, r), res["INDIRECT"][r], one_rank=True)
+            for k in res["INDIRECT"][r]:
+                assert np.array_equal(res["INDIRECT"][r][k], res["EAGER"][r][k]), k
+    finally:
+        c.nccl_comm_destroy(comm)
