@@ -120,6 +120,7 @@ struct alignas(64) GemmArgs {
   const float* ln_c2;         // kGemmLnA: [N] beta . W
   uint32_t ln_ntiles;
   float ln_eps;
+  uint32_t ln_dbg;            // measurement knob (CGX_LN_DBG): 1 = serial stats loop, 2 = skip the LN output
 };
 
 __device__ __forceinline__ void trace_at(const GemmArgs& a, int slot) {
@@ -433,7 +434,20 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
         float mean = 0.f, rstd = 0.f;
         if (m < (int)a.M) {
           float s1 = 0.f, s2 = 0.f;                // the tiles' sums in fixed tile order
-          for (uint32_t t = 0; t < a.ln_ntiles; ++t) {
+          uint32_t t = 0;
+          if (!(a.ln_dbg & 1u)) {
+            for (; t + 8 <= a.ln_ntiles; t += 8) {   // 8 loads in flight, summed in order
+              float2 v[8];
+#pragma unroll
+              for (int u = 0; u < 8; ++u) v[u] = __ldcg(a.ln_stats + (size_t)(t + u) * a.M + m);
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                s1 += v[u].x;
+                s2 += v[u].y;
+              }
+            }
+          }
+          for (; t < a.ln_ntiles; ++t) {
             const float2 v = __ldcg(a.ln_stats + (size_t)t * a.M + m);
             s1 += v.x;
             s2 += v.y;
@@ -448,7 +462,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
       const uint32_t nctas = gridDim.x * gridDim.y * gridDim.z;
       const uint32_t kc = a.K / 8;                       // 16-B chunks per row
       const uint64_t chunks = (uint64_t)a.M * kc;
-      for (uint64_t i = (uint64_t)cta_lin * 128u + et; i < chunks; i += (uint64_t)nctas * 128u) {
+      for (uint64_t i = (uint64_t)cta_lin * 128u + et; (a.ln_dbg & 2u) == 0 && i < chunks; i += (uint64_t)nctas * 128u) {
         const uint32_t mm = (uint32_t)(i / kc), k8 = (uint32_t)(i % kc) * 8;
         // the row's statistics: from shared memory when the row is in this CTA's M tile, else
         // recomputed from the sums (only when T > 128 spreads rows over several M tiles)
@@ -1038,6 +1052,7 @@ int decoder_gemm_set_ln_a(void* args, dim3 grid, const void* stats, uint32_t nti
   g->ln_b = static_cast<const __nv_bfloat16*>(beta);
   g->ln_out = static_cast<__nv_bfloat16*>(ln_out);
   g->ln_eps = eps;
+  g->ln_dbg = getenv("CGX_LN_DBG") ? (uint32_t)atoi(getenv("CGX_LN_DBG")) : 0u;
   g->flags |= kGemmLnA;
   (void)func;   // the same kernel (kGemmLnA is a runtime flag)
   return CGX_OK;

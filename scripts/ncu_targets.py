@@ -4,6 +4,8 @@
   python scripts/ncu_targets.py copy     # one COPY-arm bind at the C4 1 GiB point (copy kernel)
   python scripts/ncu_targets.py gemm     # one C3 (T=128, 1 layer) INDIRECT replay (tcgen05 GEMMs)
   python scripts/ncu_targets.py mega     # one C3 (T=128, 12 layers) megakernel launch (persistent executor)
+  python scripts/ncu_targets.py gemm_fold  # one C3 (T=128, 2 layers, fused residual) replay with the
+                                           # LayerNorms folded into their consumer GEMMs
   python scripts/ncu_targets.py replay_nopdl  # one C2 INDIRECT replay captured without PDL (the
                                               # roofline's sub-graph configuration)
 """
@@ -43,6 +45,9 @@ def main():
     elif what == "gemm":
         spec = wl.c3_chain(T=128, n_layers=1)
         mode, xp = "INDIRECT", "FIRST_NODE"
+    elif what == "gemm_fold":
+        spec = wl.c3_chain(T=128, n_layers=2, fuse_residual=True)
+        mode, xp = "INDIRECT", "FIRST_NODE"
     elif what == "mega":
         spec = wl.c3_chain(T=128, n_layers=12)
         mode, xp = "INDIRECT", "ROOT_PARAMS"
@@ -50,7 +55,8 @@ def main():
         spec = wl.c2_chain()
         mode, xp = "INDIRECT", "FIRST_NODE"
     chain = runner.Chain(spec, runner.upload_statics(spec, wl.static_values(spec), dev))
-    ex = chain.exec(mode, transport=xp, no_pdl=(what == "replay_nopdl"), megakernel=(what == "mega"))
+    ex = chain.exec(mode, transport=xp, no_pdl=(what == "replay_nopdl"), megakernel=(what == "mega"),
+                    fuse=cgx.FUSE_LN_GEMM if what == "gemm_fold" else 0)
     ts = fill(spec, dev, sh)
     torch.cuda.synchronize()
     ex.bind_ptrs([t.data_ptr() for t in ts])
