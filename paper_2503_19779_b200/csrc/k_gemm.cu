@@ -722,26 +722,35 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
 // ------------------------------------------------------------------ small-M path (decode, T <= 8)
 // At M <= 4 (the C3 T = 1 decode variant) a 128-row UMMA tile wastes 127/128 of the tensor core and
 // still pays the TMA/TMEM latency chain, while the node is a pure weight stream (N x K x 2 bytes).
-// One warp per kEvRows output columns: the warp streams those W rows (STATIC) into registers
-// BEFORE griddepcontrol.wait — the whole weight matrix is in flight while the predecessor drains —
-// then loads the M activation rows (L2), forms M dot products per row in fp32 (fixed lane order +
-// fixed shuffle tree: deterministic) and lane 0 applies bias / GELU / residual and rounds once.
+// KS warps per output column, each holding a K slice of kGvKV 16-B vectors per lane: the warps
+// stream their W slices (STATIC) into registers BEFORE griddepcontrol.wait — the whole weight matrix
+// is in flight while the predecessor drains — then load the M activation rows (L2), form M partial
+// dot products in fp32 (fixed lane order + fixed shuffle tree), and the slice-0 warp sums the KS
+// partials in slice order (deterministic) and applies bias / GELU / residual, rounding once.
+// The K split keeps every variant at 3 vectors per lane (80 registers, 3 CTAs of 256 threads per
+// SM), so the next node's CTAs fit beside this one's and start their own weight stream early: one
+// warp holding a whole K = 3072 row (207-224 registers) blocked that (profiles/r02/decode_gemv_ks.txt).
 static constexpr int kGvWarps = 8;
 static constexpr int kGvMaxM = 4;    // decode replays measured faster than tcgen05 up to T = 4, not at 8
-static constexpr int kGvMaxKV = 12;          // 16-B vectors per lane per row: K <= 12 * 256 = 3072
+static constexpr int kGvKV = 3;      // 16-B vectors per lane per K slice: a slice covers 768 columns
+static constexpr int kGvMaxKS = 8;   // slices per column: K <= 8 * 768 = 6144
 
 __device__ __forceinline__ float bf16lo(uint32_t u) { return __uint_as_float(u << 16); }
 __device__ __forceinline__ float bf16hi(uint32_t u) { return __uint_as_float(u & 0xffff0000u); }
 
-template <int R, int kGvKV>
-__global__ void __launch_bounds__(kGvWarps * 32) k_gemv_bf16(const __grid_constant__ GemmArgs a) {
+template <int KS, int MT, int R>
+__global__ void __launch_bounds__(kGvWarps * 32, MT == 1 ? (R == 1 ? 4 : 3) : 3) k_gemv_bf16(const __grid_constant__ GemmArgs a) {
+  static_assert(kGvWarps % KS == 0, "slices of a column stay in one CTA");
   const bool late_trigger = a.flags & kGemmTriggerAfterWait;
   if (threadIdx.x == 0) node_stamp(a.ntrace, 0);
   if (!late_trigger) pdl_trigger();
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t n0 = (blockIdx.x * kGvWarps + warp) * R;     // this warp's first output column
-  const uint32_t kv = a.K / 8;                                  // 16-B vectors per row
-  // ---- W rows n0 .. n0+R-1 (STATIC): all loads in flight before the wait
+  const uint32_t slice = warp % KS;                                    // this warp's K slice
+  const uint32_t n0 = (blockIdx.x * (kGvWarps / KS) + warp / KS) * R;  // this warp's R output columns
+  const uint32_t M = MT == 1 ? 1u : a.M;                               // activation rows
+  const uint32_t kv = a.K / 8;                                         // 16-B vectors per row
+  const uint32_t v0 = slice * (kGvKV * 32u);                           // the slice's first vector
+  // ---- W rows n0 .. n0 + R - 1, this slice (STATIC): all loads in flight before the wait
   const bool w_late = a.flags & kGemmWAfterWait;
   if (w_late) pdl_wait();
   uint4 w[R][kGvKV];
@@ -749,48 +758,109 @@ __global__ void __launch_bounds__(kGvWarps * 32) k_gemv_bf16(const __grid_consta
   for (int r = 0; r < R; ++r)
 #pragma unroll
     for (int i = 0; i < kGvKV; ++i) {
-      const uint32_t v = lane + 32u * i;
+      const uint32_t v = v0 + lane + 32u * i;
       if (n0 + r < a.N && v < kv) w[r][i] = *(reinterpret_cast<const uint4*>(a.w_ptr + (size_t)(n0 + r) * a.K) + v);
+    }
+  // epilogue operands no node of the graph writes (bias unless kGemmWAfterWait, the folded-LN
+  // column sums c1 / c2) and the gamma / beta of the materialised LN row: fetched before the wait
+  // too, so the epilogue after the dot products issues no dependent load but the residual's
+  const bool has_bias = a.flags & CGX_GEMM_BIAS, gelu = a.flags & CGX_GEMM_GELU;
+  const bool has_res = a.flags & CGX_GEMM_RESIDUAL;
+  const bool ln_a = a.flags & kGemmLnA;
+  const bool owner = slice == 0 && lane == 0;                          // applies the columns' epilogue
+  float e_b[R], e_c1[R], e_c2[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    e_b[r] = e_c1[r] = e_c2[r] = 0.f;
+    if (owner && n0 + r < a.N) {
+      if (has_bias && !w_late) e_b[r] = __bfloat162float(a.bias[n0 + r]);
+      if (ln_a) {
+        e_c1[r] = a.ln_c1[n0 + r];
+        e_c2[r] = a.ln_c2[n0 + r];
+      }
+    }
+  }
+  // (gamma / beta staged in shared memory by the storing warps — the first column's KS warps of
+  // CTA 0 — registers would cost occupancy; each lane reads back only what it stored itself)
+  __shared__ uint4 s_gb[2][KS][kGvKV * 32];
+  __shared__ float s_part[kGvWarps][R][MT];                            // KS > 1: per-slice partials
+  __shared__ float s_st[kGvWarps];                                     // KS > 1: per-slice LN sums
+  const bool ln_mat = ln_a && blockIdx.x == 0 && warp < (uint32_t)KS;
+  if (ln_mat)
+#pragma unroll
+    for (int i = 0; i < kGvKV; ++i) {
+      const uint32_t v = v0 + lane + 32u * i;
+      if (v < kv) {
+        s_gb[0][slice][lane + 32u * i] = __ldg(reinterpret_cast<const uint4*>(a.ln_g) + v);
+        s_gb[1][slice][lane + 32u * i] = __ldg(reinterpret_cast<const uint4*>(a.ln_b) + v);
+      }
     }
   if (!w_late) pdl_wait();
   if (late_trigger) pdl_trigger();
   if (threadIdx.x == 0) node_stamp(a.ntrace, 1);
+  if (has_bias && w_late && owner)
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (n0 + r < a.N) e_b[r] = __bfloat162float(a.bias[n0 + r]);
   // A: the patched / direct a_ptr, or table[ta] for an EXTERNAL A under INDIRECT (after the wait)
   const __nv_bfloat16* ap = a.ta >= 0 ? reinterpret_cast<const __nv_bfloat16*>(ld_table(a.table + a.ta)) : a.a_ptr;
-  float acc[R][kGvMaxM];
+  // the residual (written by an earlier node): in flight together with the A rows
+  float e_res[R][MT];
+  if (has_res && owner) {
+    const __nv_bfloat16* resp = a.tres >= 0 ? reinterpret_cast<const __nv_bfloat16*>(ld_table(a.table + a.tres))
+                                            : a.residual;
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int m = 0; m < MT; ++m)
+        e_res[r][m] = (m < (int)M && n0 + r < a.N) ? __bfloat162float(resp[(size_t)m * a.N + n0 + r]) : 0.f;
+  }
+  float acc[R][MT];
 #pragma unroll
   for (int r = 0; r < R; ++r)
 #pragma unroll
-    for (int m = 0; m < kGvMaxM; ++m) acc[r][m] = 0.f;
-  // folded LayerNorm (kGemmLnA, A = the LN input h): every warp holds its rows of h, so the row
-  // statistics come from the same loads — the LN kernel's reduction (per-lane chunk order, then the
-  // xor tree), so mean / rstd and the materialised a are bit-identical to the LN node
-  const bool ln_a = a.flags & kGemmLnA;
-  float ln_mean[kGvMaxM], ln_rstd[kGvMaxM];
-  for (uint32_t m = 0; m < a.M; ++m) {
+    for (int m = 0; m < MT; ++m) acc[r][m] = 0.f;
+  // folded LayerNorm (kGemmLnA, A = the LN input h): the dot products run on the raw h (with W'), so
+  // only the epilogue needs the row statistics; the first column group's KS warps (they hold whole
+  // rows between them) compute them from their loads while the other warps go on — at KS = 1
+  // (K <= 768) with the LN kernel's reduction (per-lane chunk order, then the xor tree), so mean /
+  // rstd and the materialised a are bit-identical to the LN node; at KS > 1 the slices' sums are
+  // added in slice order through shared memory. (Every warp computing them measured ~1.2 us per
+  // GEMV of SM issue time at T = 1, profiles/r02/decode_gemv_ks.txt.)
+  __shared__ float2 s_mr[MT];
+  const bool ln_warp = ln_a && warp < (uint32_t)KS;
+  for (uint32_t m = 0; m < M; ++m) {
     uint4 x[kGvKV];
     const uint4* ar = reinterpret_cast<const uint4*>(ap + (size_t)m * a.K);
 #pragma unroll
     for (int i = 0; i < kGvKV; ++i) {
-      const uint32_t v = lane + 32u * i;
+      const uint32_t v = v0 + lane + 32u * i;
       if (v < kv) x[i] = ar[v];
     }
-    if (ln_a) {
+    if (ln_warp) {
       float s = 0.f;
 #pragma unroll
       for (int i = 0; i < kGvKV; ++i)
-        if (lane + 32u * i < kv) {
+        if (v0 + lane + 32u * i < kv) {
           const __nv_bfloat16* xb = reinterpret_cast<const __nv_bfloat16*>(&x[i]);
 #pragma unroll
           for (int e = 0; e < 8; ++e) s += __bfloat162float(xb[e]);
         }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if constexpr (KS > 1) {
+        if (lane == 0) s_st[warp] = s;
+        asm volatile("bar.sync 1, %0;\n" ::"r"(KS * 32) : "memory");
+        s = 0.f;
+#pragma unroll
+        for (int j = 0; j < KS; ++j) s += s_st[j];
+        asm volatile("bar.sync 1, %0;\n" ::"r"(KS * 32) : "memory");
+      }
       const float mean = s / (float)a.K;
       float q = 0.f;
 #pragma unroll
       for (int i = 0; i < kGvKV; ++i)
-        if (lane + 32u * i < kv) {
+        if (v0 + lane + 32u * i < kv) {
           const __nv_bfloat16* xb = reinterpret_cast<const __nv_bfloat16*>(&x[i]);
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
@@ -800,20 +870,22 @@ __global__ void __launch_bounds__(kGvWarps * 32) k_gemv_bf16(const __grid_consta
         }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
-      const float rstd = 1.0f / sqrtf(q / (float)a.K + a.ln_eps);
+      if constexpr (KS > 1) {
+        if (lane == 0) s_st[warp] = q;
+        asm volatile("bar.sync 1, %0;\n" ::"r"(KS * 32) : "memory");
+        q = 0.f;
 #pragma unroll
-      for (int mm = 0; mm < kGvMaxM; ++mm)
-        if (mm == (int)m) {
-          ln_mean[mm] = mean;
-          ln_rstd[mm] = rstd;
-        }
-      if (blockIdx.x == 0 && warp == 0)   // the LN node's output row, materialised once
+        for (int j = 0; j < KS; ++j) q += s_st[j];
+        asm volatile("bar.sync 1, %0;\n" ::"r"(KS * 32) : "memory");
+      }
+      const float rstd = 1.0f / sqrtf(q / (float)a.K + a.ln_eps);
+      if (warp == 0 && lane == 0) s_mr[m] = make_float2(mean, rstd);
+      if (ln_mat)   // the LN node's output row, materialised once (each slice by its warp)
 #pragma unroll
         for (int i = 0; i < kGvKV; ++i) {
-          const uint32_t v = lane + 32u * i;
+          const uint32_t v = v0 + lane + 32u * i;
           if (v < kv) {
-            const uint4 gx = __ldg(reinterpret_cast<const uint4*>(a.ln_g) + v);
-            const uint4 bx = __ldg(reinterpret_cast<const uint4*>(a.ln_b) + v);
+            const uint4 gx = s_gb[0][slice][lane + 32u * i], bx = s_gb[1][slice][lane + 32u * i];
             const __nv_bfloat16* xb = reinterpret_cast<const __nv_bfloat16*>(&x[i]);
             const __nv_bfloat16* gb = reinterpret_cast<const __nv_bfloat16*>(&gx);
             const __nv_bfloat16* bb = reinterpret_cast<const __nv_bfloat16*>(&bx);
@@ -832,7 +904,7 @@ __global__ void __launch_bounds__(kGvWarps * 32) k_gemv_bf16(const __grid_consta
       float s0 = 0.f, s1 = 0.f;
 #pragma unroll
       for (int i = 0; i < kGvKV; ++i) {
-        if (lane + 32u * i < kv) {
+        if (v0 + lane + 32u * i < kv) {
           const uint32_t* xp = reinterpret_cast<const uint32_t*>(&x[i]);
           const uint32_t* wp = reinterpret_cast<const uint32_t*>(&w[r][i]);
 #pragma unroll
@@ -846,35 +918,50 @@ __global__ void __launch_bounds__(kGvWarps * 32) k_gemv_bf16(const __grid_consta
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
 #pragma unroll
-      for (int mm = 0; mm < kGvMaxM; ++mm)
+      for (int mm = 0; mm < MT; ++mm)
         if (mm == (int)m) acc[r][mm] = t;
+    }
+  }
+  if constexpr (KS > 1) {   // the slices' partials (summed below in slice order by the slice-0 warp)
+    if (lane == 0)
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int m = 0; m < MT; ++m) s_part[warp][r][m] = acc[r][m];
+  }
+  if (KS > 1 || ln_a) __syncthreads();   // partials and row statistics in shared memory
+  if constexpr (KS > 1) {
+    if (owner)
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int m = 0; m < MT; ++m) {
+          float t = s_part[warp][r][m];
+#pragma unroll
+          for (int j = 1; j < KS; ++j) t += s_part[warp + j][r][m];
+          acc[r][m] = t;
+        }
+  }
+  if (owner) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const uint32_t n = n0 + r;
+      if (n >= a.N) break;
+#pragma unroll
+      for (int m = 0; m < MT; ++m) {
+        if (m >= (int)M) break;
+        float v = acc[r][m];
+        if (ln_a) v = s_mr[m].y * v - s_mr[m].y * s_mr[m].x * e_c1[r] + e_c2[r];   // folded LN
+        v += e_b[r];
+        if (gelu) v = gelu_tanh(v);
+        if (has_res) v += e_res[r][m];
+        a.out[(size_t)m * a.N + n] = __float2bfloat16_rn(v);
+      }
     }
   }
   if (a.ntrace) {
     __syncthreads();
-    if (threadIdx.x == 0) node_stamp(a.ntrace, 2);   // (approximately: before lane 0's epilogue stores)
-  }
-  if (lane != 0) return;
-  const bool has_bias = a.flags & CGX_GEMM_BIAS, gelu = a.flags & CGX_GEMM_GELU;
-  const bool has_res = a.flags & CGX_GEMM_RESIDUAL;
-  const __nv_bfloat16* resp = !has_res ? nullptr
-                              : a.tres >= 0 ? reinterpret_cast<const __nv_bfloat16*>(ld_table(a.table + a.tres))
-                                            : a.residual;
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const uint32_t n = n0 + r;
-    if (n >= a.N) break;
-    const float b = has_bias ? __bfloat162float(a.bias[n]) : 0.f;
-#pragma unroll
-    for (int m = 0; m < kGvMaxM; ++m) {
-      if (m >= (int)a.M) break;
-      float v = acc[r][m];
-      if (ln_a) v = ln_rstd[m] * v - ln_rstd[m] * ln_mean[m] * a.ln_c1[n] + a.ln_c2[n];   // folded LN
-      v += b;
-      if (gelu) v = gelu_tanh(v);
-      if (has_res) v += __bfloat162float(resp[(size_t)m * a.N + n]);
-      a.out[(size_t)m * a.N + n] = __float2bfloat16_rn(v);
-    }
+    if (threadIdx.x == 0) node_stamp(a.ntrace, 2);   // after every warp's stores
   }
 }
 
@@ -1204,7 +1291,7 @@ void decoder_gemm_set_trigger_after_wait(void* args) {
 static bool gemv_shape(uint32_t M, uint32_t N, uint32_t K) {
   const char* ngv = getenv("CGX_GEMM_NO_GEMV");         // measurement / test knob: force tcgen05
   return !(ngv && ngv[0] == '1') && M >= 1 && M <= (uint32_t)kGvMaxM && N >= 1 && K >= 8 && K % 8 == 0 &&
-         K <= (uint32_t)kGvMaxKV * 256;
+         K <= (uint32_t)(kGvMaxKS * kGvKV * 256);
 }
 
 bool decoder_gemm_supported(uint32_t M, uint32_t N, uint32_t K) {
@@ -1216,15 +1303,21 @@ int decoder_gemm_build(uint32_t M, uint32_t N, uint32_t K, uint32_t flags, const
                        size_t* argbytes, dim3* grid, dim3* block, size_t* smem, const void** func) {
   if (!decoder_gemm_supported(M, N, K)) return CGX_E_UNSUPPORTED;
   if (gemv_shape(M, N, K) && !(flags & CGX_GEMM_ALLREDUCE)) {
-    // small-M (decode) path: one output column per warp (more warps in flight beat more rows per
-    // warp at these sizes), per-lane vector count picked from K
-    const int R = 1;
+    // small-M (decode) path: one output column per KS warps, KS = the K slices of 768 columns
+    // (rounded up to a power of two)
+    const uint32_t ks = K <= 768u ? 1u : K <= 1536u ? 2u : K <= 3072u ? 4u : 8u;
     *argbytes = sizeof(GemmArgs);
-    *grid = dim3((N + kGvWarps * R - 1) / (kGvWarps * R));
     *block = dim3(kGvWarps * 32);
     *smem = 0;
-    *func = K <= 768 ? (const void*)k_gemv_bf16<1, 3> : K <= 1536 ? (const void*)k_gemv_bf16<1, 6>
-                                                                   : (const void*)k_gemv_bf16<1, 12>;
+    // (M = 1, the T = 1 decode: scalar accumulators, 64 registers, 4 CTAs per SM; one output
+    // column per warp group: two per warp measured 142.6 -> 157.3 us per decode replay)
+    *grid = dim3((N * ks + kGvWarps - 1) / kGvWarps);
+    if (M == 1)
+      *func = ks == 1 ? (const void*)k_gemv_bf16<1, 1, 1> : ks == 2 ? (const void*)k_gemv_bf16<2, 1, 1>
+            : ks == 4 ? (const void*)k_gemv_bf16<4, 1, 1> : (const void*)k_gemv_bf16<8, 1, 1>;
+    else
+      *func = ks == 1 ? (const void*)k_gemv_bf16<1, kGvMaxM, 1> : ks == 2 ? (const void*)k_gemv_bf16<2, kGvMaxM, 1>
+            : ks == 4 ? (const void*)k_gemv_bf16<4, kGvMaxM, 1> : (const void*)k_gemv_bf16<8, kGvMaxM, 1>;
     if (!args_out) return CGX_OK;
     GemmArgs* g = static_cast<GemmArgs*>(args_out);
     memset(g, 0, sizeof(GemmArgs));

@@ -1731,7 +1731,7 @@ static bool fusable_ln_gemm(const cgx_exec* e, int k) {
     if (q != k + 1)
       for (int i = 0; i < c->nodes[q].n_in; ++i)
         if (c->nodes[q].in[i] == ln.out) return false;
-  if (gemv) return ln.attr.cols <= 3072;   // (the GEMV keeps a whole A row per warp in registers)
+  if (gemv) return true;   // (the GEMV's K slices hold whole A rows: its own statistics)
   const Launch& prev = e->L[e->L.size() - 2];   // (the slot for node k is already emplaced)
   if (prev.kind != LK_KERNEL || prev.mega || prev.pre_node >= 0) return false;
   const Node& p = c->nodes[prev.node];

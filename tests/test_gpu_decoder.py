@@ -111,7 +111,8 @@ def test_gemm_split_tilings_integer_exact(rt, monkeypatch, M, N, K, tiling):
 # the same shapes; every epilogue; integer mode makes both bit-exact against the oracle.
 @pytest.mark.parametrize("M", [1, 2, 5, 8])
 @pytest.mark.parametrize("N,K,gelu,res", [(2304, 768, False, False), (768, 3072, False, True),
-                                          (3072, 768, True, False), (768, 768, False, True), (96, 1032, False, False)])
+                                          (3072, 768, True, False), (768, 768, False, True), (96, 1032, False, False),
+                                          (512, 1536, False, True), (224, 2304, True, False), (288, 6144, False, False)])
 @pytest.mark.parametrize("gemv", [True, False])
 def test_gemm_small_m_paths(rt, monkeypatch, M, N, K, gelu, res, gemv):
     if (not gemv or M > 4) and K % 64:
@@ -477,6 +478,48 @@ def test_c3_decode_fused_ln_gemv(rt):
         # output is bit-identical to the LN kernel's (later ones follow GEMVs on the folded weights)
         first = next(n for k, n in enumerate(spec.nodes) if n.op == "LAYERNORM" and k > 1)
         assert np.array_equal(got[True][first.out], got[False][first.out]), first.out
+    chain.close()
+
+
+@pytest.mark.parametrize("T", [1, 3])
+@pytest.mark.parametrize("d", [768, 1032, 1536, 2048])
+def test_fused_ln_gemv_k_slices(rt, T, d):
+    """LayerNorm folded into a small-M GEMV whose K = d spans 1, 2, 4 or 8 K slices of 768 columns
+    (KS warps per output column, the row statistics added in slice order through shared memory;
+    d <= 2048: the LayerNorm node's own limit):
+    node-local parity of the GEMM output AND of the materialised LN output against the oracle; one
+    launch fewer than the unfused exec."""
+    cgx, runner = rt
+    n = 512
+    slots = [SlotSpec("x", "external", "bf16", T * n), SlotSpec("g0", "static", "bf16", n, "gamma"),
+             SlotSpec("b0", "static", "bf16", n, "bias"), SlotSpec("a0", "internal", "bf16", T * n),
+             SlotSpec("w0", "static", "bf16", d * n, "weight"), SlotSpec("c0", "static", "bf16", d, "bias"),
+             SlotSpec("h", "internal", "bf16", T * d), SlotSpec("g1", "static", "bf16", d, "gamma"),
+             SlotSpec("b1", "static", "bf16", d, "bias"), SlotSpec("a1", "internal", "bf16", T * d),
+             SlotSpec("w1", "static", "bf16", 200 * d, "weight"), SlotSpec("c1", "static", "bf16", 200, "bias"),
+             SlotSpec("y", "internal", "bf16", T * 200)]
+    nodes = [NodeSpec("LAYERNORM", ("x", "g0", "b0"), "a0", {"rows": T, "cols": n, "eps": 1e-5}),
+             NodeSpec("GEMM_BF16", ("a0", "w0", "c0"), "h", {"M": T, "N": d, "K": n, "bias": True, "gelu": True}),
+             NodeSpec("LAYERNORM", ("h", "g1", "b1"), "a1", {"rows": T, "cols": d, "eps": 1e-5}),
+             NodeSpec("GEMM_BF16", ("a1", "w1", "c1"), "y", {"M": T, "N": 200, "K": d, "bias": True, "gelu": False})]
+    spec = ChainSpec(f"ln_gemv_{T}x{d}", slots, nodes, [(0, 3)])
+    st = wl.static_values(spec)
+    dev = torch.device("cuda:0")
+    chain = runner.Chain(spec, runner.upload_statics(spec, st, dev))
+    ex = chain.exec("INDIRECT", fuse=cgx.FUSE_LN_GEMM)
+    ex_u = chain.exec("INDIRECT")
+    assert ex_u.stats()["kernels_per_replay"] - ex.stats()["kernels_per_replay"] == 1
+    for r in range(2):
+        ext = wl.external_values(spec, r)
+        t = runner.upload_externals(spec, ext, dev)
+        ex.bind(t)
+        ex.launch()
+        got = {s_.name: ex.output(s_.name) for s_ in spec.internals()}
+        _node_local_check(spec, st, ext, got)
+        if d == 768:   # one slice: the LN kernel's reduction order, bit-identical LN output
+            ex_u.bind(t)
+            ex_u.launch()
+            assert np.array_equal(got["a1"], ex_u.output("a1"))
     chain.close()
 
 
