@@ -1177,14 +1177,40 @@ def bench_decoder(torch, cgx, runner, wl, stream, dev, peaks):
                 bf_ = min(bf_, e0.elapsed_time(e1) * 1e3 / 300)
             best_f[nm_] = bf_
             dexf.close()
+        dchain.close()
+        # the fused-residual decode chain (84 nodes) with the LayerNorms folded (61 launches)
+        rspec = wl.c3_chain(T=1, n_layers=L, fuse_residual=True)
+        rchain = runner.Chain(rspec, runner.upload_statics(rspec, wl.static_values(rspec), dev))
+        rxs = [runner.host_to_device(wl.slot_values(rspec, "x", r), "bf16", dev) for r in range(4)]
+        rptrs = [cgx.ptr_array([x.data_ptr()]) for x in rxs]
+        rex = rchain.exec("INDIRECT", stream=stream, transport="FIRST_NODE", fuse=cgx.FUSE_LN_GEMM)
+        for i in range(20):
+            LIB.cgx_bind(rex.handle, rptrs[i % 4], 1)
+            LIB.cgx_launch(rex.handle)
+        best_r = 1e30
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            stream.synchronize()
+            e0.record(stream)
+            for i in range(300):
+                LIB.cgx_bind(rex.handle, rptrs[i % 4], 1)
+                LIB.cgx_launch(rex.handle)
+            e1.record(stream)
+            e1.synchronize()
+            best_r = min(best_r, e0.elapsed_time(e1) * 1e3 / 300)
+        r_launches = rex.stats()["kernels_per_replay"]
+        rex.close()
+        rchain.close()
         res["decode_t1"] = {"kernels_per_replay": len(dspec.nodes), "us_per_replay": best_d,
                             "us_per_replay_fused_add_ln": best_f["fused_add_ln"],
                             "us_per_replay_ln_folded": best_f["ln_folded"],
                             "tokens_per_s": 1e6 / best_d,
                             "weight_GBps": 12 * 14.16e6 / (best_d * 1e-6) / 1e9,
+                            "fused_residual_ln_folded": {"kernels_per_replay": r_launches, "us_per_replay": best_r,
+                                                         "tokens_per_s": 1e6 / best_r,
+                                                         "weight_GBps": 12 * 14.16e6 / (best_r * 1e-6) / 1e9},
                             "note": "12 layers, T = 1: GEMM nodes on the small-M weight-stream path "
                                     "(k_gemv_bf16); 170 MB of weights per replay"}
-        dchain.close()
     except Exception as exn:  # noqa: BLE001
         res["decode_t1"] = {"error": str(exn)}
     # the same decoder with the residual adds fused into the O-proj / FC2 GEMM epilogues (SURVEY

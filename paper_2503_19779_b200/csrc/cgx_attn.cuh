@@ -175,6 +175,21 @@ __device__ __forceinline__ void attn_tile(const __nv_bfloat16* qkv_in, __nv_bflo
         mma_bf16_16816(oacc[n], pa, b0, b1);
       }
     }
+    if (nchunk == 1) {
+      // one 32-key chunk (the first two query blocks; every block at T <= 16, decode): warp 0's
+      // partial is the result — normalised and stored from registers, no merge round trip
+      // (bit-identical to the merge, whose single weight is __expf(0) = 1)
+      const float inv0 = 1.0f / l0, inv1 = 1.0f / l1;
+#pragma unroll
+      for (int n = 0; n < 8; ++n) {
+        const uint32_t c = h * kAttnD + 8 * n + 2 * t4;
+        if (qi0 < T) *reinterpret_cast<uint32_t*>(out + (size_t)qi0 * (H * kAttnD) + c) =
+            pack_bf16(oacc[n][0] * inv0, oacc[n][1] * inv0);
+        if (qi1 < T) *reinterpret_cast<uint32_t*>(out + (size_t)qi1 * (H * kAttnD) + c) =
+            pack_bf16(oacc[n][2] * inv1, oacc[n][3] * inv1);
+      }
+      return;
+    }
     // ---- publish this warp's partial (m, l, O) for the merge
     float* o = sO + warp * kAttnQRows * kAttnD;
 #pragma unroll
@@ -190,6 +205,7 @@ __device__ __forceinline__ void attn_tile(const __nv_bfloat16* qkv_in, __nv_bflo
       sML[(warp * kAttnQRows + g + 8) * 2 + 1] = l1;
     }
   }
+  if (nchunk == 1) return;   // (CTA-uniform: warp 0 stored the result above)
   __syncthreads();
   // ---- merge the warps' partials in fixed order: out = sum_w e^{m_w - m} O_w / sum_w e^{m_w - m} l_w
   for (uint32_t idx = threadIdx.x; idx < kAttnQRows * kAttnD / 2; idx += blockDim.x) {
