@@ -81,6 +81,9 @@ static constexpr uint32_t kLnMaxTiles = 64;   // producer N tiles whose row sums
 // This GEMM's epilogue writes per-row {sum, sum of squares} of its bf16 output tile to
 // stats_out[n_tile][M] (float2) for a kGemmLnA consumer.
 static constexpr uint32_t kGemmStatsOut = 1u << 16;
+// Phase tracer (GemmArgs::trace) in SM clock cycles (clock64) instead of %globaltimer, whose 256 ns
+// tick is too coarse for sub-µs phases; cycle stamps are only comparable within one CTA.
+static constexpr uint32_t kGemmTraceClk = 1u << 17;
 
 struct alignas(64) GemmArgs {
   CUtensorMap tmA;            // A [M, K] bf16 as 3-D {64, M, K/64}, box {64, 128, group}
@@ -126,7 +129,8 @@ struct alignas(64) GemmArgs {
 __device__ __forceinline__ void trace_at(const GemmArgs& a, int slot) {
   if (a.trace) {
     unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (a.flags & kGemmTraceClk) t = clock64();
+    else asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     const uint32_t cta = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
     a.trace[cta * 16 + slot] = t;
   }
@@ -262,7 +266,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
   __syncthreads();
   tc_fence_after();
   if (threadIdx.x == 0) trace_at(a, 1);
-  if (S > 1) asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+  // (relaxed: fence.mbarrier_init above already orders the barrier initialisation at cluster scope;
+  // a .release arrive compiles to MEMBAR.ALL.GPU, which drains this thread's outstanding memory ops)
+  if (S > 1) asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
   const uint32_t tmem = *s_tmem;
 
   if (warp == 0) {
@@ -600,10 +606,116 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
       }
       if (threadIdx.x == 64) trace_at(a, 5);
       mbar_wait(recv_full, 0);                            // every peer's rows have landed
-      // our incoming copies are complete (so the peers' staging reads are done): release them
-      asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+      // our incoming copies are complete (so the peers' staging reads are done): let them exit
+      // (no data of ours is published by this arrive: relaxed)
+      asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
       if (threadIdx.x == 64) trace_at(a, 6);
       const uint32_t nq = my_rows * kQRow;
+      if (!ar) {
+        // The owner's quads (up to kQMax per thread) in stages over all of them, every flag test
+        // hoisted out of the per-quad work: the four quads' dependency chains interleave. (One quad
+        // at a time, with the flag branches inside, ran ~570 cycles per quad at one warp per
+        // scheduler: serial short-latency waits and branch resolution, profiles/r02/gemm_epilogue.txt.)
+        float4 acc[kQMax];
+        uint32_t qr[kQMax], qc[kQMax];
+        bool qv[kQMax];
+#pragma unroll
+        for (int j = 0; j < kQMax; ++j) {
+          const uint32_t qi = et + 128u * j;
+          qv[j] = qi < nq;
+          qr[j] = qi / kQRow;
+          qc[j] = 4u * (qi % kQRow);
+          const float* src = recv + (size_t)qr[j] * kRowF + qc[j];
+          const float* own = stg + (size_t)(my_lo + qr[j]) * kRowF + qc[j];
+          acc[j] = qv[j] ? *reinterpret_cast<const float4*>(z == 0 ? own : src) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        for (uint32_t zz = 1; zz < S; ++zz) {          // fixed split order: deterministic sums
+#pragma unroll
+          for (int j = 0; j < kQMax; ++j) {
+            if (!qv[j]) continue;
+            const float* src = recv + (size_t)qr[j] * kRowF + qc[j];
+            const float* own = stg + (size_t)(my_lo + qr[j]) * kRowF + qc[j];
+            const float4 t = *reinterpret_cast<const float4*>(zz == z ? own : src + (size_t)zz * rows_max * kRowF);
+            acc[j].x += t.x;
+            acc[j].y += t.y;
+            acc[j].z += t.z;
+            acc[j].w += t.w;
+          }
+        }
+        float w[kQMax][4];
+        if (ln_a) {   // folded LayerNorm: rstd * acc - rstd * mean * c1 + c2 (after the split sum)
+#pragma unroll
+          for (int j = 0; j < kQMax; ++j) {
+            const float2 m2 = qv[j] ? s_mr[my_lo + qr[j]] : make_float2(0.f, 0.f);   // (rows of s_mr only)
+            const uint32_t c = qc[j];
+            acc[j].x = m2.y * acc[j].x - m2.y * m2.x * s_cc[c].x + s_cc[c].y;
+            acc[j].y = m2.y * acc[j].y - m2.y * m2.x * s_cc[c + 1].x + s_cc[c + 1].y;
+            acc[j].z = m2.y * acc[j].z - m2.y * m2.x * s_cc[c + 2].x + s_cc[c + 2].y;
+            acc[j].w = m2.y * acc[j].w - m2.y * m2.x * s_cc[c + 3].x + s_cc[c + 3].y;
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < kQMax; ++j) {
+          const float4 b4 = *reinterpret_cast<const float4*>(sbias + qc[j]);
+          w[j][0] = acc[j].x + b4.x;
+          w[j][1] = acc[j].y + b4.y;
+          w[j][2] = acc[j].z + b4.z;
+          w[j][3] = acc[j].w + b4.w;
+        }
+        if (gelu) {
+#pragma unroll
+          for (int j = 0; j < kQMax; ++j)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) w[j][i] = gelu_tanh(w[j][i]);
+        }
+        if (has_res) {
+#pragma unroll
+          for (int j = 0; j < kQMax; ++j) {
+            const __nv_bfloat16* rb = reinterpret_cast<const __nv_bfloat16*>(&res_q[j]);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) w[j][i] += __bfloat162float(rb[i]);
+          }
+        }
+        uint2 ov[kQMax];
+#pragma unroll
+        for (int j = 0; j < kQMax; ++j) {
+          __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(&ov[j]);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) ob[i] = __float2bfloat16_rn(w[j][i]);
+        }
+        if (a.flags & kGemmStatsOut) {
+          // row sums of the ROUNDED output for a fused LN consumer: the kQRow threads holding a
+          // row's quads are consecutive lanes (every lane of the warp takes part: the planner keeps
+          // my_rows * kQRow a multiple of 32), reduced by a fixed shuffle tree
+#pragma unroll
+          for (int j = 0; j < kQMax; ++j) {
+            if (128u * j >= nq) break;                 // (warp-uniform: nq % 32 == 0)
+            const int mr = m0 + (int)(my_lo + qr[j]);
+            const bool valid = qv[j] && mr < (int)a.M;
+            float q1 = 0.f, q2 = 0.f;
+            if (valid) {
+              const __nv_bfloat16* ob = reinterpret_cast<const __nv_bfloat16*>(&ov[j]);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const float y = __bfloat162float(ob[i]);
+                q1 += y;
+                q2 += y * y;
+              }
+            }
+#pragma unroll
+            for (uint32_t o = kQRow / 2; o > 0; o >>= 1) {
+              q1 += __shfl_xor_sync(0xffffffffu, q1, o);
+              q2 += __shfl_xor_sync(0xffffffffu, q2, o);
+            }
+            if (valid && (et + 128u * j) % kQRow == 0) a.stats_out[(size_t)blockIdx.x * a.M + mr] = make_float2(q1, q2);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < kQMax; ++j) {
+          const int mr = m0 + (int)(my_lo + qr[j]);
+          if (qv[j] && mr < (int)a.M) *reinterpret_cast<uint2*>(a.out + (size_t)mr * a.N + n0 + qc[j]) = ov[j];
+        }
+      } else {
 #pragma unroll
       for (int j = 0; j < kQMax; ++j) {
         const uint32_t qi = et + 128u * j;
@@ -620,14 +732,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
           acc.z += t.z;
           acc.w += t.w;
         }
-        const bool valid = mr < (int)a.M;
-        if (ln_a) {   // folded LayerNorm: rstd * acc - rstd * mean * c1 + c2 (after the split sum)
-          const float2 m2 = s_mr[my_lo + r];
-          acc.x = m2.y * acc.x - m2.y * m2.x * s_cc[c].x + s_cc[c].y;
-          acc.y = m2.y * acc.y - m2.y * m2.x * s_cc[c + 1].x + s_cc[c + 1].y;
-          acc.z = m2.y * acc.z - m2.y * m2.x * s_cc[c + 2].x + s_cc[c + 2].y;
-          acc.w = m2.y * acc.w - m2.y * m2.x * s_cc[c + 3].x + s_cc[c + 3].y;
-        }
+        if (mr >= (int)a.M) continue;
         float w[4] = {acc.x + sbias[c], acc.y + sbias[c + 1], acc.z + sbias[c + 2], acc.w + sbias[c + 3]};
         if (gelu) {
 #pragma unroll
@@ -642,33 +747,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
         __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(&ov);
 #pragma unroll
         for (int i = 0; i < 4; ++i) ob[i] = __float2bfloat16_rn(w[i]);
-        if (a.flags & kGemmStatsOut) {
-          // row sums of the ROUNDED output for a fused LN consumer: the kQRow threads holding this
-          // row's quads are consecutive lanes (every lane of the warp takes part: the planner keeps
-          // my_rows * kQRow a multiple of 32), reduced by a fixed shuffle tree
-          float q1 = 0.f, q2 = 0.f;
-          if (valid)
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const float y = __bfloat162float(ob[i]);
-              q1 += y;
-              q2 += y * y;
-            }
-#pragma unroll
-          for (uint32_t o = kQRow / 2; o > 0; o >>= 1) {
-            q1 += __shfl_xor_sync(0xffffffffu, q1, o);
-            q2 += __shfl_xor_sync(0xffffffffu, q2, o);
-          }
-          if (valid && qi % kQRow == 0) a.stats_out[(size_t)blockIdx.x * a.M + mr] = make_float2(q1, q2);
-        }
-        if (!valid) continue;
-        if (!ar) {
-          *reinterpret_cast<uint2*>(a.out + (size_t)mr * a.N + n0 + c) = ov;
-        } else {                                   // this rank's bf16 quad -> slot `rank` everywhere
-          const uint32_t par = (s_ar_g - 1u) & 1u;
-          for (uint32_t p = 0; p < a.ar_world; ++p)
-            *reinterpret_cast<uint2*>(ar_slot_ptr(a, p, par, a.ar_rank) + (size_t)mr * a.N + n0 + c) = ov;
-        }
+        // this rank's bf16 quad -> slot `rank` everywhere (the AR path: no folded LN, no stats)
+        const uint32_t par = (s_ar_g - 1u) & 1u;
+        for (uint32_t p = 0; p < a.ar_world; ++p)
+          *reinterpret_cast<uint2*>(ar_slot_ptr(a, p, par, a.ar_rank) + (size_t)mr * a.N + n0 + c) = ov;
+      }
       }
       if (ar) {
         const uint32_t g = s_ar_g;
@@ -703,7 +786,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
     // every peer has received the rows it copied out of this CTA's staging tile
     if (warp < 2) {
       asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-      asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+      asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
     }
     asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
   }
@@ -1278,6 +1361,7 @@ void decoder_gemm_set_node_trace(void* args, unsigned long long* nt) {
 
 void decoder_gemm_set_trace(void* args, unsigned long long* trace) {
   static_cast<GemmArgs*>(args)->trace = trace;
+  if (const char* v = getenv("CGX_GEMM_TRACE_CLK"); v && v[0] == '1') static_cast<GemmArgs*>(args)->flags |= kGemmTraceClk;
 }
 
 void decoder_gemm_set_w_after_wait(void* args) {
