@@ -1183,23 +1183,28 @@ def bench_decoder(torch, cgx, runner, wl, stream, dev, peaks):
         rchain = runner.Chain(rspec, runner.upload_statics(rspec, wl.static_values(rspec), dev))
         rxs = [runner.host_to_device(wl.slot_values(rspec, "x", r), "bf16", dev) for r in range(4)]
         rptrs = [cgx.ptr_array([x.data_ptr()]) for x in rxs]
-        rex = rchain.exec("INDIRECT", stream=stream, transport="FIRST_NODE", fuse=cgx.FUSE_LN_GEMM)
-        for i in range(20):
-            LIB.cgx_bind(rex.handle, rptrs[i % 4], 1)
-            LIB.cgx_launch(rex.handle)
-        best_r = 1e30
-        for _ in range(3):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            stream.synchronize()
-            e0.record(stream)
-            for i in range(300):
+        # (+ the T = 1 attention folded into its O-proj GEMV, fuse = CGX_FUSE_ATTN_GEMM: 50 launches)
+        best_rf, launches_rf = {}, {}
+        for nm_, fz in (("ln", cgx.FUSE_LN_GEMM), ("ln_attn", cgx.FUSE_LN_GEMM | cgx.FUSE_ATTN_GEMM)):
+            rex = rchain.exec("INDIRECT", stream=stream, transport="FIRST_NODE", fuse=fz)
+            for i in range(20):
                 LIB.cgx_bind(rex.handle, rptrs[i % 4], 1)
                 LIB.cgx_launch(rex.handle)
-            e1.record(stream)
-            e1.synchronize()
-            best_r = min(best_r, e0.elapsed_time(e1) * 1e3 / 300)
-        r_launches = rex.stats()["kernels_per_replay"]
-        rex.close()
+            bf_ = 1e30
+            for _ in range(3):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                stream.synchronize()
+                e0.record(stream)
+                for i in range(300):
+                    LIB.cgx_bind(rex.handle, rptrs[i % 4], 1)
+                    LIB.cgx_launch(rex.handle)
+                e1.record(stream)
+                e1.synchronize()
+                bf_ = min(bf_, e0.elapsed_time(e1) * 1e3 / 300)
+            best_rf[nm_], launches_rf[nm_] = bf_, rex.stats()["kernels_per_replay"]
+            rex.close()
+        best_r, r_launches = best_rf["ln"], launches_rf["ln"]
+        best_ra = best_rf["ln_attn"]
         rchain.close()
         res["decode_t1"] = {"kernels_per_replay": len(dspec.nodes), "us_per_replay": best_d,
                             "us_per_replay_fused_add_ln": best_f["fused_add_ln"],
@@ -1209,6 +1214,10 @@ def bench_decoder(torch, cgx, runner, wl, stream, dev, peaks):
                             "fused_residual_ln_folded": {"kernels_per_replay": r_launches, "us_per_replay": best_r,
                                                          "tokens_per_s": 1e6 / best_r,
                                                          "weight_GBps": 12 * 14.16e6 / (best_r * 1e-6) / 1e9},
+                            "fused_residual_ln_attn_folded": {"kernels_per_replay": launches_rf["ln_attn"],
+                                                              "us_per_replay": best_ra, "tokens_per_s": 1e6 / best_ra,
+                                                              "weight_GBps": 12 * 14.16e6 / (best_ra * 1e-6) / 1e9,
+                                                              "hbm_frac": 12 * 14.16e6 / (best_ra * 1e-6) / 1e9 / peaks.get("hbm_gbs", 6650.0)},
                             "note": "12 layers, T = 1: GEMM nodes on the small-M weight-stream path "
                                     "(k_gemv_bf16); 170 MB of weights per replay"}
     except Exception as exn:  # noqa: BLE001

@@ -195,16 +195,23 @@ typedef struct {
   int fuse;                 /* capture-time fusions (bit mask, 0 = none). CGX_FUSE_ADD_LN runs a
                                bf16 ADD and the LAYERNORM that normalises its output as ONE launch
                                (both output slots written, bit-identical to the two kernels).
-                               CGX_FUSE_LN_GEMM runs a LAYERNORM inside the A prologue of the GEMM
-                               that consumes it when the LN input comes from the previous GEMM
-                               launch: that GEMM writes per-tile row sums, the consumer normalises
-                               A in shared memory and stores the LN output slot (mean / variance
-                               from the sums: not bit-identical to the LN kernel, within the bf16
-                               tolerance). The exec then has fewer launches than nodes (cgx_stats
-                               n_nodes counts nodes, kernels_per_replay launches) */
+                               CGX_FUSE_LN_GEMM folds a LAYERNORM into the GEMM that consumes it
+                               (a W^T = rstd (h W'^T) - rstd mean c1 + c2 with W' = gamma-scaled W,
+                               prepared once at exec creation): tcgen05 consumers take mean / rstd
+                               from per-tile row sums the previous GEMM launch writes (not
+                               bit-identical to the LN kernel, within the bf16 tolerance); small-M
+                               (GEMV) consumers compute them from their own A loads with the LN
+                               kernel's reduction order; the LN output slot is still stored.
+                               CGX_FUSE_ATTN_GEMM folds a T = 1 ATTN_CAUSAL (the decode step) into
+                               its small-M (GEMV) consumer, which forms A = attention(qkv) itself
+                               (one visible key: A = v exactly, bit-identical to the kernel) and stores
+                               the ATTN output slot. The exec then has fewer launches
+                               than nodes (cgx_stats n_nodes counts nodes, kernels_per_replay
+                               launches) */
 } cgx_exec_opts;
 #define CGX_FUSE_ADD_LN 1
 #define CGX_FUSE_LN_GEMM 2
+#define CGX_FUSE_ATTN_GEMM 4
 
 typedef enum {
   CGX_SYNC_AUTO = 0, CGX_SYNC_DEFER = 1, CGX_SYNC_CHAIN = 2, CGX_SYNC_GRAPH = 3, CGX_SYNC_DATAFLOW = 4

@@ -36,6 +36,7 @@ MAX_PROFILE_KERNELS = 1024
 MAX_PROFILE_DEPS = 8192
 FUSE_ADD_LN = 1
 FUSE_LN_GEMM = 2
+FUSE_ATTN_GEMM = 4
 
 
 class Attr(C.Structure):
@@ -225,7 +226,7 @@ def chain_destroy(chain: int):
 def exec_create(chain: int, mode: str, stream: int, transport: str = "DEFAULT", first_node: int = 0,
                 n_nodes: int = 0, no_pdl: bool = False, validate: int = 0, copy_impl: int = 0,
                 sync: str = "AUTO", graph_streams: int = 0, megakernel: bool = False, fuse: int = 0) -> int:
-    """fuse: bit mask of capture-time fusions (FUSE_ADD_LN)."""
+    """fuse: bit mask of capture-time fusions (FUSE_ADD_LN | FUSE_LN_GEMM | FUSE_ATTN_GEMM)."""
     o = ExecOpts(MODE[mode], XPORT[transport], first_node, n_nodes, int(no_pdl), validate, copy_impl,
                  SYNC[sync], graph_streams, int(megakernel), int(fuse))
     out = C.c_void_p()

@@ -84,6 +84,12 @@ static constexpr uint32_t kGemmStatsOut = 1u << 16;
 // Phase tracer (GemmArgs::trace) in SM clock cycles (clock64) instead of %globaltimer, whose 256 ns
 // tick is too coarse for sub-µs phases; cycle stamps are only comparable within one CTA.
 static constexpr uint32_t kGemmTraceClk = 1u << 17;
+// Causal attention folded into the small-M (GEMV) consumer (exec option fuse & CGX_FUSE_ATTN_GEMM,
+// T = M = 1, the decode step): every warp forms its K slice of A = softmax(q k^T *
+// scale) v from the qkv row itself (one visible key: exactly v, gv_attn_row); the first column
+// group's warps of CTA 0 store the ATTN node's output row, so every node output is still
+// materialised.
+static constexpr uint32_t kGemmAttnA = 1u << 18;
 
 struct alignas(64) GemmArgs {
   CUtensorMap tmA;            // A [M, K] bf16 as 3-D {64, M, K/64}, box {64, 128, group}
@@ -124,6 +130,8 @@ struct alignas(64) GemmArgs {
   uint32_t ln_ntiles;
   float ln_eps;
   uint32_t ln_dbg;            // measurement knob (CGX_LN_DBG): 1 = serial stats loop, 2 = skip the LN output
+  const __nv_bfloat16* attn_qkv;  // kGemmAttnA: the ATTN node's input [M][3 K] (q | k | v, head-major)
+  __nv_bfloat16* attn_out;        // kGemmAttnA: the ATTN node's output slot [M][K]
 };
 
 __device__ __forceinline__ void trace_at(const GemmArgs& a, int slot) {
@@ -821,6 +829,20 @@ static constexpr int kGvMaxKS = 8;   // slices per column: K <= 8 * 768 = 6144
 __device__ __forceinline__ float bf16lo(uint32_t u) { return __uint_as_float(u << 16); }
 __device__ __forceinline__ float bf16hi(uint32_t u) { return __uint_as_float(u & 0xffff0000u); }
 
+// kGemmAttnA (M = 1): this lane's kGvKV 16-B vectors of the attention output row. With T = 1 the
+// causal softmax has one visible key, so p_0 = __expf(s_0 - s_0) = 1, l = 1 and the output row is
+// bf16(1 * v_0 * (1 / 1)) = v_0 exactly — what the attention kernel (cgx_attn.cuh) computes for a
+// one-key tile, bit for bit — and the q / k segments of the qkv row do not enter it.
+__device__ __forceinline__ void gv_attn_row(const GemmArgs& a, uint32_t v0, uint32_t lane, uint32_t kv,
+                                            uint4 (&x)[kGvKV]) {
+  const uint4* vrow = reinterpret_cast<const uint4*>(a.attn_qkv) + 2 * kv;   // v segment of qkv row 0
+#pragma unroll
+  for (int i = 0; i < kGvKV; ++i) {
+    const uint32_t v = v0 + lane + 32u * i;
+    if (v < kv) x[i] = vrow[v];
+  }
+}
+
 template <int KS, int MT, int R>
 __global__ void __launch_bounds__(kGvWarps * 32, MT == 1 ? (R == 1 ? 4 : 3) : 3) k_gemv_bf16(const __grid_constant__ GemmArgs a) {
   static_assert(kGvWarps % KS == 0, "slices of a column stay in one CTA");
@@ -912,13 +934,25 @@ __global__ void __launch_bounds__(kGvWarps * 32, MT == 1 ? (R == 1 ? 4 : 3) : 3)
   // GEMV of SM issue time at T = 1, profiles/r02/decode_gemv_ks.txt.)
   __shared__ float2 s_mr[MT];
   const bool ln_warp = ln_a && warp < (uint32_t)KS;
+  const bool attn_a = a.flags & kGemmAttnA;
+  const bool attn_mat = attn_a && blockIdx.x == 0 && warp < (uint32_t)KS;
   for (uint32_t m = 0; m < M; ++m) {
     uint4 x[kGvKV];
-    const uint4* ar = reinterpret_cast<const uint4*>(ap + (size_t)m * a.K);
+    if (MT == 1 && attn_a) {   // (M = 1 instantiations only: the M <= 4 ones keep their registers)
+      gv_attn_row(a, v0, lane, kv, x);
+      if (attn_mat)   // the ATTN node's output row, materialised once (each slice by its warp)
 #pragma unroll
-    for (int i = 0; i < kGvKV; ++i) {
-      const uint32_t v = v0 + lane + 32u * i;
-      if (v < kv) x[i] = ar[v];
+        for (int i = 0; i < kGvKV; ++i) {
+          const uint32_t v = v0 + lane + 32u * i;
+          if (v < kv) reinterpret_cast<uint4*>(a.attn_out + (size_t)m * a.K)[v] = x[i];
+        }
+    } else {
+      const uint4* ar = reinterpret_cast<const uint4*>(ap + (size_t)m * a.K);
+#pragma unroll
+      for (int i = 0; i < kGvKV; ++i) {
+        const uint32_t v = v0 + lane + 32u * i;
+        if (v < kv) x[i] = ar[v];
+      }
     }
     if (ln_warp) {
       float s = 0.f;
@@ -1272,6 +1306,17 @@ int decoder_ln_fold_prep(const void* W, const void* gamma, const void* beta, uin
 }
 
 bool decoder_gemm_is_gemv(uint32_t M, uint32_t N, uint32_t K) { return gemv_shape(M, N, K); }
+
+int decoder_gemm_set_attn_a(void* args, const void* qkv, void* attn_out, uint32_t H, uint32_t D, float scale) {
+  GemmArgs* g = static_cast<GemmArgs*>(args);
+  if (!gemv_shape(g->M, g->N, g->K) || (g->flags & (CGX_GEMM_ALLREDUCE | kGemmLnA)) || g->ta >= 0) return CGX_E_UNSUPPORTED;
+  if (D != 64 || g->K != H * D || g->M != 1) return CGX_E_UNSUPPORTED;   // (k_gemv_bf16<KS, 1, 1> only)
+  g->attn_qkv = static_cast<const __nv_bfloat16*>(qkv);
+  g->attn_out = static_cast<__nv_bfloat16*>(attn_out);
+  (void)scale;   // one visible key: the softmax weight is 1 whatever the scaled score
+  g->flags |= kGemmAttnA;
+  return CGX_OK;
+}
 
 bool decoder_gemm_is_tcgen05(const void* func) {
   return func == (const void*)k_gemm_bf16<32, false> || func == (const void*)k_gemm_bf16<64, false> ||

@@ -1782,6 +1782,43 @@ static int build_ln_gemm(cgx_exec* e, int k, bool* fused) {
   return build_launch(e, k, l);   // not fusable after all: the LN keeps its own launch
 }
 
+// CGX_FUSE_ATTN_GEMM: node k is an ATTN_CAUSAL over T = 1 query (decode) whose output the next node, a
+// small-M GEMM (GEMV path), reads as A with K = H * D; not the first two nodes of the range (the
+// FIRST_NODE transport's by-value prefix keeps one launch per node there). Other readers of the
+// attention output are fine: the fused launch still stores it.
+static bool fusable_attn_gemm(const cgx_exec* e, int k) {
+  const cgx_chain* c = e->c;
+  if (k >= e->last || k <= e->first + 1) return false;
+  const Node& at = c->nodes[k];
+  const Node& g = c->nodes[k + 1];
+  if (at.op != CGX_OP_ATTN_CAUSAL || g.op != CGX_OP_GEMM_BF16 || g.in[0] != at.out) return false;
+  if (g.attr.flags & CGX_GEMM_ALLREDUCE) return false;
+  if (c->slots[at.in[0]].kind == CGX_SLOT_EXTERNAL) return false;
+  return at.attr.D == 64 && at.attr.T == 1 && g.attr.M == at.attr.T && g.attr.K == at.attr.H * at.attr.D &&
+         decoder_gemm_is_gemv(g.attr.M, g.attr.N, g.attr.K);
+}
+
+// Build the ATTN (k) -> GEMV (k + 1) pair as ONE launch of the GEMV forming its A operand from the
+// attention's qkv input (k_gemm.cu kGemmAttnA) and storing the ATTN output slot. *fused = false
+// (the ATTN built as a launch of its own) when the GEMV cannot take the role.
+static int build_attn_gemm(cgx_exec* e, int k, bool* fused) {
+  cgx_chain* c = e->c;
+  const Node& at = c->nodes[k];
+  Launch& l = e->L.back();
+  *fused = false;
+  Launch g;
+  CKS(build_launch(e, k + 1, g, k));
+  const Slot& qs = c->slots[at.in[0]];
+  const void* qkv = qs.kind == CGX_SLOT_STATIC ? qs.static_ptr : qs.buf;
+  if (decoder_gemm_set_attn_a(g.args.p, qkv, c->slots[at.out].buf, at.attr.H, at.attr.D, at.attr.scalar) == CGX_OK) {
+    g.pre_node = k;
+    l = std::move(g);
+    *fused = true;
+    return CGX_OK;
+  }
+  return build_launch(e, k, l);
+}
+
 // ---------------------------------------------------------------- megakernel (cgx_mega.h)
 
 // Compile the exec's node range into the stages of ONE persistent launch:
@@ -2159,7 +2196,8 @@ extern "C" int cgx_exec_create_ex(cgx_chain* c, const cgx_exec_opts* opts, void*
   if (o.sync_mode < CGX_SYNC_AUTO || o.sync_mode > CGX_SYNC_DATAFLOW) return fail(CGX_E_INVALID_ARG, "exec_create: sync_mode");
   if (o.graph_streams < 0 || o.graph_streams > 64) return fail(CGX_E_INVALID_ARG, "exec_create: graph_streams (0..64)");
   if (o.megakernel < 0 || o.megakernel > 1) return fail(CGX_E_INVALID_ARG, "exec_create: megakernel (0 or 1)");
-  if (o.fuse & ~(CGX_FUSE_ADD_LN | CGX_FUSE_LN_GEMM)) return fail(CGX_E_INVALID_ARG, "exec_create: fuse (unknown bits)");
+  if (o.fuse & ~(CGX_FUSE_ADD_LN | CGX_FUSE_LN_GEMM | CGX_FUSE_ATTN_GEMM))
+    return fail(CGX_E_INVALID_ARG, "exec_create: fuse (unknown bits)");
   const int K = (int)c->nodes.size();
   if (K == 0) return fail(CGX_E_STATE, "exec_create: empty chain");
   const int first = o.first_node, last = o.n_nodes ? o.first_node + o.n_nodes - 1 : K - 1;
@@ -2227,6 +2265,10 @@ extern "C" int cgx_exec_create_ex(cgx_chain* c, const cgx_exec_opts* opts, void*
       } else if ((o.fuse & CGX_FUSE_LN_GEMM) && fusable_ln_gemm(e, k)) {
         bool fused = false;
         if ((st = build_ln_gemm(e, k, &fused)) != CGX_OK) return bail(st);
+        if (fused) ++k;
+      } else if ((o.fuse & CGX_FUSE_ATTN_GEMM) && fusable_attn_gemm(e, k)) {
+        bool fused = false;
+        if ((st = build_attn_gemm(e, k, &fused)) != CGX_OK) return bail(st);
         if (fused) ++k;
       } else if ((st = build_launch(e, k, e->L.back())) != CGX_OK) {
         return bail(st);

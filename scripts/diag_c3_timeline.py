@@ -2,7 +2,7 @@
 PDL wait ("ready") and last CTA exit, in µs from the first entry of the replay (INDIRECT,
 ROOT_PARAMS, best of 5 replays by span). Per op class: mean post-wait work (exit - ready) and mean
 critical-path gap (ready - predecessor exit: the launch / dependency-resolution latency the chain
-pays per node). Usage: diag_c3_timeline.py [T] [layers] [--fuse]"""
+pays per node). Usage: diag_c3_timeline.py [T] [layers] [--fuse] [--ln-gemm] [--attn-gemm]"""
 import json
 import os
 import sys
@@ -26,7 +26,8 @@ dev = torch.device("cuda:0")
 spec = wl.c3_chain(T=T, n_layers=L, fuse_residual=fuse)
 chain = runner.Chain(spec, runner.upload_statics(spec, wl.static_values(spec), dev))
 xs = [runner.host_to_device(wl.slot_values(spec, "x", r), "bf16", dev) for r in range(2)]
-ex = chain.exec("INDIRECT", fuse=cgx.FUSE_LN_GEMM if ln_gemm else 0)
+fz = (cgx.FUSE_LN_GEMM if ln_gemm else 0) | (cgx.FUSE_ATTN_GEMM if "--attn-gemm" in sys.argv else 0)
+ex = chain.exec("INDIRECT", fuse=fz)
 for i in range(20):
     ex.bind({"x": xs[i % 2]})
     ex.launch()

@@ -21,7 +21,8 @@ for fr in (False, True):
     chain = runner.Chain(spec, runner.upload_statics(spec, wl.static_values(spec), dev))
     xs = [runner.host_to_device(wl.slot_values(spec, "x", r), "bf16", dev) for r in range(4)]
     ptrs = [cgx.ptr_array([x.data_ptr()]) for x in xs]
-    for name, fz in (("none", 0), ("add_ln", cgx.FUSE_ADD_LN), ("ln_gemm", cgx.FUSE_LN_GEMM)):
+    for name, fz in (("none", 0), ("add_ln", cgx.FUSE_ADD_LN), ("ln_gemm", cgx.FUSE_LN_GEMM),
+                     ("ln_attn_gemm", cgx.FUSE_LN_GEMM | cgx.FUSE_ATTN_GEMM)):
         ex = chain.exec("INDIRECT", stream=stream, transport="FIRST_NODE", fuse=fz)
         for i in range(20):
             cgx.LIB.cgx_bind(ex.handle, ptrs[i % 4], 1)

@@ -481,6 +481,63 @@ def test_c3_decode_fused_ln_gemv(rt):
     chain.close()
 
 
+@pytest.mark.parametrize("n_layers", [1, 12])
+def test_c3_decode_fused_attn_gemv(rt, n_layers):
+    """T = 1 decode with the attention folded into its O-proj GEMV (fuse = CGX_FUSE_ATTN_GEMM, on
+    top of the LN fold): one launch fewer per layer past the first two nodes; the GEMV forms
+    A = attention(qkv) itself and stores the ATTN output slot, which at T = 1 (one key: p = 1) is
+    bit-identical to the attention kernel's, so EVERY node output equals the LN-folded exec's;
+    node-local parity against the oracle; all rebinding arms bit-identical."""
+    cgx, runner = rt
+    spec = wl.c3_chain(T=1, n_layers=n_layers, fuse_residual=True)
+    st = wl.static_values(spec)
+    dev = torch.device("cuda:0")
+    attns = sum(1 for k, n in enumerate(spec.nodes) if n.op == "ATTN_CAUSAL" and k > 1)
+    arms = [("INDIRECT", "FIRST_NODE"), ("INDIRECT", "ROOT_PARAMS"), ("INDIRECT", "PRELUDE"),
+            ("COPY", "DEFAULT"), ("SETPARAMS", "DEFAULT"), ("EAGER", "DEFAULT")]
+    ref = None
+    for mode, xp in arms:
+        chain = runner.Chain(spec, runner.upload_statics(spec, st, dev))
+        ex = chain.exec(mode, transport=xp, fuse=cgx.FUSE_LN_GEMM | cgx.FUSE_ATTN_GEMM)
+        ex_l = chain.exec(mode, transport=xp, fuse=cgx.FUSE_LN_GEMM)
+        assert ex_l.stats()["kernels_per_replay"] - ex.stats()["kernels_per_replay"] == attns
+        outs = []
+        for r in range(3):
+            ext = wl.external_values(spec, r)
+            t = runner.upload_externals(spec, ext, dev)
+            got = {}
+            for e_ in (ex, ex_l):
+                e_.bind(t)
+                e_.launch()
+                got[e_ is ex] = {s_.name: e_.output(s_.name) for s_ in spec.internals()}
+            for k in got[True]:
+                assert np.array_equal(got[True][k], got[False][k]), (mode, xp, r, k)
+            outs.append(got[True])
+            if ref is None:
+                _node_local_check(spec, st, ext, got[True])
+        chain.close()
+        if ref is None:
+            ref = outs
+        else:
+            for r in range(3):
+                for k in ref[r]:
+                    assert np.array_equal(outs[r][k], ref[r][k]), (mode, xp, k)
+
+
+def test_fused_attn_gemv_not_applied_beyond_t1(rt):
+    """The attention fold is a T = 1 (decode) fusion: at T = 4 (GEMV path, several keys) and
+    T = 128 (tcgen05 path) the exec keeps one launch per ATTN node."""
+    cgx, runner = rt
+    dev = torch.device("cuda:0")
+    for T in (4, 128):
+        spec = wl.c3_chain(T=T, n_layers=1, fuse_residual=True)
+        chain = runner.Chain(spec, runner.upload_statics(spec, wl.static_values(spec), dev))
+        a = chain.exec("INDIRECT", fuse=cgx.FUSE_ATTN_GEMM).stats()["kernels_per_replay"]
+        b = chain.exec("INDIRECT").stats()["kernels_per_replay"]
+        assert a == b, T
+        chain.close()
+
+
 @pytest.mark.parametrize("T", [1, 3])
 @pytest.mark.parametrize("d", [768, 1032, 1536, 2048])
 def test_fused_ln_gemv_k_slices(rt, T, d):
