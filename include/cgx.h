@@ -350,6 +350,11 @@ int cgx_debug_gemm_trace(cgx_exec* e, int pos, uint64_t* host_out, int cap, int*
  * (an untraced launch keeps entry == ready == UINT64_MAX, exit == 0).
  * CGX_E_STATE when tracing is off. Synchronises the exec's stream. */
 int cgx_debug_node_trace(cgx_exec* e, uint64_t* host_out, int cap, int* n_out);
+/* Diagnostics: per-CTA phase stamps [cta][8] (%globaltimer ns) of the last replay of ATTN_CAUSAL
+   launch `pos`, for an exec created with the environment variable CGX_CTA_TRACE=1 (0 entry, 1 past
+   the PDL wait, 2 K/V staged, 3 partials published, 4 exit). host_out may be NULL (count only).
+   Returns the CTA count, or CGX_E_INVALID_ARG (not an attention launch) / CGX_E_STATE (no trace). */
+int cgx_debug_cta_trace(cgx_exec* e, int pos, uint64_t* host_out, int cap);
 /* Diagnostics: the chain node each launch position runs (a fused launch reports its last node;
  * cgx_exec_opts.fuse / megakernel make launches fewer than nodes). *n_out = launch count. */
 int cgx_debug_launch_nodes(const cgx_exec* e, int* nodes_out, int cap, int* n_out);

@@ -141,6 +141,7 @@ def _load():
         "cgx_debug_ext_field_offsets": ([VP, I, P(U64), I, P(I)], I),
         "cgx_debug_gemm_trace": ([VP, I, P(U64), I, P(I)], I),
         "cgx_debug_node_trace": ([VP, P(U64), I, P(I)], I),
+        "cgx_debug_cta_trace": ([VP, I, P(U64), I], I),
         "cgx_debug_mega_trace": ([VP, P(U64), I], I),
         "cgx_debug_launch_nodes": ([VP, P(I), I, P(I)], I),
         "cgx_device_loop": ([VP, VP, I, U64], I),
@@ -169,7 +170,7 @@ EXPORTED = ("cgx_version", "cgx_last_error", "cgx_chain_create", "cgx_chain_add_
             "cgx_launch", "cgx_output", "cgx_output_gather", "cgx_stats", "cgx_debug_read_table",
             "cgx_debug_setparam_nodes", "cgx_exec_destroy", "cgx_profile", "cgx_profile_ex", "cgx_select",
             "cgx_dispatch_floor", "cgx_fill_uniform_f32", "cgx_copy", "cgx_graph_floor", "cgx_kernel_times", "cgx_find_param_offset",
-            "cgx_debug_param_image", "cgx_debug_ext_field_offsets", "cgx_debug_gemm_trace", "cgx_debug_node_trace", "cgx_debug_mega_trace", "cgx_debug_launch_nodes", "cgx_device_loop", "cgx_nccl_unique_id",
+            "cgx_debug_param_image", "cgx_debug_ext_field_offsets", "cgx_debug_gemm_trace", "cgx_debug_node_trace", "cgx_debug_cta_trace", "cgx_debug_mega_trace", "cgx_debug_launch_nodes", "cgx_device_loop", "cgx_nccl_unique_id",
             "cgx_nccl_comm_init", "cgx_nccl_comm_destroy", "cgx_peer_buffer_bytes", "cgx_chain_set_peers",
             "cgx_device_alloc", "cgx_device_free",
             "cgx_ipc_handle", "cgx_ipc_open", "cgx_ipc_close", "cgx_tune_graph_streams")
@@ -341,6 +342,15 @@ def node_trace(ex: int, n_launch: int) -> list:
     buf = (C.c_uint64 * (3 * n_launch))()
     _ck(LIB.cgx_debug_node_trace(ex, buf, 3 * n_launch, C.byref(n)), "cgx_debug_node_trace")
     return [tuple(buf[3 * i: 3 * i + 3]) for i in range(n.value)]
+
+
+def cta_trace(ex: int, pos: int) -> list:
+    """[[8 ns stamps] per CTA] of ATTN launch `pos` (exec created with CGX_CTA_TRACE=1)."""
+    n = LIB.cgx_debug_cta_trace(ex, pos, None, 0)
+    _ck(n if n < 0 else 0, "cgx_debug_cta_trace")
+    buf = (C.c_uint64 * (8 * n))()
+    _ck(min(0, LIB.cgx_debug_cta_trace(ex, pos, buf, 8 * n)), "cgx_debug_cta_trace")
+    return [list(buf[8 * i: 8 * i + 8]) for i in range(n)]
 
 
 def launch_nodes(ex: int) -> list:

@@ -141,6 +141,7 @@ struct AttnArgs {
   uint32_t T, H, D, flags;
   float scale;
   unsigned long long* ntrace;   // CGX_NODE_TRACE=1 (node_stamp)
+  unsigned long long* ctrace;   // CGX_CTA_TRACE=1: per-CTA [cta][8] %globaltimer phase stamps (diagnostics)
 };
 
 // T5 (FIRST_NODE transport): the first node of the graph carries the bound pointers by value; its

@@ -39,6 +39,11 @@ __device__ __forceinline__ void ldsm_x2(uint32_t addr, uint32_t& r0, uint32_t& r
 __device__ __forceinline__ void ldsm_x2_trans(uint32_t addr, uint32_t& r0, uint32_t& r1) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0,%1}, [%2];\n" : "=r"(r0), "=r"(r1) : "r"(addr));
 }
+__device__ __forceinline__ unsigned long long attn_gtime() {   // diagnostics (per-CTA phase stamps)
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<const uint32_t*>(&v);
@@ -47,8 +52,17 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 // One attention tile: query rows [16 qblock, 16 qblock + 16) of head h, with blockDim.x threads
 // (>= one warp per 32-key chunk of the causal range; extra warps only help with the loads).
 // Shared by k_attention (one tile per CTA) and the persistent decoder executor (k_mega.cu).
+// kBulk (per-node kernel, CGX_ATTN_BULK=1 measurement variant): Q / K / V rows arrive by 128-B
+// cp.async.bulk copies issued one row per thread on the mbarrier `bar` (initialised by the caller
+// before its PDL wait), rows past the causal range zero-filled, Q fragments read from shared memory
+// with ldmatrix.x4 — instead of every thread computing and guarding 16 vector loads plus 16
+// Q-fragment loads (the deployed replay's per-CTA trace put the K/V staging at ~2 us after the
+// wait, profiles/r02/attn_cta.txt). It staged sooner (median 1.5 us) but replayed the C3 chain
+// 3.5 us slower, so the register path stays the default.
+template <bool kBulk = false>
 __device__ __forceinline__ void attn_tile(const __nv_bfloat16* qkv_in, __nv_bfloat16* out, uint32_t T, uint32_t H,
-                                          float scale, uint32_t qblock, uint32_t h, uint8_t* smem) {
+                                          float scale, uint32_t qblock, uint32_t h, uint8_t* smem,
+                                          unsigned long long* ct = nullptr, uint64_t* bar = nullptr) {
   const uint32_t q0 = qblock * kAttnQRows;
   const uint32_t kend = min(T, q0 + kAttnQRows);                 // keys [0, kend) are visible to the block
   const uint32_t nchunk = (kend + kAttnKChunk - 1) / kAttnKChunk;
@@ -61,9 +75,50 @@ __device__ __forceinline__ void attn_tile(const __nv_bfloat16* qkv_in, __nv_bflo
   uint8_t* sV = sK + cap_rows * kKVRowB;
   float* sO = reinterpret_cast<float*>(sV + cap_rows * kKVRowB);  // [warps][16][64]
   float* sML = sO + (cap_rows / kAttnKChunk) * kAttnQRows * kAttnD; // [warps][16][2]
+  uint8_t* sQ = reinterpret_cast<uint8_t*>(sML + (cap_rows / kAttnKChunk) * kAttnQRows * 2);   // kBulk: [16][kKVRowB]
 
   // ---- loads: Q fragments (registers), K/V rows [0, nchunk*32) -> smem (zero beyond kend)
   uint32_t qa[4][4];
+  if constexpr (kBulk) {
+    const uint32_t nrow = nchunk * kAttnKChunk;
+    const uint32_t qrows = min((uint32_t)kAttnQRows, T - q0);
+    const uint32_t ncopy = 2 * kend + qrows;
+    if (threadIdx.x == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"((uint32_t)__cvta_generic_to_shared(bar)),
+                   "r"(ncopy * (uint32_t)(kAttnD * 2)) : "memory");
+    for (uint32_t i = threadIdx.x; i < ncopy; i += blockDim.x) {
+      const uint32_t which = i < kend ? 0u : i < 2 * kend ? 1u : 2u;   // K, V, Q
+      const uint32_t j = which == 0 ? i : which == 1 ? i - kend : q0 + (i - 2 * kend);
+      const __nv_bfloat16* src = qkv + (size_t)j * row_el + (which == 2 ? 0u : (1 + which) * H * kAttnD) + h * kAttnD;
+      uint8_t* dst = which == 0 ? sK + j * kKVRowB : which == 1 ? sV + j * kKVRowB : sQ + (j - q0) * kKVRowB;
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                   ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src), "r"((uint32_t)(kAttnD * 2)),
+                   "r"((uint32_t)__cvta_generic_to_shared(bar)) : "memory");
+    }
+    // rows past the causal range / past T: zeros (P = 0 there, and 0 * garbage could be NaN)
+    const uint32_t zkv = (nrow - kend) * 8, nz = 2 * zkv + (kAttnQRows - qrows) * 8;
+    for (uint32_t i = threadIdx.x; i < nz; i += blockDim.x) {
+      uint8_t* d = i < zkv ? sK + (kend + i / 8) * kKVRowB + 16 * (i % 8)
+                 : i < 2 * zkv ? sV + (kend + (i - zkv) / 8) * kKVRowB + 16 * ((i - zkv) % 8)
+                               : sQ + (qrows + (i - 2 * zkv) / 8) * kKVRowB + 16 * ((i - 2 * zkv) % 8);
+      *reinterpret_cast<uint4*>(d) = make_uint4(0u, 0u, 0u, 0u);
+    }
+    {
+      const uint32_t ba = (uint32_t)__cvta_generic_to_shared(bar);
+      uint32_t done = 0;
+      while (!done)
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n selp.u32 %0, 1, 0, p;\n}\n"
+                     : "=r"(done) : "r"(ba) : "memory");
+    }
+    __syncthreads();   // (the zero fill)
+    // Q fragments from the staged rows: matrices rows 0-7 / 8-15 x dims 16kk..+8 / +8..+16
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      const uint32_t addr = (uint32_t)__cvta_generic_to_shared(sQ + (lane & 15) * kKVRowB + (16 * kk + (lane >> 4) * 8) * 2);
+      asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+                   : "=r"(qa[kk][0]), "=r"(qa[kk][1]), "=r"(qa[kk][2]), "=r"(qa[kk][3]) : "r"(addr));
+    }
+  } else {
   {
     const uint32_t r0 = q0 + g, r1 = q0 + g + 8;
 #pragma unroll
@@ -99,6 +154,8 @@ __device__ __forceinline__ void attn_tile(const __nv_bfloat16* qkv_in, __nv_bflo
     }
   }
   __syncthreads();
+  }
+  if (ct && threadIdx.x == 0) ct[2] = attn_gtime();   // (diagnostics: K/V staged)
 
   if (warp < nchunk) {
     const uint32_t k0 = warp * kAttnKChunk;
@@ -207,6 +264,7 @@ __device__ __forceinline__ void attn_tile(const __nv_bfloat16* qkv_in, __nv_bflo
   }
   if (nchunk == 1) return;   // (CTA-uniform: warp 0 stored the result above)
   __syncthreads();
+  if (ct && threadIdx.x == 0) ct[3] = attn_gtime();   // (diagnostics: partials published)
   // ---- merge the warps' partials in fixed order: out = sum_w e^{m_w - m} O_w / sum_w e^{m_w - m} l_w
   for (uint32_t idx = threadIdx.x; idx < kAttnQRows * kAttnD / 2; idx += blockDim.x) {
     const uint32_t r = idx / (kAttnD / 2), c = 2 * (idx % (kAttnD / 2));
@@ -229,9 +287,10 @@ __device__ __forceinline__ void attn_tile(const __nv_bfloat16* qkv_in, __nv_bflo
   }
 }
 
-static inline size_t attn_smem_bytes(uint32_t T) {
+static inline size_t attn_smem_bytes(uint32_t T, bool bulk = false) {
   const size_t rows = (T + kAttnKChunk - 1) / kAttnKChunk * kAttnKChunk, warps = rows / kAttnKChunk;
-  return 2 * rows * kKVRowB + warps * kAttnQRows * kAttnD * 4 + warps * kAttnQRows * 2 * 4;
+  return 2 * rows * kKVRowB + warps * kAttnQRows * kAttnD * 4 + warps * kAttnQRows * 2 * 4 +
+         (bulk ? kAttnQRows * kKVRowB : 0);
 }
 
 }  // namespace cgx

@@ -177,22 +177,41 @@ void decoder_ln_launch_dims(uint32_t rows, uint32_t cols, dim3* grid, dim3* bloc
 
 // ---------------------------------------------------------------------------- causal attention
 // (tile body: cgx_attn.cuh)
+template <bool kBulk>
 __global__ void __launch_bounds__(kAttnMaxWarps * 32) k_attention(const __grid_constant__ AttnArgs a) {
   extern __shared__ __align__(16) uint8_t sm_attn[];
+  unsigned long long* ct = a.ctrace ? a.ctrace + 8 * (blockIdx.y * gridDim.x + blockIdx.x) : nullptr;
+  if (ct && threadIdx.x == 0) ct[0] = gtimer();
+  __shared__ __align__(8) uint64_t s_bar;   // the Q / K / V row copies (one phase per launch)
+  if (kBulk && threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"((uint32_t)__cvta_generic_to_shared(&s_bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
   if (threadIdx.x == 0) node_stamp(a.ntrace, 0);
   if (!(a.flags & kFlagTriggerAfterWait)) pdl_trigger();
   pdl_wait();
   if (a.flags & kFlagTriggerAfterWait) pdl_trigger();
   if (threadIdx.x == 0) node_stamp(a.ntrace, 1);
-  attn_tile(reinterpret_cast<const __nv_bfloat16*>(a.qkv), reinterpret_cast<__nv_bfloat16*>(a.out), a.T, a.H, a.scale,
-            blockIdx.x, blockIdx.y, sm_attn);
-  if (a.ntrace) {
+  if (ct && threadIdx.x == 0) ct[1] = gtimer();
+  attn_tile<kBulk>(reinterpret_cast<const __nv_bfloat16*>(a.qkv), reinterpret_cast<__nv_bfloat16*>(a.out), a.T, a.H,
+                  a.scale, blockIdx.x, blockIdx.y, sm_attn, ct, &s_bar);
+  if (a.ntrace || ct) {
     __syncthreads();
     if (threadIdx.x == 0) node_stamp(a.ntrace, 2);
+    if (ct && threadIdx.x == 0) ct[4] = gtimer();
   }
 }
 
-const void* kfn_attention() { return (const void*)k_attention; }
+// Staging of Q / K / V: the register path by default; CGX_ATTN_BULK=1 (measurement knob, read per
+// call) selects 128-B cp.async.bulk row copies on an mbarrier (attn_tile<true>), which measured
+// 3.5 us per 12-layer C3 replay SLOWER (342.8 vs 339.2 us, A/B in one process,
+// profiles/r02/ab_attn_bulk.txt) although it needs 61 instead of 117 registers
+static bool attn_bulk() {
+  const char* v = getenv("CGX_ATTN_BULK");
+  return v && v[0] == '1';
+}
+const void* kfn_attention() { return attn_bulk() ? (const void*)k_attention<true> : (const void*)k_attention<false>; }
 bool decoder_attn_supported(uint32_t T, uint32_t H, uint32_t D) {
   return D == kAttnD && T >= 1 && T <= kAttnMaxT && H >= 1 && H <= 64;
 }
@@ -210,9 +229,10 @@ void decoder_attn_launch_dims(uint32_t T, uint32_t H, uint32_t D, dim3* grid, di
   }();
   if (nw < min_w) nw = min_w;
   *block = dim3(32 * nw);
-  *smem = attn_smem_bytes(T);
+  *smem = attn_smem_bytes(T, attn_bulk());
   // per call (build time, cheap): function attributes belong to the current device's context
-  cudaFuncSetAttribute(k_attention, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)attn_smem_bytes(kAttnMaxT));
+  cudaFuncSetAttribute(k_attention<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)attn_smem_bytes(kAttnMaxT, true));
+  cudaFuncSetAttribute(k_attention<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)attn_smem_bytes(kAttnMaxT));
 }
 
 }  // namespace cgx

@@ -887,6 +887,13 @@ static int build_launch(cgx_exec* e, int k, Launch& l, int pre = -1) {
       a->D = n.attr.D;
       a->scale = n.attr.scalar;
       decoder_attn_launch_dims(n.attr.T, n.attr.H, n.attr.D, &l.grid, &l.block, &l.smem);
+      if (const char* cv = getenv("CGX_CTA_TRACE"); cv && cv[0] == '1') {   // diagnostics (cgx_debug_cta_trace)
+        void* ctb = nullptr;
+        CK(cudaMalloc(&ctb, sizeof(unsigned long long) * 8 * l.grid.x * l.grid.y));
+        CK(cudaMemset(ctb, 0, sizeof(unsigned long long) * 8 * l.grid.x * l.grid.y));
+        e->fuse_bufs.push_back(ctb);
+        a->ctrace = static_cast<unsigned long long*>(ctb);
+      }
       l.func = kfn_attention();
       return CGX_OK;
     }
@@ -2785,6 +2792,24 @@ extern "C" int cgx_debug_node_trace(cgx_exec* e, uint64_t* host_out, int cap, in
   node_trace_reset(e);
   *n_out = (int)e->L.size();
   return CGX_OK;
+}
+
+// Diagnostics (exec created with CGX_CTA_TRACE=1): per-CTA %globaltimer phase stamps [cta][8] of the
+// last replay of launch `pos` (an ATTN_CAUSAL launch: 0 entry, 1 past the PDL wait, 2 K/V staged,
+// 3 partials published (0 when one key chunk), 4 exit). Returns the CTA count or a negative status.
+extern "C" int cgx_debug_cta_trace(cgx_exec* e, int pos, uint64_t* host_out, int cap) {
+  if (!e || pos < 0 || pos >= (int)e->L.size()) return fail(CGX_E_INVALID_ARG, "cta_trace: bad argument");
+  Launch& l = e->L[pos];
+  if (l.kind != LK_KERNEL || l.mega || e->c->nodes[l.node].op != CGX_OP_ATTN_CAUSAL)
+    return fail(CGX_E_INVALID_ARG, "cta_trace: not an attention launch");
+  const AttnArgs* a = argp<AttnArgs>(l);
+  if (!a->ctrace) return fail(CGX_E_STATE, "cta_trace: exec not created with CGX_CTA_TRACE=1");
+  const int ctas = (int)(l.grid.x * l.grid.y);
+  if (host_out) {
+    CK(cudaStreamSynchronize(e->s));
+    CK(cudaMemcpy(host_out, a->ctrace, sizeof(uint64_t) * std::min(cap, 8 * ctas), cudaMemcpyDeviceToHost));
+  }
+  return ctas;
 }
 
 // Diagnostics (megakernel exec created with CGX_MEGA_TRACE=1): [stage][cta][8] %globaltimer ns of
