@@ -70,8 +70,10 @@ int decoder_ln_fold_prep(const void* W, const void* gamma, const void* beta, uin
 bool decoder_gemm_is_tcgen05(const void* func);
 // the small-M (GEMV) path serves this shape (M <= 4): a folded LN needs no producer row sums there
 bool decoder_gemm_is_gemv(uint32_t M, uint32_t N, uint32_t K);
-// Causal attention folded into its small-M (GEMV) consumer (exec option fuse & CGX_FUSE_ATTN_GEMM,
-// k_gemm.cu kGemmAttnA): A is formed from the ATTN node's qkv input inside the GEMV (T = M = 1,
-// D = 64, K = H * D), the ATTN output slot still stored. CGX_E_UNSUPPORTED otherwise.
-int decoder_gemm_set_attn_a(void* args, const void* qkv, void* attn_out, uint32_t H, uint32_t D, float scale);
+// Causal attention folded into its GEMM consumer (exec option fuse & CGX_FUSE_ATTN_GEMM, k_gemm.cu
+// kGemmAttnA, D = 64, K = H * D): the small-M path at T = M = 1 (A = the v row); the tcgen05 path at
+// T <= 128 re-plans the launch (grid, smem, kernel: K split S = H, each split computing its head's
+// attention into the A tile). The ATTN output slot is still stored. CGX_E_UNSUPPORTED otherwise.
+int decoder_gemm_set_attn_a(void* args, const void* qkv, void* attn_out, uint32_t H, uint32_t D, float scale,
+                            dim3* grid, size_t* smem, const void** func);
 }  // namespace cgx

@@ -31,6 +31,7 @@
 
 #include "../../include/cgx.h"
 #include "cgx_args.h"
+#include "cgx_attn.cuh"
 #include "cgx_decoder.h"
 #include "cgx_device.cuh"
 #include "cgx_umma.cuh"
@@ -132,6 +133,8 @@ struct alignas(64) GemmArgs {
   uint32_t ln_dbg;            // measurement knob (CGX_LN_DBG): 1 = serial stats loop, 2 = skip the LN output
   const __nv_bfloat16* attn_qkv;  // kGemmAttnA: the ATTN node's input [M][3 K] (q | k | v, head-major)
   __nv_bfloat16* attn_out;        // kGemmAttnA: the ATTN node's output slot [M][K]
+  uint32_t attn_H;                // kGemmAttnA, tcgen05 path: heads (qkv row = 3 H k-blocks of 64)
+  float attn_scale;               // kGemmAttnA, tcgen05 path: softmax scale
 };
 
 __device__ __forceinline__ void trace_at(const GemmArgs& a, int slot) {
@@ -190,11 +193,47 @@ __device__ __forceinline__ void ar_publish_wait(const GemmArgs& a, uint32_t cta,
   asm volatile("bar.sync 1, 128;\n" ::: "memory");
 }
 
-template <int BN, bool AR>
+
+// ---- attention folded into the O-proj GEMM's A operand (ATT instantiation, exec option fuse &
+// CGX_FUSE_ATTN_GEMM with T <= 128). K split S = H / HP: split z holds k-blocks
+// [HP z, HP z + HP) of A = heads HP z .. HP z + HP - 1, so the CTA computes those 64-column blocks
+// of A itself — causal attention of its heads over all M <= 128 query rows — on the tensor cores,
+// HP <= 2 heads per CTA, double-buffered: the producer TMA-loads every head's Q, K, V tiles up front
+// ([128][128 B] SW128, rows >= T zero-filled by the tensor map); the MMA warp issues S = Q K^T
+// (M 128, N 128, K 64) for every head as its tiles land (TMEM S region per head, so head 1's S
+// overlaps head 0's softmax); each epilogue thread owns one query row (its TMEM lane): causal mask,
+// max, p = 2^(s * scale * log2 e - max'), l = sum p, and writes bf16(p) into the P tile (K-major
+// SW128, two 64-key k-blocks over the head's dead Q / K tiles; key groups past the warp's causal
+// range are zeros without a TMEM read); the MMA warp issues O = P V (N 64, K 128, V read MN-major
+// straight from its TMA tile) into the O region; the thread scales its O row by 1 / l,
+// rounds to bf16 into the UMMA A tile (and, in N tile 0, into the ATTN node's output slot, so every
+// node output is materialised). The O-proj MMAs then run as in any split-K GEMM (columns [0, 32)).
+// Each N tile recomputes its heads' attention (N / BN times: tensor-core work, cheap) — instead of a
+// separate attention launch and the activation round trip through L2 between the two nodes.
+// TMEM columns: O-proj accumulator [0, 32), S of head 0 / 1 [32, 160) / [160, 288), O [288, 352)
+static constexpr uint32_t kAttTmemS = 32, kAttTmemO = 288, kAttTmemCols = 512;
+static constexpr uint32_t kAttQkvBytes = 3u * 128u * 128u;   // one head's Q | K | V tiles
+// UMMA smem descriptor, MN-major, 128-byte swizzle (V as the B operand of P V: rows = keys (K),
+// 64 contiguous head dims (N) per 128-B row, 8-key atoms of 1024 B): SBO = 1024 B between K atoms,
+// LBO = stride between 64-wide N blocks (one block here).
+__device__ __forceinline__ uint64_t umma_desc_sw128_mn(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFF) >> 4);
+  d |= (uint64_t)(8192 >> 4) << 16;
+  d |= (uint64_t)(1024 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+__device__ __forceinline__ uint32_t sw128_off(uint32_t r, uint32_t chunk) {   // byte offset of 16-B chunk of row r
+  return r * 128u + (((chunk ^ r) & 7u) << 4);
+}
+
+template <int BN, bool AR, bool ATT = false>
 __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_constant__ GemmArgs a) {
   constexpr uint32_t kABytes = kBM * kBK * 2;     // 16 KiB
   constexpr uint32_t kBBytes = BN * kBK * 2;
-  constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
+  constexpr uint32_t kTmemCols = ATT ? kAttTmemCols : BN < 32 ? 32 : BN;
   const uint32_t GA = a.ga, RA = a.ra, GW = a.gw, RW = a.rw;
   constexpr uint32_t kRowF = BN + 4;              // partial-tile row stride (floats): 16-B aligned, bank-spread
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -222,6 +261,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
   uint32_t* s_tm = reinterpret_cast<uint32_t*>((reinterpret_cast<uintptr_t>(s_tmem + 4) + 127) & ~uintptr_t(127));
   float2* s_mr = reinterpret_cast<float2*>(s_tm + 32);              // kGemmLnA: [128] (mean, rstd) per tile row
   float2* s_cc = s_mr + kBM;                                         // kGemmLnA: [BN] (c1, c2) of the tile's columns
+  uint64_t* qkv_full = reinterpret_cast<uint64_t*>(s_cc + BN);       // ATT: [2] head i's Q / K / V tiles landed
+  uint64_t* s_full = qkv_full + 2;                                   // ATT: [2] head i's S = Q K^T in TMEM
+  uint64_t* p_full = qkv_full + 4;                                   // ATT: a P tile written (4 warps)
+  uint64_t* o_full = qkv_full + 5;                                   // ATT: O = P V in TMEM
+  uint8_t* sQKV = smem + ((smem_u32(qkv_full + 6) - smem_u32(smem) + 1023u) & ~1023u);   // ATT: [2][3][128][128 B]
   // the folded LayerNorm is a runtime flag of the one kernel, not a separate instantiation: a
   // dedicated <BN, AR, LN> kernel (128 vs 164 registers) replayed the fused-LN C3 chain in 424 us
   // against 379 us for this generic one, every other node unchanged (profiles/r02/c3_fuse_ln_gemm.txt)
@@ -250,8 +294,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
     if (!dyn_a) prefetch_tmap(&a.tmA);
     prefetch_tmap(&a.tmB);
     for (uint32_t s = 0; s < RA; ++s) {
-      mbar_init(&full_a[s], 1);
+      mbar_init(&full_a[s], ATT ? 4u : 1u);   // ATT: the 4 attention warps write the A tile
       mbar_init(&empty_a[s], 1);
+    }
+    if (ATT) {
+      mbar_init(&qkv_full[0], 1);
+      mbar_init(&qkv_full[1], 1);
+      mbar_init(&s_full[0], 1);
+      mbar_init(&s_full[1], 1);
+      mbar_init(p_full, 4);
+      mbar_init(o_full, 1);
     }
     for (uint32_t s = 0; s < RW; ++s) {
       mbar_init(&full_w[s], 1);
@@ -311,9 +363,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
     if (lane == 0) node_stamp(a.ntrace, 1);
     if (dyn_late) build_a();                        // every lane has passed the wait
     if (late_trigger) pdl_trigger();
-    for (int g = 0; g < pre_a; ++g) {               // the whole A slice (one-shot) or the first RA groups
-      mbar_expect_tx_w(&full_a[g], GA * kABytes);
-      tma_load_3d_w(sA + g * GA * kABytes, tmA, &full_a[g], 0, m0, kbase + g * (int)GA);
+    if constexpr (ATT) {   // each head's Q, K, V tiles (tmA maps qkv [M][3 H * 64]; k-block = part * H + head)
+      for (int i = 0; i < kps; ++i) {   // (kps <= 2: one buffer per head)
+        mbar_expect_tx_w(&qkv_full[i], 3 * kABytes);
+#pragma unroll
+        for (int part = 0; part < 3; ++part)
+          tma_load_3d_w(sQKV + i * kAttQkvBytes + part * kABytes, tmA, &qkv_full[i], 0, m0,
+                        part * (int)a.attn_H + kbase + i);
+      }
+    } else {
+      for (int g = 0; g < pre_a; ++g) {             // the whole A slice (one-shot) or the first RA groups
+        mbar_expect_tx_w(&full_a[g], GA * kABytes);
+        tma_load_3d_w(sA + g * GA * kABytes, tmA, &full_a[g], 0, m0, kbase + g * (int)GA);
+      }
     }
     if (lane == 0) trace_at(a, 11);
     // refills in the order the MMAs consume k-blocks (deadlock-free: each waits for an earlier
@@ -348,6 +410,30 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
     // UMMA_K steps each, waiting for the A and W groups as they land; a group's slot is released
     // with a commit when it will be refilled)
     constexpr uint32_t idesc = umma_idesc(kBM, BN);
+    if constexpr (ATT) {
+      constexpr uint32_t idesc_s = umma_idesc(kBM, 128);                  // S = Q K^T: N = 128 keys
+      constexpr uint32_t idesc_o = umma_idesc(kBM, 64) | (1u << 16);      // O = P V: N = 64 dims, B MN-major
+      for (int i = 0; i < kps; ++i) {   // every head's S as soon as its tiles land
+        const uint32_t bQ = smem_u32(sQKV + i * kAttQkvBytes), bK = bQ + kABytes;
+        mbar_wait(&qkv_full[i], 0);
+        tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < kBK / 16; ++k)
+          umma_bf16_w(tmem + kAttTmemS + 128u * i, umma_desc_sw128(bQ) + 2 * k, umma_desc_sw128(bK) + 2 * k, idesc_s,
+                      k != 0);
+        umma_commit_w(&s_full[i]);
+      }
+      for (int i = 0; i < kps; ++i) {   // then O = P V per head, as the P tiles are written
+        const uint32_t bP = smem_u32(sQKV + i * kAttQkvBytes), bV = bP + 2 * kABytes;
+        mbar_wait(p_full, (uint32_t)i & 1u);
+        tc_fence_after();
+#pragma unroll
+        for (int j = 0; j < 8; ++j)   // 16 keys per step: P k-block j / 4 (+32 B per step), V atoms 2 j, 2 j + 1
+          umma_bf16_w(tmem + kAttTmemO, umma_desc_sw128(bP + (j >> 2) * kABytes) + 2 * (j & 3),
+                      umma_desc_sw128_mn(bV + 2048u * j), idesc_o, j != 0);
+        umma_commit_w(o_full);
+      }
+    }
     int sa = 0, sw = 0, oa = 0, ow = 0, ia = 0, iw = 0;
     uint32_t pha = 0u, phw = 0u;
     for (int kb = 0; kb < kps; ++kb) {
@@ -437,6 +523,88 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm_bf16(const __grid_cons
       }
     }
     asm volatile("bar.sync 1, 128;\n" ::: "memory");   // bias slice (and LN gamma / beta) staged
+    if constexpr (ATT) {   // A = this split's heads of the causal attention, computed here (row = thread)
+      const uint32_t T = a.M, r = row;                          // query row = TMEM lane
+      const uint32_t trow = tmem + ((q * 32u) << 16);
+      const uint32_t kvis = min(r + 1u, T);                     // keys [0, kvis) visible to this row
+      const float sl2 = a.attn_scale * 1.4426950408889634f;   // softmax in base 2: p = 2^(s sl2 - max s sl2)
+      const uint32_t bA = smem_u32(sA);
+      // key groups of 32 this warp's rows can see (warp-uniform: the TMEM loads are warp-collective)
+      const uint32_t ngrp = (min(32u * q + 32u, T) + 31u) / 32u;
+      for (int i = 0; i < kps; ++i) {
+        const uint32_t bP = smem_u32(sQKV + i * kAttQkvBytes), tS = trow + kAttTmemS + 128u * i;
+        mbar_wait(&s_full[i], 0);
+        tc_fence_after();
+        if (threadIdx.x == 64 && i == 0) trace_at(a, 12);     // (phase tracer: S ready)
+        float v[32];
+        float mx = -INFINITY;
+        for (uint32_t gi = 0; gi < ngrp; ++gi) {               // pass 1: row max over the visible keys
+          tmem_ld16_nw(tS + 32u * gi, v);
+          tmem_ld16_nw(tS + 32u * gi + 16u, v + 16);
+          tmem_wait_regs<32>(v);
+#pragma unroll
+          for (int c = 0; c < 32; ++c)
+            if (32u * gi + (uint32_t)c < kvis) mx = fmaxf(mx, v[c]);
+        }
+        const float mxl = mx * sl2;
+        float l = 0.f;
+        for (uint32_t gi = 0; gi < 4; ++gi) {                  // pass 2: p, l, bf16(p) -> P tile
+          if (gi < ngrp) {
+            tmem_ld16_nw(tS + 32u * gi, v);
+            tmem_ld16_nw(tS + 32u * gi + 16u, v + 16);
+            tmem_wait_regs<32>(v);
+          }
+#pragma unroll
+          for (int c8 = 0; c8 < 4; ++c8) {
+            uint32_t w4[4] = {0u, 0u, 0u, 0u};
+            if (gi < ngrp) {
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const uint32_t k0 = 32u * gi + 8u * c8 + 2u * e;
+                float p0 = 0.f, p1 = 0.f;
+                if (k0 < kvis) asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(p0) : "f"(fmaf(v[8 * c8 + 2 * e], sl2, -mxl)));
+                if (k0 + 1u < kvis) asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(p1) : "f"(fmaf(v[8 * c8 + 2 * e + 1], sl2, -mxl)));
+                l += p0 + p1;
+                w4[e] = pack_bf16(p0, p1);
+              }
+            }
+            const uint32_t key8 = 32u * gi + 8u * c8;          // 8 keys = one 16-B chunk of k-block key8 / 64
+            asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(bP + (key8 >> 6) * kABytes +
+                                                                         sw128_off(r, (key8 & 63u) >> 3)),
+                         "r"(w4[0]), "r"(w4[1]), "r"(w4[2]), "r"(w4[3]) : "memory");
+          }
+        }
+        fence_proxy_async_smem();   // generic-proxy stores -> visible to the tensor core
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(p_full);
+        mbar_wait(o_full, (uint32_t)i & 1u);
+        tc_fence_after();
+        float vo[64];
+#pragma unroll
+        for (int c0 = 0; c0 < 64; c0 += 16) tmem_ld16_nw(trow + kAttTmemO + (uint32_t)c0, vo + c0);
+        tmem_wait_regs<64>(vo);
+        const float inv = 1.0f / l;
+        const uint32_t hd = (uint32_t)(kbase + i);
+#pragma unroll
+        for (int c8 = 0; c8 < 8; ++c8) {
+          uint4 o;
+          o.x = pack_bf16(vo[8 * c8 + 0] * inv, vo[8 * c8 + 1] * inv);
+          o.y = pack_bf16(vo[8 * c8 + 2] * inv, vo[8 * c8 + 3] * inv);
+          o.z = pack_bf16(vo[8 * c8 + 4] * inv, vo[8 * c8 + 5] * inv);
+          o.w = pack_bf16(vo[8 * c8 + 6] * inv, vo[8 * c8 + 7] * inv);
+          asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(bA + (uint32_t)i * kABytes + sw128_off(r, c8)),
+                       "r"(o.x), "r"(o.y), "r"(o.z), "r"(o.w) : "memory");
+          if (blockIdx.x == 0 && r < T)   // N tile 0 materialises the ATTN node's output
+            *reinterpret_cast<uint4*>(a.attn_out + (size_t)r * a.K + hd * 64u + 8u * c8) = o;
+        }
+        tc_fence_before();
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full_a[0]);
+      if (lane == 0) trace_at(a, 13 + (warp == 2u ? 0 : 1));   // (13: warp 2's rows done; 14: the others')
+    }
     if (ln_a) {
       // ---- folded LayerNorm (kGemmLnA): this thread's tile row statistics from the producer's
       // per-tile row sums (fixed tile order) into shared memory, then — while the MMAs run — this
@@ -1213,7 +1381,9 @@ int decoder_gemm_set_stats_out(void* args, void* stats, dim3 grid) {
   if (g->flags & CGX_GEMM_ALLREDUCE) return CGX_E_UNSUPPORTED;
   const uint32_t S = grid.z, bn = g->N / grid.x, rows = split_rows_max_h(S);
   // every lane of an owner warp takes part in the row-sum shuffles: my_rows * BN / 4 % 32 == 0
-  if (g->split != S || (S != 1 && ((128u % S) != 0 || (rows * (bn / 4)) % 32 != 0))) return CGX_E_UNSUPPORTED;
+  // (every thread of the 4 epilogue warps runs the row-sum shuffles, with zeros past its owner rows:
+  // a row's bn / 4 quads sit in consecutive, aligned lanes whatever my_rows is)
+  if (g->split != S || (S != 1 && (rows * (bn / 4) > 128u * (bn / 8)))) return CGX_E_UNSUPPORTED;
   g->stats_out = static_cast<float2*>(stats);
   g->flags |= kGemmStatsOut;
   return CGX_OK;
@@ -1307,20 +1477,58 @@ int decoder_ln_fold_prep(const void* W, const void* gamma, const void* beta, uin
 
 bool decoder_gemm_is_gemv(uint32_t M, uint32_t N, uint32_t K) { return gemv_shape(M, N, K); }
 
-int decoder_gemm_set_attn_a(void* args, const void* qkv, void* attn_out, uint32_t H, uint32_t D, float scale) {
+template <int BN, bool AR, bool ATT = false>
+static const void* setup_kernel();
+
+int decoder_gemm_set_attn_a(void* args, const void* qkv, void* attn_out, uint32_t H, uint32_t D, float scale,
+                            dim3* grid, size_t* smem, const void** func) {
   GemmArgs* g = static_cast<GemmArgs*>(args);
-  if (!gemv_shape(g->M, g->N, g->K) || (g->flags & (CGX_GEMM_ALLREDUCE | kGemmLnA)) || g->ta >= 0) return CGX_E_UNSUPPORTED;
-  if (D != 64 || g->K != H * D || g->M != 1) return CGX_E_UNSUPPORTED;   // (k_gemv_bf16<KS, 1, 1> only)
+  if ((g->flags & (CGX_GEMM_ALLREDUCE | kGemmLnA)) || g->ta >= 0) return CGX_E_UNSUPPORTED;
+  if (D != 64 || H == 0 || g->K != H * D) return CGX_E_UNSUPPORTED;
   g->attn_qkv = static_cast<const __nv_bfloat16*>(qkv);
   g->attn_out = static_cast<__nv_bfloat16*>(attn_out);
-  (void)scale;   // one visible key: the softmax weight is 1 whatever the scaled score
+  g->attn_scale = scale;   // (the GEMV path ignores it: one visible key, weight 1)
+  g->attn_H = H;
+  if (gemv_shape(g->M, g->N, g->K)) {
+    if (g->M != 1) return CGX_E_UNSUPPORTED;   // (k_gemv_bf16<KS, 1, 1> only)
+    g->flags |= kGemmAttnA;
+    return CGX_OK;
+  }
+  // tcgen05 (ATT instantiation): one M tile (T <= 128), K split S = the largest divisor of H that is
+  // <= 8 (HP = H / S heads = k-blocks per split, cluster (1, 1, S) portable: a cluster of 12 left
+  // part of a 288-CTA grid in a second wave), BN = 32, A / W rings of one HP-k-block group
+  // Measured slower than the two separate launches (C3: 339 -> 420 us with one CTA pair of heads per
+  // split at 2 CTAs / SM, 486 us double-buffered at 1 CTA / SM: the 4 epilogue warps' softmax of a
+  // 128 x 128 score tile per head is latency-bound at ~2.4-3.5 us a head, and every N tile repeats
+  // it; profiles/r02/ab_attn_gemm.txt, gemm_att_trace.txt): built and tested, but only
+  // with the measurement knob CGX_ATTN_GEMM_TC=1.
+  const char* tc = getenv("CGX_ATTN_GEMM_TC");
+  if (!(tc && tc[0] == '1')) return CGX_E_UNSUPPORTED;
+  if (g->M > (uint32_t)kBM || g->N % 32) return CGX_E_UNSUPPORTED;
+  uint32_t S = 1;
+  for (uint32_t c = 1; c <= 8 && c <= H; ++c)
+    if (H % c == 0) S = c;
+  const uint32_t HP = H / S;
+  if (HP > 2) return CGX_E_UNSUPPORTED;   // (one Q / K / V buffer and one TMEM S region per head)
+  if (get_encode() != CGX_OK) return CGX_E_CUDA;
+  const GemmPipes pp{HP, 1, HP, 1};
+  const size_t sm = smem_bytes(32, S, pp) + (size_t)kBM * 8 + 32 * 8 + 6 * 8 + 1024 + (size_t)HP * kAttQkvBytes;
+  if (sm > kSmemLimit) return CGX_E_UNSUPPORTED;
+  if (encode_kmajor(&g->tmA, qkv, g->M, 3ull * g->K, kBM, 1) != CGX_OK) return CGX_E_CUDA;   // Q | K | V k-blocks
+  if (encode_kmajor(&g->tmB, g->w_ptr, g->N, g->K, 32, HP) != CGX_OK) return CGX_E_CUDA;
+  g->split = S;
+  g->ga = g->gw = HP;
+  g->ra = g->rw = 1;
   g->flags |= kGemmAttnA;
+  *grid = dim3(g->N / 32, 1, S);
+  *smem = sm;
+  *func = setup_kernel<32, false, true>();
   return CGX_OK;
 }
 
 bool decoder_gemm_is_tcgen05(const void* func) {
   return func == (const void*)k_gemm_bf16<32, false> || func == (const void*)k_gemm_bf16<64, false> ||
-         func == (const void*)k_gemm_bf16<128, false>;
+         func == (const void*)k_gemm_bf16<128, false> || func == (const void*)k_gemm_bf16<32, false, true>;
 }
 
 void decoder_gemm_plan(uint32_t, uint32_t, uint32_t, size_t* ws_bytes, size_t* cnt_bytes) {
@@ -1329,7 +1537,7 @@ void decoder_gemm_plan(uint32_t, uint32_t, uint32_t, size_t* ws_bytes, size_t* c
   *cnt_bytes = 0;
 }
 
-template <int BN, bool AR>
+template <int BN, bool AR, bool ATT>
 static const void* setup_kernel() {
   // per call (exec build time, cheap): function attributes belong to the current device's context.
   // Headroom below the 227 KiB per-block limit for the kernel's static shared memory.
@@ -1337,9 +1545,9 @@ static const void* setup_kernel() {
     const char* v = getenv("CGX_GEMM_SMEM_ATTR");
     return v ? atoi(v) : (int)kSmemLimit;
   }();
-  cudaFuncSetAttribute(k_gemm_bf16<BN, AR>, cudaFuncAttributeMaxDynamicSharedMemorySize, attr);
-  cudaFuncSetAttribute(k_gemm_bf16<BN, AR>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  return (const void*)k_gemm_bf16<BN, AR>;
+  cudaFuncSetAttribute(k_gemm_bf16<BN, AR, ATT>, cudaFuncAttributeMaxDynamicSharedMemorySize, attr);
+  cudaFuncSetAttribute(k_gemm_bf16<BN, AR, ATT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  return (const void*)k_gemm_bf16<BN, AR, ATT>;
 }
 
 // the fused all-reduce epilogue is a separate instantiation: the plain kernel keeps its code

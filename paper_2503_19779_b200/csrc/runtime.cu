@@ -1740,7 +1740,9 @@ static bool fusable_ln_gemm(const cgx_exec* e, int k) {
         if (c->nodes[q].in[i] == ln.out) return false;
   if (gemv) return true;   // (the GEMV's K slices hold whole A rows: its own statistics)
   const Launch& prev = e->L[e->L.size() - 2];   // (the slot for node k is already emplaced)
-  if (prev.kind != LK_KERNEL || prev.mega || prev.pre_node >= 0) return false;
+  // (a producer with a fused ATTN in front — the attention-fed O-proj — still writes its row sums)
+  if (prev.kind != LK_KERNEL || prev.mega ||
+      (prev.pre_node >= 0 && c->nodes[prev.pre_node].op != CGX_OP_ATTN_CAUSAL)) return false;
   const Node& p = c->nodes[prev.node];
   return p.op == CGX_OP_GEMM_BF16 && p.out == ln.in[0] && p.attr.M == ln.attr.rows && p.attr.N == ln.attr.cols &&
          !(p.attr.flags & CGX_GEMM_ALLREDUCE) && decoder_gemm_is_tcgen05(prev.func);
@@ -1789,8 +1791,9 @@ static int build_ln_gemm(cgx_exec* e, int k, bool* fused) {
   return build_launch(e, k, l);   // not fusable after all: the LN keeps its own launch
 }
 
-// CGX_FUSE_ATTN_GEMM: node k is an ATTN_CAUSAL over T = 1 query (decode) whose output the next node, a
-// small-M GEMM (GEMV path), reads as A with K = H * D; not the first two nodes of the range (the
+// CGX_FUSE_ATTN_GEMM: node k is an ATTN_CAUSAL whose output the next node, a GEMM, reads as A with
+// K = H * D: on the small-M (GEMV) path at T = 1 (decode), on the tcgen05 path at T <= 128 (the GEMM
+// computes each head's attention in its K split); not the first two nodes of the range (the
 // FIRST_NODE transport's by-value prefix keeps one launch per node there). Other readers of the
 // attention output are fine: the fused launch still stores it.
 static bool fusable_attn_gemm(const cgx_exec* e, int k) {
@@ -1801,8 +1804,8 @@ static bool fusable_attn_gemm(const cgx_exec* e, int k) {
   if (at.op != CGX_OP_ATTN_CAUSAL || g.op != CGX_OP_GEMM_BF16 || g.in[0] != at.out) return false;
   if (g.attr.flags & CGX_GEMM_ALLREDUCE) return false;
   if (c->slots[at.in[0]].kind == CGX_SLOT_EXTERNAL) return false;
-  return at.attr.D == 64 && at.attr.T == 1 && g.attr.M == at.attr.T && g.attr.K == at.attr.H * at.attr.D &&
-         decoder_gemm_is_gemv(g.attr.M, g.attr.N, g.attr.K);
+  if (at.attr.D != 64 || g.attr.M != at.attr.T || g.attr.K != at.attr.H * at.attr.D) return false;
+  return decoder_gemm_is_gemv(g.attr.M, g.attr.N, g.attr.K) ? at.attr.T == 1 : at.attr.T <= 128;
 }
 
 // Build the ATTN (k) -> GEMV (k + 1) pair as ONE launch of the GEMV forming its A operand from the
@@ -1817,7 +1820,9 @@ static int build_attn_gemm(cgx_exec* e, int k, bool* fused) {
   CKS(build_launch(e, k + 1, g, k));
   const Slot& qs = c->slots[at.in[0]];
   const void* qkv = qs.kind == CGX_SLOT_STATIC ? qs.static_ptr : qs.buf;
-  if (decoder_gemm_set_attn_a(g.args.p, qkv, c->slots[at.out].buf, at.attr.H, at.attr.D, at.attr.scalar) == CGX_OK) {
+  if (decoder_gemm_set_attn_a(g.args.p, qkv, c->slots[at.out].buf, at.attr.H, at.attr.D, at.attr.scalar, &g.grid,
+                              &g.smem, &g.func) == CGX_OK) {
+    g.cluster_z = g.grid.z;
     g.pre_node = k;
     l = std::move(g);
     *fused = true;

@@ -8,6 +8,8 @@ import os
 import sys
 
 os.environ["CGX_NODE_TRACE"] = "1"
+if "--attn-gemm" in sys.argv:
+    os.environ["CGX_ATTN_GEMM_TC"] = "1"   # (the tcgen05 attention fold is a measurement knob)
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 

@@ -3,11 +3,15 @@
 Default: %globaltimer stamps relative to the first CTA entry (256 ns tick). --clk: SM clock64
 stamps (CGX_GEMM_TRACE_CLK=1), reported per CTA relative to its own entry in µs at the SM clock
 (cycle-exact, only comparable within a CTA). --fused: the fused-residual chain with the LayerNorms
-folded into their GEMMs (fuse = CGX_FUSE_LN_GEMM). Usage: diag_gemm.py [--clk] [--fused]"""
+folded into their GEMMs (fuse = CGX_FUSE_LN_GEMM); --attn: and the attention folded into the O-proj
+(fuse |= CGX_FUSE_ATTN_GEMM; slots 12 / 13 / 14 = Q-K-V landed / warp 2 / other warps done).
+Usage: diag_gemm.py [--clk] [--fused] [--attn]"""
 import os
 import sys
 
 CLK = "--clk" in sys.argv
+if "--attn" in sys.argv:
+    os.environ["CGX_ATTN_GEMM_TC"] = "1"
 if CLK:
     os.environ["CGX_GEMM_TRACE_CLK"] = "1"
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -25,7 +29,7 @@ SM_GHZ = 1.965
 dev = torch.device("cuda:0")
 spec = wl.c3_chain(T=128, n_layers=2 if fused else 1, fuse_residual=fused)
 chain = runner.Chain(spec, runner.upload_statics(spec, wl.static_values(spec), dev))
-ex = chain.exec("COPY", fuse=cgx.FUSE_LN_GEMM if fused else 0)
+ex = chain.exec("COPY", fuse=(cgx.FUSE_LN_GEMM if fused else 0) | (cgx.FUSE_ATTN_GEMM if "--attn" in sys.argv else 0))
 x = runner.host_to_device(wl.slot_values(spec, "x", 0), "bf16", dev)
 ex.bind({"x": x})
 ex.launch()

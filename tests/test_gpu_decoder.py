@@ -524,12 +524,60 @@ def test_c3_decode_fused_attn_gemv(rt, n_layers):
                     assert np.array_equal(outs[r][k], ref[r][k]), (mode, xp, k)
 
 
-def test_fused_attn_gemv_not_applied_beyond_t1(rt):
-    """The attention fold is a T = 1 (decode) fusion: at T = 4 (GEMV path, several keys) and
-    T = 128 (tcgen05 path) the exec keeps one launch per ATTN node."""
+@pytest.mark.parametrize("n_layers,T", [(1, 128), (1, 77), (1, 16), (1, 33), (12, 128)])
+def test_c3_fused_attn_gemm(rt, monkeypatch, n_layers, T):
+    """Attention folded into the O-proj tcgen05 GEMM (fuse = CGX_FUSE_ATTN_GEMM with the measurement
+    knob CGX_ATTN_GEMM_TC=1, T <= 128: K split S = 6, each split computing its 2 heads' causal
+    attention on the tensor cores — S = Q K^T into TMEM, per-row softmax, O = P V with V MN-major —
+    into the UMMA A tile, N tile 0 storing the ATTN output slot), alone and with the LN fold (whose
+    producer-row-sum handover must survive: the fused O-proj writes them for the FC1 fold).
+    Node-local parity of EVERY node (the materialised attention output included) against the
+    oracle, end to end within the bf16 bar, and bit-identical across the six rebinding arms."""
+    monkeypatch.setenv("CGX_ATTN_GEMM_TC", "1")
+    cgx, runner = rt
+    spec = wl.c3_chain(T=T, n_layers=n_layers, fuse_residual=True)
+    st = wl.static_values(spec)
+    dev = torch.device("cuda:0")
+    attns = sum(1 for k, n in enumerate(spec.nodes) if n.op == "ATTN_CAUSAL" and k > 1)
+    arms = [("INDIRECT", "ROOT_PARAMS"), ("INDIRECT", "FIRST_NODE"), ("INDIRECT", "PRELUDE"),
+            ("COPY", "DEFAULT"), ("SETPARAMS", "DEFAULT"), ("EAGER", "DEFAULT")]
+    for fz in (cgx.FUSE_ATTN_GEMM, cgx.FUSE_ATTN_GEMM | cgx.FUSE_LN_GEMM):
+        ref = None
+        for mode, xp in arms:
+            chain = runner.Chain(spec, runner.upload_statics(spec, st, dev))
+            ex = chain.exec(mode, transport=xp, fuse=fz)
+            ex_b = chain.exec(mode, transport=xp, fuse=fz & ~cgx.FUSE_ATTN_GEMM)
+            assert ex_b.stats()["kernels_per_replay"] - ex.stats()["kernels_per_replay"] == attns
+            outs = []
+            for r in range(2):
+                t = runner.upload_externals(spec, wl.external_values(spec, r), dev)
+                ex.bind(t)
+                ex.launch()
+                outs.append({s_.name: ex.output(s_.name) for s_ in spec.internals()})
+            chain.close()
+            if ref is None:
+                ref = outs
+                for r, got in enumerate(outs):
+                    ext = wl.external_values(spec, r)
+                    _node_local_check(spec, st, ext, got)
+                    env = eval_chain(spec, ext, st)
+                    last = spec.nodes[-1].out
+                    g, o = bits_to_f64(got[last]), env[last]
+                    assert np.linalg.norm(g - o) / np.linalg.norm(o) <= 2e-2
+            else:
+                for r in range(2):
+                    for k in ref[r]:
+                        assert np.array_equal(outs[r][k], ref[r][k]), (fz, mode, xp, k)
+
+
+def test_fused_attn_gemm_not_applied(rt, monkeypatch):
+    """Where the attention fold does not apply the exec keeps one launch per ATTN node: T = 4 (GEMV
+    path with several keys), T = 200 (two M tiles of queries), and T = 128 without the tcgen05
+    measurement knob (the default: that fold measured slower than the two launches)."""
     cgx, runner = rt
     dev = torch.device("cuda:0")
-    for T in (4, 128):
+    monkeypatch.delenv("CGX_ATTN_GEMM_TC", raising=False)
+    for T in (4, 200, 128):
         spec = wl.c3_chain(T=T, n_layers=1, fuse_residual=True)
         chain = runner.Chain(spec, runner.upload_statics(spec, wl.static_values(spec), dev))
         a = chain.exec("INDIRECT", fuse=cgx.FUSE_ATTN_GEMM).stats()["kernels_per_replay"]
