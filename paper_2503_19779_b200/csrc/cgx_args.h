@@ -136,6 +136,9 @@ struct LnArgs {
   int32_t tb, pad2;             // table index of an EXTERNAL add_b (-1: direct pointer)
 };
 
+// AttnArgs::flags: every warp loads the Q fragments (measurement knob CGX_ATTN_QALL=1, the round-1
+// behaviour; by default only the warps owning a key chunk do)
+static constexpr uint32_t kAttnQAll = 1u << 8;
 struct AttnArgs {
   const void* qkv; void* out;
   uint32_t T, H, D, flags;

@@ -62,7 +62,8 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 template <bool kBulk = false>
 __device__ __forceinline__ void attn_tile(const __nv_bfloat16* qkv_in, __nv_bfloat16* out, uint32_t T, uint32_t H,
                                           float scale, uint32_t qblock, uint32_t h, uint8_t* smem,
-                                          unsigned long long* ct = nullptr, uint64_t* bar = nullptr) {
+                                          unsigned long long* ct = nullptr, uint64_t* bar = nullptr,
+                                          bool qall = false) {
   const uint32_t q0 = qblock * kAttnQRows;
   const uint32_t kend = min(T, q0 + kAttnQRows);                 // keys [0, kend) are visible to the block
   const uint32_t nchunk = (kend + kAttnKChunk - 1) / kAttnKChunk;
@@ -119,7 +120,9 @@ __device__ __forceinline__ void attn_tile(const __nv_bfloat16* qkv_in, __nv_bflo
                    : "=r"(qa[kk][0]), "=r"(qa[kk][1]), "=r"(qa[kk][2]), "=r"(qa[kk][3]) : "r"(addr));
     }
   } else {
-  {
+  // Q fragments: only the warps that own a key chunk (the others only help stage K / V) — every
+  // warp loading them made the 4-B Q loads ~4x the request count of the K / V vectors
+  if (warp < nchunk || qall) {
     const uint32_t r0 = q0 + g, r1 = q0 + g + 8;
 #pragma unroll
     for (int kk = 0; kk < 4; ++kk) {

@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(kAttnMaxWarps * 32) k_attention(const __grid_c
   if (threadIdx.x == 0) node_stamp(a.ntrace, 1);
   if (ct && threadIdx.x == 0) ct[1] = gtimer();
   attn_tile<kBulk>(reinterpret_cast<const __nv_bfloat16*>(a.qkv), reinterpret_cast<__nv_bfloat16*>(a.out), a.T, a.H,
-                  a.scale, blockIdx.x, blockIdx.y, sm_attn, ct, &s_bar);
+                  a.scale, blockIdx.x, blockIdx.y, sm_attn, ct, &s_bar, a.flags & kAttnQAll);
   if (a.ntrace || ct) {
     __syncthreads();
     if (threadIdx.x == 0) node_stamp(a.ntrace, 2);

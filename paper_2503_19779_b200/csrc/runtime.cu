@@ -886,6 +886,7 @@ static int build_launch(cgx_exec* e, int k, Launch& l, int pre = -1) {
       a->H = n.attr.H;
       a->D = n.attr.D;
       a->scale = n.attr.scalar;
+      if (const char* qv = getenv("CGX_ATTN_QALL"); qv && qv[0] == '1') a->flags |= kAttnQAll;   // measurement knob
       decoder_attn_launch_dims(n.attr.T, n.attr.H, n.attr.D, &l.grid, &l.block, &l.smem);
       if (const char* cv = getenv("CGX_CTA_TRACE"); cv && cv[0] == '1') {   // diagnostics (cgx_debug_cta_trace)
         void* ctb = nullptr;
