@@ -269,24 +269,37 @@ __device__ __forceinline__ void attn_tile(const __nv_bfloat16* qkv_in, __nv_bflo
   __syncthreads();
   if (ct && threadIdx.x == 0) ct[3] = attn_gtime();   // (diagnostics: partials published)
   // ---- merge the warps' partials in fixed order: out = sum_w e^{m_w - m} O_w / sum_w e^{m_w - m} l_w
-  for (uint32_t idx = threadIdx.x; idx < kAttnQRows * kAttnD / 2; idx += blockDim.x) {
-    const uint32_t r = idx / (kAttnD / 2), c = 2 * (idx % (kAttnD / 2));
+  // (4 columns per item: one float4 of each warp's partial, 256 items = one per thread at 8 warps;
+  // per element the same operations in the same order as one column at a time)
+  for (uint32_t idx = threadIdx.x; idx < kAttnQRows * kAttnD / 4; idx += blockDim.x) {
+    const uint32_t r = idx / (kAttnD / 4), c = 4 * (idx % (kAttnD / 4));
     const uint32_t qi = q0 + r;
     if (qi >= T) continue;
+    float2 ml[kAttnMaxWarps];
     float m = -INFINITY;
-    for (uint32_t w = 0; w < nchunk; ++w) m = fmaxf(m, sML[(w * kAttnQRows + r) * 2]);
-    float l = 0.f, ox = 0.f, oy = 0.f;
-    for (uint32_t w = 0; w < nchunk; ++w) {
-      const float mw = sML[(w * kAttnQRows + r) * 2];
+#pragma unroll
+    for (uint32_t w = 0; w < (uint32_t)kAttnMaxWarps; ++w)
+      if (w < nchunk) {
+        ml[w] = *reinterpret_cast<const float2*>(sML + (w * kAttnQRows + r) * 2);
+        m = fmaxf(m, ml[w].x);
+      }
+    float l = 0.f;
+    float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (uint32_t w = 0; w < (uint32_t)kAttnMaxWarps; ++w) {
+      if (w >= nchunk) break;
+      const float mw = ml[w].x;
       const float f = mw == -INFINITY ? 0.f : __expf(mw - m);
-      l += f * sML[(w * kAttnQRows + r) * 2 + 1];
-      const float2 ov = *reinterpret_cast<const float2*>(sO + (w * kAttnQRows + r) * kAttnD + c);
-      ox += f * ov.x;
-      oy += f * ov.y;
+      l += f * ml[w].y;
+      const float4 ov = *reinterpret_cast<const float4*>(sO + (w * kAttnQRows + r) * kAttnD + c);
+      o.x += f * ov.x;
+      o.y += f * ov.y;
+      o.z += f * ov.z;
+      o.w += f * ov.w;
     }
     const float inv = 1.0f / l;
-    *reinterpret_cast<uint32_t*>(out + (size_t)qi * (H * kAttnD) + h * kAttnD + c) =
-        pack_bf16(ox * inv, oy * inv);
+    *reinterpret_cast<uint2*>(out + (size_t)qi * (H * kAttnD) + h * kAttnD + c) =
+        make_uint2(pack_bf16(o.x * inv, o.y * inv), pack_bf16(o.z * inv, o.w * inv));
   }
 }
 
