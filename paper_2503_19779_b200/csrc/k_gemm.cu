@@ -1364,8 +1364,11 @@ static void pick_tiling(uint32_t M, uint32_t N, uint32_t K, int* bn_out, uint32_
   if (env_sp && atoi(env_sp) >= 1 && (uint32_t)atoi(env_sp) <= nk && atoi(env_sp) <= 16) {
     sp = (uint32_t)atoi(env_sp);
   } else {
-    for (uint32_t c = 2; c <= 8; c *= 2)
-      if (tiles * c <= 192 && nk >= 3 * c) sp = c;
+    // the largest S in {2, 3, 4, 8} with <= 192 CTAs and >= 4 k-blocks per split (O-proj 768 x 768:
+    // S = 3 instead of 4, C3 327 -> 321.5 us; the other decoder shapes unchanged, every 32 / S
+    // alternative slower: profiles/r02/sweep_c3_split*.txt)
+    for (uint32_t c : {2u, 3u, 4u, 8u})
+      if (tiles * c <= 192 && nk >= 4 * c) sp = c;
   }
   *bn_out = bn;
   *split_out = sp;

@@ -90,9 +90,18 @@ def test_allreduce_integer_exact(rt, world, n):
 
 @pytest.mark.parametrize("tp", [2, 4])
 @pytest.mark.parametrize("mode,transport", [("INDIRECT", "FIRST_NODE"), ("COPY", "DEFAULT"), ("EAGER", "DEFAULT")])
-def test_tp_decoder_peer_allreduce(rt, tp, mode, transport):
+def test_tp_decoder_peer_allreduce(rt, monkeypatch, tp, mode, transport):
     """C5 (TP decoder, 2 layers, T=128) with the peer all-reduce: every rank's output identical, and
     equal to the lockstep TP oracle within the decoder tolerance."""
+    # The virtual ranks share ONE GPU: a rank's all-reduce spins until every rank's partial has
+    # arrived, so every rank's GEMMs must still find room beside the spinning CTAs. Split-K GEMMs
+    # launch as thread-block clusters, which need several free SMs of one GPC at once; with the
+    # S = 3 shard tilings EAGER at TP = 4 could not place a rank's cluster and tripped the bounded
+    # spin on every run. Unsplit BN = 32 tilings (no clusters) keep the emulation schedulable; on
+    # an NVSwitch box each rank has its own GPU (test_multigpu_tp_chain runs the default tilings).
+    hl, fl = 12 // tp, 3072 // tp
+    shapes = {(3 * hl * 64, 768), (768, hl * 64), (fl, 768), (768, fl)}
+    monkeypatch.setenv("CGX_GEMM_TILING", ",".join(f"{n}x{k}=32/1" for n, k in shapes))
     full = wl.c3_chain(T=128, n_layers=2)
     specs = [wl.c3_chain(T=128, n_layers=2, tp=tp, rank=r) for r in range(tp)]
     statics = [wl.static_values(specs[r], tp=tp, rank=r, full=full) for r in range(tp)]
