@@ -8,6 +8,8 @@
                                            # LayerNorms folded into their consumer GEMMs
   python scripts/ncu_targets.py replay_nopdl  # one C2 INDIRECT replay captured without PDL (the
                                               # roofline's sub-graph configuration)
+  python scripts/ncu_targets.py decode     # one T = 1 decode replay (2 layers, fused residual, LN and
+                                           # attention folded into their GEMV consumers)
 """
 import os
 import sys
@@ -48,6 +50,9 @@ def main():
     elif what == "gemm_fold":
         spec = wl.c3_chain(T=128, n_layers=2, fuse_residual=True)
         mode, xp = "INDIRECT", "FIRST_NODE"
+    elif what == "decode":
+        spec = wl.c3_chain(T=1, n_layers=2, fuse_residual=True)
+        mode, xp = "INDIRECT", "FIRST_NODE"
     elif what == "mega":
         spec = wl.c3_chain(T=128, n_layers=12)
         mode, xp = "INDIRECT", "ROOT_PARAMS"
@@ -56,7 +61,8 @@ def main():
         mode, xp = "INDIRECT", "FIRST_NODE"
     chain = runner.Chain(spec, runner.upload_statics(spec, wl.static_values(spec), dev))
     ex = chain.exec(mode, transport=xp, no_pdl=(what == "replay_nopdl"), megakernel=(what == "mega"),
-                    fuse=cgx.FUSE_LN_GEMM if what == "gemm_fold" else 0)
+                    fuse=cgx.FUSE_LN_GEMM if what == "gemm_fold" else
+                    cgx.FUSE_LN_GEMM | cgx.FUSE_ATTN_GEMM if what == "decode" else 0)
     ts = fill(spec, dev, sh)
     torch.cuda.synchronize()
     ex.bind_ptrs([t.data_ptr() for t in ts])
