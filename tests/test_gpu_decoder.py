@@ -660,3 +660,47 @@ def test_tp_shard_shapes_single_rank(rt, tp):
                 assert np.array_equal(res["INDIRECT"][r][k], res["EAGER"][r][k]), k
     finally:
         c.nccl_comm_destroy(comm)
+
+
+@pytest.mark.parametrize("tp", [2, 4, 8])
+def test_tp_shard_decode_folds_single_rank(rt, tp):
+    """Rank 0's TP shard of the T = 1 decode (H = 6 / 3 / 2 heads per rank, K = 384 / 192 / 128 for
+    the O-proj GEMV: K slices with partial lanes) with the LayerNorm and attention folds
+    (fuse = CGX_FUSE_LN_GEMM | CGX_FUSE_ATTN_GEMM), a one-rank NCCL communicator: fewer launches,
+    node-local parity of every node against the oracle (the folded ATTN / LN outputs included),
+    the materialised attention output bit-identical to the LN-folded-only exec's, INDIRECT and
+    EAGER bit-identical."""
+    cgx, runner = rt
+    from paper_2503_19779_b200 import cgx as c
+    full = wl.c3_chain(T=1, n_layers=2)
+    spec = wl.c3_chain(T=1, n_layers=2, tp=tp, rank=0)
+    st = wl.static_values(spec, tp=tp, rank=0, full=full)
+    dev = torch.device("cuda:0")
+    attns = [n.out for k, n in enumerate(spec.nodes) if n.op == "ATTN_CAUSAL" and k > 1]
+    comm = c.nccl_comm_init(1, 0, c.nccl_unique_id(), 0)
+    try:
+        res = {}
+        for mode in ("INDIRECT", "EAGER"):
+            chain = runner.Chain(spec, runner.upload_statics(spec, st, dev), nccl_comm=comm)
+            ex = chain.exec(mode, fuse=cgx.FUSE_LN_GEMM | cgx.FUSE_ATTN_GEMM)
+            ex_u = chain.exec(mode, fuse=cgx.FUSE_LN_GEMM)   # (same qkv inputs: the LN fold in both)
+            assert ex_u.stats()["kernels_per_replay"] - ex.stats()["kernels_per_replay"] == len(attns)
+            outs = []
+            for r in range(2):
+                t = runner.upload_externals(spec, wl.external_values(spec, r), dev)
+                got = {}
+                for e_ in (ex, ex_u):
+                    e_.bind(t)
+                    e_.launch()
+                    got[e_ is ex] = {s_.name: e_.output(s_.name) for s_ in spec.internals()}
+                for a in attns:   # (one visible key: the fold's A row is the v row, bit for bit)
+                    assert np.array_equal(got[True][a], got[False][a]), a
+                outs.append(got[True])
+            res[mode] = outs
+            chain.close()
+        for r in range(2):
+            _node_local_check(spec, st, wl.external_values(spec, r), res["INDIRECT"][r], one_rank=True)
+            for k in res["INDIRECT"][r]:
+                assert np.array_equal(res["INDIRECT"][r][k], res["EAGER"][r][k]), k
+    finally:
+        c.nccl_comm_destroy(comm)
