@@ -444,6 +444,29 @@ int cgx_device_free(void* dptr);
 int cgx_ipc_handle(void* dptr, void* handle_out /* 64 bytes */);
 int cgx_ipc_open(const void* handle /* 64 bytes */, void** dptr_out);
 int cgx_ipc_close(void* dptr);
+/* NVLS (NVSwitch multicast) all-reduce — SURVEY §8(f) NEXT-4, the in-network reduction that
+ * replaces the per-rank pushes of the peer path ("additional kernel launches for inter-GPU
+ * collective operations"). Every rank binds one region of cgx_mc_buffer_bytes() (rounded to
+ * the size cgx_mc_create returns) to a common multicast object and maps it twice: its own copy (uc)
+ * and the multicast address (mc). ALLREDUCE_SUM nodes then run k_allreduce_mc: each rank stores its
+ * partial into its own copy, the ranks arrive through one multimem.red on a per-CTA counter, and
+ * one multimem.ld_reduce (fp32 accumulation in the switch, one bf16 rounding) returns the sum to
+ * every rank. Setup order (multi-process): rank 0 cgx_mc_create(world, bytes, device) and
+ * cgx_mc_export_fd; the others cgx_mc_import_fd (the file descriptor passed over a Unix socket);
+ * EVERY rank cgx_mc_add_device; a barrier; every rank cgx_mc_bind_map; cgx_chain_set_multicast
+ * before capture. cgx_mc_supported reports CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED; without it (or
+ * without the driver entry points) the calls return CGX_E_UNSUPPORTED. A lost rank is reported as
+ * CGX_E_DEVICE by the next cgx_launch, as for the peer path. cgx_mc_release(uc) unmaps and frees one
+ * rank's region (after every exec using it is destroyed). */
+int cgx_mc_supported(int device, int* supported);
+int cgx_mc_buffer_bytes(uint64_t max_elems, int max_allreduces, uint64_t* bytes);
+int cgx_mc_create(int world, uint64_t bytes, int device, uint64_t* handle_out, uint64_t* size_out);
+int cgx_mc_export_fd(uint64_t handle, int* fd_out);
+int cgx_mc_import_fd(int fd, uint64_t* handle_out);
+int cgx_mc_add_device(uint64_t handle, int device);
+int cgx_mc_bind_map(uint64_t handle, int device, uint64_t size, void** uc_out, void** mc_out);
+int cgx_mc_release(void* uc);
+int cgx_chain_set_multicast(cgx_chain* c, int world, void* uc, void* mc, uint64_t max_elems, int max_allreduces);
 int cgx_nccl_unique_id(void* id_out /* 128 bytes */);
 int cgx_nccl_comm_init(int nranks, int rank, const void* id /* 128 bytes */, int device, void** comm_out);
 int cgx_nccl_comm_destroy(void* comm);

@@ -154,6 +154,15 @@ def _load():
         "cgx_ipc_handle": ([VP, VP], I),
         "cgx_ipc_open": ([VP, P(VP)], I),
         "cgx_ipc_close": ([VP], I),
+        "cgx_mc_supported": ([I, P(I)], I),
+        "cgx_mc_buffer_bytes": ([U64, I, P(U64)], I),
+        "cgx_mc_create": ([I, U64, I, P(U64), P(U64)], I),
+        "cgx_mc_export_fd": ([U64, P(I)], I),
+        "cgx_mc_import_fd": ([I, P(U64)], I),
+        "cgx_mc_add_device": ([U64, I], I),
+        "cgx_mc_bind_map": ([U64, I, U64, P(VP), P(VP)], I),
+        "cgx_mc_release": ([VP], I),
+        "cgx_chain_set_multicast": ([VP, I, VP, VP, U64, I], I),
         "cgx_tune_graph_streams": ([VP, P(ExecOpts), VP, VP, I, I, P(C.c_int), I, I, P(C.c_int), P(C.c_double)], I),
     }
     for name, (args, res) in sig.items():
@@ -173,7 +182,9 @@ EXPORTED = ("cgx_version", "cgx_last_error", "cgx_chain_create", "cgx_chain_add_
             "cgx_debug_param_image", "cgx_debug_ext_field_offsets", "cgx_debug_gemm_trace", "cgx_debug_node_trace", "cgx_debug_cta_trace", "cgx_debug_mega_trace", "cgx_debug_launch_nodes", "cgx_device_loop", "cgx_nccl_unique_id",
             "cgx_nccl_comm_init", "cgx_nccl_comm_destroy", "cgx_peer_buffer_bytes", "cgx_chain_set_peers",
             "cgx_device_alloc", "cgx_device_free",
-            "cgx_ipc_handle", "cgx_ipc_open", "cgx_ipc_close", "cgx_tune_graph_streams")
+            "cgx_ipc_handle", "cgx_ipc_open", "cgx_ipc_close", "cgx_mc_supported", "cgx_mc_buffer_bytes",
+            "cgx_mc_create", "cgx_mc_export_fd", "cgx_mc_import_fd", "cgx_mc_add_device", "cgx_mc_bind_map",
+            "cgx_mc_release", "cgx_chain_set_multicast", "cgx_tune_graph_streams")
 
 
 def _ck(status: int, fn: str):
@@ -441,6 +452,57 @@ def peer_buffer_bytes(world: int, max_elems: int, max_allreduces: int = 64) -> i
 def chain_set_peers(chain: int, rank: int, world: int, bases, max_elems: int, max_allreduces: int = 64) -> None:
     arr = (C.c_void_p * world)(*bases)
     _ck(LIB.cgx_chain_set_peers(chain, rank, world, arr, max_elems, max_allreduces), "cgx_chain_set_peers")
+
+
+def mc_supported(device: int) -> bool:
+    v = C.c_int()
+    _ck(LIB.cgx_mc_supported(device, C.byref(v)), "cgx_mc_supported")
+    return bool(v.value)
+
+
+def mc_buffer_bytes(max_elems: int, max_allreduces: int = 64) -> int:
+    b = C.c_uint64()
+    _ck(LIB.cgx_mc_buffer_bytes(max_elems, max_allreduces, C.byref(b)), "cgx_mc_buffer_bytes")
+    return b.value
+
+
+def mc_create(world: int, nbytes: int, device: int) -> tuple:
+    """(multicast handle, size every rank binds and maps)."""
+    h, sz = C.c_uint64(), C.c_uint64()
+    _ck(LIB.cgx_mc_create(world, nbytes, device, C.byref(h), C.byref(sz)), "cgx_mc_create")
+    return h.value, sz.value
+
+
+def mc_export_fd(handle: int) -> int:
+    fd = C.c_int()
+    _ck(LIB.cgx_mc_export_fd(handle, C.byref(fd)), "cgx_mc_export_fd")
+    return fd.value
+
+
+def mc_import_fd(fd: int) -> int:
+    h = C.c_uint64()
+    _ck(LIB.cgx_mc_import_fd(fd, C.byref(h)), "cgx_mc_import_fd")
+    return h.value
+
+
+def mc_add_device(handle: int, device: int) -> None:
+    _ck(LIB.cgx_mc_add_device(handle, device), "cgx_mc_add_device")
+
+
+def mc_bind_map(handle: int, device: int, size: int) -> tuple:
+    """(this rank's copy, the multicast address) of a zero-filled region bound to `handle`."""
+    uc, mc = C.c_void_p(), C.c_void_p()
+    _ck(LIB.cgx_mc_bind_map(handle, device, size, C.byref(uc), C.byref(mc)), "cgx_mc_bind_map")
+    return uc.value, mc.value
+
+
+def mc_release(uc: int) -> None:
+    _ck(LIB.cgx_mc_release(C.c_void_p(uc)), "cgx_mc_release")
+
+
+def chain_set_multicast(chain: int, world: int, uc: int, mc: int, max_elems: int, max_allreduces: int = 64) -> None:
+    _ck(LIB.cgx_chain_set_multicast(chain, world, C.c_void_p(uc), C.c_void_p(mc), max_elems, max_allreduces),
+        "cgx_chain_set_multicast")
 
 
 def device_alloc(device: int, nbytes: int) -> int:

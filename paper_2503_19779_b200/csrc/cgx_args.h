@@ -189,6 +189,24 @@ struct PeerArArgs {
   DevStatus st;                        // spin bound / lost-peer report
 };
 const void* kfn_allreduce_peer();
+// NVLS / multicast all-reduce (cgx_chain_set_multicast, k_allreduce_mc): every rank's region is
+// bound to one multicast object at the same offsets: data [max_ar][2 parity][slot] bf16, then the
+// arrival counters [max_ar][kArMaxCtas] uint32. uc_* address this rank's copy, mc_* the multicast
+// mapping (multimem.* instructions act on every rank's copy through the NVSwitch).
+struct McArArgs {
+  const __nv_bfloat16* in;
+  __nv_bfloat16* out;
+  uint64_t n;                          // elements (multiple of 8)
+  uint64_t slot_elems;                 // elements per parity slot
+  uint32_t world, ar_index, n_ar, pad;
+  uint32_t* counters;                  // chain-owned [kArMaxNodes][kArMaxCtas] generations
+  __nv_bfloat16* uc_data;              // this node's [2][slot] block, this rank's copy
+  __nv_bfloat16* mc_data;              // the same block through the multicast mapping
+  uint32_t* uc_flags;                  // [kArMaxCtas] arrival counters of this node, this rank's copy
+  uint32_t* mc_flags;                  // the same through the multicast mapping
+  DevStatus st;                        // spin bound / lost-peer report
+};
+const void* kfn_allreduce_mc();
 static constexpr int kGatherMax = 64;
 struct GatherArgs {
   const void* src[kGatherMax];

@@ -621,6 +621,64 @@ __global__ void __launch_bounds__(256) k_allreduce_peer(const __grid_constant__ 
   }
 }
 
+// ---------------------------------------------------------------------------- NVLS all-reduce
+// One-shot bf16 sum across `world` ranks through an NVSwitch multicast object (SURVEY §8(f)
+// NEXT-4): every rank's region is bound to the object at the same offsets, so one multimem load
+// at an address returns the reduction of that address over every rank's copy, done in the switch.
+// CTA c owns vectors [c*nv/C, (c+1)*nv/C):
+//  1. store this rank's chunk into its OWN copy of the parity slot (plain stores, no pushes);
+//  2. arrive: bar.sync, then one thread: sys-scope fence and multimem.red.release.sys.add of 1 to
+//     counter[ar][c] — on every rank's copy at once;
+//  3. wait until its own copy of counter[ar][c] reaches world * g (ld.acquire.sys polls, bounded:
+//     a lost rank is reported through the exec's status word), then fence + bar.sync;
+//  4. multimem.ld_reduce.add.acc::f32 of the chunk through the multicast mapping (fp32
+//     accumulation in the switch, one bf16 rounding) into the output.
+// g = ++counter[ar][c] (chain-owned, the same sequence on every rank); parity (g - 1) & 1 — a rank
+// writes generation g + 2's partial only after every rank arrived at g + 1, i.e. finished reading
+// g (the peer kernel's argument). PDL trigger after step 3, as in the peer kernel.
+__global__ void __launch_bounds__(256) k_allreduce_mc(const __grid_constant__ McArArgs a) {
+  pdl_wait();
+  __shared__ uint32_t s_g;
+  const uint32_t c = blockIdx.x, C = gridDim.x;
+  const uint64_t nv = a.n / 8;
+  const uint64_t lo = nv * c / C, hi = nv * (c + 1) / C;
+  if (threadIdx.x == 0) {
+    const uint32_t g = a.counters[a.ar_index * kArMaxCtas + c] + 1;
+    a.counters[a.ar_index * kArMaxCtas + c] = g;
+    s_g = g;
+  }
+  __syncthreads();
+  const uint32_t g = s_g;
+  const uint64_t off = (uint64_t)((g - 1u) & 1u) * a.slot_elems;
+  const uint4* in = reinterpret_cast<const uint4*>(a.in);
+  uint4* mine = reinterpret_cast<uint4*>(a.uc_data + off);
+  for (uint64_t v = lo + threadIdx.x; v < hi; v += blockDim.x) mine[v] = in[v];   // 1. own copy
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("fence.acq_rel.sys;\n" ::: "memory");
+    asm volatile("multimem.red.release.sys.global.add.u32 [%0], 1;\n" ::"l"(a.mc_flags + c) : "memory");   // 2.
+    const uint32_t target = a.world * g;   // 3. (monotonic: every rank adds 1 per generation)
+    uint64_t spins = 0;
+    const unsigned long long t0 = gtimer();
+    for (;;) {
+      uint32_t v;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];\n" : "=r"(v) : "l"(a.uc_flags + c) : "memory");
+      if ((int32_t)(v - target) >= 0) break;
+      if (spin_expired(a.st, t0, spins, kDevErrPeer)) break;   // lost rank: reported, no trap
+    }
+    asm volatile("fence.acq_rel.sys;\n" ::: "memory");
+  }
+  __syncthreads();
+  pdl_trigger();
+  const __nv_bfloat16* mc = a.mc_data + off;   // 4. in-switch reduction
+  for (uint64_t v = lo + threadIdx.x; v < hi; v += blockDim.x) {
+    uint4 o;
+    asm volatile("multimem.ld_reduce.weak.global.add.acc::f32.v4.bf16x2 {%0, %1, %2, %3}, [%4];\n"
+                 : "=r"(o.x), "=r"(o.y), "=r"(o.z), "=r"(o.w) : "l"(mc + 8 * v) : "memory");
+    reinterpret_cast<uint4*>(a.out)[v] = o;
+  }
+}
+
 struct FillArgs { float* out; uint64_t n; uint64_t base; };
 __global__ void k_fill_uniform_f32(const __grid_constant__ FillArgs a) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n;
@@ -711,6 +769,7 @@ const void* kfn_pdl_nop() { return (const void*)k_pdl_nop; }
 const void* kfn_fill_uniform_f32() { return (const void*)k_fill_uniform_f32; }
 const void* kfn_gather() { return (const void*)k_gather; }
 const void* kfn_allreduce_peer() { return (const void*)k_allreduce_peer; }
+const void* kfn_allreduce_mc() { return (const void*)k_allreduce_mc; }
 int elem_block_threads() { return kElemThreads; }
 int elem_tile_vecs() { return kElemVec; }
 

@@ -13,6 +13,7 @@
 //  * Capture = stream capture on a private stream with programmatic-dependent-launch edges
 //    (so NCCL collectives can be captured too); node handles are taken from
 //    cudaStreamGetCaptureInfo right after each launch.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -138,6 +139,13 @@ struct cgx_chain {
   int peer_max_ar = 0;          // all-reduce nodes the regions have receive buffers for
   std::vector<void*> peer_base;
   uint32_t* peer_counters = nullptr;
+  // NVLS / multicast all-reduce (cgx_chain_set_multicast): this rank's copy and the multicast
+  // mapping of the region bound to the node's multicast object
+  int mc_world = 0;
+  void* mc_uc = nullptr;
+  void* mc_mc = nullptr;
+  uint64_t mc_max_elems = 0;
+  int mc_max_ar = 0;
   void* arena = nullptr;        // internal buffers
   bool allocated = false;
   int live_execs = 0;
@@ -364,6 +372,183 @@ extern "C" int cgx_chain_set_peers(cgx_chain* c, int rank, int world, void* cons
   c->peer_max_elems = max_elems;
   c->peer_max_ar = max_allreduces;
   c->peer_base.assign(bases, bases + world);
+  return CGX_OK;
+}
+
+// ---------------------------------------------------------------- NVLS multicast regions
+// Region of one rank, bound to the node's multicast object at the same offsets on every rank:
+// data [max_ar][2 parity][slot] bf16, then (256-B aligned) the arrival counters [max_ar][kArMaxCtas]
+// uint32 (k_allreduce_mc). Driver API (virtual memory management + multicast objects) through
+// cudaGetDriverEntryPoint: the library links only the runtime.
+static uint64_t mc_slot_elems(uint64_t max_elems) { return (max_elems + 127) / 128 * 128; }
+static uint64_t mc_flag_offset(uint64_t max_elems, int max_ar) {
+  return ((uint64_t)max_ar * 2 * mc_slot_elems(max_elems) * sizeof(uint16_t) + 255) / 256 * 256;
+}
+template <typename F>
+static F drv_fn(const char* name) {
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+    return nullptr;
+  return reinterpret_cast<F>(fn);
+}
+#define DRV(fnname, ...)                                                                      \
+  do {                                                                                        \
+    static const auto f_ = drv_fn<decltype(&::fnname)>(#fnname);                              \
+    if (!f_) return fail(CGX_E_UNSUPPORTED, #fnname ": driver entry point unavailable");      \
+    const CUresult r_ = f_(__VA_ARGS__);                                                      \
+    if (r_ != CUDA_SUCCESS) return fail(CGX_E_CUDA, std::string(#fnname " failed: CUresult ") + std::to_string((int)r_)); \
+  } while (0)
+
+namespace {
+struct McMapping {
+  CUmemGenericAllocationHandle mc = 0, mem = 0;
+  CUdeviceptr uc = 0, mcp = 0;
+  uint64_t size = 0;
+  int device = 0;
+};
+std::vector<McMapping> g_mc_maps;   // (guarded by the caller: setup is not thread-hot)
+}  // namespace
+
+extern "C" int cgx_mc_supported(int device, int* supported) {
+  if (!supported) return fail(CGX_E_INVALID_ARG, "mc_supported: NULL");
+  *supported = 0;
+  int v = 0;
+  DRV(cuDeviceGetAttribute, &v, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, (CUdevice)device);
+  *supported = v;
+  return CGX_OK;
+}
+
+extern "C" int cgx_mc_buffer_bytes(uint64_t max_elems, int max_allreduces, uint64_t* bytes) {
+  if (!bytes || max_elems == 0 || max_allreduces < 1 || max_allreduces > kArMaxNodes)
+    return fail(CGX_E_INVALID_ARG, "mc_buffer_bytes: max_elems > 0, max_allreduces 1..64");
+  *bytes = mc_flag_offset(max_elems, max_allreduces) + sizeof(uint32_t) * (uint64_t)max_allreduces * kArMaxCtas;
+  return CGX_OK;
+}
+
+// Multicast object for `world` devices, sized up to the multicast and allocation granularities
+// (*size_out: the size every rank binds and maps). Exportable as a POSIX file descriptor.
+extern "C" int cgx_mc_create(int world, uint64_t bytes, int device, uint64_t* handle_out, uint64_t* size_out) {
+  if (!handle_out || !size_out || world < 1 || world > kArMaxWorld || bytes == 0)
+    return fail(CGX_E_INVALID_ARG, "mc_create: bad argument");
+  CUmulticastObjectProp mp{};
+  mp.numDevices = (unsigned)world;
+  mp.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  mp.size = bytes;
+  size_t g_mc = 0, g_al = 0;
+  DRV(cuMulticastGetGranularity, &g_mc, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED);
+  CUmemAllocationProp ap{};
+  ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  ap.location.id = device;
+  ap.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  DRV(cuMemGetAllocationGranularity, &g_al, &ap, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED);
+  const uint64_t g = std::max<uint64_t>(g_mc, g_al);
+  mp.size = (bytes + g - 1) / g * g;
+  CUmemGenericAllocationHandle h = 0;
+  DRV(cuMulticastCreate, &h, &mp);
+  *handle_out = (uint64_t)h;
+  *size_out = mp.size;
+  return CGX_OK;
+}
+
+extern "C" int cgx_mc_export_fd(uint64_t handle, int* fd_out) {
+  if (!fd_out) return fail(CGX_E_INVALID_ARG, "mc_export_fd: NULL");
+  int fd = -1;
+  DRV(cuMemExportToShareableHandle, (void*)&fd, (CUmemGenericAllocationHandle)handle,
+      CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0ull);
+  *fd_out = fd;
+  return CGX_OK;
+}
+
+extern "C" int cgx_mc_import_fd(int fd, uint64_t* handle_out) {
+  if (!handle_out || fd < 0) return fail(CGX_E_INVALID_ARG, "mc_import_fd: bad argument");
+  CUmemGenericAllocationHandle h = 0;
+  DRV(cuMemImportFromShareableHandle, &h, (void*)(uintptr_t)fd, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR);
+  *handle_out = (uint64_t)h;
+  return CGX_OK;
+}
+
+// Every rank adds its device before ANY rank binds memory (a barrier between the two calls).
+extern "C" int cgx_mc_add_device(uint64_t handle, int device) {
+  CK(cudaSetDevice(device));
+  CK(cudaFree(nullptr));   // (the device's primary context exists before the driver calls)
+  DRV(cuMulticastAddDevice, (CUmemGenericAllocationHandle)handle, (CUdevice)device);
+  return CGX_OK;
+}
+
+// This rank's physical region (size bytes on `device`), bound to the multicast object at offset 0,
+// mapped twice: *uc_out = this rank's copy, *mc_out = the multicast address (multimem.* only).
+// Zero-filled. Released by cgx_mc_release(uc).
+extern "C" int cgx_mc_bind_map(uint64_t handle, int device, uint64_t size, void** uc_out, void** mc_out) {
+  if (!uc_out || !mc_out || size == 0) return fail(CGX_E_INVALID_ARG, "mc_bind_map: bad argument");
+  CK(cudaSetDevice(device));
+  McMapping m;
+  m.mc = (CUmemGenericAllocationHandle)handle;
+  m.size = size;
+  m.device = device;
+  CUmemAllocationProp ap{};
+  ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  ap.location.id = device;
+  ap.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  DRV(cuMemCreate, &m.mem, (size_t)size, &ap, 0ull);
+  DRV(cuMulticastBindMem, m.mc, (size_t)0, m.mem, (size_t)0, (size_t)size, 0ull);
+  CUmemAccessDesc acc{};
+  acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  acc.location.id = device;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  DRV(cuMemAddressReserve, &m.uc, (size_t)size, (size_t)0, (CUdeviceptr)0, 0ull);
+  DRV(cuMemMap, m.uc, (size_t)size, (size_t)0, m.mem, 0ull);
+  DRV(cuMemSetAccess, m.uc, (size_t)size, &acc, (size_t)1);
+  DRV(cuMemAddressReserve, &m.mcp, (size_t)size, (size_t)0, (CUdeviceptr)0, 0ull);
+  DRV(cuMemMap, m.mcp, (size_t)size, (size_t)0, m.mc, 0ull);
+  DRV(cuMemSetAccess, m.mcp, (size_t)size, &acc, (size_t)1);
+  CK(cudaMemset(reinterpret_cast<void*>(m.uc), 0, size));
+  CK(cudaDeviceSynchronize());
+  *uc_out = reinterpret_cast<void*>(m.uc);
+  *mc_out = reinterpret_cast<void*>(m.mcp);
+  g_mc_maps.push_back(m);
+  return CGX_OK;
+}
+
+extern "C" int cgx_mc_release(void* uc) {
+  for (size_t i = 0; i < g_mc_maps.size(); ++i) {
+    McMapping& m = g_mc_maps[i];
+    if (reinterpret_cast<void*>(m.uc) != uc) continue;
+    CK(cudaSetDevice(m.device));
+    CK(cudaDeviceSynchronize());
+    DRV(cuMemUnmap, m.mcp, (size_t)m.size);
+    DRV(cuMemAddressFree, m.mcp, (size_t)m.size);
+    DRV(cuMemUnmap, m.uc, (size_t)m.size);
+    DRV(cuMemAddressFree, m.uc, (size_t)m.size);
+    DRV(cuMulticastUnbind, m.mc, (CUdevice)m.device, (size_t)0, (size_t)m.size);
+    DRV(cuMemRelease, m.mem);
+    DRV(cuMemRelease, m.mc);
+    g_mc_maps.erase(g_mc_maps.begin() + (long)i);
+    return CGX_OK;
+  }
+  return fail(CGX_E_INVALID_ARG, "mc_release: not a cgx_mc_bind_map region");
+}
+
+extern "C" int cgx_chain_set_multicast(cgx_chain* c, int world, void* uc, void* mc, uint64_t max_elems,
+                                       int max_allreduces) {
+  if (!c || !uc || !mc || world < 1 || world > kArMaxWorld || max_elems == 0 || max_allreduces < 1 ||
+      max_allreduces > kArMaxNodes)
+    return fail(CGX_E_INVALID_ARG, "set_multicast: bad argument");
+  if (c->allocated) return fail(CGX_E_STATE, "set_multicast: chain already captured");
+  if (reinterpret_cast<uintptr_t>(uc) % 256 || reinterpret_cast<uintptr_t>(mc) % 256)
+    return fail(CGX_E_MISALIGNED, "set_multicast: region not 256-B aligned");
+  CK(cudaSetDevice(c->device));
+  if (!c->peer_counters) {
+    CK(cudaMalloc(&c->peer_counters, sizeof(uint32_t) * kArMaxNodes * kArMaxCtas));
+    CK(cudaMemset(c->peer_counters, 0, sizeof(uint32_t) * kArMaxNodes * kArMaxCtas));
+  }
+  c->mc_world = world;
+  c->mc_uc = uc;
+  c->mc_mc = mc;
+  c->mc_max_elems = max_elems;
+  c->mc_max_ar = max_allreduces;
   return CGX_OK;
 }
 
@@ -900,6 +1085,37 @@ static int build_launch(cgx_exec* e, int k, Launch& l, int pre = -1) {
     }
     case CGX_OP_ALLREDUCE_SUM: {
       if (is_ext(n.in[0])) return fail(CGX_E_UNSUPPORTED, "allreduce: external input");
+      if (c->mc_world > 0) {
+        // one-shot all-reduce through the NVSwitch multicast object (k_allreduce_mc)
+        if (n.attr.n % 8 || n.attr.n > c->mc_max_elems)
+          return fail(CGX_E_UNSUPPORTED, "allreduce (multicast): n must be a multiple of 8 and <= max_elems");
+        int ar_index = 0, n_ar = 0;
+        ar_position(c, k, &ar_index, &n_ar);
+        if (n_ar > c->mc_max_ar)
+          return fail(CGX_E_UNSUPPORTED, "allreduce (multicast): more all-reduces than the region holds (max_allreduces)");
+        l.args.reset(sizeof(McArArgs));
+        McArArgs* a = argp<McArArgs>(l);
+        a->in = static_cast<const __nv_bfloat16*>(slot_ptr(n.in[0]));
+        a->out = static_cast<__nv_bfloat16*>(slot_ptr(n.out));
+        a->n = n.attr.n;
+        a->slot_elems = mc_slot_elems(c->mc_max_elems);
+        a->world = (uint32_t)c->mc_world;
+        a->ar_index = (uint32_t)ar_index;
+        a->n_ar = (uint32_t)n_ar;
+        a->counters = c->peer_counters;
+        const uint64_t doff = (uint64_t)ar_index * 2 * a->slot_elems * sizeof(uint16_t);
+        const uint64_t foff = mc_flag_offset(c->mc_max_elems, c->mc_max_ar) + (uint64_t)ar_index * kArMaxCtas * sizeof(uint32_t);
+        a->uc_data = reinterpret_cast<__nv_bfloat16*>(static_cast<uint8_t*>(c->mc_uc) + doff);
+        a->mc_data = reinterpret_cast<__nv_bfloat16*>(static_cast<uint8_t*>(c->mc_mc) + doff);
+        a->uc_flags = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(c->mc_uc) + foff);
+        a->mc_flags = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(c->mc_mc) + foff);
+        a->st = dev_status(e);
+        const uint64_t nv = n.attr.n / 8;
+        l.grid = dim3((unsigned)std::max<uint64_t>(1, std::min<uint64_t>(kArMaxCtas, ceil_div(nv, 256))));
+        l.block = dim3(256);
+        l.func = kfn_allreduce_mc();
+        return CGX_OK;
+      }
       if (c->peer_world > 0) {
         // one-shot all-reduce over peer memory (k_allreduce_peer)
         if (n.attr.n % 8 || n.attr.n > c->peer_max_elems)

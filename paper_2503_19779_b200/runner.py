@@ -62,9 +62,10 @@ class Chain:
     """A cgx chain built from `spec`, holding its static device tensors alive."""
 
     def __init__(self, spec, statics: dict, device: int = 0, nccl_comm: int | None = None,
-                 peers: tuple | None = None):
+                 peers: tuple | None = None, multicast: tuple | None = None):
         """peers = (rank, world, [region base per rank], max_elems): ALLREDUCE_SUM nodes run the
-        peer-memory one-shot all-reduce instead of NCCL (cgx_chain_set_peers)."""
+        peer-memory one-shot all-reduce instead of NCCL (cgx_chain_set_peers); multicast = (world,
+        uc, mc, max_elems): they run the NVLS multimem all-reduce (cgx_chain_set_multicast)."""
         self.spec = spec
         self.device = device
         self.handle = cgx.chain_create(device)
@@ -83,6 +84,8 @@ class Chain:
             cgx.chain_set_nccl(self.handle, nccl_comm)
         if peers is not None:
             cgx.chain_set_peers(self.handle, *peers)
+        if multicast is not None:
+            cgx.chain_set_multicast(self.handle, *multicast)
         self.ext_names = [s.name for s in spec.slots if s.kind == "external"]
         self.execs = []
 

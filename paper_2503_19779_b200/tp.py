@@ -63,3 +63,77 @@ class PeerRegions:
         if self.own:
             cgx.device_free(self.own)
             self.own = 0
+
+
+class MulticastRegion:
+    """Multi-process setup of the NVLS all-reduce (cgx_chain_set_multicast): rank 0 creates the
+    multicast object for `world` devices and exports it as a POSIX file descriptor, which reaches
+    the other ranks over a Unix socket (SCM_RIGHTS; the socket path travels through the torch
+    process group); every rank adds its device, waits for the others, binds a zero-filled region of
+    cgx_mc_buffer_bytes() and maps it (its own copy + the multicast address). world = 1 needs no
+    process group. Keep the object alive as long as the chain; close() releases the region."""
+
+    def __init__(self, world: int, rank: int, max_elems: int, device, group=None, max_allreduces: int = 64):
+        import os
+        import socket
+        import tempfile
+
+        import torch
+        dev = torch.device(device)
+        self.device = dev.index if dev.index is not None else torch.cuda.current_device()
+        if not cgx.mc_supported(self.device):
+            raise cgx.CgxError(cgx.E_UNSUPPORTED, "MulticastRegion",
+                               "CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED = 0 on this device")
+        nbytes = cgx.mc_buffer_bytes(max_elems, max_allreduces)
+        if world == 1:
+            self.handle, self.size = cgx.mc_create(1, nbytes, self.device)
+        else:
+            import torch.distributed as dist
+            path = None
+            if rank == 0:
+                self.handle, self.size = cgx.mc_create(world, nbytes, self.device)
+                fd = cgx.mc_export_fd(self.handle)
+                path = os.path.join(tempfile.mkdtemp(prefix="cgx_mc_"), "sock")
+                srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+                srv.bind(path)
+                srv.listen(world - 1)
+            meta = [path, self.size if rank == 0 else None]
+            dist.broadcast_object_list(meta, src=0, group=group)
+            path, self.size = meta
+            if rank == 0:
+                for _ in range(world - 1):
+                    conn, _ = srv.accept()
+                    socket.send_fds(conn, [b"fd"], [fd])
+                    conn.close()
+                srv.close()
+                os.close(fd)
+            else:
+                cli = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+                for _ in range(600):                       # rank 0 may not be listening yet
+                    try:
+                        cli.connect(path)
+                        break
+                    except (FileNotFoundError, ConnectionRefusedError):
+                        import time
+                        time.sleep(0.05)
+                _, fds, _, _ = socket.recv_fds(cli, 16, 1)
+                cli.close()
+                self.handle = cgx.mc_import_fd(fds[0])
+                os.close(fds[0])
+        cgx.mc_add_device(self.handle, self.device)
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier(group=group)                     # every device added before any bind
+        self.uc, self.mc = cgx.mc_bind_map(self.handle, self.device, self.size)
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier(group=group)
+        self.world, self.rank, self.max_elems, self.max_allreduces = world, rank, max_elems, max_allreduces
+
+    def multicast(self) -> tuple:
+        return (self.world, self.uc, self.mc, self.max_elems, self.max_allreduces)
+
+    def close(self):
+        if self.uc:
+            cgx.mc_release(self.uc)
+            self.uc = 0

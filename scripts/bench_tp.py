@@ -25,10 +25,11 @@ def main():
     ap.add_argument("--check", action="store_true")
     ap.add_argument("--dump", default="", help="directory: every rank saves the GPU value of every INTERNAL "
                     "slot after one INDIRECT replay with input set 0 (rank{r}.npz) for node-local parity")
-    ap.add_argument("--allreduce", choices=("nccl", "peer", "fused"), default="nccl",
+    ap.add_argument("--allreduce", choices=("nccl", "peer", "fused", "mc"), default="nccl",
                     help="ALLREDUCE_SUM nodes: captured ncclAllReduce, the peer-memory one-shot kernel "
-                         "over CUDA IPC-mapped regions (tp.PeerRegions), or that all-reduce fused into "
-                         "the row-parallel GEMM epilogues (CGX_GEMM_ALLREDUCE)")
+                         "over CUDA IPC-mapped regions (tp.PeerRegions), that all-reduce fused into "
+                         "the row-parallel GEMM epilogues (CGX_GEMM_ALLREDUCE), or the NVLS multimem "
+                         "all-reduce through an NVSwitch multicast object (tp.MulticastRegion)")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -58,9 +59,10 @@ def main():
     spec = (wl.c3_chain(T=args.T, n_layers=args.layers, tp=world, rank=rank,
                         fuse_allreduce=args.allreduce == "fused") if world > 1 else full)
     st = wl.static_values(spec, tp=world, rank=rank, full=full) if world > 1 else wl.static_values(spec)
-    regions = tp.PeerRegions(world, rank, args.T * 768, dev) if args.allreduce != "nccl" else None
+    regions = tp.PeerRegions(world, rank, args.T * 768, dev) if args.allreduce in ("peer", "fused") else None
+    mcr = tp.MulticastRegion(world, rank, args.T * 768, dev) if args.allreduce == "mc" else None
     chain = runner.Chain(spec, runner.upload_statics(spec, st, dev), device=local, nccl_comm=comm,
-                         peers=regions.peers() if regions else None)
+                         peers=regions.peers() if regions else None, multicast=mcr.multicast() if mcr else None)
     stream = torch.cuda.Stream(device=dev)
     xs = [runner.host_to_device(wl.slot_values(spec, "x", r), "bf16", dev) for r in range(4)]
     ptrs = [cgx.ptr_array([x.data_ptr()]) for x in xs]
@@ -124,6 +126,9 @@ def main():
     if regions is not None:
         dist.barrier()                  # no rank unmaps a region a peer may still write
         regions.close()
+    if mcr is not None:
+        dist.barrier()                  # no rank releases its copy while a peer's multimem op may reach it
+        mcr.close()
     dist.destroy_process_group()
 
 
