@@ -420,7 +420,9 @@ def bench_tp_leg(torch, dist, cgx, runner, wl, dev, local, rank, world, pg_gloo)
     (replicated) x bound every step. Variants: ALLREDUCE_SUM as a captured ncclAllReduce (NVLink /
     NVSwitch), and the row-parallel GEMMs with the peer all-reduce fused into their epilogue over
     CUDA-IPC-mapped regions. µs per replay = device time on each rank's stream, MAX over ranks;
-    tokens/s = T / that. Never fatal: a failing variant is reported as its error string."""
+    tokens/s = T / that. A third variant runs the all-reduces through an NVSwitch multicast object
+    (NVLS, multimem.ld_reduce) where the driver grants one. Never fatal: a failing variant is
+    reported as its error string."""
     from paper_2503_19779_b200 import tp
     T, L = 128, 12
     out = {"tp": world, "workload": f"C5: GPT-2-small decoder, {L} layers, T={T}, bf16, TP={world} "
@@ -433,8 +435,8 @@ def bench_tp_leg(torch, dist, cgx, runner, wl, dev, local, rank, world, pg_gloo)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    for name, kind in (("nccl", "nccl"), ("peer_fused", "fused")):
-        comm = regions = chain = None
+    for name, kind in (("nccl", "nccl"), ("peer_fused", "fused"), ("nvls", "mc")):
+        comm = regions = mcr = chain = None
         res = {}
         try:
             spec = wl.c3_chain(T=T, n_layers=L, tp=world, rank=rank, fuse_allreduce=kind == "fused")
@@ -443,10 +445,18 @@ def bench_tp_leg(torch, dist, cgx, runner, wl, dev, local, rank, world, pg_gloo)
                 if pg_gloo:
                     raise RuntimeError("NCCL ranks need one GPU each (CGX_BENCH_PG=gloo run)")
                 comm = tp.nccl_bootstrap(local)
+            elif kind == "mc":   # NVLS: multimem all-reduce through an NVSwitch multicast object
+                ok = cgx.mc_supported(local)
+                t_ok = torch.tensor([1.0 if ok else 0.0], dtype=torch.float64, device="cpu" if pg_gloo else dev)
+                dist.all_reduce(t_ok, op=dist.ReduceOp.MIN)
+                if t_ok.item() < 1.0:
+                    raise RuntimeError("CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED = 0 on some rank")
+                mcr = tp.MulticastRegion(world, rank, T * 768, dev, max_allreduces=2 * L)
             else:
                 regions = tp.PeerRegions(world, rank, T * 768, dev, max_allreduces=2 * L)
             chain = runner.Chain(spec, runner.upload_statics(spec, st, dev), device=local, nccl_comm=comm,
-                                 peers=regions.peers() if regions else None)
+                                 peers=regions.peers() if regions else None,
+                                 multicast=mcr.multicast() if mcr else None)
             xs = [runner.host_to_device(wl.slot_values(spec, "x", r), "bf16", dev) for r in range(4)]
             ptrs = [cgx.ptr_array([x.data_ptr()]) for x in xs]
             ex = chain.exec("INDIRECT", stream=stream, transport="FIRST_NODE")
@@ -482,6 +492,8 @@ def bench_tp_leg(torch, dist, cgx, runner, wl, dev, local, rank, world, pg_gloo)
                 cgx.nccl_comm_destroy(comm)
             if regions is not None:
                 regions.close()
+            if mcr is not None:
+                mcr.close()
         out[name] = res
     return out
 

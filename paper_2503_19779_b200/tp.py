@@ -89,17 +89,22 @@ class MulticastRegion:
             self.handle, self.size = cgx.mc_create(1, nbytes, self.device)
         else:
             import torch.distributed as dist
-            path = None
+            path, err = None, None
             if rank == 0:
-                self.handle, self.size = cgx.mc_create(world, nbytes, self.device)
-                fd = cgx.mc_export_fd(self.handle)
-                path = os.path.join(tempfile.mkdtemp(prefix="cgx_mc_"), "sock")
-                srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
-                srv.bind(path)
-                srv.listen(world - 1)
-            meta = [path, self.size if rank == 0 else None]
+                try:   # (a refusal must reach every rank, or they would wait for a socket forever)
+                    self.handle, self.size = cgx.mc_create(world, nbytes, self.device)
+                    fd = cgx.mc_export_fd(self.handle)
+                    path = os.path.join(tempfile.mkdtemp(prefix="cgx_mc_"), "sock")
+                    srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+                    srv.bind(path)
+                    srv.listen(world - 1)
+                except cgx.CgxError as exn:
+                    err = str(exn)
+            meta = [path, self.size if rank == 0 and err is None else None, err]
             dist.broadcast_object_list(meta, src=0, group=group)
-            path, self.size = meta
+            path, self.size, err = meta
+            if err is not None:
+                raise cgx.CgxError(cgx.E_CUDA, "MulticastRegion", f"rank 0: {err}")
             if rank == 0:
                 for _ in range(world - 1):
                     conn, _ = srv.accept()
