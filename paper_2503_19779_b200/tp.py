@@ -65,6 +65,47 @@ class PeerRegions:
             self.own = 0
 
 
+def share_fd(fd, rank: int, world: int, group=None) -> int:
+    """Rank 0's open file descriptor `fd` duplicated into every rank of the process group (same node):
+    rank 0 listens on a Unix socket whose path travels through the group, each other rank connects
+    and receives the descriptor (SCM_RIGHTS). Returns this rank's descriptor (rank 0: `fd` itself);
+    the caller closes it."""
+    import os
+    import socket
+    import tempfile
+    import time
+
+    import torch.distributed as dist
+    path = None
+    if rank == 0:
+        path = os.path.join(tempfile.mkdtemp(prefix="cgx_fd_"), "sock")
+        srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+        srv.bind(path)
+        srv.listen(max(1, world - 1))
+    meta = [path]
+    dist.broadcast_object_list(meta, src=0, group=group)
+    path = meta[0]
+    if rank == 0:
+        for _ in range(world - 1):
+            conn, _ = srv.accept()
+            socket.send_fds(conn, [b"fd"], [fd])
+            conn.close()
+        srv.close()
+        os.unlink(path)
+        os.rmdir(os.path.dirname(path))
+        return fd
+    cli = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+    for _ in range(1200):                       # rank 0 may not be listening yet
+        try:
+            cli.connect(path)
+            break
+        except (FileNotFoundError, ConnectionRefusedError):
+            time.sleep(0.05)
+    _, fds, _, _ = socket.recv_fds(cli, 16, 1)
+    cli.close()
+    return fds[0]
+
+
 class MulticastRegion:
     """Multi-process setup of the NVLS all-reduce (cgx_chain_set_multicast): rank 0 creates the
     multicast object for `world` devices and exports it as a POSIX file descriptor, which reaches
@@ -75,8 +116,6 @@ class MulticastRegion:
 
     def __init__(self, world: int, rank: int, max_elems: int, device, group=None, max_allreduces: int = 64):
         import os
-        import socket
-        import tempfile
 
         import torch
         dev = torch.device(device)
@@ -89,42 +128,22 @@ class MulticastRegion:
             self.handle, self.size = cgx.mc_create(1, nbytes, self.device)
         else:
             import torch.distributed as dist
-            path, err = None, None
+            err, fd = None, -1
             if rank == 0:
-                try:   # (a refusal must reach every rank, or they would wait for a socket forever)
+                try:   # (a refusal must reach every rank, or they would wait for the descriptor forever)
                     self.handle, self.size = cgx.mc_create(world, nbytes, self.device)
                     fd = cgx.mc_export_fd(self.handle)
-                    path = os.path.join(tempfile.mkdtemp(prefix="cgx_mc_"), "sock")
-                    srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
-                    srv.bind(path)
-                    srv.listen(world - 1)
                 except cgx.CgxError as exn:
                     err = str(exn)
-            meta = [path, self.size if rank == 0 and err is None else None, err]
+            meta = [self.size if rank == 0 and err is None else None, err]
             dist.broadcast_object_list(meta, src=0, group=group)
-            path, self.size, err = meta
+            self.size, err = meta
             if err is not None:
                 raise cgx.CgxError(cgx.E_CUDA, "MulticastRegion", f"rank 0: {err}")
-            if rank == 0:
-                for _ in range(world - 1):
-                    conn, _ = srv.accept()
-                    socket.send_fds(conn, [b"fd"], [fd])
-                    conn.close()
-                srv.close()
-                os.close(fd)
-            else:
-                cli = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
-                for _ in range(600):                       # rank 0 may not be listening yet
-                    try:
-                        cli.connect(path)
-                        break
-                    except (FileNotFoundError, ConnectionRefusedError):
-                        import time
-                        time.sleep(0.05)
-                _, fds, _, _ = socket.recv_fds(cli, 16, 1)
-                cli.close()
-                self.handle = cgx.mc_import_fd(fds[0])
-                os.close(fds[0])
+            fd = share_fd(fd if rank == 0 else None, rank, world, group)
+            if rank != 0:
+                self.handle = cgx.mc_import_fd(fd)
+            os.close(fd)
         cgx.mc_add_device(self.handle, self.device)
         if world > 1:
             import torch.distributed as dist

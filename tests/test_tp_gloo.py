@@ -106,3 +106,42 @@ def test_tp_lockstep_matches_tp1(tp):
         assert np.array_equal(e[chains[0].nodes[-1].out], out)
     ref = och.eval_chain(full, wl.external_values(full, 0), wl.static_values(full))[full.nodes[-1].out]
     assert np.linalg.norm(out - ref) / np.linalg.norm(ref) <= 2e-2
+
+
+def _fd_worker(rank, world, port, q):
+    """tp.share_fd over a world-2 gloo group: rank 0's descriptor of a temp file is duplicated into
+    rank 1, which reads the file's content through it (the NVLS multicast object's handle travels
+    the same way, tp.MulticastRegion)."""
+    import tempfile
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_2503_19779_b200 import tp
+        fd = None
+        if rank == 0:
+            f = tempfile.TemporaryFile()
+            f.write(b"cgx-multicast-handle")
+            f.flush()
+            fd = os.dup(f.fileno())
+        got = tp.share_fd(fd, rank, world)
+        os.lseek(got, 0, os.SEEK_SET)
+        data = os.read(got, 64)
+        os.close(got)
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, data))
+    except Exception as exn:  # noqa: BLE001
+        q.put((rank, repr(exn)))
+
+
+def test_share_fd_two_ranks_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    ps = [ctx.Process(target=_fd_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    assert res == {0: b"cgx-multicast-handle", 1: b"cgx-multicast-handle"}, res
