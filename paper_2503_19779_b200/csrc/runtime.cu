@@ -24,6 +24,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <unordered_map>
 #include <unordered_set>
@@ -407,8 +408,28 @@ struct McMapping {
   uint64_t size = 0;
   int device = 0;
 };
-std::vector<McMapping> g_mc_maps;   // (guarded by the caller: setup is not thread-hot)
+std::vector<McMapping> g_mc_maps;
+std::mutex g_mc_mu;
 }  // namespace
+
+// Undo the first `stage` steps of cgx_mc_bind_map (6 = all of them); release_mc also drops this
+// process's reference to the multicast object. Returns the first failure.
+static int mc_undo(const McMapping& m, int stage, bool release_mc = false) {
+  int st = CGX_OK;
+  auto step = [&](int r) { if (st == CGX_OK && r != CGX_OK) st = r; };
+  auto unmap = [&](CUdeviceptr p) -> int { DRV(cuMemUnmap, p, (size_t)m.size); return CGX_OK; };
+  auto vfree = [&](CUdeviceptr p) -> int { DRV(cuMemAddressFree, p, (size_t)m.size); return CGX_OK; };
+  auto unbind = [&]() -> int { DRV(cuMulticastUnbind, m.mc, (CUdevice)m.device, (size_t)0, (size_t)m.size); return CGX_OK; };
+  auto rel = [&](CUmemGenericAllocationHandle h) -> int { DRV(cuMemRelease, h); return CGX_OK; };
+  if (stage >= 6) step(unmap(m.mcp));
+  if (stage >= 5) step(vfree(m.mcp));
+  if (stage >= 4) step(unmap(m.uc));
+  if (stage >= 3) step(vfree(m.uc));
+  if (stage >= 2) step(unbind());
+  if (stage >= 1) step(rel(m.mem));
+  if (release_mc) step(rel(m.mc));
+  return st;
+}
 
 extern "C" int cgx_mc_supported(int device, int* supported) {
   if (!supported) return fail(CGX_E_INVALID_ARG, "mc_supported: NULL");
@@ -487,48 +508,62 @@ extern "C" int cgx_mc_bind_map(uint64_t handle, int device, uint64_t size, void*
   m.mc = (CUmemGenericAllocationHandle)handle;
   m.size = size;
   m.device = device;
-  CUmemAllocationProp ap{};
-  ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
-  ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
-  ap.location.id = device;
-  ap.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
-  DRV(cuMemCreate, &m.mem, (size_t)size, &ap, 0ull);
-  DRV(cuMulticastBindMem, m.mc, (size_t)0, m.mem, (size_t)0, (size_t)size, 0ull);
-  CUmemAccessDesc acc{};
-  acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
-  acc.location.id = device;
-  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
-  DRV(cuMemAddressReserve, &m.uc, (size_t)size, (size_t)0, (CUdeviceptr)0, 0ull);
-  DRV(cuMemMap, m.uc, (size_t)size, (size_t)0, m.mem, 0ull);
-  DRV(cuMemSetAccess, m.uc, (size_t)size, &acc, (size_t)1);
-  DRV(cuMemAddressReserve, &m.mcp, (size_t)size, (size_t)0, (CUdeviceptr)0, 0ull);
-  DRV(cuMemMap, m.mcp, (size_t)size, (size_t)0, m.mc, 0ull);
-  DRV(cuMemSetAccess, m.mcp, (size_t)size, &acc, (size_t)1);
-  CK(cudaMemset(reinterpret_cast<void*>(m.uc), 0, size));
-  CK(cudaDeviceSynchronize());
+  // every step acquired is undone if a later one fails (no leaked physical memory, bindings or VA)
+  int stage = 0;
+  const int st = [&]() -> int {
+    CUmemAllocationProp ap{};
+    ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    ap.location.id = device;
+    ap.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+    DRV(cuMemCreate, &m.mem, (size_t)size, &ap, 0ull);
+    stage = 1;
+    DRV(cuMulticastBindMem, m.mc, (size_t)0, m.mem, (size_t)0, (size_t)size, 0ull);
+    stage = 2;
+    CUmemAccessDesc acc{};
+    acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    acc.location.id = device;
+    acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    DRV(cuMemAddressReserve, &m.uc, (size_t)size, (size_t)0, (CUdeviceptr)0, 0ull);
+    stage = 3;
+    DRV(cuMemMap, m.uc, (size_t)size, (size_t)0, m.mem, 0ull);
+    stage = 4;
+    DRV(cuMemSetAccess, m.uc, (size_t)size, &acc, (size_t)1);
+    DRV(cuMemAddressReserve, &m.mcp, (size_t)size, (size_t)0, (CUdeviceptr)0, 0ull);
+    stage = 5;
+    DRV(cuMemMap, m.mcp, (size_t)size, (size_t)0, m.mc, 0ull);
+    stage = 6;
+    DRV(cuMemSetAccess, m.mcp, (size_t)size, &acc, (size_t)1);
+    CK(cudaMemset(reinterpret_cast<void*>(m.uc), 0, size));
+    CK(cudaDeviceSynchronize());
+    return CGX_OK;
+  }();
+  if (st != CGX_OK) {
+    const std::string err = g_err;   // (the undo below must not overwrite the first failure)
+    mc_undo(m, stage);
+    g_err = err;
+    return st;
+  }
   *uc_out = reinterpret_cast<void*>(m.uc);
   *mc_out = reinterpret_cast<void*>(m.mcp);
+  std::lock_guard<std::mutex> lk(g_mc_mu);
   g_mc_maps.push_back(m);
   return CGX_OK;
 }
 
 extern "C" int cgx_mc_release(void* uc) {
-  for (size_t i = 0; i < g_mc_maps.size(); ++i) {
-    McMapping& m = g_mc_maps[i];
-    if (reinterpret_cast<void*>(m.uc) != uc) continue;
-    CK(cudaSetDevice(m.device));
-    CK(cudaDeviceSynchronize());
-    DRV(cuMemUnmap, m.mcp, (size_t)m.size);
-    DRV(cuMemAddressFree, m.mcp, (size_t)m.size);
-    DRV(cuMemUnmap, m.uc, (size_t)m.size);
-    DRV(cuMemAddressFree, m.uc, (size_t)m.size);
-    DRV(cuMulticastUnbind, m.mc, (CUdevice)m.device, (size_t)0, (size_t)m.size);
-    DRV(cuMemRelease, m.mem);
-    DRV(cuMemRelease, m.mc);
+  McMapping m;
+  {
+    std::lock_guard<std::mutex> lk(g_mc_mu);
+    size_t i = 0;
+    while (i < g_mc_maps.size() && reinterpret_cast<void*>(g_mc_maps[i].uc) != uc) ++i;
+    if (i == g_mc_maps.size()) return fail(CGX_E_INVALID_ARG, "mc_release: not a cgx_mc_bind_map region");
+    m = g_mc_maps[i];
     g_mc_maps.erase(g_mc_maps.begin() + (long)i);
-    return CGX_OK;
   }
-  return fail(CGX_E_INVALID_ARG, "mc_release: not a cgx_mc_bind_map region");
+  CK(cudaSetDevice(m.device));
+  CK(cudaDeviceSynchronize());
+  return mc_undo(m, 6, true);
 }
 
 extern "C" int cgx_chain_set_multicast(cgx_chain* c, int world, void* uc, void* mc, uint64_t max_elems,
